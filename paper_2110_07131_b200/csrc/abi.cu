@@ -1,0 +1,499 @@
+// abi.cu -- the C ABI (include/rmips.h): validation, memory ownership, kernel orchestration.
+// No exceptions cross the boundary; every CUDA error becomes RMIPS_ERR_CUDA with a message in
+// rmips_last_error().  All work is enqueued on the caller's stream.
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+using namespace rmips;
+
+std::atomic<long long> rmips::g_launches{0};
+
+namespace {
+
+// CUDA-event phase timer (only when the caller asked for timing).
+struct PhaseTimer {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[8] = {};
+  int n = 0;
+  PhaseTimer(bool enable, cudaStream_t s) : on(enable), st(s) {}
+  void mark() {
+    if (!on || n >= 8) return;
+    if (cudaEventCreate(&ev[n]) == cudaSuccess) cudaEventRecord(ev[n], st);
+    ++n;
+  }
+  double between(int a, int b) const {
+    float ms = -1.f;
+    if (!on || a >= n || b >= n || !ev[a] || !ev[b]) return -1.0;
+    if (cudaEventElapsedTime(&ms, ev[a], ev[b]) != cudaSuccess) return -1.0;
+    return ms;
+  }
+  ~PhaseTimer() {
+    for (int i = 0; i < n; ++i)
+      if (ev[i]) cudaEventDestroy(ev[i]);
+  }
+};
+
+thread_local std::string g_err;
+
+rmips_status_t fail(rmips_status_t s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+struct CudaFail {
+  cudaError_t e;
+  const char* what;
+  int line;
+};
+
+#define CK(expr)                                                          \
+  do {                                                                    \
+    cudaError_t e_ = (expr);                                              \
+    if (e_ != cudaSuccess) throw CudaFail{e_, #expr, __LINE__};           \
+  } while (0)
+
+rmips_status_t from_cuda(const CudaFail& f) {
+  if (f.e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return fail(RMIPS_ERR_OOM, std::string("out of device memory at ") + f.what);
+  }
+  char buf[512];
+  snprintf(buf, sizeof buf, "CUDA error %d (%s) at abi.cu:%d: %s", (int)f.e, cudaGetErrorString(f.e), f.line, f.what);
+  return fail(RMIPS_ERR_CUDA, buf);
+}
+
+template <typename T>
+T* dalloc(int64_t count, cudaStream_t st) {
+  void* p = nullptr;
+  if (count <= 0) count = 1;
+  CK(cudaMallocAsync(&p, (size_t)count * sizeof(T), st));
+  return static_cast<T*>(p);
+}
+
+template <typename T>
+void dfree(T*& p, cudaStream_t st) {
+  if (p) cudaFreeAsync((void*)p, st);
+  p = nullptr;
+}
+
+void retain_pool() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done = true;
+}
+
+// small pinned host staging buffer (per thread)
+struct Pinned {
+  void* p = nullptr;
+  ~Pinned() { if (p) cudaFreeHost(p); }
+  template <typename T>
+  T* get() {
+    if (!p) CK(cudaMallocHost(&p, 4096));
+    return static_cast<T*>(p);
+  }
+};
+thread_local Pinned g_pin;
+
+void free_index_arrays(rmips_index_s* x, cudaStream_t st) {
+  dfree(x->perm_u, st); dfree(x->perm_p, st); dfree(x->unorm, st); dfree(x->unu, st);
+  dfree(x->pnorm, st); dfree(x->perr, st); dfree(x->U16, st); dfree(x->U32, st);
+  dfree(x->P16, st); dfree(x->P32, st); dfree(x->tau, st); dfree(x->ids, st);
+  dfree(x->thr, st); dfree(x->tb, st); dfree(x->d_counters, st); dfree(x->d_flags, st);
+  if (x->ws) cudaFreeAsync(x->ws, st);
+  x->ws = nullptr;
+  x->ws_bytes = 0;
+}
+
+int round_up(int v, int a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+extern "C" {
+
+const char* rmips_version(void) { return "rmips-b200 0.1 (sm_100a)"; }
+const char* rmips_last_error(void) { return g_err.c_str(); }
+
+const char* rmips_status_string(rmips_status_t s) {
+  switch (s) {
+    case RMIPS_OK: return "ok";
+    case RMIPS_ERR_INVALID: return "invalid argument";
+    case RMIPS_ERR_NONFINITE: return "non-finite input value";
+    case RMIPS_ERR_K_RANGE: return "k out of range (1 <= k <= k_max)";
+    case RMIPS_ERR_CAPACITY: return "result capacity too small";
+    case RMIPS_ERR_CUDA: return "CUDA error";
+    case RMIPS_ERR_OOM: return "out of device memory";
+  }
+  return "unknown status";
+}
+
+rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, int64_t m, int32_t d, int32_t k_max,
+                                    int32_t build_flags, void* cuda_stream, rmips_index_t* out) {
+  if (!out) return fail(RMIPS_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (n < 0 || m < 1 || d < 1) return fail(RMIPS_ERR_INVALID, "need n >= 0, m >= 1, d >= 1");
+  if (d > 256) return fail(RMIPS_ERR_INVALID, "d > 256 is not supported");
+  if (n >= (int64_t)1 << 31 || m >= (int64_t)1 << 31) return fail(RMIPS_ERR_INVALID, "n, m must be < 2^31");
+  if ((n > 0 && !Q) || !P) return fail(RMIPS_ERR_INVALID, "NULL input matrix");
+  if (k_max < 1) return fail(RMIPS_ERR_K_RANGE, "k_max < 1");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  retain_pool();
+  rmips_index_s* x = new rmips_index_s();
+  x->n = n; x->m = m; x->d = d; x->kmax = k_max; x->build_flags = build_flags;
+  x->dpad = round_up(d, 64);
+  x->nblocks = (n + kTileU - 1) / kTileU;
+  x->c1 = filter_c1(x->dpad);
+  x->c2 = filter_c2(x->dpad);
+  cudaGetDevice(&x->device);
+  BuildCtx c;
+  c.idx = x;
+  double* scratch = nullptr;
+  PhaseTimer tm((build_flags & RMIPS_BUILD_TIMING) != 0, st);
+  try {
+    x->d_flags = dalloc<int>(4, st);
+    x->d_counters = dalloc<unsigned long long>(kNumCounters + 4, st);
+    x->perm_u = dalloc<int32_t>(n, st);
+    x->perm_p = dalloc<int32_t>(m, st);
+    x->unorm = dalloc<double>(n, st);
+    x->unu = dalloc<float>(n, st);
+    x->pnorm = dalloc<double>(m, st);
+    x->perr = dalloc<float>(m, st);
+    x->U16 = dalloc<__half>(n * x->dpad, st);
+    x->U32 = dalloc<float>(n * d, st);
+    x->P16 = dalloc<__half>(m * x->dpad, st);
+    x->P32 = dalloc<float>(m * d, st);
+    x->tau = dalloc<double>((int64_t)k_max * n, st);
+    x->ids = dalloc<int32_t>((int64_t)k_max * n, st);
+    x->thr = dalloc<float>((int64_t)k_max * n, st);
+    x->tb = dalloc<float>((int64_t)k_max * x->nblocks, st);
+    c.norm_u_raw = dalloc<double>(n, st);
+    c.norm_p_raw = dalloc<double>(m, st);
+    c.iota_u = dalloc<int32_t>(n, st);
+    c.iota_p = dalloc<int32_t>(m, st);
+    c.maxabs = dalloc<unsigned int>(4, st);
+    c.scale_dev = reinterpret_cast<float*>(c.maxabs + 2);
+    c.cub_bytes = build_cub_bytes(n, m);
+    c.cub_tmp = dalloc<unsigned char>((int64_t)c.cub_bytes, st);
+    c.cand = dalloc<int32_t>(n * kCand, st);
+    c.ccount = dalloc<int32_t>(n, st);
+    c.ovf_list = dalloc<int32_t>(n, st);
+    c.ovf_count = dalloc<int>(1, st);
+    const int fb_grid = 16;
+    scratch = dalloc<double>((int64_t)fb_grid * m, st);
+    CK(cudaMemsetAsync(x->d_flags, 0, 4 * sizeof(int), st));
+    CK(cudaMemsetAsync(c.maxabs, 0, 4 * sizeof(unsigned int), st));
+    CK(cudaMemsetAsync(c.ovf_count, 0, sizeof(int), st));
+
+    const long long l0 = g_launches.load();
+    tm.mark();  // 0
+    CK(build_prep(c, Q, P, st));
+    tm.mark();  // 1
+    if (n > 0) {
+      cudaError_t e = cudaErrorNotSupported;
+      if (!(build_flags & RMIPS_BUILD_SIMT)) e = build_tc(c, st);
+      if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        x->build_flags |= RMIPS_BUILD_SIMT;
+        e = build_simt(c, st);
+      }
+      CK(e);
+      tm.mark();  // 2
+      CK(build_select(c, st));
+      CK(build_fallback(c, 1, scratch, fb_grid, st));  // no-op unless rows overflowed (device count)
+      CK(build_blocks(c, st));
+    } else {
+      tm.mark();
+    }
+    tm.mark();  // 3
+    x->phase_ms[14] = (double)(g_launches.load() - l0);
+    int* hp = g_pin.get<int>();
+    CK(cudaMemcpyAsync(hp, x->d_flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hp + 1, c.ovf_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hp + 2, c.scale_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
+    dfree(c.norm_u_raw, st); dfree(c.norm_p_raw, st); dfree(c.iota_u, st); dfree(c.iota_p, st);
+    dfree(c.maxabs, st); dfree(c.cand, st); dfree(c.ccount, st); dfree(c.ovf_list, st);
+    dfree(c.ovf_count, st); dfree(scratch, st);
+    if (c.cub_tmp) cudaFreeAsync(c.cub_tmp, st);
+    CK(cudaStreamSynchronize(st));
+    int flags = hp[0];
+    x->overflow_rows = hp[1];
+    if (tm.on) {
+      x->phase_ms[0] = tm.between(0, 1);
+      x->phase_ms[1] = tm.between(1, 2);
+      x->phase_ms[2] = tm.between(2, 3);
+      x->phase_ms[3] = tm.between(0, 3);
+    }
+    memcpy(&x->pscale, hp + 2, sizeof(float));
+    if (flags & kFlagNonfinite) {
+      free_index_arrays(x, st);
+      delete x;
+      return fail(RMIPS_ERR_NONFINITE, "Q or P contains a NaN or Inf");
+    }
+  } catch (const CudaFail& f) {
+    cudaStreamSynchronize(st);
+    free_index_arrays(x, st);
+    delete x;
+    return from_cuda(f);
+  }
+  *out = x;
+  return RMIPS_OK;
+}
+
+rmips_status_t rmips_build_index(const float* Q, int64_t n, const float* P, int64_t m, int32_t d, int32_t k_max,
+                                 void* cuda_stream, rmips_index_t* out) {
+  return rmips_build_index_ex(Q, n, P, m, d, k_max, RMIPS_BUILD_DEFAULT, cuda_stream, out);
+}
+
+rmips_status_t rmips_build_index_host(const float* Q, int64_t n, const float* P, int64_t m, int32_t d, int32_t k_max,
+                                      void* cuda_stream, rmips_index_t* out) {
+  if (!out) return fail(RMIPS_ERR_INVALID, "out is NULL");
+  if (n < 0 || m < 1 || d < 1 || (n > 0 && !Q) || !P) return fail(RMIPS_ERR_INVALID, "bad sizes or NULL input");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  float *dQ = nullptr, *dP = nullptr;
+  rmips_status_t s;
+  try {
+    dQ = dalloc<float>(n * d, st);
+    dP = dalloc<float>(m * d, st);
+    if (n) CK(cudaMemcpyAsync(dQ, Q, (size_t)n * d * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dP, P, (size_t)m * d * 4, cudaMemcpyHostToDevice, st));
+    s = rmips_build_index(n ? dQ : nullptr, n, dP, m, d, k_max, cuda_stream, out);
+  } catch (const CudaFail& f) {
+    s = from_cuda(f);
+  }
+  dfree(dQ, st);
+  dfree(dP, st);
+  return s;
+}
+
+static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cudaStream_t st) {
+  const int dpad = x->dpad;
+  size_t qcub = query_cub_bytes(cap);
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
+  size_t oQ16 = take((size_t)nsub * kQB * dpad * 2), oqn = take((size_t)nsub * kQB * 4),
+         oqe = take((size_t)nsub * kQB * 4), oqs = take((size_t)nsub * 4), oqp = take((size_t)nsub * kQB * 4),
+         oqc = take((size_t)nsub * 4), oacc = take((size_t)cap * 8), ound = take((size_t)cap * 8),
+         osrt = take((size_t)cap * 8), ocub = take(qcub);
+  if (off > x->ws_bytes) {
+    if (x->ws) cudaFreeAsync(x->ws, st);
+    x->ws = nullptr;
+    CK(cudaMallocAsync(&x->ws, off, st));
+    x->ws_bytes = off;
+  }
+  char* b = static_cast<char*>(x->ws);
+  c.Q16 = reinterpret_cast<__half*>(b + oQ16);
+  c.qn = reinterpret_cast<float*>(b + oqn);
+  c.qerr = reinterpret_cast<float*>(b + oqe);
+  c.qscale = reinterpret_cast<float*>(b + oqs);
+  c.qperm = reinterpret_cast<int32_t*>(b + oqp);
+  c.qcount = reinterpret_cast<int32_t*>(b + oqc);
+  c.acc = reinterpret_cast<uint64_t*>(b + oacc);
+  c.und = reinterpret_cast<uint64_t*>(b + ound);
+  c.acc_sorted = reinterpret_cast<uint64_t*>(b + osrt);
+  c.cub_tmp = b + ocub;
+  c.cub_bytes = qcub;
+  c.cap = cap;
+  x->pair_cap = cap;
+}
+
+rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b, int32_t k, int32_t flags,
+                              int64_t* offsets, int32_t* user_ids, int64_t capacity, int64_t* total_out,
+                              void* cuda_stream) {
+  if (!idx || !total_out) return fail(RMIPS_ERR_INVALID, "NULL index or total_out");
+  if (b < 0 || capacity < 0) return fail(RMIPS_ERR_INVALID, "b < 0 or capacity < 0");
+  if (b > 0 && (!q_batch || !offsets)) return fail(RMIPS_ERR_INVALID, "NULL q_batch or offsets");
+  if (capacity > 0 && !user_ids) return fail(RMIPS_ERR_INVALID, "NULL user_ids with capacity > 0");
+  if (k < 1 || k > idx->kmax) return fail(RMIPS_ERR_K_RANGE, "k outside [1, k_max]");
+  if (flags & ~(RMIPS_FLAG_NO_BLOCKS | RMIPS_FLAG_VERIFY_SCAN | RMIPS_FLAG_FORCE_VERIFY | RMIPS_FLAG_SIMT | RMIPS_FLAG_TIMING))
+    return fail(RMIPS_ERR_INVALID, "unknown flag bits");
+  rmips_index_s* x = idx;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  *total_out = 0;
+  memset(&x->stats, 0, sizeof x->stats);
+  x->stats.queries = b;
+  if (b == 0) {
+    if (offsets) {
+      if (cudaMemsetAsync(offsets, 0, sizeof(int64_t), st) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
+        return fail(RMIPS_ERR_CUDA, "memset of offsets failed");
+    }
+    return RMIPS_OK;
+  }
+  try {
+    QueryCtx c;
+    c.idx = x; c.q = q_batch; c.b = b; c.k = k; c.flags = flags;
+    c.nsub = (b + kQB - 1) / kQB;
+    c.counters = x->d_counters;
+    c.flags_dev = x->d_flags;
+    int64_t cap = x->pair_cap > 0 ? x->pair_cap : (int64_t)1 << 20;
+    unsigned long long* hc = g_pin.get<unsigned long long>();
+    std::unique_ptr<PhaseTimer> tm;
+    const long long l0 = g_launches.load();
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      tm.reset(new PhaseTimer((flags & RMIPS_FLAG_TIMING) != 0, st));
+      ensure_ws(x, c, c.nsub, cap, st);
+      tm->mark();  // 0
+      CK(cudaMemsetAsync(x->d_counters, 0, sizeof(unsigned long long) * (kNumCounters + 4), st));
+      CK(cudaMemsetAsync(x->d_flags, 0, sizeof(int) * 4, st));
+      CK(query_prep(c, st));
+      tm->mark();  // 1
+      if (x->n > 0) {
+        cudaError_t e = cudaErrorNotSupported;
+        if (!(flags & RMIPS_FLAG_SIMT) && !(x->build_flags & RMIPS_BUILD_SIMT)) e = query_filter_tc(c, st);
+        if (e == cudaErrorNotSupported) {
+          cudaGetLastError();
+          e = query_filter_simt(c, st);
+        }
+        CK(e);
+        tm->mark();  // 2
+        CK(query_exact(c, st));
+      } else {
+        tm->mark();
+      }
+      tm->mark();  // 3
+      CK(cudaMemcpyAsync(hc, x->d_counters, sizeof(unsigned long long) * kNumCounters, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(reinterpret_cast<int*>(hc + kNumCounters), x->d_flags, sizeof(int), cudaMemcpyDeviceToHost,
+                         st));
+      CK(cudaStreamSynchronize(st));
+      int fl = *reinterpret_cast<int*>(hc + kNumCounters);
+      if (fl & kFlagNonfinite) return fail(RMIPS_ERR_NONFINITE, "query vector contains a NaN or Inf");
+      unsigned long long need = hc[C_ACCEPTED_TOTAL] > hc[C_UND_TOTAL] ? hc[C_ACCEPTED_TOTAL] : hc[C_UND_TOTAL];
+      if ((int64_t)need <= cap) break;
+      cap = (int64_t)(need + need / 4 + 1024);
+      if (attempt == 2) return fail(RMIPS_ERR_CUDA, "pair workspace did not converge");
+    }
+    rmips_stats_t& S = x->stats;
+    S.block_query_pairs = hc[C_BLOCK_PAIRS];
+    S.block_query_pruned = hc[C_BLOCK_PRUNED];
+    S.pairs_scored = hc[C_SCORED];
+    S.pairs_rejected = hc[C_REJECTED];
+    S.pairs_accepted_fast = hc[C_ACCEPT_FAST];
+    S.pairs_undecided = hc[C_UNDECIDED];
+    S.pairs_exact_accepted = hc[C_EXACT_ACCEPT];
+    S.scans = hc[C_SCANS];
+    S.items_scanned = hc[C_ITEMS_SCANNED];
+    S.result_total = hc[C_ACCEPTED_TOTAL];
+    const int64_t total = S.result_total;
+    tm->mark();  // 4
+    CK(query_sort(c, total, 64, st));
+    CK(query_output(c, offsets, user_ids, capacity, st));
+    tm->mark();  // 5
+    CK(cudaStreamSynchronize(st));
+    x->phase_ms[15] = (double)(g_launches.load() - l0);
+    if (tm->on) {
+      x->phase_ms[8] = tm->between(0, 1);
+      x->phase_ms[9] = tm->between(1, 2);
+      x->phase_ms[10] = tm->between(2, 3);
+      x->phase_ms[11] = tm->between(4, 5);
+      x->phase_ms[12] = tm->between(0, 5);
+    }
+    *total_out = total;
+    if (total > capacity) return fail(RMIPS_ERR_CAPACITY, "result ids exceed capacity");
+  } catch (const CudaFail& f) {
+    cudaStreamSynchronize(st);
+    return from_cuda(f);
+  }
+  return RMIPS_OK;
+}
+
+rmips_status_t rmips_query(rmips_index_t idx, const float* q_batch, int32_t b, int32_t k, int64_t* offsets,
+                           int32_t* user_ids, int64_t capacity, int64_t* total_out, void* cuda_stream) {
+  return rmips_query_ex(idx, q_batch, b, k, RMIPS_FLAG_NONE, offsets, user_ids, capacity, total_out, cuda_stream);
+}
+
+rmips_status_t rmips_query_host(rmips_index_t idx, const float* q_batch, int32_t b, int32_t k, int64_t* offsets,
+                                int32_t* user_ids, int64_t capacity, int64_t* total_out, void* cuda_stream) {
+  if (!idx || !total_out) return fail(RMIPS_ERR_INVALID, "NULL index or total_out");
+  if (b < 0) return fail(RMIPS_ERR_INVALID, "b < 0");
+  if (b > 0 && (!q_batch || !offsets)) return fail(RMIPS_ERR_INVALID, "NULL q_batch or offsets");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  float* dq = nullptr;
+  int64_t* doff = nullptr;
+  int32_t* dids = nullptr;
+  rmips_status_t s;
+  try {
+    dq = dalloc<float>((int64_t)b * idx->d, st);
+    doff = dalloc<int64_t>((int64_t)b + 1, st);
+    dids = dalloc<int32_t>(capacity, st);
+    if (b) CK(cudaMemcpyAsync(dq, q_batch, (size_t)b * idx->d * 4, cudaMemcpyHostToDevice, st));
+    s = rmips_query(idx, dq, b, k, doff, dids, capacity, total_out, cuda_stream);
+    if (s == RMIPS_OK || s == RMIPS_ERR_CAPACITY) {
+      if (b) CK(cudaMemcpyAsync(offsets, doff, (size_t)(b + 1) * 8, cudaMemcpyDeviceToHost, st));
+      if (s == RMIPS_OK && *total_out > 0)
+        CK(cudaMemcpyAsync(user_ids, dids, (size_t)*total_out * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+  } catch (const CudaFail& f) {
+    s = from_cuda(f);
+  }
+  dfree(dq, st); dfree(doff, st); dfree(dids, st);
+  return s;
+}
+
+rmips_status_t rmips_phase_times(rmips_index_t idx, double ms[16]) {
+  if (!idx || !ms) return fail(RMIPS_ERR_INVALID, "NULL argument");
+  for (int i = 0; i < 16; ++i) ms[i] = idx->phase_ms[i];
+  return RMIPS_OK;
+}
+
+rmips_status_t rmips_query_stats(rmips_index_t idx, rmips_stats_t* out) {
+  if (!idx || !out) return fail(RMIPS_ERR_INVALID, "NULL argument");
+  *out = idx->stats;
+  return RMIPS_OK;
+}
+
+rmips_status_t rmips_index_info(rmips_index_t idx, int64_t info[8]) {
+  if (!idx || !info) return fail(RMIPS_ERR_INVALID, "NULL argument");
+  info[0] = idx->n; info[1] = idx->m; info[2] = idx->d; info[3] = idx->kmax;
+  info[4] = idx->dpad; info[5] = kTileU; info[6] = idx->overflow_rows; info[7] = idx->build_flags;
+  return RMIPS_OK;
+}
+
+rmips_status_t rmips_index_export(rmips_index_t idx, int64_t* perm_u, int64_t* perm_p, double* tau, int32_t* ids) {
+  if (!idx) return fail(RMIPS_ERR_INVALID, "NULL index");
+  rmips_index_s* x = idx;
+  const int64_t n = x->n, m = x->m, K = x->kmax;
+  try {
+    std::vector<int32_t> pu(n > 0 ? n : 1), pp(m);
+    if (n) CK(cudaMemcpy(pu.data(), x->perm_u, n * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(pp.data(), x->perm_p, m * 4, cudaMemcpyDeviceToHost));
+    if (perm_u) for (int64_t i = 0; i < n; ++i) perm_u[i] = pu[i];
+    if (perm_p) for (int64_t i = 0; i < m; ++i) perm_p[i] = pp[i];
+    if ((tau || ids) && n) {
+      std::vector<double> t(K * n);
+      std::vector<int32_t> d(K * n);
+      CK(cudaMemcpy(t.data(), x->tau, K * n * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(d.data(), x->ids, K * n * 4, cudaMemcpyDeviceToHost));
+      for (int64_t j = 0; j < K; ++j)
+        for (int64_t r = 0; r < n; ++r) {
+          if (tau) tau[j * n + pu[r]] = t[j * n + r];
+          if (ids) ids[j * n + pu[r]] = d[j * n + r];
+        }
+    }
+  } catch (const CudaFail& f) {
+    return from_cuda(f);
+  }
+  return RMIPS_OK;
+}
+
+void rmips_free_index(rmips_index_t idx) {
+  if (!idx) return;
+  cudaDeviceSynchronize();
+  free_index_arrays(idx, 0);
+  cudaStreamSynchronize(0);
+  delete idx;
+}
+
+}  // extern "C"

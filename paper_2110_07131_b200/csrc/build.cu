@@ -1,0 +1,381 @@
+// build.cu -- index build (Alg. 1, with L_i over ALL of P per BASELINE north star).
+//
+//   B1 k_norms          norms (Alg. 1 lines 1-4) + finite check + max |p_j|
+//   B2 cub radix sort   norm sort, descending, ties by ascending id (line 5; reading R6)
+//   B3 k_prep_*         permute; fp16 filter operands (u/nu, p*2^e); fp32 exact copies
+//   B4 k_build_simt     SIMT contraction + candidate epilogue (the tcgen05 version is build_tc.cu)
+//   B5 k_exact_select   fp64 re-evaluation of the candidates, exact top-k_max (lines 7-9)
+//   B5' k_exact_row_full exact fallback for rows whose candidate buffer overflowed
+//   B6 k_blocks         block table, Eq. (1) divided by ||u_first|| for Lemma 3
+#include <cub/cub.cuh>
+
+#include "cand.cuh"
+#include "common.cuh"
+#include "internal.h"
+
+namespace rmips {
+
+// ------------------------------------------------------------------------------ B1
+__global__ void k_norms(const float* __restrict__ X, int64_t rows, int d, double* __restrict__ norms,
+                        int* __restrict__ flags, unsigned int* __restrict__ maxabs_bits) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  float mx = 0.f;
+  if (r < rows) {
+    const float* x = X + r * d;
+    double s = 0.0;
+    bool fin = true;
+    for (int j = 0; j < d; ++j) {
+      float v = x[j];
+      fin &= isfinite(v);
+      mx = fmaxf(mx, fabsf(v));
+      s = __fma_rn((double)v, (double)v, s);
+    }
+    norms[r] = sqrt(s);
+    if (!fin) atomicOr(flags, kFlagNonfinite);
+  }
+  if (maxabs_bits) {
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && isfinite(mx)) atomicMax(maxabs_bits, __float_as_uint(mx));
+  }
+}
+
+__global__ void k_iota(int32_t* v, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int32_t)i;
+}
+
+// ------------------------------------------------------------------------------ B3
+// Users: U16 = fp16(u / nu), nu = fp32(||u||) (1 for the zero vector); U32 = u (permuted).
+__global__ void k_prep_users(const float* __restrict__ Q, int64_t n, int d, int dpad,
+                             const int32_t* __restrict__ perm, const double* __restrict__ norm_sorted,
+                             __half* __restrict__ U16, float* __restrict__ U32, float* __restrict__ unu) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= n * dpad) return;
+  int64_t r = idx / dpad;
+  int j = (int)(idx - r * dpad);
+  int64_t o = perm[r];
+  float nu = (float)norm_sorted[r];
+  if (!(nu > 0.f)) nu = 1.f;
+  if (isinf(nu)) nu = 3.0e38f;
+  float x = j < d ? Q[o * d + j] : 0.f;
+  U16[idx] = __float2half_rn(x / nu);
+  if (j < d) U32[r * d + j] = x;
+  if (j == 0) unu[r] = nu;
+}
+
+// Items: P16 = fp16(p * 2^e) with max|p*2^e| < 2^14; perr = filter error bound (scaled units).
+__global__ void k_prep_items(const float* __restrict__ P, int64_t m, int d, int dpad,
+                             const int32_t* __restrict__ perm, const double* __restrict__ norm_sorted,
+                             const unsigned int* __restrict__ maxabs_bits, double c1, double c2,
+                             __half* __restrict__ P16, float* __restrict__ P32, float* __restrict__ perr,
+                             float* __restrict__ scale_out) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= m * dpad) return;
+  float mx = __uint_as_float(*maxabs_bits);
+  int ex = 0;
+  if (mx > 0.f) frexpf(mx, &ex);               // mx < 2^ex
+  int e = 14 - ex;
+  e = max(-126, min(126, e));
+  float scale = ldexpf(1.f, e);
+  int64_t r = idx / dpad;
+  int j = (int)(idx - r * dpad);
+  int64_t o = perm[r];
+  float x = j < d ? P[o * d + j] : 0.f;
+  P16[idx] = __float2half_rn(x * scale);
+  if (j < d) P32[r * d + j] = x;
+  if (j == 0) {
+    double b = norm_sorted[r] * (double)scale;
+    perr[r] = __double2float_ru((c1 * b + c2) * (1.0 + 1e-6));
+  }
+  if (idx == 0) *scale_out = scale;
+}
+
+// ------------------------------------------------------------------------------ B4 (SIMT)
+// One thread per user row; 128 rows per CTA; items streamed through smem 32 at a time.
+// Scores use the same fp16 operands and fp32 accumulation as the tensor-core kernel, so the
+// same error bound applies.  Correctness path and the RMIPS_BUILD_SIMT option.
+template <int DPAD>
+__global__ void __launch_bounds__(128, 1)
+k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, const float* __restrict__ perr,
+             int64_t n, int64_t m, int kmax, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
+             int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* cv = reinterpret_cast<float*>(smem_raw);            // [128][kCandPitch]
+  int* ci = reinterpret_cast<int*>(cv + 128 * kCandPitch);   // [128][kCandPitch]
+  __half2* us = reinterpret_cast<__half2*>(ci + 128 * kCandPitch);  // [DPAD/2][128]
+  float* ps = reinterpret_cast<float*>(us + (DPAD / 2) * 128);      // [DPAD][32]
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int64_t row = blockIdx.x * (int64_t)128 + tid;
+  const bool live = row < n;
+  // stage this CTA's 128 user rows, transposed, as half2 pairs
+  for (int i = tid; i < 128 * (DPAD / 2); i += 128) {
+    int r = i / (DPAD / 2), k2 = i % (DPAD / 2);
+    int64_t gr = blockIdx.x * (int64_t)128 + r;
+    __half2 v = __floats2half2_rn(0.f, 0.f);
+    if (gr < n) v = reinterpret_cast<const __half2*>(U16)[gr * (DPAD / 2) + k2];
+    us[k2 * 128 + r] = v;
+  }
+  CandRow me{-__int_as_float(0x7f800000), 0};
+  bool ovf = false;
+  float* wcv = cv + warp * 32 * kCandPitch;
+  int* wci = ci + warp * 32 * kCandPitch;
+
+  for (int64_t base = 0; base < m; base += 32) {
+    __syncthreads();
+    for (int i = tid; i < 32 * DPAD; i += 128) {
+      int jj = i / DPAD, k = i % DPAD;
+      float v = 0.f;
+      if (base + jj < m) v = __half2float(P16[(base + jj) * DPAD + k]);
+      ps[k * 32 + jj] = v;
+    }
+    __syncthreads();
+    float s[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) s[j] = 0.f;
+#pragma unroll 2
+    for (int k2 = 0; k2 < DPAD / 2; ++k2) {
+      float2 a = __half22float2(us[k2 * 128 + tid]);
+      const float4* p0 = reinterpret_cast<const float4*>(ps + (2 * k2) * 32);
+      const float4* p1 = reinterpret_cast<const float4*>(ps + (2 * k2 + 1) * 32);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 b0 = p0[q], b1 = p1[q];
+        s[4 * q + 0] = fmaf(a.x, b0.x, s[4 * q + 0]);
+        s[4 * q + 1] = fmaf(a.x, b0.y, s[4 * q + 1]);
+        s[4 * q + 2] = fmaf(a.x, b0.z, s[4 * q + 2]);
+        s[4 * q + 3] = fmaf(a.x, b0.w, s[4 * q + 3]);
+        s[4 * q + 0] = fmaf(a.y, b1.x, s[4 * q + 0]);
+        s[4 * q + 1] = fmaf(a.y, b1.y, s[4 * q + 1]);
+        s[4 * q + 2] = fmaf(a.y, b1.z, s[4 * q + 2]);
+        s[4 * q + 3] = fmaf(a.y, b1.w, s[4 * q + 3]);
+      }
+    }
+    const float NEG = -__int_as_float(0x7f800000);
+    float mx = NEG;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (!live || base + j >= m) s[j] = NEG;
+      mx = fmaxf(mx, s[j]);
+    }
+    float E = __ldg(perr + base);
+    cand_chunk([&](int j) { return s[j]; }, mx, E, (int)base, me, wcv, wci, perr, kmax, &ovf);
+  }
+  cand_finish(me, wcv, wci, perr, kmax, &ovf, row, n, cand, ccount, ovf_list, ovf_count);
+}
+
+// ------------------------------------------------------------------------------ B5
+// Warp per user row: exact fp64 value of every candidate (dot64, R7), then the
+// k_max largest by (value desc, original item id asc).  Writes the column-major tables.
+__global__ void __launch_bounds__(256)
+k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, const int32_t* __restrict__ perm_p,
+               const float* __restrict__ unu, const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount,
+               int64_t n, int d, int kmax, double* __restrict__ tau, int32_t* __restrict__ ids,
+               float* __restrict__ thr) {
+  __shared__ double sv[8][kCand];
+  __shared__ int so[8][kCand];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t row = blockIdx.x * (int64_t)8 + w;
+  if (row >= n) return;
+  const int cnt = ccount[row];
+  if (cnt < 0) return;  // overflowed: k_exact_row_full
+  const float* u = U32 + row * d;
+  for (int i = lane; i < cnt; i += 32) {
+    int pid = cand[row * kCand + i];
+    sv[w][i] = dot64(u, P32 + (int64_t)pid * d, d);
+    so[w][i] = perm_p[pid];
+  }
+  __syncwarp();
+  const float nu = unu[row];
+  for (int i = lane; i < cnt; i += 32) {
+    double vi = sv[w][i];
+    int oi = so[w][i];
+    int rank = 0;
+    for (int j = 0; j < cnt; ++j) {
+      double vj = sv[w][j];
+      rank += (vj > vi) || (vj == vi && so[w][j] < oi);
+    }
+    if (rank < kmax) {
+      tau[(int64_t)rank * n + row] = vi;
+      ids[(int64_t)rank * n + row] = oi;
+      thr[(int64_t)rank * n + row] = (float)(vi / (double)nu);
+    }
+  }
+  for (int r = cnt + lane; r < kmax; r += 32) {  // only when m < kmax
+    tau[(int64_t)r * n + row] = -CUDART_INF;
+    ids[(int64_t)r * n + row] = -1;
+    thr[(int64_t)r * n + row] = -CUDART_INF_F;
+  }
+}
+
+// B5': exact top-k_max of a whole row (fp64 over all of P), for overflowed rows.  One CTA per
+// listed row; scratch holds the m exact values; k_max rounds of a block argmax in the order
+// (value desc, original id asc).  Slow, simple, rare (massive ties / duplicate items).
+__global__ void __launch_bounds__(256)
+k_exact_row_full(const float* __restrict__ U32, const float* __restrict__ P32, const int32_t* __restrict__ perm_p,
+                 const float* __restrict__ unu, const int32_t* __restrict__ ovf_list, const int* __restrict__ ovf_count,
+                 int64_t n, int64_t m, int d, int kmax, double* __restrict__ scratch, double* __restrict__ tau,
+                 int32_t* __restrict__ ids, float* __restrict__ thr) {
+  __shared__ double bv[256];
+  __shared__ int bo[256];
+  __shared__ int64_t bp[256];
+  const int nrows = *ovf_count;
+  double* sc = scratch + blockIdx.x * m;
+  for (int t = blockIdx.x; t < nrows; t += gridDim.x) {
+    const int64_t row = ovf_list[t];
+    const float* u = U32 + row * d;
+    for (int64_t j = threadIdx.x; j < m; j += blockDim.x) sc[j] = dot64(u, P32 + j * d, d);
+    __syncthreads();
+    double pv = CUDART_INF;
+    int po = -1;
+    const float nu = unu[row];
+    for (int r = 0; r < kmax; ++r) {
+      double best = -CUDART_INF;
+      int bestid = 0x7fffffff;
+      int64_t bestpos = -1;
+      for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
+        double v = sc[j];
+        int o = perm_p[j];
+        bool after = (v < pv) || (v == pv && o > po);  // strictly after the previous pick
+        bool better = (v > best) || (v == best && o < bestid);
+        if (after && better) { best = v; bestid = o; bestpos = j; }
+      }
+      bv[threadIdx.x] = best; bo[threadIdx.x] = bestid; bp[threadIdx.x] = bestpos;
+      __syncthreads();
+      for (int s = blockDim.x / 2; s; s >>= 1) {
+        if (threadIdx.x < s) {
+          double v2 = bv[threadIdx.x + s];
+          int o2 = bo[threadIdx.x + s];
+          if (bp[threadIdx.x + s] >= 0 &&
+              (bp[threadIdx.x] < 0 || v2 > bv[threadIdx.x] || (v2 == bv[threadIdx.x] && o2 < bo[threadIdx.x]))) {
+            bv[threadIdx.x] = v2; bo[threadIdx.x] = o2; bp[threadIdx.x] = bp[threadIdx.x + s];
+          }
+        }
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) {
+        bool ok = bp[0] >= 0;
+        tau[(int64_t)r * n + row] = ok ? bv[0] : -CUDART_INF;
+        ids[(int64_t)r * n + row] = ok ? bo[0] : -1;
+        thr[(int64_t)r * n + row] = ok ? (float)(bv[0] / (double)nu) : -CUDART_INF_F;
+      }
+      pv = bv[0];
+      po = bo[0];
+      bool ok = bp[0] >= 0;
+      __syncthreads();
+      if (!ok) pv = -CUDART_INF, po = 0x7fffffff;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------ B6
+// tb[j][B] = L^j(B) / ||u_first(B)|| rounded down, L^j(B) = min over members tau_j (Eq. 1).
+// Lemma 3 (strict form R1) keeps query q for block B iff ||q|| >= tb (q norm
+// rounded up); the queries of a batch are norm-sorted, so the kept ones are a prefix.
+__global__ void k_blocks(const double* __restrict__ tau, const double* __restrict__ unorm, int64_t n, int kmax,
+                         int64_t nblocks, float* __restrict__ tb) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= nblocks * kmax) return;
+  int64_t B = idx % nblocks;
+  int j = (int)(idx / nblocks);
+  int64_t lo = B * kTileU, hi = min(n, lo + kTileU);
+  double L = CUDART_INF;
+  for (int64_t i = lo; i < hi; ++i) L = fmin(L, tau[(int64_t)j * n + i]);
+  double uf = unorm[lo];
+  float t;
+  if (!(L > 0.0)) t = -CUDART_INF_F;           // L <= 0 (or -inf): ||u|| ||q|| >= 0 >= L, prune nothing
+  else if (uf == 0.0) t = CUDART_INF_F;        // all members are zero vectors: u.q = 0 < L
+  else t = __double2float_rd((L / uf) * (1.0 - 1e-12));
+  tb[(int64_t)j * nblocks + B] = t;
+}
+
+// ------------------------------------------------------------------------------ host driver
+static inline unsigned nblk(int64_t work, int t) { return (unsigned)((work + t - 1) / t); }
+
+template <int DPAD>
+static cudaError_t launch_build_simt(const BuildCtx& c, cudaStream_t st) {
+  size_t smem = (size_t)128 * kCandPitch * 8 + (DPAD / 2) * 128 * 4 + DPAD * 32 * 4;
+  cudaError_t e = cudaFuncSetAttribute(k_build_simt<DPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_build_simt<DPAD><<<nblk(c.idx->n, 128), 128, smem, st>>>(c.idx->U16, c.idx->P16, c.idx->perr, c.idx->n,
+                                                             c.idx->m, c.idx->kmax, c.cand, c.ccount,
+                                                             c.ovf_list, c.ovf_count); count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t build_simt(const BuildCtx& c, cudaStream_t st) {
+  switch (c.idx->dpad) {
+    case 64: return launch_build_simt<64>(c, st);
+    case 128: return launch_build_simt<128>(c, st);
+    case 192: return launch_build_simt<192>(c, st);
+    case 256: return launch_build_simt<256>(c, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t st) {
+  rmips_index_s* x = c.idx;
+  const int64_t n = x->n, m = x->m;
+  const int d = x->d, dpad = x->dpad;
+  // B1
+  if (n) k_norms<<<nblk(n, 256), 256, 0, st>>>(Q, n, d, c.norm_u_raw, x->d_flags, nullptr); count_launch();
+  k_norms<<<nblk(m, 256), 256, 0, st>>>(P, m, d, c.norm_p_raw, x->d_flags, c.maxabs); count_launch();
+  // B2
+  if (n) k_iota<<<nblk(n, 256), 256, 0, st>>>(c.iota_u, n); count_launch();
+  k_iota<<<nblk(m, 256), 256, 0, st>>>(c.iota_p, m); count_launch();
+  size_t tb = c.cub_bytes;
+  cudaError_t e;
+  if (n) {
+    e = cub::DeviceRadixSort::SortPairsDescending(c.cub_tmp, tb, c.norm_u_raw, x->unorm, c.iota_u, x->perm_u,
+                                                  (int)n, 0, 64, st);
+    count_launch(kCubSortKernels);
+    if (e != cudaSuccess) return e;
+  }
+  tb = c.cub_bytes;
+  e = cub::DeviceRadixSort::SortPairsDescending(c.cub_tmp, tb, c.norm_p_raw, x->pnorm, c.iota_p, x->perm_p,
+                                                (int)m, 0, 64, st);
+    count_launch(kCubSortKernels);
+  if (e != cudaSuccess) return e;
+  // B3
+  if (n)
+    k_prep_users<<<nblk(n * dpad, 256), 256, 0, st>>>(Q, n, d, dpad, x->perm_u, x->unorm, x->U16, x->U32, x->unu); count_launch();
+  k_prep_items<<<nblk(m * dpad, 256), 256, 0, st>>>(P, m, d, dpad, x->perm_p, x->pnorm, c.maxabs, x->c1, x->c2,
+                                                    x->P16, x->P32, x->perr, c.scale_dev); count_launch();
+  return cudaGetLastError();
+}
+
+size_t build_cub_bytes(int64_t n, int64_t m) {
+  size_t a = 0, b = 0;
+  int64_t mx = n > m ? n : m;
+  cub::DeviceRadixSort::SortPairsDescending((void*)nullptr, a, (const double*)nullptr, (double*)nullptr,
+                                            (const int32_t*)nullptr, (int32_t*)nullptr, (int)mx, 0, 64);
+  (void)b;
+  return a;
+}
+
+cudaError_t build_select(BuildCtx& c, cudaStream_t st) {
+  rmips_index_s* x = c.idx;
+  if (x->n == 0) return cudaSuccess;
+  k_exact_select<<<nblk(x->n, 8), 256, 0, st>>>(x->U32, x->P32, x->perm_p, x->unu, c.cand, c.ccount, x->n, x->d,
+                                                x->kmax, x->tau, x->ids, x->thr); count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t build_fallback(BuildCtx& c, int nrows, double* scratch, int grid, cudaStream_t st) {
+  rmips_index_s* x = c.idx;
+  if (nrows <= 0) return cudaSuccess;
+  k_exact_row_full<<<grid, 256, 0, st>>>(x->U32, x->P32, x->perm_p, x->unu, c.ovf_list, c.ovf_count, x->n, x->m,
+                                         x->d, x->kmax, scratch, x->tau, x->ids, x->thr); count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t build_blocks(BuildCtx& c, cudaStream_t st) {
+  rmips_index_s* x = c.idx;
+  if (x->n == 0) return cudaSuccess;
+  k_blocks<<<nblk(x->nblocks * x->kmax, 256), 256, 0, st>>>(x->tau, x->unorm, x->n, x->kmax, x->nblocks, x->tb); count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace rmips

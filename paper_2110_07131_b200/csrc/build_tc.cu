@@ -1,0 +1,256 @@
+// build_tc.cu -- B4 on the 5th-generation tensor cores: the |Q| x |P| x d contraction of
+// Alg. 1 lines 7-9 (over ALL of P per BASELINE north star) fused with the per-row
+// top-k_max candidate epilogue (cand.cuh), so the score matrix never reaches HBM.
+//
+// One CTA per SM (persistent over 128-user tiles), 6 warps:
+//   warp 0      TMA producer: the user tile A (128 x 64 fp16, once per tile) and the stream of
+//               128-item tiles B through a kStages-deep shared-memory ring (SWIZZLE_128B)
+//   warp 1      TMEM allocator + MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128, N=128,
+//               K=16 x 4, fp32 accumulators in TMEM, kAcc accumulator stages (4 x 128 columns)
+//   warps 2-5   epilogue: tcgen05.ld 32 rows x 32 columns per chunk; each thread owns one user
+//               row (TMEM lane) and runs the candidate filter on its 32 scores.
+// Pipelines: smem full/empty (TMA <-> MMA), TMEM full/empty (MMA <-> epilogue), and the A tile
+// full/empty (MMA done with the tile before the next user tile is loaded).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "cand.cuh"
+#include "common.cuh"
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace rmips {
+
+namespace {
+
+constexpr int kBM = 128;          // users per tile (TMEM lanes)
+constexpr int kBN = 128;          // items per tile (accumulator columns)
+constexpr int kStages = 4;        // smem ring depth for item tiles
+constexpr int kAcc = 4;           // TMEM accumulator stages (kAcc * kBN = 512 columns)
+constexpr int kTileBytes = kBM * 64 * 2;  // one 128 x 64 fp16 tile = 16 KB
+constexpr int kThreads = 192;
+
+struct Smem {
+  // offsets (bytes) from the 1024-aligned base
+  static constexpr int A = 0;                              // KB tiles
+  static constexpr int B(int KB) { return KB * kTileBytes; }
+  static constexpr int CV(int KB) { return B(KB) + kStages * KB * kTileBytes; }
+  static constexpr int CI(int KB) { return CV(KB) + kBM * kCandPitch * 4; }
+  static constexpr int BAR(int KB) { return CI(KB) + kBM * kCandPitch * 4; }
+  static constexpr int TOTAL(int KB) { return BAR(KB) + 256 + 1024; }  // + alignment slack
+};
+
+}  // namespace
+
+template <int KB>
+__global__ void __launch_bounds__(kThreads, 1)
+k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const float* __restrict__ perr, int64_t n, int64_t m, int kmax, int32_t* __restrict__ cand,
+           int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
+  using namespace sm100;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sA = sbase + Smem::A;
+  const uint32_t sB = sbase + Smem::B(KB);
+  float* cv = reinterpret_cast<float*>(smem + Smem::CV(KB));
+  int* ci = reinterpret_cast<int*>(smem + Smem::CI(KB));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::BAR(KB));
+  // barrier indices
+  const uint32_t bar0 = smem_u32(bars);
+  auto BAR = [&](int i) { return bar0 + 8u * i; };
+  const int A_FULL = 0, A_EMPTY = 1, B_FULL = 2, B_EMPTY = 2 + kStages, ACC_FULL = 2 + 2 * kStages,
+            ACC_EMPTY = 2 + 2 * kStages + kAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 + 2 * kStages + 2 * kAcc);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_utiles = (int)((n + kBM - 1) / kBM);
+  const int nit = (int)((m + kBN - 1) / kBN);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    mbar_init(BAR(A_FULL), 1);
+    mbar_init(BAR(A_EMPTY), 1);
+    for (int s = 0; s < kStages; ++s) mbar_init(BAR(B_FULL + s), 1), mbar_init(BAR(B_EMPTY + s), 1);
+    for (int a = 0; a < kAcc; ++a) mbar_init(BAR(ACC_FULL + a), 1), mbar_init(BAR(ACC_EMPTY + a), 4);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(smem_u32(tmem_slot), kAcc * kBN);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0;
+      int t = 0;
+      for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
+        if (t > 0) mbar_wait(BAR(A_EMPTY), (t - 1) & 1);
+        mbar_arrive_expect_tx(BAR(A_FULL), KB * kTileBytes);
+        for (int kb = 0; kb < KB; ++kb) tma_load_2d(sA + kb * kTileBytes, &tmA, kb * 64, ut * kBM, BAR(A_FULL));
+        for (int it = 0; it < nit; ++it) {
+          mbar_wait(BAR(B_EMPTY + stage), ph ^ 1);
+          mbar_arrive_expect_tx(BAR(B_FULL + stage), KB * kTileBytes);
+          for (int kb = 0; kb < KB; ++kb)
+            tma_load_2d(sB + (stage * KB + kb) * kTileBytes, &tmB, kb * 64, it * kBN, BAR(B_FULL + stage));
+          if (++stage == kStages) stage = 0, ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_f16_f32(kBM, kBN);
+      int stage = 0, as = 0;
+      uint32_t ph = 0, aph = 0;
+      int t = 0;
+      for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
+        mbar_wait(BAR(A_FULL), t & 1);
+        tc_fence_after();
+        for (int it = 0; it < nit; ++it) {
+          mbar_wait(BAR(ACC_EMPTY + as), aph ^ 1);
+          mbar_wait(BAR(B_FULL + stage), ph);
+          tc_fence_after();
+          const uint32_t d = tmem + as * kBN;
+#pragma unroll
+          for (int kb = 0; kb < KB; ++kb) {
+            const uint32_t a0 = sA + kb * kTileBytes;
+            const uint32_t b0 = sB + (stage * KB + kb) * kTileBytes;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_f16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
+          }
+          mma_commit(BAR(B_EMPTY + stage));
+          mma_commit(BAR(ACC_FULL + as));
+          if (++stage == kStages) stage = 0, ph ^= 1;
+          if (++as == kAcc) as = 0, aph ^= 1;
+        }
+        mma_commit(BAR(A_EMPTY));
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue: one thread per user row
+    const int q = warp & 3;                    // TMEM lane quadrant of this warp
+    const int rloc = q * 32 + lane;            // row within the tile
+    float* wcv = cv + q * 32 * kCandPitch;
+    int* wci = ci + q * 32 * kCandPitch;
+    const float NEG = -__int_as_float(0x7f800000);
+    int as = 0;
+    uint32_t aph = 0;
+    for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x) {
+      const int64_t row = (int64_t)ut * kBM + rloc;
+      const bool live = row < n;
+      CandRow me{NEG, 0};
+      bool ovf = false;
+      for (int it = 0; it < nit; ++it) {
+        mbar_wait(BAR(ACC_FULL + as), aph);
+        tc_fence_after();
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + as * kBN;
+#pragma unroll 1
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c * 32, r);
+          tmem_ld_wait();
+          if (c == kBN / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
+          }
+          const int64_t base = (int64_t)it * kBN + c * 32;
+          if (base >= m) continue;             // warp-uniform: whole chunk is padding
+          float s[32];
+          float mx = NEG;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            s[j] = __uint_as_float(r[j]);
+            if (!live || base + j >= m) s[j] = NEG;
+            mx = fmaxf(mx, s[j]);
+          }
+          const float E = __ldg(perr + base);
+          cand_chunk([&](int j) { return s[j]; }, mx, E, (int)base, me, wcv, wci, perr, kmax, &ovf);
+        }
+        if (++as == kAcc) as = 0, aph ^= 1;
+      }
+      cand_finish(me, wcv, wci, perr, kmax, &ovf, row, n, cand, ccount, ovf_list, ovf_count);
+      __syncwarp();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, kAcc * kBN);
+}
+
+// ------------------------------------------------------------------------------ host side
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+// 2-D fp16 tensor [rows][cols] (cols contiguous), box = 128 rows x 64 columns, SWIZZLE_128B.
+bool make_tmap_f16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static int sm_count() {
+  static int c = 0;
+  if (!c) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return c;
+}
+
+template <int KB>
+static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
+  rmips_index_s* x = c.idx;
+  CUtensorMap ta, tb;
+  if (!make_tmap_f16(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->dpad)) return cudaErrorNotSupported;
+  if (!make_tmap_f16(&tb, x->P16, (uint64_t)x->m, (uint64_t)x->dpad)) return cudaErrorNotSupported;
+  const int smem = Smem::TOTAL(KB);
+  cudaError_t e = cudaFuncSetAttribute(k_build_tc<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int tiles = (int)((x->n + kBM - 1) / kBM);
+  const int grid = tiles < sm_count() ? tiles : sm_count();
+  k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->n, x->m, x->kmax, c.cand, c.ccount, c.ovf_list,
+                                               c.ovf_count);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t build_tc(const BuildCtx& c, cudaStream_t st) {
+  if (getenv("RMIPS_DISABLE_TC")) return cudaErrorNotSupported;
+  switch (c.idx->dpad) {
+    case 64: return launch_tc<1>(c, st);
+    default: return cudaErrorNotSupported;  // d > 64: SIMT contraction (smem budget)
+  }
+}
+
+}  // namespace rmips

@@ -1,0 +1,142 @@
+// common.cuh -- internal definitions shared by the rmips CUDA sources (sm_100a only).
+//
+// Citations: P:n = PAPER.md line n (arXiv 2110.07131), SV = SURVEY.md, DESIGN.md §n.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <math_constants.h>
+#include <stdint.h>
+#include <cmath>
+#include <string>
+
+#include "../../include/rmips.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "rmips is written for sm_100a (B200) only"
+#endif
+
+namespace rmips {
+
+// ---------------------------------------------------------------------------------------
+// Fixed geometry.
+constexpr int kTileU = 128;        // users per tile == Lemma 3 block size (reading R5)
+constexpr int kCand = 128;         // candidate slots per user row in the build epilogue
+constexpr int kCandPitch = kCand + 1;  // smem row pitch (bank-conflict-free appends)
+constexpr int kQB = 256;           // queries per kernel batch (tcgen05 N <= 256)
+
+// Device status flags (bitwise OR into Index::d_flags[0]).
+constexpr int kFlagNonfinite = 1;
+constexpr int kFlagPairOverflow = 2;
+
+// Counter slots (Index::d_counters), mirrored into rmips_stats_t.
+enum Counter {
+  C_BLOCK_PAIRS = 0, C_BLOCK_PRUNED, C_SCORED, C_REJECTED, C_ACCEPT_FAST, C_UNDECIDED,
+  C_EXACT_ACCEPT, C_SCANS, C_ITEMS_SCANNED, C_ACCEPTED_TOTAL, C_UND_TOTAL, kNumCounters
+};
+
+// ---------------------------------------------------------------------------------------
+// The exact inner product (R7).  Left-to-right fp64 sum of the products of the
+// fp32 inputs.  Each product of two fp32 values is exact in fp64, so fma(a, b, s) rounds
+// exactly once, like s + a*b: the result is bit-identical to the oracle's orc_dot and,
+// crucially, the SAME routine evaluates q.u and p.u, so a query equal to an item gives
+// bitwise-equal values (the identity ties of DESIGN.md R9).
+__device__ __forceinline__ double dot64(const float* __restrict__ a, const float* __restrict__ b, int d) {
+  double s = 0.0;
+  for (int j = 0; j < d; ++j) s = __fma_rn((double)__ldg(a + j), (double)__ldg(b + j), s);
+  return s;
+}
+
+// Order-preserving float <-> uint32 key (for radix selection).
+__device__ __forceinline__ uint32_t f2key(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+  uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+// Warp-aggregated append of one 64-bit record per active predicate into a global list.
+__device__ __forceinline__ void warp_append_u64(bool pred, uint64_t rec, unsigned long long* count,
+                                                uint64_t* list, int64_t cap) {
+  uint32_t bal = __ballot_sync(0xffffffffu, pred);
+  if (!bal) return;
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(bal) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(count, (unsigned long long)__popc(bal));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (pred) {
+    unsigned long long pos = base + __popc(bal & lanemask_lt());
+    if ((int64_t)pos < cap) list[pos] = rec;
+  }
+}
+
+__device__ __forceinline__ void warp_count(bool pred, unsigned long long* ctr) {
+  uint32_t bal = __ballot_sync(0xffffffffu, pred);
+  if ((threadIdx.x & 31) == __ffs(bal | 0x80000000u) - 1 && bal) atomicAdd(ctr, (unsigned long long)__popc(bal));
+}
+
+// ---------------------------------------------------------------------------------------
+// Filter error bound (SV Appendix D).  Users are scaled by 1/nu (nu ~ |u|),
+// items and queries by a power of two, both rounded to fp16; products are exact in fp32;
+// accumulation in fp32 (tensor core or FFMA).  For a = u/nu, b = p*2^e:
+//   |fl(a_hat . b_hat) - a.b| <= c1 * |b| + c2
+// c1 = 2^-10 (1 + 2^-9)            two fp16 roundings (2^-11 each) + fp32 pre-rounding of u/nu
+//    + (dpad + 4) * 2^-22          fp32 accumulation (4x the sequential fp32 bound)
+//    + 2^-25 sqrt(dpad)            fp16 subnormal absolute error of a, summed against |b|
+//    + 2^-20                       every fp32 evaluation of lo/hi/threshold arithmetic
+// c2 = 2^-24 sqrt(dpad)            fp16 subnormal absolute error of b, summed against |a| <= 1+
+// The GPU test "filter_error_bound" measures the observed error against this bound.
+inline double filter_c1(int dpad) {
+  return std::ldexp(1.0, -10) * (1.0 + std::ldexp(1.0, -9)) + (dpad + 4) * std::ldexp(1.0, -22) +
+         std::ldexp(1.0, -25) * std::sqrt((double)dpad) + std::ldexp(1.0, -20);
+}
+inline double filter_c2(int dpad) { return std::ldexp(1.0, -24) * std::sqrt((double)dpad); }
+
+}  // namespace rmips
+
+// ---------------------------------------------------------------------------------------
+// The index (opaque to callers).
+struct rmips_index_s {
+  int64_t n = 0, m = 0;
+  int d = 0, dpad = 0, kmax = 0, build_flags = 0;
+  int device = 0;
+  int64_t nblocks = 0;
+  int64_t overflow_rows = 0;
+  float pscale = 1.f;       // items are scaled by 2^e before fp16 rounding
+  double c1 = 0, c2 = 0;    // filter error constants (see common.cuh)
+
+  // norm-sorted stores (Alg. 1 line 5)
+  int32_t* perm_u = nullptr;   // [n] sorted position -> original user id
+  int32_t* perm_p = nullptr;   // [m] sorted position -> original item id
+  double* unorm = nullptr;     // [n] ||u|| fp64 (sorted order)
+  float* unu = nullptr;        // [n] nu = fp32 scale used to unit-normalise the fp16 user rows
+  double* pnorm = nullptr;     // [m] ||p|| fp64 (sorted order)
+  float* perr = nullptr;       // [m] filter error bound of item p in scaled score units
+  __half* U16 = nullptr;       // [n][dpad] fp16 u/nu (sorted)
+  float* U32 = nullptr;        // [n][d] fp32 u (sorted) -- exact path
+  __half* P16 = nullptr;       // [m][dpad] fp16 p*2^e (sorted)
+  float* P32 = nullptr;        // [m][d] fp32 p (sorted) -- exact path
+
+  // exact lower-bound arrays (Def. 4), column-major by rank: x[j*n + u]
+  double* tau = nullptr;       // [kmax][n] (j+1)-th largest u.p over P, fp64 (sorted users)
+  int32_t* ids = nullptr;      // [kmax][n] original item id of that value
+  float* thr = nullptr;        // [kmax][n] tau/nu in fp32 (filter threshold, unscaled)
+  float* tb = nullptr;         // [kmax][nblocks] Lemma 3: L^j(B) / ||u_first(B)||, rounded down
+
+  // build scratch (freed after build)
+  // query workspace (grown on demand)
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  int64_t pair_cap = 0;
+  unsigned long long* d_counters = nullptr;  // [kNumCounters + 4]
+  int* d_flags = nullptr;                    // [4]
+  rmips_stats_t stats{};
+  double phase_ms[16] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+};

@@ -1,0 +1,75 @@
+// internal.h -- host-side declarations shared between the rmips translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+#include <atomic>
+
+namespace rmips {
+
+// Kernel launches issued by this library (own kernels + CUB device-sort kernels), for the
+// bench's gpu_launches claim.  kCubSortKernels = kernels one CUB radix sort call launches
+// (counted from the ncu launch list, profiles/).
+extern std::atomic<long long> g_launches;
+constexpr int kCubSortKernels = 10;  // histogram + exclusive-sum + 8 onesweep passes (64-bit keys)
+inline void count_launch(int k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+// Scratch of one build call (owned by abi.cu, freed before rmips_build_index returns).
+struct BuildCtx {
+  rmips_index_s* idx = nullptr;
+  double* norm_u_raw = nullptr;   // [n] norms in original order
+  double* norm_p_raw = nullptr;   // [m]
+  int32_t* iota_u = nullptr;      // [n]
+  int32_t* iota_p = nullptr;      // [m]
+  unsigned int* maxabs = nullptr; // max |p_j| bits
+  float* scale_dev = nullptr;     // 2^e
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  int32_t* cand = nullptr;        // [n][kCand] candidate item positions
+  int32_t* ccount = nullptr;      // [n] candidates per row, -1 = overflowed
+  int32_t* ovf_list = nullptr;    // [n] overflowed rows
+  int* ovf_count = nullptr;       // device counter
+};
+
+size_t build_cub_bytes(int64_t n, int64_t m);
+cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t st);
+cudaError_t build_simt(const BuildCtx& c, cudaStream_t st);
+cudaError_t build_tc(const BuildCtx& c, cudaStream_t st);  // build_tc.cu; cudaErrorNotSupported if unusable
+cudaError_t build_select(BuildCtx& c, cudaStream_t st);
+cudaError_t build_fallback(BuildCtx& c, int nrows, double* scratch, int grid, cudaStream_t st);
+cudaError_t build_blocks(BuildCtx& c, cudaStream_t st);
+
+// Query workspace layout (carved from rmips_index_s::ws by abi.cu).
+struct QueryCtx {
+  rmips_index_s* idx = nullptr;
+  const float* q = nullptr;      // [b][d] caller's queries (device)
+  int b = 0, k = 0, flags = 0;
+  int nsub = 0;                  // sub-batches of kQB queries
+  // per sub-batch, sorted by norm descending (Alg. 3 line 1 computes ||q||)
+  __half* Q16 = nullptr;         // [nsub][kQB][dpad] fp16 q*2^eq (sorted)
+  float* qn = nullptr;           // [nsub][kQB] ||q|| rounded up (sorted; -1 padding)
+  float* qerr = nullptr;         // [nsub][kQB] filter error bound, scaled units
+  float* qscale = nullptr;       // [nsub] 2^eq
+  int32_t* qperm = nullptr;      // [nsub][kQB] sorted slot -> input query index (-1 padding)
+  int32_t* qcount = nullptr;     // [nsub] queries in the sub-batch
+  // outputs of the filter
+  unsigned long long* counters = nullptr;  // kNumCounters (+ accepted / undecided list sizes)
+  uint64_t* acc = nullptr;       // accepted keys (q_input << 32 | original user id)
+  uint64_t* und = nullptr;       // undecided (q_input << 32 | sorted user position)
+  int64_t cap = 0;               // capacity of acc and of und
+  uint64_t* acc_sorted = nullptr;
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  int* flags_dev = nullptr;
+};
+
+cudaError_t query_prep(QueryCtx& c, cudaStream_t st);
+cudaError_t query_filter_simt(QueryCtx& c, cudaStream_t st);
+cudaError_t query_filter_tc(QueryCtx& c, cudaStream_t st);  // query_tc.cu
+cudaError_t query_exact(QueryCtx& c, cudaStream_t st);
+cudaError_t query_output(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st);
+size_t query_cub_bytes(int64_t cap);
+cudaError_t query_sort(QueryCtx& c, int64_t total, int end_bit, cudaStream_t st);
+
+}  // namespace rmips

@@ -1,0 +1,362 @@
+// query.cu -- batched query evaluation (Alg. 3) except the tcgen05 filter.
+//
+//   Q1 k_query_prep      ||q|| (Alg. 3 line 1), norm sort of each 256-query tile, fp16 q*2^eq
+//   Q2+Q3 k_query_simt   Lemma 3 prefix + SIMT filter with Lemma 1
+//                        against tau_k, accept / reject / undecided (tcgen05 version: query_tc.cu)
+//   Q4 k_exact_decide    exact decision of undecided pairs from the exact top list (reading R8)
+//   Q5 k_verify_scan     Alg. 2 with Cor. 1-2, readings R3/R4 -- used
+//                        with RMIPS_FLAG_VERIFY_SCAN
+//   Q6 output            sort (query, original user id) keys; CSR offsets; copy to the caller
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace rmips {
+
+// ------------------------------------------------------------------------------ Q1
+__global__ void __launch_bounds__(kQB)
+k_query_prep(const float* __restrict__ q, int b, int d, int dpad, double c1, double c2, __half* __restrict__ Q16,
+             float* __restrict__ qn, float* __restrict__ qerr, float* __restrict__ qscale,
+             int32_t* __restrict__ qperm, int32_t* __restrict__ qcount, int* __restrict__ flags) {
+  __shared__ double nrm[kQB];
+  __shared__ float smax[kQB / 32];
+  __shared__ float s_scale;
+  const int s = blockIdx.x, t = threadIdx.x;
+  const int i = s * kQB + t;
+  const int cnt = min(kQB, b - s * kQB);
+  double nr = -1.0;
+  float mx = 0.f;
+  if (t < cnt) {
+    const float* x = q + (int64_t)i * d;
+    double acc = 0.0;
+    bool fin = true;
+    for (int j = 0; j < d; ++j) {
+      float v = x[j];
+      fin &= isfinite(v);
+      mx = fmaxf(mx, fabsf(v));
+      acc = __fma_rn((double)v, (double)v, acc);
+    }
+    nr = sqrt(acc);
+    if (!fin) atomicOr(flags, kFlagNonfinite), mx = 0.f, nr = 0.0;
+  }
+  nrm[t] = nr;
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((t & 31) == 0) smax[t >> 5] = mx;
+  __syncthreads();
+  if (t == 0) {
+    float m2 = 0.f;
+    for (int w = 0; w < kQB / 32; ++w) m2 = fmaxf(m2, smax[w]);
+    int ex = 0;
+    if (m2 > 0.f) frexpf(m2, &ex);
+    int e = max(-126, min(126, 14 - ex));
+    s_scale = ldexpf(1.f, e);
+    qscale[s] = s_scale;
+    qcount[s] = cnt;
+  }
+  __syncthreads();
+  // rank = position in (norm desc, index asc) order
+  int rank = t;
+  if (t < cnt) {
+    rank = 0;
+    for (int j = 0; j < cnt; ++j) {
+      double o = nrm[j];
+      rank += (o > nr) || (o == nr && j < t);
+    }
+  }
+  const float scale = s_scale;
+  const int64_t slot = (int64_t)s * kQB + rank;
+  if (t < cnt) {
+    qperm[slot] = i;
+    qn[slot] = __double2float_ru(nr * (1.0 + 1e-12));
+    qerr[slot] = __double2float_ru((c1 * nr * (double)scale + c2) * (1.0 + 1e-6));
+    const float* x = q + (int64_t)i * d;
+    for (int j = 0; j < dpad; ++j) Q16[slot * dpad + j] = __float2half_rn(j < d ? x[j] * scale : 0.f);
+  } else {
+    qperm[slot] = -1;
+    qn[slot] = -CUDART_INF_F;
+    qerr[slot] = 0.f;
+    for (int j = 0; j < dpad; ++j) Q16[slot * dpad + j] = __float2half_rn(0.f);
+  }
+}
+
+// Lemma 3 prefix of a (tile, sub-batch): #{slots < cnt : qn[slot] >= tbv}.  Queries are sorted
+// by norm descending, so the kept queries are exactly this prefix.
+__device__ __forceinline__ int lemma3_prefix(const float* qn_sub, int cnt, float tbv) {
+  int lo = 0, hi = cnt;  // first slot with qn < tbv
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (qn_sub[mid] >= tbv) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Classification of one (user, query) filter score.  acc ~ (u/nu).(q*2^eq);
+// thr_s = (tau_k/nu)*2^eq; E = qerr + |thr_s| 2^-22 (fp32 rounding of thr).
+// returns 0 reject (Lemma 1: u.q < tau_k), 1 accept (u.q >= tau_k), 2 undecided.
+__device__ __forceinline__ int classify(float acc, float thr_s, float qe) {
+  float E = __fadd_ru(qe, fabsf(thr_s) * 2.384185791015625e-07f);
+  if (__fadd_ru(acc, E) < thr_s) return 0;
+  if (__fsub_rd(acc, E) >= thr_s) return 1;
+  return 2;
+}
+
+// ------------------------------------------------------------------------------ Q2 + Q3 (SIMT)
+template <int DPAD>
+__global__ void __launch_bounds__(128)
+k_query_simt(const __half* __restrict__ U16, const float* __restrict__ thrk, const float* __restrict__ tbk,
+             const int32_t* __restrict__ perm_u, int64_t n, const __half* __restrict__ Q16,
+             const float* __restrict__ qn, const float* __restrict__ qerr, const float* __restrict__ qscale,
+             const int32_t* __restrict__ qperm, const int32_t* __restrict__ qcount, int flags,
+             unsigned long long* __restrict__ ctr, uint64_t* __restrict__ acc_list, uint64_t* __restrict__ und_list,
+             int64_t cap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __half2* us = reinterpret_cast<__half2*>(smem_raw);        // [DPAD/2][128]
+  __half2* qs = us + (DPAD / 2) * 128;                        // [kQB][DPAD/2]
+  __shared__ int s_len;
+  const int tile = blockIdx.x, s = blockIdx.y, tid = threadIdx.x;
+  const int cnt = qcount[s];
+  const float* qn_sub = qn + (int64_t)s * kQB;
+  if (tid == 0) {
+    float tbv = (flags & RMIPS_FLAG_NO_BLOCKS) ? -CUDART_INF_F : tbk[tile];
+    int len = lemma3_prefix(qn_sub, cnt, tbv);
+    s_len = len;
+    atomicAdd(ctr + C_BLOCK_PAIRS, (unsigned long long)cnt);
+    atomicAdd(ctr + C_BLOCK_PRUNED, (unsigned long long)(cnt - len));
+  }
+  __syncthreads();
+  const int len = s_len;
+  if (len == 0) return;
+  const int64_t row = (int64_t)tile * 128 + tid;
+  const bool live = row < n;
+  for (int i = tid; i < 128 * (DPAD / 2); i += 128) {
+    int r = i / (DPAD / 2), k2 = i % (DPAD / 2);
+    int64_t gr = (int64_t)tile * 128 + r;
+    us[k2 * 128 + r] = gr < n ? reinterpret_cast<const __half2*>(U16)[gr * (DPAD / 2) + k2]
+                              : __floats2half2_rn(0.f, 0.f);
+  }
+  const __half2* qsrc = reinterpret_cast<const __half2*>(Q16) + (int64_t)s * kQB * (DPAD / 2);
+  for (int i = tid; i < len * (DPAD / 2); i += 128) qs[i] = qsrc[i];
+  __syncthreads();
+  const float sc = qscale[s];
+  const float thr_s = live ? thrk[row] * sc : 0.f;
+  const uint64_t uo = live ? (uint64_t)(uint32_t)perm_u[row] : 0;
+  for (int q0 = 0; q0 < len; q0 += 8) {
+    float a8[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a8[j] = 0.f;
+    for (int k2 = 0; k2 < DPAD / 2; ++k2) {
+      float2 a = __half22float2(us[k2 * 128 + tid]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        int qq = min(q0 + j, len - 1);
+        float2 bq = __half22float2(qs[qq * (DPAD / 2) + k2]);
+        a8[j] = fmaf(a.x, bq.x, a8[j]);
+        a8[j] = fmaf(a.y, bq.y, a8[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int slot = q0 + j;
+      const bool ok = live && slot < len;
+      int cls = ok ? classify(a8[j], thr_s, qerr[(int64_t)s * kQB + slot]) : 0;
+      if ((flags & RMIPS_FLAG_FORCE_VERIFY) && cls == 1) cls = 2;
+      const uint64_t qin = ok ? (uint64_t)(uint32_t)qperm[(int64_t)s * kQB + slot] : 0;
+      warp_count(ok, ctr + C_SCORED);
+      warp_count(ok && cls == 0, ctr + C_REJECTED);
+      warp_count(ok && cls == 1, ctr + C_ACCEPT_FAST);
+      warp_append_u64(ok && cls == 1, (qin << 32) | uo, ctr + C_ACCEPTED_TOTAL, acc_list, cap);
+      warp_append_u64(ok && cls == 2, (qin << 32) | (uint64_t)row, ctr + C_UND_TOTAL, und_list, cap);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ Q4
+// u in R_k(q) <=> dot64(q, u) >= tau_k(u)  (reading R8; same dot routine as the build).
+__global__ void k_exact_decide(const float* __restrict__ q, const float* __restrict__ U32,
+                               const double* __restrict__ tauk, const int32_t* __restrict__ perm_u, int d,
+                               unsigned long long* __restrict__ ctr, const uint64_t* __restrict__ und_list,
+                               uint64_t* __restrict__ acc_list, int64_t cap) {
+  const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_UND_TOTAL]);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < total; base += stride) {
+    int64_t i = base + threadIdx.x;
+    bool ok = i < total;
+    bool yes = false;
+    uint64_t key = 0;
+    if (ok) {
+      uint64_t rec = und_list[i];
+      uint32_t qin = (uint32_t)(rec >> 32);
+      int64_t row = (int64_t)(rec & 0xffffffffu);
+      double g = dot64(q + (int64_t)qin * d, U32 + row * d, d);
+      yes = g >= tauk[row];
+      key = ((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row];
+    }
+    warp_count(ok, ctr + C_UNDECIDED);
+    warp_count(yes, ctr + C_EXACT_ACCEPT);
+    warp_append_u64(yes, key, ctr + C_ACCEPTED_TOTAL, acc_list, cap);
+  }
+}
+
+// ------------------------------------------------------------------------------ Q5
+// Alg. 2 for one undecided pair per warp.  Items are streamed in norm-descending order
+// (Alg. 1 line 5) 32 at a time: the warp stages the 32 item rows in shared memory with
+// coalesced 16-byte loads (consecutive sorted rows are contiguous), then lane j evaluates
+// gamma_j = p_j.u with dot64.  Corollary 1 (yes): u.q >= ||u|| ||p_j|| (rounded up to cover the
+// fp64 rounding of every later gamma) means no later item can beat q.  Corollary 2 (no): once
+// k items have gamma > u.q (the k-th value tau of I exceeds u.q).  Falling off the end: yes (R4).
+constexpr int kScanWarps = 4;
+constexpr int kScanPitch = 257;  // floats per staged item row (d <= 256), odd => conflict-free
+__global__ void __launch_bounds__(32 * kScanWarps)
+k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const double* __restrict__ unorm,
+              const float* __restrict__ P32, const double* __restrict__ pnorm, const int32_t* __restrict__ perm_u,
+              int64_t m, int d, int k, unsigned long long* __restrict__ ctr, const uint64_t* __restrict__ und_list,
+              uint64_t* __restrict__ acc_list, int64_t cap) {
+  extern __shared__ float sp[];  // [kScanWarps][32][kScanPitch]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* my = sp + (size_t)w * 32 * kScanPitch;
+  const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_UND_TOTAL]);
+  const double slack = 1.0 + (d + 8) * 2.220446049250313e-16;
+  for (int64_t i = blockIdx.x * (int64_t)kScanWarps + w; i < total; i += (int64_t)gridDim.x * kScanWarps) {
+    uint64_t rec = und_list[i];
+    uint32_t qin = (uint32_t)(rec >> 32);
+    int64_t row = (int64_t)(rec & 0xffffffffu);
+    const float* u = U32 + row * d;
+    const double uq = dot64(q + (int64_t)qin * d, u, d);
+    const double un = unorm[row] * slack;
+    int beats = 0;
+    int64_t scanned = 0;
+    bool yes = true, decided = false;
+    for (int64_t base = 0; base < m && !decided; base += 32) {
+      const int nrow = (int)min((int64_t)32, m - base);
+      // Corollary 1 on the first item of the chunk (lane-parallel over the chunk below)
+      const float* src = P32 + base * d;
+      __syncwarp();
+      for (int e = lane; e < nrow * d; e += 32) my[(e / d) * kScanPitch + (e % d)] = __ldg(src + e);
+      __syncwarp();
+      const int64_t j = base + lane;
+      bool in = lane < nrow;
+      bool cor1 = in && (uq >= un * pnorm[j] * slack);
+      uint32_t ycut = __ballot_sync(0xffffffffu, cor1);   // first lane where Cor. 1 fires
+      int lim = ycut ? (__ffs(ycut) - 1) : nrow;
+      bool eval = lane < lim;
+      bool beat = false;
+      if (eval) {
+        double g = 0.0;
+        const float* pr = my + lane * kScanPitch;
+        for (int t = 0; t < d; ++t) g = __fma_rn((double)pr[t], (double)__ldg(u + t), g);
+        beat = g > uq;
+      }
+      scanned += lim;
+      uint32_t bb = __ballot_sync(0xffffffffu, beat);
+      // Alg. 2 visits items in order: the k-th beat (if any) at lane position decides "no"
+      int nb = __popc(bb);
+      if (beats + nb >= k) { yes = false; decided = true; }
+      else if (ycut) { yes = true; decided = true; }
+      beats += nb;
+    }
+    if (lane == 0) {
+      atomicAdd(ctr + C_SCANS, 1ull);
+      atomicAdd(ctr + C_ITEMS_SCANNED, (unsigned long long)scanned);
+      atomicAdd(ctr + C_UNDECIDED, 1ull);
+      if (yes) {
+        atomicAdd(ctr + C_EXACT_ACCEPT, 1ull);
+        unsigned long long pos = atomicAdd(ctr + C_ACCEPTED_TOTAL, 1ull);
+        if ((int64_t)pos < cap) acc_list[pos] = ((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ Q6
+__global__ void k_offsets(const uint64_t* __restrict__ keys, int64_t total, int b, int64_t* __restrict__ offsets) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > b) return;
+  uint64_t target = (uint64_t)i << 32;
+  int64_t lo = 0, hi = total;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  offsets[i] = lo;
+}
+
+__global__ void k_copy_ids(const uint64_t* __restrict__ keys, int64_t total, int32_t* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < total) out[i] = (int32_t)(keys[i] & 0xffffffffu);
+}
+
+// ------------------------------------------------------------------------------ host side
+static inline unsigned nblk(int64_t work, int t) { return (unsigned)((work + t - 1) / t); }
+
+cudaError_t query_prep(QueryCtx& c, cudaStream_t st) {
+  rmips_index_s* x = c.idx;
+  k_query_prep<<<c.nsub, kQB, 0, st>>>(c.q, c.b, x->d, x->dpad, x->c1, x->c2, c.Q16, c.qn, c.qerr, c.qscale, c.qperm,
+                                       c.qcount, c.flags_dev); count_launch();
+  return cudaGetLastError();
+}
+
+template <int DPAD>
+static cudaError_t launch_query_simt(QueryCtx& c, cudaStream_t st) {
+  rmips_index_s* x = c.idx;
+  size_t smem = (size_t)(DPAD / 2) * 128 * 4 + (size_t)kQB * (DPAD / 2) * 4;
+  cudaError_t e = cudaFuncSetAttribute(k_query_simt<DPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)x->nblocks, (unsigned)c.nsub);
+  k_query_simt<DPAD><<<grid, 128, smem, st>>>(x->U16, x->thr + (int64_t)(c.k - 1) * x->n,
+                                              x->tb + (int64_t)(c.k - 1) * x->nblocks, x->perm_u, x->n, c.Q16, c.qn,
+                                              c.qerr, c.qscale, c.qperm, c.qcount, c.flags, c.counters, c.acc, c.und,
+                                              c.cap); count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t query_filter_simt(QueryCtx& c, cudaStream_t st) {
+  if (c.idx->n == 0) return cudaSuccess;
+  switch (c.idx->dpad) {
+    case 64: return launch_query_simt<64>(c, st);
+    case 128: return launch_query_simt<128>(c, st);
+    case 192: return launch_query_simt<192>(c, st);
+    case 256: return launch_query_simt<256>(c, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t query_exact(QueryCtx& c, cudaStream_t st) {
+  rmips_index_s* x = c.idx;
+  if (x->n == 0) return cudaSuccess;
+  if (c.flags & RMIPS_FLAG_VERIFY_SCAN) {
+    size_t smem = (size_t)kScanWarps * 32 * kScanPitch * 4;
+    cudaError_t e = cudaFuncSetAttribute(k_verify_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_verify_scan<<<148 * 4, 32 * kScanWarps, smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
+                                                           x->d, c.k, c.counters, c.und, c.acc, c.cap); count_launch();
+  } else {
+    k_exact_decide<<<148 * 8, 256, 0, st>>>(c.q, x->U32, x->tau + (int64_t)(c.k - 1) * x->n, x->perm_u, x->d,
+                                            c.counters, c.und, c.acc, c.cap); count_launch();
+  }
+  return cudaGetLastError();
+}
+
+size_t query_cub_bytes(int64_t cap) {
+  size_t a = 0;
+  cub::DeviceRadixSort::SortKeys((void*)nullptr, a, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int)cap, 0, 64);
+  return a;
+}
+
+// total = number of accepted keys (host-known after the mid-call sync).
+cudaError_t query_sort(QueryCtx& c, int64_t total, int end_bit, cudaStream_t st) {
+  size_t tb = c.cub_bytes;
+  if (total == 0) return cudaSuccess;
+  count_launch(kCubSortKernels);
+  return cub::DeviceRadixSort::SortKeys(c.cub_tmp, tb, c.acc, c.acc_sorted, (int)total, 0, end_bit, st);
+}
+
+cudaError_t query_output(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st) {
+  // offsets from the sorted keys; ids copied only if they fit
+  const int64_t total = c.idx->stats.result_total;
+  k_offsets<<<nblk(c.b + 1, 256), 256, 0, st>>>(c.acc_sorted, total, c.b, offsets); count_launch();
+  if (total <= capacity && total > 0) k_copy_ids<<<nblk(total, 256), 256, 0, st>>>(c.acc_sorted, total, user_ids); count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace rmips

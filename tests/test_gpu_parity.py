@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by element.
+
+The bar (BASELINE north star): identical user-id sets; any disagreement must be a borderline
+user (|q.u - tau_k(u)| <= 1e-5 |q||u|, reading R9) and there must be none on configs[0].  In
+practice the exact fp64 path leaves no disagreement anywhere, which is what these tests assert.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth import generator as gen
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+from paper_2110_07131_b200 import rmips  # noqa: E402
+
+DEV = torch.device("cuda:0")
+BUILDS = [("tc", rmips.RMIPS_BUILD_DEFAULT), ("simt", rmips.RMIPS_BUILD_SIMT)]
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(DEV)
+
+
+def gpu_sets(U, P, Qy, k, k_max, build_flags=0, qflags=0, idx=None):
+    own = idx is None
+    if own:
+        idx = rmips.rmips_build_index(_t(U), _t(P), k_max, build_flags)
+    off, ids = rmips.rmips_query(idx, _t(Qy), k, qflags)
+    sets = rmips.split_sets(off, ids)
+    if own:
+        idx.close()
+    return sets
+
+
+def assert_same(got, member, U=None, P=None, Qy=None, k=None, label=""):
+    want = oracle.sets_from_member(member)
+    assert len(got) == len(want)
+    bad = []
+    for i, (g, w) in enumerate(zip(got, want)):
+        assert (np.diff(g) > 0).all(), "ids not strictly ascending (query %d)" % i
+        if not np.array_equal(g, w):
+            bad.append((i, np.setxor1d(g, w)))
+    if bad and U is not None:
+        pairs = np.array([(i, u) for i, us in bad for u in us])
+        mu = oracle.margins(U, P, Qy, pairs, k)
+        raise AssertionError("%s: %d disagreements on %d queries; margins %s" % (label, len(pairs), len(bad), mu[:10]))
+    assert not bad, label
+
+
+# ---------------------------------------------------------------- configs[0] (whole config, naive oracle)
+
+@pytest.fixture(scope="module")
+def cfg0():
+    w = gen.make_workload(0)
+    member = oracle.rkmips_naive(w.U, w.P, w.Qy, 10)
+    return w, member
+
+
+@pytest.mark.parametrize("name,bf", BUILDS)
+def test_cfg0_full_parity(cfg0, name, bf):
+    w, member = cfg0
+    got = gpu_sets(w.U, w.P, w.Qy, 10, 10, bf)
+    assert_same(got, member, w.U, w.P, w.Qy, 10, "cfg0/" + name)
+
+
+def test_cfg0_index_tables_bitwise(cfg0):
+    """T6: exported tau equals the oracle's exact top list bit for bit (reading R7); ids equal."""
+    w, _ = cfg0
+    idx = rmips.rmips_build_index(_t(w.U), _t(w.P), 10)
+    pu, pp, tau, ids = idx.export()
+    vals, oids = oracle.topk(w.U, w.P, 10)
+    assert np.array_equal(tau.T, vals)
+    assert np.array_equal(ids.T, oids)
+    assert np.array_equal(pu, oracle.sort_by_norm_desc(oracle.norms(w.U)))
+    assert np.array_equal(pp, oracle.sort_by_norm_desc(oracle.norms(w.P)))
+    assert idx.overflow_rows == 0
+    idx.close()
+
+
+@pytest.mark.parametrize("qflags", [rmips.RMIPS_FLAG_NO_BLOCKS, rmips.RMIPS_FLAG_VERIFY_SCAN,
+                                    rmips.RMIPS_FLAG_FORCE_VERIFY,
+                                    rmips.RMIPS_FLAG_FORCE_VERIFY | rmips.RMIPS_FLAG_VERIFY_SCAN,
+                                    rmips.RMIPS_FLAG_SIMT])
+def test_cfg0_query_modes_agree(cfg0, qflags):
+    w, member = cfg0
+    got = gpu_sets(w.U, w.P, w.Qy, 10, 10, 0, qflags)
+    assert_same(got, member, w.U, w.P, w.Qy, 10, "cfg0 flags=%d" % qflags)
+
+
+def test_cfg0_every_k_and_invariant(cfg0):
+    """Queries over ALL of P: every user appears in exactly k sets (north-star invariant)."""
+    w, _ = cfg0
+    idx = rmips.rmips_build_index(_t(w.U), _t(w.P), 10)
+    vals, _ = oracle.topk(w.U, w.P, 10)
+    for k in (1, 3, 10):
+        off, ids = rmips.rmips_query(idx, _t(w.P), k)
+        counts = np.bincount(ids.cpu().numpy(), minlength=w.U.shape[0])
+        assert (counts == k).all(), k
+        member = oracle.rkmips_twophase(w.U, vals, w.P, k)
+        assert_same(rmips.split_sets(off, ids), member, label="all-P k=%d" % k)
+    idx.close()
+
+
+# ---------------------------------------------------------------- random small instances, ragged shapes
+
+CASES = [
+    # seed, n, m, d, k_max, k, dist, nq
+    (1, 129, 33, 8, 10, 3, "gaussian", 20),
+    (2, 300, 70, 50, 25, 10, "skewed", 30),
+    (3, 257, 200, 65, 16, 16, "uniform", 25),
+    (4, 500, 300, 2, 5, 1, "gaussian", 40),
+    (5, 64, 40, 1, 4, 2, "gaussian", 10),
+    (6, 400, 150, 200, 50, 50, "skewed", 16),
+    (7, 1000, 600, 50, 10, 5, "uniform", 30),
+    (8, 130, 7, 12, 10, 9, "gaussian", 12),     # m < k_max, k > m
+    (9, 333, 250, 128, 20, 7, "skewed", 20),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[str(c[0]) for c in CASES])
+@pytest.mark.parametrize("name,bf", BUILDS)
+def test_random_instances(case, name, bf):
+    seed, n, m, d, kmax, k, dist, nq = case
+    U, P = gen.random_instance(seed, n, m, d, dist)
+    fresh, _ = gen.random_instance(seed + 1000, nq - nq // 2, 1, d, dist)
+    Qy = np.concatenate([P[: nq // 2], fresh])
+    member = oracle.rkmips_naive(U, P, Qy, k)
+    got = gpu_sets(U, P, Qy, k, kmax, bf)
+    assert_same(got, member, U, P, Qy, k, "case %d/%s" % (seed, name))
+
+
+def test_duplicate_items_and_ties():
+    """Many identical items force candidate-buffer overflow -> exact fallback rows."""
+    U, P = gen.random_instance(11, 300, 40, 16, "gaussian")
+    P = np.concatenate([P] + [P[:3]] * 60)        # 180 copies of 3 items
+    Qy = np.concatenate([P[:5], P[100:103]])
+    member = oracle.rkmips_naive(U, P, Qy, 7)
+    idx = rmips.rmips_build_index(_t(U), _t(P), 20)
+    got = rmips.split_sets(*rmips.rmips_query(idx, _t(Qy), 7))
+    assert_same(got, member, U, P, Qy, 7, "dups")
+    _, _, tau, _ = idx.export()
+    vals, _ = oracle.topk(U, P, 20)
+    assert np.array_equal(tau.T, vals)
+    idx.close()
+
+
+def test_zero_vectors_and_all_equal_norms():
+    rng = np.random.default_rng(12)
+    U = rng.standard_normal((200, 10)).astype(np.float32)
+    U[::7] = 0.0
+    P = rng.standard_normal((90, 10)).astype(np.float32)
+    P /= np.linalg.norm(P, axis=1, keepdims=True)       # all item norms ~equal
+    P[5] = 0.0
+    Qy = np.concatenate([P[:6], np.zeros((1, 10), np.float32), -P[:3]])
+    for k in (1, 4):
+        member = oracle.rkmips_naive(U, P, Qy, k)
+        assert_same(gpu_sets(U, P, Qy, k, 8), member, U, P, Qy, k, "zeros k=%d" % k)
+
+
+def test_huge_norm_range():
+    """Norms over ~2^40 (fp16 subnormal range for small items) stay exact."""
+    rng = np.random.default_rng(13)
+    U = (rng.standard_normal((300, 20)) * np.exp(rng.normal(0, 6, (300, 1)))).astype(np.float32)
+    P = (rng.standard_normal((200, 20)) * np.exp(rng.normal(0, 6, (200, 1)))).astype(np.float32)
+    Qy = np.concatenate([P[:10], (rng.standard_normal((10, 20)) * 1e-3).astype(np.float32)])
+    member = oracle.rkmips_naive(U, P, Qy, 5)
+    assert_same(gpu_sets(U, P, Qy, 5, 10), member, U, P, Qy, 5, "norm range")
+
+
+# ---------------------------------------------------------------- boundary behaviour
+
+def test_empty_users_and_empty_batch():
+    _, P = gen.random_instance(14, 1, 30, 8)
+    idx = rmips.rmips_build_index(None, _t(P), 5)
+    off, ids = rmips.rmips_query(idx, _t(P[:4]), 3)
+    assert off.cpu().tolist() == [0] * 5 and ids.numel() == 0
+    off, ids = rmips.rmips_query(idx, torch.zeros((0, 8), dtype=torch.float32, device=DEV), 3)
+    assert off.numel() == 1 and ids.numel() == 0
+    idx.close()
+
+
+def test_errors_k_range_nonfinite_capacity():
+    U, P = gen.random_instance(15, 100, 30, 8)
+    idx = rmips.rmips_build_index(_t(U), _t(P), 5)
+    with pytest.raises(rmips.RmipsError) as e:
+        rmips.rmips_query(idx, _t(P[:2]), 6)
+    assert e.value.status == rmips.RMIPS_ERR_K_RANGE
+    bad = P[:2].copy()
+    bad[1, 3] = np.nan
+    with pytest.raises(rmips.RmipsError) as e:
+        rmips.rmips_query(idx, _t(bad), 2)
+    assert e.value.status == rmips.RMIPS_ERR_NONFINITE
+    with pytest.raises(rmips.RmipsError) as e:
+        rmips.rmips_query(idx, _t(P[:10]), 5, capacity=1)
+    assert e.value.status == rmips.RMIPS_ERR_CAPACITY
+    Ub = U.copy()
+    Ub[3, 0] = np.inf
+    with pytest.raises(rmips.RmipsError) as e:
+        rmips.rmips_build_index(_t(Ub), _t(P), 5)
+    assert e.value.status == rmips.RMIPS_ERR_NONFINITE
+    idx.close()
+
+
+def test_host_variants_match_device():
+    U, P = gen.random_instance(16, 400, 120, 50)
+    Qy = P[:30]
+    idx_d = rmips.rmips_build_index(_t(U), _t(P), 10)
+    idx_h = rmips.rmips_build_index_host(U, P, 10)
+    a = rmips.split_sets(*rmips.rmips_query(idx_d, _t(Qy), 4))
+    off, ids = rmips.rmips_query_host(idx_h, Qy, 4)
+    b = [ids[off[i]:off[i + 1]] for i in range(len(off) - 1)]
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    idx_d.close()
+    idx_h.close()
+
+
+def test_stats_counters_consistent(cfg0):
+    w, member = cfg0
+    idx = rmips.rmips_build_index(_t(w.U), _t(w.P), 10)
+    rmips.rmips_query(idx, _t(w.Qy), 10)
+    s = idx.stats()
+    assert s["queries"] == 100
+    assert s["result_total"] == int(member.sum())
+    assert s["pairs_scored"] == s["pairs_rejected"] + s["pairs_accepted_fast"] + s["pairs_undecided"]
+    assert s["result_total"] == s["pairs_accepted_fast"] + s["pairs_exact_accepted"]
+    assert s["block_query_pairs"] == 100 * ((idx.n + 127) // 128)
+    idx.close()
+
+
+# ---------------------------------------------------------------- configs[1] at full size (sampled oracle)
+
+def test_cfg1_full_size_sampled():
+    """BJ configs[1] at full size, in the bench's launch configuration (all 1,000 queries in one
+    call).  The oracle checks a fixed sample of 1,500 users: exact top lists (two-phase form,
+    equal to the definition by reading R8) and every query's decision for those users."""
+    w = gen.make_workload(1)
+    idx = rmips.rmips_build_index(_t(w.U), _t(w.P), 50)
+    off, ids = rmips.rmips_query(idx, _t(w.Qy), 10)
+    sets = rmips.split_sets(off, ids)
+    rng = np.random.default_rng(0)
+    sample = np.sort(rng.choice(w.U.shape[0], 1500, replace=False))
+    vals, oids = oracle.topk(w.U[sample], w.P, 50)
+    _, _, tau, tids = idx.export()
+    assert np.array_equal(tau[:, sample].T, vals)
+    member = oracle.rkmips_twophase(w.U[sample], vals, w.Qy, 10)
+    for qi in range(w.Qy.shape[0]):
+        got = np.intersect1d(sets[qi], sample)
+        want = sample[member[qi]]
+        assert np.array_equal(got, want), qi
+    # invariant-style global check: totals are plausible and ids ascending
+    assert all((np.diff(s) > 0).all() for s in sets)
+    idx.close()
