@@ -100,13 +100,12 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
              int64_t n, int64_t m, int kmax, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
              int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* cv = reinterpret_cast<float*>(smem_raw);            // [128][kCandPitch]
-  int* ci = reinterpret_cast<int*>(cv + 128 * kCandPitch);   // [128][kCandPitch]
-  __half2* us = reinterpret_cast<__half2*>(ci + 128 * kCandPitch);  // [DPAD/2][128]
+  float* clo = reinterpret_cast<float*>(smem_raw);           // [kCand][128]
+  int* cid = reinterpret_cast<int*>(clo + 128 * kCand);      // [kCand][128]
+  __half2* us = reinterpret_cast<__half2*>(cid + 128 * kCand);  // [DPAD/2][128]
   float* ps = reinterpret_cast<float*>(us + (DPAD / 2) * 128);      // [DPAD][32]
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5;
   const int64_t row = blockIdx.x * (int64_t)128 + tid;
   const bool live = row < n;
   // stage this CTA's 128 user rows, transposed, as half2 pairs
@@ -117,10 +116,7 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
     if (gr < n) v = reinterpret_cast<const __half2*>(U16)[gr * (DPAD / 2) + k2];
     us[k2 * 128 + r] = v;
   }
-  CandRow me{-__int_as_float(0x7f800000), 0};
-  bool ovf = false;
-  float* wcv = cv + warp * 32 * kCandPitch;
-  int* wci = ci + warp * 32 * kCandPitch;
+  CandRow me{live ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000), 0, false};
 
   for (int64_t base = 0; base < m; base += 32) {
     __syncthreads();
@@ -153,16 +149,13 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
       }
     }
     const float NEG = -__int_as_float(0x7f800000);
-    float mx = NEG;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (!live || base + j >= m) s[j] = NEG;
-      mx = fmaxf(mx, s[j]);
-    }
+    for (int j = 0; j < 32; ++j)
+      if (base + j >= m) s[j] = NEG;
     float E = __ldg(perr + base);
-    cand_chunk([&](int j) { return s[j]; }, mx, E, (int)base, me, wcv, wci, perr, kmax, &ovf);
+    cand_chunk([&](int j) { return s[j]; }, E, (int)base, me, clo, cid, tid, perr, kmax);
   }
-  cand_finish(me, wcv, wci, perr, kmax, &ovf, row, n, cand, ccount, ovf_list, ovf_count);
+  cand_finish(me, clo, cid, tid, perr, kmax, row, n, cand, ccount, ovf_list, ovf_count);
 }
 
 // ------------------------------------------------------------------------------ B5
@@ -296,7 +289,7 @@ static inline unsigned nblk(int64_t work, int t) { return (unsigned)((work + t -
 
 template <int DPAD>
 static cudaError_t launch_build_simt(const BuildCtx& c, cudaStream_t st) {
-  size_t smem = (size_t)128 * kCandPitch * 8 + (DPAD / 2) * 128 * 4 + DPAD * 32 * 4;
+  size_t smem = (size_t)128 * kCand * 8 + (DPAD / 2) * 128 * 4 + DPAD * 32 * 4;
   cudaError_t e = cudaFuncSetAttribute(k_build_simt<DPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_build_simt<DPAD><<<nblk(c.idx->n, 128), 128, smem, st>>>(c.idx->U16, c.idx->P16, c.idx->perr, c.idx->n,

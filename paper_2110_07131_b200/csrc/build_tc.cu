@@ -35,8 +35,8 @@ struct Smem {
   static constexpr int A = 0;                              // KB tiles
   static constexpr int B(int KB) { return KB * kTileBytes; }
   static constexpr int CV(int KB) { return B(KB) + kStages * KB * kTileBytes; }
-  static constexpr int CI(int KB) { return CV(KB) + kBM * kCandPitch * 4; }
-  static constexpr int BAR(int KB) { return CI(KB) + kBM * kCandPitch * 4; }
+  static constexpr int CI(int KB) { return CV(KB) + kBM * kCand * 4; }
+  static constexpr int BAR(int KB) { return CI(KB) + kBM * kCand * 4; }
   static constexpr int TOTAL(int KB) { return BAR(KB) + 256 + 1024; }  // + alignment slack
 };
 
@@ -53,8 +53,8 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
   const uint32_t sbase = smem_u32(smem);
   const uint32_t sA = sbase + Smem::A;
   const uint32_t sB = sbase + Smem::B(KB);
-  float* cv = reinterpret_cast<float*>(smem + Smem::CV(KB));
-  int* ci = reinterpret_cast<int*>(smem + Smem::CI(KB));
+  float* clo = reinterpret_cast<float*>(smem + Smem::CV(KB));  // [kCand][128] candidate lower bounds
+  int* cid = reinterpret_cast<int*>(smem + Smem::CI(KB));      // [kCand][128] candidate item positions
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::BAR(KB));
   // barrier indices
   const uint32_t bar0 = smem_u32(bars);
@@ -92,11 +92,11 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       uint32_t ph = 0;
       int t = 0;
       for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
-        if (t > 0) mbar_wait(BAR(A_EMPTY), (t - 1) & 1);
+        if (t > 0) mbar_wait_sleep(BAR(A_EMPTY), (t - 1) & 1);
         mbar_arrive_expect_tx(BAR(A_FULL), KB * kTileBytes);
         for (int kb = 0; kb < KB; ++kb) tma_load_2d(sA + kb * kTileBytes, &tmA, kb * 64, ut * kBM, BAR(A_FULL));
         for (int it = 0; it < nit; ++it) {
-          mbar_wait(BAR(B_EMPTY + stage), ph ^ 1);
+          mbar_wait_sleep(BAR(B_EMPTY + stage), ph ^ 1);
           mbar_arrive_expect_tx(BAR(B_FULL + stage), KB * kTileBytes);
           for (int kb = 0; kb < KB; ++kb)
             tma_load_2d(sB + (stage * KB + kb) * kTileBytes, &tmB, kb * 64, it * kBN, BAR(B_FULL + stage));
@@ -112,11 +112,11 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       uint32_t ph = 0, aph = 0;
       int t = 0;
       for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
-        mbar_wait(BAR(A_FULL), t & 1);
+        mbar_wait_sleep(BAR(A_FULL), t & 1);
         tc_fence_after();
         for (int it = 0; it < nit; ++it) {
-          mbar_wait(BAR(ACC_EMPTY + as), aph ^ 1);
-          mbar_wait(BAR(B_FULL + stage), ph);
+          mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
+          mbar_wait_sleep(BAR(B_FULL + stage), ph);
           tc_fence_after();
           const uint32_t d = tmem + as * kBN;
 #pragma unroll
@@ -139,46 +139,68 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     // ------------------------------------------------ epilogue: one thread per user row
     const int q = warp & 3;                    // TMEM lane quadrant of this warp
     const int rloc = q * 32 + lane;            // row within the tile
-    float* wcv = cv + q * 32 * kCandPitch;
-    int* wci = ci + q * 32 * kCandPitch;
     const float NEG = -__int_as_float(0x7f800000);
+    const float POS = __int_as_float(0x7f800000);
+    const int mi = (int)m;
     int as = 0;
     uint32_t aph = 0;
     for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x) {
       const int64_t row = (int64_t)ut * kBM + rloc;
-      const bool live = row < n;
-      CandRow me{NEG, 0};
-      bool ovf = false;
+      // dead rows (user >= n) have theta = +inf and never pass
+      CandRow me{row < n ? NEG : POS, 0, false};
       for (int it = 0; it < nit; ++it) {
+        const int base0 = it * kBN;
+        float E[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) E[c] = (base0 + 32 * c < mi) ? __ldg(perr + base0 + 32 * c) : 0.f;
         mbar_wait(BAR(ACC_FULL + as), aph);
         tc_fence_after();
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + as * kBN;
-#pragma unroll 1
-        for (int c = 0; c < kBN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c * 32, r);
-          tmem_ld_wait();
-          if (c == kBN / 32 - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
-          }
-          const int64_t base = (int64_t)it * kBN + c * 32;
-          if (base >= m) continue;             // warp-uniform: whole chunk is padding
-          float s[32];
-          float mx = NEG;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            s[j] = __uint_as_float(r[j]);
-            if (!live || base + j >= m) s[j] = NEG;
-            mx = fmaxf(mx, s[j]);
-          }
-          const float E = __ldg(perr + base);
-          cand_chunk([&](int j) { return s[j]; }, mx, E, (int)base, me, wcv, wci, perr, kmax, &ovf);
-        }
+        // all 128 columns of the tile in one go: 4 TMEM loads in flight, one wait
+        uint32_t r[4][32];
+        tmem_ld32(taddr, r[0]);
+        tmem_ld32(taddr + 32, r[1]);
+        tmem_ld32(taddr + 64, r[2]);
+        tmem_ld32(taddr + 96, r[3]);
+        tmem_ld_wait(r[0]);
+        reg_fence(r[1]);
+        reg_fence(r[2]);
+        reg_fence(r[3]);
+        tc_fence_before();  // this accumulator stage is fully read: hand it back to the MMA warp
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
         if (++as == kAcc) as = 0, aph ^= 1;
+        if (base0 + kBN > mi) {  // last item tile only (warp-uniform): mask padding columns
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (base0 + 32 * c + j >= mi) r[c][j] = __float_as_uint(NEG);
+        }
+        // 4 independent max trees (3-input FMNMX), one compare per chunk
+        float g4[4][8];
+        bool pass[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            g4[c][g] = fmaxf(fmaxf(__uint_as_float(r[c][4 * g]), __uint_as_float(r[c][4 * g + 1])),
+                             fmaxf(__uint_as_float(r[c][4 * g + 2]), __uint_as_float(r[c][4 * g + 3])));
+          const float mx = fmaxf(fmaxf(fmaxf(g4[c][0], g4[c][1]), fmaxf(g4[c][2], g4[c][3])),
+                                 fmaxf(fmaxf(g4[c][4], g4[c][5]), fmaxf(g4[c][6], g4[c][7])));
+          pass[c] = __fadd_ru(mx, E[c]) >= me.theta;
+        }
+        if (!__any_sync(0xffffffffu, pass[0] | pass[1] | pass[2] | pass[3])) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (!__any_sync(0xffffffffu, pass[c])) continue;
+          if (pass[c])
+            cand_append_chunk([&](int j) { return __uint_as_float(r[c][j]); }, g4[c], E[c], base0 + 32 * c, me, clo,
+                              cid, rloc);
+          cand_maybe_refresh(me, clo, cid, rloc, perr, kmax);
+        }
       }
-      cand_finish(me, wcv, wci, perr, kmax, &ovf, row, n, cand, ccount, ovf_list, ovf_count);
+      cand_finish(me, clo, cid, rloc, perr, kmax, row, n, cand, ccount, ovf_list, ovf_count);
       __syncwarp();
     }
   }
