@@ -86,6 +86,7 @@ typedef struct {
   int64_t scans;                /* Alg. 2 scans run (VERIFY_SCAN) */
   int64_t items_scanned;        /* items whose u.p the scans evaluated */
   int64_t result_total;         /* sum over queries of |R(q)| */
+  int64_t filter_kernel;        /* 1 = tcgen05 filter (query_tc.cu), 0 = SIMT filter */
 } rmips_stats_t;
 
 /* rmips_build_index -- Alg. 1 (PAPER.md 267-298) with L_i over all of P.

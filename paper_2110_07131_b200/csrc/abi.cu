@@ -352,6 +352,7 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
       if (x->n > 0) {
         cudaError_t e = cudaErrorNotSupported;
         if (!(flags & RMIPS_FLAG_SIMT) && !(x->build_flags & RMIPS_BUILD_SIMT)) e = query_filter_tc(c, st);
+        x->stats.filter_kernel = (e != cudaErrorNotSupported);
         if (e == cudaErrorNotSupported) {
           cudaGetLastError();
           e = query_filter_simt(c, st);
@@ -375,6 +376,7 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
       if (attempt == 2) return fail(RMIPS_ERR_CUDA, "pair workspace did not converge");
     }
     rmips_stats_t& S = x->stats;
+    S.queries = b;
     S.block_query_pairs = hc[C_BLOCK_PAIRS];
     S.block_query_pruned = hc[C_BLOCK_PRUNED];
     S.pairs_scored = hc[C_SCORED];

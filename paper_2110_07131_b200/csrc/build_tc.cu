@@ -226,13 +226,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 }  // namespace
 
-// 2-D fp16 tensor [rows][cols] (cols contiguous), box = 128 rows x 64 columns, SWIZZLE_128B.
-bool make_tmap_f16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols) {
+// 2-D fp16 tensor [rows][cols] (cols contiguous), box = box_rows rows x 64 columns, SWIZZLE_128B.
+bool make_tmap_f16_box(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -254,8 +254,8 @@ template <int KB>
 static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   CUtensorMap ta, tb;
-  if (!make_tmap_f16(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->dpad)) return cudaErrorNotSupported;
-  if (!make_tmap_f16(&tb, x->P16, (uint64_t)x->m, (uint64_t)x->dpad)) return cudaErrorNotSupported;
+  if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM)) return cudaErrorNotSupported;
+  if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)x->m, (uint64_t)x->dpad, kBN)) return cudaErrorNotSupported;
   const int smem = Smem::TOTAL(KB);
   cudaError_t e = cudaFuncSetAttribute(k_build_tc<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

@@ -1,5 +1,6 @@
 // internal.h -- host-side declarations shared between the rmips translation units.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -63,6 +64,9 @@ struct QueryCtx {
   size_t cub_bytes = 0;
   int* flags_dev = nullptr;
 };
+
+// TMA descriptor of a 2-D fp16 tensor [rows][cols], box box_rows x 64, SWIZZLE_128B (build_tc.cu).
+bool make_tmap_f16_box(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 
 cudaError_t query_prep(QueryCtx& c, cudaStream_t st);
 cudaError_t query_filter_simt(QueryCtx& c, cudaStream_t st);

@@ -1,5 +1,341 @@
-// query_tc.cu -- tcgen05 fused query x user contraction + classify epilogue.
+// query_tc.cu -- Q2 + Q3 on the 5th-generation tensor cores: Lemma 3 block pruning
+// and the fused query x user contraction with the O(1) Lemma 1 classify epilogue (
+// Alg. 3 lines 4-9).  The |B| x |Q| score block never leaves TMEM.
+//
+// Work item = (query sub-batch s of <= 256 norm-sorted queries, user tile t of 128 norm-sorted
+// users).  One persistent CTA per SM walks the work items, 6 warps:
+//   warp 0      TMA producer: the sub-batch's queries Q16 (256 x 64 fp16 per K block, kept in
+//               shared memory while the CTA stays on that sub-batch) and the stream of user tiles
+//               (128 x 64 fp16 per K block) through a kStages-deep ring (SWIZZLE_128B)
+//   warp 1      TMEM allocator + MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M = 128 users,
+//               N = the Lemma 3 prefix of the sub-batch rounded up to 16 (<= 256 queries),
+//               K = 16 x 4 per K block, fp32 accumulators in TMEM, 2 stages x 256 columns
+//   warps 2-5   epilogue: one thread per user row (TMEM lane); 32 query columns per tcgen05.ld;
+//               a chunk whose max score is below the row's threshold minus the chunk's error
+//               bound is rejected wholesale (the common case), otherwise each pair is classified
+//               exactly like the SIMT kernel (classify(), query.cu) and accepted / undecided
+//               pairs are compacted per warp (one atomic per list per chunk).
+// Every role evaluates the Lemma 3 prefix of a work item itself (same inputs, same answer), so a
+// pruned item costs neither HBM traffic nor MMA nor epilogue time.
+#include <cuda.h>
+
+#include "common.cuh"
 #include "internal.h"
+#include "sm100.cuh"
+
 namespace rmips {
-cudaError_t query_filter_tc(QueryCtx&, cudaStream_t) { return cudaErrorNotSupported; }
+
+namespace {
+
+constexpr int kBM = 128;                  // users per tile (TMEM lanes)
+constexpr int kStages = 4;                // user-tile ring depth
+constexpr int kUTileBytes = kBM * 64 * 2; // 128 x 64 fp16 = 16 KB
+constexpr int kQTileBytes = kQB * 64 * 2; // 256 x 64 fp16 = 32 KB
+constexpr int kThreads = 192;
+constexpr int kAccCols = 256;             // TMEM columns per accumulator stage
+constexpr int kAcc = 2;
+
+struct QSmem {
+  static constexpr int Q = 0;
+  static constexpr int A(int KB) { return KB * kQTileBytes; }
+  static constexpr int BAR(int KB) { return A(KB) + kStages * KB * kUTileBytes; }
+  static constexpr int TOTAL(int KB) { return BAR(KB) + 256 + 1024; }
+};
+
+__device__ __forceinline__ int lemma3_len(const float* __restrict__ qn_sub, int cnt, float tbv) {
+  int lo = 0, hi = cnt;  // queries are norm-sorted: the kept ones are a prefix (#{qn >= tbv})
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (__ldg(qn_sub + mid) >= tbv) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Same decision rule as classify() in query.cu: 0 reject, 1 accept, 2 undecided.
+__device__ __forceinline__ int classify_tc(float acc, float thr_s, float qe) {
+  float E = __fadd_ru(qe, fabsf(thr_s) * 2.384185791015625e-07f);
+  if (__fadd_ru(acc, E) < thr_s) return 0;
+  if (__fsub_rd(acc, E) >= thr_s) return 1;
+  return 2;
+}
+
+}  // namespace
+
+template <int KB>
+__global__ void __launch_bounds__(kThreads, 1)
+k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmQ,
+           const float* __restrict__ thrk, const float* __restrict__ tbk, const int32_t* __restrict__ perm_u,
+           int64_t n, int nblocks, const float* __restrict__ qn, const float* __restrict__ qerr,
+           const float* __restrict__ qscale, const int32_t* __restrict__ qperm, const int32_t* __restrict__ qcount,
+           int nsub, int flags, unsigned long long* __restrict__ ctr, uint64_t* __restrict__ acc_list,
+           uint64_t* __restrict__ und_list, int64_t cap) {
+  using namespace sm100;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sQ = sbase + QSmem::Q;
+  const uint32_t sA = sbase + QSmem::A(KB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + QSmem::BAR(KB));
+  const uint32_t bar0 = smem_u32(bars);
+  auto BAR = [&](int i) { return bar0 + 8u * i; };
+  const int Q_FULL = 0, Q_EMPTY = 1, A_FULL = 2, A_EMPTY = 2 + kStages, ACC_FULL = 2 + 2 * kStages,
+            ACC_EMPTY = 2 + 2 * kStages + kAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 + 2 * kStages + 2 * kAcc);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nwork = (int64_t)nsub * nblocks;
+  const bool use_blocks = !(flags & RMIPS_FLAG_NO_BLOCKS);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmU);
+    tma_prefetch(&tmQ);
+    mbar_init(BAR(Q_FULL), 1);
+    mbar_init(BAR(Q_EMPTY), 1);
+    for (int s = 0; s < kStages; ++s) mbar_init(BAR(A_FULL + s), 1), mbar_init(BAR(A_EMPTY + s), 1);
+    for (int a = 0; a < kAcc; ++a) mbar_init(BAR(ACC_FULL + a), 1), mbar_init(BAR(ACC_EMPTY + a), 4);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(smem_u32(tmem_slot), kAcc * kAccCols);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // Lemma 3 prefix of work item w (identical in every role)
+  auto work_len = [&](int64_t w, int& s, int& t) {
+    s = (int)(w / nblocks);
+    t = (int)(w - (int64_t)s * nblocks);
+    const int cnt = __ldg(qcount + s);
+    const float tbv = use_blocks ? __ldg(tbk + t) : -CUDART_INF_F;
+    return lemma3_len(qn + (int64_t)s * kQB, cnt, tbv);
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0, cur_s = -1, nq = 0;
+      uint32_t ph = 0;
+      unsigned long long pairs = 0, pruned = 0;
+      for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+        int s, t;
+        const int len = work_len(w, s, t);
+        const int cnt = __ldg(qcount + s);
+        pairs += cnt;
+        pruned += cnt - len;
+        if (len == 0) continue;
+        if (s != cur_s) {
+          if (nq > 0) mbar_wait_sleep(BAR(Q_EMPTY), (nq - 1) & 1);
+          mbar_arrive_expect_tx(BAR(Q_FULL), KB * kQTileBytes);
+          for (int kb = 0; kb < KB; ++kb) tma_load_2d(sQ + kb * kQTileBytes, &tmQ, kb * 64, s * kQB, BAR(Q_FULL));
+          ++nq;
+          cur_s = s;
+        }
+        mbar_wait_sleep(BAR(A_EMPTY + stage), ph ^ 1);
+        mbar_arrive_expect_tx(BAR(A_FULL + stage), KB * kUTileBytes);
+        for (int kb = 0; kb < KB; ++kb)
+          tma_load_2d(sA + (stage * KB + kb) * kUTileBytes, &tmU, kb * 64, t * kBM, BAR(A_FULL + stage));
+        if (++stage == kStages) stage = 0, ph ^= 1;
+      }
+      atomicAdd(ctr + C_BLOCK_PAIRS, pairs);
+      atomicAdd(ctr + C_BLOCK_PRUNED, pruned);
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int stage = 0, as = 0, cur_s = -1, nq = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+        int s, t;
+        const int len = work_len(w, s, t);
+        if (len == 0) continue;
+        if (s != cur_s) {
+          if (nq > 0) mma_commit(BAR(Q_EMPTY));  // all MMAs on the previous sub-batch's queries
+          mbar_wait_sleep(BAR(Q_FULL), nq & 1);
+          ++nq;
+          cur_s = s;
+        }
+        mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
+        mbar_wait_sleep(BAR(A_FULL + stage), ph);
+        tc_fence_after();
+        const int N = (len + 15) & ~15;
+        const uint32_t idesc = idesc_f16_f32(kBM, N);
+        const uint32_t d = tmem + as * kAccCols;
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+          const uint32_t a0 = sA + (stage * KB + kb) * kUTileBytes;
+          const uint32_t b0 = sQ + kb * kQTileBytes;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_f16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
+        }
+        mma_commit(BAR(A_EMPTY + stage));
+        mma_commit(BAR(ACC_FULL + as));
+        if (++stage == kStages) stage = 0, ph ^= 1;
+        if (++as == kAcc) as = 0, aph ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue: one thread per user row
+    const int q = warp & 3;  // TMEM lane quadrant of this warp
+    const int rloc = q * 32 + lane;
+    const bool force = (flags & RMIPS_FLAG_FORCE_VERIFY) != 0;
+    unsigned long long n_scored = 0, n_fast = 0, n_und = 0;
+    int as = 0;
+    uint32_t aph = 0;
+    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+      int s, t;
+      const int len = work_len(w, s, t);
+      if (len == 0) continue;
+      const int64_t row = (int64_t)t * kBM + rloc;
+      const bool live = row < n;
+      const float sc = __ldg(qscale + s);
+      const float thr_s = live ? __ldg(thrk + row) * sc : CUDART_INF_F;  // dead rows reject everything
+      const float thr_abs = fabsf(thr_s) * 2.384185791015625e-07f;
+      const uint64_t uo = live ? (uint64_t)(uint32_t)__ldg(perm_u + row) : 0;
+      const float* qe_sub = qerr + (int64_t)s * kQB;
+      const int32_t* qp_sub = qperm + (int64_t)s * kQB;
+      if (live) n_scored += len;
+      mbar_wait(BAR(ACC_FULL + as), aph);
+      tc_fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + as * kAccCols;
+#pragma unroll 1
+      for (int h = 0; h * 128 < len; ++h) {
+        uint32_t r[4][32];
+        tmem_ld32(tbase + h * 128, r[0]);
+        tmem_ld32(tbase + h * 128 + 32, r[1]);
+        tmem_ld32(tbase + h * 128 + 64, r[2]);
+        tmem_ld32(tbase + h * 128 + 96, r[3]);
+        tmem_ld_wait(r[0]);
+        reg_fence(r[1]);
+        reg_fence(r[2]);
+        reg_fence(r[3]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int col0 = h * 128 + 32 * c;
+          if (col0 >= len) break;  // warp-uniform
+          if (col0 + 32 > len) {   // partial last chunk: columns >= len are not scored
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j >= len) r[c][j] = __float_as_uint(-CUDART_INF_F);
+          }
+          float g[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            g[i] = fmaxf(fmaxf(__uint_as_float(r[c][4 * i]), __uint_as_float(r[c][4 * i + 1])),
+                         fmaxf(__uint_as_float(r[c][4 * i + 2]), __uint_as_float(r[c][4 * i + 3])));
+          const float mx = fmaxf(fmaxf(fmaxf(g[0], g[1]), fmaxf(g[2], g[3])), fmaxf(fmaxf(g[4], g[5]), fmaxf(g[6], g[7])));
+          // qerr is non-increasing along the norm-sorted slots: the chunk's first slot bounds it
+          const float Emax = __fadd_ru(__ldg(qe_sub + col0), thr_abs);
+          const bool all_rej = !live || (__fadd_ru(mx, Emax) < thr_s);
+          if (__all_sync(0xffffffffu, all_rej)) continue;
+          // slow path: classify every pair of the chunk (lane-private masks, then one compaction)
+          uint32_t am = 0, um = 0;
+          if (!all_rej) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (col0 + j < len) {
+                int cls = classify_tc(__uint_as_float(r[c][j]), thr_s, __ldg(qe_sub + col0 + j));
+                if (force && cls == 1) cls = 2;
+                am |= (uint32_t)(cls == 1) << j;
+                um |= (uint32_t)(cls == 2) << j;
+              }
+            }
+          }
+          const int na = __popc(am), nu = __popc(um);
+          n_fast += na;
+          n_und += nu;
+          // warp-exclusive prefix sums -> one atomic per list per chunk
+          int pa = na, pu = nu;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int xa = __shfl_up_sync(0xffffffffu, pa, o), xu = __shfl_up_sync(0xffffffffu, pu, o);
+            if (lane >= o) pa += xa, pu += xu;
+          }
+          const int ta = __shfl_sync(0xffffffffu, pa, 31), tu = __shfl_sync(0xffffffffu, pu, 31);
+          unsigned long long ba = 0, bu = 0;
+          if (lane == 31) {
+            if (ta) ba = atomicAdd(ctr + C_ACCEPTED_TOTAL, (unsigned long long)ta);
+            if (tu) bu = atomicAdd(ctr + C_UND_TOTAL, (unsigned long long)tu);
+          }
+          ba = __shfl_sync(0xffffffffu, ba, 31) + (pa - na);
+          bu = __shfl_sync(0xffffffffu, bu, 31) + (pu - nu);
+          while (am) {
+            const int j = __ffs(am) - 1;
+            am &= am - 1;
+            if ((int64_t)ba < cap) acc_list[ba] = ((uint64_t)(uint32_t)__ldg(qp_sub + col0 + j) << 32) | uo;
+            ++ba;
+          }
+          while (um) {
+            const int j = __ffs(um) - 1;
+            um &= um - 1;
+            if ((int64_t)bu < cap) und_list[bu] = ((uint64_t)(uint32_t)__ldg(qp_sub + col0 + j) << 32) | (uint64_t)row;
+            ++bu;
+          }
+        }
+      }
+      tc_fence_before();  // this accumulator stage is fully read: hand it back to the MMA warp
+      __syncwarp();
+      if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
+      if (++as == kAcc) as = 0, aph ^= 1;
+    }
+    // counters: one atomic per warp
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      n_scored += __shfl_xor_sync(0xffffffffu, n_scored, o);
+      n_fast += __shfl_xor_sync(0xffffffffu, n_fast, o);
+      n_und += __shfl_xor_sync(0xffffffffu, n_und, o);
+    }
+    if (lane == 0 && n_scored) {
+      atomicAdd(ctr + C_SCORED, n_scored);
+      atomicAdd(ctr + C_ACCEPT_FAST, n_fast);
+      atomicAdd(ctr + C_REJECTED, n_scored - n_fast - n_und);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, kAcc * kAccCols);
+}
+
+// ------------------------------------------------------------------------------ host side
+static int sm_count_q() {
+  static int c = 0;
+  if (!c) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return c;
+}
+
+template <int KB>
+static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
+  rmips_index_s* x = c.idx;
+  CUtensorMap tu, tq;
+  if (!make_tmap_f16_box(&tu, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM)) return cudaErrorNotSupported;
+  if (!make_tmap_f16_box(&tq, c.Q16, (uint64_t)c.nsub * kQB, (uint64_t)x->dpad, kQB)) return cudaErrorNotSupported;
+  const int smem = QSmem::TOTAL(KB);
+  cudaError_t e = cudaFuncSetAttribute(k_query_tc<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t nwork = (int64_t)c.nsub * x->nblocks;
+  const int grid = (int)(nwork < sm_count_q() ? nwork : sm_count_q());
+  k_query_tc<KB><<<grid, kThreads, smem, st>>>(tu, tq, x->thr + (int64_t)(c.k - 1) * x->n,
+                                               x->tb + (int64_t)(c.k - 1) * x->nblocks, x->perm_u, x->n,
+                                               (int)x->nblocks, c.qn, c.qerr, c.qscale, c.qperm, c.qcount, c.nsub,
+                                               c.flags, c.counters, c.acc, c.und, c.cap);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t query_filter_tc(QueryCtx& c, cudaStream_t st) {
+  if (getenv("RMIPS_DISABLE_TC")) return cudaErrorNotSupported;
+  if (c.idx->n == 0) return cudaSuccess;
+  switch (c.idx->dpad) {
+    case 64: return launch_query_tc<1>(c, st);
+    default: return cudaErrorNotSupported;  // d > 64: SIMT filter
+  }
+}
+
 }  // namespace rmips

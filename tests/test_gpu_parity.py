@@ -229,6 +229,12 @@ def test_stats_counters_consistent(cfg0):
     assert s["pairs_scored"] == s["pairs_rejected"] + s["pairs_accepted_fast"] + s["pairs_undecided"]
     assert s["result_total"] == s["pairs_accepted_fast"] + s["pairs_exact_accepted"]
     assert s["block_query_pairs"] == 100 * ((idx.n + 127) // 128)
+    assert s["filter_kernel"] == 1          # the tcgen05 filter ran (query_tc.cu), not the SIMT one
+    rmips.rmips_query(idx, _t(w.Qy), 10, rmips.RMIPS_FLAG_SIMT)
+    s2 = idx.stats()
+    assert s2["filter_kernel"] == 0
+    for key in ("block_query_pairs", "block_query_pruned", "pairs_scored", "result_total"):
+        assert s2[key] == s[key], key
     idx.close()
 
 
@@ -241,7 +247,11 @@ def test_cfg1_full_size_sampled():
     w = gen.make_workload(1)
     idx = rmips.rmips_build_index(_t(w.U), _t(w.P), 50)
     off, ids = rmips.rmips_query(idx, _t(w.Qy), 10)
+    assert idx.stats()["filter_kernel"] == 1
     sets = rmips.split_sets(off, ids)
+    # the SIMT filter must give the identical sets (different fp32 summation order, same decisions)
+    off2, ids2 = rmips.rmips_query(idx, _t(w.Qy), 10, rmips.RMIPS_FLAG_SIMT)
+    assert torch.equal(off, off2) and torch.equal(ids, ids2)
     rng = np.random.default_rng(0)
     sample = np.sort(rng.choice(w.U.shape[0], 1500, replace=False))
     vals, oids = oracle.topk(w.U[sample], w.P, 50)
