@@ -21,14 +21,14 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-DRMIPS_BUILD"]
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+def _compile(src: str, verbose: bool, extra=(), tag: str = "") -> str:
+    obj = os.path.join(BUILD, src.replace(".cu", tag + ".o"))
     srcp = os.path.join(CSRC, src)
     deps = [srcp] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     deps.append(os.path.join(HERE, "..", "include", "rmips.h"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(p) for p in deps):
         return obj
-    cmd = [NVCC] + FLAGS + ["-c", srcp, "-o", obj]
+    cmd = [NVCC] + FLAGS + list(extra) + ["-c", srcp, "-o", obj]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -39,13 +39,17 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, profile: bool = False) -> str:
+    """profile=True builds the development-only instrumented variant librmips_prof.so
+    (-DRMIPS_EPI_PROFILE, see tools/epi_profile.py); the product library is librmips.so."""
     os.makedirs(BUILD, exist_ok=True)
+    extra, tag = (["-DRMIPS_EPI_PROFILE"], "_prof") if profile else ((), "")
+    OUT = os.path.join(HERE, "librmips_prof.so" if profile else "librmips.so")
     if force:
         for f in os.listdir(BUILD):
             os.remove(os.path.join(BUILD, f))
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+        objs = list(ex.map(lambda s: _compile(s, verbose, extra, tag), SOURCES))
     if force or not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", OUT + ".tmp"] + objs + \
               ["-lcudart_static", "-lrt", "-ldl", "-lpthread", "-Xlinker", "--no-undefined"]
@@ -57,4 +61,4 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, profile="--profile" in sys.argv))

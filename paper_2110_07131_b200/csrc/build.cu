@@ -116,7 +116,8 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
     if (gr < n) v = reinterpret_cast<const __half2*>(U16)[gr * (DPAD / 2) + k2];
     us[k2 * 128 + r] = v;
   }
-  CandRow me{live ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000), 0, false};
+  CandRow me = cand_init(live);
+  const float e0x2 = cand_e0x2(perr);
 
   for (int64_t base = 0; base < m; base += 32) {
     __syncthreads();
@@ -153,9 +154,9 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
     for (int j = 0; j < 32; ++j)
       if (base + j >= m) s[j] = NEG;
     float E = __ldg(perr + base);
-    cand_chunk([&](int j) { return s[j]; }, E, (int)base, me, clo, cid, tid, perr, kmax);
+    cand_chunk([&](int j) { return s[j]; }, E, (int)base, me, clo, cid, tid, e0x2, kmax);
   }
-  cand_finish(me, clo, cid, tid, perr, kmax, row, n, cand, ccount, ovf_list, ovf_count);
+  cand_finish(me, clo, cid, tid, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
 }
 
 // ------------------------------------------------------------------------------ B5

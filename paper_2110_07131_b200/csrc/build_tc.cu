@@ -21,6 +21,12 @@
 
 namespace rmips {
 
+#ifdef RMIPS_EPI_PROFILE
+// Development-only instrumentation (tools/epi_profile.py): per item-tile index, epilogue
+// cycles spent waiting for the accumulator, cycles of work, and warp-chunks that appended.
+__device__ unsigned long long g_epi_prof[4][256];
+#endif
+
 namespace {
 
 constexpr int kBM = 128;          // users per tile (TMEM lanes)
@@ -40,6 +46,70 @@ struct Smem {
   static constexpr int TOTAL(int KB) { return BAR(KB) + 256 + 1024; }  // + alignment slack
 };
 
+// Fast path of one half tile (64 scores of this thread's row, columns base .. base + 63):
+// 3-input max trees and one compare per 32-column chunk.  Returns a warp-uniform 2-bit mask of
+// the chunks in which some lane may append (handled later by epi_slow from TMEM).
+// Padding columns of a ragged last tile (TMA zero fill) are not masked here: at worst they flag
+// a chunk, and epi_slow masks them before anything is appended.
+__device__ __forceinline__ uint32_t epi_fast(const uint32_t (&h)[64], float E0, float E1, float theta) {
+  uint32_t bits = 0;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    float g4[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      g4[g] = fmaxf(fmaxf(__uint_as_float(h[32 * c + 4 * g]), __uint_as_float(h[32 * c + 4 * g + 1])),
+                    fmaxf(__uint_as_float(h[32 * c + 4 * g + 2]), __uint_as_float(h[32 * c + 4 * g + 3])));
+    const float mx = fmaxf(fmaxf(fmaxf(g4[0], g4[1]), fmaxf(g4[2], g4[3])), fmaxf(fmaxf(g4[4], g4[5]), fmaxf(g4[6], g4[7])));
+    bits |= (uint32_t)__any_sync(0xffffffffu, __fadd_ru(mx, c ? E1 : E0) >= theta) << c;
+  }
+  return bits;
+}
+
+// Slow path (one copy in the kernel, so the hot loop stays inside the instruction cache):
+// re-read each flagged chunk of the current accumulator stage from TMEM, append and refresh.
+__device__ __noinline__ CandRow epi_slow(uint32_t bits, uint32_t taddr, int base0, int mi, float4 E4, CandRow me,
+                                         float* clo, int* cid, int rloc, float e0x2, int kmax) {
+#pragma unroll 1
+  while (bits) {
+    const int c = __ffs(bits) - 1;
+    bits &= bits - 1;
+    uint32_t r[32];
+    sm100::tmem_ld32(taddr + 32 * c, r);
+    sm100::tmem_ld_wait(r);
+    const int pos0 = base0 + 32 * c;
+    if (pos0 + 32 > mi) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (pos0 + j >= mi) r[j] = 0xff800000u;
+    }
+    const float E = c == 0 ? E4.x : c == 1 ? E4.y : c == 2 ? E4.z : E4.w;
+    float g4[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      g4[g] = fmaxf(fmaxf(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1])),
+                    fmaxf(__uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3])));
+#ifdef RMIPS_EPI_PROFILE
+    const long long p0 = clock64();
+#endif
+    cand_append_chunk([&](int j) { return __uint_as_float(r[j]); }, g4, E, pos0, me, clo, cid, rloc);
+#ifdef RMIPS_EPI_PROFILE
+    const long long p1 = clock64();
+    const bool rf = __any_sync(0xffffffffu, me.cnt > kCand - 32);
+#endif
+    cand_maybe_refresh(me, clo, cid, rloc, e0x2, kmax);
+#ifdef RMIPS_EPI_PROFILE
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&g_epi_prof[2][0], 1ull);
+      atomicAdd(&g_epi_prof[2][1], (unsigned long long)(p1 - p0));
+      atomicAdd(&g_epi_prof[2][2], (unsigned long long)(clock64() - p1));
+      atomicAdd(&g_epi_prof[2][3], (unsigned long long)rf);
+    }
+#endif
+  }
+  return me;
+}
+
 }  // namespace
 
 template <int KB>
@@ -49,7 +119,9 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
            int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
   using namespace sm100;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base, derived from smem_raw by pointer arithmetic so that the compiler
+  // keeps the shared state space (LDS/STS rather than generic loads/stores)
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t sA = sbase + Smem::A;
   const uint32_t sB = sbase + Smem::B(KB);
@@ -137,70 +209,64 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     }
   } else {
     // ------------------------------------------------ epilogue: one thread per user row
+    // Half tiles (64 columns) are software-pipelined: the TMEM load of the next half (of this
+    // tile or the next one) is in flight while the current half is filtered.  Chunks in which a
+    // lane may append are re-read from TMEM by epi_slow before the stage is released.
     const int q = warp & 3;                    // TMEM lane quadrant of this warp
     const int rloc = q * 32 + lane;            // row within the tile
-    const float NEG = -__int_as_float(0x7f800000);
-    const float POS = __int_as_float(0x7f800000);
     const int mi = (int)m;
+    const float e0x2 = cand_e0x2(perr);
     int as = 0;
     uint32_t aph = 0;
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+    uint32_t hA[64], hB[64];
     for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x) {
       const int64_t row = (int64_t)ut * kBM + rloc;
-      // dead rows (user >= n) have theta = +inf and never pass
-      CandRow me{row < n ? NEG : POS, 0, false};
+      CandRow me = cand_init(row < n);  // dead rows (user >= n) have theta = +inf and never pass
+      float En[4];                      // error bounds of the next tile's chunks (prefetched)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) En[c] = (32 * c < mi) ? __ldg(perr + 32 * c) : 0.f;
+      mbar_wait(BAR(ACC_FULL + as), aph);
+      tc_fence_after();
+      tmem_ld64(tq + as * kBN, hA);
+      tmem_ld_wait64(hA);
       for (int it = 0; it < nit; ++it) {
         const int base0 = it * kBN;
         float E[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) E[c] = (base0 + 32 * c < mi) ? __ldg(perr + base0 + 32 * c) : 0.f;
-        mbar_wait(BAR(ACC_FULL + as), aph);
-        tc_fence_after();
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + as * kBN;
-        // all 128 columns of the tile in one go: 4 TMEM loads in flight, one wait
-        uint32_t r[4][32];
-        tmem_ld32(taddr, r[0]);
-        tmem_ld32(taddr + 32, r[1]);
-        tmem_ld32(taddr + 64, r[2]);
-        tmem_ld32(taddr + 96, r[3]);
-        tmem_ld_wait(r[0]);
-        reg_fence(r[1]);
-        reg_fence(r[2]);
-        reg_fence(r[3]);
-        tc_fence_before();  // this accumulator stage is fully read: hand it back to the MMA warp
+        for (int c = 0; c < 4; ++c) {
+          E[c] = En[c];
+          En[c] = (base0 + kBN + 32 * c < mi) ? __ldg(perr + base0 + kBN + 32 * c) : 0.f;
+        }
+#ifdef RMIPS_EPI_PROFILE
+        const long long t1 = clock64();
+        const int pb = it < 255 ? it : 255;
+#endif
+        const uint32_t tcur = tq + as * kBN;
+        tmem_ld64(tcur + 64, hB);                 // second half of this tile
+        uint32_t bits = epi_fast(hA, E[0], E[1], me.theta);
+        tmem_ld_wait64(hB);
+        const bool more = it + 1 < nit;
+        int as_next = as + 1 == kAcc ? 0 : as + 1;
+        uint32_t aph_next = as + 1 == kAcc ? aph ^ 1 : aph;
+        if (more) {                               // first half of the next tile
+          mbar_wait(BAR(ACC_FULL + as_next), aph_next);
+          tc_fence_after();
+          tmem_ld64(tq + as_next * kBN, hA);
+        }
+        bits |= epi_fast(hB, E[2], E[3], me.theta) << 2;
+        if (bits) me = epi_slow(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, clo, cid, rloc, e0x2, kmax);
+        tc_fence_before();                        // this stage is no longer read: release it
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
-        if (++as == kAcc) as = 0, aph ^= 1;
-        if (base0 + kBN > mi) {  // last item tile only (warp-uniform): mask padding columns
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (base0 + 32 * c + j >= mi) r[c][j] = __float_as_uint(NEG);
-        }
-        // 4 independent max trees (3-input FMNMX), one compare per chunk
-        float g4[4][8];
-        bool pass[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-#pragma unroll
-          for (int g = 0; g < 8; ++g)
-            g4[c][g] = fmaxf(fmaxf(__uint_as_float(r[c][4 * g]), __uint_as_float(r[c][4 * g + 1])),
-                             fmaxf(__uint_as_float(r[c][4 * g + 2]), __uint_as_float(r[c][4 * g + 3])));
-          const float mx = fmaxf(fmaxf(fmaxf(g4[c][0], g4[c][1]), fmaxf(g4[c][2], g4[c][3])),
-                                 fmaxf(fmaxf(g4[c][4], g4[c][5]), fmaxf(g4[c][6], g4[c][7])));
-          pass[c] = __fadd_ru(mx, E[c]) >= me.theta;
-        }
-        if (!__any_sync(0xffffffffu, pass[0] | pass[1] | pass[2] | pass[3])) continue;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (!__any_sync(0xffffffffu, pass[c])) continue;
-          if (pass[c])
-            cand_append_chunk([&](int j) { return __uint_as_float(r[c][j]); }, g4[c], E[c], base0 + 32 * c, me, clo,
-                              cid, rloc);
-          cand_maybe_refresh(me, clo, cid, rloc, perr, kmax);
-        }
+        as = as_next;
+        aph = aph_next;
+        if (more) tmem_ld_wait64(hA);
+#ifdef RMIPS_EPI_PROFILE
+        if (lane == 0) atomicAdd(&g_epi_prof[1][pb], (unsigned long long)(clock64() - t1));
+#endif
       }
-      cand_finish(me, clo, cid, rloc, perr, kmax, row, n, cand, ccount, ovf_list, ovf_count);
+      cand_finish(me, clo, cid, rloc, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
       __syncwarp();
     }
   }
@@ -276,3 +342,14 @@ cudaError_t build_tc(const BuildCtx& c, cudaStream_t st) {
 }
 
 }  // namespace rmips
+
+#ifdef RMIPS_EPI_PROFILE
+extern "C" RMIPS_API int rmips_debug_epi_profile(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, rmips::g_epi_prof, sizeof(rmips::g_epi_prof));
+  if (reset) {
+    static unsigned long long z[4][256] = {};
+    cudaMemcpyToSymbol(rmips::g_epi_prof, z, sizeof z);
+  }
+  return 0;
+}
+#endif

@@ -13,7 +13,7 @@ from typing import Optional, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librmips.so")
+LIB_PATH = os.environ.get("RMIPS_LIB") or os.path.join(_HERE, "librmips.so")  # RMIPS_LIB: dev-only profiling build
 
 RMIPS_OK, RMIPS_ERR_INVALID, RMIPS_ERR_NONFINITE, RMIPS_ERR_K_RANGE, RMIPS_ERR_CAPACITY, RMIPS_ERR_CUDA, \
     RMIPS_ERR_OOM = range(7)
