@@ -100,10 +100,9 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
              int64_t n, int64_t m, int kmax, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
              int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* clo = reinterpret_cast<float*>(smem_raw);           // [kCand][128]
-  int* cid = reinterpret_cast<int*>(clo + 128 * kCand);      // [kCand][128]
-  __half2* us = reinterpret_cast<__half2*>(cid + 128 * kCand);  // [DPAD/2][128]
-  float* ps = reinterpret_cast<float*>(us + (DPAD / 2) * 128);      // [DPAD][32]
+  const CandSmem sm = CandSmem::at(smem_raw);                               // candidate buffers
+  __half2* us = reinterpret_cast<__half2*>(smem_raw + kCandSmemBytes);     // [DPAD/2][128]
+  __half* ps = reinterpret_cast<__half*>(us + (DPAD / 2) * 128);   // [DPAD][32] (fp16: exact copies of P16)
 
   const int tid = threadIdx.x;
   const int64_t row = blockIdx.x * (int64_t)128 + tid;
@@ -123,8 +122,8 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
     __syncthreads();
     for (int i = tid; i < 32 * DPAD; i += 128) {
       int jj = i / DPAD, k = i % DPAD;
-      float v = 0.f;
-      if (base + jj < m) v = __half2float(P16[(base + jj) * DPAD + k]);
+      __half v = __float2half_rn(0.f);
+      if (base + jj < m) v = P16[(base + jj) * DPAD + k];
       ps[k * 32 + jj] = v;
     }
     __syncthreads();
@@ -134,19 +133,15 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
 #pragma unroll 2
     for (int k2 = 0; k2 < DPAD / 2; ++k2) {
       float2 a = __half22float2(us[k2 * 128 + tid]);
-      const float4* p0 = reinterpret_cast<const float4*>(ps + (2 * k2) * 32);
-      const float4* p1 = reinterpret_cast<const float4*>(ps + (2 * k2 + 1) * 32);
+      const __half2* p0 = reinterpret_cast<const __half2*>(ps + (2 * k2) * 32);
+      const __half2* p1 = reinterpret_cast<const __half2*>(ps + (2 * k2 + 1) * 32);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float4 b0 = p0[q], b1 = p1[q];
-        s[4 * q + 0] = fmaf(a.x, b0.x, s[4 * q + 0]);
-        s[4 * q + 1] = fmaf(a.x, b0.y, s[4 * q + 1]);
-        s[4 * q + 2] = fmaf(a.x, b0.z, s[4 * q + 2]);
-        s[4 * q + 3] = fmaf(a.x, b0.w, s[4 * q + 3]);
-        s[4 * q + 0] = fmaf(a.y, b1.x, s[4 * q + 0]);
-        s[4 * q + 1] = fmaf(a.y, b1.y, s[4 * q + 1]);
-        s[4 * q + 2] = fmaf(a.y, b1.z, s[4 * q + 2]);
-        s[4 * q + 3] = fmaf(a.y, b1.w, s[4 * q + 3]);
+      for (int q = 0; q < 16; ++q) {
+        const float2 b0 = __half22float2(p0[q]), b1 = __half22float2(p1[q]);
+        s[2 * q + 0] = fmaf(a.x, b0.x, s[2 * q + 0]);
+        s[2 * q + 1] = fmaf(a.x, b0.y, s[2 * q + 1]);
+        s[2 * q + 0] = fmaf(a.y, b1.x, s[2 * q + 0]);
+        s[2 * q + 1] = fmaf(a.y, b1.y, s[2 * q + 1]);
       }
     }
     const float NEG = -__int_as_float(0x7f800000);
@@ -154,9 +149,9 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
     for (int j = 0; j < 32; ++j)
       if (base + j >= m) s[j] = NEG;
     float E = __ldg(perr + base);
-    cand_chunk([&](int j) { return s[j]; }, E, (int)base, me, clo, cid, tid, e0x2, kmax);
+    cand_chunk([&](int j) { return s[j]; }, E, (int)base, me, sm, tid, e0x2, kmax);
   }
-  cand_finish(me, clo, cid, tid, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
+  cand_finish(me, sm, tid, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
 }
 
 // ------------------------------------------------------------------------------ B5
@@ -290,7 +285,7 @@ static inline unsigned nblk(int64_t work, int t) { return (unsigned)((work + t -
 
 template <int DPAD>
 static cudaError_t launch_build_simt(const BuildCtx& c, cudaStream_t st) {
-  size_t smem = (size_t)128 * kCand * 8 + (DPAD / 2) * 128 * 4 + DPAD * 32 * 4;
+  size_t smem = (size_t)kCandSmemBytes + (DPAD / 2) * 128 * 4 + DPAD * 32 * 2;
   cudaError_t e = cudaFuncSetAttribute(k_build_simt<DPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_build_simt<DPAD><<<nblk(c.idx->n, 128), 128, smem, st>>>(c.idx->U16, c.idx->P16, c.idx->perr, c.idx->n,

@@ -41,8 +41,7 @@ struct Smem {
   static constexpr int A = 0;                              // KB tiles
   static constexpr int B(int KB) { return KB * kTileBytes; }
   static constexpr int CV(int KB) { return B(KB) + kStages * KB * kTileBytes; }
-  static constexpr int CI(int KB) { return CV(KB) + kBM * kCand * 4; }
-  static constexpr int BAR(int KB) { return CI(KB) + kBM * kCand * 4; }
+  static constexpr int BAR(int KB) { return CV(KB) + kCandSmemBytes; }
   static constexpr int TOTAL(int KB) { return BAR(KB) + 256 + 1024; }  // + alignment slack
 };
 
@@ -69,7 +68,8 @@ __device__ __forceinline__ uint32_t epi_fast(const uint32_t (&h)[64], float E0, 
 // Slow path (one copy in the kernel, so the hot loop stays inside the instruction cache):
 // re-read each flagged chunk of the current accumulator stage from TMEM, append and refresh.
 __device__ __noinline__ CandRow epi_slow(uint32_t bits, uint32_t taddr, int base0, int mi, float4 E4, CandRow me,
-                                         float* clo, int* cid, int rloc, float e0x2, int kmax) {
+                                         CandSmem sm, int rloc, float e0x2, int kmax) {
+  sm.assume_shared();
 #pragma unroll 1
   while (bits) {
     const int c = __ffs(bits) - 1;
@@ -92,12 +92,12 @@ __device__ __noinline__ CandRow epi_slow(uint32_t bits, uint32_t taddr, int base
 #ifdef RMIPS_EPI_PROFILE
     const long long p0 = clock64();
 #endif
-    cand_append_chunk([&](int j) { return __uint_as_float(r[j]); }, g4, E, pos0, me, clo, cid, rloc);
+    cand_append_chunk([&](int j) { return __uint_as_float(r[j]); }, g4, E, pos0, me, sm, rloc);
 #ifdef RMIPS_EPI_PROFILE
     const long long p1 = clock64();
     const bool rf = __any_sync(0xffffffffu, me.cnt > kCand - 32);
 #endif
-    cand_maybe_refresh(me, clo, cid, rloc, e0x2, kmax);
+    cand_maybe_refresh(me, sm, rloc, e0x2, kmax);
 #ifdef RMIPS_EPI_PROFILE
     if ((threadIdx.x & 31) == 0) {
       atomicAdd(&g_epi_prof[2][0], 1ull);
@@ -125,8 +125,7 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
   const uint32_t sbase = smem_u32(smem);
   const uint32_t sA = sbase + Smem::A;
   const uint32_t sB = sbase + Smem::B(KB);
-  float* clo = reinterpret_cast<float*>(smem + Smem::CV(KB));  // [kCand][128] candidate lower bounds
-  int* cid = reinterpret_cast<int*>(smem + Smem::CI(KB));      // [kCand][128] candidate item positions
+  const CandSmem sm = CandSmem::at(smem + Smem::CV(KB));  // candidate buffers + refresh histograms
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::BAR(KB));
   // barrier indices
   const uint32_t bar0 = smem_u32(bars);
@@ -255,7 +254,7 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
           tmem_ld64(tq + as_next * kBN, hA);
         }
         bits |= epi_fast(hB, E[2], E[3], me.theta) << 2;
-        if (bits) me = epi_slow(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, clo, cid, rloc, e0x2, kmax);
+        if (bits) me = epi_slow(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, sm, rloc, e0x2, kmax);
         tc_fence_before();                        // this stage is no longer read: release it
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
@@ -266,7 +265,7 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         if (lane == 0) atomicAdd(&g_epi_prof[1][pb], (unsigned long long)(clock64() - t1));
 #endif
       }
-      cand_finish(me, clo, cid, rloc, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
+      cand_finish(me, sm, rloc, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
       __syncwarp();
     }
   }

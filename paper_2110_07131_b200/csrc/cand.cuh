@@ -7,108 +7,142 @@
 //   theta : a valid lower bound (scaled units) of the k_max-th largest TRUE score seen so far
 //           (at least k_max buffered entries have lo >= theta, and lo <= true score);
 //   vmax  : the largest lo in its buffer;
-//   a candidate buffer in shared memory, slot-major ([slot][128 rows]) so that every lane
-//   reads/writes its own row conflict-free: lo = s~ - E (rounded down) and the item position.
+//   a candidate buffer in shared memory, slot-major ([slot][128 rows], 8-byte entries
+//   {lo bits, item position}) so that every lane reads/writes its own row conflict-free;
+//   lo = s~ - E rounded down.
 // An item is appended iff s~ >= theta - E (it may still be in the final top-k_max).  When any
 // row of a warp may not have room for another 32-column chunk, the whole warp refreshes at
-// once, every thread on its own row: theta <- the largest of a 4-level quaternary search
-// (3 thresholds per pass over the buffer, 256-way resolution of [theta, vmax]) that keeps at
-// least k_max entries lo >= theta; then entries whose upper bound lo + 2 E0 (E0 = perr of the
-// largest-norm item >= every E) is below theta are dropped.  Every true top-k_max item has
-// s >= tau_kmax >= theta at all times, so it is never rejected or dropped.
-// A row that cannot be compacted below kCand - 32 entries (massive ties) is flagged and
-// recomputed exactly by the fallback kernel.
+// once, every thread on its own row:
+//   1. theta' = the largest of 4 quaternary search levels over [theta, vmax] (3 thresholds per
+//      pass; 256-way resolution) that keeps at least k_max entries lo >= theta' (exact counts of
+//      the fp32 thresholds themselves, so theta' is valid by construction);
+//   2. one compaction pass that drops entries whose upper bound lo + 2 E0 (E0 = perr of the
+//      largest-norm item >= every E) is below theta' and re-counts #{lo >= theta'} (a
+//      belt-and-braces check: were it ever below k_max the row would go to the exact fallback).
+// Every true top-k_max item has s >= tau_kmax >= theta at all times, so it is never rejected
+// or dropped.  A row that cannot be compacted below kCand - 32 entries (massive
+// ties) is likewise flagged and recomputed exactly by the fallback kernel.
 #pragma once
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace rmips {
 
 constexpr int kCandRows = 128;  // rows per CTA buffer (slot stride)
+constexpr int kHistBins = 32;
+// shared-memory bytes the filter needs for 128 rows
+constexpr int kCandSmemBytes = kCand * kCandRows * 8 + kHistBins * kCandRows * 4;
+
+// Shared-memory pointers.  Functions that are not inlined re-assert the state space
+// (__builtin_assume(__isShared(..))) so that they still compile to LDS/STS/ATOMS.
+struct CandSmem {
+  uint2* buf;       // [kCand][kCandRows] {lo bits, item position}
+  uint32_t* hist;   // [kHistBins][kCandRows]
+  __device__ __forceinline__ static CandSmem at(uint8_t* base) {
+    return CandSmem{reinterpret_cast<uint2*>(base), reinterpret_cast<uint32_t*>(base + kCand * kCandRows * 8)};
+  }
+  __device__ __forceinline__ void assume_shared() const {
+    __builtin_assume(__isShared(buf));
+    __builtin_assume(__isShared(hist));
+  }
+};
 
 struct CandRow {
   float theta;   // running lower bound (scaled units); +inf for dead / overflowed rows
   float vmax;    // max lo in the buffer (-inf when empty)
   int cnt;       // live candidates in this row's buffer
-  bool ovf;      // overflowed: exact fallback
+  int ovf;       // overflowed: exact fallback
 };
 
 __device__ __forceinline__ CandRow cand_init(bool live) {
   const float inf = __int_as_float(0x7f800000);
-  return CandRow{live ? -inf : inf, -inf, 0, false};
+  return CandRow{live ? -inf : inf, -inf, 0, 0};
 }
 
-// Per-thread refresh of this thread's row (called by all 32 lanes together).
-// clo/cid: slot-major buffers, entry i of this row at [i * kCandRows + rloc].
-// e0x2 >= 2 * (every chunk error bound E used at append time), rounded up.
-// Not inlined (one copy per kernel keeps the hot loops inside the instruction cache); the row
-// state travels in registers (by value).
-static __device__ __noinline__ CandRow cand_refresh(CandRow me, float* __restrict__ clo, int* __restrict__ cid,
-                                                    int rloc, float e0x2, int kmax) {
+// Per-thread refresh of this thread's row (called by all 32 lanes together).  Not inlined (one
+// copy per kernel keeps the hot loops inside the instruction cache); the row state travels in
+// registers.  e0x2 >= 2 * (every chunk error bound E used at append time), rounded up.
+static __device__ __noinline__ CandRow cand_refresh(CandRow me, CandSmem sm, int rloc, float e0x2, int kmax) {
   if (me.ovf) return me;
   const int cn = me.cnt;
-  float th = me.theta;
+  sm.assume_shared();
+  uint2* b = sm.buf + rloc;
+  const float th = me.theta;
+  float nth = th;  // proposed new theta
   if (cn >= kmax) {
-    // invariant: #{lo >= L} >= kmax (L = theta_old holds for the survivors of the last refresh)
-    float L = th, U = me.vmax;
+    float L = th;
+    const float U = me.vmax;
     if (!(L > -3.402823466e38f)) {  // first refresh: bracket from the smallest entry
-      L = U;
-#pragma unroll 8
-      for (int i = 0; i < cn; ++i) L = fminf(L, clo[i * kCandRows + rloc]);
+      float m0 = U, m1 = U, m2 = U, m3 = U;
+      int i = 0;
+      for (; i + 4 <= cn; i += 4) {
+        m0 = fminf(m0, __uint_as_float(b[i * kCandRows].x));
+        m1 = fminf(m1, __uint_as_float(b[(i + 1) * kCandRows].x));
+        m2 = fminf(m2, __uint_as_float(b[(i + 2) * kCandRows].x));
+        m3 = fminf(m3, __uint_as_float(b[(i + 3) * kCandRows].x));
+      }
+      for (; i < cn; ++i) m0 = fminf(m0, __uint_as_float(b[i * kCandRows].x));
+      L = fminf(fminf(m0, m1), fminf(m2, m3));
     }
+    // 4 quaternary passes (3 thresholds each, 256-way resolution of [L, U]); the counts are
+    // kept in 4 independent accumulators per threshold so the loop is not a dependency chain
+    float U2 = U;
 #pragma unroll 1
     for (int pass = 0; pass < 4; ++pass) {
-      const float w = U - L;
+      const float w = U2 - L;
       const float t1 = fmaf(w, 0.25f, L), t2 = fmaf(w, 0.5f, L), t3 = fmaf(w, 0.75f, L);
-      int c1 = 0, c2 = 0, c3 = 0;
+      int a1[4] = {0, 0, 0, 0}, a2[4] = {0, 0, 0, 0}, a3[4] = {0, 0, 0, 0};
       int i = 0;
-      // 8 independent shared loads in flight per step (the loop is latency-, not issue-bound)
       for (; i + 8 <= cn; i += 8) {
         float v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = clo[(i + u) * kCandRows + rloc];
+        for (int u = 0; u < 8; ++u) v[u] = __uint_as_float(b[(i + u) * kCandRows].x);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) c1 += v[u] >= t1, c2 += v[u] >= t2, c3 += v[u] >= t3;
+        for (int u = 0; u < 8; ++u) a1[u & 3] += v[u] >= t1, a2[u & 3] += v[u] >= t2, a3[u & 3] += v[u] >= t3;
       }
       for (; i < cn; ++i) {
-        const float v0 = clo[i * kCandRows + rloc];
-        c1 += v0 >= t1, c2 += v0 >= t2, c3 += v0 >= t3;
+        const float v0 = __uint_as_float(b[i * kCandRows].x);
+        a1[0] += v0 >= t1, a2[0] += v0 >= t2, a3[0] += v0 >= t3;
       }
+      const int c1 = (a1[0] + a1[1]) + (a1[2] + a1[3]), c2 = (a2[0] + a2[1]) + (a2[2] + a2[3]),
+                c3 = (a3[0] + a3[1]) + (a3[2] + a3[3]);
       if (c3 >= kmax) L = t3;
-      else if (c2 >= kmax) L = t2, U = t3;
-      else if (c1 >= kmax) L = t1, U = t2;
-      else U = t1;
+      else if (c2 >= kmax) L = t2, U2 = t3;
+      else if (c1 >= kmax) L = t1, U2 = t2;
+      else U2 = t1;
     }
-    th = fmaxf(th, L);
+    nth = L;
+    nth = fmaxf(nth, th);
   }
-  const float keep = __fsub_rd(th, e0x2);  // lo < keep  =>  lo + 2E < theta: the item cannot be top-k_max
-  int w = 0, i = 0;
+  const float keep = __fsub_rd(nth, e0x2);  // lo < keep  =>  lo + 2E < theta: cannot be top-k_max
+  int wpos = 0, ge = 0, i = 0;
   for (; i + 8 <= cn; i += 8) {
-    float v[8];
-    int id[8];
+    uint2 v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = clo[(i + u) * kCandRows + rloc], id[u] = cid[(i + u) * kCandRows + rloc];
+    for (int u = 0; u < 8; ++u) v[u] = b[(i + u) * kCandRows];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      if (v[u] >= keep) {  // w <= i + u: the write never overtakes an unread entry
-        clo[w * kCandRows + rloc] = v[u];
-        cid[w * kCandRows + rloc] = id[u];
-        ++w;
+      const float lo = __uint_as_float(v[u].x);
+      ge += lo >= nth;
+      if (lo >= keep) {  // wpos <= i + u: never overtakes an unread entry
+        b[wpos * kCandRows] = v[u];
+        ++wpos;
       }
     }
   }
   for (; i < cn; ++i) {
-    const float lo = clo[i * kCandRows + rloc];
-    const int id = cid[i * kCandRows + rloc];
+    const uint2 v = b[i * kCandRows];
+    const float lo = __uint_as_float(v.x);
+    ge += lo >= nth;
     if (lo >= keep) {
-      clo[w * kCandRows + rloc] = lo;
-      cid[w * kCandRows + rloc] = id;
-      ++w;
+      b[wpos * kCandRows] = v;
+      ++wpos;
     }
   }
-  me.cnt = w;
-  me.theta = th;
-  if (w > kCand - 32) {
-    me.ovf = true;
+  me.theta = nth;
+  me.cnt = wpos;
+  if (wpos > kCand - 32 || (nth > th && ge < kmax)) {  // no room / unverified theta: exact fallback
+    me.ovf = 1;
     me.theta = __int_as_float(0x7f800000);
   }
   return me;
@@ -120,9 +154,10 @@ static __device__ __noinline__ CandRow cand_refresh(CandRow me, float* __restric
 // so the stores are independent of each other.
 template <typename ScoreFn>
 __device__ __forceinline__ void cand_append_chunk(ScoreFn s_of, const float (&g4)[8], float E, int pos0,
-                                                  CandRow& me, float* __restrict__ clo, int* __restrict__ cid,
-                                                  int rloc) {
+                                                  CandRow& me, CandSmem sm, int rloc) {
+  sm.assume_shared();
   const float thr = fmaxf(__fsub_rd(me.theta, E), -3.402823466e38f);  // padding (-inf) never passes
+  uint2* b = sm.buf + rloc;
   int c = me.cnt;
   float vmax = me.vmax;
 #pragma unroll
@@ -132,10 +167,10 @@ __device__ __forceinline__ void cand_append_chunk(ScoreFn s_of, const float (&g4
       const float s0 = s_of(4 * g), s1 = s_of(4 * g + 1), s2 = s_of(4 * g + 2), s3 = s_of(4 * g + 3);
       const bool p0 = s0 >= thr, p1 = s1 >= thr, p2 = s2 >= thr, p3 = s3 >= thr;
       const int o1 = c + p0, o2 = o1 + p1, o3 = o2 + p2;
-      if (p0) clo[c * kCandRows + rloc] = __fsub_rd(s0, E), cid[c * kCandRows + rloc] = pos0 + 4 * g;
-      if (p1) clo[o1 * kCandRows + rloc] = __fsub_rd(s1, E), cid[o1 * kCandRows + rloc] = pos0 + 4 * g + 1;
-      if (p2) clo[o2 * kCandRows + rloc] = __fsub_rd(s2, E), cid[o2 * kCandRows + rloc] = pos0 + 4 * g + 2;
-      if (p3) clo[o3 * kCandRows + rloc] = __fsub_rd(s3, E), cid[o3 * kCandRows + rloc] = pos0 + 4 * g + 3;
+      if (p0) b[c * kCandRows] = make_uint2(__float_as_uint(__fsub_rd(s0, E)), (uint32_t)(pos0 + 4 * g));
+      if (p1) b[o1 * kCandRows] = make_uint2(__float_as_uint(__fsub_rd(s1, E)), (uint32_t)(pos0 + 4 * g + 1));
+      if (p2) b[o2 * kCandRows] = make_uint2(__float_as_uint(__fsub_rd(s2, E)), (uint32_t)(pos0 + 4 * g + 2));
+      if (p3) b[o3 * kCandRows] = make_uint2(__float_as_uint(__fsub_rd(s3, E)), (uint32_t)(pos0 + 4 * g + 3));
       c = o3 + p3;
       if (gp) vmax = fmaxf(vmax, __fsub_rd(g4[g], E));
     }
@@ -145,15 +180,14 @@ __device__ __forceinline__ void cand_append_chunk(ScoreFn s_of, const float (&g4
 }
 
 // After a chunk: if any row of the warp may not have room for another chunk, refresh all.
-__device__ __forceinline__ void cand_maybe_refresh(CandRow& me, float* clo, int* cid, int rloc, float e0x2,
-                                                   int kmax) {
-  if (__any_sync(0xffffffffu, me.cnt > kCand - 32)) me = cand_refresh(me, clo, cid, rloc, e0x2, kmax);
+__device__ __forceinline__ void cand_maybe_refresh(CandRow& me, CandSmem sm, int rloc, float e0x2, int kmax) {
+  if (__any_sync(0xffffffffu, me.cnt > kCand - 32)) me = cand_refresh(me, sm, rloc, e0x2, kmax);
 }
 
 // Process one chunk of 32 scores: group maxima, one compare, appends only if needed.
 template <typename ScoreFn>
-__device__ __forceinline__ void cand_chunk(ScoreFn s_of, float E, int pos0, CandRow& me, float* clo, int* cid,
-                                           int rloc, float e0x2, int kmax) {
+__device__ __forceinline__ void cand_chunk(ScoreFn s_of, float E, int pos0, CandRow& me, CandSmem sm, int rloc,
+                                           float e0x2, int kmax) {
   float g4[8];
 #pragma unroll
   for (int g = 0; g < 8; ++g)
@@ -161,16 +195,15 @@ __device__ __forceinline__ void cand_chunk(ScoreFn s_of, float E, int pos0, Cand
   const float mx = fmaxf(fmaxf(fmaxf(g4[0], g4[1]), fmaxf(g4[2], g4[3])), fmaxf(fmaxf(g4[4], g4[5]), fmaxf(g4[6], g4[7])));
   const bool pass = __fadd_ru(mx, E) >= me.theta;
   if (!__any_sync(0xffffffffu, pass)) return;
-  cand_append_chunk(s_of, g4, E, pos0, me, clo, cid, rloc);
-  cand_maybe_refresh(me, clo, cid, rloc, e0x2, kmax);
+  cand_append_chunk(s_of, g4, E, pos0, me, sm, rloc);
+  cand_maybe_refresh(me, sm, rloc, e0x2, kmax);
 }
 
 // Final compaction of every row of the warp, then write the candidates out.
-__device__ __forceinline__ void cand_finish(CandRow& me, float* clo, int* cid, int rloc, float e0x2, int kmax,
-                                            int64_t row, int64_t n, int32_t* __restrict__ cand,
-                                            int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list,
-                                            int* __restrict__ ovf_count) {
-  me = cand_refresh(me, clo, cid, rloc, e0x2, kmax);
+__device__ __forceinline__ void cand_finish(CandRow& me, CandSmem sm, int rloc, float e0x2, int kmax, int64_t row,
+                                            int64_t n, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
+                                            int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
+  me = cand_refresh(me, sm, rloc, e0x2, kmax);
   if (row < n) {
     if (me.ovf) {
       ccount[row] = -1;
@@ -178,7 +211,8 @@ __device__ __forceinline__ void cand_finish(CandRow& me, float* clo, int* cid, i
       ovf_list[slot] = (int32_t)row;
     } else {
       ccount[row] = me.cnt;
-      for (int i = 0; i < me.cnt; ++i) cand[row * kCand + i] = cid[i * kCandRows + rloc];
+      const uint2* b = sm.buf + rloc;
+      for (int i = 0; i < me.cnt; ++i) cand[row * kCand + i] = (int32_t)b[i * kCandRows].y;
     }
   }
 }
