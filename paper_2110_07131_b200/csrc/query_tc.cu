@@ -59,6 +59,70 @@ __device__ __forceinline__ int classify_tc(float acc, float thr_s, float qe) {
   return 2;
 }
 
+// Classify every pair of the flagged 32-column chunks (re-read from TMEM), then compact the
+// accepted and undecided pairs of the warp: one atomic per list per chunk.  Returns this
+// thread's (accepted, undecided) counts.
+__device__ __noinline__ uint2 q_slow(uint32_t flag, uint32_t tbase, int len, bool live, float thr_s,
+                                     const float* __restrict__ qe_sub, const int32_t* __restrict__ qp_sub,
+                                     uint64_t uo, int64_t row, bool force, unsigned long long* __restrict__ ctr,
+                                     uint64_t* __restrict__ acc_list, uint64_t* __restrict__ und_list, int64_t cap) {
+  using namespace sm100;
+  const int lane = threadIdx.x & 31;
+  uint32_t n_acc = 0, n_und = 0;
+#pragma unroll 1
+  while (flag) {
+    const int ci = __ffs(flag) - 1;
+    flag &= flag - 1;
+    const int col0 = 32 * ci;
+    uint32_t r[32];
+    tmem_ld32(tbase + col0, r);
+    tmem_ld_wait(r);
+    uint32_t am = 0, um = 0;
+    if (live) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (col0 + j < len) {
+          int cls = classify_tc(__uint_as_float(r[j]), thr_s, __ldg(qe_sub + col0 + j));
+          if (force && cls == 1) cls = 2;
+          am |= (uint32_t)(cls == 1) << j;
+          um |= (uint32_t)(cls == 2) << j;
+        }
+      }
+    }
+    const int na = __popc(am), nu = __popc(um);
+    n_acc += na;
+    n_und += nu;
+    // warp-inclusive prefix sums -> one atomic per list per chunk
+    int pa = na, pu = nu;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int xa = __shfl_up_sync(0xffffffffu, pa, o), xu = __shfl_up_sync(0xffffffffu, pu, o);
+      if (lane >= o) pa += xa, pu += xu;
+    }
+    const int ta = __shfl_sync(0xffffffffu, pa, 31), tu = __shfl_sync(0xffffffffu, pu, 31);
+    unsigned long long ba = 0, bu = 0;
+    if (lane == 31) {
+      if (ta) ba = atomicAdd(ctr + C_ACCEPTED_TOTAL, (unsigned long long)ta);
+      if (tu) bu = atomicAdd(ctr + C_UND_TOTAL, (unsigned long long)tu);
+    }
+    ba = __shfl_sync(0xffffffffu, ba, 31) + (pa - na);
+    bu = __shfl_sync(0xffffffffu, bu, 31) + (pu - nu);
+    while (am) {
+      const int j = __ffs(am) - 1;
+      am &= am - 1;
+      if ((int64_t)ba < cap) acc_list[ba] = ((uint64_t)(uint32_t)__ldg(qp_sub + col0 + j) << 32) | uo;
+      ++ba;
+    }
+    while (um) {
+      const int j = __ffs(um) - 1;
+      um &= um - 1;
+      if ((int64_t)bu < cap) und_list[bu] = ((uint64_t)(uint32_t)__ldg(qp_sub + col0 + j) << 32) | (uint64_t)row;
+      ++bu;
+    }
+  }
+  return make_uint2(n_acc, n_und);
+}
+
 }  // namespace
 
 template <int KB>
@@ -179,6 +243,10 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     }
   } else {
     // ------------------------------------------------ epilogue: one thread per user row
+    // Fast pass over the len scored columns (two halves of 4 chunks): chunk max vs the row's
+    // threshold.  Chunks where some pair may be accepted / undecided are flagged and classified
+    // by q_slow (one out-of-line copy: the hot loop stays inside the instruction cache), which
+    // re-reads them from TMEM before the stage is released.
     const int q = warp & 3;  // TMEM lane quadrant of this warp
     const int rloc = q * 32 + lane;
     const bool force = (flags & RMIPS_FLAG_FORCE_VERIFY) != 0;
@@ -194,13 +262,16 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
       const float sc = __ldg(qscale + s);
       const float thr_s = live ? __ldg(thrk + row) * sc : CUDART_INF_F;  // dead rows reject everything
       const float thr_abs = fabsf(thr_s) * 2.384185791015625e-07f;
-      const uint64_t uo = live ? (uint64_t)(uint32_t)__ldg(perm_u + row) : 0;
       const float* qe_sub = qerr + (int64_t)s * kQB;
-      const int32_t* qp_sub = qperm + (int64_t)s * kQB;
       if (live) n_scored += len;
+      // qerr is non-increasing along the norm-sorted slots: a chunk's first slot bounds it
+      float Emax[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) Emax[c] = __fadd_ru(__ldg(qe_sub + (32 * c < len ? 32 * c : 0)), thr_abs);
       mbar_wait(BAR(ACC_FULL + as), aph);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + as * kAccCols;
+      uint32_t flag = 0;  // warp-uniform: chunks that need the slow path
 #pragma unroll 1
       for (int h = 0; h * 128 < len; ++h) {
         uint32_t r[4][32];
@@ -214,67 +285,27 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
         reg_fence(r[3]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const int col0 = h * 128 + 32 * c;
-          if (col0 >= len) break;  // warp-uniform
-          if (col0 + 32 > len) {   // partial last chunk: columns >= len are not scored
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j >= len) r[c][j] = __float_as_uint(-CUDART_INF_F);
-          }
+          // columns >= len hold stale or zero values: a spurious flag only costs a slow-path
+          // visit, which masks them
           float g[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             g[i] = fmaxf(fmaxf(__uint_as_float(r[c][4 * i]), __uint_as_float(r[c][4 * i + 1])),
                          fmaxf(__uint_as_float(r[c][4 * i + 2]), __uint_as_float(r[c][4 * i + 3])));
           const float mx = fmaxf(fmaxf(fmaxf(g[0], g[1]), fmaxf(g[2], g[3])), fmaxf(fmaxf(g[4], g[5]), fmaxf(g[6], g[7])));
-          // qerr is non-increasing along the norm-sorted slots: the chunk's first slot bounds it
-          const float Emax = __fadd_ru(__ldg(qe_sub + col0), thr_abs);
-          const bool all_rej = !live || (__fadd_ru(mx, Emax) < thr_s);
-          if (__all_sync(0xffffffffu, all_rej)) continue;
-          // slow path: classify every pair of the chunk (lane-private masks, then one compaction)
-          uint32_t am = 0, um = 0;
-          if (!all_rej) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (col0 + j < len) {
-                int cls = classify_tc(__uint_as_float(r[c][j]), thr_s, __ldg(qe_sub + col0 + j));
-                if (force && cls == 1) cls = 2;
-                am |= (uint32_t)(cls == 1) << j;
-                um |= (uint32_t)(cls == 2) << j;
-              }
-            }
-          }
-          const int na = __popc(am), nu = __popc(um);
-          n_fast += na;
-          n_und += nu;
-          // warp-exclusive prefix sums -> one atomic per list per chunk
-          int pa = na, pu = nu;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int xa = __shfl_up_sync(0xffffffffu, pa, o), xu = __shfl_up_sync(0xffffffffu, pu, o);
-            if (lane >= o) pa += xa, pu += xu;
-          }
-          const int ta = __shfl_sync(0xffffffffu, pa, 31), tu = __shfl_sync(0xffffffffu, pu, 31);
-          unsigned long long ba = 0, bu = 0;
-          if (lane == 31) {
-            if (ta) ba = atomicAdd(ctr + C_ACCEPTED_TOTAL, (unsigned long long)ta);
-            if (tu) bu = atomicAdd(ctr + C_UND_TOTAL, (unsigned long long)tu);
-          }
-          ba = __shfl_sync(0xffffffffu, ba, 31) + (pa - na);
-          bu = __shfl_sync(0xffffffffu, bu, 31) + (pu - nu);
-          while (am) {
-            const int j = __ffs(am) - 1;
-            am &= am - 1;
-            if ((int64_t)ba < cap) acc_list[ba] = ((uint64_t)(uint32_t)__ldg(qp_sub + col0 + j) << 32) | uo;
-            ++ba;
-          }
-          while (um) {
-            const int j = __ffs(um) - 1;
-            um &= um - 1;
-            if ((int64_t)bu < cap) und_list[bu] = ((uint64_t)(uint32_t)__ldg(qp_sub + col0 + j) << 32) | (uint64_t)row;
-            ++bu;
-          }
+          const float em = h ? Emax[4 + c] : Emax[c];
+          const bool all_rej = !live || (__fadd_ru(mx, em) < thr_s);
+          flag |= (uint32_t)(!__all_sync(0xffffffffu, all_rej)) << (4 * h + c);
         }
+      }
+      // chunks at or beyond len are never classified
+      flag &= len >= 256 ? 0xffu : ((1u << ((len + 31) >> 5)) - 1u);
+      if (flag) {
+        const uint64_t uo = live ? (uint64_t)(uint32_t)__ldg(perm_u + row) : 0;
+        const uint2 cnts = q_slow(flag, tbase, len, live, thr_s, qe_sub, qperm + (int64_t)s * kQB, uo, row, force,
+                                  ctr, acc_list, und_list, cap);
+        n_fast += cnts.x;
+        n_und += cnts.y;
       }
       tc_fence_before();  // this accumulator stage is fully read: hand it back to the MMA warp
       __syncwarp();
