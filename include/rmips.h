@@ -133,12 +133,13 @@ RMIPS_API rmips_status_t rmips_query_host(rmips_index_t idx, const float* q_batc
 RMIPS_API rmips_status_t rmips_query_stats(rmips_index_t idx, rmips_stats_t* out);
 
 /* Index introspection (for tests and tools).  All outputs are HOST buffers.
- *   info[0..7] = n, m, d, k_max, d_pad, block_size, overflow_rows, build_flags
+ *   info[0..8] = n, m, d, k_max, d_pad, block_size, overflow_rows, build_flags,
+ *                candidates kept by the build filter (sum over rows; info[9..15] reserved, 0)
  *   perm_u[n], perm_p[m]: sorted position -> original id (norm descending, ties by id)
  *   tau[k_max * n] fp64 and ids[k_max * n] int32: column-major by rank, users in ORIGINAL
  *   order: tau[j * n + u] = (j+1)-th largest u.p over P, ids = its original item id.
  *   Any of perm_u/perm_p/tau/ids may be NULL to skip it. */
-RMIPS_API rmips_status_t rmips_index_info(rmips_index_t idx, int64_t info[8]);
+RMIPS_API rmips_status_t rmips_index_info(rmips_index_t idx, int64_t info[16]);
 RMIPS_API rmips_status_t rmips_index_export(rmips_index_t idx, int64_t* perm_u, int64_t* perm_p, double* tau,
                                   int32_t* ids);
 

@@ -154,6 +154,7 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
   rmips_index_s* x = new rmips_index_s();
   x->n = n; x->m = m; x->d = d; x->kmax = k_max; x->build_flags = build_flags;
   x->dpad = round_up(d, 64);
+  x->pd = round_up(d, 8);
   x->nblocks = (n + kTileU - 1) / kTileU;
   x->c1 = filter_c1(x->dpad);
   x->c2 = filter_c2(x->dpad);
@@ -174,7 +175,7 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
     x->U16 = dalloc<__half>(n * x->dpad, st);
     x->U32 = dalloc<float>(n * d, st);
     x->P16 = dalloc<__half>(m * x->dpad, st);
-    x->P32 = dalloc<float>(m * d, st);
+    x->P32 = dalloc<float>(m * x->pd, st);
     x->tau = dalloc<double>((int64_t)k_max * n, st);
     x->ids = dalloc<int32_t>((int64_t)k_max * n, st);
     x->thr = dalloc<float>((int64_t)k_max * n, st);
@@ -191,6 +192,8 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
     c.ccount = dalloc<int32_t>(n, st);
     c.ovf_list = dalloc<int32_t>(n, st);
     c.ovf_count = dalloc<int>(1, st);
+    c.cand_total = dalloc<unsigned long long>(1, st);
+    CK(cudaMemsetAsync(c.cand_total, 0, sizeof(unsigned long long), st));
     const int fb_grid = 16;
     scratch = dalloc<double>((int64_t)fb_grid * m, st);
     CK(cudaMemsetAsync(x->d_flags, 0, 4 * sizeof(int), st));
@@ -223,13 +226,15 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
     CK(cudaMemcpyAsync(hp, x->d_flags, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hp + 1, c.ovf_count, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hp + 2, c.scale_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hp + 4, c.cand_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     dfree(c.norm_u_raw, st); dfree(c.norm_p_raw, st); dfree(c.iota_u, st); dfree(c.iota_p, st);
     dfree(c.maxabs, st); dfree(c.cand, st); dfree(c.ccount, st); dfree(c.ovf_list, st);
-    dfree(c.ovf_count, st); dfree(scratch, st);
+    dfree(c.ovf_count, st); dfree(c.cand_total, st); dfree(scratch, st);
     if (c.cub_tmp) cudaFreeAsync(c.cub_tmp, st);
     CK(cudaStreamSynchronize(st));
     int flags = hp[0];
     x->overflow_rows = hp[1];
+    memcpy(&x->cand_total, hp + 4, sizeof(int64_t));
     if (tm.on) {
       x->phase_ms[0] = tm.between(0, 1);
       x->phase_ms[1] = tm.between(1, 2);
@@ -456,8 +461,10 @@ rmips_status_t rmips_query_stats(rmips_index_t idx, rmips_stats_t* out) {
   return RMIPS_OK;
 }
 
-rmips_status_t rmips_index_info(rmips_index_t idx, int64_t info[8]) {
+rmips_status_t rmips_index_info(rmips_index_t idx, int64_t info[16]) {
   if (!idx || !info) return fail(RMIPS_ERR_INVALID, "NULL argument");
+  for (int i = 8; i < 16; ++i) info[i] = 0;
+  info[8] = idx->cand_total;
   info[0] = idx->n; info[1] = idx->m; info[2] = idx->d; info[3] = idx->kmax;
   info[4] = idx->dpad; info[5] = kTileU; info[6] = idx->overflow_rows; info[7] = idx->build_flags;
   return RMIPS_OK;

@@ -64,7 +64,7 @@ __global__ void k_prep_users(const float* __restrict__ Q, int64_t n, int d, int 
 }
 
 // Items: P16 = fp16(p * 2^e) with max|p*2^e| < 2^14; perr = filter error bound (scaled units).
-__global__ void k_prep_items(const float* __restrict__ P, int64_t m, int d, int dpad,
+__global__ void k_prep_items(const float* __restrict__ P, int64_t m, int d, int dpad, int pd,
                              const int32_t* __restrict__ perm, const double* __restrict__ norm_sorted,
                              const unsigned int* __restrict__ maxabs_bits, double c1, double c2,
                              __half* __restrict__ P16, float* __restrict__ P32, float* __restrict__ perr,
@@ -82,7 +82,7 @@ __global__ void k_prep_items(const float* __restrict__ P, int64_t m, int d, int 
   int64_t o = perm[r];
   float x = j < d ? P[o * d + j] : 0.f;
   P16[idx] = __float2half_rn(x * scale);
-  if (j < d) P32[r * d + j] = x;
+  if (j < pd) P32[r * pd + j] = x;  // zero padding up to pd
   if (j == 0) {
     double b = norm_sorted[r] * (double)scale;
     perr[r] = __double2float_ru((c1 * b + c2) * (1.0 + 1e-6));
@@ -155,47 +155,138 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
 }
 
 // ------------------------------------------------------------------------------ B5
-// Warp per user row: exact fp64 value of every candidate (dot64, R7), then the
-// k_max largest by (value desc, original item id asc).  Writes the column-major tables.
-__global__ void __launch_bounds__(256)
+// Warp per user row (grid-stride): exact fp64 value of every candidate (dot64 order, DESIGN.md
+// R7), then the k_max largest by (value desc, original item id asc) with a warp bitonic sort,
+// written to the column-major tables.  Candidate item rows are staged in shared memory 32 at a
+// time with coalesced loads (the rows are scattered in P32), then each lane runs the sequential
+// fp64 sum of its own candidate from shared memory.
+struct SelKey {
+  double v;
+  int id;
+};
+// (value desc, id asc); non-short-circuit operators keep it branch-free (predicate logic only)
+__device__ __forceinline__ bool sel_better(const SelKey& a, const SelKey& b) {
+  return (a.v > b.v) | ((a.v == b.v) & (a.id < b.id));
+}
+__device__ __forceinline__ SelKey shfl_xor_key(const SelKey& k, int m) {
+  SelKey r;
+  r.v = __shfl_xor_sync(0xffffffffu, k.v, m);
+  r.id = __shfl_xor_sync(0xffffffffu, k.id, m);
+  return r;
+}
+
+// Bitonic sort of 32*E keys held striped (element e = i*32 + lane in key[i]), best first.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(SelKey (&key)[E]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {  // partner in the same lane, register i ^ (j / 32)
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int ip = i ^ (j >> 5);
+          if (ip > i) {
+            const int e = i * 32 + lane;
+            const bool up = (e & k) == 0;  // this k-block sorts best-first
+            const bool ob = sel_better(key[ip], key[i]), mb = sel_better(key[i], key[ip]);
+            const bool sw = up ? ob : mb;
+            const SelKey a = key[i], b = key[ip];
+            key[i].v = sw ? b.v : a.v;
+            key[i].id = sw ? b.id : a.id;
+            key[ip].v = sw ? a.v : b.v;
+            key[ip].id = sw ? a.id : b.id;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int e = i * 32 + lane;
+          const SelKey o = shfl_xor_key(key[i], j);
+          const bool up = (e & k) == 0;
+          const bool lower = (e & j) == 0;  // this element sits at the lower index of the pair
+          // the lower index keeps the better key when sorting best-first, the worse otherwise
+          const bool ob = sel_better(o, key[i]), mb = sel_better(key[i], o);
+          const bool take = (lower == up) ? ob : mb;
+          key[i].v = take ? o.v : key[i].v;
+          key[i].id = take ? o.id : key[i].id;
+        }
+      }
+    }
+  }
+}
+
+constexpr int kSelWarps = 8;
+__global__ void __launch_bounds__(32 * kSelWarps)
 k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, const int32_t* __restrict__ perm_p,
                const float* __restrict__ unu, const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount,
-               int64_t n, int d, int kmax, double* __restrict__ tau, int32_t* __restrict__ ids,
-               float* __restrict__ thr) {
-  __shared__ double sv[8][kCand];
-  __shared__ int so[8][kCand];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t row = blockIdx.x * (int64_t)8 + w;
-  if (row >= n) return;
-  const int cnt = ccount[row];
-  if (cnt < 0) return;  // overflowed: k_exact_row_full
-  const float* u = U32 + row * d;
-  for (int i = lane; i < cnt; i += 32) {
-    int pid = cand[row * kCand + i];
-    sv[w][i] = dot64(u, P32 + (int64_t)pid * d, d);
-    so[w][i] = perm_p[pid];
-  }
-  __syncwarp();
-  const float nu = unu[row];
-  for (int i = lane; i < cnt; i += 32) {
-    double vi = sv[w][i];
-    int oi = so[w][i];
-    int rank = 0;
-    for (int j = 0; j < cnt; ++j) {
-      double vj = sv[w][j];
-      rank += (vj > vi) || (vj == vi && so[w][j] < oi);
+               int64_t n, int d, int pd, int kmax, double* __restrict__ tau, int32_t* __restrict__ ids,
+               float* __restrict__ thr, unsigned long long* __restrict__ cand_total) {
+  extern __shared__ double ssel[];  // per warp: the user row [pd], widened to fp64 once, zero-padded
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  double* urow = ssel + (size_t)w * pd;
+  unsigned long long my_total = 0;
+  for (int64_t row = blockIdx.x * (int64_t)wpb + w; row < n; row += (int64_t)gridDim.x * wpb) {
+    const int cnt = ccount[row];
+    if (cnt < 0) continue;  // overflowed: k_exact_row_full
+    my_total += cnt;
+    __syncwarp();
+    for (int t = lane; t < pd; t += 32) urow[t] = t < d ? (double)U32[row * d + t] : 0.0;
+    __syncwarp();
+    SelKey key[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) key[i].v = -CUDART_INF, key[i].id = 0x7fffffff;
+    // one candidate per lane per round, 16-byte loads of the sector-padded item row.  The zero
+    // padding adds fma(0, 0, s) = s exactly (s is never -0: it starts at +0).
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (32 * i >= cnt) break;  // warp-uniform
+      const int c = 32 * i + lane;
+      if (c < cnt) {
+        const int pos = cand[row * kCand + c];
+        const float4* pr = reinterpret_cast<const float4*>(P32 + (int64_t)pos * pd);
+        double sacc = 0.0;  // dot64: left-to-right fp64 sum of exact fp32 x fp32 products
+#pragma unroll 4
+        for (int t = 0; t < pd / 4; ++t) {
+          const float4 a = __ldg(pr + t);
+          sacc = __fma_rn((double)a.x, urow[4 * t], sacc);
+          sacc = __fma_rn((double)a.y, urow[4 * t + 1], sacc);
+          sacc = __fma_rn((double)a.z, urow[4 * t + 2], sacc);
+          sacc = __fma_rn((double)a.w, urow[4 * t + 3], sacc);
+        }
+        key[i].v = sacc;
+        key[i].id = perm_p[pos];
+      }
     }
-    if (rank < kmax) {
-      tau[(int64_t)rank * n + row] = vi;
-      ids[(int64_t)rank * n + row] = oi;
-      thr[(int64_t)rank * n + row] = (float)(vi / (double)nu);
+    if (cnt <= 64) {
+      SelKey k2[2] = {key[0], key[1]};
+      warp_bitonic<2>(k2);
+      key[0] = k2[0];
+      key[1] = k2[1];
+    } else {
+      warp_bitonic<4>(key);
+    }
+    const float nu = unu[row];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rank = i * 32 + lane;
+      if (rank < kmax) {
+        const bool ok = rank < cnt;
+        tau[(int64_t)rank * n + row] = ok ? key[i].v : -CUDART_INF;
+        ids[(int64_t)rank * n + row] = ok ? key[i].id : -1;
+        thr[(int64_t)rank * n + row] = ok ? (float)(key[i].v / (double)nu) : -CUDART_INF_F;
+      }
+    }
+    if (kmax > 128 && lane == 0) {  // k_max beyond the candidate buffer: only when m < k_max
+      for (int r = 128; r < kmax; ++r) {
+        tau[(int64_t)r * n + row] = -CUDART_INF;
+        ids[(int64_t)r * n + row] = -1;
+        thr[(int64_t)r * n + row] = -CUDART_INF_F;
+      }
     }
   }
-  for (int r = cnt + lane; r < kmax; r += 32) {  // only when m < kmax
-    tau[(int64_t)r * n + row] = -CUDART_INF;
-    ids[(int64_t)r * n + row] = -1;
-    thr[(int64_t)r * n + row] = -CUDART_INF_F;
-  }
+  if (lane == 0 && my_total) atomicAdd(cand_total, my_total);
 }
 
 // B5': exact top-k_max of a whole row (fp64 over all of P), for overflowed rows.  One CTA per
@@ -204,7 +295,7 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
 __global__ void __launch_bounds__(256)
 k_exact_row_full(const float* __restrict__ U32, const float* __restrict__ P32, const int32_t* __restrict__ perm_p,
                  const float* __restrict__ unu, const int32_t* __restrict__ ovf_list, const int* __restrict__ ovf_count,
-                 int64_t n, int64_t m, int d, int kmax, double* __restrict__ scratch, double* __restrict__ tau,
+                 int64_t n, int64_t m, int d, int pd, int kmax, double* __restrict__ scratch, double* __restrict__ tau,
                  int32_t* __restrict__ ids, float* __restrict__ thr) {
   __shared__ double bv[256];
   __shared__ int bo[256];
@@ -214,7 +305,7 @@ k_exact_row_full(const float* __restrict__ U32, const float* __restrict__ P32, c
   for (int t = blockIdx.x; t < nrows; t += gridDim.x) {
     const int64_t row = ovf_list[t];
     const float* u = U32 + row * d;
-    for (int64_t j = threadIdx.x; j < m; j += blockDim.x) sc[j] = dot64(u, P32 + j * d, d);
+    for (int64_t j = threadIdx.x; j < m; j += blockDim.x) sc[j] = dot64(u, P32 + j * pd, d);
     __syncthreads();
     double pv = CUDART_INF;
     int po = -1;
@@ -330,7 +421,7 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
   // B3
   if (n)
     k_prep_users<<<nblk(n * dpad, 256), 256, 0, st>>>(Q, n, d, dpad, x->perm_u, x->unorm, x->U16, x->U32, x->unu); count_launch();
-  k_prep_items<<<nblk(m * dpad, 256), 256, 0, st>>>(P, m, d, dpad, x->perm_p, x->pnorm, c.maxabs, x->c1, x->c2,
+  k_prep_items<<<nblk(m * dpad, 256), 256, 0, st>>>(P, m, d, dpad, x->pd, x->perm_p, x->pnorm, c.maxabs, x->c1, x->c2,
                                                     x->P16, x->P32, x->perr, c.scale_dev); count_launch();
   return cudaGetLastError();
 }
@@ -347,8 +438,14 @@ size_t build_cub_bytes(int64_t n, int64_t m) {
 cudaError_t build_select(BuildCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   if (x->n == 0) return cudaSuccess;
-  k_exact_select<<<nblk(x->n, 8), 256, 0, st>>>(x->U32, x->P32, x->perm_p, x->unu, c.cand, c.ccount, x->n, x->d,
-                                                x->kmax, x->tau, x->ids, x->thr); count_launch();
+  const size_t smem = (size_t)kSelWarps * x->pd * sizeof(double);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->device);
+  const int64_t want = (x->n + kSelWarps - 1) / kSelWarps;
+  const int grid = (int)(want < (int64_t)sms * 8 ? want : (int64_t)sms * 8);
+  k_exact_select<<<grid, 32 * kSelWarps, smem, st>>>(x->U32, x->P32, x->perm_p, x->unu, c.cand, c.ccount, x->n,
+                                                     x->d, x->pd, x->kmax, x->tau, x->ids, x->thr, c.cand_total);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -356,7 +453,7 @@ cudaError_t build_fallback(BuildCtx& c, int nrows, double* scratch, int grid, cu
   rmips_index_s* x = c.idx;
   if (nrows <= 0) return cudaSuccess;
   k_exact_row_full<<<grid, 256, 0, st>>>(x->U32, x->P32, x->perm_p, x->unu, c.ovf_list, c.ovf_count, x->n, x->m,
-                                         x->d, x->kmax, scratch, x->tau, x->ids, x->thr); count_launch();
+                                         x->d, x->pd, x->kmax, scratch, x->tau, x->ids, x->thr); count_launch();
   return cudaGetLastError();
 }
 

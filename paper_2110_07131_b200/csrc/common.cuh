@@ -106,9 +106,11 @@ inline double filter_c2(int dpad) { return std::ldexp(1.0, -24) * std::sqrt((dou
 struct rmips_index_s {
   int64_t n = 0, m = 0;
   int d = 0, dpad = 0, kmax = 0, build_flags = 0;
+  int pd = 0;               // P32 row pitch in floats: d rounded up to 8 (whole 32-byte sectors)
   int device = 0;
   int64_t nblocks = 0;
   int64_t overflow_rows = 0;
+  int64_t cand_total = 0;   // candidates kept by the build filter (sum over non-overflowed rows)
   float pscale = 1.f;       // items are scaled by 2^e before fp16 rounding
   double c1 = 0, c2 = 0;    // filter error constants (see common.cuh)
 
@@ -122,7 +124,7 @@ struct rmips_index_s {
   __half* U16 = nullptr;       // [n][dpad] fp16 u/nu (sorted)
   float* U32 = nullptr;        // [n][d] fp32 u (sorted) -- exact path
   __half* P16 = nullptr;       // [m][dpad] fp16 p*2^e (sorted)
-  float* P32 = nullptr;        // [m][d] fp32 p (sorted) -- exact path
+  float* P32 = nullptr;        // [m][pd] fp32 p (sorted, zero-padded rows) -- exact path
 
   // exact lower-bound arrays (Def. 4), column-major by rank: x[j*n + u]
   double* tau = nullptr;       // [kmax][n] (j+1)-th largest u.p over P, fp64 (sorted users)

@@ -31,6 +31,7 @@ struct BuildCtx {
   int32_t* ccount = nullptr;      // [n] candidates per row, -1 = overflowed
   int32_t* ovf_list = nullptr;    // [n] overflowed rows
   int* ovf_count = nullptr;       // device counter
+  unsigned long long* cand_total = nullptr;  // device: candidates kept by the filter (sum over rows)
 };
 
 size_t build_cub_bytes(int64_t n, int64_t m);

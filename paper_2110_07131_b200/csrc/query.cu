@@ -210,8 +210,8 @@ constexpr int kScanPitch = 257;  // floats per staged item row (d <= 256), odd =
 __global__ void __launch_bounds__(32 * kScanWarps)
 k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const double* __restrict__ unorm,
               const float* __restrict__ P32, const double* __restrict__ pnorm, const int32_t* __restrict__ perm_u,
-              int64_t m, int d, int k, unsigned long long* __restrict__ ctr, const uint64_t* __restrict__ und_list,
-              uint64_t* __restrict__ acc_list, int64_t cap) {
+              int64_t m, int d, int pd, int k, unsigned long long* __restrict__ ctr,
+              const uint64_t* __restrict__ und_list, uint64_t* __restrict__ acc_list, int64_t cap) {
   extern __shared__ float sp[];  // [kScanWarps][32][kScanPitch]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float* my = sp + (size_t)w * 32 * kScanPitch;
@@ -230,9 +230,9 @@ k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const 
     for (int64_t base = 0; base < m && !decided; base += 32) {
       const int nrow = (int)min((int64_t)32, m - base);
       // Corollary 1 on the first item of the chunk (lane-parallel over the chunk below)
-      const float* src = P32 + base * d;
+      const float* src = P32 + base * pd;  // rows of pd floats (zero-padded)
       __syncwarp();
-      for (int e = lane; e < nrow * d; e += 32) my[(e / d) * kScanPitch + (e % d)] = __ldg(src + e);
+      for (int e = lane; e < nrow * pd; e += 32) my[(e / pd) * kScanPitch + (e % pd)] = __ldg(src + e);
       __syncwarp();
       const int64_t j = base + lane;
       bool in = lane < nrow;
@@ -329,7 +329,7 @@ cudaError_t query_exact(QueryCtx& c, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(k_verify_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_verify_scan<<<148 * 4, 32 * kScanWarps, smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
-                                                           x->d, c.k, c.counters, c.und, c.acc, c.cap); count_launch();
+                                                           x->d, x->pd, c.k, c.counters, c.und, c.acc, c.cap); count_launch();
   } else {
     k_exact_decide<<<148 * 8, 256, 0, st>>>(c.q, x->U32, x->tau + (int64_t)(c.k - 1) * x->n, x->perm_u, x->d,
                                             c.counters, c.und, c.acc, c.cap); count_launch();

@@ -106,10 +106,10 @@ class Index:
 
     def __init__(self, handle: int):
         self.handle = ctypes.c_void_p(handle)
-        info = (ctypes.c_int64 * 8)()
+        info = (ctypes.c_int64 * 16)()
         _check(lib.rmips_index_info(self.handle, info))
-        self.n, self.m, self.d, self.k_max, self.d_pad, self.block_size, self.overflow_rows, self.build_flags = \
-            [int(v) for v in info]
+        self.n, self.m, self.d, self.k_max, self.d_pad, self.block_size, self.overflow_rows, self.build_flags, \
+            self.cand_total = [int(v) for v in info[:9]]
 
     def close(self):
         if self.handle:
