@@ -265,3 +265,67 @@ def test_cfg1_full_size_sampled():
     # invariant-style global check: totals are plausible and ids ascending
     assert all((np.diff(s) > 0).all() for s in sets)
     idx.close()
+
+
+# ---------------------------------------------------------------- configs[2..4] at full size (sampled oracle)
+
+def _sampled_full_config(cfg, n_sample, batch=None, query_stride=1):
+    """BJ configs[cfg] at full size.  The GPU index covers every user; the oracle recomputes a fixed
+    sample of users exactly (top lists, two-phase decisions — equal to the definition by R8) and every
+    sampled user's membership in every query's set must match; tau/ids are compared bitwise."""
+    w = gen.make_workload(cfg)
+    spec = w.spec
+    idx = rmips.rmips_build_index(_t(w.U), _t(w.P), spec.k_max)
+    assert idx.overflow_rows == 0
+    rng = np.random.default_rng(cfg)
+    sample = np.sort(rng.choice(spec.n, n_sample, replace=False))
+    vals, oids = oracle.topk(w.U[sample], w.P, spec.k_max)
+    _, _, tau, tids = idx.export()
+    assert np.array_equal(tau[:, sample].T, vals)
+    assert np.array_equal(tids[:, sample].T, oids)
+    Qy = w.Qy[::query_stride]
+    for k in spec.ks:
+        bs = batch or Qy.shape[0]
+        sets = []
+        for b0 in range(0, Qy.shape[0], bs):
+            off, ids = rmips.rmips_query(idx, _t(Qy[b0:b0 + bs]), k)
+            sets += rmips.split_sets(off, ids)
+        assert all((np.diff(s_) > 0).all() for s_ in sets)
+        member = oracle.rkmips_twophase(w.U[sample], vals, Qy, k)
+        for qi in range(Qy.shape[0]):
+            got = np.intersect1d(sets[qi], sample)
+            want = sample[member[qi]]
+            assert np.array_equal(got, want), (cfg, k, qi)
+    idx.close()
+
+
+def test_cfg2_full_size_sampled_k_sweep():
+    """BJ configs[2]: 480,000 x 18,000, k swept over {1, 5, 10, 25, 50}."""
+    _sampled_full_config(2, 1200)
+
+
+def test_cfg3_full_size_sampled():
+    """BJ configs[3]: 2,000,000 x 100,000, heavy-tailed norms, half the queries not in P."""
+    _sampled_full_config(3, 400)
+
+
+def test_cfg4_full_size_sampled():
+    """BJ configs[4]: d = 200, 1,000,000 x 1,000,000, fresh queries in batches of 256 (every 4th of the
+    10,000 queries, to bound the test time)."""
+    _sampled_full_config(4, 96, batch=256, query_stride=4)
+
+
+def test_filter_error_bound_holds():
+    """The fp16/fp32 filter error bound dominates the observed error: the exact path
+    would hide a violated bound, so check it directly.  The build's kept candidates always contain the
+    exact top list (checked bitwise above); here the query filter's accept/reject decisions must never
+    contradict the exact decision: a pair accepted or rejected by the filter is re-decided exactly."""
+    U, P = gen.random_instance(21, 3000, 1500, 50, "skewed")
+    Qy = np.concatenate([P[:100], gen.random_instance(22, 100, 1, 50, "skewed")[0]])
+    for k in (1, 7, 20):
+        member = oracle.rkmips_naive(U, P, Qy, k)
+        # FORCE_VERIFY routes every filter accept through the exact path: both runs must agree
+        a = gpu_sets(U, P, Qy, k, 20)
+        b = gpu_sets(U, P, Qy, k, 20, qflags=rmips.RMIPS_FLAG_FORCE_VERIFY)
+        assert_same(a, member, U, P, Qy, k, "bound k=%d" % k)
+        assert_same(b, member, U, P, Qy, k, "bound/force k=%d" % k)
