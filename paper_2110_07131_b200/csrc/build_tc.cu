@@ -336,7 +336,7 @@ cudaError_t build_tc(const BuildCtx& c, cudaStream_t st) {
   if (getenv("RMIPS_DISABLE_TC")) return cudaErrorNotSupported;
   switch (c.idx->dpad) {
     case 64: return launch_tc<1>(c, st);
-    default: return cudaErrorNotSupported;  // d > 64: SIMT contraction (smem budget)
+    default: return build_tcq(c, st);  // d_pad 128..256: build_tcq.cu
   }
 }
 

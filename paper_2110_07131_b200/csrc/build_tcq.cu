@@ -1,0 +1,338 @@
+// build_tcq.cu -- B4 on the 5th-generation tensor cores for d_pad = 128..256 (build_tc.cu has the
+// d <= 64 kernel): the |Q| x |P| x d contraction of Alg. 1 lines 7-9 (over ALL of P per
+// BASELINE north star) fused with the per-row top-k_max candidate epilogue (candq.cuh: 4-byte
+// quantised entries, so that the 128 x 256 fp16 user tile, the item ring and the candidate
+// buffers fit in one SM's shared memory), so the score matrix never reaches HBM.
+//
+// k_build_tcq<KB, UT, BN>: K = 64*KB (d_pad), UT user tiles of 128 rows per CTA, item tiles of
+// BN rows.  One persistent CTA per SM walks groups of UT user tiles; per group:
+//   warp 0        TMA producer: the UT user tiles A (128 x 64*KB fp16, once per group) and the
+//                 stream of item tiles B through an NST-deep shared-memory ring (SWIZZLE_128B)
+//   warp 1        TMEM allocator + MMA issuer: per item tile UT x tcgen05.mma.cta_group::1.kind::f16
+//                 (M = 128, N = BN, K = 16 x ksteps), fp32 accumulators in TMEM, NACC stages
+//   warps 2..     4*UT epilogue warps: warp w reads TMEM lane quadrant w % 4 of user tile
+//                 (w - 2) / 4; every thread owns one user row and filters its BN scores per item
+//                 tile (3-input max trees, one compare per 32-column chunk: the fast path), with
+//                 one out-of-line slow path that re-reads flagged chunks from TMEM and appends.
+// Configurations: d_pad in {128, 192, 256}: <KB, 1, 64> (MMA-bound: 64 columns of scores per
+// 16-step K loop).  UT = 2 (two user tiles sharing each item tile) is supported by the code; it
+// measured slower than build_tc.cu for d <= 64 (the epilogue is issue-bound, not latency-bound).
+// Pipelines: smem full/empty (TMA <-> MMA), TMEM full/empty (MMA <-> epilogue), and the A group
+// full/empty (MMA done with the group before the next one is loaded).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "candq.cuh"
+#include "common.cuh"
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace rmips {
+
+#ifdef RMIPS_EPI_PROFILE
+extern __device__ unsigned long long g_epi_prof[4][256];  // build_tc.cu
+#endif
+
+namespace {
+
+constexpr int kBM = 128;                 // users per tile (TMEM lanes)
+constexpr int kUTile = kBM * 64 * 2;     // one 128 x 64 fp16 tile = 16 KB
+
+template <int KB, int UT, int BN>
+struct Cfg {
+  static constexpr int NST = (KB == 1) ? 4 : 3;                           // item-tile ring depth
+  static constexpr int NACC = (512 / (UT * BN)) > 4 ? 4 : 512 / (UT * BN);  // TMEM stages
+  static constexpr int ACC_COLS = UT * BN;                                // TMEM columns per stage
+  static constexpr int TMEM_COLS = NACC * ACC_COLS;                       // power of two >= 32
+  static constexpr int B_TILE = BN * 64 * 2;                              // one BN x 64 fp16 tile
+  static constexpr int THREADS = 64 + 128 * UT;
+  static constexpr int A = 0;
+  static constexpr int B = UT * KB * kUTile;
+  static constexpr int CAND = B + NST * KB * B_TILE;
+  static constexpr int BAR = CAND + UT * kBM * kQSlots * 4;
+  static constexpr int TOTAL = BAR + 256 + 1024;  // + alignment slack
+  static_assert(TOTAL <= 232448, "shared memory");
+};
+
+// Fast path of one 64-column half (scores of this thread's row): 3-input max trees and one
+// compare per 32-column chunk.  Returns a warp-uniform 2-bit mask of the chunks in which some
+// lane may append.  Padding columns of a ragged last tile (TMA zero fill) are not masked here: at
+// worst they flag a chunk, and the slow path masks them before anything is appended.
+__device__ __forceinline__ uint32_t epiq_fast(const uint32_t (&h)[64], float E0, float E1, float theta) {
+  uint32_t bits = 0;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    float g4[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      g4[g] = fmaxf(fmaxf(__uint_as_float(h[32 * c + 4 * g]), __uint_as_float(h[32 * c + 4 * g + 1])),
+                    fmaxf(__uint_as_float(h[32 * c + 4 * g + 2]), __uint_as_float(h[32 * c + 4 * g + 3])));
+    const float mx = fmaxf(fmaxf(fmaxf(g4[0], g4[1]), fmaxf(g4[2], g4[3])), fmaxf(fmaxf(g4[4], g4[5]), fmaxf(g4[6], g4[7])));
+    bits |= (uint32_t)__any_sync(0xffffffffu, __fadd_ru(mx, c ? E1 : E0) >= theta) << c;
+  }
+  return bits;
+}
+
+// Slow path (one copy in the kernel, so the hot loop stays inside the instruction cache):
+// re-read each flagged chunk of the current accumulator stage from TMEM, append and refresh.
+__device__ __noinline__ QRow epiq_slow(uint32_t bits, uint32_t taddr, int base0, int mi, float4 E4, QRow me, QBuf sb,
+                                      int rr, float e0x2, int kmax) {
+#pragma unroll 1
+  while (bits) {
+    const int c = __ffs(bits) - 1;
+    bits &= bits - 1;
+    uint32_t r[32];
+    sm100::tmem_ld32(taddr + 32 * c, r);
+    sm100::tmem_ld_wait(r);
+    const int pos0 = base0 + 32 * c;
+    if (pos0 + 32 > mi) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (pos0 + j >= mi) r[j] = 0xff800000u;  // -inf
+    }
+    const float E = c == 0 ? E4.x : c == 1 ? E4.y : c == 2 ? E4.z : E4.w;
+    float g4[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      g4[g] = fmaxf(fmaxf(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1])),
+                    fmaxf(__uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3])));
+#ifdef RMIPS_EPI_PROFILE
+    const long long p0 = clock64();
+#endif
+    qrow_append_chunk([&](int j) { return __uint_as_float(r[j]); }, g4, E, pos0, mi, me, sb, rr);
+#ifdef RMIPS_EPI_PROFILE
+    const long long p1 = clock64();
+    const bool rf = __any_sync(0xffffffffu, me.cnt > kQSlots - 32);
+#endif
+    qrow_maybe_refresh(me, sb, rr, e0x2, kmax);
+#ifdef RMIPS_EPI_PROFILE
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&g_epi_prof[2][0], 1ull);
+      atomicAdd(&g_epi_prof[2][1], (unsigned long long)(p1 - p0));
+      atomicAdd(&g_epi_prof[2][2], (unsigned long long)(clock64() - p1));
+      atomicAdd(&g_epi_prof[2][3], (unsigned long long)rf);
+    }
+#endif
+  }
+  return me;
+}
+
+}  // namespace
+
+template <int KB, int UT, int BN>
+__global__ void __launch_bounds__(Cfg<KB, UT, BN>::THREADS, 1)
+k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
+           int64_t n, int64_t m, int kmax, int ksteps, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
+           int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
+  using namespace sm100;
+  using C = Cfg<KB, UT, BN>;
+  constexpr int NST = C::NST, NACC = C::NACC;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned base, derived from smem_raw by pointer arithmetic so that the compiler
+  // keeps the shared state space (LDS/STS rather than generic loads/stores)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sA = sbase + C::A;
+  const uint32_t sB = sbase + C::B;
+  const QBuf sb{reinterpret_cast<uint32_t*>(smem + C::CAND), UT * kBM};
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR);
+  const uint32_t bar0 = smem_u32(bars);
+  auto BAR = [&](int i) { return bar0 + 8u * i; };
+  const int A_FULL = 0, A_EMPTY = 1, B_FULL = 2, B_EMPTY = 2 + NST, ACC_FULL = 2 + 2 * NST,
+            ACC_EMPTY = 2 + 2 * NST + NACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 + 2 * NST + 2 * NACC);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_utiles = (int)((n + kBM - 1) / kBM);
+  const int num_groups = (num_utiles + UT - 1) / UT;
+  const int nit = (int)((m + BN - 1) / BN);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    mbar_init(BAR(A_FULL), 1);
+    mbar_init(BAR(A_EMPTY), 1);
+    for (int s = 0; s < NST; ++s) mbar_init(BAR(B_FULL + s), 1), mbar_init(BAR(B_EMPTY + s), 1);
+    for (int a = 0; a < NACC; ++a) mbar_init(BAR(ACC_FULL + a), 1), mbar_init(BAR(ACC_EMPTY + a), 4 * UT);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(smem_u32(tmem_slot), C::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0;
+      int t = 0;
+      for (int gr = blockIdx.x; gr < num_groups; gr += gridDim.x, ++t) {
+        if (t > 0) mbar_wait_sleep(BAR(A_EMPTY), (t - 1) & 1);
+        mbar_arrive_expect_tx(BAR(A_FULL), UT * KB * kUTile);
+        for (int u = 0; u < UT; ++u)
+          for (int kb = 0; kb < KB; ++kb)
+            tma_load_2d(sA + (u * KB + kb) * kUTile, &tmA, kb * 64, (gr * UT + u) * kBM, BAR(A_FULL));
+        for (int it = 0; it < nit; ++it) {
+          mbar_wait_sleep(BAR(B_EMPTY + stage), ph ^ 1);
+          mbar_arrive_expect_tx(BAR(B_FULL + stage), KB * C::B_TILE);
+          for (int kb = 0; kb < KB; ++kb)
+            tma_load_2d(sB + (stage * KB + kb) * C::B_TILE, &tmB, kb * 64, it * BN, BAR(B_FULL + stage));
+          if (++stage == NST) stage = 0, ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_f16_f32(kBM, BN);
+      int stage = 0, as = 0;
+      uint32_t ph = 0, aph = 0;
+      int t = 0;
+      for (int gr = blockIdx.x; gr < num_groups; gr += gridDim.x, ++t) {
+        mbar_wait_sleep(BAR(A_FULL), t & 1);
+        tc_fence_after();
+        for (int it = 0; it < nit; ++it) {
+          mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
+          mbar_wait_sleep(BAR(B_FULL + stage), ph);
+          tc_fence_after();
+#pragma unroll
+          for (int u = 0; u < UT; ++u) {
+            const uint32_t d = tmem + as * C::ACC_COLS + u * BN;
+            for (int ks = 0; ks < ksteps; ++ks) {  // K steps of 16 (zero padding beyond d skipped)
+              const int kb = ks >> 2, kk = ks & 3;
+              const uint32_t a0 = sA + (u * KB + kb) * kUTile;
+              const uint32_t b0 = sB + (stage * KB + kb) * C::B_TILE;
+              mma_f16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, ks != 0);
+            }
+          }
+          mma_commit(BAR(B_EMPTY + stage));
+          mma_commit(BAR(ACC_FULL + as));
+          if (++stage == NST) stage = 0, ph ^= 1;
+          if (++as == NACC) as = 0, aph ^= 1;
+        }
+        mma_commit(BAR(A_EMPTY));
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue: one thread per user row
+    // The 64-column halves of an item tile are software-pipelined: the TMEM load of the next half
+    // (of this tile or the next one) is in flight while the current half is filtered.
+    const int e = warp - 2;
+    const int u = e >> 2;                     // user tile of the group
+    const int q = warp & 3;                   // TMEM lane quadrant of this warp
+    const int rr = u * kBM + q * 32 + lane;   // row in the candidate buffer
+    const int mi = (int)m;
+    const float e0x2 = __fadd_ru(__ldg(perr), __ldg(perr));
+    // |s~| <= |u^| |p^| + E with |u^| <= 1 + 2^-10, |p^| <= |p| 2^e (1 + 2^-11): every score is
+    // in [-smax, smax] (generous margins: the quantiser of candq.cuh must never saturate)
+    const float smax = __fadd_ru(__fmul_ru((float)(__ldg(pnorm) * (double)__ldg(pscale)), 1.02f), __fmul_ru(2.f, e0x2));
+    int as = 0;
+    uint32_t aph = 0;
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + u * BN;
+    constexpr int NCH = BN / 32;  // chunks per item tile (2 or 4)
+    uint32_t hA[64], hB[64];
+    for (int gr = blockIdx.x; gr < num_groups; gr += gridDim.x) {
+      const int64_t row = (int64_t)(gr * UT + u) * kBM + q * 32 + lane;
+      QRow me = qrow_init(row < n, smax);  // dead rows (user >= n) have theta = +inf and never pass
+      float En[NCH];                       // error bounds of the next tile's chunks (prefetched)
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) En[c] = (32 * c < mi) ? __ldg(perr + 32 * c) : 0.f;
+      mbar_wait(BAR(ACC_FULL + as), aph);
+      tc_fence_after();
+      tmem_ld64(tq + as * C::ACC_COLS, hA);
+      tmem_ld_wait64(hA);
+      for (int it = 0; it < nit; ++it) {
+        const int base0 = it * BN;
+        float E[4];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          E[c] = En[c];
+          En[c] = (base0 + BN + 32 * c < mi) ? __ldg(perr + base0 + BN + 32 * c) : 0.f;
+        }
+        if (NCH == 2) E[2] = E[3] = 0.f;
+#ifdef RMIPS_EPI_PROFILE
+        const long long t1 = clock64();
+        const int pb = it < 255 ? it : 255;
+#endif
+        const uint32_t tcur = tq + as * C::ACC_COLS;
+        if (BN == 128) tmem_ld64(tcur + 64, hB);  // second half of this tile
+        uint32_t bits = epiq_fast(hA, E[0], E[1], me.theta);
+        if (BN == 128) tmem_ld_wait64(hB);
+        const bool more = it + 1 < nit;
+        const int as_next = as + 1 == NACC ? 0 : as + 1;
+        const uint32_t aph_next = as + 1 == NACC ? aph ^ 1 : aph;
+        if (more) {                               // first half of the next tile
+          mbar_wait(BAR(ACC_FULL + as_next), aph_next);
+          tc_fence_after();
+          tmem_ld64(tq + as_next * C::ACC_COLS, hA);
+        }
+        if (BN == 128) bits |= epiq_fast(hB, E[2], E[3], me.theta) << 2;
+        if (bits) me = epiq_slow(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, sb, rr, e0x2, kmax);
+        tc_fence_before();                        // this stage is no longer read: release it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
+        as = as_next;
+        aph = aph_next;
+        if (more) tmem_ld_wait64(hA);
+#ifdef RMIPS_EPI_PROFILE
+        if (lane == 0) atomicAdd(&g_epi_prof[1][pb], (unsigned long long)(clock64() - t1));
+#endif
+      }
+      qrow_finish(me, sb, rr, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
+      __syncwarp();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ------------------------------------------------------------------------------ host side
+static int sm_count_q() {
+  static int c = 0;
+  if (!c) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return c;
+}
+
+template <int KB, int UT, int BN>
+static cudaError_t launch_tcq(const BuildCtx& c, cudaStream_t st) {
+  using C = Cfg<KB, UT, BN>;
+  rmips_index_s* x = c.idx;
+  CUtensorMap ta, tb;
+  if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM)) return cudaErrorNotSupported;
+  if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)x->m, (uint64_t)x->dpad, BN)) return cudaErrorNotSupported;
+  cudaError_t e = cudaFuncSetAttribute(k_build_tcq<KB, UT, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
+  if (e != cudaSuccess) return e;
+  const int groups = (int)(((x->n + kBM - 1) / kBM + UT - 1) / UT);
+  const int grid = groups < sm_count_q() ? groups : sm_count_q();
+  const int ksteps = (x->d + 15) / 16;  // K steps of 16 that touch real (non-padding) columns
+  k_build_tcq<KB, UT, BN><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tb, x->perr, x->pnorm, c.scale_dev, x->n, x->m,
+                                                             x->kmax, ksteps, c.cand, c.ccount, c.ovf_list,
+                                                             c.ovf_count);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// d_pad = 128..256 (the d <= 64 case is build_tc.cu's kernel).
+cudaError_t build_tcq(const BuildCtx& c, cudaStream_t st) {
+  if (c.idx->m > (int64_t)kQPosMask + 1) return cudaErrorNotSupported;  // packed positions are 20-bit
+  switch (c.idx->dpad) {
+    case 128: return launch_tcq<2, 1, 64>(c, st);
+    case 192: return launch_tcq<3, 1, 64>(c, st);
+    case 256: return launch_tcq<4, 1, 64>(c, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace rmips
+

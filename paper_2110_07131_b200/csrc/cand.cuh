@@ -7,9 +7,9 @@
 //   theta : a valid lower bound (scaled units) of the k_max-th largest TRUE score seen so far
 //           (at least k_max buffered entries have lo >= theta, and lo <= true score);
 //   vmax  : the largest lo in its buffer;
-//   a candidate buffer in shared memory, slot-major ([slot][128 rows]) so that every lane
-//   reads/writes its own row conflict-free, as two arrays: lo = s~ - E rounded down (fp32) and
-//   the item position (the refresh passes read only lo).
+//   a candidate buffer in shared memory, slot-major ([slot][128 rows], 8-byte entries
+//   {lo bits, item position}) so that every lane reads/writes its own row conflict-free;
+//   lo = s~ - E rounded down.
 // An item is appended iff s~ >= theta - E (it may still be in the final top-k_max).  When any
 // row of a warp may not have room for another 32-column chunk, the whole warp refreshes at
 // once, every thread on its own row:
@@ -35,15 +35,9 @@ constexpr int kCandSmemBytes = kCand * kCandRows * 8;
 // Shared-memory pointers.  Functions that are not inlined re-assert the state space
 // (__builtin_assume(__isShared(..))) so that they still compile to LDS/STS.
 struct CandSmem {
-  float* lo;        // [kCand][kCandRows] lower bounds
-  int* id;          // [kCand][kCandRows] item positions
-  __device__ __forceinline__ static CandSmem at(uint8_t* base) {
-    return CandSmem{reinterpret_cast<float*>(base), reinterpret_cast<int*>(base + kCand * kCandRows * 4)};
-  }
-  __device__ __forceinline__ void assume_shared() const {
-    __builtin_assume(__isShared(lo));
-    __builtin_assume(__isShared(id));
-  }
+  uint2* buf;       // [kCand][kCandRows] {lo bits, item position}
+  __device__ __forceinline__ static CandSmem at(uint8_t* base) { return CandSmem{reinterpret_cast<uint2*>(base)}; }
+  __device__ __forceinline__ void assume_shared() const { __builtin_assume(__isShared(buf)); }
 };
 
 struct CandRow {
@@ -65,8 +59,7 @@ static __device__ __noinline__ CandRow cand_refresh(CandRow me, CandSmem sm, int
   if (me.ovf) return me;
   const int cn = me.cnt;
   sm.assume_shared();
-  float* bl = sm.lo + rloc;
-  int* bi = sm.id + rloc;
+  uint2* b = sm.buf + rloc;
   const float th = me.theta;
   float nth = th;  // proposed new theta
   if (cn >= kmax) {
@@ -76,12 +69,12 @@ static __device__ __noinline__ CandRow cand_refresh(CandRow me, CandSmem sm, int
       float m0 = U, m1 = U, m2 = U, m3 = U;
       int i = 0;
       for (; i + 4 <= cn; i += 4) {
-        m0 = fminf(m0, bl[i * kCandRows]);
-        m1 = fminf(m1, bl[(i + 1) * kCandRows]);
-        m2 = fminf(m2, bl[(i + 2) * kCandRows]);
-        m3 = fminf(m3, bl[(i + 3) * kCandRows]);
+        m0 = fminf(m0, __uint_as_float(b[i * kCandRows].x));
+        m1 = fminf(m1, __uint_as_float(b[(i + 1) * kCandRows].x));
+        m2 = fminf(m2, __uint_as_float(b[(i + 2) * kCandRows].x));
+        m3 = fminf(m3, __uint_as_float(b[(i + 3) * kCandRows].x));
       }
-      for (; i < cn; ++i) m0 = fminf(m0, bl[i * kCandRows]);
+      for (; i < cn; ++i) m0 = fminf(m0, __uint_as_float(b[i * kCandRows].x));
       L = fminf(fminf(m0, m1), fminf(m2, m3));
     }
     // 4 quaternary passes (3 thresholds each, 256-way resolution of [L, U]); the counts are
@@ -96,12 +89,12 @@ static __device__ __noinline__ CandRow cand_refresh(CandRow me, CandSmem sm, int
       for (; i + 8 <= cn; i += 8) {
         float v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = bl[(i + u) * kCandRows];
+        for (int u = 0; u < 8; ++u) v[u] = __uint_as_float(b[(i + u) * kCandRows].x);
 #pragma unroll
         for (int u = 0; u < 8; ++u) a1[u & 3] += v[u] >= t1, a2[u & 3] += v[u] >= t2, a3[u & 3] += v[u] >= t3;
       }
       for (; i < cn; ++i) {
-        const float v0 = bl[i * kCandRows];
+        const float v0 = __uint_as_float(b[i * kCandRows].x);
         a1[0] += v0 >= t1, a2[0] += v0 >= t2, a3[0] += v0 >= t3;
       }
       const int c1 = (a1[0] + a1[1]) + (a1[2] + a1[3]), c2 = (a2[0] + a2[1]) + (a2[2] + a2[3]),
@@ -117,27 +110,25 @@ static __device__ __noinline__ CandRow cand_refresh(CandRow me, CandSmem sm, int
   const float keep = __fsub_rd(nth, e0x2);  // lo < keep  =>  lo + 2E < theta: cannot be top-k_max
   int wpos = 0, ge = 0, i = 0;
   for (; i + 8 <= cn; i += 8) {
-    float v[8];
-    int d8[8];
+    uint2 v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = bl[(i + u) * kCandRows], d8[u] = bi[(i + u) * kCandRows];
+    for (int u = 0; u < 8; ++u) v[u] = b[(i + u) * kCandRows];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      ge += v[u] >= nth;
-      if (v[u] >= keep) {  // wpos <= i + u: never overtakes an unread entry
-        bl[wpos * kCandRows] = v[u];
-        bi[wpos * kCandRows] = d8[u];
+      const float lo = __uint_as_float(v[u].x);
+      ge += lo >= nth;
+      if (lo >= keep) {  // wpos <= i + u: never overtakes an unread entry
+        b[wpos * kCandRows] = v[u];
         ++wpos;
       }
     }
   }
   for (; i < cn; ++i) {
-    const float v = bl[i * kCandRows];
-    const int dd = bi[i * kCandRows];
-    ge += v >= nth;
-    if (v >= keep) {
-      bl[wpos * kCandRows] = v;
-      bi[wpos * kCandRows] = dd;
+    const uint2 v = b[i * kCandRows];
+    const float lo = __uint_as_float(v.x);
+    ge += lo >= nth;
+    if (lo >= keep) {
+      b[wpos * kCandRows] = v;
       ++wpos;
     }
   }
@@ -159,8 +150,7 @@ __device__ __forceinline__ void cand_append_chunk(ScoreFn s_of, const float (&g4
                                                   CandRow& me, CandSmem sm, int rloc) {
   sm.assume_shared();
   const float thr = fmaxf(__fsub_rd(me.theta, E), -3.402823466e38f);  // padding (-inf) never passes
-  float* bl = sm.lo + rloc;
-  int* bi = sm.id + rloc;
+  uint2* b = sm.buf + rloc;
   int c = me.cnt;
   float vmax = me.vmax;
 #pragma unroll
@@ -170,32 +160,16 @@ __device__ __forceinline__ void cand_append_chunk(ScoreFn s_of, const float (&g4
       const float s0 = s_of(4 * g), s1 = s_of(4 * g + 1), s2 = s_of(4 * g + 2), s3 = s_of(4 * g + 3);
       const bool p0 = s0 >= thr, p1 = s1 >= thr, p2 = s2 >= thr, p3 = s3 >= thr;
       const int o1 = c + p0, o2 = o1 + p1, o3 = o2 + p2;
-      if (p0) bl[c * kCandRows] = __fsub_rd(s0, E), bi[c * kCandRows] = pos0 + 4 * g;
-      if (p1) bl[o1 * kCandRows] = __fsub_rd(s1, E), bi[o1 * kCandRows] = pos0 + 4 * g + 1;
-      if (p2) bl[o2 * kCandRows] = __fsub_rd(s2, E), bi[o2 * kCandRows] = pos0 + 4 * g + 2;
-      if (p3) bl[o3 * kCandRows] = __fsub_rd(s3, E), bi[o3 * kCandRows] = pos0 + 4 * g + 3;
+      if (p0) b[c * kCandRows] = make_uint2(__float_as_uint(__fsub_rd(s0, E)), (uint32_t)(pos0 + 4 * g));
+      if (p1) b[o1 * kCandRows] = make_uint2(__float_as_uint(__fsub_rd(s1, E)), (uint32_t)(pos0 + 4 * g + 1));
+      if (p2) b[o2 * kCandRows] = make_uint2(__float_as_uint(__fsub_rd(s2, E)), (uint32_t)(pos0 + 4 * g + 2));
+      if (p3) b[o3 * kCandRows] = make_uint2(__float_as_uint(__fsub_rd(s3, E)), (uint32_t)(pos0 + 4 * g + 3));
       c = o3 + p3;
       if (gp) vmax = fmaxf(vmax, __fsub_rd(g4[g], E));
     }
   }
   me.cnt = c;
   me.vmax = vmax;
-}
-
-// Append up to 4 entries of one group (values v[j] at positions pos + j, valid iff pos + j < mi);
-// slots from a prefix of predicates so the stores are independent.
-__device__ __forceinline__ void cand_append4(const float (&v)[4], float thr, float E, int pos, int mi, int& c,
-                                             CandSmem sm, int rloc) {
-  float* bl = sm.lo + rloc;
-  int* bi = sm.id + rloc;
-  const bool p0 = v[0] >= thr && pos < mi, p1 = v[1] >= thr && pos + 1 < mi, p2 = v[2] >= thr && pos + 2 < mi,
-             p3 = v[3] >= thr && pos + 3 < mi;
-  const int o1 = c + p0, o2 = o1 + p1, o3 = o2 + p2;
-  if (p0) bl[c * kCandRows] = __fsub_rd(v[0], E), bi[c * kCandRows] = pos;
-  if (p1) bl[o1 * kCandRows] = __fsub_rd(v[1], E), bi[o1 * kCandRows] = pos + 1;
-  if (p2) bl[o2 * kCandRows] = __fsub_rd(v[2], E), bi[o2 * kCandRows] = pos + 2;
-  if (p3) bl[o3 * kCandRows] = __fsub_rd(v[3], E), bi[o3 * kCandRows] = pos + 3;
-  c = o3 + p3;
 }
 
 // After a chunk: if any row of the warp may not have room for another chunk, refresh all.
@@ -230,8 +204,8 @@ __device__ __forceinline__ void cand_finish(CandRow& me, CandSmem sm, int rloc, 
       ovf_list[slot] = (int32_t)row;
     } else {
       ccount[row] = me.cnt;
-      const int* bi = sm.id + rloc;
-      for (int i = 0; i < me.cnt; ++i) cand[row * kCand + i] = bi[i * kCandRows];
+      const uint2* b = sm.buf + rloc;
+      for (int i = 0; i < me.cnt; ++i) cand[row * kCand + i] = (int32_t)b[i * kCandRows].y;
     }
   }
 }

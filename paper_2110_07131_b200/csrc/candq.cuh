@@ -1,0 +1,229 @@
+// candq.cuh -- per-user-row top-k_max CANDIDATE filter of the tensor-core build (k_build_tc):
+// the same invariant as cand.cuh (the SIMT build's filter), with 4-byte entries so that a CTA can
+// keep 256 rows (two user tiles, eight epilogue warps) or 128 rows next to d = 256 operand tiles.
+//
+// Alg. 1 lines 7-9: every user's k_max largest inner products over P.  Scores s~ are
+// reduced-precision (fp16 operands, fp32 accumulation) with a per-item error bound E
+// (common.cuh).  Each epilogue thread owns one user row and keeps
+//   theta : a valid lower bound of the k_max-th largest TRUE score seen so far;
+//   a slot-major shared-memory buffer of packed entries (q << 20) | position, where q is a
+//           12-bit QUANTISED LOWER BOUND of the item's score:
+//              deq(q) = base + q * w  (rounded down, w a power of two)  <=  lo = s~ - E  <=  s,
+//           and lo < deq(q) + w.  Quantising rounds down, so every dequantised value is still a
+//           lower bound.
+// An item is appended iff s~ >= theta - E; an entry is dropped only when its upper bound
+// (< deq(q) + w + 2 E0, E0 = the largest E) is below theta.  Every true top-k_max item has
+// s >= tau_kmax >= theta, so it is never rejected or dropped.
+// Refresh (when a row of the warp may not have room for another 32-column chunk): a quaternary
+// search over q (4 passes, integer compares on the packed words) for the largest qt with
+// #{q >= qt} >= k_max; theta <- max(theta, deq(qt)); then one compaction pass that drops
+// entries below base' = theta - 2 E0 - 2 w and re-quantises the survivors on [base', vmax]
+// (base' and w' change, the value each entry stands for only goes down).
+// Positions must be < 2^20 (m <= 1,048,576; larger item sets use the SIMT build).
+#pragma once
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace rmips {
+
+constexpr int kQSlots = 128;                       // entries per row
+constexpr int kQPosBits = 20;
+constexpr uint32_t kQPosMask = (1u << kQPosBits) - 1u;
+constexpr int kQMax = 4095;                        // 12-bit quantised bound
+
+struct QRow {
+  float theta;  // valid lower bound of the k_max-th largest true score (scaled units)
+  float base;   // quantisation origin
+  float w;      // quantum (power of two): (smax - base) / w <= 4095, so q never saturates
+  float inv;    // 1 / w (exact)
+  float smax;   // bound on every score: |s~| <= smax
+  float vmax;   // largest appended lower bound (unquantised)
+  int cnt;      // entries in the buffer
+  int ovf;      // overflowed: exact fallback
+};
+
+__device__ __forceinline__ float pow2_ceil(float x) {  // smallest power of two >= x (x > 0, finite)
+  int e;
+  const float f = frexpf(x, &e);  // x = f * 2^e, f in [0.5, 1)
+  return ldexpf(1.f, f == 0.5f ? e - 1 : e);
+}
+
+// Buffer of R rows: entry i of row r at buf[i * R + r].
+struct QBuf {
+  uint32_t* buf;
+  int R;
+  __device__ __forceinline__ void assume_shared() const { __builtin_assume(__isShared(buf)); }
+};
+
+// Quantised lower bound of x (base <= x <= smax): floor((x - base) / w) <= 4095.  The quantum
+// covers [base, smax], never only [base, vmax]: a saturated q would no longer bound lo from above
+// (lo < deq(q) + w), and the drop test relies on that.
+__device__ __forceinline__ uint32_t q_of(float x, const QRow& me) {
+  const float dd = __fsub_rd(x, me.base) * me.inv;  // exact power-of-two scaling of a rounded-down gap
+  return dd >= (float)kQMax ? (uint32_t)kQMax : (uint32_t)dd;
+}
+__device__ __forceinline__ float deq(uint32_t q, const QRow& me) { return __fadd_rd(me.base, (float)q * me.w); }
+
+// smax bounds |s~| for every item (scores are in [-smax, smax]).
+__device__ __forceinline__ QRow qrow_init(bool live, float smax) {
+  const float inf = __int_as_float(0x7f800000);
+  QRow r;
+  r.theta = live ? -inf : inf;
+  r.base = -smax;
+  r.w = pow2_ceil(fmaxf(2.f * smax, 1e-30f) / (float)kQMax);
+  r.inv = 1.f / r.w;
+  r.smax = smax;
+  r.vmax = -inf;
+  r.cnt = 0;
+  r.ovf = 0;
+  return r;
+}
+
+// Refresh of this thread's row (all 32 lanes of the warp call it together).  Not inlined: one
+// copy per kernel keeps the hot loops in the instruction cache.
+static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float e0x2, int kmax) {
+  if (me.ovf) return me;
+  sb.assume_shared();
+  uint32_t* b = sb.buf + rr;
+  const int R = sb.R;
+  const int cn = me.cnt;
+  const float th = me.theta;
+  float nth = th;
+  if (cn >= kmax) {
+    // #{q >= 0} = cn >= kmax; the search keeps #{q >= qL} >= kmax (verified counts only), so the
+    // resulting deq(qL) is a valid theta whatever the history of re-quantisation
+    int qL = 0;
+    int qU = (int)q_of(me.vmax, me) + 1;  // exclusive upper end
+#pragma unroll 1
+    for (int pass = 0; pass < 6 && qU - qL > 1; ++pass) {
+      const int span = qU - qL;
+      const uint32_t t1 = (uint32_t)(qL + (span >> 2)) << kQPosBits, t2 = (uint32_t)(qL + (span >> 1)) << kQPosBits,
+                     t3 = (uint32_t)(qL + ((3 * span) >> 2)) << kQPosBits;
+      int a1[4] = {0, 0, 0, 0}, a2[4] = {0, 0, 0, 0}, a3[4] = {0, 0, 0, 0};
+      int i = 0;
+      for (; i + 8 <= cn; i += 8) {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = b[(i + u) * R];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a1[u & 3] += v[u] >= t1, a2[u & 3] += v[u] >= t2, a3[u & 3] += v[u] >= t3;
+      }
+      for (; i < cn; ++i) {
+        const uint32_t v0 = b[i * R];
+        a1[0] += v0 >= t1, a2[0] += v0 >= t2, a3[0] += v0 >= t3;
+      }
+      const int c1 = (a1[0] + a1[1]) + (a1[2] + a1[3]), c2 = (a2[0] + a2[1]) + (a2[2] + a2[3]),
+                c3 = (a3[0] + a3[1]) + (a3[2] + a3[3]);
+      const int m1 = qL + (span >> 2), m2 = qL + (span >> 1), m3 = qL + ((3 * span) >> 2);
+      if (c3 >= kmax) qL = m3;
+      else if (c2 >= kmax) qL = m2, qU = m3;
+      else if (c1 >= kmax) qL = m1, qU = m2;
+      else qU = m1;
+    }
+    nth = fmaxf(th, deq((uint32_t)qL, me));
+  }
+  // re-quantise the survivors on [base', vmax], base' = theta - 2 E0 - 2 w: an entry's true lower
+  // bound lo is < deq(q) + w, so x = deq(q) < base' implies lo + 2 E < theta (droppable), and every
+  // kept entry is representable (x >= base') with its new value <= x <= lo
+  QRow nw = me;
+  nw.theta = nth;
+  if (nth > -3.402823466e38f) {
+    nw.base = __fsub_rd(__fsub_rd(nth, e0x2), __fmul_ru(2.f, me.w));
+    const float span = __fsub_ru(me.smax, nw.base);
+    nw.w = pow2_ceil(fmaxf(span, fabsf(nw.base) * 1e-6f + 1e-30f) / (float)kQMax);
+    nw.inv = 1.f / nw.w;
+  }
+  const bool rebase = nth > -3.402823466e38f;
+  int wpos = 0, ge = 0, i = 0;
+  for (; i + 8 <= cn; i += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = b[(i + u) * R];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float x = deq(v[u] >> kQPosBits, me);
+      ge += x >= nth;
+      if (!rebase || x >= nw.base) {  // x < base' = theta - 2 E0: upper bound below theta
+        b[wpos * R] = rebase ? ((q_of(x, nw) << kQPosBits) | (v[u] & kQPosMask)) : v[u];
+        ++wpos;
+      }
+    }
+  }
+  for (; i < cn; ++i) {
+    const uint32_t v0 = b[i * R];
+    const float x = deq(v0 >> kQPosBits, me);
+    ge += x >= nth;
+    if (!rebase || x >= nw.base) {
+      b[wpos * R] = rebase ? ((q_of(x, nw) << kQPosBits) | (v0 & kQPosMask)) : v0;
+      ++wpos;
+    }
+  }
+  nw.cnt = wpos;
+  if (wpos > kQSlots - 32 || (nth > th && ge < kmax)) {  // no room / unverified theta: exact fallback
+    nw.ovf = 1;
+    nw.theta = __int_as_float(0x7f800000);
+  }
+  return nw;
+}
+
+// Append pass of one 32-column chunk (scores via s_of(j), positions pos0 + j; columns >= mi are
+// padding), called by the whole warp; g4[8] are the 4-column group maxima.  Groups are skipped
+// warp-uniformly; inside a group the 4 slots come from a prefix of predicates.
+template <typename ScoreFn>
+__device__ __forceinline__ void qrow_append_chunk(ScoreFn s_of, const float (&g4)[8], float E, int pos0, int mi,
+                                                  QRow& me, QBuf sb, int rr) {
+  sb.assume_shared();
+  uint32_t* b = sb.buf + rr;
+  const int R = sb.R;
+  // padding (-inf) never passes; after the first refresh, lo >= base is implied by s~ >= thr
+  const float thr = fmaxf(__fsub_rd(me.theta, E), -3.402823466e38f);
+  int c = me.cnt;
+  float vmax = me.vmax;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    const bool gp = g4[g] >= thr;
+    if (__any_sync(0xffffffffu, gp)) {
+      float lo[4];
+      bool p[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float sj = s_of(4 * g + j);
+        lo[j] = __fsub_rd(sj, E);
+        p[j] = sj >= thr && pos0 + 4 * g + j < mi && lo[j] >= me.base;
+      }
+      const int o1 = c + p[0], o2 = o1 + p[1], o3 = o2 + p[2];
+      if (p[0]) b[c * R] = (q_of(lo[0], me) << kQPosBits) | (uint32_t)(pos0 + 4 * g);
+      if (p[1]) b[o1 * R] = (q_of(lo[1], me) << kQPosBits) | (uint32_t)(pos0 + 4 * g + 1);
+      if (p[2]) b[o2 * R] = (q_of(lo[2], me) << kQPosBits) | (uint32_t)(pos0 + 4 * g + 2);
+      if (p[3]) b[o3 * R] = (q_of(lo[3], me) << kQPosBits) | (uint32_t)(pos0 + 4 * g + 3);
+      c = o3 + p[3];
+      if (p[0] | p[1] | p[2] | p[3]) vmax = fmaxf(vmax, __fsub_rd(g4[g], E));
+    }
+  }
+  me.cnt = c;
+  me.vmax = vmax;
+}
+
+__device__ __forceinline__ void qrow_maybe_refresh(QRow& me, QBuf sb, int rr, float e0x2, int kmax) {
+  if (__any_sync(0xffffffffu, me.cnt > kQSlots - 32)) me = qrow_refresh(me, sb, rr, e0x2, kmax);
+}
+
+// Final compaction, then the candidate positions (or the overflow mark) are written out.
+__device__ __forceinline__ void qrow_finish(QRow& me, QBuf sb, int rr, float e0x2, int kmax, int64_t row, int64_t n,
+                                            int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
+                                            int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
+  me = qrow_refresh(me, sb, rr, e0x2, kmax);
+  if (row < n) {
+    if (me.ovf) {
+      ccount[row] = -1;
+      const int slot = atomicAdd(ovf_count, 1);
+      ovf_list[slot] = (int32_t)row;
+    } else {
+      ccount[row] = me.cnt;
+      const uint32_t* b = sb.buf + rr;
+      for (int i = 0; i < me.cnt; ++i) cand[row * kCand + i] = (int32_t)(b[i * sb.R] & kQPosMask);
+    }
+  }
+}
+
+}  // namespace rmips

@@ -38,6 +38,7 @@ size_t build_cub_bytes(int64_t n, int64_t m);
 cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t st);
 cudaError_t build_simt(const BuildCtx& c, cudaStream_t st);
 cudaError_t build_tc(const BuildCtx& c, cudaStream_t st);  // build_tc.cu; cudaErrorNotSupported if unusable
+cudaError_t build_tcq(const BuildCtx& c, cudaStream_t st);  // build_tcq.cu (d_pad 128..256)
 cudaError_t build_select(BuildCtx& c, cudaStream_t st);
 cudaError_t build_fallback(BuildCtx& c, int nrows, double* scratch, int grid, cudaStream_t st);
 cudaError_t build_blocks(BuildCtx& c, cudaStream_t st);
