@@ -180,10 +180,8 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
     x->ids = dalloc<int32_t>((int64_t)k_max * n, st);
     x->thr = dalloc<float>((int64_t)k_max * n, st);
     x->tb = dalloc<float>((int64_t)k_max * x->nblocks, st);
-    c.norm_u_raw = dalloc<double>(n, st);
-    c.norm_p_raw = dalloc<double>(m, st);
-    c.iota_u = dalloc<int32_t>(n, st);
-    c.iota_p = dalloc<int32_t>(m, st);
+    c.nkey = dalloc<uint64_t>(2 * (m + n), st);
+    c.nval = dalloc<int32_t>(2 * (m + n), st);
     c.maxabs = dalloc<unsigned int>(4, st);
     c.scale_dev = reinterpret_cast<float*>(c.maxabs + 2);
     c.cub_bytes = build_cub_bytes(n, m);
@@ -227,7 +225,7 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
     CK(cudaMemcpyAsync(hp + 1, c.ovf_count, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hp + 2, c.scale_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hp + 4, c.cand_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    dfree(c.norm_u_raw, st); dfree(c.norm_p_raw, st); dfree(c.iota_u, st); dfree(c.iota_p, st);
+    dfree(c.nkey, st); dfree(c.nval, st);
     dfree(c.maxabs, st); dfree(c.cand, st); dfree(c.ccount, st); dfree(c.ovf_list, st);
     dfree(c.ovf_count, st); dfree(c.cand_total, st); dfree(scratch, st);
     if (c.cub_tmp) cudaFreeAsync(c.cub_tmp, st);

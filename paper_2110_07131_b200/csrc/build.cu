@@ -1,7 +1,8 @@
 // build.cu -- index build (Alg. 1, with L_i over ALL of P per BASELINE north star).
 //
 //   B1 k_norms          norms (Alg. 1 lines 1-4) + finite check + max |p_j|
-//   B2 cub radix sort   norm sort, descending, ties by ascending id (line 5; reading R6)
+//   B2 cub radix sort   one norm sort of [items | users], descending, ties by ascending id (line 5,
+//                       P:279; reading R6), split into the two permutations
 //   B3 k_prep_*         permute; fp16 filter operands (u/nu, p*2^e); fp32 exact copies
 //   B4 k_build_simt     SIMT contraction + candidate epilogue (the tcgen05 version is build_tc.cu)
 //   B5 k_exact_select   fp64 re-evaluation of the candidates, exact top-k_max (lines 7-9)
@@ -16,8 +17,9 @@
 namespace rmips {
 
 // ------------------------------------------------------------------------------ B1
-__global__ void k_norms(const float* __restrict__ X, int64_t rows, int d, double* __restrict__ norms,
-                        int* __restrict__ flags, unsigned int* __restrict__ maxabs_bits) {
+// keys[r] = bits of the fp64 norm (non-negative, so its bits order like the value) | topbit.
+__global__ void k_norms(const float* __restrict__ X, int64_t rows, int d, uint64_t* __restrict__ keys,
+                        uint64_t topbit, int* __restrict__ flags, unsigned int* __restrict__ maxabs_bits) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   float mx = 0.f;
   if (r < rows) {
@@ -30,7 +32,7 @@ __global__ void k_norms(const float* __restrict__ X, int64_t rows, int d, double
       mx = fmaxf(mx, fabsf(v));
       s = __fma_rn((double)v, (double)v, s);
     }
-    norms[r] = sqrt(s);
+    keys[r] = (uint64_t)__double_as_longlong(sqrt(s)) | topbit;
     if (!fin) atomicOr(flags, kFlagNonfinite);
   }
   if (maxabs_bits) {
@@ -42,6 +44,17 @@ __global__ void k_norms(const float* __restrict__ X, int64_t rows, int d, double
 __global__ void k_iota(int32_t* v, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) v[i] = (int32_t)i;
+}
+
+// Split the one sorted [items | users] sequence into the two norm-sorted permutations.
+__global__ void k_split_sorted(const uint64_t* __restrict__ keys, const int32_t* __restrict__ vals, int64_t m,
+                               int64_t n, double* __restrict__ pnorm, int32_t* __restrict__ perm_p,
+                               double* __restrict__ unorm, int32_t* __restrict__ perm_u) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= m + n) return;
+  const double v = __longlong_as_double((long long)(keys[r] & 0x7fffffffffffffffull));
+  if (r < m) pnorm[r] = v, perm_p[r] = vals[r];
+  else unorm[r - m] = v, perm_u[r - m] = vals[r] - (int32_t)m;
 }
 
 // ------------------------------------------------------------------------------ B3
@@ -399,25 +412,23 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
   rmips_index_s* x = c.idx;
   const int64_t n = x->n, m = x->m;
   const int d = x->d, dpad = x->dpad;
-  // B1
-  if (n) k_norms<<<nblk(n, 256), 256, 0, st>>>(Q, n, d, c.norm_u_raw, x->d_flags, nullptr); count_launch();
-  k_norms<<<nblk(m, 256), 256, 0, st>>>(P, m, d, c.norm_p_raw, x->d_flags, c.maxabs); count_launch();
-  // B2
-  if (n) k_iota<<<nblk(n, 256), 256, 0, st>>>(c.iota_u, n); count_launch();
-  k_iota<<<nblk(m, 256), 256, 0, st>>>(c.iota_p, m); count_launch();
+  // B1: norms as sort keys of one concatenated [items | users] sequence (items carry the top
+  // bit, so a descending sort puts them first); non-finite check; max |p_j|
+  const int64_t tot = m + n;
+  uint64_t* kin = c.nkey;
+  uint64_t* kout = c.nkey + tot;
+  int32_t* vin = c.nval;
+  int32_t* vout = c.nval + tot;
+  k_norms<<<nblk(m, 256), 256, 0, st>>>(P, m, d, kin, 1ull << 63, x->d_flags, c.maxabs); count_launch();
+  if (n) k_norms<<<nblk(n, 256), 256, 0, st>>>(Q, n, d, kin + m, 0ull, x->d_flags, nullptr); count_launch();
+  // B2: one stable radix sort (descending norm, ties by ascending index: reading R6)
+  k_iota<<<nblk(tot, 256), 256, 0, st>>>(vin, tot); count_launch();
   size_t tb = c.cub_bytes;
-  cudaError_t e;
-  if (n) {
-    e = cub::DeviceRadixSort::SortPairsDescending(c.cub_tmp, tb, c.norm_u_raw, x->unorm, c.iota_u, x->perm_u,
-                                                  (int)n, 0, 64, st);
-    count_launch(kCubSortKernels);
-    if (e != cudaSuccess) return e;
-  }
-  tb = c.cub_bytes;
-  e = cub::DeviceRadixSort::SortPairsDescending(c.cub_tmp, tb, c.norm_p_raw, x->pnorm, c.iota_p, x->perm_p,
-                                                (int)m, 0, 64, st);
-    count_launch(kCubSortKernels);
+  cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(c.cub_tmp, tb, kin, kout, vin, vout, (int)tot, 0, 64, st);
+  count_launch(kCubSortKernels);
   if (e != cudaSuccess) return e;
+  k_split_sorted<<<nblk(tot, 256), 256, 0, st>>>(kout, vout, m, n, x->pnorm, x->perm_p, x->unorm, x->perm_u);
+  count_launch();
   // B3
   if (n)
     k_prep_users<<<nblk(n * dpad, 256), 256, 0, st>>>(Q, n, d, dpad, x->perm_u, x->unorm, x->U16, x->U32, x->unu); count_launch();
@@ -427,11 +438,9 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
 }
 
 size_t build_cub_bytes(int64_t n, int64_t m) {
-  size_t a = 0, b = 0;
-  int64_t mx = n > m ? n : m;
-  cub::DeviceRadixSort::SortPairsDescending((void*)nullptr, a, (const double*)nullptr, (double*)nullptr,
-                                            (const int32_t*)nullptr, (int32_t*)nullptr, (int)mx, 0, 64);
-  (void)b;
+  size_t a = 0;
+  cub::DeviceRadixSort::SortPairsDescending((void*)nullptr, a, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                            (const int32_t*)nullptr, (int32_t*)nullptr, (int)(n + m), 0, 64);
   return a;
 }
 

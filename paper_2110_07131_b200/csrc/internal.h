@@ -19,10 +19,8 @@ inline void count_launch(int k = 1) { g_launches.fetch_add(k, std::memory_order_
 // Scratch of one build call (owned by abi.cu, freed before rmips_build_index returns).
 struct BuildCtx {
   rmips_index_s* idx = nullptr;
-  double* norm_u_raw = nullptr;   // [n] norms in original order
-  double* norm_p_raw = nullptr;   // [m]
-  int32_t* iota_u = nullptr;      // [n]
-  int32_t* iota_p = nullptr;      // [m]
+  uint64_t* nkey = nullptr;       // [2][m + n] sort keys in/out: fp64 norm bits, top bit set for items
+  int32_t* nval = nullptr;        // [2][m + n] sort values in/out: concatenated index (items first)
   unsigned int* maxabs = nullptr; // max |p_j| bits
   float* scale_dev = nullptr;     // 2^e
   void* cub_tmp = nullptr;
@@ -61,7 +59,7 @@ struct QueryCtx {
   uint64_t* acc = nullptr;       // accepted keys (q_input << 32 | original user id)
   uint64_t* und = nullptr;       // undecided (q_input << 32 | sorted user position)
   int64_t cap = 0;               // capacity of acc and of und
-  uint64_t* acc_sorted = nullptr;
+  uint64_t* acc_sorted = nullptr;  // (also holds the 32-bit packed keys of the fast output path)
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   int* flags_dev = nullptr;

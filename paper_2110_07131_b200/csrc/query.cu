@@ -337,16 +337,58 @@ cudaError_t query_exact(QueryCtx& c, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Fast output path when b * n < 2^32: accepted (q, user) pairs packed as one 32-bit key q * n + u,
+// so the radix sort needs ceil(log2(b n)) bits (4 passes) instead of 64.
+__global__ void k_pack32(const uint64_t* __restrict__ acc, int64_t total, uint32_t n, uint32_t* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < total) {
+    const uint64_t r = acc[i];
+    out[i] = (uint32_t)(r >> 32) * n + (uint32_t)(r & 0xffffffffu);
+  }
+}
+__global__ void k_offsets32(const uint32_t* __restrict__ keys, int64_t total, int b, uint32_t n,
+                            int64_t* __restrict__ offsets) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > b) return;
+  const uint64_t target = (uint64_t)i * n;
+  int64_t lo = 0, hi = total;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if ((uint64_t)keys[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  offsets[i] = lo;
+}
+__global__ void k_copy_ids32(const uint32_t* __restrict__ keys, int64_t total, uint32_t n, int32_t* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < total) out[i] = (int32_t)(keys[i] % n);
+}
+
+static bool use_keys32(const QueryCtx& c) { return c.idx->n > 0 && (uint64_t)c.b * (uint64_t)c.idx->n < (1ull << 32); }
+
 size_t query_cub_bytes(int64_t cap) {
-  size_t a = 0;
+  size_t a = 0, b = 0;
   cub::DeviceRadixSort::SortKeys((void*)nullptr, a, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int)cap, 0, 64);
-  return a;
+  cub::DeviceRadixSort::SortKeys((void*)nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)cap, 0, 32);
+  return a > b ? a : b;
 }
 
 // total = number of accepted keys (host-known after the mid-call sync).
 cudaError_t query_sort(QueryCtx& c, int64_t total, int end_bit, cudaStream_t st) {
   size_t tb = c.cub_bytes;
   if (total == 0) return cudaSuccess;
+  if (use_keys32(c)) {
+    // packed keys in the first half of acc_sorted's space, sorted into the second half (both fit: the
+    // workspace holds cap 8-byte records)
+    uint32_t* kin = reinterpret_cast<uint32_t*>(c.acc_sorted);
+    uint32_t* kout = kin + total;
+    k_pack32<<<nblk(total, 256), 256, 0, st>>>(c.acc, total, (uint32_t)c.idx->n, kin);
+    count_launch();
+    const uint64_t span = (uint64_t)c.b * (uint64_t)c.idx->n;
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) < span) ++bits;
+    count_launch(kCubSortKernels);
+    return cub::DeviceRadixSort::SortKeys(c.cub_tmp, tb, kin, kout, (int)total, 0, bits, st);
+  }
   count_launch(kCubSortKernels);
   return cub::DeviceRadixSort::SortKeys(c.cub_tmp, tb, c.acc, c.acc_sorted, (int)total, 0, end_bit, st);
 }
@@ -354,6 +396,16 @@ cudaError_t query_sort(QueryCtx& c, int64_t total, int end_bit, cudaStream_t st)
 cudaError_t query_output(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st) {
   // offsets from the sorted keys; ids copied only if they fit
   const int64_t total = c.idx->stats.result_total;
+  if (use_keys32(c)) {
+    const uint32_t* keys = reinterpret_cast<const uint32_t*>(c.acc_sorted) + total;
+    const uint32_t n32 = (uint32_t)c.idx->n;
+    k_offsets32<<<nblk(c.b + 1, 256), 256, 0, st>>>(keys, total, c.b, n32, offsets); count_launch();
+    if (total <= capacity && total > 0) {
+      k_copy_ids32<<<nblk(total, 256), 256, 0, st>>>(keys, total, n32, user_ids);
+      count_launch();
+    }
+    return cudaGetLastError();
+  }
   k_offsets<<<nblk(c.b + 1, 256), 256, 0, st>>>(c.acc_sorted, total, c.b, offsets); count_launch();
   if (total <= capacity && total > 0) k_copy_ids<<<nblk(total, 256), 256, 0, st>>>(c.acc_sorted, total, user_ids); count_launch();
   return cudaGetLastError();
