@@ -6,7 +6,7 @@
 // users).  One persistent CTA per SM walks the work items, 6 warps:
 //   warp 0      TMA producer: the sub-batch's queries Q16 (256 x 64 fp16 per K block, kept in
 //               shared memory while the CTA stays on that sub-batch) and the stream of user tiles
-//               (128 x 64 fp16 per K block) through a kStages-deep ring (SWIZZLE_128B)
+//               through a ring of K-block units (128 x 64 fp16 each, SWIZZLE_128B); d_pad <= 256
 //   warp 1      TMEM allocator + MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M = 128 users,
 //               N = the Lemma 3 prefix of the sub-batch rounded up to 16 (<= 256 queries),
 //               K = 16 x 4 per K block, fp32 accumulators in TMEM, 2 stages x 256 columns
@@ -28,17 +28,19 @@ namespace rmips {
 namespace {
 
 constexpr int kBM = 128;                  // users per tile (TMEM lanes)
-constexpr int kStages = 4;                // user-tile ring depth
-constexpr int kUTileBytes = kBM * 64 * 2; // 128 x 64 fp16 = 16 KB
+constexpr int kUTileBytes = kBM * 64 * 2; // one K block of a user tile: 128 x 64 fp16 = 16 KB
 constexpr int kQTileBytes = kQB * 64 * 2; // 256 x 64 fp16 = 32 KB
 constexpr int kThreads = 192;
 constexpr int kAccCols = 256;             // TMEM columns per accumulator stage
 constexpr int kAcc = 2;
 
+// The user stream is a ring of K-block units (16 KB each): a user tile of d_pad = 64*KB columns
+// takes KB consecutive units, and the MMA on K block kb starts as soon as that unit has landed.
 struct QSmem {
+  static constexpr int NU(int KB) { return KB == 1 ? 4 : 6; }  // ring units
   static constexpr int Q = 0;
   static constexpr int A(int KB) { return KB * kQTileBytes; }
-  static constexpr int BAR(int KB) { return A(KB) + kStages * KB * kUTileBytes; }
+  static constexpr int BAR(int KB) { return A(KB) + NU(KB) * kUTileBytes; }
   static constexpr int TOTAL(int KB) { return BAR(KB) + 256 + 1024; }
 };
 
@@ -131,9 +133,10 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
            const float* __restrict__ thrk, const float* __restrict__ tbk, const int32_t* __restrict__ perm_u,
            int64_t n, int nblocks, const float* __restrict__ qn, const float* __restrict__ qerr,
            const float* __restrict__ qscale, const int32_t* __restrict__ qperm, const int32_t* __restrict__ qcount,
-           int nsub, int flags, unsigned long long* __restrict__ ctr, uint64_t* __restrict__ acc_list,
+           int nsub, int flags, int ksteps, unsigned long long* __restrict__ ctr, uint64_t* __restrict__ acc_list,
            uint64_t* __restrict__ und_list, int64_t cap) {
   using namespace sm100;
+  constexpr int kStages = QSmem::NU(KB);  // ring units
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -197,11 +200,12 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
           ++nq;
           cur_s = s;
         }
-        mbar_wait_sleep(BAR(A_EMPTY + stage), ph ^ 1);
-        mbar_arrive_expect_tx(BAR(A_FULL + stage), KB * kUTileBytes);
-        for (int kb = 0; kb < KB; ++kb)
-          tma_load_2d(sA + (stage * KB + kb) * kUTileBytes, &tmU, kb * 64, t * kBM, BAR(A_FULL + stage));
-        if (++stage == kStages) stage = 0, ph ^= 1;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait_sleep(BAR(A_EMPTY + stage), ph ^ 1);
+          mbar_arrive_expect_tx(BAR(A_FULL + stage), kUTileBytes);
+          tma_load_2d(sA + stage * kUTileBytes, &tmU, kb * 64, t * kBM, BAR(A_FULL + stage));
+          if (++stage == kStages) stage = 0, ph ^= 1;
+        }
       }
       atomicAdd(ctr + C_BLOCK_PAIRS, pairs);
       atomicAdd(ctr + C_BLOCK_PRUNED, pruned);
@@ -222,22 +226,21 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
           cur_s = s;
         }
         mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
-        mbar_wait_sleep(BAR(A_FULL + stage), ph);
-        tc_fence_after();
         const int N = (len + 15) & ~15;
         const uint32_t idesc = idesc_f16_f32(kBM, N);
         const uint32_t d = tmem + as * kAccCols;
-#pragma unroll
         for (int kb = 0; kb < KB; ++kb) {
-          const uint32_t a0 = sA + (stage * KB + kb) * kUTileBytes;
+          mbar_wait_sleep(BAR(A_FULL + stage), ph);
+          tc_fence_after();
+          const uint32_t a0 = sA + stage * kUTileBytes;
           const uint32_t b0 = sQ + kb * kQTileBytes;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
+          const int kk_end = min(4, ksteps - 4 * kb);  // zero-padding K steps are skipped
+          for (int kk = 0; kk < kk_end; ++kk)
             mma_f16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
+          mma_commit(BAR(A_EMPTY + stage));
+          if (++stage == kStages) stage = 0, ph ^= 1;
         }
-        mma_commit(BAR(A_EMPTY + stage));
         mma_commit(BAR(ACC_FULL + as));
-        if (++stage == kStages) stage = 0, ph ^= 1;
         if (++as == kAcc) as = 0, aph ^= 1;
       }
     }
@@ -355,7 +358,7 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
   k_query_tc<KB><<<grid, kThreads, smem, st>>>(tu, tq, x->thr + (int64_t)(c.k - 1) * x->n,
                                                x->tb + (int64_t)(c.k - 1) * x->nblocks, x->perm_u, x->n,
                                                (int)x->nblocks, c.qn, c.qerr, c.qscale, c.qperm, c.qcount, c.nsub,
-                                               c.flags, c.counters, c.acc, c.und, c.cap);
+                                               c.flags, (x->d + 15) / 16, c.counters, c.acc, c.und, c.cap);
   count_launch();
   return cudaGetLastError();
 }
@@ -365,7 +368,10 @@ cudaError_t query_filter_tc(QueryCtx& c, cudaStream_t st) {
   if (c.idx->n == 0) return cudaSuccess;
   switch (c.idx->dpad) {
     case 64: return launch_query_tc<1>(c, st);
-    default: return cudaErrorNotSupported;  // d > 64: SIMT filter
+    case 128: return launch_query_tc<2>(c, st);
+    case 192: return launch_query_tc<3>(c, st);
+    case 256: return launch_query_tc<4>(c, st);
+    default: return cudaErrorNotSupported;
   }
 }
 

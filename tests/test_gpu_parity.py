@@ -277,6 +277,7 @@ def _sampled_full_config(cfg, n_sample, batch=None, query_stride=1):
     spec = w.spec
     idx = rmips.rmips_build_index(_t(w.U), _t(w.P), spec.k_max)
     assert idx.overflow_rows == 0
+    assert idx.build_flags & rmips.RMIPS_BUILD_SIMT == 0  # the tcgen05 build ran
     rng = np.random.default_rng(cfg)
     sample = np.sort(rng.choice(spec.n, n_sample, replace=False))
     vals, oids = oracle.topk(w.U[sample], w.P, spec.k_max)
@@ -289,6 +290,7 @@ def _sampled_full_config(cfg, n_sample, batch=None, query_stride=1):
         sets = []
         for b0 in range(0, Qy.shape[0], bs):
             off, ids = rmips.rmips_query(idx, _t(Qy[b0:b0 + bs]), k)
+            assert idx.stats()["filter_kernel"] == 1  # the tcgen05 filter ran
             sets += rmips.split_sets(off, ids)
         assert all((np.diff(s_) > 0).all() for s_ in sets)
         member = oracle.rkmips_twophase(w.U[sample], vals, Qy, k)
