@@ -115,8 +115,9 @@ __device__ __noinline__ CandRow epi_slow(uint32_t bits, uint32_t taddr, int base
 template <int KB>
 __global__ void __launch_bounds__(kThreads, 1)
 k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const float* __restrict__ perr, int64_t n, int64_t m, int kmax, int32_t* __restrict__ cand,
-           int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
+           const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
+           int64_t n, int64_t m, int kmax, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
+           int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
   using namespace sm100;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base, derived from smem_raw by pointer arithmetic so that the compiler
@@ -133,6 +134,13 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
   const int A_FULL = 0, A_EMPTY = 1, B_FULL = 2, B_EMPTY = 2 + kStages, ACC_FULL = 2 + 2 * kStages,
             ACC_EMPTY = 2 + 2 * kStages + kAcc;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 + 2 * kStages + 2 * kAcc);
+  // early-termination control words (Cauchy-Schwarz on the norm-sorted items, see below):
+  //   done_cum   epilogue warps that finished (or gave up) a user tile, cumulative (4 per tile)
+  //   stage_end  producer -> MMA: "user tile t ends here" marker (t + 1) per smem stage
+  //   acc_end    MMA -> epilogue: the same marker per accumulator stage
+  volatile int* done_cum = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  volatile int* stage_end = done_cum + 1;
+  volatile int* acc_end = stage_end + kStages;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_utiles = (int)((n + kBM - 1) / kBM);
@@ -145,6 +153,9 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     mbar_init(BAR(A_EMPTY), 1);
     for (int s = 0; s < kStages; ++s) mbar_init(BAR(B_FULL + s), 1), mbar_init(BAR(B_EMPTY + s), 1);
     for (int a = 0; a < kAcc; ++a) mbar_init(BAR(ACC_FULL + a), 1), mbar_init(BAR(ACC_EMPTY + a), 4);
+    *done_cum = 0;
+    for (int s = 0; s < kStages; ++s) stage_end[s] = 0;
+    for (int a = 0; a < kAcc; ++a) acc_end[a] = 0;
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -168,6 +179,12 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         for (int kb = 0; kb < KB; ++kb) tma_load_2d(sA + kb * kTileBytes, &tmA, kb * 64, ut * kBM, BAR(A_FULL));
         for (int it = 0; it < nit; ++it) {
           mbar_wait_sleep(BAR(B_EMPTY + stage), ph ^ 1);
+          if (*done_cum >= 4 * (t + 1)) {  // every epilogue warp is done with this user tile
+            stage_end[stage] = t + 1;
+            mbar_arrive(BAR(B_FULL + stage));  // release: the marker is visible to the MMA warp
+            if (++stage == kStages) stage = 0, ph ^= 1;
+            break;
+          }
           mbar_arrive_expect_tx(BAR(B_FULL + stage), KB * kTileBytes);
           for (int kb = 0; kb < KB; ++kb)
             tma_load_2d(sB + (stage * KB + kb) * kTileBytes, &tmB, kb * 64, it * kBN, BAR(B_FULL + stage));
@@ -189,6 +206,14 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
           mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
           mbar_wait_sleep(BAR(B_FULL + stage), ph);
           tc_fence_after();
+          if (stage_end[stage] == t + 1) {  // the producer ended this user tile: forward the marker
+            mbar_arrive(BAR(B_EMPTY + stage));
+            acc_end[as] = t + 1;
+            mbar_arrive(BAR(ACC_FULL + as));
+            if (++stage == kStages) stage = 0, ph ^= 1;
+            if (++as == kAcc) as = 0, aph ^= 1;
+            break;
+          }
           const uint32_t d = tmem + as * kBN;
 #pragma unroll
           for (int kb = 0; kb < KB; ++kb) {
@@ -211,25 +236,40 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     // Half tiles (64 columns) are software-pipelined: the TMEM load of the next half (of this
     // tile or the next one) is in flight while the current half is filtered.  Chunks in which a
     // lane may append are re-read from TMEM by epi_slow before the stage is released.
+    // Early termination (Cauchy-Schwarz, cf. Lemma 3 / Cor. 1 of the paper, applied to the build):
+    // items are norm-sorted, so once |p_first(next tile)| 2^e (1 + 2^-16) -- an upper bound of
+    // every later scaled true score u.p / nu -- is below the smallest theta of the warp's rows,
+    // no later item can enter any of its top-k_max lists.  The warp then stops reading TMEM and
+    // reports to the producer; when all 4 warps are done the producer ends the user tile and the
+    // end marker travels producer -> MMA -> epilogue with the stage barriers.
     const int q = warp & 3;                    // TMEM lane quadrant of this warp
     const int rloc = q * 32 + lane;            // row within the tile
     const int mi = (int)m;
     const float e0x2 = cand_e0x2(perr);
+    const float pscl = pscale ? __ldg(pscale) : __int_as_float(0x7f800000);  // NULL: no early termination
     int as = 0;
     uint32_t aph = 0;
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
     uint32_t hA[64], hB[64];
-    for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x) {
+    int t = 0;
+    for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
       const int64_t row = (int64_t)ut * kBM + rloc;
       CandRow me = cand_init(row < n);  // dead rows (user >= n) have theta = +inf and never pass
       float En[4];                      // error bounds of the next tile's chunks (prefetched)
 #pragma unroll
       for (int c = 0; c < 4; ++c) En[c] = (32 * c < mi) ? __ldg(perr + 32 * c) : 0.f;
+      // C-S check every kCsEvery tiles, on the scaled norm of the first item of the next tile
+      // (prefetched one check ahead).  A warp that is not done never meets an end marker: the
+      // producer ends a user tile only after all four warps (this one included) reported.
+      constexpr int kCsEvery = 4;
+      float pnn = nit > kCsEvery ? __double2float_ru(__ldg(pnorm + kCsEvery * kBN) * (double)pscl) : 0.f;
       mbar_wait(BAR(ACC_FULL + as), aph);
       tc_fence_after();
       tmem_ld64(tq + as * kBN, hA);
       tmem_ld_wait64(hA);
-      for (int it = 0; it < nit; ++it) {
+      int it = 0;
+      bool done = false;                        // warp-uniform: this warp's rows cannot gain any more
+      for (; it < nit; ++it) {
         const int base0 = it * kBN;
         float E[4];
 #pragma unroll
@@ -242,28 +282,52 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         const int pb = it < 255 ? it : 255;
 #endif
         const uint32_t tcur = tq + as * kBN;
-        tmem_ld64(tcur + 64, hB);                 // second half of this tile
+        tmem_ld64(tcur + 64, hB);               // second half of this tile
         uint32_t bits = epi_fast(hA, E[0], E[1], me.theta);
-        tmem_ld_wait64(hB);
         const bool more = it + 1 < nit;
         int as_next = as + 1 == kAcc ? 0 : as + 1;
         uint32_t aph_next = as + 1 == kAcc ? aph ^ 1 : aph;
-        if (more) {                               // first half of the next tile
+        if (more) {                             // first half of the next tile
           mbar_wait(BAR(ACC_FULL + as_next), aph_next);
           tc_fence_after();
           tmem_ld64(tq + as_next * kBN, hA);
         }
+        // (the wait sits after the prefetch so that no use of hB can be scheduled before it)
+        tmem_ld_wait64(hB);
         bits |= epi_fast(hB, E[2], E[3], me.theta) << 2;
         if (bits) me = epi_slow(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, sm, rloc, e0x2, kmax);
-        tc_fence_before();                        // this stage is no longer read: release it
+        tc_fence_before();                      // this stage is no longer read: release it
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
         as = as_next;
         aph = aph_next;
-        if (more) tmem_ld_wait64(hA);
+        if (more) tmem_ld_wait64(hA);  // (completed with hB's wait; re-anchors hA's uses)
 #ifdef RMIPS_EPI_PROFILE
         if (lane == 0) atomicAdd(&g_epi_prof[1][pb], (unsigned long long)(clock64() - t1));
 #endif
+        if ((it + 1) % kCsEvery == 0 && more) {
+          // every item from tile it + 1 on has scaled true score <= pnn (1 + 2^-16)
+          const uint32_t mk = __reduce_min_sync(0xffffffffu, f2key(me.theta));
+          if (__fmul_ru(pnn, 1.0000153f) < key2f(mk)) {
+            done = true;
+            break;
+          }
+          if (base0 + (kCsEvery + 1) * kBN < mi)
+            pnn = __double2float_ru(__ldg(pnorm + base0 + (kCsEvery + 1) * kBN) * (double)pscl);
+        }
+      }
+      if (lane == 0) atomicAdd(const_cast<int*>(done_cum), 1);  // one event per warp and user tile
+      if (done) {                               // drain: release the remaining stages unread
+        for (++it; it < nit; ++it) {            // stage `as` (tile it) is already full
+          const bool end = acc_end[as] == t + 1;
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
+          if (++as == kAcc) as = 0, aph ^= 1;
+          if (end || it + 1 == nit) break;
+          mbar_wait(BAR(ACC_FULL + as), aph);
+          tc_fence_after();
+        }
       }
       cand_finish(me, sm, rloc, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
       __syncwarp();
@@ -326,8 +390,9 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int tiles = (int)((x->n + kBM - 1) / kBM);
   const int grid = tiles < sm_count() ? tiles : sm_count();
-  k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->n, x->m, x->kmax, c.cand, c.ccount, c.ovf_list,
-                                               c.ovf_count);
+  const float* cs = getenv("RMIPS_NO_CS") ? nullptr : c.scale_dev;  // dev A/B switch for the C-S exit
+  k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, x->n, x->m, x->kmax, c.cand,
+                                               c.ccount, c.ovf_list, c.ovf_count);
   count_launch();
   return cudaGetLastError();
 }
