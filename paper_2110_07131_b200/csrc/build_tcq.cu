@@ -142,6 +142,11 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   const int A_FULL = 0, A_EMPTY = 1, B_FULL = 2, B_EMPTY = 2 + NST, ACC_FULL = 2 + 2 * NST,
             ACC_EMPTY = 2 + 2 * NST + NACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 + 2 * NST + 2 * NACC);
+  // early-termination control words (Cauchy-Schwarz, as in build_tc.cu): epilogue warps done
+  // with a group (cumulative, 4*UT per group), and the producer -> MMA -> epilogue end markers
+  volatile int* done_cum = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  volatile int* stage_end = done_cum + 1;
+  volatile int* acc_end = stage_end + NST;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_utiles = (int)((n + kBM - 1) / kBM);
@@ -155,6 +160,9 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     mbar_init(BAR(A_EMPTY), 1);
     for (int s = 0; s < NST; ++s) mbar_init(BAR(B_FULL + s), 1), mbar_init(BAR(B_EMPTY + s), 1);
     for (int a = 0; a < NACC; ++a) mbar_init(BAR(ACC_FULL + a), 1), mbar_init(BAR(ACC_EMPTY + a), 4 * UT);
+    *done_cum = 0;
+    for (int s = 0; s < NST; ++s) stage_end[s] = 0;
+    for (int a = 0; a < NACC; ++a) acc_end[a] = 0;
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -180,6 +188,12 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             tma_load_2d(sA + (u * KB + kb) * kUTile, &tmA, kb * 64, (gr * UT + u) * kBM, BAR(A_FULL));
         for (int it = 0; it < nit; ++it) {
           mbar_wait_sleep(BAR(B_EMPTY + stage), ph ^ 1);
+          if (*done_cum >= 4 * UT * (t + 1)) {  // every epilogue warp is done with this group
+            stage_end[stage] = t + 1;
+            mbar_arrive(BAR(B_FULL + stage));  // release: the marker is visible to the MMA warp
+            if (++stage == NST) stage = 0, ph ^= 1;
+            break;
+          }
           mbar_arrive_expect_tx(BAR(B_FULL + stage), KB * C::B_TILE);
           for (int kb = 0; kb < KB; ++kb)
             tma_load_2d(sB + (stage * KB + kb) * C::B_TILE, &tmB, kb * 64, it * BN, BAR(B_FULL + stage));
@@ -201,6 +215,14 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
           mbar_wait_sleep(BAR(B_FULL + stage), ph);
           tc_fence_after();
+          if (stage_end[stage] == t + 1) {  // the producer ended this group: forward the marker
+            mbar_arrive(BAR(B_EMPTY + stage));
+            acc_end[as] = t + 1;
+            mbar_arrive(BAR(ACC_FULL + as));
+            if (++stage == NST) stage = 0, ph ^= 1;
+            if (++as == NACC) as = 0, aph ^= 1;
+            break;
+          }
 #pragma unroll
           for (int u = 0; u < UT; ++u) {
             const uint32_t d = tmem + as * C::ACC_COLS + u * BN;
@@ -232,22 +254,28 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     // |s~| <= |u^| |p^| + E with |u^| <= 1 + 2^-10, |p^| <= |p| 2^e (1 + 2^-11): every score is
     // in [-smax, smax] (generous margins: the quantiser of candq.cuh must never saturate)
     const float smax = __fadd_ru(__fmul_ru((float)(__ldg(pnorm) * (double)__ldg(pscale)), 1.02f), __fmul_ru(2.f, e0x2));
+    const float pscl = __ldg(pscale);
     int as = 0;
     uint32_t aph = 0;
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + u * BN;
     constexpr int NCH = BN / 32;  // chunks per item tile (2 or 4)
+    constexpr int kCsEvery = 4;   // Cauchy-Schwarz check period (item tiles)
     uint32_t hA[64], hB[64];
-    for (int gr = blockIdx.x; gr < num_groups; gr += gridDim.x) {
+    int t = 0;
+    for (int gr = blockIdx.x; gr < num_groups; gr += gridDim.x, ++t) {
       const int64_t row = (int64_t)(gr * UT + u) * kBM + q * 32 + lane;
       QRow me = qrow_init(row < n, smax);  // dead rows (user >= n) have theta = +inf and never pass
       float En[NCH];                       // error bounds of the next tile's chunks (prefetched)
 #pragma unroll
       for (int c = 0; c < NCH; ++c) En[c] = (32 * c < mi) ? __ldg(perr + 32 * c) : 0.f;
+      float pnn = nit > kCsEvery ? __double2float_ru(__ldg(pnorm + kCsEvery * BN) * (double)pscl) : 0.f;
       mbar_wait(BAR(ACC_FULL + as), aph);
       tc_fence_after();
       tmem_ld64(tq + as * C::ACC_COLS, hA);
       tmem_ld_wait64(hA);
-      for (int it = 0; it < nit; ++it) {
+      int it = 0;
+      bool done = false;  // warp-uniform: this warp's rows cannot gain any more
+      for (; it < nit; ++it) {
         const int base0 = it * BN;
         float E[4];
 #pragma unroll
@@ -256,14 +284,9 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           En[c] = (base0 + BN + 32 * c < mi) ? __ldg(perr + base0 + BN + 32 * c) : 0.f;
         }
         if (NCH == 2) E[2] = E[3] = 0.f;
-#ifdef RMIPS_EPI_PROFILE
-        const long long t1 = clock64();
-        const int pb = it < 255 ? it : 255;
-#endif
         const uint32_t tcur = tq + as * C::ACC_COLS;
         if (BN == 128) tmem_ld64(tcur + 64, hB);  // second half of this tile
         uint32_t bits = epiq_fast(hA, E[0], E[1], me.theta);
-        if (BN == 128) tmem_ld_wait64(hB);
         const bool more = it + 1 < nit;
         const int as_next = as + 1 == NACC ? 0 : as + 1;
         const uint32_t aph_next = as + 1 == NACC ? aph ^ 1 : aph;
@@ -272,7 +295,10 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           tc_fence_after();
           tmem_ld64(tq + as_next * C::ACC_COLS, hA);
         }
-        if (BN == 128) bits |= epiq_fast(hB, E[2], E[3], me.theta) << 2;
+        if (BN == 128) {
+          tmem_ld_wait64(hB);
+          bits |= epiq_fast(hB, E[2], E[3], me.theta) << 2;
+        }
         if (bits) me = epiq_slow(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, sb, rr, e0x2, kmax);
         tc_fence_before();                        // this stage is no longer read: release it
         __syncwarp();
@@ -280,9 +306,29 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         as = as_next;
         aph = aph_next;
         if (more) tmem_ld_wait64(hA);
-#ifdef RMIPS_EPI_PROFILE
-        if (lane == 0) atomicAdd(&g_epi_prof[1][pb], (unsigned long long)(clock64() - t1));
-#endif
+        if ((it + 1) % kCsEvery == 0 && more) {
+          // every item from tile it + 1 on has scaled true score <= pnn (1 + 2^-16)
+          const uint32_t mk = __reduce_min_sync(0xffffffffu, f2key(me.theta));
+          if (__fmul_ru(pnn, 1.0000153f) < key2f(mk)) {
+            done = true;
+            break;
+          }
+          if (base0 + (kCsEvery + 1) * BN < mi)
+            pnn = __double2float_ru(__ldg(pnorm + base0 + (kCsEvery + 1) * BN) * (double)pscl);
+        }
+      }
+      if (lane == 0) atomicAdd(const_cast<int*>(done_cum), 1);  // one event per warp and group
+      if (done) {                                 // drain: release the remaining stages unread
+        for (++it; it < nit; ++it) {              // stage `as` (tile it) is already full
+          const bool end = acc_end[as] == t + 1;
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
+          if (++as == NACC) as = 0, aph ^= 1;
+          if (end || it + 1 == nit) break;
+          mbar_wait(BAR(ACC_FULL + as), aph);
+          tc_fence_after();
+        }
       }
       qrow_finish(me, sb, rr, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
       __syncwarp();
