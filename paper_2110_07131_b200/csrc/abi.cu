@@ -390,6 +390,7 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
     S.scans = hc[C_SCANS];
     S.items_scanned = hc[C_ITEMS_SCANNED];
     S.result_total = hc[C_ACCEPTED_TOTAL];
+    S.tiles_scored = hc[C_TILES_SCORED];
     const int64_t total = S.result_total;
     tm->mark();  // 4
     CK(query_sort(c, total, 64, st));

@@ -31,7 +31,7 @@ constexpr int kFlagPairOverflow = 2;
 // Counter slots (Index::d_counters), mirrored into rmips_stats_t.
 enum Counter {
   C_BLOCK_PAIRS = 0, C_BLOCK_PRUNED, C_SCORED, C_REJECTED, C_ACCEPT_FAST, C_UNDECIDED,
-  C_EXACT_ACCEPT, C_SCANS, C_ITEMS_SCANNED, C_ACCEPTED_TOTAL, C_UND_TOTAL, kNumCounters
+  C_EXACT_ACCEPT, C_SCANS, C_ITEMS_SCANNED, C_ACCEPTED_TOTAL, C_UND_TOTAL, C_TILES_SCORED, kNumCounters
 };
 
 // ---------------------------------------------------------------------------------------

@@ -127,6 +127,7 @@ k_query_simt(const __half* __restrict__ U16, const float* __restrict__ thrk, con
   __syncthreads();
   const int len = s_len;
   if (len == 0) return;
+  if (tid == 0) atomicAdd(ctr + C_TILES_SCORED, 1ull);
   const int64_t row = (int64_t)tile * 128 + tid;
   const bool live = row < n;
   for (int i = tid; i < 128 * (DPAD / 2); i += 128) {

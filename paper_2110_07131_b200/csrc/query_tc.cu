@@ -185,7 +185,7 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     if (lane == 0) {
       int stage = 0, cur_s = -1, nq = 0;
       uint32_t ph = 0;
-      unsigned long long pairs = 0, pruned = 0;
+      unsigned long long pairs = 0, pruned = 0, scored = 0;
       for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
         int s, t;
         const int len = work_len(w, s, t);
@@ -193,6 +193,7 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
         pairs += cnt;
         pruned += cnt - len;
         if (len == 0) continue;
+        ++scored;
         if (s != cur_s) {
           if (nq > 0) mbar_wait_sleep(BAR(Q_EMPTY), (nq - 1) & 1);
           mbar_arrive_expect_tx(BAR(Q_FULL), KB * kQTileBytes);
@@ -209,6 +210,7 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
       }
       atomicAdd(ctr + C_BLOCK_PAIRS, pairs);
       atomicAdd(ctr + C_BLOCK_PRUNED, pruned);
+      atomicAdd(ctr + C_TILES_SCORED, scored);
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
