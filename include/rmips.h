@@ -134,8 +134,11 @@ RMIPS_API rmips_status_t rmips_query_host(rmips_index_t idx, const float* q_batc
 RMIPS_API rmips_status_t rmips_query_stats(rmips_index_t idx, rmips_stats_t* out);
 
 /* Index introspection (for tests and tools).  All outputs are HOST buffers.
- *   info[0..8] = n, m, d, k_max, d_pad, block_size, overflow_rows, build_flags,
- *                candidates kept by the build filter (sum over rows; info[9..15] reserved, 0)
+ *   info[0..9] = n, m, d, k_max, d_pad, block_size, overflow_rows, build_flags,
+ *                candidates kept by the build filter (sum over rows),
+ *                (128-user tile, item tile) contractions issued by the tensor-core build (0 for the
+ *                SIMT build; fewer than all when the Cauchy-Schwarz early exit fired);
+ *                info[10..15] reserved, 0
  *   perm_u[n], perm_p[m]: sorted position -> original id (norm descending, ties by id)
  *   tau[k_max * n] fp64 and ids[k_max * n] int32: column-major by rank, users in ORIGINAL
  *   order: tau[j * n + u] = (j+1)-th largest u.p over P, ids = its original item id.

@@ -190,8 +190,9 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
     c.ccount = dalloc<int32_t>(n, st);
     c.ovf_list = dalloc<int32_t>(n, st);
     c.ovf_count = dalloc<int>(1, st);
-    c.cand_total = dalloc<unsigned long long>(1, st);
-    CK(cudaMemsetAsync(c.cand_total, 0, sizeof(unsigned long long), st));
+    c.cand_total = dalloc<unsigned long long>(2, st);
+    c.tiles_done = c.cand_total + 1;
+    CK(cudaMemsetAsync(c.cand_total, 0, 2 * sizeof(unsigned long long), st));
     const int fb_grid = 16;
     scratch = dalloc<double>((int64_t)fb_grid * m, st);
     CK(cudaMemsetAsync(x->d_flags, 0, 4 * sizeof(int), st));
@@ -224,7 +225,7 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
     CK(cudaMemcpyAsync(hp, x->d_flags, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hp + 1, c.ovf_count, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hp + 2, c.scale_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hp + 4, c.cand_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hp + 4, c.cand_total, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     dfree(c.nkey, st); dfree(c.nval, st);
     dfree(c.maxabs, st); dfree(c.cand, st); dfree(c.ccount, st); dfree(c.ovf_list, st);
     dfree(c.ovf_count, st); dfree(c.cand_total, st); dfree(scratch, st);
@@ -233,6 +234,7 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
     int flags = hp[0];
     x->overflow_rows = hp[1];
     memcpy(&x->cand_total, hp + 4, sizeof(int64_t));
+    memcpy(&x->tiles_done, hp + 6, sizeof(int64_t));
     if (tm.on) {
       x->phase_ms[0] = tm.between(0, 1);
       x->phase_ms[1] = tm.between(1, 2);
@@ -464,6 +466,7 @@ rmips_status_t rmips_index_info(rmips_index_t idx, int64_t info[16]) {
   if (!idx || !info) return fail(RMIPS_ERR_INVALID, "NULL argument");
   for (int i = 8; i < 16; ++i) info[i] = 0;
   info[8] = idx->cand_total;
+  info[9] = idx->tiles_done;
   info[0] = idx->n; info[1] = idx->m; info[2] = idx->d; info[3] = idx->kmax;
   info[4] = idx->dpad; info[5] = kTileU; info[6] = idx->overflow_rows; info[7] = idx->build_flags;
   return RMIPS_OK;

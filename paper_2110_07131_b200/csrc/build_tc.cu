@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
            int64_t n, int64_t m, int kmax, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
-           int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
+           int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count, unsigned long long* __restrict__ tiles_done) {
   using namespace sm100;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base, derived from smem_raw by pointer arithmetic so that the compiler
@@ -196,6 +196,7 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_f16_f32(kBM, kBN);
+      unsigned long long tiles_issued = 0;  // (user tile, item tile) contractions issued
       int stage = 0, as = 0;
       uint32_t ph = 0, aph = 0;
       int t = 0;
@@ -225,11 +226,13 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
           }
           mma_commit(BAR(B_EMPTY + stage));
           mma_commit(BAR(ACC_FULL + as));
+          tiles_issued += 1;
           if (++stage == kStages) stage = 0, ph ^= 1;
           if (++as == kAcc) as = 0, aph ^= 1;
         }
         mma_commit(BAR(A_EMPTY));
       }
+      atomicAdd(tiles_done, (unsigned long long)tiles_issued);
     }
   } else {
     // ------------------------------------------------ epilogue: one thread per user row
@@ -392,7 +395,7 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   const int grid = tiles < sm_count() ? tiles : sm_count();
   const float* cs = getenv("RMIPS_NO_CS") ? nullptr : c.scale_dev;  // dev A/B switch for the C-S exit
   k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, x->n, x->m, x->kmax, c.cand,
-                                               c.ccount, c.ovf_list, c.ovf_count);
+                                               c.ccount, c.ovf_list, c.ovf_count, c.tiles_done);
   count_launch();
   return cudaGetLastError();
 }

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(Cfg<KB, UT, BN>::THREADS, 1)
 k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
            int64_t n, int64_t m, int kmax, int ksteps, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
-           int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
+           int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count, unsigned long long* __restrict__ tiles_done) {
   using namespace sm100;
   using C = Cfg<KB, UT, BN>;
   constexpr int NST = C::NST, NACC = C::NACC;
@@ -205,6 +205,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_f16_f32(kBM, BN);
+      unsigned long long tiles_issued = 0;  // (user tile, item tile) contractions issued
       int stage = 0, as = 0;
       uint32_t ph = 0, aph = 0;
       int t = 0;
@@ -235,11 +236,13 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           }
           mma_commit(BAR(B_EMPTY + stage));
           mma_commit(BAR(ACC_FULL + as));
+          tiles_issued += UT;
           if (++stage == NST) stage = 0, ph ^= 1;
           if (++as == NACC) as = 0, aph ^= 1;
         }
         mma_commit(BAR(A_EMPTY));
       }
+      atomicAdd(tiles_done, (unsigned long long)tiles_issued);
     }
   } else {
     // ------------------------------------------------ epilogue: one thread per user row
@@ -364,7 +367,7 @@ static cudaError_t launch_tcq(const BuildCtx& c, cudaStream_t st) {
   const int ksteps = (x->d + 15) / 16;  // K steps of 16 that touch real (non-padding) columns
   k_build_tcq<KB, UT, BN><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tb, x->perr, x->pnorm, c.scale_dev, x->n, x->m,
                                                              x->kmax, ksteps, c.cand, c.ccount, c.ovf_list,
-                                                             c.ovf_count);
+                                                             c.ovf_count, c.tiles_done);
   count_launch();
   return cudaGetLastError();
 }

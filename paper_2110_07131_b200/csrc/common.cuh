@@ -111,6 +111,7 @@ struct rmips_index_s {
   int64_t nblocks = 0;
   int64_t overflow_rows = 0;
   int64_t cand_total = 0;   // candidates kept by the build filter (sum over non-overflowed rows)
+  int64_t tiles_done = 0;   // (128-user tile, item tile) contractions issued by the tensor-core build
   float pscale = 1.f;       // items are scaled by 2^e before fp16 rounding
   double c1 = 0, c2 = 0;    // filter error constants (see common.cuh)
 

@@ -30,6 +30,7 @@ struct BuildCtx {
   int32_t* ovf_list = nullptr;    // [n] overflowed rows
   int* ovf_count = nullptr;       // device counter
   unsigned long long* cand_total = nullptr;  // device: candidates kept by the filter (sum over rows)
+  unsigned long long* tiles_done = nullptr;  // device: (128-user tile, item tile) contractions issued
 };
 
 size_t build_cub_bytes(int64_t n, int64_t m);

@@ -109,7 +109,7 @@ class Index:
         info = (ctypes.c_int64 * 16)()
         _check(lib.rmips_index_info(self.handle, info))
         self.n, self.m, self.d, self.k_max, self.d_pad, self.block_size, self.overflow_rows, self.build_flags, \
-            self.cand_total = [int(v) for v in info[:9]]
+            self.cand_total, self.tiles_done = [int(v) for v in info[:10]]
 
     def close(self):
         if self.handle:
