@@ -290,7 +290,8 @@ static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cuda
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
   size_t oQ16 = take((size_t)nsub * kQB * dpad * 2), oqn = take((size_t)nsub * kQB * 4),
          oqe = take((size_t)nsub * kQB * 4), oqs = take((size_t)nsub * 4), oqp = take((size_t)nsub * kQB * 4),
-         oqc = take((size_t)nsub * 4), oacc = take((size_t)cap * 8), ound = take((size_t)cap * 8),
+         oqc = take((size_t)nsub * 4), owl = take((size_t)nsub * x->nblocks * 4), oacc = take((size_t)cap * 8),
+         ound = take((size_t)cap * 8),
          osrt = take((size_t)cap * 8), ocub = take(qcub);
   if (off > x->ws_bytes) {
     if (x->ws) cudaFreeAsync(x->ws, st);
@@ -305,6 +306,7 @@ static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cuda
   c.qscale = reinterpret_cast<float*>(b + oqs);
   c.qperm = reinterpret_cast<int32_t*>(b + oqp);
   c.qcount = reinterpret_cast<int32_t*>(b + oqc);
+  c.wlen = reinterpret_cast<int32_t*>(b + owl);
   c.acc = reinterpret_cast<uint64_t*>(b + oacc);
   c.und = reinterpret_cast<uint64_t*>(b + ound);
   c.acc_sorted = reinterpret_cast<uint64_t*>(b + osrt);

@@ -55,6 +55,7 @@ struct QueryCtx {
   float* qscale = nullptr;       // [nsub] 2^eq
   int32_t* qperm = nullptr;      // [nsub][kQB] sorted slot -> input query index (-1 padding)
   int32_t* qcount = nullptr;     // [nsub] queries in the sub-batch
+  int32_t* wlen = nullptr;       // [nsub * nblocks] Lemma 3 prefix of every (sub-batch, user tile)
   // outputs of the filter
   unsigned long long* counters = nullptr;  // kNumCounters (+ accepted / undecided list sizes)
   uint64_t* acc = nullptr;       // accepted keys (q_input << 32 | original user id)

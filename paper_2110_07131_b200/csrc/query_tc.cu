@@ -127,14 +127,44 @@ __device__ __noinline__ uint2 q_slow(uint32_t flag, uint32_t tbase, int len, boo
 
 }  // namespace
 
+// Lemma 3 for every work item (sub-batch s, user tile t): the number of leading
+// norm-sorted queries with ||q|| >= tb_k(t) (0 prunes the item whole), plus the block counters.
+__global__ void __launch_bounds__(256)
+k_lemma3_lens(const float* __restrict__ tbk, const float* __restrict__ qn, const int32_t* __restrict__ qcount,
+              int nblocks, int64_t nwork, int flags, int32_t* __restrict__ wlen, unsigned long long* __restrict__ ctr) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned long long pairs = 0, pruned = 0, scored = 0;
+  if (w < nwork) {
+    const int s = (int)(w / nblocks), t = (int)(w - (int64_t)s * nblocks);
+    const int cnt = qcount[s];
+    const float tbv = (flags & RMIPS_FLAG_NO_BLOCKS) ? -CUDART_INF_F : tbk[t];
+    const int len = lemma3_len(qn + (int64_t)s * kQB, cnt, tbv);
+    wlen[w] = len;
+    pairs = cnt;
+    pruned = cnt - len;
+    scored = len > 0;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
+    pruned += __shfl_xor_sync(0xffffffffu, pruned, o);
+    scored += __shfl_xor_sync(0xffffffffu, scored, o);
+  }
+  if ((threadIdx.x & 31) == 0 && pairs) {
+    atomicAdd(ctr + C_BLOCK_PAIRS, pairs);
+    atomicAdd(ctr + C_BLOCK_PRUNED, pruned);
+    atomicAdd(ctr + C_TILES_SCORED, scored);
+  }
+}
+
 template <int KB>
 __global__ void __launch_bounds__(kThreads, 1)
 k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmQ,
            const float* __restrict__ thrk, const float* __restrict__ tbk, const int32_t* __restrict__ perm_u,
            int64_t n, int nblocks, const float* __restrict__ qn, const float* __restrict__ qerr,
            const float* __restrict__ qscale, const int32_t* __restrict__ qperm, const int32_t* __restrict__ qcount,
-           int nsub, int flags, int ksteps, unsigned long long* __restrict__ ctr, uint64_t* __restrict__ acc_list,
-           uint64_t* __restrict__ und_list, int64_t cap) {
+           int nsub, int flags, int ksteps, const int32_t* __restrict__ wlen, unsigned long long* __restrict__ ctr,
+           uint64_t* __restrict__ acc_list, uint64_t* __restrict__ und_list, int64_t cap) {
   using namespace sm100;
   constexpr int kStages = QSmem::NU(KB);  // ring units
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -171,13 +201,15 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // Lemma 3 prefix of work item w (identical in every role)
-  auto work_len = [&](int64_t w, int& s, int& t) {
-    s = (int)(w / nblocks);
-    t = (int)(w - (int64_t)s * nblocks);
-    const int cnt = __ldg(qcount + s);
-    const float tbv = use_blocks ? __ldg(tbk + t) : -CUDART_INF_F;
-    return lemma3_len(qn + (int64_t)s * kQB, cnt, tbv);
+  // Work items w = blockIdx.x + i * gridDim.x; (sub-batch s, user tile t) advanced without
+  // divisions; the Lemma 3 prefix of every item comes from k_lemma3_lens (one load).
+  auto first_item = [&](int& s, int& t) {
+    s = (int)((int64_t)blockIdx.x / nblocks);
+    t = (int)((int64_t)blockIdx.x - (int64_t)s * nblocks);
+  };
+  auto next_item = [&](int& s, int& t) {
+    t += gridDim.x;
+    while (t >= nblocks) t -= nblocks, ++s;
   };
 
   if (warp == 0) {
@@ -185,15 +217,11 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     if (lane == 0) {
       int stage = 0, cur_s = -1, nq = 0;
       uint32_t ph = 0;
-      unsigned long long pairs = 0, pruned = 0, scored = 0;
-      for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
-        int s, t;
-        const int len = work_len(w, s, t);
-        const int cnt = __ldg(qcount + s);
-        pairs += cnt;
-        pruned += cnt - len;
+      int s, t;
+      first_item(s, t);
+      for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x, next_item(s, t)) {
+        const int len = __ldg(wlen + w);
         if (len == 0) continue;
-        ++scored;
         if (s != cur_s) {
           if (nq > 0) mbar_wait_sleep(BAR(Q_EMPTY), (nq - 1) & 1);
           mbar_arrive_expect_tx(BAR(Q_FULL), KB * kQTileBytes);
@@ -208,18 +236,16 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
           if (++stage == kStages) stage = 0, ph ^= 1;
         }
       }
-      atomicAdd(ctr + C_BLOCK_PAIRS, pairs);
-      atomicAdd(ctr + C_BLOCK_PRUNED, pruned);
-      atomicAdd(ctr + C_TILES_SCORED, scored);
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       int stage = 0, as = 0, cur_s = -1, nq = 0;
       uint32_t ph = 0, aph = 0;
-      for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
-        int s, t;
-        const int len = work_len(w, s, t);
+      int s, t;
+      first_item(s, t);
+      for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x, next_item(s, t)) {
+        const int len = __ldg(wlen + w);
         if (len == 0) continue;
         if (s != cur_s) {
           if (nq > 0) mma_commit(BAR(Q_EMPTY));  // all MMAs on the previous sub-batch's queries
@@ -258,9 +284,10 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     unsigned long long n_scored = 0, n_fast = 0, n_und = 0;
     int as = 0;
     uint32_t aph = 0;
-    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
-      int s, t;
-      const int len = work_len(w, s, t);
+    int s, t;
+    first_item(s, t);
+    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x, next_item(s, t)) {
+      const int len = __ldg(wlen + w);
       if (len == 0) continue;
       const int64_t row = (int64_t)t * kBM + rloc;
       const bool live = row < n;
@@ -357,10 +384,14 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int64_t nwork = (int64_t)c.nsub * x->nblocks;
   const int grid = (int)(nwork < sm_count_q() ? nwork : sm_count_q());
+  k_lemma3_lens<<<(unsigned)((nwork + 255) / 256), 256, 0, st>>>(x->tb + (int64_t)(c.k - 1) * x->nblocks, c.qn,
+                                                                 c.qcount, (int)x->nblocks, nwork, c.flags, c.wlen,
+                                                                 c.counters);
+  count_launch();
   k_query_tc<KB><<<grid, kThreads, smem, st>>>(tu, tq, x->thr + (int64_t)(c.k - 1) * x->n,
                                                x->tb + (int64_t)(c.k - 1) * x->nblocks, x->perm_u, x->n,
                                                (int)x->nblocks, c.qn, c.qerr, c.qscale, c.qperm, c.qcount, c.nsub,
-                                               c.flags, (x->d + 15) / 16, c.counters, c.acc, c.und, c.cap);
+                                               c.flags, (x->d + 15) / 16, c.wlen, c.counters, c.acc, c.und, c.cap);
   count_launch();
   return cudaGetLastError();
 }
