@@ -70,6 +70,7 @@ __device__ __noinline__ uint2 q_slow(uint32_t flag, uint32_t tbase, int len, boo
                                      uint64_t* __restrict__ acc_list, uint64_t* __restrict__ und_list, int64_t cap) {
   using namespace sm100;
   const int lane = threadIdx.x & 31;
+  const float thr_abs = fabsf(thr_s) * 2.384185791015625e-07f;
   uint32_t n_acc = 0, n_und = 0;
 #pragma unroll 1
   while (flag) {
@@ -80,17 +81,29 @@ __device__ __noinline__ uint2 q_slow(uint32_t flag, uint32_t tbase, int len, boo
     tmem_ld32(tbase + col0, r);
     tmem_ld_wait(r);
     uint32_t am = 0, um = 0;
-    if (live) {
+    // groups of 4 columns whose max cannot be rejected with the chunk's largest error bound (qerr
+    // is non-increasing along the slots); only those are classified pair by pair
+    const float emax = __fadd_ru(__ldg(qe_sub + col0), thr_abs);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (col0 + j < len) {
-          int cls = classify_tc(__uint_as_float(r[j]), thr_s, __ldg(qe_sub + col0 + j));
-          if (force && cls == 1) cls = 2;
-          am |= (uint32_t)(cls == 1) << j;
-          um |= (uint32_t)(cls == 2) << j;
+    for (int g = 0; g < 8; ++g) {
+      const float gm = fmaxf(fmaxf(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1])),
+                             fmaxf(__uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3])));
+      const bool gp = live && col0 + 4 * g < len && !(__fadd_ru(gm, emax) < thr_s);
+      if (__any_sync(0xffffffffu, gp)) {
+        if (gp) {
+#pragma unroll
+          for (int j = 4 * g; j < 4 * g + 4; ++j) {
+            if (col0 + j < len) {
+              int cls = classify_tc(__uint_as_float(r[j]), thr_s, __ldg(qe_sub + col0 + j));
+              if (force && cls == 1) cls = 2;
+              am |= (uint32_t)(cls == 1) << j;
+              um |= (uint32_t)(cls == 2) << j;
+            }
+          }
         }
       }
     }
+    if (!__any_sync(0xffffffffu, (am | um) != 0)) continue;
     const int na = __popc(am), nu = __popc(um);
     n_acc += na;
     n_und += nu;
@@ -223,14 +236,14 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
         const int len = __ldg(wlen + w);
         if (len == 0) continue;
         if (s != cur_s) {
-          if (nq > 0) mbar_wait_sleep(BAR(Q_EMPTY), (nq - 1) & 1);
+          if (nq > 0) mbar_wait(BAR(Q_EMPTY), (nq - 1) & 1);
           mbar_arrive_expect_tx(BAR(Q_FULL), KB * kQTileBytes);
           for (int kb = 0; kb < KB; ++kb) tma_load_2d(sQ + kb * kQTileBytes, &tmQ, kb * 64, s * kQB, BAR(Q_FULL));
           ++nq;
           cur_s = s;
         }
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait_sleep(BAR(A_EMPTY + stage), ph ^ 1);
+          mbar_wait(BAR(A_EMPTY + stage), ph ^ 1);
           mbar_arrive_expect_tx(BAR(A_FULL + stage), kUTileBytes);
           tma_load_2d(sA + stage * kUTileBytes, &tmU, kb * 64, t * kBM, BAR(A_FULL + stage));
           if (++stage == kStages) stage = 0, ph ^= 1;
@@ -249,16 +262,16 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
         if (len == 0) continue;
         if (s != cur_s) {
           if (nq > 0) mma_commit(BAR(Q_EMPTY));  // all MMAs on the previous sub-batch's queries
-          mbar_wait_sleep(BAR(Q_FULL), nq & 1);
+          mbar_wait(BAR(Q_FULL), nq & 1);
           ++nq;
           cur_s = s;
         }
-        mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
+        mbar_wait(BAR(ACC_EMPTY + as), aph ^ 1);
         const int N = (len + 15) & ~15;
         const uint32_t idesc = idesc_f16_f32(kBM, N);
         const uint32_t d = tmem + as * kAccCols;
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait_sleep(BAR(A_FULL + stage), ph);
+          mbar_wait(BAR(A_FULL + stage), ph);
           tc_fence_after();
           const uint32_t a0 = sA + stage * kUTileBytes;
           const uint32_t b0 = sQ + kb * kQTileBytes;
