@@ -30,7 +30,7 @@ namespace {
 constexpr int kBM = 128;                  // users per tile (TMEM lanes)
 constexpr int kUTileBytes = kBM * 64 * 2; // one K block of a user tile: 128 x 64 fp16 = 16 KB
 constexpr int kQTileBytes = kQB * 64 * 2; // 256 x 64 fp16 = 32 KB
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;           // producer, MMA, 8 epilogue warps (2 per TMEM lane quadrant)
 constexpr int kAccCols = 256;             // TMEM columns per accumulator stage
 constexpr int kAcc = 2;
 
@@ -202,7 +202,7 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     mbar_init(BAR(Q_FULL), 1);
     mbar_init(BAR(Q_EMPTY), 1);
     for (int s = 0; s < kStages; ++s) mbar_init(BAR(A_FULL + s), 1), mbar_init(BAR(A_EMPTY + s), 1);
-    for (int a = 0; a < kAcc; ++a) mbar_init(BAR(ACC_FULL + a), 1), mbar_init(BAR(ACC_EMPTY + a), 4);
+    for (int a = 0; a < kAcc; ++a) mbar_init(BAR(ACC_FULL + a), 1), mbar_init(BAR(ACC_EMPTY + a), 8);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -291,7 +291,10 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     // threshold.  Chunks where some pair may be accepted / undecided are flagged and classified
     // by q_slow (one out-of-line copy: the hot loop stays inside the instruction cache), which
     // re-reads them from TMEM before the stage is released.
+    // Eight epilogue warps: warp w reads TMEM lane quadrant w % 4 and the query-column half
+    // (w - 2) / 4 (pairs are independent, so the two warps of a quadrant share nothing).
     const int q = warp & 3;  // TMEM lane quadrant of this warp
+    const int hsel = (warp - 2) >> 2;
     const int rloc = q * 32 + lane;
     const bool force = (flags & RMIPS_FLAG_FORCE_VERIFY) != 0;
     unsigned long long n_scored = 0, n_fast = 0, n_und = 0;
@@ -308,7 +311,8 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
       const float thr_s = live ? __ldg(thrk + row) * sc : CUDART_INF_F;  // dead rows reject everything
       const float thr_abs = fabsf(thr_s) * 2.384185791015625e-07f;
       const float* qe_sub = qerr + (int64_t)s * kQB;
-      if (live) n_scored += len;
+      const int hlen = min(128, max(0, len - 128 * hsel));  // scored columns of this warp's half
+      if (live) n_scored += hlen;
       // qerr is non-increasing along the norm-sorted slots: a chunk's first slot bounds it
       float Emax[8];
 #pragma unroll
@@ -317,8 +321,8 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + as * kAccCols;
       uint32_t flag = 0;  // warp-uniform: chunks that need the slow path
-#pragma unroll 1
-      for (int h = 0; h * 128 < len; ++h) {
+      if (hsel * 128 < len) {
+        const int h = hsel;
         uint32_t r[4][32];
         tmem_ld32(tbase + h * 128, r[0]);
         tmem_ld32(tbase + h * 128 + 32, r[1]);
