@@ -393,11 +393,12 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
     S.pairs_exact_accepted = hc[C_EXACT_ACCEPT];
     S.scans = hc[C_SCANS];
     S.items_scanned = hc[C_ITEMS_SCANNED];
-    S.result_total = hc[C_ACCEPTED_TOTAL];
+    S.result_total = hc[C_ACC_REAL];
     S.tiles_scored = hc[C_TILES_SCORED];
     const int64_t total = S.result_total;
+    const int64_t reserved = (int64_t)hc[C_ACCEPTED_TOTAL];  // >= total: sentinel padding sorts last
     tm->mark();  // 4
-    CK(query_sort(c, total, 64, st));
+    CK(query_sort(c, reserved, 64, st));
     CK(query_output(c, offsets, user_ids, capacity, st));
     tm->mark();  // 5
     CK(cudaStreamSynchronize(st));

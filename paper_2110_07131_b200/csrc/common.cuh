@@ -31,8 +31,12 @@ constexpr int kFlagPairOverflow = 2;
 // Counter slots (Index::d_counters), mirrored into rmips_stats_t.
 enum Counter {
   C_BLOCK_PAIRS = 0, C_BLOCK_PRUNED, C_SCORED, C_REJECTED, C_ACCEPT_FAST, C_UNDECIDED,
-  C_EXACT_ACCEPT, C_SCANS, C_ITEMS_SCANNED, C_ACCEPTED_TOTAL, C_UND_TOTAL, C_TILES_SCORED, kNumCounters
+  C_EXACT_ACCEPT, C_SCANS, C_ITEMS_SCANNED, C_ACCEPTED_TOTAL, C_UND_TOTAL, C_TILES_SCORED, C_ACC_REAL,
+  kNumCounters
 };
+// C_ACCEPTED_TOTAL / C_UND_TOTAL count RESERVED list slots (the tcgen05 filter reserves in blocks and
+// pads unused slots with kSentinel); C_ACC_REAL counts the accepted records themselves.
+constexpr uint64_t kSentinel = ~0ull;
 
 // ---------------------------------------------------------------------------------------
 // The exact inner product (R7).  Left-to-right fp64 sum of the products of the

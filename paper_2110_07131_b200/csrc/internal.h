@@ -61,6 +61,7 @@ struct QueryCtx {
   uint64_t* acc = nullptr;       // accepted keys (q_input << 32 | original user id)
   uint64_t* und = nullptr;       // undecided (q_input << 32 | sorted user position)
   int64_t cap = 0;               // capacity of acc and of und
+  int64_t sorted_n = 0;          // keys sorted by query_sort (reserved slots, sentinels last)
   uint64_t* acc_sorted = nullptr;  // (also holds the 32-bit packed keys of the fast output path)
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;

@@ -167,6 +167,7 @@ k_query_simt(const __half* __restrict__ U16, const float* __restrict__ thrk, con
       warp_count(ok && cls == 0, ctr + C_REJECTED);
       warp_count(ok && cls == 1, ctr + C_ACCEPT_FAST);
       warp_append_u64(ok && cls == 1, (qin << 32) | uo, ctr + C_ACCEPTED_TOTAL, acc_list, cap);
+      warp_count(ok && cls == 1, ctr + C_ACC_REAL);
       warp_append_u64(ok && cls == 2, (qin << 32) | (uint64_t)row, ctr + C_UND_TOTAL, und_list, cap);
     }
   }
@@ -185,6 +186,7 @@ __global__ void k_exact_decide(const float* __restrict__ q, const float* __restr
     bool ok = i < total;
     bool yes = false;
     uint64_t key = 0;
+    if (ok && und_list[i] == kSentinel) ok = false;  // unused reserved slot
     if (ok) {
       uint64_t rec = und_list[i];
       uint32_t qin = (uint32_t)(rec >> 32);
@@ -196,6 +198,7 @@ __global__ void k_exact_decide(const float* __restrict__ q, const float* __restr
     warp_count(ok, ctr + C_UNDECIDED);
     warp_count(yes, ctr + C_EXACT_ACCEPT);
     warp_append_u64(yes, key, ctr + C_ACCEPTED_TOTAL, acc_list, cap);
+    warp_count(yes, ctr + C_ACC_REAL);
   }
 }
 
@@ -220,6 +223,7 @@ k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const 
   const double slack = 1.0 + (d + 8) * 2.220446049250313e-16;
   for (int64_t i = blockIdx.x * (int64_t)kScanWarps + w; i < total; i += (int64_t)gridDim.x * kScanWarps) {
     uint64_t rec = und_list[i];
+    if (rec == kSentinel) continue;  // unused reserved slot (warp-uniform: one record per warp)
     uint32_t qin = (uint32_t)(rec >> 32);
     int64_t row = (int64_t)(rec & 0xffffffffu);
     const float* u = U32 + row * d;
@@ -262,6 +266,7 @@ k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const 
       atomicAdd(ctr + C_UNDECIDED, 1ull);
       if (yes) {
         atomicAdd(ctr + C_EXACT_ACCEPT, 1ull);
+        atomicAdd(ctr + C_ACC_REAL, 1ull);
         unsigned long long pos = atomicAdd(ctr + C_ACCEPTED_TOTAL, 1ull);
         if ((int64_t)pos < cap) acc_list[pos] = ((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row];
       }
@@ -344,7 +349,7 @@ __global__ void k_pack32(const uint64_t* __restrict__ acc, int64_t total, uint32
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < total) {
     const uint64_t r = acc[i];
-    out[i] = (uint32_t)(r >> 32) * n + (uint32_t)(r & 0xffffffffu);
+    out[i] = r == kSentinel ? 0xffffffffu : (uint32_t)(r >> 32) * n + (uint32_t)(r & 0xffffffffu);
   }
 }
 __global__ void k_offsets32(const uint32_t* __restrict__ keys, int64_t total, int b, uint32_t n,
@@ -376,6 +381,7 @@ size_t query_cub_bytes(int64_t cap) {
 // total = number of accepted keys (host-known after the mid-call sync).
 cudaError_t query_sort(QueryCtx& c, int64_t total, int end_bit, cudaStream_t st) {
   size_t tb = c.cub_bytes;
+  c.sorted_n = total;
   if (total == 0) return cudaSuccess;
   if (use_keys32(c)) {
     // packed keys in the first half of acc_sorted's space, sorted into the second half (both fit: the
@@ -398,7 +404,7 @@ cudaError_t query_output(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64
   // offsets from the sorted keys; ids copied only if they fit
   const int64_t total = c.idx->stats.result_total;
   if (use_keys32(c)) {
-    const uint32_t* keys = reinterpret_cast<const uint32_t*>(c.acc_sorted) + total;
+    const uint32_t* keys = reinterpret_cast<const uint32_t*>(c.acc_sorted) + c.sorted_n;
     const uint32_t n32 = (uint32_t)c.idx->n;
     k_offsets32<<<nblk(c.b + 1, 256), 256, 0, st>>>(keys, total, c.b, n32, offsets); count_launch();
     if (total <= capacity && total > 0) {

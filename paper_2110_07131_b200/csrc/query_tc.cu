@@ -61,13 +61,56 @@ __device__ __forceinline__ int classify_tc(float acc, float thr_s, float qe) {
   return 2;
 }
 
+// Per-warp slot pools: a warp reserves list slots kPoolChunk at a time (one returning atomic per
+// reservation instead of one per chunk); slots it does not fill are padded with kSentinel at the
+// end of the kernel, which sorts last and is skipped by the exact path.
+constexpr int kPoolChunk = 128;
+struct QPool {
+  unsigned long long abase, ubase;  // next free slot of the accepted / undecided pool
+  int aleft, uleft;                 // slots left in it
+};
+
+// Position of this lane's first record among `tot` records of the warp (prefix p, count c):
+// records beyond the pool continue in a freshly reserved block.
+__device__ __forceinline__ void pool_take(unsigned long long& base, int& left, int tot, unsigned long long* counter,
+                                          unsigned long long& nbase) {
+  nbase = 0;
+  if (tot > left) {  // warp-uniform
+    const int need = tot - left;
+    const int res = (need + kPoolChunk - 1) / kPoolChunk * kPoolChunk;
+    if ((threadIdx.x & 31) == 0) nbase = atomicAdd(counter, (unsigned long long)res);
+    nbase = __shfl_sync(0xffffffffu, nbase, 0);
+  }
+}
+__device__ __forceinline__ unsigned long long pool_slot(unsigned long long base, int left, unsigned long long nbase,
+                                                        int p) {
+  return p < left ? base + p : nbase + (p - left);
+}
+__device__ __forceinline__ void pool_advance(unsigned long long& base, int& left, int tot, unsigned long long nbase) {
+  if (tot > left) {
+    const int need = tot - left;
+    const int res = (need + kPoolChunk - 1) / kPoolChunk * kPoolChunk;
+    base = nbase + need;
+    left = res - need;
+  } else {
+    base += tot;
+    left -= tot;
+  }
+}
+
+struct QSlowOut {
+  QPool pool;
+  uint32_t na, nu;
+};
+
 // Classify every pair of the flagged 32-column chunks (re-read from TMEM), then compact the
 // accepted and undecided pairs of the warp: one atomic per list per chunk.  Returns this
 // thread's (accepted, undecided) counts.
-__device__ __noinline__ uint2 q_slow(uint32_t flag, uint32_t tbase, int len, bool live, float thr_s,
-                                     const float* __restrict__ qe_sub, const int32_t* __restrict__ qp_sub,
-                                     uint64_t uo, int64_t row, bool force, unsigned long long* __restrict__ ctr,
-                                     uint64_t* __restrict__ acc_list, uint64_t* __restrict__ und_list, int64_t cap) {
+__device__ __noinline__ QSlowOut q_slow(QPool pool, uint32_t flag, uint32_t tbase, int len, bool live, float thr_s,
+                                        const float* __restrict__ qe_sub, const int32_t* __restrict__ qp_sub,
+                                        uint64_t uo, int64_t row, bool force, unsigned long long* __restrict__ ctr,
+                                        uint64_t* __restrict__ acc_list, uint64_t* __restrict__ und_list,
+                                        int64_t cap) {
   using namespace sm100;
   const int lane = threadIdx.x & 31;
   const float thr_abs = fabsf(thr_s) * 2.384185791015625e-07f;
@@ -107,7 +150,7 @@ __device__ __noinline__ uint2 q_slow(uint32_t flag, uint32_t tbase, int len, boo
     const int na = __popc(am), nu = __popc(um);
     n_acc += na;
     n_und += nu;
-    // warp-inclusive prefix sums -> one atomic per list per chunk
+    // warp-inclusive prefix sums; slots come from the warp's pools (rarely an atomic)
     int pa = na, pu = nu;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -115,27 +158,31 @@ __device__ __noinline__ uint2 q_slow(uint32_t flag, uint32_t tbase, int len, boo
       if (lane >= o) pa += xa, pu += xu;
     }
     const int ta = __shfl_sync(0xffffffffu, pa, 31), tu = __shfl_sync(0xffffffffu, pu, 31);
-    unsigned long long ba = 0, bu = 0;
-    if (lane == 31) {
-      if (ta) ba = atomicAdd(ctr + C_ACCEPTED_TOTAL, (unsigned long long)ta);
-      if (tu) bu = atomicAdd(ctr + C_UND_TOTAL, (unsigned long long)tu);
-    }
-    ba = __shfl_sync(0xffffffffu, ba, 31) + (pa - na);
-    bu = __shfl_sync(0xffffffffu, bu, 31) + (pu - nu);
+    unsigned long long na_base, nu_base;
+    pool_take(pool.abase, pool.aleft, ta, ctr + C_ACCEPTED_TOTAL, na_base);
+    pool_take(pool.ubase, pool.uleft, tu, ctr + C_UND_TOTAL, nu_base);
+    int p = pa - na;
     while (am) {
       const int j = __ffs(am) - 1;
       am &= am - 1;
-      if ((int64_t)ba < cap) acc_list[ba] = ((uint64_t)(uint32_t)__ldg(qp_sub + col0 + j) << 32) | uo;
-      ++ba;
+      const unsigned long long slot = pool_slot(pool.abase, pool.aleft, na_base, p++);
+      if ((int64_t)slot < cap) acc_list[slot] = ((uint64_t)(uint32_t)__ldg(qp_sub + col0 + j) << 32) | uo;
     }
+    p = pu - nu;
     while (um) {
       const int j = __ffs(um) - 1;
       um &= um - 1;
-      if ((int64_t)bu < cap) und_list[bu] = ((uint64_t)(uint32_t)__ldg(qp_sub + col0 + j) << 32) | (uint64_t)row;
-      ++bu;
+      const unsigned long long slot = pool_slot(pool.ubase, pool.uleft, nu_base, p++);
+      if ((int64_t)slot < cap) und_list[slot] = ((uint64_t)(uint32_t)__ldg(qp_sub + col0 + j) << 32) | (uint64_t)row;
     }
+    pool_advance(pool.abase, pool.aleft, ta, na_base);
+    pool_advance(pool.ubase, pool.uleft, tu, nu_base);
   }
-  return make_uint2(n_acc, n_und);
+  QSlowOut out;
+  out.pool = pool;
+  out.na = n_acc;
+  out.nu = n_und;
+  return out;
 }
 
 }  // namespace
@@ -298,6 +345,7 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     const int rloc = q * 32 + lane;
     const bool force = (flags & RMIPS_FLAG_FORCE_VERIFY) != 0;
     unsigned long long n_scored = 0, n_fast = 0, n_und = 0;
+    QPool pool{0ull, 0ull, 0, 0};
     int as = 0;
     uint32_t aph = 0;
     int s, t;
@@ -351,16 +399,22 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
       flag &= len >= 256 ? 0xffu : ((1u << ((len + 31) >> 5)) - 1u);
       if (flag) {
         const uint64_t uo = live ? (uint64_t)(uint32_t)__ldg(perm_u + row) : 0;
-        const uint2 cnts = q_slow(flag, tbase, len, live, thr_s, qe_sub, qperm + (int64_t)s * kQB, uo, row, force,
-                                  ctr, acc_list, und_list, cap);
-        n_fast += cnts.x;
-        n_und += cnts.y;
+        const QSlowOut o = q_slow(pool, flag, tbase, len, live, thr_s, qe_sub, qperm + (int64_t)s * kQB, uo, row,
+                                  force, ctr, acc_list, und_list, cap);
+        pool = o.pool;
+        n_fast += o.na;
+        n_und += o.nu;
       }
       tc_fence_before();  // this accumulator stage is fully read: hand it back to the MMA warp
       __syncwarp();
       if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
       if (++as == kAcc) as = 0, aph ^= 1;
     }
+    // pad the unused pool slots (warp-uniform pools; lanes share the work)
+    for (int i = lane; i < pool.aleft; i += 32)
+      if ((int64_t)(pool.abase + i) < cap) acc_list[pool.abase + i] = kSentinel;
+    for (int i = lane; i < pool.uleft; i += 32)
+      if ((int64_t)(pool.ubase + i) < cap) und_list[pool.ubase + i] = kSentinel;
     // counters: one atomic per warp
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -371,6 +425,7 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     if (lane == 0 && n_scored) {
       atomicAdd(ctr + C_SCORED, n_scored);
       atomicAdd(ctr + C_ACCEPT_FAST, n_fast);
+      atomicAdd(ctr + C_ACC_REAL, n_fast);
       atomicAdd(ctr + C_REJECTED, n_scored - n_fast - n_und);
     }
   }
