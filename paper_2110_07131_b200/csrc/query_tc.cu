@@ -25,6 +25,15 @@
 
 namespace rmips {
 
+#ifdef RMIPS_EPI_PROFILE
+__device__ unsigned long long g_qprof[8];  // development-only wait-time counters (tools/query_profile.py)
+#define QPROF_T0() const long long _t0 = clock64()
+#define QPROF_ADD(slot) atomicAdd(&g_qprof[slot], (unsigned long long)(clock64() - _t0))
+#else
+#define QPROF_T0()
+#define QPROF_ADD(slot)
+#endif
+
 namespace {
 
 constexpr int kBM = 128;                  // users per tile (TMEM lanes)
@@ -290,7 +299,11 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
           cur_s = s;
         }
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(BAR(A_EMPTY + stage), ph ^ 1);
+          {
+            QPROF_T0();
+            mbar_wait(BAR(A_EMPTY + stage), ph ^ 1);
+            QPROF_ADD(4);
+          }
           mbar_arrive_expect_tx(BAR(A_FULL + stage), kUTileBytes);
           tma_load_2d(sA + stage * kUTileBytes, &tmU, kb * 64, t * kBM, BAR(A_FULL + stage));
           if (++stage == kStages) stage = 0, ph ^= 1;
@@ -309,16 +322,26 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
         if (len == 0) continue;
         if (s != cur_s) {
           if (nq > 0) mma_commit(BAR(Q_EMPTY));  // all MMAs on the previous sub-batch's queries
+          QPROF_T0();
           mbar_wait(BAR(Q_FULL), nq & 1);
+          QPROF_ADD(0);
           ++nq;
           cur_s = s;
         }
-        mbar_wait(BAR(ACC_EMPTY + as), aph ^ 1);
+        {
+          QPROF_T0();
+          mbar_wait(BAR(ACC_EMPTY + as), aph ^ 1);
+          QPROF_ADD(1);
+        }
         const int N = (len + 15) & ~15;
         const uint32_t idesc = idesc_f16_f32(kBM, N);
         const uint32_t d = tmem + as * kAccCols;
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(BAR(A_FULL + stage), ph);
+          {
+            QPROF_T0();
+            mbar_wait(BAR(A_FULL + stage), ph);
+            QPROF_ADD(2);
+          }
           tc_fence_after();
           const uint32_t a0 = sA + stage * kUTileBytes;
           const uint32_t b0 = sQ + kb * kQTileBytes;
@@ -365,7 +388,11 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
       float Emax[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) Emax[c] = __fadd_ru(__ldg(qe_sub + (32 * c < len ? 32 * c : 0)), thr_abs);
-      mbar_wait(BAR(ACC_FULL + as), aph);
+      {
+        QPROF_T0();
+        mbar_wait(BAR(ACC_FULL + as), aph);
+        if (lane == 0) QPROF_ADD(3);
+      }
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + as * kAccCols;
       uint32_t flag = 0;  // warp-uniform: chunks that need the slow path
@@ -481,3 +508,14 @@ cudaError_t query_filter_tc(QueryCtx& c, cudaStream_t st) {
 }
 
 }  // namespace rmips
+
+#ifdef RMIPS_EPI_PROFILE
+extern "C" RMIPS_API int rmips_debug_query_profile(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, rmips::g_qprof, sizeof(rmips::g_qprof));
+  if (reset) {
+    static unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(rmips::g_qprof, z, sizeof z);
+  }
+  return 0;
+}
+#endif
