@@ -15,34 +15,45 @@
 namespace rmips {
 
 // ------------------------------------------------------------------------------ Q1
+// One CTA (8 warps) per 256-query sub-batch.  Warps compute the norms of 32 queries each with
+// coalesced row loads and a warp reduction (the norm is only used rounded up, so the summation
+// order does not matter); every thread then ranks its query in (norm desc, index asc) order, and
+// the warps write the fp16 rows (q * 2^eq, zero-padded to d_pad) cooperatively.
 __global__ void __launch_bounds__(kQB)
 k_query_prep(const float* __restrict__ q, int b, int d, int dpad, double c1, double c2, __half* __restrict__ Q16,
              float* __restrict__ qn, float* __restrict__ qerr, float* __restrict__ qscale,
              int32_t* __restrict__ qperm, int32_t* __restrict__ qcount, int* __restrict__ flags) {
   __shared__ double nrm[kQB];
   __shared__ float smax[kQB / 32];
+  __shared__ int srank[kQB];
   __shared__ float s_scale;
-  const int s = blockIdx.x, t = threadIdx.x;
-  const int i = s * kQB + t;
+  const int s = blockIdx.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int cnt = min(kQB, b - s * kQB);
-  double nr = -1.0;
   float mx = 0.f;
-  if (t < cnt) {
-    const float* x = q + (int64_t)i * d;
+  for (int j = 0; j < 32; ++j) {  // warp wid: queries wid * 32 + j
+    const int slot = wid * 32 + j;
     double acc = 0.0;
     bool fin = true;
-    for (int j = 0; j < d; ++j) {
-      float v = x[j];
-      fin &= isfinite(v);
-      mx = fmaxf(mx, fabsf(v));
-      acc = __fma_rn((double)v, (double)v, acc);
+    if (slot < cnt) {
+      const float* x = q + (int64_t)(s * kQB + slot) * d;
+      for (int e = lane; e < d; e += 32) {
+        const float v = x[e];
+        fin &= isfinite(v);
+        mx = fmaxf(mx, fabsf(v));
+        acc = __fma_rn((double)v, (double)v, acc);
+      }
     }
-    nr = sqrt(acc);
-    if (!fin) atomicOr(flags, kFlagNonfinite), mx = 0.f, nr = 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    fin = __all_sync(0xffffffffu, fin);
+    if (lane == 0) {
+      double nr = slot < cnt ? sqrt(acc) : -1.0;
+      if (slot < cnt && !fin) atomicOr(flags, kFlagNonfinite), nr = 0.0;
+      nrm[slot] = nr;
+    }
   }
-  nrm[t] = nr;
   for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((t & 31) == 0) smax[t >> 5] = mx;
+  if (lane == 0) smax[wid] = isfinite(mx) ? mx : 0.f;
   __syncthreads();
   if (t == 0) {
     float m2 = 0.f;
@@ -54,29 +65,37 @@ k_query_prep(const float* __restrict__ q, int b, int d, int dpad, double c1, dou
     qscale[s] = s_scale;
     qcount[s] = cnt;
   }
-  __syncthreads();
   // rank = position in (norm desc, index asc) order
+  const double nr = nrm[t];
   int rank = t;
   if (t < cnt) {
     rank = 0;
     for (int j = 0; j < cnt; ++j) {
-      double o = nrm[j];
+      const double o = nrm[j];
       rank += (o > nr) || (o == nr && j < t);
     }
   }
+  srank[t] = rank;
+  __syncthreads();
   const float scale = s_scale;
-  const int64_t slot = (int64_t)s * kQB + rank;
-  if (t < cnt) {
-    qperm[slot] = i;
-    qn[slot] = __double2float_ru(nr * (1.0 + 1e-12));
-    qerr[slot] = __double2float_ru((c1 * nr * (double)scale + c2) * (1.0 + 1e-6));
-    const float* x = q + (int64_t)i * d;
-    for (int j = 0; j < dpad; ++j) Q16[slot * dpad + j] = __float2half_rn(j < d ? x[j] * scale : 0.f);
-  } else {
-    qperm[slot] = -1;
-    qn[slot] = -CUDART_INF_F;
-    qerr[slot] = 0.f;
-    for (int j = 0; j < dpad; ++j) Q16[slot * dpad + j] = __float2half_rn(0.f);
+  {
+    const int64_t slot = (int64_t)s * kQB + rank;
+    if (t < cnt) {
+      qperm[slot] = s * kQB + t;
+      qn[slot] = __double2float_ru(nr * (1.0 + 1e-12));
+      qerr[slot] = __double2float_ru((c1 * nr * (double)scale + c2) * (1.0 + 1e-6));
+    } else {
+      qperm[slot] = -1;
+      qn[slot] = -CUDART_INF_F;
+      qerr[slot] = 0.f;
+    }
+  }
+  for (int j = 0; j < 32; ++j) {  // warp wid writes the fp16 rows of its 32 queries (coalesced)
+    const int src = wid * 32 + j;
+    const int64_t slot = (int64_t)s * kQB + srank[src];
+    const float* x = q + (int64_t)(s * kQB + src) * d;
+    for (int e = lane; e < dpad; e += 32)
+      Q16[slot * dpad + e] = __float2half_rn(src < cnt && e < d ? x[e] * scale : 0.f);
   }
 }
 
