@@ -157,6 +157,8 @@ RMIPS_API rmips_status_t rmips_index_export(rmips_index_t idx, int64_t* perm_u, 
  * Entries not measured are -1.  ms must hold 16 doubles. */
 RMIPS_API rmips_status_t rmips_phase_times(rmips_index_t idx, double ms[16]);
 
+/* Frees the index (stream-ordered on the stream of the index's last call; no host sync).  Call it
+ * before destroying that stream. */
 RMIPS_API void rmips_free_index(rmips_index_t idx);
 RMIPS_API const char* rmips_status_string(rmips_status_t s);
 RMIPS_API const char* rmips_last_error(void);  /* thread-local detail of the last failure */

@@ -83,6 +83,18 @@ void dfree(T*& p, cudaStream_t st) {
   p = nullptr;
 }
 
+// One allocation carved into many arrays (256-byte aligned): one host API call instead of ~25.
+struct Arena {
+  size_t off = 0;
+  template <typename T>
+  size_t take(int64_t count) {
+    const size_t o = off;
+    if (count <= 0) count = 1;
+    off += ((size_t)count * sizeof(T) + 255) / 256 * 256;
+    return o;
+  }
+};
+
 void retain_pool() {
   static bool done = false;
   if (done) return;
@@ -109,10 +121,16 @@ struct Pinned {
 thread_local Pinned g_pin;
 
 void free_index_arrays(rmips_index_s* x, cudaStream_t st) {
-  dfree(x->perm_u, st); dfree(x->perm_p, st); dfree(x->unorm, st); dfree(x->unu, st);
-  dfree(x->pnorm, st); dfree(x->perr, st); dfree(x->U16, st); dfree(x->U32, st);
-  dfree(x->P16, st); dfree(x->P32, st); dfree(x->tau, st); dfree(x->ids, st);
-  dfree(x->thr, st); dfree(x->tb, st); dfree(x->d_counters, st); dfree(x->d_flags, st);
+  if (x->arena) cudaFreeAsync(x->arena, st);  // every index array lives in the arena
+  x->arena = nullptr;
+  x->perm_u = x->perm_p = nullptr;
+  x->unorm = x->pnorm = nullptr;
+  x->unu = x->perr = x->U32 = x->P32 = x->thr = x->tb = nullptr;
+  x->U16 = x->P16 = nullptr;
+  x->tau = nullptr;
+  x->ids = nullptr;
+  x->d_counters = nullptr;
+  x->d_flags = nullptr;
   if (x->ws) cudaFreeAsync(x->ws, st);
   x->ws = nullptr;
   x->ws_bytes = 0;
@@ -164,37 +182,58 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
   double* scratch = nullptr;
   PhaseTimer tm((build_flags & RMIPS_BUILD_TIMING) != 0, st);
   try {
-    x->d_flags = dalloc<int>(4, st);
-    x->d_counters = dalloc<unsigned long long>(kNumCounters + 4, st);
-    x->perm_u = dalloc<int32_t>(n, st);
-    x->perm_p = dalloc<int32_t>(m, st);
-    x->unorm = dalloc<double>(n, st);
-    x->unu = dalloc<float>(n, st);
-    x->pnorm = dalloc<double>(m, st);
-    x->perr = dalloc<float>(m, st);
-    x->U16 = dalloc<__half>(n * x->dpad, st);
-    x->U32 = dalloc<float>(n * d, st);
-    x->P16 = dalloc<__half>(m * x->dpad, st);
-    x->P32 = dalloc<float>(m * x->pd, st);
-    x->tau = dalloc<double>((int64_t)k_max * n, st);
-    x->ids = dalloc<int32_t>((int64_t)k_max * n, st);
-    x->thr = dalloc<float>((int64_t)k_max * n, st);
-    x->tb = dalloc<float>((int64_t)k_max * x->nblocks, st);
-    c.nkey = dalloc<uint64_t>(2 * (m + n), st);
-    c.nval = dalloc<int32_t>(2 * (m + n), st);
-    c.maxabs = dalloc<unsigned int>(4, st);
-    c.scale_dev = reinterpret_cast<float*>(c.maxabs + 2);
+    // index arrays (kept) and build scratch (freed before return): two allocations
+    Arena ia;
+    const size_t o_flags = ia.take<int>(4), o_ctr = ia.take<unsigned long long>(kNumCounters + 4),
+                 o_pu = ia.take<int32_t>(n), o_pp = ia.take<int32_t>(m), o_un = ia.take<double>(n),
+                 o_unu = ia.take<float>(n), o_pn = ia.take<double>(m), o_perr = ia.take<float>(m),
+                 o_u16 = ia.take<__half>(n * x->dpad), o_u32 = ia.take<float>(n * d),
+                 o_p16 = ia.take<__half>(m * x->dpad), o_p32 = ia.take<float>(m * x->pd),
+                 o_tau = ia.take<double>((int64_t)k_max * n), o_ids = ia.take<int32_t>((int64_t)k_max * n),
+                 o_thr = ia.take<float>((int64_t)k_max * n), o_tb = ia.take<float>((int64_t)k_max * x->nblocks);
+    CK(cudaMallocAsync(&x->arena, ia.off, st));
+    char* A = static_cast<char*>(x->arena);
+    x->d_flags = reinterpret_cast<int*>(A + o_flags);
+    x->d_counters = reinterpret_cast<unsigned long long*>(A + o_ctr);
+    x->perm_u = reinterpret_cast<int32_t*>(A + o_pu);
+    x->perm_p = reinterpret_cast<int32_t*>(A + o_pp);
+    x->unorm = reinterpret_cast<double*>(A + o_un);
+    x->unu = reinterpret_cast<float*>(A + o_unu);
+    x->pnorm = reinterpret_cast<double*>(A + o_pn);
+    x->perr = reinterpret_cast<float*>(A + o_perr);
+    x->U16 = reinterpret_cast<__half*>(A + o_u16);
+    x->U32 = reinterpret_cast<float*>(A + o_u32);
+    x->P16 = reinterpret_cast<__half*>(A + o_p16);
+    x->P32 = reinterpret_cast<float*>(A + o_p32);
+    x->tau = reinterpret_cast<double*>(A + o_tau);
+    x->ids = reinterpret_cast<int32_t*>(A + o_ids);
+    x->thr = reinterpret_cast<float*>(A + o_thr);
+    x->tb = reinterpret_cast<float*>(A + o_tb);
+    Arena sa;
     c.cub_bytes = build_cub_bytes(n, m);
-    c.cub_tmp = dalloc<unsigned char>((int64_t)c.cub_bytes, st);
-    c.cand = dalloc<int32_t>(n * kCand, st);
-    c.ccount = dalloc<int32_t>(n, st);
-    c.ovf_list = dalloc<int32_t>(n, st);
-    c.ovf_count = dalloc<int>(1, st);
-    c.cand_total = dalloc<unsigned long long>(2, st);
-    c.tiles_done = c.cand_total + 1;
-    CK(cudaMemsetAsync(c.cand_total, 0, 2 * sizeof(unsigned long long), st));
     const int fb_grid = 16;
-    scratch = dalloc<double>((int64_t)fb_grid * m, st);
+    const size_t o_key = sa.take<uint64_t>(2 * (m + n)), o_val = sa.take<int32_t>(2 * (m + n)),
+                 o_max = sa.take<unsigned int>(4), o_cub = sa.take<unsigned char>((int64_t)c.cub_bytes),
+                 o_cand = sa.take<int32_t>(n * kCand), o_cc = sa.take<int32_t>(n), o_ovl = sa.take<int32_t>(n),
+                 o_ovc = sa.take<int>(1), o_ct = sa.take<unsigned long long>(2),
+                 o_scr = sa.take<double>((int64_t)fb_grid * m);
+    void* sarena = nullptr;
+    CK(cudaMallocAsync(&sarena, sa.off, st));
+    char* S = static_cast<char*>(sarena);
+    c.nkey = reinterpret_cast<uint64_t*>(S + o_key);
+    c.nval = reinterpret_cast<int32_t*>(S + o_val);
+    c.maxabs = reinterpret_cast<unsigned int*>(S + o_max);
+    c.scale_dev = reinterpret_cast<float*>(c.maxabs + 2);
+    c.cub_tmp = S + o_cub;
+    c.cand = reinterpret_cast<int32_t*>(S + o_cand);
+    c.ccount = reinterpret_cast<int32_t*>(S + o_cc);
+    c.ovf_list = reinterpret_cast<int32_t*>(S + o_ovl);
+    c.ovf_count = reinterpret_cast<int*>(S + o_ovc);
+    c.cand_total = reinterpret_cast<unsigned long long*>(S + o_ct);
+    c.tiles_done = c.cand_total + 1;
+    scratch = reinterpret_cast<double*>(S + o_scr);
+    c.scratch_arena = sarena;
+    CK(cudaMemsetAsync(c.cand_total, 0, 2 * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(x->d_flags, 0, 4 * sizeof(int), st));
     CK(cudaMemsetAsync(c.maxabs, 0, 4 * sizeof(unsigned int), st));
     CK(cudaMemsetAsync(c.ovf_count, 0, sizeof(int), st));
@@ -226,10 +265,8 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
     CK(cudaMemcpyAsync(hp + 1, c.ovf_count, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hp + 2, c.scale_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hp + 4, c.cand_total, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    dfree(c.nkey, st); dfree(c.nval, st);
-    dfree(c.maxabs, st); dfree(c.cand, st); dfree(c.ccount, st); dfree(c.ovf_list, st);
-    dfree(c.ovf_count, st); dfree(c.cand_total, st); dfree(scratch, st);
-    if (c.cub_tmp) cudaFreeAsync(c.cub_tmp, st);
+    cudaFreeAsync(c.scratch_arena, st);
+    c.scratch_arena = nullptr;
     CK(cudaStreamSynchronize(st));
     int flags = hp[0];
     x->overflow_rows = hp[1];
@@ -249,10 +286,12 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
     }
   } catch (const CudaFail& f) {
     cudaStreamSynchronize(st);
+    if (c.scratch_arena) cudaFreeAsync(c.scratch_arena, st);
     free_index_arrays(x, st);
     delete x;
     return from_cuda(f);
   }
+  x->last_stream = st;
   *out = x;
   return RMIPS_OK;
 }
@@ -328,6 +367,7 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
     return fail(RMIPS_ERR_INVALID, "unknown flag bits");
   rmips_index_s* x = idx;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  x->last_stream = st;
   *total_out = 0;
   memset(&x->stats, 0, sizeof x->stats);
   x->stats.queries = b;
@@ -504,9 +544,8 @@ rmips_status_t rmips_index_export(rmips_index_t idx, int64_t* perm_u, int64_t* p
 
 void rmips_free_index(rmips_index_t idx) {
   if (!idx) return;
-  cudaDeviceSynchronize();
-  free_index_arrays(idx, 0);
-  cudaStreamSynchronize(0);
+  // stream-ordered after the index's last call (no host synchronisation)
+  free_index_arrays(idx, idx->last_stream);
   delete idx;
 }
 

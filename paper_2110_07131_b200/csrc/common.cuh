@@ -137,7 +137,8 @@ struct rmips_index_s {
   float* thr = nullptr;        // [kmax][n] tau/nu in fp32 (filter threshold, unscaled)
   float* tb = nullptr;         // [kmax][nblocks] Lemma 3: L^j(B) / ||u_first(B)||, rounded down
 
-  // build scratch (freed after build)
+  void* arena = nullptr;       // the single allocation every array above lives in
+  cudaStream_t last_stream = nullptr;  // stream of the last call (rmips_free_index frees on it)
   // query workspace (grown on demand)
   void* ws = nullptr;
   size_t ws_bytes = 0;

@@ -19,6 +19,7 @@ inline void count_launch(int k = 1) { g_launches.fetch_add(k, std::memory_order_
 // Scratch of one build call (owned by abi.cu, freed before rmips_build_index returns).
 struct BuildCtx {
   rmips_index_s* idx = nullptr;
+  void* scratch_arena = nullptr;  // the single allocation of the build scratch below
   uint64_t* nkey = nullptr;       // [2][m + n] sort keys in/out: fp64 norm bits, top bit set for items
   int32_t* nval = nullptr;        // [2][m + n] sort values in/out: concatenated index (items first)
   unsigned int* maxabs = nullptr; // max |p_j| bits
