@@ -402,6 +402,13 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
 
 cudaError_t build_tc(const BuildCtx& c, cudaStream_t st) {
   if (getenv("RMIPS_DISABLE_TC")) return cudaErrorNotSupported;
+  if (c.idx->dpad == 64 && c.idx->m <= 65536 && getenv("RMIPS_BUILD_TC2")) {
+    // experiment switch: two user tiles per CTA with 4-byte bf16-bound entries (build_tcq.cu,
+    // candh.cuh); measured 10% slower than this kernel on configs[1] (the epilogue's TMEM reads
+    // and issue, not its latency, bound both)
+    const cudaError_t e = build_tcq(c, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   switch (c.idx->dpad) {
     case 64: return launch_tc<1>(c, st);
     default: return build_tcq(c, st);  // d_pad 128..256: build_tcq.cu

@@ -4,7 +4,7 @@
 // quantised entries, so that the 128 x 256 fp16 user tile, the item ring and the candidate
 // buffers fit in one SM's shared memory), so the score matrix never reaches HBM.
 //
-// k_build_tcq<KB, UT, BN>: K = 64*KB (d_pad), UT user tiles of 128 rows per CTA, item tiles of
+// k_build_tcq<KB, UT, BN, Pol>: K = 64*KB (d_pad), UT user tiles of 128 rows per CTA, item tiles of
 // BN rows.  One persistent CTA per SM walks groups of UT user tiles; per group:
 //   warp 0        TMA producer: the UT user tiles A (128 x 64*KB fp16, once per group) and the
 //                 stream of item tiles B through an NST-deep shared-memory ring (SWIZZLE_128B)
@@ -22,6 +22,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include "candh.cuh"
 #include "candq.cuh"
 #include "common.cuh"
 #include "internal.h"
@@ -49,9 +50,46 @@ struct Cfg {
   static constexpr int A = 0;
   static constexpr int B = UT * KB * kUTile;
   static constexpr int CAND = B + NST * KB * B_TILE;
-  static constexpr int BAR = CAND + UT * kBM * kQSlots * 4;
+  static constexpr int BAR = CAND + UT * kBM * 128 * 4;  // 128 four-byte candidate slots per row
   static constexpr int TOTAL = BAR + 256 + 1024;  // + alignment slack
   static_assert(TOTAL <= 232448, "shared memory");
+};
+
+// Candidate-filter policies (4-byte entries both): candq.cuh (12-bit quantised bound, 20-bit
+// position: m <= 2^20) and candh.cuh (bf16 bound, 16-bit position: m <= 2^16).
+struct QPol {
+  using Row = QRow;
+  using Buf = QBuf;
+  static constexpr int kSlots = kQSlots;
+  __device__ static Row init(bool live, float smax) { return qrow_init(live, smax); }
+  template <typename F>
+  __device__ static void append(F f, const float (&g4)[8], float E, int pos0, int mi, Row& me, Buf sb, int rr) {
+    qrow_append_chunk(f, g4, E, pos0, mi, me, sb, rr);
+  }
+  __device__ static void maybe_refresh(Row& me, Buf sb, int rr, float e0x2, int kmax) {
+    qrow_maybe_refresh(me, sb, rr, e0x2, kmax);
+  }
+  __device__ static void finish(Row& me, Buf sb, int rr, float e0x2, int kmax, int64_t row, int64_t n, int32_t* cand,
+                                int32_t* ccount, int32_t* ovf_list, int* ovf_count) {
+    qrow_finish(me, sb, rr, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
+  }
+};
+struct HPol {
+  using Row = HRow;
+  using Buf = HBuf;
+  static constexpr int kSlots = kHSlots;
+  __device__ static Row init(bool live, float) { return hrow_init(live); }
+  template <typename F>
+  __device__ static void append(F f, const float (&g4)[8], float E, int pos0, int mi, Row& me, Buf sb, int rr) {
+    hrow_append_chunk(f, g4, E, pos0, mi, me, sb, rr);
+  }
+  __device__ static void maybe_refresh(Row& me, Buf sb, int rr, float e0x2, int kmax) {
+    hrow_maybe_refresh(me, sb, rr, e0x2, kmax);
+  }
+  __device__ static void finish(Row& me, Buf sb, int rr, float e0x2, int kmax, int64_t row, int64_t n, int32_t* cand,
+                                int32_t* ccount, int32_t* ovf_list, int* ovf_count) {
+    hrow_finish(me, sb, rr, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
+  }
 };
 
 // Fast path of one 64-column half (scores of this thread's row): 3-input max trees and one
@@ -75,7 +113,9 @@ __device__ __forceinline__ uint32_t epiq_fast(const uint32_t (&h)[64], float E0,
 
 // Slow path (one copy in the kernel, so the hot loop stays inside the instruction cache):
 // re-read each flagged chunk of the current accumulator stage from TMEM, append and refresh.
-__device__ __noinline__ QRow epiq_slow(uint32_t bits, uint32_t taddr, int base0, int mi, float4 E4, QRow me, QBuf sb,
+template <class Pol>
+__device__ __noinline__ typename Pol::Row epiq_slow(uint32_t bits, uint32_t taddr, int base0, int mi, float4 E4,
+                                                    typename Pol::Row me, typename Pol::Buf sb,
                                       int rr, float e0x2, int kmax) {
 #pragma unroll 1
   while (bits) {
@@ -99,12 +139,12 @@ __device__ __noinline__ QRow epiq_slow(uint32_t bits, uint32_t taddr, int base0,
 #ifdef RMIPS_EPI_PROFILE
     const long long p0 = clock64();
 #endif
-    qrow_append_chunk([&](int j) { return __uint_as_float(r[j]); }, g4, E, pos0, mi, me, sb, rr);
+    Pol::append([&](int j) { return __uint_as_float(r[j]); }, g4, E, pos0, mi, me, sb, rr);
 #ifdef RMIPS_EPI_PROFILE
     const long long p1 = clock64();
-    const bool rf = __any_sync(0xffffffffu, me.cnt > kQSlots - 32);
+    const bool rf = __any_sync(0xffffffffu, me.cnt > Pol::kSlots - 32);
 #endif
-    qrow_maybe_refresh(me, sb, rr, e0x2, kmax);
+    Pol::maybe_refresh(me, sb, rr, e0x2, kmax);
 #ifdef RMIPS_EPI_PROFILE
     if ((threadIdx.x & 31) == 0) {
       atomicAdd(&g_epi_prof[2][0], 1ull);
@@ -119,7 +159,7 @@ __device__ __noinline__ QRow epiq_slow(uint32_t bits, uint32_t taddr, int base0,
 
 }  // namespace
 
-template <int KB, int UT, int BN>
+template <int KB, int UT, int BN, class Pol>
 __global__ void __launch_bounds__(Cfg<KB, UT, BN>::THREADS, 1)
 k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
@@ -135,7 +175,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   const uint32_t sbase = smem_u32(smem);
   const uint32_t sA = sbase + C::A;
   const uint32_t sB = sbase + C::B;
-  const QBuf sb{reinterpret_cast<uint32_t*>(smem + C::CAND), UT * kBM};
+  const typename Pol::Buf sb{reinterpret_cast<uint32_t*>(smem + C::CAND), UT * kBM};
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR);
   const uint32_t bar0 = smem_u32(bars);
   auto BAR = [&](int i) { return bar0 + 8u * i; };
@@ -267,7 +307,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     int t = 0;
     for (int gr = blockIdx.x; gr < num_groups; gr += gridDim.x, ++t) {
       const int64_t row = (int64_t)(gr * UT + u) * kBM + q * 32 + lane;
-      QRow me = qrow_init(row < n, smax);  // dead rows (user >= n) have theta = +inf and never pass
+      typename Pol::Row me = Pol::init(row < n, smax);  // dead rows (user >= n): theta = +inf, never pass
       float En[NCH];                       // error bounds of the next tile's chunks (prefetched)
 #pragma unroll
       for (int c = 0; c < NCH; ++c) En[c] = (32 * c < mi) ? __ldg(perr + 32 * c) : 0.f;
@@ -302,7 +342,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           tmem_ld_wait64(hB);
           bits |= epiq_fast(hB, E[2], E[3], me.theta) << 2;
         }
-        if (bits) me = epiq_slow(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, sb, rr, e0x2, kmax);
+        if (bits) me = epiq_slow<Pol>(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, sb, rr, e0x2, kmax);
         tc_fence_before();                        // this stage is no longer read: release it
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
@@ -333,7 +373,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           tc_fence_after();
         }
       }
-      qrow_finish(me, sb, rr, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
+      Pol::finish(me, sb, rr, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
       __syncwarp();
     }
   }
@@ -353,32 +393,34 @@ static int sm_count_q() {
   return c;
 }
 
-template <int KB, int UT, int BN>
+template <int KB, int UT, int BN, class Pol>
 static cudaError_t launch_tcq(const BuildCtx& c, cudaStream_t st) {
   using C = Cfg<KB, UT, BN>;
   rmips_index_s* x = c.idx;
   CUtensorMap ta, tb;
   if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM)) return cudaErrorNotSupported;
   if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)x->m, (uint64_t)x->dpad, BN)) return cudaErrorNotSupported;
-  cudaError_t e = cudaFuncSetAttribute(k_build_tcq<KB, UT, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
+  cudaError_t e = cudaFuncSetAttribute(k_build_tcq<KB, UT, BN, Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
   if (e != cudaSuccess) return e;
   const int groups = (int)(((x->n + kBM - 1) / kBM + UT - 1) / UT);
   const int grid = groups < sm_count_q() ? groups : sm_count_q();
   const int ksteps = (x->d + 15) / 16;  // K steps of 16 that touch real (non-padding) columns
-  k_build_tcq<KB, UT, BN><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tb, x->perr, x->pnorm, c.scale_dev, x->n, x->m,
+  k_build_tcq<KB, UT, BN, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tb, x->perr, x->pnorm, c.scale_dev, x->n, x->m,
                                                              x->kmax, ksteps, c.cand, c.ccount, c.ovf_list,
                                                              c.ovf_count, c.tiles_done);
   count_launch();
   return cudaGetLastError();
 }
 
-// d_pad = 128..256 (the d <= 64 case is build_tc.cu's kernel).
+// d_pad = 128..256, and d_pad = 64 with m <= 2^16 (two user tiles per CTA, bf16-bound entries);
+// other d <= 64 cases use build_tc.cu's kernel.
 cudaError_t build_tcq(const BuildCtx& c, cudaStream_t st) {
   if (c.idx->m > (int64_t)kQPosMask + 1) return cudaErrorNotSupported;  // packed positions are 20-bit
   switch (c.idx->dpad) {
-    case 128: return launch_tcq<2, 1, 64>(c, st);
-    case 192: return launch_tcq<3, 1, 64>(c, st);
-    case 256: return launch_tcq<4, 1, 64>(c, st);
+    case 64: return c.idx->m <= 65536 ? launch_tcq<1, 2, 128, HPol>(c, st) : cudaErrorNotSupported;
+    case 128: return launch_tcq<2, 1, 64, QPol>(c, st);
+    case 192: return launch_tcq<3, 1, 64, QPol>(c, st);
+    case 256: return launch_tcq<4, 1, 64, QPol>(c, st);
     default: return cudaErrorNotSupported;
   }
 }
