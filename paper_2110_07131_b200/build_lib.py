@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "librmips.so")
 BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["abi.cu", "build.cu", "build_tc.cu", "build_tcq.cu", "query.cu", "query_tc.cu"]
+SOURCES = ["abi.cu", "build.cu", "build_tc.cu", "build_tc2.cu", "build_tcq.cu", "query.cu", "query_tc.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-DRMIPS_BUILD"]
@@ -39,12 +39,17 @@ def _compile(src: str, verbose: bool, extra=(), tag: str = "") -> str:
     return obj
 
 
-def build(verbose: bool = False, force: bool = False, profile: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, profile: bool = False, variant: str = "",
+          defines=()) -> str:
     """profile=True builds the development-only instrumented variant librmips_prof.so
-    (-DRMIPS_EPI_PROFILE, see tools/epi_profile.py); the product library is librmips.so."""
+    (-DRMIPS_EPI_PROFILE, see tools/epi_profile.py); variant="x" with defines=["-DFOO"] builds the
+    development-only A/B library librmips_x.so (tools/gpu_ab.sh).  The product library is
+    librmips.so."""
     os.makedirs(BUILD, exist_ok=True)
     extra, tag = (["-DRMIPS_EPI_PROFILE"], "_prof") if profile else ((), "")
-    OUT = os.path.join(HERE, "librmips_prof.so" if profile else "librmips.so")
+    if variant:
+        extra, tag = tuple(defines), "_" + variant
+    OUT = os.path.join(HERE, "librmips%s.so" % tag)
     if force:
         for f in os.listdir(BUILD):
             os.remove(os.path.join(BUILD, f))

@@ -92,7 +92,8 @@ __device__ __noinline__ CandRow epi_slow(uint32_t bits, uint32_t taddr, int base
 #ifdef RMIPS_EPI_PROFILE
     const long long p0 = clock64();
 #endif
-    cand_append_chunk([&](int j) { return __uint_as_float(r[j]); }, g4, E, pos0, me, sm, rloc);
+    const float mx = fmaxf(fmaxf(fmaxf(g4[0], g4[1]), fmaxf(g4[2], g4[3])), fmaxf(fmaxf(g4[4], g4[5]), fmaxf(g4[6], g4[7])));
+    cand_append_flat([&](int j) { return __uint_as_float(r[j]); }, mx, E, pos0, me, sm, rloc);
 #ifdef RMIPS_EPI_PROFILE
     const long long p1 = clock64();
     const bool rf = __any_sync(0xffffffffu, me.cnt > kCand - 32);
@@ -110,13 +111,24 @@ __device__ __noinline__ CandRow epi_slow(uint32_t bits, uint32_t taddr, int base
   return me;
 }
 
+// maxima of the two 16-column groups of chunk c of a half tile, minus E (rounded down)
+__device__ __forceinline__ uint2 group_max16(const uint32_t (&h)[64], int c, float E) {
+  float g[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    g[i] = fmaxf(fmaxf(__uint_as_float(h[32 * c + 4 * i]), __uint_as_float(h[32 * c + 4 * i + 1])),
+                 fmaxf(__uint_as_float(h[32 * c + 4 * i + 2]), __uint_as_float(h[32 * c + 4 * i + 3])));
+  return make_uint2(__float_as_uint(__fsub_rd(fmaxf(fmaxf(g[0], g[1]), fmaxf(g[2], g[3])), E)),
+                    __float_as_uint(__fsub_rd(fmaxf(fmaxf(g[4], g[5]), fmaxf(g[6], g[7])), E)));
+}
+
 }  // namespace
 
 template <int KB>
 __global__ void __launch_bounds__(kThreads, 1)
 k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
-           int64_t n, int64_t m, int kmax, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
+           int64_t n, int64_t m, int kmax, int seed_tiles, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
            int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count, unsigned long long* __restrict__ tiles_done) {
   using namespace sm100;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -177,7 +189,8 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         if (t > 0) mbar_wait_sleep(BAR(A_EMPTY), (t - 1) & 1);
         mbar_arrive_expect_tx(BAR(A_FULL), KB * kTileBytes);
         for (int kb = 0; kb < KB; ++kb) tma_load_2d(sA + kb * kTileBytes, &tmA, kb * 64, ut * kBM, BAR(A_FULL));
-        for (int it = 0; it < nit; ++it) {
+        for (int j = 0; j < seed_tiles + nit; ++j) {  // seed pass, then all item tiles
+          const int it = j < seed_tiles ? j : j - seed_tiles;
           mbar_wait_sleep(BAR(B_EMPTY + stage), ph ^ 1);
           if (*done_cum >= 4 * (t + 1)) {  // every epilogue warp is done with this user tile
             stage_end[stage] = t + 1;
@@ -203,7 +216,7 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
         mbar_wait_sleep(BAR(A_FULL), t & 1);
         tc_fence_after();
-        for (int it = 0; it < nit; ++it) {
+        for (int j = 0; j < seed_tiles + nit; ++j) {
           mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
           mbar_wait_sleep(BAR(B_FULL + stage), ph);
           tc_fence_after();
@@ -226,7 +239,7 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
           }
           mma_commit(BAR(B_EMPTY + stage));
           mma_commit(BAR(ACC_FULL + as));
-          tiles_issued += 1;
+          tiles_issued += j >= seed_tiles;  // the seed pass repeats tiles: not counted
           if (++stage == kStages) stage = 0, ph ^= 1;
           if (++as == kAcc) as = 0, aph ^= 1;
         }
@@ -270,6 +283,47 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       tc_fence_after();
       tmem_ld64(tq + as * kBN, hA);
       tmem_ld_wait64(hA);
+      if (seed_tiles > 0) {
+        // Seed pass over item tiles 0 .. seed_tiles-1 (full tiles; contracted again below): the
+        // 16-column group maxima minus E are lower bounds of distinct items' true scores, so the
+        // k_max-th largest of them (cand_seed) is a valid starting theta.  It spares the filter
+        // the dense phase in which theta would otherwise climb from -inf through appends and
+        // refreshes.  The maxima sit in this row's (still empty) candidate slots, two per slot.
+        uint2* sb = sm.buf + rloc;
+        float vmx = -__int_as_float(0x7f800000);
+        for (int j = 0; j < seed_tiles; ++j) {
+          const int base0 = j * kBN;
+          tmem_ld64(tq + as * kBN + 64, hB);
+          const float E0 = __ldg(perr + base0), E1 = __ldg(perr + base0 + 32), E2 = __ldg(perr + base0 + 64),
+                      E3 = __ldg(perr + base0 + 96);
+          uint2 l0 = group_max16(hA, 0, E0), l1 = group_max16(hA, 1, E1);
+          const int as_next = as + 1 == kAcc ? 0 : as + 1;
+          const uint32_t aph_next = as + 1 == kAcc ? aph ^ 1 : aph;
+          mbar_wait(BAR(ACC_FULL + as_next), aph_next);  // the main pass follows: always a next stage
+          tc_fence_after();
+          tmem_ld64(tq + as_next * kBN, hA);
+          tmem_ld_wait64(hB);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
+          as = as_next;
+          aph = aph_next;
+          const uint2 l2 = group_max16(hB, 0, E2), l3 = group_max16(hB, 1, E3);
+          sb[(4 * j) * kCandRows] = l0;
+          sb[(4 * j + 1) * kCandRows] = l1;
+          sb[(4 * j + 2) * kCandRows] = l2;
+          sb[(4 * j + 3) * kCandRows] = l3;
+          const auto f = [](uint32_t u) { return __uint_as_float(u); };
+          vmx = fmaxf(vmx, fmaxf(fmaxf(fmaxf(f(l0.x), f(l0.y)), fmaxf(f(l1.x), f(l1.y))),
+                                 fmaxf(fmaxf(f(l2.x), f(l2.y)), fmaxf(f(l3.x), f(l3.y)))));
+          tmem_ld_wait64(hA);
+        }
+        me.cnt = 4 * seed_tiles;
+        me.vmax = vmx;
+        me.theta = fmaxf(me.theta, cand_seed(me, sm, rloc, kmax));  // dead rows keep +inf
+        me.cnt = 0;
+        me.vmax = -__int_as_float(0x7f800000);
+      }
       int it = 0;
       bool done = false;                        // warp-uniform: this warp's rows cannot gain any more
       for (; it < nit; ++it) {
@@ -394,7 +448,18 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   const int tiles = (int)((x->n + kBM - 1) / kBM);
   const int grid = tiles < sm_count() ? tiles : sm_count();
   const float* cs = getenv("RMIPS_NO_CS") ? nullptr : c.scale_dev;  // dev A/B switch for the C-S exit
-  k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, x->n, x->m, x->kmax, c.cand,
+  // seed pass length: 16 full tiles (8 maxima per tile, 128 slots of two), at least k_max maxima.
+  // Measured (profiles/): -10% contraction on configs[1] (m = 25,000) but +15% on configs[3]
+  // (m = 100,000), where the Cauchy-Schwarz exit ends a user tile after a few dozen tiles and the
+  // 16 repeated tiles are a large share of the work; so no seed pass for m > 32,768.
+  const int nit = (int)((x->m + kBN - 1) / kBN);
+  int seed = (nit >= 32 && nit <= 256) ? 16 : 0;
+  if (const char* e = getenv("RMIPS_SEED_TILES")) {  // dev switch: 0 .. min(32, nit - 1) seed tiles
+    seed = atoi(e);
+    seed = seed < 0 ? 0 : seed > 32 ? 32 : seed > nit - 1 ? nit - 1 : seed;
+  }
+  if (8 * seed < x->kmax) seed = 0;
+  k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, x->n, x->m, x->kmax, seed, c.cand,
                                                c.ccount, c.ovf_list, c.ovf_count, c.tiles_done);
   count_launch();
   return cudaGetLastError();
@@ -407,6 +472,12 @@ cudaError_t build_tc(const BuildCtx& c, cudaStream_t st) {
     // candh.cuh); measured 10% slower than this kernel on configs[1] (the epilogue's TMEM reads
     // and issue, not its latency, bound both)
     const cudaError_t e = build_tcq(c, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  if (getenv("RMIPS_BUILD_8W")) {
+    // experiment switch: 8 epilogue warps splitting each tile's columns, 4-byte quantised entries
+    // (build_tc2.cu); measured 35% slower than this kernel on configs[1]
+    const cudaError_t e = build_tc2(c, st);
     if (e != cudaErrorNotSupported) return e;
   }
   switch (c.idx->dpad) {

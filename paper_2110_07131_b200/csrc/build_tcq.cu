@@ -22,8 +22,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
-#include "candh.cuh"
-#include "candq.cuh"
+#include "candpol.cuh"
 #include "common.cuh"
 #include "internal.h"
 #include "sm100.cuh"
@@ -53,43 +52,6 @@ struct Cfg {
   static constexpr int BAR = CAND + UT * kBM * 128 * 4;  // 128 four-byte candidate slots per row
   static constexpr int TOTAL = BAR + 256 + 1024;  // + alignment slack
   static_assert(TOTAL <= 232448, "shared memory");
-};
-
-// Candidate-filter policies (4-byte entries both): candq.cuh (12-bit quantised bound, 20-bit
-// position: m <= 2^20) and candh.cuh (bf16 bound, 16-bit position: m <= 2^16).
-struct QPol {
-  using Row = QRow;
-  using Buf = QBuf;
-  static constexpr int kSlots = kQSlots;
-  __device__ static Row init(bool live, float smax) { return qrow_init(live, smax); }
-  template <typename F>
-  __device__ static void append(F f, const float (&g4)[8], float E, int pos0, int mi, Row& me, Buf sb, int rr) {
-    qrow_append_chunk(f, g4, E, pos0, mi, me, sb, rr);
-  }
-  __device__ static void maybe_refresh(Row& me, Buf sb, int rr, float e0x2, int kmax) {
-    qrow_maybe_refresh(me, sb, rr, e0x2, kmax);
-  }
-  __device__ static void finish(Row& me, Buf sb, int rr, float e0x2, int kmax, int64_t row, int64_t n, int32_t* cand,
-                                int32_t* ccount, int32_t* ovf_list, int* ovf_count) {
-    qrow_finish(me, sb, rr, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
-  }
-};
-struct HPol {
-  using Row = HRow;
-  using Buf = HBuf;
-  static constexpr int kSlots = kHSlots;
-  __device__ static Row init(bool live, float) { return hrow_init(live); }
-  template <typename F>
-  __device__ static void append(F f, const float (&g4)[8], float E, int pos0, int mi, Row& me, Buf sb, int rr) {
-    hrow_append_chunk(f, g4, E, pos0, mi, me, sb, rr);
-  }
-  __device__ static void maybe_refresh(Row& me, Buf sb, int rr, float e0x2, int kmax) {
-    hrow_maybe_refresh(me, sb, rr, e0x2, kmax);
-  }
-  __device__ static void finish(Row& me, Buf sb, int rr, float e0x2, int kmax, int64_t row, int64_t n, int32_t* cand,
-                                int32_t* ccount, int32_t* ovf_list, int* ovf_count) {
-    hrow_finish(me, sb, rr, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
-  }
 };
 
 // Fast path of one 64-column half (scores of this thread's row): 3-input max trees and one

@@ -141,6 +141,55 @@ static __device__ __noinline__ CandRow cand_refresh(CandRow me, CandSmem sm, int
   return me;
 }
 
+// Seed threshold (build_tc.cu, seed pass): slots [0, me.cnt) of this thread's row hold, in both
+// halves of each entry, lower bounds of the maxima of disjoint item groups (lo = group max of s~
+// minus E, rounded down, so lo <= the true score of a distinct item).  The k_max-th largest lo is
+// therefore a valid lower bound of tau_kmax; this returns the largest level of a 5-pass
+// quaternary search over [min lo, me.vmax] that keeps at least k_max of them (-inf if there are
+// fewer than k_max).
+static __device__ __noinline__ float cand_seed(CandRow me, CandSmem sm, int rloc, int kmax) {
+  const int cn = me.cnt;
+  if (2 * cn < kmax) return -__int_as_float(0x7f800000);
+  sm.assume_shared();
+  const uint2* b = sm.buf + rloc;
+  float m0 = me.vmax, m1 = me.vmax;
+  for (int i = 0; i < cn; ++i) {
+    const uint2 v = b[i * kCandRows];
+    m0 = fminf(m0, __uint_as_float(v.x)), m1 = fminf(m1, __uint_as_float(v.y));
+  }
+  float L = fminf(m0, m1), U2 = me.vmax;
+#pragma unroll 1
+  for (int pass = 0; pass < 5; ++pass) {
+    const float w = U2 - L;
+    const float t1 = fmaf(w, 0.25f, L), t2 = fmaf(w, 0.5f, L), t3 = fmaf(w, 0.75f, L);
+    int a1[4] = {0, 0, 0, 0}, a2[4] = {0, 0, 0, 0}, a3[4] = {0, 0, 0, 0};
+    int i = 0;
+    for (; i + 4 <= cn; i += 4) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint2 e = b[(i + u) * kCandRows];
+        v[2 * u] = __uint_as_float(e.x), v[2 * u + 1] = __uint_as_float(e.y);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a1[u & 3] += v[u] >= t1, a2[u & 3] += v[u] >= t2, a3[u & 3] += v[u] >= t3;
+    }
+    for (; i < cn; ++i) {
+      const uint2 e = b[i * kCandRows];
+      const float v0 = __uint_as_float(e.x), v1 = __uint_as_float(e.y);
+      a1[0] += v0 >= t1, a2[0] += v0 >= t2, a3[0] += v0 >= t3;
+      a1[1] += v1 >= t1, a2[1] += v1 >= t2, a3[1] += v1 >= t3;
+    }
+    const int c1 = (a1[0] + a1[1]) + (a1[2] + a1[3]), c2 = (a2[0] + a2[1]) + (a2[2] + a2[3]),
+              c3 = (a3[0] + a3[1]) + (a3[2] + a3[3]);
+    if (c3 >= kmax) L = t3;
+    else if (c2 >= kmax) L = t2, U2 = t3;
+    else if (c1 >= kmax) L = t1, U2 = t2;
+    else U2 = t1;
+  }
+  return L;
+}
+
 // Append pass of one 32-column chunk (scores via s_of(j), positions pos0 + j), called by the
 // whole warp when any lane's chunk max passed; g4[8] are the 4-column group maxima.  Groups are
 // skipped warp-uniformly; inside a group the 4 slots are computed from a prefix of predicates
@@ -170,6 +219,26 @@ __device__ __forceinline__ void cand_append_chunk(ScoreFn s_of, const float (&g4
   }
   me.cnt = c;
   me.vmax = vmax;
+}
+
+// Branch-free append of one 32-column chunk (dense chunks: no per-group votes); the slot of
+// column j is cnt + #{passing columns < j}.
+template <typename ScoreFn>
+__device__ __forceinline__ void cand_append_flat(ScoreFn s_of, float mx, float E, int pos0, CandRow& me, CandSmem sm,
+                                                 int rloc) {
+  sm.assume_shared();
+  const float thr = fmaxf(__fsub_rd(me.theta, E), -3.402823466e38f);  // padding (-inf) never passes
+  uint2* b = sm.buf + rloc;
+  int c = me.cnt;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float sj = s_of(j);
+    const bool p = sj >= thr;
+    if (p) b[c * kCandRows] = make_uint2(__float_as_uint(__fsub_rd(sj, E)), (uint32_t)(pos0 + j));
+    c += p;
+  }
+  if (mx >= thr) me.vmax = fmaxf(me.vmax, __fsub_rd(mx, E));
+  me.cnt = c;
 }
 
 // After a chunk: if any row of the warp may not have room for another chunk, refresh all.

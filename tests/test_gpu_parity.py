@@ -331,3 +331,26 @@ def test_filter_error_bound_holds():
         b = gpu_sets(U, P, Qy, k, 20, qflags=rmips.RMIPS_FLAG_FORCE_VERIFY)
         assert_same(a, member, U, P, Qy, k, "bound k=%d" % k)
         assert_same(b, member, U, P, Qy, k, "bound/force k=%d" % k)
+
+
+# ---------------------------------------------------------------- build-kernel variants (dev switches)
+
+@pytest.mark.parametrize("env", [{}, {"RMIPS_SEED_TILES": "0"}, {"RMIPS_SEED_TILES": "32"},
+                                 {"RMIPS_SEED_TILES": "3"}, {"RMIPS_BUILD_8W": "1"},
+                                 {"RMIPS_BUILD_8W": "1", "RMIPS_SEED_TILES": "0"}, {"RMIPS_BUILD_TC2": "1"}],
+                         ids=["default", "seed0", "seed32", "seed3", "8w", "8w-seed0", "tcq-ut2"])
+def test_build_variants_bitwise(env, monkeypatch):
+    """Every tensor-core build variant (seed-pass lengths, the 8-warp and two-user-tile kernels)
+    gives the oracle's exact top-k_max lists (tau and ids bitwise) on a sample of users, with
+    m = 6,000 items (47 item tiles, a ragged last tile) and k_max = 50."""
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    U, P = gen.random_instance(77, 20000, 6000, 50, "skewed")
+    idx = rmips.rmips_build_index(_t(U), _t(P), 50)
+    assert idx.build_flags & rmips.RMIPS_BUILD_SIMT == 0
+    sample = np.sort(np.random.default_rng(7).choice(U.shape[0], 600, replace=False))
+    vals, oids = oracle.topk(U[sample], P, 50)
+    _, _, tau, tids = idx.export()
+    assert np.array_equal(tau[:, sample].T, vals)
+    assert np.array_equal(tids[:, sample].T, oids)
+    idx.close()
