@@ -367,21 +367,28 @@ k_exact_row_full(const float* __restrict__ U32, const float* __restrict__ P32, c
 // tb[j][B] = L^j(B) / ||u_first(B)|| rounded down, L^j(B) = min over members tau_j (Eq. 1).
 // Lemma 3 (strict form R1) keeps query q for block B iff ||q|| >= tb (q norm
 // rounded up); the queries of a batch are norm-sorted, so the kept ones are a prefix.
+// One warp per (block B, rank j): the block's kTileU values of column j are read coalesced (lane
+// r reads rows lo + r, lo + r + 32, ...) and min-reduced.
 __global__ void k_blocks(const double* __restrict__ tau, const double* __restrict__ unorm, int64_t n, int kmax,
                          int64_t nblocks, float* __restrict__ tb) {
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= nblocks * kmax) return;
-  int64_t B = idx % nblocks;
-  int j = (int)(idx / nblocks);
-  int64_t lo = B * kTileU, hi = min(n, lo + kTileU);
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= nblocks * kmax) return;
+  const int64_t B = wid % nblocks;
+  const int j = (int)(wid / nblocks);
+  const int64_t lo = B * kTileU, hi = min(n, lo + kTileU);
   double L = CUDART_INF;
-  for (int64_t i = lo; i < hi; ++i) L = fmin(L, tau[(int64_t)j * n + i]);
-  double uf = unorm[lo];
-  float t;
-  if (!(L > 0.0)) t = -CUDART_INF_F;           // L <= 0 (or -inf): ||u|| ||q|| >= 0 >= L, prune nothing
-  else if (uf == 0.0) t = CUDART_INF_F;        // all members are zero vectors: u.q = 0 < L
-  else t = __double2float_rd((L / uf) * (1.0 - 1e-12));
-  tb[(int64_t)j * nblocks + B] = t;
+  for (int64_t i = lo + lane; i < hi; i += 32) L = fmin(L, tau[(int64_t)j * n + i]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) L = fmin(L, __shfl_xor_sync(0xffffffffu, L, o));
+  if (lane == 0) {
+    const double uf = unorm[lo];
+    float t;
+    if (!(L > 0.0)) t = -CUDART_INF_F;           // L <= 0 (or -inf): ||u|| ||q|| >= 0 >= L, prune nothing
+    else if (uf == 0.0) t = CUDART_INF_F;        // all members are zero vectors: u.q = 0 < L
+    else t = __double2float_rd((L / uf) * (1.0 - 1e-12));
+    tb[(int64_t)j * nblocks + B] = t;
+  }
 }
 
 // ------------------------------------------------------------------------------ host driver
@@ -469,7 +476,8 @@ cudaError_t build_fallback(BuildCtx& c, int nrows, double* scratch, int grid, cu
 cudaError_t build_blocks(BuildCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   if (x->n == 0) return cudaSuccess;
-  k_blocks<<<nblk(x->nblocks * x->kmax, 256), 256, 0, st>>>(x->tau, x->unorm, x->n, x->kmax, x->nblocks, x->tb); count_launch();
+  k_blocks<<<nblk(x->nblocks * x->kmax * 32, 256), 256, 0, st>>>(x->tau, x->unorm, x->n, x->kmax, x->nblocks, x->tb);
+  count_launch();
   return cudaGetLastError();
 }
 
