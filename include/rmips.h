@@ -105,6 +105,19 @@ RMIPS_API rmips_status_t rmips_build_index(const float* Q, int64_t n, const floa
 RMIPS_API rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, int64_t m, int32_t d,
                                     int32_t k_max, int32_t build_flags, void* cuda_stream,
                                     rmips_index_t* out);
+/* rmips_build_index_pprime -- Alg. 1 as printed (PAPER.md 267-298): the lists L_i^j are the
+ * k_max largest u_i.p over P' = the first m_prime items of the norm-sorted P (line 6, P:280,
+ * "the first O(k_max) vectors"; SPEC uses m_prime = 2 k_max), so they are LOWER bounds of the
+ * k-th largest over P (Def. 4).  Queries on such an index decide a pair by Lemma 1 (reject
+ * when u.q < L^k), Lemma 2 (accept when u.q >= ||u|| ||p_k||), Cor. 1 at item m_prime
+ * (accept when u.q >= ||u|| ||p_{m_prime+1}||: no item outside P' can beat q), and otherwise
+ * Alg. 2's early-terminating scan over the items after P', started with the count of
+ * P' items that beat q (exact: the list holds P''s exact top k_max).
+ *   m_prime  1 <= m_prime; values >= m build the exact index (same as rmips_build_index_ex)
+ * Other arguments and errors as rmips_build_index_ex. */
+RMIPS_API rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* P, int64_t m, int32_t d,
+                                        int32_t k_max, int64_t m_prime, int32_t build_flags,
+                                        void* cuda_stream, rmips_index_t* out);
 /* Same, with Q and P in HOST memory (copied to the device inside the call). */
 RMIPS_API rmips_status_t rmips_build_index_host(const float* Q, int64_t n, const float* P, int64_t m, int32_t d,
                                       int32_t k_max, void* cuda_stream, rmips_index_t* out);
@@ -137,11 +150,13 @@ RMIPS_API rmips_status_t rmips_query_stats(rmips_index_t idx, rmips_stats_t* out
  *   info[0..9] = n, m, d, k_max, d_pad, block_size, overflow_rows, build_flags,
  *                candidates kept by the build filter (sum over rows),
  *                (128-user tile, item tile) contractions issued by the tensor-core build (0 for the
- *                SIMT build; fewer than all when the Cauchy-Schwarz early exit fired);
- *                info[10..15] reserved, 0
+ *                SIMT build; fewer than all when the Cauchy-Schwarz early exit fired),
+ *                m_prime (items the lists are built over; = m for the exact index);
+ *                info[11..15] reserved, 0
  *   perm_u[n], perm_p[m]: sorted position -> original id (norm descending, ties by id)
  *   tau[k_max * n] fp64 and ids[k_max * n] int32: column-major by rank, users in ORIGINAL
- *   order: tau[j * n + u] = (j+1)-th largest u.p over P, ids = its original item id.
+ *   order: tau[j * n + u] = (j+1)-th largest u.p over P (over P' for a P' index), ids = its
+ *   original item id.
  *   Any of perm_u/perm_p/tau/ids may be NULL to skip it. */
 RMIPS_API rmips_status_t rmips_index_info(rmips_index_t idx, int64_t info[16]);
 RMIPS_API rmips_status_t rmips_index_export(rmips_index_t idx, int64_t* perm_u, int64_t* perm_p, double* tau,

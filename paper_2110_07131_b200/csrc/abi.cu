@@ -158,9 +158,11 @@ const char* rmips_status_string(rmips_status_t s) {
   return "unknown status";
 }
 
-rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, int64_t m, int32_t d, int32_t k_max,
-                                    int32_t build_flags, void* cuda_stream, rmips_index_t* out) {
+rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* P, int64_t m, int32_t d,
+                                        int32_t k_max, int64_t m_prime, int32_t build_flags, void* cuda_stream,
+                                        rmips_index_t* out) {
   if (!out) return fail(RMIPS_ERR_INVALID, "out is NULL");
+  if (m_prime < 1) return fail(RMIPS_ERR_INVALID, "m_prime < 1");
   *out = nullptr;
   if (n < 0 || m < 1 || d < 1) return fail(RMIPS_ERR_INVALID, "need n >= 0, m >= 1, d >= 1");
   if (d > 256) return fail(RMIPS_ERR_INVALID, "d > 256 is not supported");
@@ -171,6 +173,7 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
   retain_pool();
   rmips_index_s* x = new rmips_index_s();
   x->n = n; x->m = m; x->d = d; x->kmax = k_max; x->build_flags = build_flags;
+  x->mprime = m_prime < m ? m_prime : m;
   x->dpad = round_up(d, 64);
   x->pd = round_up(d, 8);
   x->nblocks = (n + kTileU - 1) / kTileU;
@@ -179,6 +182,7 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
   cudaGetDevice(&x->device);
   BuildCtx c;
   c.idx = x;
+  c.mb = x->mprime;
   double* scratch = nullptr;
   PhaseTimer tm((build_flags & RMIPS_BUILD_TIMING) != 0, st);
   try {
@@ -296,6 +300,11 @@ rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, i
   return RMIPS_OK;
 }
 
+rmips_status_t rmips_build_index_ex(const float* Q, int64_t n, const float* P, int64_t m, int32_t d, int32_t k_max,
+                                    int32_t build_flags, void* cuda_stream, rmips_index_t* out) {
+  return rmips_build_index_pprime(Q, n, P, m, d, k_max, m, build_flags, cuda_stream, out);
+}
+
 rmips_status_t rmips_build_index(const float* Q, int64_t n, const float* P, int64_t m, int32_t d, int32_t k_max,
                                  void* cuda_stream, rmips_index_t* out) {
   return rmips_build_index_ex(Q, n, P, m, d, k_max, RMIPS_BUILD_DEFAULT, cuda_stream, out);
@@ -330,7 +339,7 @@ static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cuda
   size_t oQ16 = take((size_t)nsub * kQB * dpad * 2), oqn = take((size_t)nsub * kQB * 4),
          oqe = take((size_t)nsub * kQB * 4), oqs = take((size_t)nsub * 4), oqp = take((size_t)nsub * kQB * 4),
          oqc = take((size_t)nsub * 4), owl = take((size_t)nsub * x->nblocks * 4), oacc = take((size_t)cap * 8),
-         ound = take((size_t)cap * 8),
+         ound = take((size_t)cap * 8), oscn = take((size_t)cap * 4),
          osrt = take((size_t)cap * 8), ocub = take(qcub);
   if (off > x->ws_bytes) {
     if (x->ws) cudaFreeAsync(x->ws, st);
@@ -348,6 +357,7 @@ static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cuda
   c.wlen = reinterpret_cast<int32_t*>(b + owl);
   c.acc = reinterpret_cast<uint64_t*>(b + oacc);
   c.und = reinterpret_cast<uint64_t*>(b + ound);
+  c.scan_cnt = reinterpret_cast<int32_t*>(b + oscn);
   c.acc_sorted = reinterpret_cast<uint64_t*>(b + osrt);
   c.cub_tmp = b + ocub;
   c.cub_bytes = qcub;
@@ -381,6 +391,9 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
   try {
     QueryCtx c;
     c.idx = x; c.q = q_batch; c.b = b; c.k = k; c.flags = flags;
+    // P' index (lists over the first mprime items): the lists only bound tau_k from below, so the
+    // filter may reject (Lemma 1) but never accept; every other pair goes to the exact path
+    if (x->mprime < x->m) c.flags |= RMIPS_FLAG_FORCE_VERIFY;
     c.nsub = (b + kQB - 1) / kQB;
     c.counters = x->d_counters;
     c.flags_dev = x->d_flags;
@@ -510,6 +523,7 @@ rmips_status_t rmips_index_info(rmips_index_t idx, int64_t info[16]) {
   for (int i = 8; i < 16; ++i) info[i] = 0;
   info[8] = idx->cand_total;
   info[9] = idx->tiles_done;
+  info[10] = idx->mprime;
   info[0] = idx->n; info[1] = idx->m; info[2] = idx->d; info[3] = idx->kmax;
   info[4] = idx->dpad; info[5] = kTileU; info[6] = idx->overflow_rows; info[7] = idx->build_flags;
   return RMIPS_OK;

@@ -400,7 +400,7 @@ static cudaError_t launch_build_simt(const BuildCtx& c, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(k_build_simt<DPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_build_simt<DPAD><<<nblk(c.idx->n, 128), 128, smem, st>>>(c.idx->U16, c.idx->P16, c.idx->perr, c.idx->n,
-                                                             c.idx->m, c.idx->kmax, c.cand, c.ccount,
+                                                             c.mb, c.idx->kmax, c.cand, c.ccount,
                                                              c.ovf_list, c.ovf_count); count_launch();
   return cudaGetLastError();
 }
@@ -468,7 +468,7 @@ cudaError_t build_select(BuildCtx& c, cudaStream_t st) {
 cudaError_t build_fallback(BuildCtx& c, int nrows, double* scratch, int grid, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   if (nrows <= 0) return cudaSuccess;
-  k_exact_row_full<<<grid, 256, 0, st>>>(x->U32, x->P32, x->perm_p, x->unu, c.ovf_list, c.ovf_count, x->n, x->m,
+  k_exact_row_full<<<grid, 256, 0, st>>>(x->U32, x->P32, x->perm_p, x->unu, c.ovf_list, c.ovf_count, x->n, c.mb,
                                          x->d, x->pd, x->kmax, scratch, x->tau, x->ids, x->thr); count_launch();
   return cudaGetLastError();
 }

@@ -441,7 +441,7 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   CUtensorMap ta, tb;
   if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM)) return cudaErrorNotSupported;
-  if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)x->m, (uint64_t)x->dpad, kBN)) return cudaErrorNotSupported;
+  if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->dpad, kBN)) return cudaErrorNotSupported;
   const int smem = Smem::TOTAL(KB);
   cudaError_t e = cudaFuncSetAttribute(k_build_tc<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -452,14 +452,14 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   // Measured (profiles/): -10% contraction on configs[1] (m = 25,000) but +15% on configs[3]
   // (m = 100,000), where the Cauchy-Schwarz exit ends a user tile after a few dozen tiles and the
   // 16 repeated tiles are a large share of the work; so no seed pass for m > 32,768.
-  const int nit = (int)((x->m + kBN - 1) / kBN);
+  const int nit = (int)((c.mb + kBN - 1) / kBN);
   int seed = (nit >= 32 && nit <= 256) ? 16 : 0;
   if (const char* e = getenv("RMIPS_SEED_TILES")) {  // dev switch: 0 .. min(32, nit - 1) seed tiles
     seed = atoi(e);
     seed = seed < 0 ? 0 : seed > 32 ? 32 : seed > nit - 1 ? nit - 1 : seed;
   }
   if (8 * seed < x->kmax) seed = 0;
-  k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, x->n, x->m, x->kmax, seed, c.cand,
+  k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, x->n, c.mb, x->kmax, seed, c.cand,
                                                c.ccount, c.ovf_list, c.ovf_count, c.tiles_done);
   count_launch();
   return cudaGetLastError();
@@ -467,7 +467,7 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
 
 cudaError_t build_tc(const BuildCtx& c, cudaStream_t st) {
   if (getenv("RMIPS_DISABLE_TC")) return cudaErrorNotSupported;
-  if (c.idx->dpad == 64 && c.idx->m <= 65536 && getenv("RMIPS_BUILD_TC2")) {
+  if (c.idx->dpad == 64 && c.mb <= 65536 && getenv("RMIPS_BUILD_TC2")) {
     // experiment switch: two user tiles per CTA with 4-byte bf16-bound entries (build_tcq.cu,
     // candh.cuh); measured 10% slower than this kernel on configs[1] (the epilogue's TMEM reads
     // and issue, not its latency, bound both)

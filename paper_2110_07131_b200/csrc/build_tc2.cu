@@ -485,18 +485,18 @@ static cudaError_t launch_tc2(const BuildCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   CUtensorMap ta, tb;
   if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM)) return cudaErrorNotSupported;
-  if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)x->m, (uint64_t)x->dpad, kBN)) return cudaErrorNotSupported;
+  if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->dpad, kBN)) return cudaErrorNotSupported;
   cudaError_t e = cudaFuncSetAttribute(k_build_tc2<Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem2::TOTAL);
   if (e != cudaSuccess) return e;
   const int tiles = (int)((x->n + kBM - 1) / kBM);
   const int grid = tiles < sm_count2() ? tiles : sm_count2();
   const int cs = getenv("RMIPS_NO_CS") ? 0 : 1;  // dev A/B switch for the C-S exit
   // seed pass: at most 32 full tiles (128 maxima fill the float view of the buffer), >= k_max maxima
-  const int nit = (int)((x->m + kBN - 1) / kBN);
+  const int nit = (int)((c.mb + kBN - 1) / kBN);
   int seed = nit >= 16 ? (nit / 4 < 32 ? nit / 4 : 32) : 0;
   if (const char* s = getenv("RMIPS_SEED_TILES")) seed = atoi(s) < seed ? atoi(s) : seed;  // dev switch
   if (4 * seed < x->kmax) seed = 0;
-  k_build_tc2<Pol><<<grid, kThreads, Smem2::TOTAL, st>>>(ta, tb, x->perr, x->pnorm, c.scale_dev, cs, x->n, x->m,
+  k_build_tc2<Pol><<<grid, kThreads, Smem2::TOTAL, st>>>(ta, tb, x->perr, x->pnorm, c.scale_dev, cs, x->n, c.mb,
                                                           x->kmax, seed, c.cand, c.ccount, c.ovf_list, c.ovf_count,
                                                           c.tiles_done);
   count_launch();
@@ -508,7 +508,7 @@ static cudaError_t launch_tc2(const BuildCtx& c, cudaStream_t st) {
 // (build_tc.cu's 8-byte-entry kernel).
 cudaError_t build_tc2(const BuildCtx& c, cudaStream_t st) {
   if (c.idx->dpad != 64 || c.idx->kmax > 64) return cudaErrorNotSupported;
-  if (c.idx->m <= (int64_t)kQPosMask + 1) return launch_tc2<QPol>(c, st);
+  if (c.mb <= (int64_t)kQPosMask + 1) return launch_tc2<QPol>(c, st);
   return cudaErrorNotSupported;
 }
 

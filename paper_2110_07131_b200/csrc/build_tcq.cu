@@ -361,13 +361,13 @@ static cudaError_t launch_tcq(const BuildCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   CUtensorMap ta, tb;
   if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM)) return cudaErrorNotSupported;
-  if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)x->m, (uint64_t)x->dpad, BN)) return cudaErrorNotSupported;
+  if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->dpad, BN)) return cudaErrorNotSupported;
   cudaError_t e = cudaFuncSetAttribute(k_build_tcq<KB, UT, BN, Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
   if (e != cudaSuccess) return e;
   const int groups = (int)(((x->n + kBM - 1) / kBM + UT - 1) / UT);
   const int grid = groups < sm_count_q() ? groups : sm_count_q();
   const int ksteps = (x->d + 15) / 16;  // K steps of 16 that touch real (non-padding) columns
-  k_build_tcq<KB, UT, BN, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tb, x->perr, x->pnorm, c.scale_dev, x->n, x->m,
+  k_build_tcq<KB, UT, BN, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tb, x->perr, x->pnorm, c.scale_dev, x->n, c.mb,
                                                              x->kmax, ksteps, c.cand, c.ccount, c.ovf_list,
                                                              c.ovf_count, c.tiles_done);
   count_launch();
@@ -377,9 +377,9 @@ static cudaError_t launch_tcq(const BuildCtx& c, cudaStream_t st) {
 // d_pad = 128..256, and d_pad = 64 with m <= 2^16 (two user tiles per CTA, bf16-bound entries);
 // other d <= 64 cases use build_tc.cu's kernel.
 cudaError_t build_tcq(const BuildCtx& c, cudaStream_t st) {
-  if (c.idx->m > (int64_t)kQPosMask + 1) return cudaErrorNotSupported;  // packed positions are 20-bit
+  if (c.mb > (int64_t)kQPosMask + 1) return cudaErrorNotSupported;  // packed positions are 20-bit
   switch (c.idx->dpad) {
-    case 64: return c.idx->m <= 65536 ? launch_tcq<1, 2, 128, HPol>(c, st) : cudaErrorNotSupported;
+    case 64: return c.mb <= 65536 ? launch_tcq<1, 2, 128, HPol>(c, st) : cudaErrorNotSupported;
     case 128: return launch_tcq<2, 1, 64, QPol>(c, st);
     case 192: return launch_tcq<3, 1, 64, QPol>(c, st);
     case 256: return launch_tcq<4, 1, 64, QPol>(c, st);

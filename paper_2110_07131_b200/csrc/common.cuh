@@ -109,6 +109,8 @@ inline double filter_c2(int dpad) { return std::ldexp(1.0, -24) * std::sqrt((dou
 // The index (opaque to callers).
 struct rmips_index_s {
   int64_t n = 0, m = 0;
+  int64_t mprime = 0;       // items the top-k_max lists are built over: the first mprime of the
+                            // norm-sorted P (Alg. 1 line 6); mprime = m is the exact index
   int d = 0, dpad = 0, kmax = 0, build_flags = 0;
   int pd = 0;               // P32 row pitch in floats: d rounded up to 8 (whole 32-byte sectors)
   int device = 0;

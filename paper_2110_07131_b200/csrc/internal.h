@@ -19,6 +19,7 @@ inline void count_launch(int k = 1) { g_launches.fetch_add(k, std::memory_order_
 // Scratch of one build call (owned by abi.cu, freed before rmips_build_index returns).
 struct BuildCtx {
   rmips_index_s* idx = nullptr;
+  int64_t mb = 0;                 // items the lists are built over (idx->mprime)
   void* scratch_arena = nullptr;  // the single allocation of the build scratch below
   uint64_t* nkey = nullptr;       // [2][m + n] sort keys in/out: fp64 norm bits, top bit set for items
   int32_t* nval = nullptr;        // [2][m + n] sort values in/out: concatenated index (items first)
@@ -62,6 +63,7 @@ struct QueryCtx {
   unsigned long long* counters = nullptr;  // kNumCounters (+ accepted / undecided list sizes)
   uint64_t* acc = nullptr;       // accepted keys (q_input << 32 | original user id)
   uint64_t* und = nullptr;       // undecided (q_input << 32 | sorted user position)
+  int32_t* scan_cnt = nullptr;   // [cap] P' index: items of P' that beat q, for the scan after P'
   int64_t cap = 0;               // capacity of acc and of und
   int64_t sorted_n = 0;          // keys sorted by query_sort (reserved slots, sentinels last)
   uint64_t* acc_sorted = nullptr;  // (also holds the 32-bit packed keys of the fast output path)

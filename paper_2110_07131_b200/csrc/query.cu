@@ -221,6 +221,56 @@ __global__ void k_exact_decide(const float* __restrict__ q, const float* __restr
   }
 }
 
+// Q4 on a P' index (lists = exact top k_max over the first mprime norm-sorted items, reading
+// NEXT-1 / DESIGN.md §8).  g = dot64(q, u); c' = #{listed j : L^j > g}:
+//   g < L^k                                  -> no   (Lemma 1: k items of P' beat q)
+//   k > m, or g >= ||u|| ||p_k|| (rounded up) -> yes  (Lemma 2)
+//   g >= ||u|| ||p_{mprime+1}||  (rounded up) -> yes  (Cor. 1 at the first item after P': no item
+//                                               outside P' can beat q, and c' < k inside it)
+//   otherwise the pair goes to the scan over the items after P' with beats = c' (exact: P' items
+//   outside the list score <= L^{k_max} <= L^k <= g, so exactly c' items of P' beat q).
+// Decided records are overwritten with the sentinel; undecided ones keep theirs for k_verify_scan.
+__global__ void k_exact_decide_pp(const float* __restrict__ q, const float* __restrict__ U32,
+                                  const double* __restrict__ unorm, const double* __restrict__ pnorm,
+                                  const double* __restrict__ tau, int64_t n, int64_t m, int64_t mprime, int k,
+                                  const int32_t* __restrict__ perm_u, int d, unsigned long long* __restrict__ ctr,
+                                  uint64_t* __restrict__ und_list, int32_t* __restrict__ scan_cnt,
+                                  uint64_t* __restrict__ acc_list, int64_t cap) {
+  const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_UND_TOTAL]);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const double slack = 1.0 + (d + 8) * 2.220446049250313e-16;  // as k_verify_scan's Cor. 1 test
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < total; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool ok = i < total;
+    bool yes = false, scan = false;
+    uint64_t key = 0;
+    uint64_t rec = ok ? und_list[i] : kSentinel;
+    if (rec == kSentinel) ok = false;  // unused reserved slot
+    if (ok) {
+      const uint32_t qin = (uint32_t)(rec >> 32);
+      const int64_t row = (int64_t)(rec & 0xffffffffu);
+      const double g = dot64(q + (int64_t)qin * d, U32 + row * d, d);
+      if (g >= tau[(int64_t)(k - 1) * n + row]) {
+        const double un = unorm[row] * slack;
+        if (k > m || g >= un * pnorm[k - 1] * slack || g >= un * pnorm[mprime] * slack) {
+          yes = true;
+        } else {
+          int c = 0;
+          for (int j = 0; j < k - 1; ++j) c += tau[(int64_t)j * n + row] > g;
+          scan_cnt[i] = c;
+          scan = true;
+        }
+      }
+      key = ((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row];
+      if (!scan) und_list[i] = kSentinel;
+    }
+    warp_count(ok, ctr + C_UNDECIDED);
+    warp_count(yes, ctr + C_EXACT_ACCEPT);
+    warp_append_u64(yes, key, ctr + C_ACCEPTED_TOTAL, acc_list, cap);
+    warp_count(yes, ctr + C_ACC_REAL);
+  }
+}
+
 // ------------------------------------------------------------------------------ Q5
 // Alg. 2 for one undecided pair per warp.  Items are streamed in norm-descending order
 // (Alg. 1 line 5) 32 at a time: the warp stages the 32 item rows in shared memory with
@@ -228,13 +278,16 @@ __global__ void k_exact_decide(const float* __restrict__ q, const float* __restr
 // gamma_j = p_j.u with dot64.  Corollary 1 (yes): u.q >= ||u|| ||p_j|| (rounded up to cover the
 // fp64 rounding of every later gamma) means no later item can beat q.  Corollary 2 (no): once
 // k items have gamma > u.q (the k-th value tau of I exceeds u.q).  Falling off the end: yes (R4).
+// start / beats0: the scan begins at item `start` with beats0[i] items already known to beat q
+// (P' index: start = mprime, beats0 = c' from k_exact_decide_pp); 0 / NULL scans all of P.
 constexpr int kScanWarps = 4;
 constexpr int kScanPitch = 257;  // floats per staged item row (d <= 256), odd => conflict-free
 __global__ void __launch_bounds__(32 * kScanWarps)
 k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const double* __restrict__ unorm,
               const float* __restrict__ P32, const double* __restrict__ pnorm, const int32_t* __restrict__ perm_u,
               int64_t m, int d, int pd, int k, unsigned long long* __restrict__ ctr,
-              const uint64_t* __restrict__ und_list, uint64_t* __restrict__ acc_list, int64_t cap) {
+              const uint64_t* __restrict__ und_list, uint64_t* __restrict__ acc_list, int64_t cap, int64_t start,
+              const int32_t* __restrict__ beats0) {
   extern __shared__ float sp[];  // [kScanWarps][32][kScanPitch]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float* my = sp + (size_t)w * 32 * kScanPitch;
@@ -248,10 +301,10 @@ k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const 
     const float* u = U32 + row * d;
     const double uq = dot64(q + (int64_t)qin * d, u, d);
     const double un = unorm[row] * slack;
-    int beats = 0;
+    int beats = beats0 ? beats0[i] : 0;
     int64_t scanned = 0;
     bool yes = true, decided = false;
-    for (int64_t base = 0; base < m && !decided; base += 32) {
+    for (int64_t base = start; base < m && !decided; base += 32) {
       const int nrow = (int)min((int64_t)32, m - base);
       // Corollary 1 on the first item of the chunk (lane-parallel over the chunk below)
       const float* src = P32 + base * pd;  // rows of pd floats (zero-padded)
@@ -282,7 +335,7 @@ k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const 
     if (lane == 0) {
       atomicAdd(ctr + C_SCANS, 1ull);
       atomicAdd(ctr + C_ITEMS_SCANNED, (unsigned long long)scanned);
-      atomicAdd(ctr + C_UNDECIDED, 1ull);
+      if (!beats0) atomicAdd(ctr + C_UNDECIDED, 1ull);  // (P' index: counted by k_exact_decide_pp)
       if (yes) {
         atomicAdd(ctr + C_EXACT_ACCEPT, 1ull);
         atomicAdd(ctr + C_ACC_REAL, 1ull);
@@ -349,12 +402,22 @@ cudaError_t query_filter_simt(QueryCtx& c, cudaStream_t st) {
 cudaError_t query_exact(QueryCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   if (x->n == 0) return cudaSuccess;
-  if (c.flags & RMIPS_FLAG_VERIFY_SCAN) {
-    size_t smem = (size_t)kScanWarps * 32 * kScanPitch * 4;
+  const size_t smem = (size_t)kScanWarps * 32 * kScanPitch * 4;
+  if (c.flags & RMIPS_FLAG_VERIFY_SCAN) {  // every undecided pair scans all of P (Alg. 2)
     cudaError_t e = cudaFuncSetAttribute(k_verify_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_verify_scan<<<148 * 4, 32 * kScanWarps, smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
-                                                           x->d, x->pd, c.k, c.counters, c.und, c.acc, c.cap); count_launch();
+                                                           x->d, x->pd, c.k, c.counters, c.und, c.acc, c.cap, 0,
+                                                           nullptr); count_launch();
+  } else if (x->mprime < x->m) {  // P' index: Lemmas 1-2 / Cor. 1 per pair, then the scan after P'
+    k_exact_decide_pp<<<148 * 8, 256, 0, st>>>(c.q, x->U32, x->unorm, x->pnorm, x->tau, x->n, x->m, x->mprime, c.k,
+                                               x->perm_u, x->d, c.counters, c.und, c.scan_cnt, c.acc, c.cap);
+    count_launch();
+    cudaError_t e = cudaFuncSetAttribute(k_verify_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_verify_scan<<<148 * 4, 32 * kScanWarps, smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
+                                                           x->d, x->pd, c.k, c.counters, c.und, c.acc, c.cap,
+                                                           x->mprime, c.scan_cnt); count_launch();
   } else {
     k_exact_decide<<<148 * 8, 256, 0, st>>>(c.q, x->U32, x->tau + (int64_t)(c.k - 1) * x->n, x->perm_u, x->d,
                                             c.counters, c.und, c.acc, c.cap); count_launch();

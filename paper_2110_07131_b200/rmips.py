@@ -27,7 +27,7 @@ RMIPS_BUILD_DEFAULT = 0
 RMIPS_BUILD_SIMT = 1
 RMIPS_BUILD_TIMING = 2
 
-EXPORTED = ["rmips_build_index", "rmips_build_index_ex", "rmips_build_index_host", "rmips_query", "rmips_query_ex",
+EXPORTED = ["rmips_build_index", "rmips_build_index_ex", "rmips_build_index_pprime", "rmips_build_index_host", "rmips_query", "rmips_query_ex",
             "rmips_query_host", "rmips_query_stats", "rmips_phase_times", "rmips_index_info", "rmips_index_export", "rmips_free_index",
             "rmips_status_string", "rmips_last_error", "rmips_version"]
 
@@ -57,6 +57,7 @@ def _load() -> ctypes.CDLL:
     pidx = ctypes.POINTER(ctypes.c_void_p)
     lib.rmips_build_index.argtypes = [P, I64, P, I64, I32, I32, VP, pidx]
     lib.rmips_build_index_ex.argtypes = [P, I64, P, I64, I32, I32, I32, VP, pidx]
+    lib.rmips_build_index_pprime.argtypes = [P, I64, P, I64, I32, I32, I64, I32, VP, pidx]
     lib.rmips_build_index_host.argtypes = [P, I64, P, I64, I32, I32, VP, pidx]
     lib.rmips_query.argtypes = [VP, P, I32, I32, P, P, I64, ctypes.POINTER(I64), VP]
     lib.rmips_query_ex.argtypes = [VP, P, I32, I32, I32, P, P, I64, ctypes.POINTER(I64), VP]
@@ -70,7 +71,8 @@ def _load() -> ctypes.CDLL:
     for f in ("rmips_status_string", "rmips_last_error", "rmips_version"):
         getattr(lib, f).restype = ctypes.c_char_p
     lib.rmips_status_string.argtypes = [ctypes.c_int]
-    for f in ("rmips_build_index", "rmips_build_index_ex", "rmips_build_index_host", "rmips_query",
+    for f in ("rmips_build_index", "rmips_build_index_ex", "rmips_build_index_pprime", "rmips_build_index_host",
+              "rmips_query",
               "rmips_query_ex", "rmips_query_host", "rmips_query_stats", "rmips_phase_times", "rmips_index_info", "rmips_index_export"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
@@ -109,7 +111,7 @@ class Index:
         info = (ctypes.c_int64 * 16)()
         _check(lib.rmips_index_info(self.handle, info))
         self.n, self.m, self.d, self.k_max, self.d_pad, self.block_size, self.overflow_rows, self.build_flags, \
-            self.cand_total, self.tiles_done = [int(v) for v in info[:10]]
+            self.cand_total, self.tiles_done, self.m_prime = [int(v) for v in info[:11]]
 
     def close(self):
         if self.handle:
@@ -152,6 +154,19 @@ def rmips_build_index(Q, P, k_max: int, build_flags: int = RMIPS_BUILD_DEFAULT, 
     h = ctypes.c_void_p()
     _check(lib.rmips_build_index_ex(qptr, n, P.data_ptr(), int(P.shape[0]), int(P.shape[1]), int(k_max),
                                     int(build_flags), _stream_ptr(stream), ctypes.byref(h)))
+    return Index(h.value)
+
+
+def rmips_build_index_pprime(Q, P, k_max: int, m_prime: int, build_flags: int = RMIPS_BUILD_DEFAULT,
+                             stream=None) -> Index:
+    """Alg. 1 as printed: lists over the first m_prime norm-sorted items (P'); queries then
+    decide by Lemmas 1-2 and the scan after P' (include/rmips.h)."""
+    P = _dev_f32(P)
+    n = int(Q.shape[0]) if Q is not None else 0
+    qptr = _dev_f32(Q).data_ptr() if n else None
+    h = ctypes.c_void_p()
+    _check(lib.rmips_build_index_pprime(qptr, n, P.data_ptr(), int(P.shape[0]), int(P.shape[1]), int(k_max),
+                                        int(m_prime), int(build_flags), _stream_ptr(stream), ctypes.byref(h)))
     return Index(h.value)
 
 

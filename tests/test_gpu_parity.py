@@ -354,3 +354,60 @@ def test_build_variants_bitwise(env, monkeypatch):
     assert np.array_equal(tau[:, sample].T, vals)
     assert np.array_equal(tids[:, sample].T, oids)
     idx.close()
+
+
+# ---------------------------------------------------------------- P' index (NEXT-1: Alg. 1 as printed)
+
+@pytest.mark.parametrize("name,bf", BUILDS)
+@pytest.mark.parametrize("c", [1, 2, 5])
+def test_cfg0_pprime_parity(cfg0, name, bf, c):
+    """configs[0] with lists over P' = the first c * k_max norm-sorted items: the query path
+    decides by Lemma 1 / Lemma 2 / Cor. 1 and the scan after P', and must give the same sets."""
+    w, member = cfg0
+    idx = rmips.rmips_build_index_pprime(_t(w.U), _t(w.P), 10, c * 10, bf)
+    assert idx.m_prime == c * 10
+    got = gpu_sets(w.U, w.P, w.Qy, 10, 10, idx=idx)
+    assert_same(got, member, w.U, w.P, w.Qy, 10, "cfg0/pprime c=%d/%s" % (c, name))
+    st = idx.stats()
+    assert st["pairs_accepted_fast"] == 0  # the filter never accepts on a P' index
+    assert st["scans"] > 0 and st["items_scanned"] > 0
+    # Alg. 2 over all of P (stress) on the same index agrees
+    off, ids = rmips.rmips_query(idx, _t(w.Qy), 10, rmips.RMIPS_FLAG_VERIFY_SCAN)
+    assert_same(rmips.split_sets(off, ids), member, label="cfg0/pprime scan-all")
+    for k in (1, 3, 7):
+        mk = oracle.rkmips_naive(w.U, w.P, w.Qy, k)
+        assert_same(gpu_sets(w.U, w.P, w.Qy, k, 10, idx=idx), mk, label="cfg0/pprime k=%d" % k)
+    idx.close()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[str(c[0]) for c in CASES])
+@pytest.mark.parametrize("mp", ["1", "2kmax", "m-1"])
+def test_random_instances_pprime(case, mp):
+    seed, n, m, d, kmax, k, dist, nq = case
+    U, P = gen.random_instance(seed, n, m, d, dist)
+    fresh, _ = gen.random_instance(seed + 1000, nq - nq // 2, 1, d, dist)
+    Qy = np.concatenate([P[: nq // 2], fresh])
+    member = oracle.rkmips_naive(U, P, Qy, k)
+    m_prime = {"1": 1, "2kmax": 2 * kmax, "m-1": max(1, m - 1)}[mp]
+    idx = rmips.rmips_build_index_pprime(_t(U), _t(P), kmax, m_prime)
+    got = gpu_sets(U, P, Qy, k, kmax, idx=idx)
+    idx.close()
+    assert_same(got, member, U, P, Qy, k, "case %d/pprime %s" % (seed, mp))
+
+
+def test_cfg1_pprime_sampled():
+    """configs[1] at full size with |P'| = 2 k_max (SPEC's choice): sampled users' memberships in
+    every query's set equal the oracle's (two-phase form over all of P)."""
+    w = gen.make_workload(1)
+    idx = rmips.rmips_build_index_pprime(_t(w.U), _t(w.P), 50, 100)
+    off, ids = rmips.rmips_query(idx, _t(w.Qy), 10)
+    sets = rmips.split_sets(off, ids)
+    st = idx.stats()
+    assert st["scans"] > 0
+    rng = np.random.default_rng(1)
+    sample = np.sort(rng.choice(w.U.shape[0], 1000, replace=False))
+    vals, _ = oracle.topk(w.U[sample], w.P, 50)
+    member = oracle.rkmips_twophase(w.U[sample], vals, w.Qy, 10)
+    for qi in range(w.Qy.shape[0]):
+        assert np.array_equal(np.intersect1d(sets[qi], sample), sample[member[qi]]), qi
+    idx.close()
