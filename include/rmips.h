@@ -88,6 +88,7 @@ typedef struct {
   int64_t result_total;         /* sum over queries of |R(q)| */
   int64_t filter_kernel;        /* 1 = tcgen05 filter (query_tc.cu), 0 = SIMT filter */
   int64_t tiles_scored;         /* (128-user tile, query sub-batch) work items not pruned whole by Lemma 3 */
+  int64_t scan_exact;           /* scanned items re-evaluated in fp64 (inside the scan's fp32 error band) */
 } rmips_stats_t;
 
 /* rmips_build_index -- Alg. 1 (PAPER.md 267-298) with L_i over all of P.

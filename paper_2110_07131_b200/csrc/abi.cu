@@ -448,6 +448,7 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
     S.items_scanned = hc[C_ITEMS_SCANNED];
     S.result_total = hc[C_ACC_REAL];
     S.tiles_scored = hc[C_TILES_SCORED];
+    S.scan_exact = hc[C_SCAN_EXACT];
     const int64_t total = S.result_total;
     const int64_t reserved = (int64_t)hc[C_ACCEPTED_TOTAL];  // >= total: sentinel padding sorts last
     tm->mark();  // 4

@@ -32,6 +32,7 @@ constexpr int kFlagPairOverflow = 2;
 enum Counter {
   C_BLOCK_PAIRS = 0, C_BLOCK_PRUNED, C_SCORED, C_REJECTED, C_ACCEPT_FAST, C_UNDECIDED,
   C_EXACT_ACCEPT, C_SCANS, C_ITEMS_SCANNED, C_ACCEPTED_TOTAL, C_UND_TOTAL, C_TILES_SCORED, C_ACC_REAL,
+  C_SCAN_EXACT,
   kNumCounters
 };
 // C_ACCEPTED_TOTAL / C_UND_TOTAL count RESERVED list slots (the tcgen05 filter reserves in blocks and

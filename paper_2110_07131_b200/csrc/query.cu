@@ -272,69 +272,97 @@ __global__ void k_exact_decide_pp(const float* __restrict__ q, const float* __re
 }
 
 // ------------------------------------------------------------------------------ Q5
-// Alg. 2 for one undecided pair per warp.  Items are streamed in norm-descending order
-// (Alg. 1 line 5) 32 at a time: the warp stages the 32 item rows in shared memory with
-// coalesced 16-byte loads (consecutive sorted rows are contiguous), then lane j evaluates
-// gamma_j = p_j.u with dot64.  Corollary 1 (yes): u.q >= ||u|| ||p_j|| (rounded up to cover the
-// fp64 rounding of every later gamma) means no later item can beat q.  Corollary 2 (no): once
-// k items have gamma > u.q (the k-th value tau of I exceeds u.q).  Falling off the end: yes (R4).
+// Alg. 2 for one undecided pair per warp.  Items are visited in norm-descending order (Alg. 1
+// line 5), 32 per step, lane j taking item base + j straight from the sector-padded P32 rows
+// (consecutive lanes read consecutive rows: one contiguous 32 x pd x 4-byte stream per step).
+// Corollary 1 (yes): u.q >= ||u|| ||p_j|| (both rounded up to cover the fp64 rounding of every
+// later gamma) means no later item can beat q.  Corollary 2 (no): once k items have
+// gamma = p.u > u.q.  Falling off the end: yes (R4).
+// Each gamma is first scored in fp32 (four independent FMA chains over the zero-padded row,
+// u from shared memory) with a rigorous bound |s - dot64(p, u)| <= E = (gamma32(pd/4 + 2) +
+// gamma64(d)) ||p|| ||u|| (rounded up, plus an absolute term for subnormal products); only items
+// with |s - u.q| <= E (or a non-finite s) are re-evaluated with dot64, so every "beats" decision
+// is the exact fp64 one of the oracle (reading R7).
 // start / beats0: the scan begins at item `start` with beats0[i] items already known to beat q
 // (P' index: start = mprime, beats0 = c' from k_exact_decide_pp); 0 / NULL scans all of P.
-constexpr int kScanWarps = 4;
-constexpr int kScanPitch = 257;  // floats per staged item row (d <= 256), odd => conflict-free
+constexpr int kScanWarps = 8;
 __global__ void __launch_bounds__(32 * kScanWarps)
 k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const double* __restrict__ unorm,
               const float* __restrict__ P32, const double* __restrict__ pnorm, const int32_t* __restrict__ perm_u,
               int64_t m, int d, int pd, int k, unsigned long long* __restrict__ ctr,
               const uint64_t* __restrict__ und_list, uint64_t* __restrict__ acc_list, int64_t cap, int64_t start,
               const int32_t* __restrict__ beats0) {
-  extern __shared__ float sp[];  // [kScanWarps][32][kScanPitch]
+  __shared__ __align__(16) float su[kScanWarps][256];  // the pair's u, fp32, zero-padded to pd
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float* my = sp + (size_t)w * 32 * kScanPitch;
+  float* uw = su[w];
   const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_UND_TOTAL]);
   const double slack = 1.0 + (d + 8) * 2.220446049250313e-16;
+  const double n32 = pd / 4 + 2, g32 = n32 * 5.9604644775390625e-08 / (1.0 - n32 * 5.9604644775390625e-08);
+  const double g64 = (d + 2) * 1.1102230246251565e-16 / (1.0 - (d + 2) * 1.1102230246251565e-16);
+  const double efac = (g32 + g64) * slack * slack * (1.0 + 1e-6);
+  const int nq4 = pd / 4;
   for (int64_t i = blockIdx.x * (int64_t)kScanWarps + w; i < total; i += (int64_t)gridDim.x * kScanWarps) {
-    uint64_t rec = und_list[i];
-    if (rec == kSentinel) continue;  // unused reserved slot (warp-uniform: one record per warp)
-    uint32_t qin = (uint32_t)(rec >> 32);
-    int64_t row = (int64_t)(rec & 0xffffffffu);
+    const uint64_t rec = und_list[i];
+    if (rec == kSentinel) continue;  // decided / unused slot (warp-uniform: one record per warp)
+    const uint32_t qin = (uint32_t)(rec >> 32);
+    const int64_t row = (int64_t)(rec & 0xffffffffu);
     const float* u = U32 + row * d;
+    __syncwarp();
+    for (int t = lane; t < pd; t += 32) uw[t] = t < d ? __ldg(u + t) : 0.f;
+    __syncwarp();
     const double uq = dot64(q + (int64_t)qin * d, u, d);
-    const double un = unorm[row] * slack;
+    const double un = unorm[row];
+    const double unc = un * slack;
     int beats = beats0 ? beats0[i] : 0;
-    int64_t scanned = 0;
+    int64_t scanned = 0, exact = 0;
     bool yes = true, decided = false;
     for (int64_t base = start; base < m && !decided; base += 32) {
       const int nrow = (int)min((int64_t)32, m - base);
-      // Corollary 1 on the first item of the chunk (lane-parallel over the chunk below)
-      const float* src = P32 + base * pd;  // rows of pd floats (zero-padded)
-      __syncwarp();
-      for (int e = lane; e < nrow * pd; e += 32) my[(e / pd) * kScanPitch + (e % pd)] = __ldg(src + e);
-      __syncwarp();
       const int64_t j = base + lane;
-      bool in = lane < nrow;
-      bool cor1 = in && (uq >= un * pnorm[j] * slack);
-      uint32_t ycut = __ballot_sync(0xffffffffu, cor1);   // first lane where Cor. 1 fires
-      int lim = ycut ? (__ffs(ycut) - 1) : nrow;
-      bool eval = lane < lim;
+      const bool in = lane < nrow;
+      const double pn = in ? pnorm[j] : 0.0;
+      const bool cor1 = in && (uq >= unc * pn * slack);
+      const uint32_t ycut = __ballot_sync(0xffffffffu, cor1);  // first lane where Cor. 1 fires
+      const int lim = ycut ? (__ffs(ycut) - 1) : nrow;
       bool beat = false;
-      if (eval) {
-        double g = 0.0;
-        const float* pr = my + lane * kScanPitch;
-        for (int t = 0; t < d; ++t) g = __fma_rn((double)pr[t], (double)__ldg(u + t), g);
-        beat = g > uq;
+      if (lane < lim) {
+        const float4* pr = reinterpret_cast<const float4*>(P32 + j * pd);
+        const float4* u4 = reinterpret_cast<const float4*>(uw);
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 4
+        for (int t = 0; t < nq4; ++t) {
+          const float4 x = __ldg(pr + t), y = u4[t];
+          a0 = fmaf(x.x, y.x, a0);
+          a1 = fmaf(x.y, y.y, a1);
+          a2 = fmaf(x.z, y.z, a2);
+          a3 = fmaf(x.w, y.w, a3);
+        }
+        const float s = (a0 + a1) + (a2 + a3);
+        const double E = efac * pn * un + 1e-40;
+        const double sd = (double)s;
+        if (isfinite(s) && sd - E > uq) {
+          beat = true;
+        } else if (!(isfinite(s) && sd + E <= uq)) {  // inside the band: the exact fp64 value
+          double g = 0.0;
+          const float* prf = P32 + j * pd;
+          for (int t = 0; t < d; ++t) g = __fma_rn((double)__ldg(prf + t), (double)uw[t], g);
+          beat = g > uq;
+          ++exact;
+        }
       }
       scanned += lim;
-      uint32_t bb = __ballot_sync(0xffffffffu, beat);
+      const uint32_t bb = __ballot_sync(0xffffffffu, beat);
       // Alg. 2 visits items in order: the k-th beat (if any) at lane position decides "no"
-      int nb = __popc(bb);
+      const int nb = __popc(bb);
       if (beats + nb >= k) { yes = false; decided = true; }
       else if (ycut) { yes = true; decided = true; }
       beats += nb;
     }
+    for (int o = 16; o; o >>= 1) exact += __shfl_xor_sync(0xffffffffu, exact, o);
     if (lane == 0) {
       atomicAdd(ctr + C_SCANS, 1ull);
       atomicAdd(ctr + C_ITEMS_SCANNED, (unsigned long long)scanned);
+      atomicAdd(ctr + C_SCAN_EXACT, (unsigned long long)exact);
       if (!beats0) atomicAdd(ctr + C_UNDECIDED, 1ull);  // (P' index: counted by k_exact_decide_pp)
       if (yes) {
         atomicAdd(ctr + C_EXACT_ACCEPT, 1ull);
@@ -402,20 +430,15 @@ cudaError_t query_filter_simt(QueryCtx& c, cudaStream_t st) {
 cudaError_t query_exact(QueryCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   if (x->n == 0) return cudaSuccess;
-  const size_t smem = (size_t)kScanWarps * 32 * kScanPitch * 4;
   if (c.flags & RMIPS_FLAG_VERIFY_SCAN) {  // every undecided pair scans all of P (Alg. 2)
-    cudaError_t e = cudaFuncSetAttribute(k_verify_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_verify_scan<<<148 * 4, 32 * kScanWarps, smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
+    k_verify_scan<<<148 * 8, 32 * kScanWarps, 0, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
                                                            x->d, x->pd, c.k, c.counters, c.und, c.acc, c.cap, 0,
                                                            nullptr); count_launch();
   } else if (x->mprime < x->m) {  // P' index: Lemmas 1-2 / Cor. 1 per pair, then the scan after P'
     k_exact_decide_pp<<<148 * 8, 256, 0, st>>>(c.q, x->U32, x->unorm, x->pnorm, x->tau, x->n, x->m, x->mprime, c.k,
                                                x->perm_u, x->d, c.counters, c.und, c.scan_cnt, c.acc, c.cap);
     count_launch();
-    cudaError_t e = cudaFuncSetAttribute(k_verify_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_verify_scan<<<148 * 4, 32 * kScanWarps, smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
+    k_verify_scan<<<148 * 8, 32 * kScanWarps, 0, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
                                                            x->d, x->pd, c.k, c.counters, c.und, c.acc, c.cap,
                                                            x->mprime, c.scan_cnt); count_launch();
   } else {

@@ -42,7 +42,7 @@ class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in (
         "queries", "block_query_pairs", "block_query_pruned", "pairs_scored", "pairs_rejected",
         "pairs_accepted_fast", "pairs_undecided", "pairs_exact_accepted", "scans", "items_scanned",
-        "result_total", "filter_kernel", "tiles_scored")]
+        "result_total", "filter_kernel", "tiles_scored", "scan_exact")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
