@@ -47,7 +47,7 @@ typedef enum {
   RMIPS_OK = 0,
   RMIPS_ERR_INVALID = 1,   /* null pointer, n < 0, m < 1, d < 1, b < 0, bad flags */
   RMIPS_ERR_NONFINITE = 2, /* a NaN/Inf in Q, P or a query vector */
-  RMIPS_ERR_K_RANGE = 3,   /* k < 1, k_max < 1, k > k_max (rebuild with a larger k_max) */
+  RMIPS_ERR_K_RANGE = 3,   /* k < 1, k_max < 1, or k > k_max with RMIPS_FLAG_NO_EXTEND */
   RMIPS_ERR_CAPACITY = 4,  /* result ids exceed `capacity`; *total_out and offsets hold the needed size */
   RMIPS_ERR_CUDA = 5,      /* a CUDA runtime error (message via rmips_last_error) */
   RMIPS_ERR_OOM = 6        /* device allocation failed */
@@ -62,7 +62,8 @@ enum {
   RMIPS_FLAG_FORCE_VERIFY = 4,  /* stress mode: every pair that Lemma 1 does not reject goes to the
                                    undecided path (with VERIFY_SCAN: through the scan kernel) */
   RMIPS_FLAG_SIMT = 8,          /* use the SIMT (CUDA-core) filter kernels instead of tcgen05 */
-  RMIPS_FLAG_TIMING = 16        /* record per-phase CUDA-event times (rmips_phase_times) */
+  RMIPS_FLAG_TIMING = 16,       /* record per-phase CUDA-event times (rmips_phase_times) */
+  RMIPS_FLAG_NO_EXTEND = 32     /* k > k_max fails with RMIPS_ERR_K_RANGE instead of extending the index */
 };
 
 /* Per-index build options (rmips_build_index_ex). */
@@ -127,7 +128,11 @@ RMIPS_API rmips_status_t rmips_build_index_host(const float* Q, int64_t n, const
  *   idx        index from rmips_build_index
  *   q_batch    device, b x d fp32 query vectors (may be NULL iff b == 0)
  *   b          number of queries, >= 0 (any size; processed internally in tiles of 256)
- *   k          1 <= k <= k_max
+ *   k          k >= 1.  k > k_max first EXTENDS the index in place to k_max = k (the paper's
+ *              "re-builds the data structures"): the lists, the block
+ *              table and the candidate filter are rebuilt from the index's own sorted operands
+ *              (no caller rebuild; the cost of one build without its prep phase).  With
+ *              RMIPS_FLAG_NO_EXTEND it fails with RMIPS_ERR_K_RANGE instead.
  *   offsets    device, b + 1 int64: query i's users are user_ids[offsets[i] .. offsets[i+1])
  *   user_ids   device, capacity int32: 0-based ORIGINAL row indices of Q, ascending per query
  *   capacity   number of int32 slots in user_ids

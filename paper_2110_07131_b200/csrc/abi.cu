@@ -123,6 +123,8 @@ thread_local Pinned g_pin;
 void free_index_arrays(rmips_index_s* x, cudaStream_t st) {
   if (x->arena) cudaFreeAsync(x->arena, st);  // every index array lives in the arena
   x->arena = nullptr;
+  if (x->list_arena) cudaFreeAsync(x->list_arena, st);
+  x->list_arena = nullptr;
   x->perm_u = x->perm_p = nullptr;
   x->unorm = x->pnorm = nullptr;
   x->unu = x->perr = x->U32 = x->P32 = x->thr = x->tb = nullptr;
@@ -137,6 +139,86 @@ void free_index_arrays(rmips_index_s* x, cudaStream_t st) {
 }
 
 int round_up(int v, int a) { return (v + a - 1) / a * a; }
+
+int fallback_grid(int64_t m) {
+  const int64_t cap = ((int64_t)256 << 20) / (8 * (m > 0 ? m : 1));
+  return (int)(cap < 1 ? 1 : cap > 148 * 4 ? 148 * 4 : cap);
+}
+
+// NEXT-2 ("re-builds the data structures"): a query with k > k_max extends the
+// index in place to k_max' = k.  The norm-sorted, converted operands are reused; only B4-B6 run
+// again (contraction + candidate filter, exact select + fallback, block table) into new list
+// arrays, stream-ordered, with no host synchronisation.
+void extend_lists(rmips_index_s* x, int kmax_new, cudaStream_t st) {
+  const int64_t n = x->n, m = x->m;
+  Arena la;
+  const size_t o_tau = la.take<double>((int64_t)kmax_new * n), o_ids = la.take<int32_t>((int64_t)kmax_new * n),
+               o_thr = la.take<float>((int64_t)kmax_new * n), o_tb = la.take<float>((int64_t)kmax_new * x->nblocks);
+  void* larena = nullptr;
+  CK(cudaMallocAsync(&larena, la.off, st));
+  BuildCtx c;
+  c.idx = x;
+  c.mb = x->mprime;
+  const int fb_grid = fallback_grid(m);
+  Arena sa;
+  const size_t o_sc = sa.take<float>(4), o_cand = sa.take<int32_t>(n * kCand), o_cc = sa.take<int32_t>(n),
+               o_ovl = sa.take<int32_t>(n), o_ovc = sa.take<int>(1), o_ct = sa.take<unsigned long long>(2),
+               o_scr = sa.take<double>((int64_t)fb_grid * m);
+  void* sarena = nullptr;
+  try {
+    CK(cudaMallocAsync(&sarena, sa.off, st));
+  } catch (...) {
+    cudaFreeAsync(larena, st);
+    throw;
+  }
+  char* S = static_cast<char*>(sarena);
+  c.scale_dev = reinterpret_cast<float*>(S + o_sc);
+  c.cand = reinterpret_cast<int32_t*>(S + o_cand);
+  c.ccount = reinterpret_cast<int32_t*>(S + o_cc);
+  c.ovf_list = reinterpret_cast<int32_t*>(S + o_ovl);
+  c.ovf_count = reinterpret_cast<int*>(S + o_ovc);
+  c.cand_total = reinterpret_cast<unsigned long long*>(S + o_ct);
+  c.tiles_done = c.cand_total + 1;
+  double* scratch = reinterpret_cast<double*>(S + o_scr);
+  c.scratch_arena = sarena;
+  float* hs = g_pin.get<float>();
+  hs[0] = x->pscale;
+  CK(cudaMemcpyAsync(c.scale_dev, hs, sizeof(float), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(c.ovf_count, 0, sizeof(int), st));
+  CK(cudaMemsetAsync(c.cand_total, 0, 2 * sizeof(unsigned long long), st));
+  char* L = static_cast<char*>(larena);
+  double* old_tau = x->tau;
+  int32_t* old_ids = x->ids;
+  float *old_thr = x->thr, *old_tb = x->tb;
+  const int old_kmax = x->kmax;
+  x->tau = reinterpret_cast<double*>(L + o_tau);
+  x->ids = reinterpret_cast<int32_t*>(L + o_ids);
+  x->thr = reinterpret_cast<float*>(L + o_thr);
+  x->tb = reinterpret_cast<float*>(L + o_tb);
+  x->kmax = kmax_new;
+  try {
+    cudaError_t e = cudaErrorNotSupported;
+    if (!(x->build_flags & RMIPS_BUILD_SIMT)) e = build_tc(c, st);
+    if (e == cudaErrorNotSupported) {
+      cudaGetLastError();
+      e = build_simt(c, st);
+    }
+    CK(e);
+    CK(build_select(c, st));
+    CK(build_fallback(c, 1, scratch, fb_grid, st));
+    CK(build_blocks(c, st));
+  } catch (...) {
+    x->tau = old_tau, x->ids = old_ids, x->thr = old_thr, x->tb = old_tb, x->kmax = old_kmax;
+    cudaFreeAsync(sarena, st);
+    cudaFreeAsync(larena, st);
+    throw;
+  }
+  cudaFreeAsync(sarena, st);
+  if (x->list_arena) cudaFreeAsync(x->list_arena, st);  // (the first lists stay in the main arena)
+  x->list_arena = larena;
+  x->cand_total = -1;  // not read back (no host synchronisation)
+  x->tiles_done = -1;
+}
 
 }  // namespace
 
@@ -215,7 +297,8 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
     x->tb = reinterpret_cast<float*>(A + o_tb);
     Arena sa;
     c.cub_bytes = build_cub_bytes(n, m);
-    const int fb_grid = 16;
+    // exact-fallback CTAs (each with m fp64 of scratch): up to 4 per SM, scratch <= 256 MB
+    const int fb_grid = fallback_grid(m);
     const size_t o_key = sa.take<uint64_t>(2 * (m + n)), o_val = sa.take<int32_t>(2 * (m + n)),
                  o_max = sa.take<unsigned int>(4), o_cub = sa.take<unsigned char>((int64_t)c.cub_bytes),
                  o_cand = sa.take<int32_t>(n * kCand), o_cc = sa.take<int32_t>(n), o_ovl = sa.take<int32_t>(n),
@@ -372,8 +455,9 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
   if (b < 0 || capacity < 0) return fail(RMIPS_ERR_INVALID, "b < 0 or capacity < 0");
   if (b > 0 && (!q_batch || !offsets)) return fail(RMIPS_ERR_INVALID, "NULL q_batch or offsets");
   if (capacity > 0 && !user_ids) return fail(RMIPS_ERR_INVALID, "NULL user_ids with capacity > 0");
-  if (k < 1 || k > idx->kmax) return fail(RMIPS_ERR_K_RANGE, "k outside [1, k_max]");
-  if (flags & ~(RMIPS_FLAG_NO_BLOCKS | RMIPS_FLAG_VERIFY_SCAN | RMIPS_FLAG_FORCE_VERIFY | RMIPS_FLAG_SIMT | RMIPS_FLAG_TIMING))
+  if (k < 1) return fail(RMIPS_ERR_K_RANGE, "k < 1");
+  if (k > idx->kmax && (flags & RMIPS_FLAG_NO_EXTEND)) return fail(RMIPS_ERR_K_RANGE, "k > k_max");
+  if (flags & ~(RMIPS_FLAG_NO_EXTEND | RMIPS_FLAG_NO_BLOCKS | RMIPS_FLAG_VERIFY_SCAN | RMIPS_FLAG_FORCE_VERIFY | RMIPS_FLAG_SIMT | RMIPS_FLAG_TIMING))
     return fail(RMIPS_ERR_INVALID, "unknown flag bits");
   rmips_index_s* x = idx;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
@@ -389,6 +473,7 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
     return RMIPS_OK;
   }
   try {
+    if (k > x->kmax) extend_lists(x, k, st);  // NEXT-2: k_max' = k, in place
     QueryCtx c;
     c.idx = x; c.q = q_batch; c.b = b; c.k = k; c.flags = flags;
     // P' index (lists over the first mprime items): the lists only bound tau_k from below, so the

@@ -141,6 +141,7 @@ struct rmips_index_s {
   float* tb = nullptr;         // [kmax][nblocks] Lemma 3: L^j(B) / ||u_first(B)||, rounded down
 
   void* arena = nullptr;       // the single allocation every array above lives in
+  void* list_arena = nullptr;  // tau / ids / thr / tb after an in-place extension of k_max (NEXT-2)
   cudaStream_t last_stream = nullptr;  // stream of the last call (rmips_free_index frees on it)
   // query workspace (grown on demand)
   void* ws = nullptr;

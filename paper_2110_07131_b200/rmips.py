@@ -23,6 +23,7 @@ RMIPS_FLAG_VERIFY_SCAN = 2
 RMIPS_FLAG_FORCE_VERIFY = 4
 RMIPS_FLAG_SIMT = 8
 RMIPS_FLAG_TIMING = 16
+RMIPS_FLAG_NO_EXTEND = 32
 RMIPS_BUILD_DEFAULT = 0
 RMIPS_BUILD_SIMT = 1
 RMIPS_BUILD_TIMING = 2
@@ -124,8 +125,15 @@ class Index:
         except Exception:
             pass
 
+    def refresh_info(self):
+        """Re-read the index header (k_max grows when a query with k > k_max extended the index)."""
+        info = (ctypes.c_int64 * 16)()
+        _check(lib.rmips_index_info(self.handle, info))
+        self.k_max = int(info[3])
+
     def export(self):
         """(perm_u, perm_p, tau [k_max, n] fp64, ids [k_max, n] int32), users in ORIGINAL order."""
+        self.refresh_info()
         pu = np.empty(self.n, np.int64)
         pp = np.empty(self.m, np.int64)
         tau = np.empty((self.k_max, self.n), np.float64)

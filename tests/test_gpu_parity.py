@@ -188,7 +188,10 @@ def test_errors_k_range_nonfinite_capacity():
     U, P = gen.random_instance(15, 100, 30, 8)
     idx = rmips.rmips_build_index(_t(U), _t(P), 5)
     with pytest.raises(rmips.RmipsError) as e:
-        rmips.rmips_query(idx, _t(P[:2]), 6)
+        rmips.rmips_query(idx, _t(P[:2]), 6, rmips.RMIPS_FLAG_NO_EXTEND)
+    assert e.value.status == rmips.RMIPS_ERR_K_RANGE
+    with pytest.raises(rmips.RmipsError) as e:
+        rmips.rmips_query(idx, _t(P[:2]), 0)
     assert e.value.status == rmips.RMIPS_ERR_K_RANGE
     bad = P[:2].copy()
     bad[1, 3] = np.nan
@@ -410,4 +413,27 @@ def test_cfg1_pprime_sampled():
     member = oracle.rkmips_twophase(w.U[sample], vals, w.Qy, 10)
     for qi in range(w.Qy.shape[0]):
         assert np.array_equal(np.intersect1d(sets[qi], sample), sample[member[qi]]), qi
+    idx.close()
+
+
+# ---------------------------------------------------------------- NEXT-2: k > k_max extends the index
+
+@pytest.mark.parametrize("pp", [0, 2])
+def test_k_beyond_kmax_extends_index(cfg0, pp):
+    """configs[0] built with k_max = 4 (exact and P' indexes); queries with k = 7, 10, 25 extend the
+    index in place and must give the oracle's sets; the extended lists equal the
+    oracle's exact top-k lists bit for bit (exact index)."""
+    w, member10 = cfg0
+    if pp:
+        idx = rmips.rmips_build_index_pprime(_t(w.U), _t(w.P), 4, pp * 4)
+    else:
+        idx = rmips.rmips_build_index(_t(w.U), _t(w.P), 4)
+    for k in (7, 10, 25, 3):
+        member = member10 if k == 10 else oracle.rkmips_naive(w.U, w.P, w.Qy, k)
+        assert_same(gpu_sets(w.U, w.P, w.Qy, k, 4, idx=idx), member, label="extend k=%d pp=%d" % (k, pp))
+    if not pp:
+        _, _, tau, ids = idx.export()
+        assert idx.k_max == 25
+        vals, oids = oracle.topk(w.U, w.P, 25)
+        assert np.array_equal(tau.T, vals) and np.array_equal(ids.T, oids)
     idx.close()
