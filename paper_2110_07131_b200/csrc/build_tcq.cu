@@ -205,47 +205,60 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_f16_f32(kBM, BN);
-      unsigned long long tiles_issued = 0;  // (user tile, item tile) contractions issued
-      int stage = 0, as = 0;
-      uint32_t ph = 0, aph = 0;
-      int t = 0;
-      for (int gr = blockIdx.x; gr < num_groups; gr += gridDim.x, ++t) {
-        mbar_wait_sleep(BAR(A_FULL), t & 1);
+    // The whole warp runs the loop (warp-uniform state, descriptors in uniform registers); the
+    // elected lane issues.  The K loop is unrolled to its compile-time bound 4 KB with the runtime
+    // ksteps as a predicate, and every descriptor is the stage's base descriptor plus a constant
+    // (K advance of 16 fp16 = 32 bytes = 2 in the 16-byte address field; K-block = tile / 16).
+    constexpr uint32_t idesc = idesc_f16_f32(kBM, BN);
+    unsigned long long tiles_issued = 0;  // (user tile, item tile) contractions issued
+    int stage = 0, as = 0;
+    uint32_t ph = 0, aph = 0;
+    int t = 0;
+    for (int gr = blockIdx.x; gr < num_groups; gr += gridDim.x, ++t) {
+      mbar_wait_sleep(BAR(A_FULL), t & 1);
+      tc_fence_after();
+      for (int it = 0; it < nit; ++it) {
+        mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
+        mbar_wait_sleep(BAR(B_FULL + stage), ph);
         tc_fence_after();
-        for (int it = 0; it < nit; ++it) {
-          mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
-          mbar_wait_sleep(BAR(B_FULL + stage), ph);
-          tc_fence_after();
-          if (stage_end[stage] == t + 1) {  // the producer ended this group: forward the marker
+        if (stage_end[stage] == t + 1) {  // the producer ended this group: forward the marker
+          if (elect_one()) {
             mbar_arrive(BAR(B_EMPTY + stage));
             acc_end[as] = t + 1;
             mbar_arrive(BAR(ACC_FULL + as));
-            if (++stage == NST) stage = 0, ph ^= 1;
-            if (++as == NACC) as = 0, aph ^= 1;
-            break;
           }
+          __syncwarp();
+          if (++stage == NST) stage = 0, ph ^= 1;
+          if (++as == NACC) as = 0, aph ^= 1;
+          break;
+        }
+        const uint64_t bdesc = sdesc_sw128(sB + stage * KB * C::B_TILE);
+        if (elect_one()) {
 #pragma unroll
           for (int u = 0; u < UT; ++u) {
             const uint32_t d = tmem + as * C::ACC_COLS + u * BN;
-            for (int ks = 0; ks < ksteps; ++ks) {  // K steps of 16 (zero padding beyond d skipped)
-              const int kb = ks >> 2, kk = ks & 3;
-              const uint32_t a0 = sA + (u * KB + kb) * kUTile;
-              const uint32_t b0 = sB + (stage * KB + kb) * C::B_TILE;
-              mma_f16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, ks != 0);
+            const uint64_t adesc = sdesc_sw128(sA + u * KB * kUTile);
+#pragma unroll
+            for (int ks = 0; ks < 4 * KB; ++ks) {  // K steps of 16 (zero padding beyond d skipped)
+              if (ks < ksteps) {
+                const int kb = ks >> 2, kk = ks & 3;
+                mma_f16(d, adesc + (uint64_t)((kb * kUTile + kk * 32) >> 4),
+                        bdesc + (uint64_t)((kb * C::B_TILE + kk * 32) >> 4), idesc, ks != 0);
+              }
             }
           }
           mma_commit(BAR(B_EMPTY + stage));
           mma_commit(BAR(ACC_FULL + as));
-          tiles_issued += UT;
-          if (++stage == NST) stage = 0, ph ^= 1;
-          if (++as == NACC) as = 0, aph ^= 1;
         }
-        mma_commit(BAR(A_EMPTY));
+        __syncwarp();
+        tiles_issued += UT;
+        if (++stage == NST) stage = 0, ph ^= 1;
+        if (++as == NACC) as = 0, aph ^= 1;
       }
-      atomicAdd(tiles_done, (unsigned long long)tiles_issued);
+      if (elect_one()) mma_commit(BAR(A_EMPTY));
+      __syncwarp();
     }
+    if (lane == 0) atomicAdd(tiles_done, (unsigned long long)tiles_issued);
   } else {
     // ------------------------------------------------ epilogue: one thread per user row
     // The 64-column halves of an item tile are software-pipelined: the TMEM load of the next half
