@@ -207,46 +207,54 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_f16_f32(kBM, kBN);
-      unsigned long long tiles_issued = 0;  // (user tile, item tile) contractions issued
-      int stage = 0, as = 0;
-      uint32_t ph = 0, aph = 0;
-      int t = 0;
-      for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
-        mbar_wait_sleep(BAR(A_FULL), t & 1);
+    // The whole warp runs the loop (warp-uniform state: descriptors in uniform registers); the
+    // elected lane issues the tcgen05 instructions (build_tcq.cu, same scheme).
+    constexpr uint32_t idesc = idesc_f16_f32(kBM, kBN);
+    unsigned long long tiles_issued = 0;  // (user tile, item tile) contractions issued
+    int stage = 0, as = 0;
+    uint32_t ph = 0, aph = 0;
+    int t = 0;
+    const uint64_t adesc = sdesc_sw128(sA);
+    for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
+      mbar_wait_sleep(BAR(A_FULL), t & 1);
+      tc_fence_after();
+      for (int j = 0; j < seed_tiles + nit; ++j) {
+        mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
+        mbar_wait_sleep(BAR(B_FULL + stage), ph);
         tc_fence_after();
-        for (int j = 0; j < seed_tiles + nit; ++j) {
-          mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
-          mbar_wait_sleep(BAR(B_FULL + stage), ph);
-          tc_fence_after();
-          if (stage_end[stage] == t + 1) {  // the producer ended this user tile: forward the marker
+        if (stage_end[stage] == t + 1) {  // the producer ended this user tile: forward the marker
+          if (elect_one()) {
             mbar_arrive(BAR(B_EMPTY + stage));
             acc_end[as] = t + 1;
             mbar_arrive(BAR(ACC_FULL + as));
-            if (++stage == kStages) stage = 0, ph ^= 1;
-            if (++as == kAcc) as = 0, aph ^= 1;
-            break;
           }
-          const uint32_t d = tmem + as * kBN;
+          __syncwarp();
+          if (++stage == kStages) stage = 0, ph ^= 1;
+          if (++as == kAcc) as = 0, aph ^= 1;
+          break;
+        }
+        const uint32_t d = tmem + as * kBN;
+        const uint64_t bdesc = sdesc_sw128(sB + stage * KB * kTileBytes);
+        if (elect_one()) {
 #pragma unroll
           for (int kb = 0; kb < KB; ++kb) {
-            const uint32_t a0 = sA + kb * kTileBytes;
-            const uint32_t b0 = sB + (stage * KB + kb) * kTileBytes;
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              mma_f16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < 4; ++kk)  // K advance: 32 bytes = 2 in the 16-byte address field
+              mma_f16(d, adesc + (uint64_t)((kb * kTileBytes + kk * 32) >> 4),
+                      bdesc + (uint64_t)((kb * kTileBytes + kk * 32) >> 4), idesc, (kb | kk) != 0);
           }
           mma_commit(BAR(B_EMPTY + stage));
           mma_commit(BAR(ACC_FULL + as));
-          tiles_issued += j >= seed_tiles;  // the seed pass repeats tiles: not counted
-          if (++stage == kStages) stage = 0, ph ^= 1;
-          if (++as == kAcc) as = 0, aph ^= 1;
         }
-        mma_commit(BAR(A_EMPTY));
+        __syncwarp();
+        tiles_issued += j >= seed_tiles;  // the seed pass repeats tiles: not counted
+        if (++stage == kStages) stage = 0, ph ^= 1;
+        if (++as == kAcc) as = 0, aph ^= 1;
       }
-      atomicAdd(tiles_done, (unsigned long long)tiles_issued);
+      if (elect_one()) mma_commit(BAR(A_EMPTY));
+      __syncwarp();
     }
+    if (lane == 0) atomicAdd(tiles_done, (unsigned long long)tiles_issued);
   } else {
     // ------------------------------------------------ epilogue: one thread per user row
     // Half tiles (64 columns) are software-pipelined: the TMEM load of the next half (of this

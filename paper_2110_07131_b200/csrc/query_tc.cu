@@ -312,48 +312,56 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      int stage = 0, as = 0, cur_s = -1, nq = 0;
-      uint32_t ph = 0, aph = 0;
-      int s, t;
-      first_item(s, t);
-      for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x, next_item(s, t)) {
-        const int len = __ldg(wlen + w);
-        if (len == 0) continue;
-        if (s != cur_s) {
-          if (nq > 0) mma_commit(BAR(Q_EMPTY));  // all MMAs on the previous sub-batch's queries
-          QPROF_T0();
-          mbar_wait(BAR(Q_FULL), nq & 1);
-          QPROF_ADD(0);
-          ++nq;
-          cur_s = s;
+    // The whole warp walks the work (warp-uniform state: descriptors in uniform registers); the
+    // elected lane issues the tcgen05 instructions (as in build_tcq.cu).
+    int stage = 0, as = 0, cur_s = -1, nq = 0;
+    uint32_t ph = 0, aph = 0;
+    int s, t;
+    first_item(s, t);
+    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x, next_item(s, t)) {
+      const int len = __ldg(wlen + w);
+      if (len == 0) continue;
+      if (s != cur_s) {
+        if (nq > 0) {
+          if (elect_one()) mma_commit(BAR(Q_EMPTY));  // all MMAs on the previous sub-batch's queries
+          __syncwarp();
         }
+        QPROF_T0();
+        mbar_wait(BAR(Q_FULL), nq & 1);
+        QPROF_ADD(0);
+        ++nq;
+        cur_s = s;
+      }
+      {
+        QPROF_T0();
+        mbar_wait(BAR(ACC_EMPTY + as), aph ^ 1);
+        QPROF_ADD(1);
+      }
+      const int N = (len + 15) & ~15;
+      const uint32_t idesc = idesc_f16_f32(kBM, N);
+      const uint32_t d = tmem + as * kAccCols;
+      for (int kb = 0; kb < KB; ++kb) {
         {
           QPROF_T0();
-          mbar_wait(BAR(ACC_EMPTY + as), aph ^ 1);
-          QPROF_ADD(1);
+          mbar_wait(BAR(A_FULL + stage), ph);
+          QPROF_ADD(2);
         }
-        const int N = (len + 15) & ~15;
-        const uint32_t idesc = idesc_f16_f32(kBM, N);
-        const uint32_t d = tmem + as * kAccCols;
-        for (int kb = 0; kb < KB; ++kb) {
-          {
-            QPROF_T0();
-            mbar_wait(BAR(A_FULL + stage), ph);
-            QPROF_ADD(2);
-          }
-          tc_fence_after();
-          const uint32_t a0 = sA + stage * kUTileBytes;
-          const uint32_t b0 = sQ + kb * kQTileBytes;
-          const int kk_end = min(4, ksteps - 4 * kb);  // zero-padding K steps are skipped
-          for (int kk = 0; kk < kk_end; ++kk)
-            mma_f16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
+        tc_fence_after();
+        const uint64_t adesc = sdesc_sw128(sA + stage * kUTileBytes);
+        const uint64_t bdesc = sdesc_sw128(sQ + kb * kQTileBytes);
+        const int kk_end = min(4, ksteps - 4 * kb);  // zero-padding K steps are skipped
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)  // K advance: 32 bytes = 2 in the 16-byte address field
+            if (kk < kk_end) mma_f16(d, adesc + (uint64_t)(2 * kk), bdesc + (uint64_t)(2 * kk), idesc, (kb | kk) != 0);
           mma_commit(BAR(A_EMPTY + stage));
-          if (++stage == kStages) stage = 0, ph ^= 1;
         }
-        mma_commit(BAR(ACC_FULL + as));
-        if (++as == kAcc) as = 0, aph ^= 1;
+        __syncwarp();
+        if (++stage == kStages) stage = 0, ph ^= 1;
       }
+      if (elect_one()) mma_commit(BAR(ACC_FULL + as));
+      __syncwarp();
+      if (++as == kAcc) as = 0, aph ^= 1;
     }
   } else {
     // ------------------------------------------------ epilogue: one thread per user row
