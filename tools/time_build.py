@@ -1,0 +1,27 @@
+"""Development timing of one build shape (synthetic cfg4 recipe, custom n / m / d): median contraction
+and build times over a few builds.  Usage: python tools/time_build.py n m d [k_max] [reps]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2110_07131_b200 import rmips  # noqa: E402
+from synth.generator import make_workload  # noqa: E402
+
+n, m, d = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+kmax = int(sys.argv[4]) if len(sys.argv) > 4 else 50
+reps = int(sys.argv[5]) if len(sys.argv) > 5 else 3
+w = make_workload(4, n=n, m=m, d=d, nq=16)
+U = torch.from_numpy(w.U).cuda()
+P = torch.from_numpy(w.P).cuda()
+ts = []
+for r in range(reps + 1):
+    idx = rmips.rmips_build_index(U, P, kmax, rmips.RMIPS_BUILD_TIMING)
+    pt = idx.phase_times()
+    if r:
+        ts.append((pt[1], pt[3], idx.tiles_done))
+    idx.close()
+print("n %d m %d d %d: contraction %.3f ms build %.3f ms tiles %d" % (n, m, d, np.median([t[0] for t in ts]),
+                                                                 np.median([t[1] for t in ts]), ts[-1][2]))
