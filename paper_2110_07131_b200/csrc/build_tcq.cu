@@ -43,7 +43,9 @@ struct Cfg {
   static constexpr int NST = (KB == 1) ? 4 : 3;  // item-tile ring depth (4 measured no faster at KB = 3)
   static constexpr int NACC = (512 / (UT * BN)) > 4 ? 4 : 512 / (UT * BN);  // TMEM stages
   static constexpr int ACC_COLS = UT * BN;                                // TMEM columns per stage
-  static constexpr int TMEM_COLS = NACC * ACC_COLS;                       // power of two >= 32
+  // A in tensor memory (UT = 1): the user tile's K steps, 8 columns each, after the accumulators
+  static constexpr int A_TMEM = NACC * ACC_COLS;
+  static constexpr int TMEM_COLS = (UT == 1 && A_TMEM + 32 * KB <= 512) ? 512 : NACC * ACC_COLS;
   static constexpr int B_TILE = BN * 64 * 2;                              // one BN x 64 fp16 tile
   static constexpr int THREADS = 64 + 128 * UT;
   static constexpr int A = 0;
@@ -130,6 +132,11 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   using namespace sm100;
   using C = Cfg<KB, UT, BN>;
   constexpr int NST = C::NST, NACC = C::NACC;
+#ifdef RMIPS_TCQ_SS
+  constexpr bool kATmem = false;  // dev switch: A re-read from shared memory by every MMA
+#else
+  constexpr bool kATmem = UT == 1 && C::TMEM_COLS == 512;
+#endif
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base, derived from smem_raw by pointer arithmetic so that the compiler
   // keeps the shared state space (LDS/STS rather than generic loads/stores)
@@ -217,6 +224,21 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     for (int gr = blockIdx.x; gr < num_groups; gr += gridDim.x, ++t) {
       mbar_wait_sleep(BAR(A_FULL), t & 1);
       tc_fence_after();
+      if constexpr (kATmem) {
+        // the user tile goes to tensor memory once (tcgen05.cp runs after the previous tile's MMAs,
+        // in issue order), so the MMAs read only the item tile from shared memory: with N = 64
+        // an MMA that also re-read A (4 KB per K step) would need 192 B/clk of shared-memory
+        // bandwidth at the tensor peak, above the 128 B/clk the SM has
+        if (elect_one()) {
+          const uint64_t adesc = sdesc_sw128(sA);
+#pragma unroll
+          for (int ks = 0; ks < 4 * KB; ++ks)
+            if (ks < ksteps)
+              tmem_cp_128x256b(tmem + C::A_TMEM + 8 * ks, adesc + (uint64_t)(((ks >> 2) * kUTile + (ks & 3) * 32) >> 4));
+          mma_commit(BAR(A_EMPTY));  // the shared-memory A tile may be reloaded
+        }
+        __syncwarp();
+      }
       for (int it = 0; it < nit; ++it) {
         mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
         mbar_wait_sleep(BAR(B_FULL + stage), ph);
@@ -233,7 +255,16 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           break;
         }
         const uint64_t bdesc = sdesc_sw128(sB + stage * KB * C::B_TILE);
-        if (elect_one()) {
+        if (kATmem && elect_one()) {
+          const uint32_t d = tmem + as * C::ACC_COLS;
+#pragma unroll
+          for (int ks = 0; ks < 4 * KB; ++ks)
+            if (ks < ksteps)
+              mma_f16_ts(d, tmem + C::A_TMEM + 8 * ks, bdesc + (uint64_t)(((ks >> 2) * C::B_TILE + (ks & 3) * 32) >> 4),
+                         idesc, ks != 0);
+          mma_commit(BAR(B_EMPTY + stage));
+          mma_commit(BAR(ACC_FULL + as));
+        } else if (!kATmem && elect_one()) {
 #pragma unroll
           for (int u = 0; u < UT; ++u) {
             const uint32_t d = tmem + as * C::ACC_COLS + u * BN;
@@ -255,8 +286,10 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         if (++stage == NST) stage = 0, ph ^= 1;
         if (++as == NACC) as = 0, aph ^= 1;
       }
-      if (elect_one()) mma_commit(BAR(A_EMPTY));
-      __syncwarp();
+      if (!kATmem) {
+        if (elect_one()) mma_commit(BAR(A_EMPTY));
+        __syncwarp();
+      }
     }
     if (lane == 0) atomicAdd(tiles_done, (unsigned long long)tiles_issued);
   } else {
