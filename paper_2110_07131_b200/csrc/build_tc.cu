@@ -279,13 +279,14 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
       const int64_t row = (int64_t)ut * kBM + rloc;
       CandRow me = cand_init(row < n);  // dead rows (user >= n) have theta = +inf and never pass
-      float En[4];                      // error bounds of the next tile's chunks (prefetched)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) En[c] = (32 * c < mi) ? __ldg(perr + 32 * c) : 0.f;
       // C-S check every kCsEvery tiles, on the scaled norm of the first item of the next tile
       // (prefetched one check ahead).  A warp that is not done never meets an end marker: the
       // producer ends a user tile only after all four warps (this one included) reported.
       constexpr int kCsEvery = 4;
+      // error bound of every chunk of a group of kCsEvery item tiles: perr of the group's first item
+      // (perr is non-increasing along the norm-sorted items, so it bounds every later item's);
+      // the next group's is prefetched a whole group ahead
+      float Eg = __ldg(perr), EgN = (kCsEvery * kBN < mi) ? __ldg(perr + kCsEvery * kBN) : 0.f;
       // (the raw fp64 norm is prefetched; it is scaled and rounded only at the check, so the load's
       // latency is not exposed where it is issued)
       double pnr = nit > kCsEvery ? __ldg(pnorm + kCsEvery * kBN) : 0.0;
@@ -338,12 +339,7 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       bool done = false;                        // warp-uniform: this warp's rows cannot gain any more
       for (; it < nit; ++it) {
         const int base0 = it * kBN;
-        float E[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          E[c] = En[c];
-          En[c] = (base0 + kBN + 32 * c < mi) ? __ldg(perr + base0 + kBN + 32 * c) : 0.f;
-        }
+        const float E[4] = {Eg, Eg, Eg, Eg};
 #ifdef RMIPS_EPI_PROFILE
         const long long t1 = clock64();
         const int pb = it < 255 ? it : 255;
@@ -381,8 +377,11 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
             done = true;
             break;
           }
-          if (base0 + (kCsEvery + 1) * kBN < mi)
+          Eg = EgN;
+          if (base0 + (kCsEvery + 1) * kBN < mi) {
             pnr = __ldg(pnorm + base0 + (kCsEvery + 1) * kBN);
+            EgN = __ldg(perr + base0 + (kCsEvery + 1) * kBN);
+          }
         }
       }
       if (lane == 0) atomicAdd(const_cast<int*>(done_cum), 1);  // one event per warp and user tile

@@ -41,7 +41,11 @@ constexpr int kUTile = kBM * 64 * 2;     // one 128 x 64 fp16 tile = 16 KB
 template <int KB, int UT, int BN>
 struct Cfg {
   static constexpr int NST = (KB == 1) ? 4 : 3;  // item-tile ring depth (4 measured no faster at KB = 3)
+#ifdef RMIPS_TCQ_NACC
+  static constexpr int NACC = UT == 1 ? RMIPS_TCQ_NACC : ((512 / (UT * BN)) > 4 ? 4 : 512 / (UT * BN));
+#else
   static constexpr int NACC = (512 / (UT * BN)) > 4 ? 4 : 512 / (UT * BN);  // TMEM stages
+#endif
   static constexpr int ACC_COLS = UT * BN;                                // TMEM columns per stage
   // A in tensor memory (UT = 1): the user tile's K steps, 8 columns each, after the accumulators
   static constexpr int A_TMEM = NACC * ACC_COLS;
@@ -316,9 +320,10 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     for (int gr = blockIdx.x; gr < num_groups; gr += gridDim.x, ++t) {
       const int64_t row = (int64_t)(gr * UT + u) * kBM + q * 32 + lane;
       typename Pol::Row me = Pol::init(row < n, smax);  // dead rows (user >= n): theta = +inf, never pass
-      float En[NCH];                       // error bounds of the next tile's chunks (prefetched)
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) En[c] = (32 * c < mi) ? __ldg(perr + 32 * c) : 0.f;
+      // error bound of every chunk of a group of kCsEvery item tiles: perr of the group's first item
+      // (perr is non-increasing along the norm-sorted items, so it bounds every later item's);
+      // the next group's is prefetched a whole group ahead
+      float Eg = __ldg(perr), EgN = (kCsEvery * BN < mi) ? __ldg(perr + kCsEvery * BN) : 0.f;
       double pnr = nit > kCsEvery ? __ldg(pnorm + kCsEvery * BN) : 0.0;  // raw norm, scaled at the check
       mbar_wait(BAR(ACC_FULL + as), aph);
       tc_fence_after();
@@ -328,13 +333,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       bool done = false;  // warp-uniform: this warp's rows cannot gain any more
       for (; it < nit; ++it) {
         const int base0 = it * BN;
-        float E[4];
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-          E[c] = En[c];
-          En[c] = (base0 + BN + 32 * c < mi) ? __ldg(perr + base0 + BN + 32 * c) : 0.f;
-        }
-        if (NCH == 2) E[2] = E[3] = 0.f;
+        const float E[4] = {Eg, Eg, Eg, Eg};
         const uint32_t tcur = tq + as * C::ACC_COLS;
         if (BN == 128) tmem_ld64(tcur + 64, hB);  // second half of this tile
         uint32_t bits = epiq_fast(hA, E[0], E[1], me.theta);
@@ -365,8 +364,11 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             done = true;
             break;
           }
-          if (base0 + (kCsEvery + 1) * BN < mi)
+          Eg = EgN;
+          if (base0 + (kCsEvery + 1) * BN < mi) {
             pnr = __ldg(pnorm + base0 + (kCsEvery + 1) * BN);
+            EgN = __ldg(perr + base0 + (kCsEvery + 1) * BN);
+          }
         }
       }
       if (lane == 0) atomicAdd(const_cast<int*>(done_cum), 1);  // one event per warp and group
