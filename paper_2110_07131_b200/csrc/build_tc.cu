@@ -478,13 +478,6 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
 
 cudaError_t build_tc(const BuildCtx& c, cudaStream_t st) {
   if (getenv("RMIPS_DISABLE_TC")) return cudaErrorNotSupported;
-  if (c.idx->dpad == 64 && c.mb <= 65536 && getenv("RMIPS_BUILD_TC2")) {
-    // experiment switch: two user tiles per CTA with 4-byte bf16-bound entries (build_tcq.cu,
-    // candh.cuh); measured 10% slower than this kernel on configs[1] (the epilogue's TMEM reads
-    // and issue, not its latency, bound both)
-    const cudaError_t e = build_tcq(c, st);
-    if (e != cudaErrorNotSupported) return e;
-  }
   if (getenv("RMIPS_BUILD_8W")) {
     // experiment switch: 8 epilogue warps splitting each tile's columns, 4-byte quantised entries
     // (build_tc2.cu); measured 35% slower than this kernel on configs[1]

@@ -1,24 +1,23 @@
 // build_tcq.cu -- B4 on the 5th-generation tensor cores for d_pad = 128..256 (build_tc.cu has the
 // d <= 64 kernel): the |Q| x |P| x d contraction of Alg. 1 lines 7-9 (over ALL of P per
 // BASELINE north star) fused with the per-row top-k_max candidate epilogue (candq.cuh: 4-byte
-// quantised entries, so that the 128 x 256 fp16 user tile, the item ring and the candidate
-// buffers fit in one SM's shared memory), so the score matrix never reaches HBM.
+// quantised entries), so the score matrix never reaches HBM.
 //
-// k_build_tcq<KB, UT, BN, Pol>: K = 64*KB (d_pad), UT user tiles of 128 rows per CTA, item tiles of
-// BN rows.  One persistent CTA per SM walks groups of UT user tiles; per group:
-//   warp 0        TMA producer: the UT user tiles A (128 x 64*KB fp16, once per group) and the
-//                 stream of item tiles B through an NST-deep shared-memory ring (SWIZZLE_128B)
-//   warp 1        TMEM allocator + MMA issuer: per item tile UT x tcgen05.mma.cta_group::1.kind::f16
-//                 (M = 128, N = BN, K = 16 x ksteps), fp32 accumulators in TMEM, NACC stages
-//   warps 2..     4*UT epilogue warps: warp w reads TMEM lane quadrant w % 4 of user tile
-//                 (w - 2) / 4; every thread owns one user row and filters its BN scores per item
-//                 tile (3-input max trees, one compare per 32-column chunk: the fast path), with
-//                 one out-of-line slow path that re-reads flagged chunks from TMEM and appends.
-// Configurations: d_pad in {128, 192, 256}: <KB, 1, 64> (MMA-bound: 64 columns of scores per
-// 16-step K loop).  UT = 2 (two user tiles sharing each item tile) is supported by the code; it
-// measured slower than build_tc.cu for d <= 64 (the epilogue is issue-bound, not latency-bound).
-// Pipelines: smem full/empty (TMA <-> MMA), TMEM full/empty (MMA <-> epilogue), and the A group
-// full/empty (MMA done with the group before the next one is loaded).
+// k_build_tcq<KB, Pol>: K = 64*KB (d_pad), 128-user tiles, 128-item tiles.  One persistent CTA per
+// SM; per user tile:
+//   warp 0      TMA producer: one ring of NST entries of KB x 16 KB; each user tile's sequence is its
+//               A tile (128 x 64*KB fp16) followed by the item tiles B (128 x 64*KB), all SWIZZLE_128B
+//   warp 1      MMA warp (all lanes run the loop, one elected lane issues): the A entry is copied
+//               into TENSOR memory with tcgen05.cp (8 columns per K step, in issue order after the
+//               previous tile's MMAs) and its ring slot released; every item tile is then one
+//               tcgen05.mma.cta_group::1.kind::f16 chain, M = N = 128, K = 16 x ksteps, with A read
+//               from TMEM and only B from shared memory (an N = 64 MMA that also re-read A from
+//               shared memory needs 192 B/clk at the tensor peak, above the SM's 128 B/clk)
+//   warps 2-5   epilogue: warp w reads TMEM lane quadrant w % 4; every thread owns one user row
+//               and filters its 128 scores per item tile (3-input max trees, one compare per
+//               32-column chunk), with one out-of-line slow path that re-reads flagged chunks.
+// TMEM: NACC = 3 accumulator stages of 128 columns, then the A tile (32 KB columns).
+// Early termination (Cauchy-Schwarz on the norm-sorted items) as in build_tc.cu.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -38,25 +37,21 @@ namespace {
 constexpr int kBM = 128;                 // users per tile (TMEM lanes)
 constexpr int kUTile = kBM * 64 * 2;     // one 128 x 64 fp16 tile = 16 KB
 
-template <int KB, int UT, int BN>
+template <int KB>
 struct Cfg {
-  static constexpr int NST = (KB == 1) ? 4 : 3;  // item-tile ring depth (4 measured no faster at KB = 3)
-#ifdef RMIPS_TCQ_NACC
-  static constexpr int NACC = UT == 1 ? RMIPS_TCQ_NACC : ((512 / (UT * BN)) > 4 ? 4 : 512 / (UT * BN));
-#else
-  static constexpr int NACC = (512 / (UT * BN)) > 4 ? 4 : 512 / (UT * BN);  // TMEM stages
-#endif
-  static constexpr int ACC_COLS = UT * BN;                                // TMEM columns per stage
-  // A in tensor memory (UT = 1): the user tile's K steps, 8 columns each, after the accumulators
-  static constexpr int A_TMEM = NACC * ACC_COLS;
-  static constexpr int TMEM_COLS = (UT == 1 && A_TMEM + 32 * KB <= 512) ? 512 : NACC * ACC_COLS;
-  static constexpr int B_TILE = BN * 64 * 2;                              // one BN x 64 fp16 tile
-  static constexpr int THREADS = 64 + 128 * UT;
-  static constexpr int A = 0;
-  static constexpr int B = UT * KB * kUTile;
-  static constexpr int CAND = B + NST * KB * B_TILE;
-  static constexpr int BAR = CAND + UT * kBM * 128 * 4;  // 128 four-byte candidate slots per row
-  static constexpr int TOTAL = BAR + 256 + 1024;  // + alignment slack
+  static constexpr int BN = 128;                              // items per tile (= kBM: A and B entries alike)
+  static constexpr int ENTRY = KB * kUTile;                   // one ring entry (A or B tile), bytes
+  static constexpr int NST = (128 * 1024) / ENTRY;           // ring depth: 4 (KB 2), 2 (KB 3, 4)
+  static constexpr int ACC_COLS = BN;                         // TMEM columns per accumulator stage
+  static constexpr int NACC = 3;
+  static constexpr int A_TMEM = NACC * ACC_COLS;              // column of the A tile in TMEM
+  static constexpr int TMEM_COLS = 512;
+  static_assert(A_TMEM + 32 * KB <= TMEM_COLS, "tensor memory");
+  static constexpr int THREADS = 192;
+  static constexpr int RING = 0;
+  static constexpr int CAND = RING + NST * ENTRY;
+  static constexpr int BAR = CAND + kBM * 128 * 4;  // 128 four-byte candidate slots per row
+  static constexpr int TOTAL = BAR + 256 + 1024;    // + alignment slack
   static_assert(TOTAL <= 232448, "shared memory");
 };
 
@@ -127,52 +122,42 @@ __device__ __noinline__ typename Pol::Row epiq_slow(uint32_t bits, uint32_t tadd
 
 }  // namespace
 
-template <int KB, int UT, int BN, class Pol>
-__global__ void __launch_bounds__(Cfg<KB, UT, BN>::THREADS, 1)
+template <int KB, class Pol>
+__global__ void __launch_bounds__(Cfg<KB>::THREADS, 1)
 k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
            int64_t n, int64_t m, int kmax, int ksteps, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
            int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count, unsigned long long* __restrict__ tiles_done) {
   using namespace sm100;
-  using C = Cfg<KB, UT, BN>;
-  constexpr int NST = C::NST, NACC = C::NACC;
-#ifdef RMIPS_TCQ_SS
-  constexpr bool kATmem = false;  // dev switch: A re-read from shared memory by every MMA
-#else
-  constexpr bool kATmem = UT == 1 && C::TMEM_COLS == 512;
-#endif
+  using C = Cfg<KB>;
+  constexpr int NST = C::NST, NACC = C::NACC, BN = C::BN;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base, derived from smem_raw by pointer arithmetic so that the compiler
   // keeps the shared state space (LDS/STS rather than generic loads/stores)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t sA = sbase + C::A;
-  const uint32_t sB = sbase + C::B;
-  const typename Pol::Buf sb{reinterpret_cast<uint32_t*>(smem + C::CAND), UT * kBM};
+  const uint32_t sR = sbase + C::RING;
+  const typename Pol::Buf sb{reinterpret_cast<uint32_t*>(smem + C::CAND), kBM};
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR);
   const uint32_t bar0 = smem_u32(bars);
   auto BAR = [&](int i) { return bar0 + 8u * i; };
-  const int A_FULL = 0, A_EMPTY = 1, B_FULL = 2, B_EMPTY = 2 + NST, ACC_FULL = 2 + 2 * NST,
-            ACC_EMPTY = 2 + 2 * NST + NACC;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 + 2 * NST + 2 * NACC);
+  const int R_FULL = 0, R_EMPTY = NST, ACC_FULL = 2 * NST, ACC_EMPTY = 2 * NST + NACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 2 * NACC);
   // early-termination control words (Cauchy-Schwarz, as in build_tc.cu): epilogue warps done
-  // with a group (cumulative, 4*UT per group), and the producer -> MMA -> epilogue end markers
+  // with a user tile (cumulative, 4 per tile), and the producer -> MMA -> epilogue end markers
   volatile int* done_cum = reinterpret_cast<volatile int*>(tmem_slot + 1);
   volatile int* stage_end = done_cum + 1;
   volatile int* acc_end = stage_end + NST;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_utiles = (int)((n + kBM - 1) / kBM);
-  const int num_groups = (num_utiles + UT - 1) / UT;
   const int nit = (int)((m + BN - 1) / BN);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    mbar_init(BAR(A_FULL), 1);
-    mbar_init(BAR(A_EMPTY), 1);
-    for (int s = 0; s < NST; ++s) mbar_init(BAR(B_FULL + s), 1), mbar_init(BAR(B_EMPTY + s), 1);
-    for (int a = 0; a < NACC; ++a) mbar_init(BAR(ACC_FULL + a), 1), mbar_init(BAR(ACC_EMPTY + a), 4 * UT);
+    for (int s = 0; s < NST; ++s) mbar_init(BAR(R_FULL + s), 1), mbar_init(BAR(R_EMPTY + s), 1);
+    for (int a = 0; a < NACC; ++a) mbar_init(BAR(ACC_FULL + a), 1), mbar_init(BAR(ACC_EMPTY + a), 4);
     *done_cum = 0;
     for (int s = 0; s < NST; ++s) stage_end[s] = 0;
     for (int a = 0; a < NACC; ++a) acc_end[a] = 0;
@@ -193,63 +178,57 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       int stage = 0;
       uint32_t ph = 0;
       int t = 0;
-      for (int gr = blockIdx.x; gr < num_groups; gr += gridDim.x, ++t) {
-        if (t > 0) mbar_wait_sleep(BAR(A_EMPTY), (t - 1) & 1);
-        mbar_arrive_expect_tx(BAR(A_FULL), UT * KB * kUTile);
-        for (int u = 0; u < UT; ++u)
-          for (int kb = 0; kb < KB; ++kb)
-            tma_load_2d(sA + (u * KB + kb) * kUTile, &tmA, kb * 64, (gr * UT + u) * kBM, BAR(A_FULL));
+      for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
+        mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);  // the user tile A
+        mbar_arrive_expect_tx(BAR(R_FULL + stage), C::ENTRY);
+        for (int kb = 0; kb < KB; ++kb)
+          tma_load_2d(sR + stage * C::ENTRY + kb * kUTile, &tmA, kb * 64, ut * kBM, BAR(R_FULL + stage));
+        if (++stage == NST) stage = 0, ph ^= 1;
         for (int it = 0; it < nit; ++it) {
-          mbar_wait_sleep(BAR(B_EMPTY + stage), ph ^ 1);
-          if (*done_cum >= 4 * UT * (t + 1)) {  // every epilogue warp is done with this group
+          mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
+          if (*done_cum >= 4 * (t + 1)) {  // every epilogue warp is done with this user tile
             stage_end[stage] = t + 1;
-            mbar_arrive(BAR(B_FULL + stage));  // release: the marker is visible to the MMA warp
+            mbar_arrive(BAR(R_FULL + stage));  // release: the marker is visible to the MMA warp
             if (++stage == NST) stage = 0, ph ^= 1;
             break;
           }
-          mbar_arrive_expect_tx(BAR(B_FULL + stage), KB * C::B_TILE);
+          mbar_arrive_expect_tx(BAR(R_FULL + stage), C::ENTRY);
           for (int kb = 0; kb < KB; ++kb)
-            tma_load_2d(sB + (stage * KB + kb) * C::B_TILE, &tmB, kb * 64, it * BN, BAR(B_FULL + stage));
+            tma_load_2d(sR + stage * C::ENTRY + kb * kUTile, &tmB, kb * 64, it * BN, BAR(R_FULL + stage));
           if (++stage == NST) stage = 0, ph ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    // The whole warp runs the loop (warp-uniform state, descriptors in uniform registers); the
-    // elected lane issues.  The K loop is unrolled to its compile-time bound 4 KB with the runtime
-    // ksteps as a predicate, and every descriptor is the stage's base descriptor plus a constant
-    // (K advance of 16 fp16 = 32 bytes = 2 in the 16-byte address field; K-block = tile / 16).
+    // ------------------------------------------------ MMA warp
+    // All lanes run the loop (warp-uniform state, descriptors in uniform registers); the elected
+    // lane issues.  Descriptors: the entry's base plus a constant per K step (16 fp16 = 32 bytes =
+    // 2 in the 16-byte address field; K block = 16 KB).
     constexpr uint32_t idesc = idesc_f16_f32(kBM, BN);
     unsigned long long tiles_issued = 0;  // (user tile, item tile) contractions issued
     int stage = 0, as = 0;
     uint32_t ph = 0, aph = 0;
     int t = 0;
-    for (int gr = blockIdx.x; gr < num_groups; gr += gridDim.x, ++t) {
-      mbar_wait_sleep(BAR(A_FULL), t & 1);
+    auto koff = [](int ks) { return (uint64_t)(((ks >> 2) * kUTile + (ks & 3) * 32) >> 4); };
+    for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
+      mbar_wait_sleep(BAR(R_FULL + stage), ph);  // the user tile: into tensor memory
       tc_fence_after();
-      if constexpr (kATmem) {
-        // the user tile goes to tensor memory once (tcgen05.cp runs after the previous tile's MMAs,
-        // in issue order), so the MMAs read only the item tile from shared memory: with N = 64
-        // an MMA that also re-read A (4 KB per K step) would need 192 B/clk of shared-memory
-        // bandwidth at the tensor peak, above the 128 B/clk the SM has
-        if (elect_one()) {
-          const uint64_t adesc = sdesc_sw128(sA);
+      if (elect_one()) {
+        const uint64_t adesc = sdesc_sw128(sR + stage * C::ENTRY);
 #pragma unroll
-          for (int ks = 0; ks < 4 * KB; ++ks)
-            if (ks < ksteps)
-              tmem_cp_128x256b(tmem + C::A_TMEM + 8 * ks, adesc + (uint64_t)(((ks >> 2) * kUTile + (ks & 3) * 32) >> 4));
-          mma_commit(BAR(A_EMPTY));  // the shared-memory A tile may be reloaded
-        }
-        __syncwarp();
+        for (int ks = 0; ks < 4 * KB; ++ks)
+          if (ks < ksteps) tmem_cp_128x256b(tmem + C::A_TMEM + 8 * ks, adesc + koff(ks));
+        mma_commit(BAR(R_EMPTY + stage));  // the entry is free once the copy has completed
       }
+      __syncwarp();
+      if (++stage == NST) stage = 0, ph ^= 1;
       for (int it = 0; it < nit; ++it) {
         mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
-        mbar_wait_sleep(BAR(B_FULL + stage), ph);
+        mbar_wait_sleep(BAR(R_FULL + stage), ph);
         tc_fence_after();
-        if (stage_end[stage] == t + 1) {  // the producer ended this group: forward the marker
+        if (stage_end[stage] == t + 1) {  // the producer ended this user tile: forward the marker
           if (elect_one()) {
-            mbar_arrive(BAR(B_EMPTY + stage));
+            mbar_arrive(BAR(R_EMPTY + stage));
             acc_end[as] = t + 1;
             mbar_arrive(BAR(ACC_FULL + as));
           }
@@ -258,52 +237,28 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           if (++as == NACC) as = 0, aph ^= 1;
           break;
         }
-        const uint64_t bdesc = sdesc_sw128(sB + stage * KB * C::B_TILE);
-        if (kATmem && elect_one()) {
+        if (elect_one()) {
+          const uint64_t bdesc = sdesc_sw128(sR + stage * C::ENTRY);
           const uint32_t d = tmem + as * C::ACC_COLS;
 #pragma unroll
-          for (int ks = 0; ks < 4 * KB; ++ks)
-            if (ks < ksteps)
-              mma_f16_ts(d, tmem + C::A_TMEM + 8 * ks, bdesc + (uint64_t)(((ks >> 2) * C::B_TILE + (ks & 3) * 32) >> 4),
-                         idesc, ks != 0);
-          mma_commit(BAR(B_EMPTY + stage));
-          mma_commit(BAR(ACC_FULL + as));
-        } else if (!kATmem && elect_one()) {
-#pragma unroll
-          for (int u = 0; u < UT; ++u) {
-            const uint32_t d = tmem + as * C::ACC_COLS + u * BN;
-            const uint64_t adesc = sdesc_sw128(sA + u * KB * kUTile);
-#pragma unroll
-            for (int ks = 0; ks < 4 * KB; ++ks) {  // K steps of 16 (zero padding beyond d skipped)
-              if (ks < ksteps) {
-                const int kb = ks >> 2, kk = ks & 3;
-                mma_f16(d, adesc + (uint64_t)((kb * kUTile + kk * 32) >> 4),
-                        bdesc + (uint64_t)((kb * C::B_TILE + kk * 32) >> 4), idesc, ks != 0);
-              }
-            }
-          }
-          mma_commit(BAR(B_EMPTY + stage));
+          for (int ks = 0; ks < 4 * KB; ++ks)  // K steps of 16 (zero padding beyond d skipped)
+            if (ks < ksteps) mma_f16_ts(d, tmem + C::A_TMEM + 8 * ks, bdesc + koff(ks), idesc, ks != 0);
+          mma_commit(BAR(R_EMPTY + stage));
           mma_commit(BAR(ACC_FULL + as));
         }
         __syncwarp();
-        tiles_issued += UT;
+        ++tiles_issued;
         if (++stage == NST) stage = 0, ph ^= 1;
         if (++as == NACC) as = 0, aph ^= 1;
       }
-      if (!kATmem) {
-        if (elect_one()) mma_commit(BAR(A_EMPTY));
-        __syncwarp();
-      }
     }
-    if (lane == 0) atomicAdd(tiles_done, (unsigned long long)tiles_issued);
+    if (lane == 0) atomicAdd(tiles_done, tiles_issued);
   } else {
     // ------------------------------------------------ epilogue: one thread per user row
     // The 64-column halves of an item tile are software-pipelined: the TMEM load of the next half
     // (of this tile or the next one) is in flight while the current half is filtered.
-    const int e = warp - 2;
-    const int u = e >> 2;                     // user tile of the group
     const int q = warp & 3;                   // TMEM lane quadrant of this warp
-    const int rr = u * kBM + q * 32 + lane;   // row in the candidate buffer
+    const int rr = q * 32 + lane;             // row in the candidate buffer
     const int mi = (int)m;
     const float e0x2 = __fadd_ru(__ldg(perr), __ldg(perr));
     // |s~| <= |u^| |p^| + E with |u^| <= 1 + 2^-10, |p^| <= |p| 2^e (1 + 2^-11): every score is
@@ -312,13 +267,12 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const float pscl = __ldg(pscale);
     int as = 0;
     uint32_t aph = 0;
-    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + u * BN;
-    constexpr int NCH = BN / 32;  // chunks per item tile (2 or 4)
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
     constexpr int kCsEvery = 4;   // Cauchy-Schwarz check period (item tiles)
     uint32_t hA[64], hB[64];
     int t = 0;
-    for (int gr = blockIdx.x; gr < num_groups; gr += gridDim.x, ++t) {
-      const int64_t row = (int64_t)(gr * UT + u) * kBM + q * 32 + lane;
+    for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
+      const int64_t row = (int64_t)ut * kBM + q * 32 + lane;
       typename Pol::Row me = Pol::init(row < n, smax);  // dead rows (user >= n): theta = +inf, never pass
       // error bound of every chunk of a group of kCsEvery item tiles: perr of the group's first item
       // (perr is non-increasing along the norm-sorted items, so it bounds every later item's);
@@ -335,7 +289,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         const int base0 = it * BN;
         const float E[4] = {Eg, Eg, Eg, Eg};
         const uint32_t tcur = tq + as * C::ACC_COLS;
-        if (BN == 128) tmem_ld64(tcur + 64, hB);  // second half of this tile
+        tmem_ld64(tcur + 64, hB);                 // second half of this tile
         uint32_t bits = epiq_fast(hA, E[0], E[1], me.theta);
         const bool more = it + 1 < nit;
         const int as_next = as + 1 == NACC ? 0 : as + 1;
@@ -345,10 +299,8 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           tc_fence_after();
           tmem_ld64(tq + as_next * C::ACC_COLS, hA);
         }
-        if (BN == 128) {
-          tmem_ld_wait64(hB);
-          bits |= epiq_fast(hB, E[2], E[3], me.theta) << 2;
-        }
+        tmem_ld_wait64(hB);
+        bits |= epiq_fast(hB, E[2], E[3], me.theta) << 2;
         if (bits) me = epiq_slow<Pol>(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, sb, rr, e0x2, kmax);
         tc_fence_before();                        // this stage is no longer read: release it
         __syncwarp();
@@ -371,7 +323,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           }
         }
       }
-      if (lane == 0) atomicAdd(const_cast<int*>(done_cum), 1);  // one event per warp and group
+      if (lane == 0) atomicAdd(const_cast<int*>(done_cum), 1);  // one event per warp and user tile
       if (done) {                                 // drain: release the remaining stages unread
         for (++it; it < nit; ++it) {              // stage `as` (tile it) is already full
           const bool end = acc_end[as] == t + 1;
@@ -404,34 +356,33 @@ static int sm_count_q() {
   return c;
 }
 
-template <int KB, int UT, int BN, class Pol>
+template <int KB, class Pol>
 static cudaError_t launch_tcq(const BuildCtx& c, cudaStream_t st) {
-  using C = Cfg<KB, UT, BN>;
+  using C = Cfg<KB>;
   rmips_index_s* x = c.idx;
   CUtensorMap ta, tb;
   if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM)) return cudaErrorNotSupported;
-  if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->dpad, BN)) return cudaErrorNotSupported;
-  cudaError_t e = cudaFuncSetAttribute(k_build_tcq<KB, UT, BN, Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
+  if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->dpad, C::BN)) return cudaErrorNotSupported;
+  cudaError_t e = cudaFuncSetAttribute(k_build_tcq<KB, Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
   if (e != cudaSuccess) return e;
-  const int groups = (int)(((x->n + kBM - 1) / kBM + UT - 1) / UT);
-  const int grid = groups < sm_count_q() ? groups : sm_count_q();
+  const int tiles = (int)((x->n + kBM - 1) / kBM);
+  const int grid = tiles < sm_count_q() ? tiles : sm_count_q();
   const int ksteps = (x->d + 15) / 16;  // K steps of 16 that touch real (non-padding) columns
-  k_build_tcq<KB, UT, BN, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tb, x->perr, x->pnorm, c.scale_dev, x->n, c.mb,
-                                                             x->kmax, ksteps, c.cand, c.ccount, c.ovf_list,
-                                                             c.ovf_count, c.tiles_done);
+  k_build_tcq<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tb, x->perr, x->pnorm, c.scale_dev, x->n, c.mb,
+                                                          x->kmax, ksteps, c.cand, c.ccount, c.ovf_list,
+                                                          c.ovf_count, c.tiles_done);
   count_launch();
   return cudaGetLastError();
 }
 
-// d_pad = 128..256, and d_pad = 64 with m <= 2^16 (two user tiles per CTA, bf16-bound entries);
-// other d <= 64 cases use build_tc.cu's kernel.
+// d_pad = 128..256 with m <= 2^20 (20-bit packed positions); otherwise cudaErrorNotSupported
+// (the SIMT build).
 cudaError_t build_tcq(const BuildCtx& c, cudaStream_t st) {
-  if (c.mb > (int64_t)kQPosMask + 1) return cudaErrorNotSupported;  // packed positions are 20-bit
+  if (c.mb > (int64_t)kQPosMask + 1) return cudaErrorNotSupported;
   switch (c.idx->dpad) {
-    case 64: return c.mb <= 65536 ? launch_tcq<1, 2, 128, HPol>(c, st) : cudaErrorNotSupported;
-    case 128: return launch_tcq<2, 1, 64, QPol>(c, st);
-    case 192: return launch_tcq<3, 1, 64, QPol>(c, st);
-    case 256: return launch_tcq<4, 1, 64, QPol>(c, st);
+    case 128: return launch_tcq<2, QPol>(c, st);
+    case 192: return launch_tcq<3, QPol>(c, st);
+    case 256: return launch_tcq<4, QPol>(c, st);
     default: return cudaErrorNotSupported;
   }
 }

@@ -1,12 +1,10 @@
-// candpol.cuh -- the two 4-byte candidate-entry policies of the tensor-core build kernels
-// (build_tc2.cu, build_tcq.cu), behind one interface:
+// candpol.cuh -- the 4-byte candidate-entry policy of the tensor-core build kernels (build_tc2.cu,
+// build_tcq.cu) behind a small interface:
 //   QPol  candq.cuh: 12-bit quantised lower bound | 20-bit position (m <= 2^20)
-//   HPol  candh.cuh: bf16 lower bound | 16-bit position (m <= 2^16)
-// Both keep cand.cuh's invariant: theta is a valid lower bound of the row's
+// It keeps cand.cuh's invariant: theta is a valid lower bound of the row's
 // k_max-th largest true score, an item is appended iff s~ >= theta - E, and an entry is dropped
 // only when its upper bound is below theta.
 #pragma once
-#include "candh.cuh"
 #include "candq.cuh"
 #include "common.cuh"
 
@@ -42,31 +40,6 @@ struct QPol {
     qrow_finish(me, sb, rr, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
   }
   __device__ static int32_t pos(uint32_t e) { return (int32_t)(e & kQPosMask); }
-};
-
-struct HPol {
-  using Row = HRow;
-  using Buf = HBuf;
-  static constexpr int kSlots = kHSlots;
-  __device__ static Row init(bool live, float) { return hrow_init(live); }
-  __device__ static void seed(Row& me, float s, float) {
-    if (!me.ovf) me.theta = fmaxf(me.theta, s);
-  }
-  template <typename F>
-  __device__ static void append(F f, const float (&g4)[8], float E, int pos0, int mi, Row& me, Buf sb, int rr) {
-    hrow_append_chunk(f, g4, E, pos0, mi, me, sb, rr);
-  }
-  __device__ static Row refresh(Row me, Buf sb, int rr, float e0x2, int kmax) {
-    return hrow_refresh(me, sb, rr, e0x2, kmax);
-  }
-  __device__ static void maybe_refresh(Row& me, Buf sb, int rr, float e0x2, int kmax) {
-    hrow_maybe_refresh(me, sb, rr, e0x2, kmax);
-  }
-  __device__ static void finish(Row& me, Buf sb, int rr, float e0x2, int kmax, int64_t row, int64_t n, int32_t* cand,
-                                int32_t* ccount, int32_t* ovf_list, int* ovf_count) {
-    hrow_finish(me, sb, rr, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
-  }
-  __device__ static int32_t pos(uint32_t e) { return (int32_t)(e & 0xffffu); }
 };
 
 }  // namespace rmips

@@ -340,10 +340,10 @@ def test_filter_error_bound_holds():
 
 @pytest.mark.parametrize("env", [{}, {"RMIPS_SEED_TILES": "0"}, {"RMIPS_SEED_TILES": "32"},
                                  {"RMIPS_SEED_TILES": "3"}, {"RMIPS_BUILD_8W": "1"},
-                                 {"RMIPS_BUILD_8W": "1", "RMIPS_SEED_TILES": "0"}, {"RMIPS_BUILD_TC2": "1"}],
-                         ids=["default", "seed0", "seed32", "seed3", "8w", "8w-seed0", "tcq-ut2"])
+                                 {"RMIPS_BUILD_8W": "1", "RMIPS_SEED_TILES": "0"}],
+                         ids=["default", "seed0", "seed32", "seed3", "8w", "8w-seed0"])
 def test_build_variants_bitwise(env, monkeypatch):
-    """Every tensor-core build variant (seed-pass lengths, the 8-warp and two-user-tile kernels)
+    """Every tensor-core build variant (seed-pass lengths, the 8-warp kernel)
     gives the oracle's exact top-k_max lists (tau and ids bitwise) on a sample of users, with
     m = 6,000 items (47 item tiles, a ragged last tile) and k_max = 50."""
     for k_, v_ in env.items():
