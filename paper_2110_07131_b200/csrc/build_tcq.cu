@@ -5,11 +5,11 @@
 //
 // k_build_tcq<KB, Pol>: K = 64*KB (d_pad), 128-user tiles, 128-item tiles.  One persistent CTA per
 // SM; per user tile:
-//   warp 0      TMA producer: one ring of NST entries of KB x 16 KB; each user tile's sequence is its
-//               A tile (128 x 64*KB fp16) followed by the item tiles B (128 x 64*KB), all SWIZZLE_128B
-//   warp 1      MMA warp (all lanes run the loop, one elected lane issues): the A entry is copied
+//   warp 0      TMA producer: one ring of 16 KB K-block units; each user tile's sequence is its A tile
+//               (128 x 64*KB fp16, KB units) followed by the item tiles B (KB units each), SWIZZLE_128B
+//   warp 1      MMA warp (all lanes run the loop, one elected lane issues): the A units are copied
 //               into TENSOR memory with tcgen05.cp (8 columns per K step, in issue order after the
-//               previous tile's MMAs) and its ring slot released; every item tile is then one
+//               previous tile's MMAs) and their ring slots released; every item tile is then one
 //               tcgen05.mma.cta_group::1.kind::f16 chain, M = N = 128, K = 16 x ksteps, with A read
 //               from TMEM and only B from shared memory (an N = 64 MMA that also re-read A from
 //               shared memory needs 192 B/clk at the tensor peak, above the SM's 128 B/clk)
@@ -39,9 +39,10 @@ constexpr int kUTile = kBM * 64 * 2;     // one 128 x 64 fp16 tile = 16 KB
 
 template <int KB>
 struct Cfg {
-  static constexpr int BN = 128;                              // items per tile (= kBM: A and B entries alike)
-  static constexpr int ENTRY = KB * kUTile;                   // one ring entry (A or B tile), bytes
-  static constexpr int NST = (128 * 1024) / ENTRY;           // ring depth: 4 (KB 2), 2 (KB 3, 4)
+  static constexpr int BN = 128;                              // items per tile (= kBM: A and B tiles alike)
+  // the ring holds K-block units (128 rows x 64 fp16 = 16 KB): a tile (A or B) is KB consecutive
+  // units, and the MMA on K block kb starts as soon as that unit has landed
+  static constexpr int NST = 10;
   static constexpr int ACC_COLS = BN;                         // TMEM columns per accumulator stage
   static constexpr int NACC = 3;
   static constexpr int A_TMEM = NACC * ACC_COLS;              // column of the A tile in TMEM
@@ -49,9 +50,9 @@ struct Cfg {
   static_assert(A_TMEM + 32 * KB <= TMEM_COLS, "tensor memory");
   static constexpr int THREADS = 192;
   static constexpr int RING = 0;
-  static constexpr int CAND = RING + NST * ENTRY;
+  static constexpr int CAND = RING + NST * kUTile;
   static constexpr int BAR = CAND + kBM * 128 * 4;  // 128 four-byte candidate slots per row
-  static constexpr int TOTAL = BAR + 256 + 1024;    // + alignment slack
+  static constexpr int TOTAL = BAR + 512 + 1024;    // barriers + control words, alignment slack
   static_assert(TOTAL <= 232448, "shared memory");
 };
 
@@ -179,23 +180,28 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       uint32_t ph = 0;
       int t = 0;
       for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
-        mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);  // the user tile A
-        mbar_arrive_expect_tx(BAR(R_FULL + stage), C::ENTRY);
-        for (int kb = 0; kb < KB; ++kb)
-          tma_load_2d(sR + stage * C::ENTRY + kb * kUTile, &tmA, kb * 64, ut * kBM, BAR(R_FULL + stage));
-        if (++stage == NST) stage = 0, ph ^= 1;
-        for (int it = 0; it < nit; ++it) {
+        for (int kb = 0; kb < KB; ++kb) {  // the user tile A
           mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
-          if (*done_cum >= 4 * (t + 1)) {  // every epilogue warp is done with this user tile
-            stage_end[stage] = t + 1;
-            mbar_arrive(BAR(R_FULL + stage));  // release: the marker is visible to the MMA warp
-            if (++stage == NST) stage = 0, ph ^= 1;
-            break;
-          }
-          mbar_arrive_expect_tx(BAR(R_FULL + stage), C::ENTRY);
-          for (int kb = 0; kb < KB; ++kb)
-            tma_load_2d(sR + stage * C::ENTRY + kb * kUTile, &tmB, kb * 64, it * BN, BAR(R_FULL + stage));
+          mbar_arrive_expect_tx(BAR(R_FULL + stage), kUTile);
+          tma_load_2d(sR + stage * kUTile, &tmA, kb * 64, ut * kBM, BAR(R_FULL + stage));
           if (++stage == NST) stage = 0, ph ^= 1;
+        }
+        for (int it = 0; it < nit; ++it) {
+          bool ended = false;
+          for (int kb = 0; kb < KB; ++kb) {
+            mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
+            if (kb == 0 && *done_cum >= 4 * (t + 1)) {  // every epilogue warp is done with this user tile
+              stage_end[stage] = t + 1;
+              mbar_arrive(BAR(R_FULL + stage));  // release: the marker is visible to the MMA warp
+              if (++stage == NST) stage = 0, ph ^= 1;
+              ended = true;
+              break;
+            }
+            mbar_arrive_expect_tx(BAR(R_FULL + stage), kUTile);
+            tma_load_2d(sR + stage * kUTile, &tmB, kb * 64, it * BN, BAR(R_FULL + stage));
+            if (++stage == NST) stage = 0, ph ^= 1;
+          }
+          if (ended) break;
         }
       }
     }
@@ -209,19 +215,20 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     int stage = 0, as = 0;
     uint32_t ph = 0, aph = 0;
     int t = 0;
-    auto koff = [](int ks) { return (uint64_t)(((ks >> 2) * kUTile + (ks & 3) * 32) >> 4); };
     for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
-      mbar_wait_sleep(BAR(R_FULL + stage), ph);  // the user tile: into tensor memory
-      tc_fence_after();
-      if (elect_one()) {
-        const uint64_t adesc = sdesc_sw128(sR + stage * C::ENTRY);
+      for (int kb = 0; kb < KB; ++kb) {  // the user tile: into tensor memory, unit by unit
+        mbar_wait_sleep(BAR(R_FULL + stage), ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t adesc = sdesc_sw128(sR + stage * kUTile);
 #pragma unroll
-        for (int ks = 0; ks < 4 * KB; ++ks)
-          if (ks < ksteps) tmem_cp_128x256b(tmem + C::A_TMEM + 8 * ks, adesc + koff(ks));
-        mma_commit(BAR(R_EMPTY + stage));  // the entry is free once the copy has completed
+          for (int kk = 0; kk < 4; ++kk)
+            if (4 * kb + kk < ksteps) tmem_cp_128x256b(tmem + C::A_TMEM + 8 * (4 * kb + kk), adesc + (uint64_t)(2 * kk));
+          mma_commit(BAR(R_EMPTY + stage));  // the unit is free once the copy has completed
+        }
+        __syncwarp();
+        if (++stage == NST) stage = 0, ph ^= 1;
       }
-      __syncwarp();
-      if (++stage == NST) stage = 0, ph ^= 1;
       for (int it = 0; it < nit; ++it) {
         mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
         mbar_wait_sleep(BAR(R_FULL + stage), ph);
@@ -237,18 +244,26 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           if (++as == NACC) as = 0, aph ^= 1;
           break;
         }
-        if (elect_one()) {
-          const uint64_t bdesc = sdesc_sw128(sR + stage * C::ENTRY);
-          const uint32_t d = tmem + as * C::ACC_COLS;
+        const uint32_t d = tmem + as * C::ACC_COLS;
+        for (int kb = 0; kb < KB; ++kb) {
+          if (kb > 0) {
+            mbar_wait_sleep(BAR(R_FULL + stage), ph);
+            tc_fence_after();
+          }
+          if (elect_one()) {
+            const uint64_t bdesc = sdesc_sw128(sR + stage * kUTile);
 #pragma unroll
-          for (int ks = 0; ks < 4 * KB; ++ks)  // K steps of 16 (zero padding beyond d skipped)
-            if (ks < ksteps) mma_f16_ts(d, tmem + C::A_TMEM + 8 * ks, bdesc + koff(ks), idesc, ks != 0);
-          mma_commit(BAR(R_EMPTY + stage));
-          mma_commit(BAR(ACC_FULL + as));
+            for (int kk = 0; kk < 4; ++kk)  // K steps of 16 (zero padding beyond d skipped)
+              if (4 * kb + kk < ksteps)
+                mma_f16_ts(d, tmem + C::A_TMEM + 8 * (4 * kb + kk), bdesc + (uint64_t)(2 * kk), idesc, (kb | kk) != 0);
+            mma_commit(BAR(R_EMPTY + stage));
+          }
+          __syncwarp();
+          if (++stage == NST) stage = 0, ph ^= 1;
         }
+        if (elect_one()) mma_commit(BAR(ACC_FULL + as));
         __syncwarp();
         ++tiles_issued;
-        if (++stage == NST) stage = 0, ph ^= 1;
         if (++as == NACC) as = 0, aph ^= 1;
       }
     }
