@@ -240,12 +240,39 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   double* urow = ssel + (size_t)w * pd;
   unsigned long long my_total = 0;
-  for (int64_t row = blockIdx.x * (int64_t)wpb + w; row < n; row += (int64_t)gridDim.x * wpb) {
-    const int cnt = ccount[row];
+  // the next row's count, first two rounds of candidate positions and user values are loaded one
+  // row ahead (the chain count -> positions -> item rows is otherwise three dependent latencies)
+  const int64_t stride = (int64_t)gridDim.x * wpb;
+  int64_t row = blockIdx.x * (int64_t)wpb + w;
+  int cnt_n = -1, pn0 = 0, pn1 = 0;
+  float un[8];
+  auto prefetch = [&](int64_t r) {
+    if (r < n) {
+      cnt_n = ccount[r];
+      pn0 = cand[r * kCand + lane];
+      pn1 = cand[r * kCand + 32 + lane];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int t = lane + 32 * i;
+        un[i] = t < d ? U32[r * d + t] : 0.f;
+      }
+    }
+  };
+  prefetch(row);
+  for (; row < n; row += stride) {
+    const int cnt = cnt_n, pc0 = pn0, pc1 = pn1;
+    float uc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) uc[i] = un[i];
+    prefetch(row + stride);
     if (cnt < 0) continue;  // overflowed: k_exact_row_full
     my_total += cnt;
     __syncwarp();
-    for (int t = lane; t < pd; t += 32) urow[t] = t < d ? (double)U32[row * d + t] : 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int t = lane + 32 * i;
+      if (t < pd) urow[t] = (double)uc[i];  // zero padding for d <= t < pd
+    }
     __syncwarp();
     SelKey key[4];
 #pragma unroll
@@ -257,7 +284,7 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
       if (32 * i >= cnt) break;  // warp-uniform
       const int c = 32 * i + lane;
       if (c < cnt) {
-        const int pos = cand[row * kCand + c];
+        const int pos = i == 0 ? pc0 : i == 1 ? pc1 : cand[row * kCand + c];
         const float4* pr = reinterpret_cast<const float4*>(P32 + (int64_t)pos * pd);
         double sacc = 0.0;  // dot64: left-to-right fp64 sum of exact fp32 x fp32 products
 #pragma unroll 4
