@@ -119,6 +119,8 @@ CASES = [
     (7, 1000, 600, 50, 10, 5, "uniform", 30),
     (8, 130, 7, 12, 10, 9, "gaussian", 12),     # m < k_max, k > m
     (9, 333, 250, 128, 20, 7, "skewed", 20),
+    (10, 300, 260, 90, 12, 6, "gaussian", 20),   # d_pad 128, 6 K steps: 32-column tail K block (SW64)
+    (11, 270, 140, 100, 9, 4, "uniform", 18),    # 7 K steps: full tail K block
 ]
 
 
