@@ -310,13 +310,13 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
           uint2 l0 = group_max16(hA, 0, E0), l1 = group_max16(hA, 1, E1);
           const int as_next = as + 1 == kAcc ? 0 : as + 1;
           const uint32_t aph_next = as + 1 == kAcc ? aph ^ 1 : aph;
-          mbar_wait(BAR(ACC_FULL + as_next), aph_next);  // the main pass follows: always a next stage
-          tc_fence_after();
-          tmem_ld64(tq + as_next * kBN, hA);
           tmem_ld_wait64(hB);
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
+          if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));  // released before the next tile is awaited
+          mbar_wait(BAR(ACC_FULL + as_next), aph_next);  // the main pass follows: always a next stage
+          tc_fence_after();
+          tmem_ld64(tq + as_next * kBN, hA);
           as = as_next;
           aph = aph_next;
           const uint2 l2 = group_max16(hB, 0, E2), l3 = group_max16(hB, 1, E3);
@@ -350,22 +350,24 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         const bool more = it + 1 < nit;
         int as_next = as + 1 == kAcc ? 0 : as + 1;
         uint32_t aph_next = as + 1 == kAcc ? aph ^ 1 : aph;
-        if (more) {                             // first half of the next tile
-          mbar_wait(BAR(ACC_FULL + as_next), aph_next);
-          tc_fence_after();
-          tmem_ld64(tq + as_next * kBN, hA);
-        }
-        // (the wait sits after the prefetch so that no use of hB can be scheduled before it; waiting
-        // before the prefetch measured 2 % slower)
+        // The stage is released as soon as this tile is done (before the next tile's accumulator is
+        // awaited): the MMA may then run up to kAcc tiles ahead.  (Prefetching the next tile's first
+        // half before the release measured 5 % slower: it delays the release past the next tile's
+        // completion, and the MMA -> epilogue -> MMA round trip then throttles the tensor pipe.)
         tmem_ld_wait64(hB);
         bits |= epi_fast(hB, E[2], E[3], me.theta) << 2;
         if (bits) me = epi_slow(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, sm, rloc, e0x2, kmax);
         tc_fence_before();                      // this stage is no longer read: release it
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
+        if (more) {                             // first half of the next tile
+          mbar_wait(BAR(ACC_FULL + as_next), aph_next);
+          tc_fence_after();
+          tmem_ld64(tq + as_next * kBN, hA);
+          tmem_ld_wait64(hA);
+        }
         as = as_next;
         aph = aph_next;
-        if (more) tmem_ld_wait64(hA);  // (completed with hB's wait; re-anchors hA's uses)
 #ifdef RMIPS_EPI_PROFILE
         if (lane == 0) atomicAdd(&g_epi_prof[1][pb], (unsigned long long)(clock64() - t1));
 #endif

@@ -309,20 +309,22 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         const bool more = it + 1 < nit;
         const int as_next = as + 1 == NACC ? 0 : as + 1;
         const uint32_t aph_next = as + 1 == NACC ? aph ^ 1 : aph;
-        if (more) {                               // first half of the next tile
-          mbar_wait(BAR(ACC_FULL + as_next), aph_next);
-          tc_fence_after();
-          tmem_ld64(tq + as_next * C::ACC_COLS, hA);
-        }
+        // the stage is released as soon as this tile is done, before the next tile's accumulator is
+        // awaited (build_tc.cu: the MMA may then run NACC tiles ahead)
         tmem_ld_wait64(hB);
         bits |= epiq_fast(hB, E[2], E[3], me.theta) << 2;
         if (bits) me = epiq_slow<Pol>(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, sb, rr, e0x2, kmax);
         tc_fence_before();                        // this stage is no longer read: release it
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
+        if (more) {                               // first half of the next tile
+          mbar_wait(BAR(ACC_FULL + as_next), aph_next);
+          tc_fence_after();
+          tmem_ld64(tq + as_next * C::ACC_COLS, hA);
+          tmem_ld_wait64(hA);
+        }
         as = as_next;
         aph = aph_next;
-        if (more) tmem_ld_wait64(hA);
         if ((it + 1) % kCsEvery == 0 && more) {
           // every item from tile it + 1 on has scaled true score <= pnn (1 + 2^-16)
           const uint32_t mk = __reduce_min_sync(0xffffffffu, f2key(me.theta));
