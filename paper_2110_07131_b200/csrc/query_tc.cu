@@ -381,21 +381,45 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     uint32_t aph = 0;
     int s, t;
     first_item(s, t);
+    // the per-item inputs (Lemma 3 prefix, the row's threshold, the sub-batch scale and error
+    // bounds) are loaded one work item ahead, so their latency hides behind the current item
+    int p_len = 0;
+    float p_sc = 0.f, p_thr = 0.f, p_qe[8];
+    auto preload = [&](int64_t w_, int s_, int t_) {
+      if (w_ >= nwork) return;
+      p_len = __ldg(wlen + w_);
+      p_sc = __ldg(qscale + s_);
+      const int64_t r_ = (int64_t)t_ * kBM + rloc;
+      p_thr = r_ < n ? __ldg(thrk + r_) : 0.f;
+      const float* qs_ = qerr + (int64_t)s_ * kQB;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) p_qe[c] = __ldg(qs_ + 32 * c);
+    };
+    preload(blockIdx.x, s, t);
     for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x, next_item(s, t)) {
-      const int len = __ldg(wlen + w);
+      const int len = p_len;
+      const float sc = p_sc, thr_raw = p_thr;
+      float qe[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) qe[c] = p_qe[c];
+      {
+        int s2 = s, t2 = t;
+        next_item(s2, t2);
+        preload(w + gridDim.x, s2, t2);
+      }
       if (len == 0) continue;
       const int64_t row = (int64_t)t * kBM + rloc;
       const bool live = row < n;
-      const float sc = __ldg(qscale + s);
-      const float thr_s = live ? __ldg(thrk + row) * sc : CUDART_INF_F;  // dead rows reject everything
+      const float thr_s = live ? thr_raw * sc : CUDART_INF_F;  // dead rows reject everything
       const float thr_abs = fabsf(thr_s) * 2.384185791015625e-07f;
       const float* qe_sub = qerr + (int64_t)s * kQB;
       const int hlen = min(128, max(0, len - 128 * hsel));  // scored columns of this warp's half
       if (live) n_scored += hlen;
       // qerr is non-increasing along the norm-sorted slots: a chunk's first slot bounds it
+      // (chunks at or beyond len are masked below, so their entries never matter)
       float Emax[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) Emax[c] = __fadd_ru(__ldg(qe_sub + (32 * c < len ? 32 * c : 0)), thr_abs);
+      for (int c = 0; c < 8; ++c) Emax[c] = __fadd_ru(qe[c], thr_abs);
       {
         QPROF_T0();
         mbar_wait(BAR(ACC_FULL + as), aph);
