@@ -231,22 +231,40 @@ __device__ __forceinline__ void warp_bitonic(SelKey (&key)[E]) {
 }
 
 constexpr int kSelWarps = 8;
+constexpr int kSelRows = 32;  // rows per CTA block: each rank's 32 outputs are written as one coalesced run
+// One CTA per block of kSelRows consecutive rows (warp w takes rows w, w + 8, ...); a warp
+// evaluates one row at a time: one candidate per lane per round (16-byte loads of the
+// sector-padded item row; the zero padding adds fma(0, 0, s) = s exactly, s never -0), then a
+// bitonic sort (value desc, original id asc).  The sorted lists are staged in shared memory
+// [rank][row] and written per rank as one contiguous run of the block's rows: the column-major
+// tables (tau, ids, thr: rank-major, users contiguous) then take full sectors instead of one
+// 4- or 8-byte piece of a sector per (row, rank).
 __global__ void __launch_bounds__(32 * kSelWarps)
 k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, const int32_t* __restrict__ perm_p,
                const float* __restrict__ unu, const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount,
                int64_t n, int d, int pd, int kmax, double* __restrict__ tau, int32_t* __restrict__ ids,
                float* __restrict__ thr, unsigned long long* __restrict__ cand_total) {
-  extern __shared__ double ssel[];  // per warp: the user row [pd], widened to fp64 once, zero-padded
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  // shared: per warp the user row [pd] (fp64, zero-padded); the block's staged lists
+  extern __shared__ double ssel[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int kc = kmax < kCand ? kmax : kCand;  // ranks staged (beyond kCand: -inf, only when m < k_max)
   double* urow = ssel + (size_t)w * pd;
+  double* stau = ssel + (size_t)kSelWarps * pd;                    // [kc][kSelRows]
+  int32_t* sids = reinterpret_cast<int32_t*>(stau + (size_t)kc * kSelRows);
+  float* sthr = reinterpret_cast<float*>(sids + (size_t)kc * kSelRows);
   unsigned long long my_total = 0;
+  const int64_t nblk = (n + kSelRows - 1) / kSelRows;
+  constexpr int kPer = kSelRows / kSelWarps;  // rows per warp per block
   // the next row's count, first two rounds of candidate positions and user values are loaded one
   // row ahead (the chain count -> positions -> item rows is otherwise three dependent latencies)
-  const int64_t stride = (int64_t)gridDim.x * wpb;
-  int64_t row = blockIdx.x * (int64_t)wpb + w;
+  auto row_of = [&](int64_t q) {  // q-th row of this warp: block blockIdx.x + (q / kPer) gridDim.x
+    const int64_t b = blockIdx.x + (q / kPer) * (int64_t)gridDim.x;
+    return b * kSelRows + w + kSelWarps * (int)(q % kPer);
+  };
   int cnt_n = -1, pn0 = 0, pn1 = 0;
   float un[8];
   auto prefetch = [&](int64_t r) {
+    cnt_n = -1;
     if (r < n) {
       cnt_n = ccount[r];
       pn0 = cand[r * kCand + lane];
@@ -258,77 +276,90 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
       }
     }
   };
-  prefetch(row);
-  for (; row < n; row += stride) {
-    const int cnt = cnt_n, pc0 = pn0, pc1 = pn1;
-    float uc[8];
+  int64_t q = 0;
+  prefetch(row_of(0));
+  for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    for (int j = 0; j < kPer; ++j, ++q) {
+      const int64_t row = row_of(q);
+      const int rloc = w + kSelWarps * j;
+      const int cnt = cnt_n, pc0 = pn0, pc1 = pn1;
+      float uc[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) uc[i] = un[i];
-    prefetch(row + stride);
-    if (cnt < 0) continue;  // overflowed: k_exact_row_full
-    my_total += cnt;
-    __syncwarp();
+      for (int i = 0; i < 8; ++i) uc[i] = un[i];
+      prefetch(row_of(q + 1));
+      if (row >= n) continue;
+      if (cnt < 0) {  // overflowed: k_exact_row_full rewrites the row after this kernel
+        for (int r = lane; r < kc; r += 32) stau[r * kSelRows + rloc] = -CUDART_INF, sids[r * kSelRows + rloc] = -1,
+                                            sthr[r * kSelRows + rloc] = -CUDART_INF_F;
+        continue;
+      }
+      my_total += cnt;
+      __syncwarp();
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int t = lane + 32 * i;
-      if (t < pd) urow[t] = (double)uc[i];  // zero padding for d <= t < pd
-    }
-    __syncwarp();
-    SelKey key[4];
+      for (int i = 0; i < 8; ++i) {
+        const int t = lane + 32 * i;
+        if (t < pd) urow[t] = (double)uc[i];  // zero padding for d <= t < pd
+      }
+      __syncwarp();
+      SelKey key[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) key[i].v = -CUDART_INF, key[i].id = 0x7fffffff;
-    // one candidate per lane per round, 16-byte loads of the sector-padded item row.  The zero
-    // padding adds fma(0, 0, s) = s exactly (s is never -0: it starts at +0).
+      for (int i = 0; i < 4; ++i) key[i].v = -CUDART_INF, key[i].id = 0x7fffffff;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (32 * i >= cnt) break;  // warp-uniform
-      const int c = 32 * i + lane;
-      if (c < cnt) {
-        const int pos = i == 0 ? pc0 : i == 1 ? pc1 : cand[row * kCand + c];
-        const float4* pr = reinterpret_cast<const float4*>(P32 + (int64_t)pos * pd);
-        double sacc = 0.0;  // dot64: left-to-right fp64 sum of exact fp32 x fp32 products
+      for (int i = 0; i < 4; ++i) {
+        if (32 * i >= cnt) break;  // warp-uniform
+        const int c = 32 * i + lane;
+        if (c < cnt) {
+          const int pos = i == 0 ? pc0 : i == 1 ? pc1 : cand[row * kCand + c];
+          const float4* pr = reinterpret_cast<const float4*>(P32 + (int64_t)pos * pd);
+          double sacc = 0.0;  // dot64: left-to-right fp64 sum of exact fp32 x fp32 products
 #pragma unroll 4
-        for (int t = 0; t < pd / 4; ++t) {
-          const float4 a = __ldg(pr + t);
-          sacc = __fma_rn((double)a.x, urow[4 * t], sacc);
-          sacc = __fma_rn((double)a.y, urow[4 * t + 1], sacc);
-          sacc = __fma_rn((double)a.z, urow[4 * t + 2], sacc);
-          sacc = __fma_rn((double)a.w, urow[4 * t + 3], sacc);
+          for (int t = 0; t < pd / 4; ++t) {
+            const float4 a = __ldg(pr + t);
+            sacc = __fma_rn((double)a.x, urow[4 * t], sacc);
+            sacc = __fma_rn((double)a.y, urow[4 * t + 1], sacc);
+            sacc = __fma_rn((double)a.z, urow[4 * t + 2], sacc);
+            sacc = __fma_rn((double)a.w, urow[4 * t + 3], sacc);
+          }
+          key[i].v = sacc;
+          key[i].id = perm_p[pos];
         }
-        key[i].v = sacc;
-        key[i].id = perm_p[pos];
       }
-    }
-    if (cnt <= 32) {  // one key per lane: 15 compare-exchange steps instead of 21 (64) or 28 (128)
-      SelKey k1[1] = {key[0]};
-      warp_bitonic<1>(k1);
-      key[0] = k1[0];
-    } else if (cnt <= 64) {
-      SelKey k2[2] = {key[0], key[1]};
-      warp_bitonic<2>(k2);
-      key[0] = k2[0];
-      key[1] = k2[1];
-    } else {
-      warp_bitonic<4>(key);
-    }
-    const float nu = unu[row];
+      if (cnt <= 32) {  // one key per lane: 15 compare-exchange steps instead of 21 (64) or 28 (128)
+        SelKey k1[1] = {key[0]};
+        warp_bitonic<1>(k1);
+        key[0] = k1[0];
+      } else if (cnt <= 64) {
+        SelKey k2[2] = {key[0], key[1]};
+        warp_bitonic<2>(k2);
+        key[0] = k2[0];
+        key[1] = k2[1];
+      } else {
+        warp_bitonic<4>(key);
+      }
+      const float nu = unu[row];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int rank = i * 32 + lane;
-      if (rank < kmax) {
-        const bool ok = rank < cnt;
-        tau[(int64_t)rank * n + row] = ok ? key[i].v : -CUDART_INF;
-        ids[(int64_t)rank * n + row] = ok ? key[i].id : -1;
-        thr[(int64_t)rank * n + row] = ok ? (float)(key[i].v / (double)nu) : -CUDART_INF_F;
+      for (int i = 0; i < 4; ++i) {
+        const int rank = i * 32 + lane;
+        if (rank < kc) {
+          const bool ok = rank < cnt;
+          stau[rank * kSelRows + rloc] = ok ? key[i].v : -CUDART_INF;
+          sids[rank * kSelRows + rloc] = ok ? key[i].id : -1;
+          sthr[rank * kSelRows + rloc] = ok ? (float)(key[i].v / (double)nu) : -CUDART_INF_F;
+        }
       }
     }
-    if (kmax > 128 && lane == 0) {  // k_max beyond the candidate buffer: only when m < k_max
-      for (int r = 128; r < kmax; ++r) {
-        tau[(int64_t)r * n + row] = -CUDART_INF;
-        ids[(int64_t)r * n + row] = -1;
-        thr[(int64_t)r * n + row] = -CUDART_INF_F;
-      }
+    __syncthreads();  // the block's lists are staged: one coalesced run per rank
+    const int64_t r0 = b * kSelRows;
+    const int nr = (int)(n - r0 < kSelRows ? n - r0 : kSelRows);
+    for (int e = threadIdx.x; e < kmax * kSelRows; e += blockDim.x) {
+      const int rank = e / kSelRows, r = e % kSelRows;
+      if (r >= nr) continue;
+      const bool st = rank < kc;
+      tau[(int64_t)rank * n + r0 + r] = st ? stau[rank * kSelRows + r] : -CUDART_INF;
+      ids[(int64_t)rank * n + r0 + r] = st ? sids[rank * kSelRows + r] : -1;
+      thr[(int64_t)rank * n + r0 + r] = st ? sthr[rank * kSelRows + r] : -CUDART_INF_F;
     }
+    __syncthreads();  // before the next block's lists overwrite the stage
   }
   if (lane == 0 && my_total) atomicAdd(cand_total, my_total);
 }
@@ -485,10 +516,15 @@ size_t build_cub_bytes(int64_t n, int64_t m) {
 cudaError_t build_select(BuildCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   if (x->n == 0) return cudaSuccess;
-  const size_t smem = (size_t)kSelWarps * x->pd * sizeof(double);
+  const int kc = x->kmax < kCand ? x->kmax : kCand;
+  const size_t smem = (size_t)kSelWarps * x->pd * sizeof(double) + (size_t)kc * kSelRows * (8 + 4 + 4);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_exact_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->device);
-  const int64_t want = (x->n + kSelWarps - 1) / kSelWarps;
+  const int64_t want = (x->n + kSelRows - 1) / kSelRows;
   const int grid = (int)(want < (int64_t)sms * 8 ? want : (int64_t)sms * 8);
   k_exact_select<<<grid, 32 * kSelWarps, smem, st>>>(x->U32, x->P32, x->perm_p, x->unu, c.cand, c.ccount, x->n,
                                                      x->d, x->pd, x->kmax, x->tau, x->ids, x->thr, c.cand_total);
