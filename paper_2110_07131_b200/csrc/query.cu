@@ -15,10 +15,9 @@
 namespace rmips {
 
 // ------------------------------------------------------------------------------ Q1
-// One CTA (8 warps) per 256-query sub-batch.  Warps compute the norms of 32 queries each with
-// coalesced row loads and a warp reduction (the norm is only used rounded up, so the summation
-// order does not matter); every thread then ranks its query in (norm desc, index asc) order, and
-// the warps write the fp16 rows (q * 2^eq, zero-padded to d_pad) cooperatively.
+// One CTA (256 threads) per 256-query sub-batch.  Thread t computes the norm of query t; every
+// thread then ranks its query in (norm desc, index asc) order, and all threads write the fp16 rows
+// (q * 2^eq, zero-padded to d_pad) element-parallel.
 __global__ void __launch_bounds__(kQB)
 k_query_prep(const float* __restrict__ q, int b, int d, int dpad, double c1, double c2, __half* __restrict__ Q16,
              float* __restrict__ qn, float* __restrict__ qerr, float* __restrict__ qscale,
@@ -30,27 +29,23 @@ k_query_prep(const float* __restrict__ q, int b, int d, int dpad, double c1, dou
   const int s = blockIdx.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int cnt = min(kQB, b - s * kQB);
   float mx = 0.f;
-  for (int j = 0; j < 32; ++j) {  // warp wid: queries wid * 32 + j
-    const int slot = wid * 32 + j;
+  {  // thread t: the norm of query t of the sub-batch (a sequential fp64 sum; only its rounded-up
+     // value is used, so the order does not matter)
     double acc = 0.0;
     bool fin = true;
-    if (slot < cnt) {
-      const float* x = q + (int64_t)(s * kQB + slot) * d;
-      for (int e = lane; e < d; e += 32) {
+    if (t < cnt) {
+      const float* x = q + (int64_t)(s * kQB + t) * d;
+#pragma unroll 4
+      for (int e = 0; e < d; ++e) {
         const float v = x[e];
         fin &= isfinite(v);
         mx = fmaxf(mx, fabsf(v));
         acc = __fma_rn((double)v, (double)v, acc);
       }
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    fin = __all_sync(0xffffffffu, fin);
-    if (lane == 0) {
-      double nr = slot < cnt ? sqrt(acc) : -1.0;
-      if (slot < cnt && !fin) atomicOr(flags, kFlagNonfinite), nr = 0.0;
-      nrm[slot] = nr;
-    }
+    double nr = t < cnt ? sqrt(acc) : -1.0;
+    if (t < cnt && !fin) atomicOr(flags, kFlagNonfinite), nr = 0.0;
+    nrm[t] = nr;
   }
   for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if (lane == 0) smax[wid] = isfinite(mx) ? mx : 0.f;
@@ -90,12 +85,11 @@ k_query_prep(const float* __restrict__ q, int b, int d, int dpad, double c1, dou
       qerr[slot] = 0.f;
     }
   }
-  for (int j = 0; j < 32; ++j) {  // warp wid writes the fp16 rows of its 32 queries (coalesced)
-    const int src = wid * 32 + j;
+#pragma unroll 4
+  for (int idx = t; idx < kQB * dpad; idx += kQB) {  // fp16 rows, all threads over (query, element)
+    const int src = idx / dpad, e = idx - src * dpad;
     const int64_t slot = (int64_t)s * kQB + srank[src];
-    const float* x = q + (int64_t)(s * kQB + src) * d;
-    for (int e = lane; e < dpad; e += 32)
-      Q16[slot * dpad + e] = __float2half_rn(src < cnt && e < d ? x[e] * scale : 0.f);
+    Q16[slot * dpad + e] = __float2half_rn(src < cnt && e < d ? q[(int64_t)(s * kQB + src) * d + e] * scale : 0.f);
   }
 }
 
