@@ -230,8 +230,102 @@ __device__ __forceinline__ void warp_bitonic(SelKey (&key)[E]) {
   }
 }
 
+// Fast path of the same sort: the value alone as an order-preserving 64-bit integer (larger key =
+// larger value; dot64 never returns -0, so key equality is value equality) with the id carried
+// along.  One unsigned compare and three selects per compare-exchange instead of the two-field
+// comparator.  Ties in value are left in an unspecified id order, so the caller checks the sorted
+// run for adjacent equal keys and re-sorts with warp_bitonic when it finds one.
+__device__ __forceinline__ uint64_t sel_okey(double v) {
+  const uint64_t b = (uint64_t)__double_as_longlong(v);
+  return b ^ ((b >> 63) ? ~0ull : (1ull << 63));
+}
+__device__ __forceinline__ double sel_oval(uint64_t k) {
+  return __longlong_as_double((long long)(k ^ ((k >> 63) ? (1ull << 63) : ~0ull)));
+}
+template <int E>
+__device__ __forceinline__ void warp_bitonic_u64(uint64_t (&key)[E], int (&id)[E]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int ip = i ^ (j >> 5);
+          if (ip > i) {
+            const bool up = ((i * 32 + lane) & k) == 0;
+            const bool sw = up == (key[ip] > key[i]);
+            const uint64_t a = key[i], b = key[ip];
+            const int ia = id[i], ib = id[ip];
+            key[i] = sw ? b : a;
+            key[ip] = sw ? a : b;
+            id[i] = sw ? ib : ia;
+            id[ip] = sw ? ia : ib;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, key[i], j);
+          const int oi = __shfl_xor_sync(0xffffffffu, id[i], j);
+          // keep the larger key at the lower index of an ascending-best block, the smaller otherwise
+          // (equal keys: the two lanes of a pair may both take, duplicating one id; the caller's
+          // tie check then re-sorts from its own copy of the unsorted keys)
+          const bool keep_big = ((((i * 32 + lane) & k) == 0) == ((lane & j) == 0));
+          const bool take = keep_big == (o > key[i]);
+          key[i] = take ? o : key[i];
+          id[i] = take ? oi : id[i];
+        }
+      }
+    }
+  }
+}
+
+// Sort the first E*32 keys of key[] best first: the integer fast path, then (only when two real
+// keys share a value) the two-field comparator from the unsorted copy.
+template <int E>
+__device__ __forceinline__ void sel_sort(SelKey (&key)[4], int cnt) {
+  const int lane = threadIdx.x & 31;
+  uint64_t k[E];
+  int id[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) k[i] = sel_okey(key[i].v), id[i] = key[i].id;
+  warp_bitonic_u64<E>(k, id);
+  bool tie = false;
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const uint64_t dn = __shfl_down_sync(0xffffffffu, k[i], 1);
+    uint64_t nx = dn;
+    if (i + 1 < E) {
+      const uint64_t w0 = __shfl_sync(0xffffffffu, k[i + 1 < E ? i + 1 : i], 0);
+      if (lane == 31) nx = w0;
+    }
+    tie |= (i * 32 + lane + 1 < cnt) & (nx == k[i]);
+  }
+  if (__any_sync(0xffffffffu, tie)) {
+    SelKey kk[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) kk[i] = key[i];
+    warp_bitonic<E>(kk);
+#pragma unroll
+    for (int i = 0; i < E; ++i) key[i] = kk[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < E; ++i) key[i].v = sel_oval(k[i]), key[i].id = id[i];
+  }
+}
+
+// 256-bit read-only global load (LDG.256; the address is 32-byte aligned)
+__device__ __forceinline__ void ldg_nc_v8(const float* p, float (&v)[8]) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+
 constexpr int kSelWarps = 8;
 constexpr int kSelRows = 32;  // rows per CTA block: each rank's 32 outputs are written as one coalesced run
+constexpr int kSelStride = kSelRows + 1;  // odd stage stride: a warp's 32 ranks of one row hit 32 banks
 // One CTA per block of kSelRows consecutive rows (warp w takes rows w, w + 8, ...); a warp
 // evaluates one row at a time: one candidate per lane per round (16-byte loads of the
 // sector-padded item row; the zero padding adds fma(0, 0, s) = s exactly, s never -0), then a
@@ -239,19 +333,23 @@ constexpr int kSelRows = 32;  // rows per CTA block: each rank's 32 outputs are 
 // [rank][row] and written per rank as one contiguous run of the block's rows: the column-major
 // tables (tau, ids, thr: rank-major, users contiguous) then take full sectors instead of one
 // 4- or 8-byte piece of a sector per (row, rank).
+#ifdef RMIPS_SEL_MINB
+__global__ void __launch_bounds__(32 * kSelWarps, RMIPS_SEL_MINB)
+#else
 __global__ void __launch_bounds__(32 * kSelWarps)
+#endif
 k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, const int32_t* __restrict__ perm_p,
                const float* __restrict__ unu, const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount,
                int64_t n, int d, int pd, int kmax, double* __restrict__ tau, int32_t* __restrict__ ids,
                float* __restrict__ thr, unsigned long long* __restrict__ cand_total) {
   // shared: per warp the user row [pd] (fp64, zero-padded); the block's staged lists
-  extern __shared__ double ssel[];
+  extern __shared__ __align__(16) double ssel[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int kc = kmax < kCand ? kmax : kCand;  // ranks staged (beyond kCand: -inf, only when m < k_max)
   double* urow = ssel + (size_t)w * pd;
-  double* stau = ssel + (size_t)kSelWarps * pd;                    // [kc][kSelRows]
-  int32_t* sids = reinterpret_cast<int32_t*>(stau + (size_t)kc * kSelRows);
-  float* sthr = reinterpret_cast<float*>(sids + (size_t)kc * kSelRows);
+  double* stau = ssel + (size_t)kSelWarps * pd;                    // [kc][kSelStride]
+  int32_t* sids = reinterpret_cast<int32_t*>(stau + (size_t)kc * kSelStride);
+  float* sthr = reinterpret_cast<float*>(sids + (size_t)kc * kSelStride);
   unsigned long long my_total = 0;
   const int64_t nblk = (n + kSelRows - 1) / kSelRows;
   constexpr int kPer = kSelRows / kSelWarps;  // rows per warp per block
@@ -289,8 +387,8 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
       prefetch(row_of(q + 1));
       if (row >= n) continue;
       if (cnt < 0) {  // overflowed: k_exact_row_full rewrites the row after this kernel
-        for (int r = lane; r < kc; r += 32) stau[r * kSelRows + rloc] = -CUDART_INF, sids[r * kSelRows + rloc] = -1,
-                                            sthr[r * kSelRows + rloc] = -CUDART_INF_F;
+        for (int r = lane; r < kc; r += 32) stau[r * kSelStride + rloc] = -CUDART_INF, sids[r * kSelStride + rloc] = -1,
+                                            sthr[r * kSelStride + rloc] = -CUDART_INF_F;
         continue;
       }
       my_total += cnt;
@@ -304,37 +402,41 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
       SelKey key[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) key[i].v = -CUDART_INF, key[i].id = 0x7fffffff;
+      // candidates c and c + 32 of a lane as two interleaved chains (twice the loads in flight)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 4; i += 2) {
         if (32 * i >= cnt) break;  // warp-uniform
-        const int c = 32 * i + lane;
-        if (c < cnt) {
-          const int pos = i == 0 ? pc0 : i == 1 ? pc1 : cand[row * kCand + c];
-          const float4* pr = reinterpret_cast<const float4*>(P32 + (int64_t)pos * pd);
-          double sacc = 0.0;  // dot64: left-to-right fp64 sum of exact fp32 x fp32 products
-#pragma unroll 4
-          for (int t = 0; t < pd / 4; ++t) {
-            const float4 a = __ldg(pr + t);
-            sacc = __fma_rn((double)a.x, urow[4 * t], sacc);
-            sacc = __fma_rn((double)a.y, urow[4 * t + 1], sacc);
-            sacc = __fma_rn((double)a.z, urow[4 * t + 2], sacc);
-            sacc = __fma_rn((double)a.w, urow[4 * t + 3], sacc);
+        const int c0 = 32 * i + lane, c1 = c0 + 32;
+        const bool l0 = c0 < cnt, l1 = c1 < cnt;
+        int pos0 = 0, pos1 = 0;  // inactive lanes read item row 0 and discard it
+        if (l0) pos0 = i == 0 ? pc0 : cand[row * kCand + c0];
+        if (l1) pos1 = i == 0 ? pc1 : cand[row * kCand + c1];
+        const float* pr0 = P32 + (int64_t)pos0 * pd;  // pd = round_up(d, 8): 32-byte rows
+        const float* pr1 = P32 + (int64_t)pos1 * pd;
+        double s0 = 0.0, s1 = 0.0;  // dot64: left-to-right fp64 sums of exact fp32 x fp32 products
+#pragma unroll 2
+        for (int t = 0; t < pd; t += 8) {
+          float a[8], bb[8];
+          ldg_nc_v8(pr0 + t, a);
+          ldg_nc_v8(pr1 + t, bb);
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            const double2 uu = *reinterpret_cast<const double2*>(urow + t + e);
+            s0 = __fma_rn((double)a[e], uu.x, s0);
+            s1 = __fma_rn((double)bb[e], uu.x, s1);
+            s0 = __fma_rn((double)a[e + 1], uu.y, s0);
+            s1 = __fma_rn((double)bb[e + 1], uu.y, s1);
           }
-          key[i].v = sacc;
-          key[i].id = perm_p[pos];
         }
+        if (l0) key[i].v = s0, key[i].id = perm_p[pos0];
+        if (l1) key[i + 1].v = s1, key[i + 1].id = perm_p[pos1];
       }
       if (cnt <= 32) {  // one key per lane: 15 compare-exchange steps instead of 21 (64) or 28 (128)
-        SelKey k1[1] = {key[0]};
-        warp_bitonic<1>(k1);
-        key[0] = k1[0];
+        sel_sort<1>(key, cnt);
       } else if (cnt <= 64) {
-        SelKey k2[2] = {key[0], key[1]};
-        warp_bitonic<2>(k2);
-        key[0] = k2[0];
-        key[1] = k2[1];
+        sel_sort<2>(key, cnt);
       } else {
-        warp_bitonic<4>(key);
+        sel_sort<4>(key, cnt);
       }
       const float nu = unu[row];
 #pragma unroll
@@ -342,9 +444,9 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
         const int rank = i * 32 + lane;
         if (rank < kc) {
           const bool ok = rank < cnt;
-          stau[rank * kSelRows + rloc] = ok ? key[i].v : -CUDART_INF;
-          sids[rank * kSelRows + rloc] = ok ? key[i].id : -1;
-          sthr[rank * kSelRows + rloc] = ok ? (float)(key[i].v / (double)nu) : -CUDART_INF_F;
+          stau[rank * kSelStride + rloc] = ok ? key[i].v : -CUDART_INF;
+          sids[rank * kSelStride + rloc] = ok ? key[i].id : -1;
+          sthr[rank * kSelStride + rloc] = ok ? (float)(key[i].v / (double)nu) : -CUDART_INF_F;
         }
       }
     }
@@ -355,9 +457,9 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
       const int rank = e / kSelRows, r = e % kSelRows;
       if (r >= nr) continue;
       const bool st = rank < kc;
-      tau[(int64_t)rank * n + r0 + r] = st ? stau[rank * kSelRows + r] : -CUDART_INF;
-      ids[(int64_t)rank * n + r0 + r] = st ? sids[rank * kSelRows + r] : -1;
-      thr[(int64_t)rank * n + r0 + r] = st ? sthr[rank * kSelRows + r] : -CUDART_INF_F;
+      tau[(int64_t)rank * n + r0 + r] = st ? stau[rank * kSelStride + r] : -CUDART_INF;
+      ids[(int64_t)rank * n + r0 + r] = st ? sids[rank * kSelStride + r] : -1;
+      thr[(int64_t)rank * n + r0 + r] = st ? sthr[rank * kSelStride + r] : -CUDART_INF_F;
     }
     __syncthreads();  // before the next block's lists overwrite the stage
   }
@@ -517,7 +619,7 @@ cudaError_t build_select(BuildCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   if (x->n == 0) return cudaSuccess;
   const int kc = x->kmax < kCand ? x->kmax : kCand;
-  const size_t smem = (size_t)kSelWarps * x->pd * sizeof(double) + (size_t)kc * kSelRows * (8 + 4 + 4);
+  const size_t smem = (size_t)kSelWarps * x->pd * sizeof(double) + (size_t)kc * kSelStride * (8 + 4 + 4);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_exact_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
