@@ -18,23 +18,34 @@ namespace rmips {
 
 // ------------------------------------------------------------------------------ B1
 // keys[r] = bits of the fp64 norm (non-negative, so its bits order like the value) | topbit.
-__global__ void k_norms(const float* __restrict__ X, int64_t rows, int d, uint64_t* __restrict__ keys,
-                        uint64_t topbit, int* __restrict__ flags, unsigned int* __restrict__ maxabs_bits) {
-  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// A CTA stages its kNormRows rows in shared memory with coalesced loads (odd row stride: no bank
+// conflicts), then each thread sums its own row left to right (the oracle's order).
+constexpr int kNormRows = 128;
+__global__ void __launch_bounds__(kNormRows)
+k_norms(const float* __restrict__ X, int64_t rows, int d, uint64_t* __restrict__ keys,
+        uint64_t topbit, int* __restrict__ flags, unsigned int* __restrict__ maxabs_bits) {
+  extern __shared__ float xs[];
+  const int ds = d | 1;
+  const int64_t r0 = blockIdx.x * (int64_t)kNormRows;
+  const int nr = (int)(rows - r0 < kNormRows ? rows - r0 : kNormRows);
+  const float* src = X + r0 * d;
   float mx = 0.f;
-  if (r < rows) {
-    const float* x = X + r * d;
-    double s = 0.0;
-    bool fin = true;
-    for (int j = 0; j < d; ++j) {
-      float v = x[j];
-      fin &= isfinite(v);
-      mx = fmaxf(mx, fabsf(v));
-      s = __fma_rn((double)v, (double)v, s);
-    }
-    keys[r] = (uint64_t)__double_as_longlong(sqrt(s)) | topbit;
-    if (!fin) atomicOr(flags, kFlagNonfinite);
+  bool fin = true;
+  for (int e = threadIdx.x; e < nr * d; e += kNormRows) {
+    const float v = src[e];
+    fin &= isfinite(v);
+    mx = fmaxf(mx, fabsf(v));
+    const int rr = e / d;
+    xs[rr * ds + (e - rr * d)] = v;
   }
+  __syncthreads();
+  if (threadIdx.x < nr) {
+    const float* x = xs + threadIdx.x * ds;
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) s = __fma_rn((double)x[j], (double)x[j], s);
+    keys[r0 + threadIdx.x] = (uint64_t)__double_as_longlong(sqrt(s)) | topbit;
+  }
+  if (__any_sync(0xffffffffu, !fin) && (threadIdx.x & 31) == 0) atomicOr(flags, kFlagNonfinite);
   if (maxabs_bits) {
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0 && isfinite(mx)) atomicMax(maxabs_bits, __float_as_uint(mx));
@@ -59,48 +70,56 @@ __global__ void k_split_sorted(const uint64_t* __restrict__ keys, const int32_t*
 
 // ------------------------------------------------------------------------------ B3
 // Users: U16 = fp16(u / nu), nu = fp32(||u||) (1 for the zero vector); U32 = u (permuted).
+// One warp per row: lane l handles the column pairs 2l, 2l + 64, ... (coalesced reads and writes).
 __global__ void k_prep_users(const float* __restrict__ Q, int64_t n, int d, int dpad,
                              const int32_t* __restrict__ perm, const double* __restrict__ norm_sorted,
                              __half* __restrict__ U16, float* __restrict__ U32, float* __restrict__ unu) {
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= n * dpad) return;
-  int64_t r = idx / dpad;
-  int j = (int)(idx - r * dpad);
-  int64_t o = perm[r];
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  const int64_t o = perm[r];
   float nu = (float)norm_sorted[r];
   if (!(nu > 0.f)) nu = 1.f;
   if (isinf(nu)) nu = 3.0e38f;
-  float x = j < d ? Q[o * d + j] : 0.f;
-  U16[idx] = __float2half_rn(x / nu);
-  if (j < d) U32[r * d + j] = x;
-  if (j == 0) unu[r] = nu;
+  const float* q = Q + o * d;
+  for (int j = 2 * lane; j < dpad; j += 64) {
+    const float x0 = j < d ? q[j] : 0.f, x1 = j + 1 < d ? q[j + 1] : 0.f;
+    reinterpret_cast<__half2*>(U16 + r * dpad)[j >> 1] = __halves2half2(__float2half_rn(x0 / nu), __float2half_rn(x1 / nu));
+    if (j < d) U32[r * d + j] = x0;
+    if (j + 1 < d) U32[r * d + j + 1] = x1;
+  }
+  if (lane == 0) unu[r] = nu;
 }
 
 // Items: P16 = fp16(p * 2^e) with max|p*2^e| < 2^14; perr = filter error bound (scaled units).
+// One warp per row as above; P32 is zero-padded to pd (a multiple of 8, <= dpad).
 __global__ void k_prep_items(const float* __restrict__ P, int64_t m, int d, int dpad, int pd,
                              const int32_t* __restrict__ perm, const double* __restrict__ norm_sorted,
                              const unsigned int* __restrict__ maxabs_bits, double c1, double c2,
                              __half* __restrict__ P16, float* __restrict__ P32, float* __restrict__ perr,
                              float* __restrict__ scale_out) {
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= m * dpad) return;
-  float mx = __uint_as_float(*maxabs_bits);
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= m) return;
+  const float mx = __uint_as_float(*maxabs_bits);
   int ex = 0;
   if (mx > 0.f) frexpf(mx, &ex);               // mx < 2^ex
   int e = 14 - ex;
   e = max(-126, min(126, e));
-  float scale = ldexpf(1.f, e);
-  int64_t r = idx / dpad;
-  int j = (int)(idx - r * dpad);
-  int64_t o = perm[r];
-  float x = j < d ? P[o * d + j] : 0.f;
-  P16[idx] = __float2half_rn(x * scale);
-  if (j < pd) P32[r * pd + j] = x;  // zero padding up to pd
-  if (j == 0) {
-    double b = norm_sorted[r] * (double)scale;
-    perr[r] = __double2float_ru((c1 * b + c2) * (1.0 + 1e-6));
+  const float scale = ldexpf(1.f, e);
+  const int64_t o = perm[r];
+  const float* p = P + o * d;
+  for (int j = 2 * lane; j < dpad; j += 64) {
+    const float x0 = j < d ? p[j] : 0.f, x1 = j + 1 < d ? p[j + 1] : 0.f;
+    reinterpret_cast<__half2*>(P16 + r * dpad)[j >> 1] = __halves2half2(__float2half_rn(x0 * scale), __float2half_rn(x1 * scale));
+    if (j < pd) P32[r * pd + j] = x0;
+    if (j + 1 < pd) P32[r * pd + j + 1] = x1;
   }
-  if (idx == 0) *scale_out = scale;
+  if (lane == 0) {
+    const double b = norm_sorted[r] * (double)scale;
+    perr[r] = __double2float_ru((c1 * b + c2) * (1.0 + 1e-6));
+    if (r == 0) *scale_out = scale;
+  }
 }
 
 // ------------------------------------------------------------------------------ B4 (SIMT)
@@ -590,8 +609,13 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
   uint64_t* kout = c.nkey + tot;
   int32_t* vin = c.nval;
   int32_t* vout = c.nval + tot;
-  k_norms<<<nblk(m, 256), 256, 0, st>>>(P, m, d, kin, 1ull << 63, x->d_flags, c.maxabs); count_launch();
-  if (n) k_norms<<<nblk(n, 256), 256, 0, st>>>(Q, n, d, kin + m, 0ull, x->d_flags, nullptr); count_launch();
+  const size_t nsm = (size_t)kNormRows * (d | 1) * sizeof(float);
+  if (nsm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_norms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nsm);
+    if (e != cudaSuccess) return e;
+  }
+  k_norms<<<nblk(m, kNormRows), kNormRows, nsm, st>>>(P, m, d, kin, 1ull << 63, x->d_flags, c.maxabs); count_launch();
+  if (n) k_norms<<<nblk(n, kNormRows), kNormRows, nsm, st>>>(Q, n, d, kin + m, 0ull, x->d_flags, nullptr); count_launch();
   // B2: one stable radix sort (descending norm, ties by ascending index: reading R6)
   k_iota<<<nblk(tot, 256), 256, 0, st>>>(vin, tot); count_launch();
   size_t tb = c.cub_bytes;
@@ -602,8 +626,8 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
   count_launch();
   // B3
   if (n)
-    k_prep_users<<<nblk(n * dpad, 256), 256, 0, st>>>(Q, n, d, dpad, x->perm_u, x->unorm, x->U16, x->U32, x->unu); count_launch();
-  k_prep_items<<<nblk(m * dpad, 256), 256, 0, st>>>(P, m, d, dpad, x->pd, x->perm_p, x->pnorm, c.maxabs, x->c1, x->c2,
+    k_prep_users<<<nblk(n * 32, 256), 256, 0, st>>>(Q, n, d, dpad, x->perm_u, x->unorm, x->U16, x->U32, x->unu); count_launch();
+  k_prep_items<<<nblk(m * 32, 256), 256, 0, st>>>(P, m, d, dpad, x->pd, x->perm_p, x->pnorm, c.maxabs, x->c1, x->c2,
                                                     x->P16, x->P32, x->perr, c.scale_dev); count_launch();
   return cudaGetLastError();
 }

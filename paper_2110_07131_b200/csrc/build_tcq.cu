@@ -64,12 +64,7 @@ __device__ __forceinline__ uint32_t epiq_fast(const uint32_t (&h)[64], float E0,
   uint32_t bits = 0;
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
-    float g4[8];
-#pragma unroll
-    for (int g = 0; g < 8; ++g)
-      g4[g] = fmaxf(fmaxf(__uint_as_float(h[32 * c + 4 * g]), __uint_as_float(h[32 * c + 4 * g + 1])),
-                    fmaxf(__uint_as_float(h[32 * c + 4 * g + 2]), __uint_as_float(h[32 * c + 4 * g + 3])));
-    const float mx = fmaxf(fmaxf(fmaxf(g4[0], g4[1]), fmaxf(g4[2], g4[3])), fmaxf(fmaxf(g4[4], g4[5]), fmaxf(g4[6], g4[7])));
+    const float mx = sm100::max32_bits(h + 32 * c);
     bits |= (uint32_t)__any_sync(0xffffffffu, __fadd_ru(mx, c ? E1 : E0) >= theta) << c;
   }
   return bits;

@@ -443,12 +443,7 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
         for (int c = 0; c < 4; ++c) {
           // columns >= len hold stale or zero values: a spurious flag only costs a slow-path
           // visit, which masks them
-          float g[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            g[i] = fmaxf(fmaxf(__uint_as_float(r[c][4 * i]), __uint_as_float(r[c][4 * i + 1])),
-                         fmaxf(__uint_as_float(r[c][4 * i + 2]), __uint_as_float(r[c][4 * i + 3])));
-          const float mx = fmaxf(fmaxf(fmaxf(g[0], g[1]), fmaxf(g[2], g[3])), fmaxf(fmaxf(g[4], g[5]), fmaxf(g[6], g[7])));
+          const float mx = sm100::max32_bits(r[c]);
           const float em = h ? Emax[4 + c] : Emax[c];
           const bool all_rej = !live || (__fadd_ru(mx, em) < thr_s);
           flag |= (uint32_t)(!__all_sync(0xffffffffu, all_rej)) << (4 * h + c);

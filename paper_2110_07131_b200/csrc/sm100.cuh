@@ -113,6 +113,25 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64
 // One lane of the (converged) warp returns true: the MMA issuer runs its loop with the whole warp
 // so that the loop state and the descriptors stay warp-uniform (uniform registers), and only the
 // elected lane issues the tcgen05 instructions.
+// Three-input fp32 max (FMNMX3, sm_100).
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// Max of 32 fp32 values held as bits: 15 three-input + 1 two-input max (a two-input tree takes 31).
+__device__ __forceinline__ float max32_bits(const uint32_t* h) {
+  float m[12];
+#pragma unroll
+  for (int i = 0; i < 10; ++i)
+    m[i] = fmax3f(__uint_as_float(h[3 * i]), __uint_as_float(h[3 * i + 1]), __uint_as_float(h[3 * i + 2]));
+  m[10] = __uint_as_float(h[30]);
+  m[11] = __uint_as_float(h[31]);
+  const float a = fmax3f(m[0], m[1], m[2]), b = fmax3f(m[3], m[4], m[5]), c = fmax3f(m[6], m[7], m[8]),
+              d = fmax3f(m[9], m[10], m[11]);
+  return fmaxf(fmax3f(a, b, c), d);
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t p;
   asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(p));

@@ -1,0 +1,49 @@
+"""Warm per-kernel device times of one bench-shaped step (build + query) via the CUDA activity
+trace of torch.profiler (CUPTI): unlike the ncu launch list these are not serialised or cold-cache.
+Usage: python tools/kernel_times.py [config] [steps]"""
+import collections
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+from paper_2110_07131_b200 import rmips  # noqa: E402
+from synth.generator import make_workload  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+w = make_workload(cfg)
+dev = torch.device("cuda", 0)
+U = torch.from_numpy(w.U).to(dev)
+P = torch.from_numpy(w.P).to(dev)
+Qy = torch.from_numpy(w.Qy).to(dev)
+k = w.spec.ks[0]
+
+
+def step():
+    idx = rmips.rmips_build_index(U, P, w.spec.k_max)
+    rmips.rmips_query(idx, Qy, k)
+    idx.close()
+
+
+for _ in range(3):
+    step()
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+tot = collections.defaultdict(float)
+cnt = collections.Counter()
+for e in prof.events():
+    if e.device_type == torch.autograd.DeviceType.CUDA:
+        name = e.name if len(e.name) < 70 else e.name[:67] + "..."
+        tot[name] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
+        cnt[name] += 1
+allt = sum(tot.values())
+print("config %d, %d steps, per-step device time by kernel (us):" % (cfg, steps))
+for name, t in sorted(tot.items(), key=lambda kv: -kv[1]):
+    print("%9.1f  %5.1f%%  x%-3d %s" % (t / steps, 100 * t / allt, cnt[name] // steps, name))
+print("%9.1f  total" % (allt / steps))
