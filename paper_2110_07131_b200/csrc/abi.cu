@@ -414,17 +414,26 @@ rmips_status_t rmips_build_index_host(const float* Q, int64_t n, const float* P,
   return s;
 }
 
+constexpr size_t kBitsMaxBytes = (size_t)64 << 20;  // largest bit-matrix output (rmips.h)
+
 static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cudaStream_t st) {
   const int dpad = x->dpad;
   size_t qcub = query_cub_bytes(cap);
+  const size_t qscan = query_scan_bytes(c.b);
+  if (qscan > qcub) qcub = qscan;
+  // accepted pairs as a bit matrix when it is small enough (no key sort, no mid-call sync)
+  const int64_t nw = (x->n + 31) / 32;
+  const bool use_bits = x->n > 0 && !(c.flags & RMIPS_FLAG_KEY_SORT) && (size_t)c.b * (size_t)nw * 4 <= kBitsMaxBytes &&
+                        c.b <= cap;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
   size_t oQ16 = take((size_t)nsub * kQB * dpad * 2), oqn = take((size_t)nsub * kQB * 4),
          oqe = take((size_t)nsub * kQB * 4), oqs = take((size_t)nsub * 4), oqp = take((size_t)nsub * kQB * 4),
          oqc = take((size_t)nsub * 4), owl = take((size_t)nsub * x->nblocks * 4), oacc = take((size_t)cap * 8),
          ound = take((size_t)cap * 8), oscn = take((size_t)cap * 4),
-         osrt = take((size_t)cap * 8), ocub = take(qcub);
+         osrt = take((size_t)cap * 8), ocub = take(qcub), obits = take(use_bits ? (size_t)c.b * nw * 4 : 0);
   if (off > x->ws_bytes) {
+    x->bits_len = 0;
     if (x->ws) cudaFreeAsync(x->ws, st);
     x->ws = nullptr;
     CK(cudaMallocAsync(&x->ws, off, st));
@@ -443,6 +452,17 @@ static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cuda
   c.scan_cnt = reinterpret_cast<int32_t*>(b + oscn);
   c.acc_sorted = reinterpret_cast<uint64_t*>(b + osrt);
   c.cub_tmp = b + ocub;
+  c.bits = use_bits ? reinterpret_cast<uint32_t*>(b + obits) : nullptr;
+  c.nw = nw;
+  // the matrix is left all zero by every completed query (k_bits_emit clears what it reads); it
+  // is cleared here only when its place or size changed, or after a failed call
+  const size_t nbits = use_bits ? (size_t)c.b * nw * 4 : 0;
+  if (!use_bits) x->bits_len = 0;  // this layout may write over the old matrix
+  if (use_bits && (x->bits_off != obits || x->bits_len < nbits)) {
+    CK(cudaMemsetAsync(c.bits, 0, nbits, st));
+    x->bits_off = obits;
+    x->bits_len = nbits;
+  }
   c.cub_bytes = qcub;
   c.cap = cap;
   x->pair_cap = cap;
@@ -457,7 +477,8 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
   if (capacity > 0 && !user_ids) return fail(RMIPS_ERR_INVALID, "NULL user_ids with capacity > 0");
   if (k < 1) return fail(RMIPS_ERR_K_RANGE, "k < 1");
   if (k > idx->kmax && (flags & RMIPS_FLAG_NO_EXTEND)) return fail(RMIPS_ERR_K_RANGE, "k > k_max");
-  if (flags & ~(RMIPS_FLAG_NO_EXTEND | RMIPS_FLAG_NO_BLOCKS | RMIPS_FLAG_VERIFY_SCAN | RMIPS_FLAG_FORCE_VERIFY | RMIPS_FLAG_SIMT | RMIPS_FLAG_TIMING))
+  if (flags & ~(RMIPS_FLAG_NO_EXTEND | RMIPS_FLAG_NO_BLOCKS | RMIPS_FLAG_VERIFY_SCAN | RMIPS_FLAG_FORCE_VERIFY | RMIPS_FLAG_SIMT | RMIPS_FLAG_TIMING |
+                RMIPS_FLAG_KEY_SORT))
     return fail(RMIPS_ERR_INVALID, "unknown flag bits");
   rmips_index_s* x = idx;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
@@ -505,6 +526,7 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
         CK(e);
         tm->mark();  // 2
         CK(query_exact(c, st));
+        if (c.bits) CK(query_output_bits(c, offsets, user_ids, capacity, st));  // before the sync
       } else {
         tm->mark();
       }
@@ -537,8 +559,10 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
     const int64_t total = S.result_total;
     const int64_t reserved = (int64_t)hc[C_ACCEPTED_TOTAL];  // >= total: sentinel padding sorts last
     tm->mark();  // 4
-    CK(query_sort(c, reserved, 64, st));
-    CK(query_output(c, offsets, user_ids, capacity, st));
+    if (!c.bits) {
+      CK(query_sort(c, reserved, 64, st));
+      CK(query_output(c, offsets, user_ids, capacity, st));
+    }
     tm->mark();  // 5
     CK(cudaStreamSynchronize(st));
     x->phase_ms[15] = (double)(g_launches.load() - l0);
@@ -553,6 +577,7 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
     if (total > capacity) return fail(RMIPS_ERR_CAPACITY, "result ids exceed capacity");
   } catch (const CudaFail& f) {
     cudaStreamSynchronize(st);
+    x->bits_len = 0;
     return from_cuda(f);
   }
   return RMIPS_OK;

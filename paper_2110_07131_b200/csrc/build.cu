@@ -82,6 +82,7 @@ __global__ void k_prep_users(const float* __restrict__ Q, int64_t n, int d, int 
   if (!(nu > 0.f)) nu = 1.f;
   if (isinf(nu)) nu = 3.0e38f;
   const float* q = Q + o * d;
+#pragma unroll 4
   for (int j = 2 * lane; j < dpad; j += 64) {
     const float x0 = j < d ? q[j] : 0.f, x1 = j + 1 < d ? q[j + 1] : 0.f;
     reinterpret_cast<__half2*>(U16 + r * dpad)[j >> 1] = __halves2half2(__float2half_rn(x0 / nu), __float2half_rn(x1 / nu));
@@ -109,6 +110,7 @@ __global__ void k_prep_items(const float* __restrict__ P, int64_t m, int d, int 
   const float scale = ldexpf(1.f, e);
   const int64_t o = perm[r];
   const float* p = P + o * d;
+#pragma unroll 4
   for (int j = 2 * lane; j < dpad; j += 64) {
     const float x0 = j < d ? p[j] : 0.f, x1 = j + 1 < d ? p[j + 1] : 0.f;
     reinterpret_cast<__half2*>(P16 + r * dpad)[j >> 1] = __halves2half2(__float2half_rn(x0 * scale), __float2half_rn(x1 * scale));

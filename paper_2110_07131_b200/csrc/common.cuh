@@ -82,6 +82,35 @@ __device__ __forceinline__ void warp_append_u64(bool pred, uint64_t rec, unsigne
   }
 }
 
+// Where accepted (query, user) pairs go: appended to a key list (sorted afterwards), or, when
+// the batch's b x n bit matrix fits the workspace, set as bit (q, u) of that matrix (row stride
+// nw words), which the output kernels read back in (q, u) order without a sort.
+struct AccSink {
+  uint64_t* list;
+  uint32_t* bits;
+  int64_t nw;
+  // warp-collective: every lane calls it (bits is warp-uniform)
+  __device__ __forceinline__ void put(bool pred, uint64_t key, unsigned long long* count, int64_t cap) const {
+    if (bits) {
+      if (pred) set(key);
+    } else {
+      warp_append_u64(pred, key, count, list, cap);
+    }
+  }
+  __device__ __forceinline__ void put_one(uint64_t key, unsigned long long* count, int64_t cap) const {
+    if (bits) {
+      set(key);
+    } else {
+      const unsigned long long pos = atomicAdd(count, 1ull);
+      if ((int64_t)pos < cap) list[pos] = key;
+    }
+  }
+  __device__ __forceinline__ void set(uint64_t key) const {
+    const uint32_t u = (uint32_t)key;
+    atomicOr(bits + (int64_t)(key >> 32) * nw + (u >> 5), 1u << (u & 31));
+  }
+};
+
 __device__ __forceinline__ void warp_count(bool pred, unsigned long long* ctr) {
   uint32_t bal = __ballot_sync(0xffffffffu, pred);
   if ((threadIdx.x & 31) == __ffs(bal | 0x80000000u) - 1 && bal) atomicAdd(ctr, (unsigned long long)__popc(bal));
@@ -146,6 +175,7 @@ struct rmips_index_s {
   // query workspace (grown on demand)
   void* ws = nullptr;
   size_t ws_bytes = 0;
+  size_t bits_off = 0, bits_len = 0;  // all-zero bit-matrix region of ws (query output)
   int64_t pair_cap = 0;
   unsigned long long* d_counters = nullptr;  // [kNumCounters + 4]
   int* d_flags = nullptr;                    // [4]

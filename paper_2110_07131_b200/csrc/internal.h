@@ -62,6 +62,8 @@ struct QueryCtx {
   // outputs of the filter
   unsigned long long* counters = nullptr;  // kNumCounters (+ accepted / undecided list sizes)
   uint64_t* acc = nullptr;       // accepted keys (q_input << 32 | original user id)
+  uint32_t* bits = nullptr;      // or: accepted pairs as bits of a [b][nw] word matrix (no sort)
+  int64_t nw = 0;                // words per query row of bits, ceil(n / 32)
   uint64_t* und = nullptr;       // undecided (q_input << 32 | sorted user position)
   int32_t* scan_cnt = nullptr;   // [cap] P' index: items of P' that beat q, for the scan after P'
   int64_t cap = 0;               // capacity of acc and of und
@@ -81,6 +83,8 @@ cudaError_t query_filter_tc(QueryCtx& c, cudaStream_t st);  // query_tc.cu
 cudaError_t query_exact(QueryCtx& c, cudaStream_t st);
 cudaError_t query_output(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st);
 size_t query_cub_bytes(int64_t cap);
+size_t query_scan_bytes(int b);
 cudaError_t query_sort(QueryCtx& c, int64_t total, int end_bit, cudaStream_t st);
+cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st);
 
 }  // namespace rmips

@@ -121,7 +121,7 @@ k_query_simt(const __half* __restrict__ U16, const float* __restrict__ thrk, con
              const int32_t* __restrict__ perm_u, int64_t n, const __half* __restrict__ Q16,
              const float* __restrict__ qn, const float* __restrict__ qerr, const float* __restrict__ qscale,
              const int32_t* __restrict__ qperm, const int32_t* __restrict__ qcount, int flags,
-             unsigned long long* __restrict__ ctr, uint64_t* __restrict__ acc_list, uint64_t* __restrict__ und_list,
+             unsigned long long* __restrict__ ctr, AccSink acc_list, uint64_t* __restrict__ und_list,
              int64_t cap) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __half2* us = reinterpret_cast<__half2*>(smem_raw);        // [DPAD/2][128]
@@ -179,7 +179,7 @@ k_query_simt(const __half* __restrict__ U16, const float* __restrict__ thrk, con
       warp_count(ok, ctr + C_SCORED);
       warp_count(ok && cls == 0, ctr + C_REJECTED);
       warp_count(ok && cls == 1, ctr + C_ACCEPT_FAST);
-      warp_append_u64(ok && cls == 1, (qin << 32) | uo, ctr + C_ACCEPTED_TOTAL, acc_list, cap);
+      acc_list.put(ok && cls == 1, (qin << 32) | uo, ctr + C_ACCEPTED_TOTAL, cap);
       warp_count(ok && cls == 1, ctr + C_ACC_REAL);
       warp_append_u64(ok && cls == 2, (qin << 32) | (uint64_t)row, ctr + C_UND_TOTAL, und_list, cap);
     }
@@ -191,7 +191,7 @@ k_query_simt(const __half* __restrict__ U16, const float* __restrict__ thrk, con
 __global__ void k_exact_decide(const float* __restrict__ q, const float* __restrict__ U32,
                                const double* __restrict__ tauk, const int32_t* __restrict__ perm_u, int d,
                                unsigned long long* __restrict__ ctr, const uint64_t* __restrict__ und_list,
-                               uint64_t* __restrict__ acc_list, int64_t cap) {
+                               AccSink acc_list, int64_t cap) {
   const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_UND_TOTAL]);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < total; base += stride) {
@@ -210,7 +210,7 @@ __global__ void k_exact_decide(const float* __restrict__ q, const float* __restr
     }
     warp_count(ok, ctr + C_UNDECIDED);
     warp_count(yes, ctr + C_EXACT_ACCEPT);
-    warp_append_u64(yes, key, ctr + C_ACCEPTED_TOTAL, acc_list, cap);
+    acc_list.put(yes, key, ctr + C_ACCEPTED_TOTAL, cap);
     warp_count(yes, ctr + C_ACC_REAL);
   }
 }
@@ -229,7 +229,7 @@ __global__ void k_exact_decide_pp(const float* __restrict__ q, const float* __re
                                   const double* __restrict__ tau, int64_t n, int64_t m, int64_t mprime, int k,
                                   const int32_t* __restrict__ perm_u, int d, unsigned long long* __restrict__ ctr,
                                   uint64_t* __restrict__ und_list, int32_t* __restrict__ scan_cnt,
-                                  uint64_t* __restrict__ acc_list, int64_t cap) {
+                                  AccSink acc_list, int64_t cap) {
   const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_UND_TOTAL]);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const double slack = 1.0 + (d + 8) * 2.220446049250313e-16;  // as k_verify_scan's Cor. 1 test
@@ -260,7 +260,7 @@ __global__ void k_exact_decide_pp(const float* __restrict__ q, const float* __re
     }
     warp_count(ok, ctr + C_UNDECIDED);
     warp_count(yes, ctr + C_EXACT_ACCEPT);
-    warp_append_u64(yes, key, ctr + C_ACCEPTED_TOTAL, acc_list, cap);
+    acc_list.put(yes, key, ctr + C_ACCEPTED_TOTAL, cap);
     warp_count(yes, ctr + C_ACC_REAL);
   }
 }
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(32 * kScanWarps)
 k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const double* __restrict__ unorm,
               const float* __restrict__ P32, const double* __restrict__ pnorm, const int32_t* __restrict__ perm_u,
               int64_t m, int d, int pd, int k, unsigned long long* __restrict__ ctr,
-              const uint64_t* __restrict__ und_list, uint64_t* __restrict__ acc_list, int64_t cap, int64_t start,
+              const uint64_t* __restrict__ und_list, AccSink acc_list, int64_t cap, int64_t start,
               const int32_t* __restrict__ beats0) {
   __shared__ __align__(16) float su[kScanWarps][256];  // the pair's u, fp32, zero-padded to pd
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -361,8 +361,7 @@ k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const 
       if (yes) {
         atomicAdd(ctr + C_EXACT_ACCEPT, 1ull);
         atomicAdd(ctr + C_ACC_REAL, 1ull);
-        unsigned long long pos = atomicAdd(ctr + C_ACCEPTED_TOTAL, 1ull);
-        if ((int64_t)pos < cap) acc_list[pos] = ((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row];
+        acc_list.put_one(((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row], ctr + C_ACCEPTED_TOTAL, cap);
       }
     }
   }
@@ -405,7 +404,7 @@ static cudaError_t launch_query_simt(QueryCtx& c, cudaStream_t st) {
   dim3 grid((unsigned)x->nblocks, (unsigned)c.nsub);
   k_query_simt<DPAD><<<grid, 128, smem, st>>>(x->U16, x->thr + (int64_t)(c.k - 1) * x->n,
                                               x->tb + (int64_t)(c.k - 1) * x->nblocks, x->perm_u, x->n, c.Q16, c.qn,
-                                              c.qerr, c.qscale, c.qperm, c.qcount, c.flags, c.counters, c.acc, c.und,
+                                              c.qerr, c.qscale, c.qperm, c.qcount, c.flags, c.counters, AccSink{c.acc, c.bits, c.nw}, c.und,
                                               c.cap); count_launch();
   return cudaGetLastError();
 }
@@ -426,18 +425,18 @@ cudaError_t query_exact(QueryCtx& c, cudaStream_t st) {
   if (x->n == 0) return cudaSuccess;
   if (c.flags & RMIPS_FLAG_VERIFY_SCAN) {  // every undecided pair scans all of P (Alg. 2)
     k_verify_scan<<<148 * 8, 32 * kScanWarps, 0, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
-                                                           x->d, x->pd, c.k, c.counters, c.und, c.acc, c.cap, 0,
+                                                           x->d, x->pd, c.k, c.counters, c.und, AccSink{c.acc, c.bits, c.nw}, c.cap, 0,
                                                            nullptr); count_launch();
   } else if (x->mprime < x->m) {  // P' index: Lemmas 1-2 / Cor. 1 per pair, then the scan after P'
     k_exact_decide_pp<<<148 * 8, 256, 0, st>>>(c.q, x->U32, x->unorm, x->pnorm, x->tau, x->n, x->m, x->mprime, c.k,
-                                               x->perm_u, x->d, c.counters, c.und, c.scan_cnt, c.acc, c.cap);
+                                               x->perm_u, x->d, c.counters, c.und, c.scan_cnt, AccSink{c.acc, c.bits, c.nw}, c.cap);
     count_launch();
     k_verify_scan<<<148 * 8, 32 * kScanWarps, 0, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
-                                                           x->d, x->pd, c.k, c.counters, c.und, c.acc, c.cap,
+                                                           x->d, x->pd, c.k, c.counters, c.und, AccSink{c.acc, c.bits, c.nw}, c.cap,
                                                            x->mprime, c.scan_cnt); count_launch();
   } else {
     k_exact_decide<<<148 * 8, 256, 0, st>>>(c.q, x->U32, x->tau + (int64_t)(c.k - 1) * x->n, x->perm_u, x->d,
-                                            c.counters, c.und, c.acc, c.cap); count_launch();
+                                            c.counters, c.und, AccSink{c.acc, c.bits, c.nw}, c.cap); count_launch();
   }
   return cudaGetLastError();
 }
@@ -466,6 +465,88 @@ __global__ void k_offsets32(const uint32_t* __restrict__ keys, int64_t total, in
 __global__ void k_copy_ids32(const uint32_t* __restrict__ keys, int64_t total, uint32_t n, int32_t* __restrict__ out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < total) out[i] = (int32_t)(keys[i] % n);
+}
+
+// Bit-matrix output (QueryCtx::bits): per query the popcount of its row, an inclusive scan into
+// offsets[1..b], then the set bits of every row written in ascending user order (the order the
+// sorted-key path produces).  One CTA per query.  The emit pass clears every word it read, so the
+// matrix is all zero again for the next batch (it is memset only when its place in the workspace
+// changes).
+constexpr int kBitsThreads = 256;
+__device__ __forceinline__ int64_t block_sum64(int64_t v, int64_t* red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int64_t t = 0;
+  for (int w = 0; w < kBitsThreads / 32; ++w) t += red[w];
+  __syncthreads();
+  return t;
+}
+__global__ void __launch_bounds__(kBitsThreads)
+k_bits_count(const uint32_t* __restrict__ bits, int64_t nw, int64_t* __restrict__ counts) {
+  __shared__ int64_t red[kBitsThreads / 32];
+  const uint32_t* row = bits + (int64_t)blockIdx.x * nw;
+  int64_t c = 0;
+  for (int64_t i = threadIdx.x; i < nw; i += kBitsThreads) c += __popc(row[i]);
+  c = block_sum64(c, red);
+  if (threadIdx.x == 0) counts[blockIdx.x] = c;
+}
+__global__ void k_offsets_head(int64_t* offsets) { offsets[0] = 0; }
+__global__ void __launch_bounds__(kBitsThreads)
+k_bits_emit(uint32_t* __restrict__ bits, int64_t nw, int b, const int64_t* __restrict__ offsets,
+            int64_t capacity, int32_t* __restrict__ out) {
+  __shared__ int wsum[kBitsThreads / 32];
+  const int q = blockIdx.x;
+  const bool fits = offsets[b] <= capacity;  // ids only when all of them fit (as the sorted-key path)
+  int64_t base = offsets[q];
+  if (offsets[q + 1] == base) return;
+  uint32_t* row = bits + (int64_t)q * nw;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t i0 = 0; i0 < nw; i0 += kBitsThreads) {
+    const int64_t i = i0 + threadIdx.x;
+    uint32_t w = i < nw ? row[i] : 0u;
+    if (w) row[i] = 0u;
+    if (!fits) continue;  // (CTA-uniform: no barrier is skipped by part of the CTA)
+    const int c = __popc(w);
+    int incl = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int v = 0; v < kBitsThreads / 32; ++v) {
+      before += v < wid ? wsum[v] : 0;
+      total += wsum[v];
+    }
+    int64_t pos = base + before + incl - c;
+    while (w) {
+      const int j = __ffs(w) - 1;
+      w &= w - 1;
+      out[pos++] = (int32_t)(i * 32 + j);
+    }
+    base += total;
+    __syncthreads();
+  }
+}
+
+size_t query_scan_bytes(int b) {
+  size_t a = 0;
+  cub::DeviceScan::InclusiveSum((void*)nullptr, a, (const int64_t*)nullptr, (int64_t*)nullptr, b);
+  return a;
+}
+
+cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st) {
+  int64_t* counts = reinterpret_cast<int64_t*>(c.acc_sorted);  // the sort's space is unused on this path
+  k_bits_count<<<c.b, kBitsThreads, 0, st>>>(c.bits, c.nw, counts); count_launch();
+  k_offsets_head<<<1, 1, 0, st>>>(offsets); count_launch();
+  size_t tb = c.cub_bytes;
+  cudaError_t e = cub::DeviceScan::InclusiveSum(c.cub_tmp, tb, counts, offsets + 1, c.b, st);
+  count_launch(2);
+  if (e != cudaSuccess) return e;
+  k_bits_emit<<<c.b, kBitsThreads, 0, st>>>(c.bits, c.nw, c.b, offsets, capacity, user_ids); count_launch();
+  return cudaGetLastError();
 }
 
 static bool use_keys32(const QueryCtx& c) { return c.idx->n > 0 && (uint64_t)c.b * (uint64_t)c.idx->n < (1ull << 32); }

@@ -118,7 +118,7 @@ struct QSlowOut {
 __device__ __noinline__ QSlowOut q_slow(QPool pool, uint32_t flag, uint32_t tbase, int len, bool live, float thr_s,
                                         const float* __restrict__ qe_sub, const int32_t* __restrict__ qp_sub,
                                         uint64_t uo, int64_t row, bool force, unsigned long long* __restrict__ ctr,
-                                        uint64_t* __restrict__ acc_list, uint64_t* __restrict__ und_list,
+                                        AccSink acc_list, uint64_t* __restrict__ und_list,
                                         int64_t cap) {
   using namespace sm100;
   const int lane = threadIdx.x & 31;
@@ -168,14 +168,19 @@ __device__ __noinline__ QSlowOut q_slow(QPool pool, uint32_t flag, uint32_t tbas
     }
     const int ta = __shfl_sync(0xffffffffu, pa, 31), tu = __shfl_sync(0xffffffffu, pu, 31);
     unsigned long long na_base, nu_base;
-    pool_take(pool.abase, pool.aleft, ta, ctr + C_ACCEPTED_TOTAL, na_base);
+    if (!acc_list.bits) pool_take(pool.abase, pool.aleft, ta, ctr + C_ACCEPTED_TOTAL, na_base);
     pool_take(pool.ubase, pool.uleft, tu, ctr + C_UND_TOTAL, nu_base);
     int p = pa - na;
     while (am) {
       const int j = __ffs(am) - 1;
       am &= am - 1;
-      const unsigned long long slot = pool_slot(pool.abase, pool.aleft, na_base, p++);
-      if ((int64_t)slot < cap) acc_list[slot] = ((uint64_t)(uint32_t)__ldg(qp_sub + col0 + j) << 32) | uo;
+      const uint64_t key = ((uint64_t)(uint32_t)__ldg(qp_sub + col0 + j) << 32) | uo;
+      if (acc_list.bits) {
+        acc_list.set(key);
+      } else {
+        const unsigned long long slot = pool_slot(pool.abase, pool.aleft, na_base, p++);
+        if ((int64_t)slot < cap) acc_list.list[slot] = key;
+      }
     }
     p = pu - nu;
     while (um) {
@@ -184,7 +189,7 @@ __device__ __noinline__ QSlowOut q_slow(QPool pool, uint32_t flag, uint32_t tbas
       const unsigned long long slot = pool_slot(pool.ubase, pool.uleft, nu_base, p++);
       if ((int64_t)slot < cap) und_list[slot] = ((uint64_t)(uint32_t)__ldg(qp_sub + col0 + j) << 32) | (uint64_t)row;
     }
-    pool_advance(pool.abase, pool.aleft, ta, na_base);
+    if (!acc_list.bits) pool_advance(pool.abase, pool.aleft, ta, na_base);
     pool_advance(pool.ubase, pool.uleft, tu, nu_base);
   }
   QSlowOut out;
@@ -233,7 +238,7 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
            int64_t n, int nblocks, const float* __restrict__ qn, const float* __restrict__ qerr,
            const float* __restrict__ qscale, const int32_t* __restrict__ qperm, const int32_t* __restrict__ qcount,
            int nsub, int flags, int ksteps, const int32_t* __restrict__ wlen, unsigned long long* __restrict__ ctr,
-           uint64_t* __restrict__ acc_list, uint64_t* __restrict__ und_list, int64_t cap) {
+           AccSink acc_list, uint64_t* __restrict__ und_list, int64_t cap) {
   using namespace sm100;
   constexpr int kStages = QSmem::NU(KB);  // ring units
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -466,7 +471,7 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     }
     // pad the unused pool slots (warp-uniform pools; lanes share the work)
     for (int i = lane; i < pool.aleft; i += 32)
-      if ((int64_t)(pool.abase + i) < cap) acc_list[pool.abase + i] = kSentinel;
+      if ((int64_t)(pool.abase + i) < cap) acc_list.list[pool.abase + i] = kSentinel;
     for (int i = lane; i < pool.uleft; i += 32)
       if ((int64_t)(pool.ubase + i) < cap) und_list[pool.ubase + i] = kSentinel;
     // counters: one atomic per warp
@@ -517,7 +522,7 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
   k_query_tc<KB><<<grid, kThreads, smem, st>>>(tu, tq, x->thr + (int64_t)(c.k - 1) * x->n,
                                                x->tb + (int64_t)(c.k - 1) * x->nblocks, x->perm_u, x->n,
                                                (int)x->nblocks, c.qn, c.qerr, c.qscale, c.qperm, c.qcount, c.nsub,
-                                               c.flags, (x->d + 15) / 16, c.wlen, c.counters, c.acc, c.und, c.cap);
+                                               c.flags, (x->d + 15) / 16, c.wlen, c.counters, AccSink{c.acc, c.bits, c.nw}, c.und, c.cap);
   count_launch();
   return cudaGetLastError();
 }

@@ -24,6 +24,7 @@ RMIPS_FLAG_FORCE_VERIFY = 4
 RMIPS_FLAG_SIMT = 8
 RMIPS_FLAG_TIMING = 16
 RMIPS_FLAG_NO_EXTEND = 32
+RMIPS_FLAG_KEY_SORT = 64
 RMIPS_BUILD_DEFAULT = 0
 RMIPS_BUILD_SIMT = 1
 RMIPS_BUILD_TIMING = 2

@@ -85,7 +85,8 @@ def test_cfg0_index_tables_bitwise(cfg0):
 @pytest.mark.parametrize("qflags", [rmips.RMIPS_FLAG_NO_BLOCKS, rmips.RMIPS_FLAG_VERIFY_SCAN,
                                     rmips.RMIPS_FLAG_FORCE_VERIFY,
                                     rmips.RMIPS_FLAG_FORCE_VERIFY | rmips.RMIPS_FLAG_VERIFY_SCAN,
-                                    rmips.RMIPS_FLAG_SIMT])
+                                    rmips.RMIPS_FLAG_SIMT, rmips.RMIPS_FLAG_KEY_SORT,
+                                    rmips.RMIPS_FLAG_KEY_SORT | rmips.RMIPS_FLAG_FORCE_VERIFY])
 def test_cfg0_query_modes_agree(cfg0, qflags):
     w, member = cfg0
     got = gpu_sets(w.U, w.P, w.Qy, 10, 10, 0, qflags)
@@ -208,6 +209,32 @@ def test_errors_k_range_nonfinite_capacity():
     with pytest.raises(rmips.RmipsError) as e:
         rmips.rmips_build_index(_t(Ub), _t(P), 5)
     assert e.value.status == rmips.RMIPS_ERR_NONFINITE
+    idx.close()
+
+
+def test_output_paths_identical():
+    """The bit-matrix output and the sorted-key output give the same offsets and ids (ragged n,
+    several batch sizes incl. one query and more than one 256-query sub-batch), and both report
+    RMIPS_ERR_CAPACITY with valid offsets when the ids do not fit."""
+    U, P = gen.random_instance(21, 3001, 400, 24)
+    idx = rmips.rmips_build_index(_t(U), _t(P), 12)
+    for b in (1, 7, 300, 700):
+        Q = _t(P[:b] if b <= len(P) else P[np.arange(b) % len(P)])
+        for k in (1, 5, 12):
+            o1, i1 = rmips.rmips_query(idx, Q, k)
+            o2, i2 = rmips.rmips_query(idx, Q, k, rmips.RMIPS_FLAG_KEY_SORT)
+            assert np.array_equal(o1.cpu().numpy(), o2.cpu().numpy()), (b, k)
+            assert np.array_equal(i1.cpu().numpy(), i2.cpu().numpy()), (b, k)
+    for fl in (0, rmips.RMIPS_FLAG_KEY_SORT):
+        with pytest.raises(rmips.RmipsError) as e:
+            rmips.rmips_query(idx, _t(P[:50]), 12, fl, capacity=3)
+        assert e.value.status == rmips.RMIPS_ERR_CAPACITY
+    # the matrix is clean again after a capacity failure and across batch-size changes
+    for b in (50, 700, 50):
+        o1, i1 = rmips.rmips_query(idx, _t(P[np.arange(b) % len(P)]), 12)
+        o2, i2 = rmips.rmips_query(idx, _t(P[np.arange(b) % len(P)]), 12, rmips.RMIPS_FLAG_KEY_SORT)
+        assert np.array_equal(o1.cpu().numpy(), o2.cpu().numpy())
+        assert np.array_equal(i1.cpu().numpy(), i2.cpu().numpy())
     idx.close()
 
 
