@@ -320,10 +320,7 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
     c.tiles_done = c.cand_total + 1;
     scratch = reinterpret_cast<double*>(S + o_scr);
     c.scratch_arena = sarena;
-    CK(cudaMemsetAsync(c.cand_total, 0, 2 * sizeof(unsigned long long), st));
-    CK(cudaMemsetAsync(x->d_flags, 0, 4 * sizeof(int), st));
-    CK(cudaMemsetAsync(c.maxabs, 0, 4 * sizeof(unsigned int), st));
-    CK(cudaMemsetAsync(c.ovf_count, 0, sizeof(int), st));
+    CK(zero4(st, c.cand_total, 4, x->d_flags, 4, c.maxabs, 4, c.ovf_count, 1));
 
     const long long l0 = g_launches.load();
     tm.mark();  // 0
@@ -511,8 +508,8 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
       tm.reset(new PhaseTimer((flags & RMIPS_FLAG_TIMING) != 0, st));
       ensure_ws(x, c, c.nsub, cap, st);
       tm->mark();  // 0
-      CK(cudaMemsetAsync(x->d_counters, 0, sizeof(unsigned long long) * (kNumCounters + 4), st));
-      CK(cudaMemsetAsync(x->d_flags, 0, sizeof(int) * 4, st));
+      static_assert(2 * (kNumCounters + 4) <= 128, "zero4 region");
+      CK(zero4(st, x->d_counters, 2 * (kNumCounters + 4), x->d_flags, 4, nullptr, 0, nullptr, 0));
       CK(query_prep(c, st));
       tm->mark();  // 1
       if (x->n > 0) {

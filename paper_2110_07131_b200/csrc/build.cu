@@ -10,6 +10,9 @@
 //   B6 k_blocks         block table, Eq. (1) divided by ||u_first|| for Lemma 3
 #include <cub/cub.cuh>
 
+#include <mutex>
+#include <vector>
+
 #include "cand.cuh"
 #include "common.cuh"
 #include "internal.h"
@@ -600,6 +603,108 @@ cudaError_t build_simt(const BuildCtx& c, cudaStream_t st) {
   }
 }
 
+// B2 as a CUDA graph: the radix sort is ~20 small launches and memsets whose host enqueue time
+// (~5 us each) exceeds their device time, so the GPU idles through the prep phase.  The iota +
+// sort sequence is captured once per (stream, size) into a graph over persistent buffers and
+// replayed with one launch.  Buffers are stream-ordered: builds on one stream reuse them in
+// order; different streams get different entries.  At most kSortCache entries (the oldest is
+// freed with cudaFree, which waits for the device).
+namespace {
+struct SortGraph {
+  cudaStream_t st = nullptr;
+  int dev = -1;
+  int64_t tot = 0;
+  uint64_t* keys = nullptr;  // [2 tot]: in, out
+  int32_t* vals = nullptr;   // [2 tot]: in, out
+  void* tmp = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int busy = 0;  // host threads between sort_graph_get and sort_graph_put (never evicted then)
+};
+constexpr int kSortCache = 4;
+std::mutex g_sort_mu;
+std::vector<SortGraph*> g_sort;
+void sort_graph_free(SortGraph* g) {
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  cudaFree(g->keys);
+  cudaFree(g->vals);
+  cudaFree(g->tmp);
+  delete g;
+}
+SortGraph* sort_graph_get(cudaStream_t st, int64_t tot) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_sort_mu);
+  for (size_t i = 0; i < g_sort.size(); ++i)
+    if (g_sort[i]->st == st && g_sort[i]->tot == tot && g_sort[i]->dev == dev) {
+      SortGraph* g = g_sort[i];
+      g_sort.erase(g_sort.begin() + i);
+      g_sort.push_back(g);  // most recently used last
+      ++g->busy;
+      return g;
+    }
+  SortGraph* g = new SortGraph;
+  g->st = st; g->dev = dev; g->tot = tot;
+  size_t tb = 0;
+  cudaStream_t cs = nullptr;
+  cudaGraph_t graph = nullptr;
+  bool ok = cub::DeviceRadixSort::SortPairsDescending((void*)nullptr, tb, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                                      (const int32_t*)nullptr, (int32_t*)nullptr, (int)tot, 0, 64) ==
+                cudaSuccess &&
+            cudaMalloc(&g->keys, 2 * tot * sizeof(uint64_t)) == cudaSuccess &&
+            cudaMalloc(&g->vals, 2 * tot * sizeof(int32_t)) == cudaSuccess && cudaMalloc(&g->tmp, tb) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    k_iota<<<(unsigned)((tot + 255) / 256), 256, 0, cs>>>(g->vals, tot);
+    size_t tb2 = tb;
+    cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(g->tmp, tb2, g->keys, g->keys + tot, g->vals,
+                                                              g->vals + tot, (int)tot, 0, 64, cs);
+    ok = cudaStreamEndCapture(cs, &graph) == cudaSuccess && e == cudaSuccess &&
+         cudaGraphInstantiate(&g->exec, graph, 0) == cudaSuccess;
+  }
+  if (graph) cudaGraphDestroy(graph);
+  if (cs) cudaStreamDestroy(cs);
+  if (!ok) {
+    cudaGetLastError();
+    sort_graph_free(g);
+    return nullptr;
+  }
+  if ((int)g_sort.size() >= kSortCache) {
+    size_t i = 0;
+    while (i < g_sort.size() && g_sort[i]->busy) ++i;
+    if (i == g_sort.size()) {  // every entry is being enqueued right now: do not cache
+      sort_graph_free(g);
+      return nullptr;
+    }
+    sort_graph_free(g_sort[i]);
+    g_sort.erase(g_sort.begin() + i);
+  }
+  ++g->busy;
+  g_sort.push_back(g);
+  return g;
+}
+void sort_graph_put(SortGraph* g) {
+  if (!g) return;
+  std::lock_guard<std::mutex> lk(g_sort_mu);
+  --g->busy;
+}
+}  // namespace
+
+// Zero up to four small device regions (word counts) in one launch instead of four memsets.
+__global__ void k_zero4(uint32_t* a, int na, uint32_t* b, int nb, uint32_t* c, int nc, uint32_t* d, int nd) {
+  const int t = threadIdx.x;
+  if (t < na) a[t] = 0u;
+  if (t < nb) b[t] = 0u;
+  if (t < nc) c[t] = 0u;
+  if (t < nd) d[t] = 0u;
+}
+cudaError_t zero4(cudaStream_t st, void* a, int na, void* b, int nb, void* c, int nc, void* d, int nd) {
+  k_zero4<<<1, 128, 0, st>>>(static_cast<uint32_t*>(a), na, static_cast<uint32_t*>(b), nb, static_cast<uint32_t*>(c),
+                             nc, static_cast<uint32_t*>(d), nd);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   const int64_t n = x->n, m = x->m;
@@ -607,25 +712,36 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
   // B1: norms as sort keys of one concatenated [items | users] sequence (items carry the top
   // bit, so a descending sort puts them first); non-finite check; max |p_j|
   const int64_t tot = m + n;
-  uint64_t* kin = c.nkey;
-  uint64_t* kout = c.nkey + tot;
-  int32_t* vin = c.nval;
-  int32_t* vout = c.nval + tot;
   const size_t nsm = (size_t)kNormRows * (d | 1) * sizeof(float);
   if (nsm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_norms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nsm);
     if (e != cudaSuccess) return e;
   }
+  SortGraph* sg = sort_graph_get(st, tot);  // (nullptr: the direct path below)
+  uint64_t* kin = sg ? sg->keys : c.nkey;
+  uint64_t* kout = kin + tot;
+  int32_t* vin = sg ? sg->vals : c.nval;
+  int32_t* vout = vin + tot;
   k_norms<<<nblk(m, kNormRows), kNormRows, nsm, st>>>(P, m, d, kin, 1ull << 63, x->d_flags, c.maxabs); count_launch();
   if (n) k_norms<<<nblk(n, kNormRows), kNormRows, nsm, st>>>(Q, n, d, kin + m, 0ull, x->d_flags, nullptr); count_launch();
   // B2: one stable radix sort (descending norm, ties by ascending index: reading R6)
-  k_iota<<<nblk(tot, 256), 256, 0, st>>>(vin, tot); count_launch();
-  size_t tb = c.cub_bytes;
-  cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(c.cub_tmp, tb, kin, kout, vin, vout, (int)tot, 0, 64, st);
-  count_launch(kCubSortKernels);
-  if (e != cudaSuccess) return e;
+  if (sg) {
+    cudaError_t e = cudaGraphLaunch(sg->exec, st);
+    count_launch(1 + kCubSortKernels);
+    if (e != cudaSuccess) {
+      sort_graph_put(sg);
+      return e;
+    }
+  } else {
+    k_iota<<<nblk(tot, 256), 256, 0, st>>>(vin, tot); count_launch();
+    size_t tb = c.cub_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(c.cub_tmp, tb, kin, kout, vin, vout, (int)tot, 0, 64, st);
+    count_launch(kCubSortKernels);
+    if (e != cudaSuccess) return e;
+  }
   k_split_sorted<<<nblk(tot, 256), 256, 0, st>>>(kout, vout, m, n, x->pnorm, x->perm_p, x->unorm, x->perm_u);
   count_launch();
+  sort_graph_put(sg);  // last use of the sort buffers is enqueued
   // B3
   if (n)
     k_prep_users<<<nblk(n * 32, 256), 256, 0, st>>>(Q, n, d, dpad, x->perm_u, x->unorm, x->U16, x->U32, x->unu); count_launch();

@@ -47,3 +47,21 @@ print("config %d, %d steps, per-step device time by kernel (us):" % (cfg, steps)
 for name, t in sorted(tot.items(), key=lambda kv: -kv[1]):
     print("%9.1f  %5.1f%%  x%-3d %s" % (t / steps, 100 * t / allt, cnt[name] // steps, name))
 print("%9.1f  total" % (allt / steps))
+
+# idle gaps on the device between consecutive activities (where the GPU waits for the host)
+evs = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA],
+             key=lambda e: e.time_range.start)
+gaps = collections.defaultdict(float)
+gcount = collections.Counter()
+span = (evs[-1].time_range.end - evs[0].time_range.start) if evs else 0
+idle = 0.0
+for a, b_ in zip(evs, evs[1:]):
+    g = b_.time_range.start - a.time_range.end
+    if g > 0:
+        idle += g
+        key = "%s -> %s" % (a.name[:40], b_.name[:40])
+        gaps[key] += g
+        gcount[key] += 1
+print("device span %.1f us/step, idle %.1f us/step; largest idle gaps (us/step):" % (span / steps, idle / steps))
+for key, g in sorted(gaps.items(), key=lambda kv: -kv[1])[:20]:
+    print("%8.1f  x%-3d %s" % (g / steps, gcount[key] // steps, key))
