@@ -459,18 +459,42 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
         const float* pr0 = P32 + (int64_t)pos0 * pd;  // pd = round_up(d, 8): 32-byte rows
         const float* pr1 = P32 + (int64_t)pos1 * pd;
         double s0 = 0.0, s1 = 0.0;  // dot64: left-to-right fp64 sums of exact fp32 x fp32 products
+        if (32 * i + 32 < cnt) {    // warp-uniform: both chains have work
 #pragma unroll 2
-        for (int t = 0; t < pd; t += 8) {
-          float a[8], bb[8];
-          ldg_nc_v8(pr0 + t, a);
-          ldg_nc_v8(pr1 + t, bb);
+          for (int t = 0; t < pd; t += 8) {
+            float a[8], bb[8];
+            ldg_nc_v8(pr0 + t, a);
+            if (l1) {
+              ldg_nc_v8(pr1 + t, bb);
+            } else {
 #pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            const double2 uu = *reinterpret_cast<const double2*>(urow + t + e);
-            s0 = __fma_rn((double)a[e], uu.x, s0);
-            s1 = __fma_rn((double)bb[e], uu.x, s1);
-            s0 = __fma_rn((double)a[e + 1], uu.y, s0);
-            s1 = __fma_rn((double)bb[e + 1], uu.y, s1);
+              for (int e = 0; e < 8; ++e) bb[e] = 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const double2 uu = *reinterpret_cast<const double2*>(urow + t + e);
+              s0 = __fma_rn((double)a[e], uu.x, s0);
+              s1 = __fma_rn((double)bb[e], uu.x, s1);
+              s0 = __fma_rn((double)a[e + 1], uu.y, s0);
+              s1 = __fma_rn((double)bb[e + 1], uu.y, s1);
+            }
+          }
+        } else {                    // one chain (rows with at most 32 * i + 32 candidates)
+#pragma unroll 2
+          for (int t = 0; t < pd; t += 8) {
+            float a[8];
+            if (l0) {
+              ldg_nc_v8(pr0 + t, a);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) a[e] = 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const double2 uu = *reinterpret_cast<const double2*>(urow + t + e);
+              s0 = __fma_rn((double)a[e], uu.x, s0);
+              s0 = __fma_rn((double)a[e + 1], uu.y, s0);
+            }
           }
         }
         if (l0) key[i].v = s0, key[i].id = perm_p[pos0];
