@@ -16,7 +16,10 @@ std::atomic<long long> rmips::g_launches{0};
 
 namespace {
 
-// CUDA-event phase timer (only when the caller asked for timing).
+// CUDA-event phase timer (only when the caller asked for timing).  Events come from a per-thread
+// pool (cudaEventCreate / Destroy per mark cost several microseconds of host time between the
+// launches of a timed call).
+thread_local std::vector<cudaEvent_t> g_ev_pool;
 struct PhaseTimer {
   bool on = false;
   cudaStream_t st = nullptr;
@@ -25,7 +28,13 @@ struct PhaseTimer {
   PhaseTimer(bool enable, cudaStream_t s) : on(enable), st(s) {}
   void mark() {
     if (!on || n >= 8) return;
-    if (cudaEventCreate(&ev[n]) == cudaSuccess) cudaEventRecord(ev[n], st);
+    if (!g_ev_pool.empty()) {
+      ev[n] = g_ev_pool.back();
+      g_ev_pool.pop_back();
+    } else if (cudaEventCreate(&ev[n]) != cudaSuccess) {
+      ev[n] = nullptr;
+    }
+    if (ev[n]) cudaEventRecord(ev[n], st);
     ++n;
   }
   double between(int a, int b) const {
@@ -36,7 +45,7 @@ struct PhaseTimer {
   }
   ~PhaseTimer() {
     for (int i = 0; i < n; ++i)
-      if (ev[i]) cudaEventDestroy(ev[i]);
+      if (ev[i]) g_ev_pool.push_back(ev[i]);
   }
 };
 
