@@ -308,7 +308,7 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
     c.cub_bytes = build_cub_bytes(n, m);
     // exact-fallback CTAs (each with m fp64 of scratch): up to 4 per SM, scratch <= 256 MB
     const int fb_grid = fallback_grid(m);
-    const size_t o_key = sa.take<uint64_t>(2 * (m + n)), o_val = sa.take<int32_t>(2 * (m + n)),
+    const size_t o_key = sa.take<uint64_t>(2 * (m + n)), o_val = sa.take<int32_t>(2 * (m + n)), o_inv = sa.take<int32_t>(n),
                  o_max = sa.take<unsigned int>(4), o_cub = sa.take<unsigned char>((int64_t)c.cub_bytes),
                  o_cand = sa.take<int32_t>(n * kCand), o_cc = sa.take<int32_t>(n), o_ovl = sa.take<int32_t>(n),
                  o_ovc = sa.take<int>(1), o_ct = sa.take<unsigned long long>(2),
@@ -318,6 +318,7 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
     char* S = static_cast<char*>(sarena);
     c.nkey = reinterpret_cast<uint64_t*>(S + o_key);
     c.nval = reinterpret_cast<int32_t*>(S + o_val);
+    c.inv_u = reinterpret_cast<int32_t*>(S + o_inv);
     c.maxabs = reinterpret_cast<unsigned int*>(S + o_max);
     c.scale_dev = reinterpret_cast<float*>(c.maxabs + 2);
     c.cub_tmp = S + o_cub;

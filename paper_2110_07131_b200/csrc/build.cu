@@ -60,53 +60,59 @@ __global__ void k_iota(int32_t* v, int64_t n) {
   if (i < n) v[i] = (int32_t)i;
 }
 
-// Split the one sorted [items | users] sequence into the two norm-sorted permutations.
+// Split the one sorted [items | users] sequence into the two norm-sorted permutations (and the
+// inverse user permutation for the user prep).
 __global__ void k_split_sorted(const uint64_t* __restrict__ keys, const int32_t* __restrict__ vals, int64_t m,
                                int64_t n, double* __restrict__ pnorm, int32_t* __restrict__ perm_p,
-                               double* __restrict__ unorm, int32_t* __restrict__ perm_u) {
+                               double* __restrict__ unorm, int32_t* __restrict__ perm_u, int32_t* __restrict__ inv_u) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= m + n) return;
   const double v = __longlong_as_double((long long)(keys[r] & 0x7fffffffffffffffull));
-  if (r < m) pnorm[r] = v, perm_p[r] = vals[r];
-  else unorm[r - m] = v, perm_u[r - m] = vals[r] - (int32_t)m;
+  if (r < m) {
+    pnorm[r] = v, perm_p[r] = vals[r];
+  } else {
+    const int32_t o = vals[r] - (int32_t)m;
+    unorm[r - m] = v, perm_u[r - m] = o;
+    inv_u[o] = (int32_t)(r - m);
+  }
 }
 
 // ------------------------------------------------------------------------------ B3
 // Users: U16 = fp16(u / nu), nu = fp32(||u||) (1 for the zero vector); U32 = u (permuted).
-// One warp per kPrepRows consecutive sorted rows: the rows' permuted sources are gathered with all
-// of their loads in flight at once (one row per warp left three dependent DRAM latencies per row
-// exposed: 0.68 ms on configs[3]); lane l handles the column pairs 2l, 2l + 64, ...
+// One warp per kPrepRows consecutive ORIGINAL rows: the reads of Q stream in order and each row is
+// written to its norm-sorted place (whole 128-byte U16 rows; a row-gather version left the reads
+// scattered: 0.68 / 0.52 ms on configs[3]); lane l handles the column pairs 2l, 2l + 64, ...
+// keys_u[o] = bits of ||u_o|| (the sort's input keys: the same fp64 value as the sorted norms).
 constexpr int kPrepRows = 8;
 __global__ void k_prep_users(const float* __restrict__ Q, int64_t n, int d, int dpad,
-                             const int32_t* __restrict__ perm, const double* __restrict__ norm_sorted,
+                             const int32_t* __restrict__ inv_u, const uint64_t* __restrict__ keys_u,
                              __half* __restrict__ U16, float* __restrict__ U32, float* __restrict__ unu) {
-  const int64_t r0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * kPrepRows;
+  const int64_t o0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * kPrepRows;
   const int lane = threadIdx.x & 31;
-  if (r0 >= n) return;
-  int64_t o_l = 0;
+  if (o0 >= n) return;
+  int64_t r_l = 0;
   float nu_l = 1.f;
-  if (lane < kPrepRows && r0 + lane < n) {
-    o_l = perm[r0 + lane];
-    nu_l = (float)norm_sorted[r0 + lane];
+  if (lane < kPrepRows && o0 + lane < n) {
+    r_l = inv_u[o0 + lane];
+    nu_l = (float)__longlong_as_double((long long)keys_u[o0 + lane]);
     if (!(nu_l > 0.f)) nu_l = 1.f;
     if (isinf(nu_l)) nu_l = 3.0e38f;
-    unu[r0 + lane] = nu_l;
+    unu[r_l] = nu_l;
   }
   for (int j = 2 * lane; j < dpad; j += 64) {
     float x0[kPrepRows], x1[kPrepRows];
 #pragma unroll
     for (int i = 0; i < kPrepRows; ++i) {
-      const int64_t o = __shfl_sync(0xffffffffu, o_l, i);
-      const float* q = Q + o * d;
-      const bool live = r0 + i < n;
+      const float* q = Q + (o0 + i) * d;
+      const bool live = o0 + i < n;
       x0[i] = live && j < d ? q[j] : 0.f;
       x1[i] = live && j + 1 < d ? q[j + 1] : 0.f;
     }
 #pragma unroll
     for (int i = 0; i < kPrepRows; ++i) {
       const float nu = __shfl_sync(0xffffffffu, nu_l, i);
-      const int64_t r = r0 + i;
-      if (r < n) {
+      const int64_t r = __shfl_sync(0xffffffffu, r_l, i);
+      if (o0 + i < n) {
         reinterpret_cast<__half2*>(U16 + r * dpad)[j >> 1] =
             __halves2half2(__float2half_rn(x0[i] / nu), __float2half_rn(x1[i] / nu));
         if (j < d) U32[r * d + j] = x0[i];
@@ -784,14 +790,16 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
     count_launch(kCubSortKernels);
     if (e != cudaSuccess) return e;
   }
-  k_split_sorted<<<nblk(tot, 256), 256, 0, st>>>(kout, vout, m, n, x->pnorm, x->perm_p, x->unorm, x->perm_u);
+  k_split_sorted<<<nblk(tot, 256), 256, 0, st>>>(kout, vout, m, n, x->pnorm, x->perm_p, x->unorm, x->perm_u,
+                                                 c.inv_u);
   count_launch();
-  sort_graph_put(sg);  // last use of the sort buffers is enqueued
   // B3
   if (n)
-    k_prep_users<<<nblk((n + kPrepRows - 1) / kPrepRows * 32, 256), 256, 0, st>>>(Q, n, d, dpad, x->perm_u, x->unorm, x->U16, x->U32, x->unu); count_launch();
+    k_prep_users<<<nblk((n + kPrepRows - 1) / kPrepRows * 32, 256), 256, 0, st>>>(Q, n, d, dpad, c.inv_u, kin + m, x->U16,
+                                                                               x->U32, x->unu); count_launch();
   k_prep_items<<<nblk(m * 32, 256), 256, 0, st>>>(P, m, d, dpad, x->pd, x->perm_p, x->pnorm, c.maxabs, x->c1, x->c2,
                                                     x->P16, x->P32, x->perr, c.scale_dev); count_launch();
+  sort_graph_put(sg);  // last use of the sort buffers (kin) is enqueued
   return cudaGetLastError();
 }
 

@@ -23,6 +23,7 @@ struct BuildCtx {
   void* scratch_arena = nullptr;  // the single allocation of the build scratch below
   uint64_t* nkey = nullptr;       // [2][m + n] sort keys in/out: fp64 norm bits, top bit set for items
   int32_t* nval = nullptr;        // [2][m + n] sort values in/out: concatenated index (items first)
+  int32_t* inv_u = nullptr;       // [n] original user row -> norm-sorted row
   unsigned int* maxabs = nullptr; // max |p_j| bits
   float* scale_dev = nullptr;     // 2^e
   void* cub_tmp = nullptr;
