@@ -656,8 +656,8 @@ cudaError_t build_simt(const BuildCtx& c, cudaStream_t st) {
 
 // B2 as a CUDA graph: the radix sort is ~20 small launches and memsets whose host enqueue time
 // (~5 us each) exceeds their device time, so the GPU idles through the prep phase.  The iota +
-// sort sequence is captured once per (stream, size) into a graph over persistent buffers and
-// replayed with one launch.  Buffers are stream-ordered: builds on one stream reuse them in
+// sort sequence is captured once per (stream, size) — when that size is built a second time —
+// into a graph over persistent buffers and replayed with one launch.  Buffers are stream-ordered: builds on one stream reuse them in
 // order; different streams get different entries.  At most kSortCache entries (the oldest is
 // freed with cudaFree, which waits for the device).
 namespace {
@@ -674,6 +674,14 @@ struct SortGraph {
 constexpr int kSortCache = 4;
 std::mutex g_sort_mu;
 std::vector<SortGraph*> g_sort;
+// (stream, size, device) of recent builds: a graph is captured only when a size repeats, so
+// one-off sizes do not pay the capture (they take the direct path)
+struct SortSeen {
+  cudaStream_t st;
+  int64_t tot;
+  int dev;
+};
+std::vector<SortSeen> g_sort_seen;
 void sort_graph_free(SortGraph* g) {
   if (g->exec) cudaGraphExecDestroy(g->exec);
   cudaFree(g->keys);
@@ -693,6 +701,13 @@ SortGraph* sort_graph_get(cudaStream_t st, int64_t tot) {
       ++g->busy;
       return g;
     }
+  bool seen = false;
+  for (const SortSeen& s : g_sort_seen) seen |= s.st == st && s.tot == tot && s.dev == dev;
+  if (!seen) {
+    if (g_sort_seen.size() >= 16) g_sort_seen.erase(g_sort_seen.begin());
+    g_sort_seen.push_back(SortSeen{st, tot, dev});
+    return nullptr;
+  }
   SortGraph* g = new SortGraph;
   g->st = st; g->dev = dev; g->tot = tot;
   size_t tb = 0;
