@@ -374,8 +374,14 @@ __device__ __forceinline__ void ldg_nc_v8(const float* p, float (&v)[8]) {
                : "l"(p));
 }
 
-constexpr int kSelWarps = 8;
-constexpr int kSelRows = 32;  // rows per CTA block: each rank's 32 outputs are written as one coalesced run
+#ifndef RMIPS_SEL_WARPS
+#define RMIPS_SEL_WARPS 8
+#endif
+#ifndef RMIPS_SEL_ROWS
+#define RMIPS_SEL_ROWS 32
+#endif
+constexpr int kSelWarps = RMIPS_SEL_WARPS;
+constexpr int kSelRows = RMIPS_SEL_ROWS;  // rows per CTA block: each rank's outputs are written as one coalesced run
 constexpr int kSelStride = kSelRows + 1;  // odd stage stride: a warp's 32 ranks of one row hit 32 banks
 // One CTA per block of kSelRows consecutive rows (warp w takes rows w, w + 8, ...); a warp
 // evaluates one row at a time: one candidate per lane per round (16-byte loads of the
