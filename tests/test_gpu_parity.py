@@ -388,6 +388,32 @@ def test_build_variants_bitwise(env, monkeypatch):
     idx.close()
 
 
+def test_repeated_builds_two_streams_identical():
+    """Builds of one instance repeated on two streams (the first build of a size takes the direct
+    sort, later ones the cached per-stream sort graph) export identical permutations and lists,
+    equal to the oracle's on a sample."""
+    import torch
+    U, P = gen.random_instance(91, 3000, 900, 20)
+    Ut, Pt = _t(U), _t(P)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    ref = None
+    for rep in range(3):
+        for s in streams:
+            idx = rmips.rmips_build_index(Ut, Pt, 8, stream=s)
+            s.synchronize()
+            out = idx.export()
+            idx.close()
+            if ref is None:
+                ref = out
+                sample = np.arange(0, U.shape[0], 37)
+                vals, oids = oracle.topk(U[sample], P, 8)
+                assert np.array_equal(out[2][:, sample].T, vals)
+                assert np.array_equal(out[3][:, sample].T, oids)
+            else:
+                for a, b in zip(ref, out):
+                    assert np.array_equal(a, b), rep
+
+
 # ---------------------------------------------------------------- P' index (NEXT-1: Alg. 1 as printed)
 
 @pytest.mark.parametrize("name,bf", BUILDS)
