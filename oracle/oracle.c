@@ -21,8 +21,9 @@
  *
  * Parity status of each entry point:
  *   orc_dot, orc_norms, orc_sort_by_norm_desc, orc_topk, orc_rkmips_naive,
- *   orc_rkmips_twophase, orc_linear_scan, orc_block_bounds        -- pinned by tests/test_oracle_pins.py
- *   orc_margin                                                     -- parity bookkeeping only ("parity unpinned")
+ *   orc_rkmips_twophase, orc_linear_scan, orc_block_bounds,
+ *   orc_margin (Table 1 hand margins, exclusion of copies of q), orc_margin_lists (equals
+ *   orc_margin by brute force)                                     -- pinned by tests/test_oracle_pins.py
  */
 #include <math.h>
 #include <stdint.h>
@@ -213,5 +214,44 @@ void orc_margin(const float* U, int64_t n, const float* P, int64_t m, int d,
         double den = nq * nu;
         mu[t] = (den > 0) ? (g - tau) / den : (g - tau);
         free(top);
+    }
+}
+
+/* The same margin (reading R9) from a user's exact top-kk list over P (orc_topk output:
+ * values descending, item ids; -1 padding), so that it costs O(d + kk) per pair instead of a
+ * scan of P: tau'_k(u) is the k-th listed value whose item is not bitwise-equal to q.  Items
+ * outside the list score <= the last listed value, so the k-th surviving listed value IS the
+ * k-th largest over P minus the copies of q whenever k survivors exist; when fewer survive and
+ * the list is full (copies of q used up the slack), the pair falls back to orc_margin's scan.
+ * Used by the bench and the parity tests for the BASELINE borderline bookkeeping. */
+void orc_margin_lists(const float* U, int64_t n, const float* P, int64_t m, int d,
+                      const float* Qy, const double* topvals, const int32_t* topids, int kk,
+                      const int64_t* pairs, int64_t npairs, int k, double* mu, int threads) {
+    (void)n;
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel for schedule(dynamic, 256)
+#endif
+    for (int64_t t = 0; t < npairs; ++t) {
+        int64_t qi = pairs[2 * t], i = pairs[2 * t + 1];
+        const float* q = Qy + qi * d;
+        const float* u = U + i * d;
+        const double* v = topvals + i * kk;
+        const int32_t* id = topids + i * kk;
+        double tau = -INFINITY;
+        int seen = 0, full = 1, found = 0;
+        for (int j = 0; j < kk; ++j) {
+            if (id[j] < 0) { full = 0; break; }
+            if (memcmp(P + (int64_t)id[j] * d, q, sizeof(float) * (size_t)d) == 0) continue;
+            if (++seen == k) { tau = v[j]; found = 1; break; }
+        }
+        if (!found && full && kk < m) { /* not resolvable from the list: the definition */
+            orc_margin(U, n, P, m, d, Qy, pairs + 2 * t, 1, k, mu + t, 1);
+            continue;
+        }
+        double g = orc_dot(q, u, d);
+        double nq = sqrt(orc_dot(q, q, d)), nu = sqrt(orc_dot(u, u, d));
+        double den = nq * nu;
+        mu[t] = (den > 0) ? (g - tau) / den : (g - tau);
     }
 }

@@ -49,6 +49,8 @@ def _load():
                                         ctypes.POINTER(ctypes.c_int64)]
         lib.orc_block_bounds.argtypes = [_f64p, _I64, _I32, _I64, _f64p]
         lib.orc_margin.argtypes = [_f32p, _I64, _f32p, _I64, _I32, _f32p, _i64p, _I64, _I32, _f64p, _I32]
+        lib.orc_margin_lists.argtypes = [_f32p, _I64, _f32p, _I64, _I32, _f32p, _f64p, _i32p, _I32, _i64p, _I64,
+                                         _I32, _f64p, _I32]
         _lib = lib
     return _lib
 
@@ -142,6 +144,21 @@ def margins(U, P, Qy, pairs, k: int, threads: int = 0) -> np.ndarray:
     mu = np.empty(pairs.shape[0], np.float64)
     if pairs.shape[0]:
         _load().orc_margin(U, U.shape[0], P, P.shape[0], U.shape[1], Qy, pairs, pairs.shape[0], k, mu, threads)
+    return mu
+
+
+def margins_from_lists(U, P, Qy, topvals, topids, pairs, k: int, threads: int = 0) -> np.ndarray:
+    """Same margins as margins(), from exact top-kk lists (topk(U, P, kk) output, kk > k so that a
+    copy of q in the list still leaves k competitors); O(d + kk) per pair (reading R9)."""
+    U, P, Qy = _c32(U), _c32(P), _c32(Qy)
+    topvals = np.ascontiguousarray(topvals, np.float64)
+    topids = np.ascontiguousarray(topids, np.int32)
+    assert topvals.shape == topids.shape and topvals.shape[0] == U.shape[0]
+    pairs = np.ascontiguousarray(pairs, np.int64).reshape(-1, 2)
+    mu = np.empty(pairs.shape[0], np.float64)
+    if pairs.shape[0]:
+        _load().orc_margin_lists(U, U.shape[0], P, P.shape[0], U.shape[1], Qy, topvals, topids, topvals.shape[1],
+                                 pairs, pairs.shape[0], k, mu, threads)
     return mu
 
 

@@ -253,8 +253,71 @@ def test_block_bounds_against_library():
         assert np.array_equal(oracle.block_bounds(L, b), ref)
 
 
+def test_margin_table1_hand_values():
+    """orc_margin against hand arithmetic on Table 1 (golden decimals; reading R9):
+    q = p5 is itself an item, so tau'_k(u) is taken over P minus p5.
+      u3, k = 1: tau'_1 = u3.p4 = 7.82  -> mu = (8.23 - 7.82) / (|p5| |u3|)
+      u4, k = 2: tau'_2 = u4.p2 = 10.26 -> mu = (11.78 - 10.26) / (|p5| |u4|)   (u4.p4 = 10.84 is tau'_1)
+      u1, k = 1: tau'_1 = u1.p3 = 10.02 -> mu = (1.89 - 10.02) / (|p5| |u1|)   (negative: not a member)
+    A dropped exclusion (tau = 8.23 itself -> mu = 0), a dropped normalisation (mu = 0.41) or a wrong
+    rank each fail here."""
+    U, P = _t1()
+    ip, hn = GOLD["hand_inner_products"], GOLD["hand_norms"]
+    nrm = lambda s: np.sqrt(hn[s + "_sq"])  # noqa: E731
+    cases = [(2, 1, ip["u3"]["p5"], ip["u3"]["p4"], "u3"), (3, 2, ip["u4"]["p5"], ip["u4"]["p2"], "u4"),
+             (0, 1, ip["u1"]["p5"], ip["u1"]["p3"], "u1")]
+    q = P[[4]]
+    for i, k, g, tau, un in cases:
+        want = (g - tau) / (nrm("p5") * nrm(un))
+        mu = oracle.margins(U, P, q, np.array([[0, i]]), k)[0]
+        assert abs(mu - want) < 1e-6, (un, k, mu, want)
+    assert abs(oracle.margins(U, P, q, np.array([[0, 2]]), 1)[0] - 0.04481) < 5e-5   # VERDICT r1 figure
+
+
+def test_margin_excludes_every_copy_of_q():
+    """Two more bitwise copies of p5 in P change nothing (Def. 2 takes P u {q} as a set, R8/R9); a
+    vector that differs from p5 in one ulp is a competitor and sets tau'_1 = its score."""
+    U, P = _t1()
+    q = P[[4]]
+    P2 = np.concatenate([P, q, q])
+    pairs = np.array([[0, 2], [0, 3]])
+    assert np.array_equal(oracle.margins(U, P2, q, pairs, 1), oracle.margins(U, P, q, pairs, 1))
+    near = q.copy()
+    near[0, 1] = np.nextafter(near[0, 1], np.float32(0))      # 3.4 - 1 ulp: scores just below u.q
+    P3 = np.concatenate([P, near])
+    mu = oracle.margins(U, P3, q, pairs, 1)
+    assert (mu > 0).all() and (mu < 1e-6).all()               # competitor now sits right under q
+
+
+@pytest.mark.parametrize("seed", [50, 51, 52])
+def test_margin_lists_equals_brute_force(seed):
+    """orc_margin_lists (top-list form) equals orc_margin (scan of P) on every pair: queries from P,
+    duplicated items (copies of q inside the list), fresh queries; k up to the list length - 1."""
+    U, P = _inst(seed, 40, 30, 6, "skewed")
+    P = np.concatenate([P, P[[2, 2, 5]]])                      # items 30, 31 copy item 2; 32 copies 5
+    Qy = np.concatenate([P[[2, 5, 7]], _inst(seed + 7, 3, 1, 6)[0]])
+    kk = 9
+    vals, ids = oracle.topk(U, P, kk)
+    pairs = np.array([(qi, i) for qi in range(Qy.shape[0]) for i in range(U.shape[0])])
+    for k in (1, 4, 8):
+        a = oracle.margins(U, P, Qy, pairs, k)
+        b = oracle.margins_from_lists(U, P, Qy, vals, ids, pairs, k)
+        assert np.array_equal(a, b), k
+
+
+def test_sort_tie_order_ascending_id():
+    """Reading R6 (P:279 says only 'descending'): equal norms keep ascending original ids.  Checked
+    against numpy's stable lexsort on (-norm, id) (a library routine), on exact power-of-two norms."""
+    X = np.zeros((9, 3), np.float32)
+    X[:, 0] = [1, 2, 1, 4, 2, 1, 4, 0, 2]
+    nrm = oracle.norms(X)
+    perm = oracle.sort_by_norm_desc(nrm)
+    assert perm.tolist() == [3, 6, 1, 4, 8, 0, 2, 5, 7]
+    assert np.array_equal(perm, np.lexsort((np.arange(9), -nrm)))
+
+
 def test_margin_sign_matches_membership_for_fresh_queries():
-    """Bookkeeping helper (parity unpinned): for q not in P, mu >= 0 <=> member."""
+    """For q not in P, mu >= 0 <=> member (Def. 2 with reading R1)."""
     U, P = _inst(30, 25, 20, 8)
     Qy = _inst(31, 4, 1, 8)[0]
     mem = oracle.rkmips_naive(U, P, Qy, 3)
