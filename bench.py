@@ -2,25 +2,33 @@
 """bench.py -- one JSON line per run for the exact reverse k-MIPS hot path on B200.
 
 A step = one pass of the whole hot path (SURVEY §8(a) rows B1-B6 + Q1-Q6) over one batch of
-synthetic input: rmips_build_index over (Q, P) followed by rmips_query over the config's whole
-query set (k fixed), then rmips_free_index.  Inputs are device-resident when the timed region
-starts; L2 (126 MB) is flushed before every timed step (a 512 MiB memset).
+synthetic input: rmips_build_index over (Q, P), then rmips_query over the config's whole query set
+in calls of the config's batch size (BASELINE.json configs[4]: 10,000 fresh queries "in batches of
+256" = 40 calls), then rmips_free_index.  Inputs are device-resident when the timed region starts;
+L2 (126 MB) is flushed before every timed step (a 512 MiB memset).
 
-Default workload: BASELINE.json configs[1] (100,000 users x 25,000 items, d = 50, k_max = 50,
-1,000 queries drawn from P, k = 10), generated by synth/ (seed 0).
+Default workload: BASELINE.json configs[4] -- d = 200, |Q| = 1,000,000 users, |P| = 1,000,000 items,
+lognormal(0, 0.75) norms, k_max = 50, k = 50 -- the largest single-GPU configuration ("index build
+dominated"); BASELINE.json's metric names no config.  configs[0..3] run after it as extra keys
+("configs"), each with its own parity block (the small oracle case and the paper-shaped ones).
 
 value = inner products evaluated exactly per second over the whole step:
         (n*m  [index build, Alg. 1 over all of P]  +  nq*n  [query x user]) / step time.
 The JSON also carries the build rate (n*m / build time) and queries/s separately.
 
---impl reference runs the reference arm: the fp64 CPU oracle (oracle/), the only reference this
-paper has, on a bounded user sample of the same workload on the host cores.
+parity: the timed step's own output, checked against the fp64 oracle (oracle/) on a fixed user
+sample (every query's decision for those users), with SURVEY §8(c)'s borderline bookkeeping:
+disagreements and in-band pairs (|q.u - tau'_k(u)| <= 1e-5 |q||u|, reading R9).
+
+--impl reference runs the reference arm: the fp64 CPU oracle, the only reference this paper has,
+on a bounded user sample of the same workload on the host cores.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -34,6 +42,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "reverse k-MIPS queries/sec + index-build inner products/sec; % of roofline"
 UNIT = "inner products/s (build n*m + query nq*n, whole step)"
+BAND = 1e-5  # BASELINE north star: borderline users |q.u - tau_k(u)| <= 1e-5 |q||u|
 
 
 def _peaks():
@@ -45,8 +54,18 @@ def _peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
 
 
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -63,13 +82,14 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.3)  # the first samples land before the timed region starts
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
     def __exit__(self, *a):
         if self.proc:
@@ -79,16 +99,19 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
-        sm, mx, reasons = [], None, set()
+    def summary(self, t0=None, t1=None):
+        sm, mx, reasons, power = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ts, ln in self.lines:
+            if t0 is not None and not (t0 <= ts <= t1):
+                continue
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
             try:
                 sm.append(float(f[1]))
                 mx = float(f[2])
+                power.append(float(f[3]))
             except ValueError:
                 continue
             for nm, v in zip(names, f[5:9]):
@@ -96,7 +119,8 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
 
 
 def _dist():
@@ -106,75 +130,347 @@ def _dist():
     return ws, rank, local
 
 
+def _batches(nq, bs):
+    return [(b0, min(nq, b0 + bs)) for b0 in range(0, nq, bs)]
+
+
+# ------------------------------------------------------------------------------ the oracle legs
+
+def oracle_sample(w, k, users: int, threads: int, seed: int):
+    """The fp64 oracle on a fixed user sample of the workload: phase 1 = exact top-(k_max + 1) lists
+    over all of P (Alg. 1 lines 7-9 over P, the index build's analogue), phase 2 = every query's
+    decision for those users (two-phase form, equal to Def. 2 by reading R8).  Timed separately."""
+    import oracle
+    spec = w.spec
+    rng = np.random.default_rng(seed)
+    sample = np.sort(rng.choice(spec.n, min(users, spec.n), replace=False))
+    Us = np.ascontiguousarray(w.U[sample])
+    t0 = time.perf_counter()
+    vals, ids = oracle.topk(Us, w.P, spec.k_max + 1, threads=threads)
+    t1 = time.perf_counter()
+    member = oracle.rkmips_twophase(Us, np.ascontiguousarray(vals[:, :spec.k_max]), w.Qy, k, threads=threads)
+    t2 = time.perf_counter()
+    return sample, vals, ids, member, t1 - t0, t2 - t1
+
+
+def cpu_baseline(w, k, users: int, users_1t: int, seed: int = 2):
+    """The oracle as it stands, timed on the host: all cores on `users` sampled users, and one thread on
+    `users_1t` of them (phase 1 inner products/s and phase 2 queries/s reported separately)."""
+    spec = w.spec
+    cores = os.cpu_count() or 1
+    sample, vals, ids, member, p1, p2 = oracle_sample(w, k, users, cores, seed)
+    s1 = oracle_sample(w, k, users_1t, 1, seed + 1)
+    S, S1 = len(sample), len(s1[0])
+    units = S * spec.m + spec.nq * S
+    out = {"value": units / (p1 + p2), "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
+           "sample": "%d of %d users: exact fp64 top-%d over all %d items (phase 1, %.2f s) + %d query decisions "
+                     "each (phase 2, %.2f s), %d threads" % (S, spec.n, spec.k_max + 1, spec.m, p1, spec.nq, p2, cores),
+           "phase1_inner_products_per_s": S * spec.m / p1,
+           "phase2_queries_per_s": spec.nq / p2, "phase2_note": "decisions for the %d sampled users per query" % S,
+           "one_thread": {"users": S1, "phase1_inner_products_per_s": S1 * spec.m / s1[4],
+                          "phase2_queries_per_s": spec.nq / s1[5], "value": (S1 * spec.m + spec.nq * S1) / (s1[4] + s1[5])}}
+    return out, (sample, vals, ids, member)
+
+
+def parity_block(w, k, sets, sample, vals, ids, member, threads):
+    """SURVEY §8(c) comparison procedure on the sampled users: per query, GPU set restricted to the
+    sample vs the oracle's; every disagreement's margin; in-band pairs over all (query, sampled user)."""
+    import oracle
+    spec = w.spec
+    nq = len(sets)
+    assert nq == spec.nq
+    mine = np.zeros((nq, len(sample)), bool)
+    ascending = True
+    for qi, s_ in enumerate(sets):
+        ascending &= bool((np.diff(s_) > 0).all())
+        mine[qi] = np.isin(sample, s_, assume_unique=True)
+    dis = np.argwhere(mine != member)
+    qq, jj = np.meshgrid(np.arange(nq, dtype=np.int64), np.arange(len(sample), dtype=np.int64), indexing="ij")
+    pairs = np.stack([qq.ravel(), jj.ravel()], axis=1)
+    mu = oracle.margins_from_lists(w.U[sample], w.P, w.Qy, vals, ids, pairs, k, threads=threads)
+    inband = int((np.abs(mu) <= BAND).sum())
+    dis_mu = mu[dis[:, 0] * len(sample) + dis[:, 1]] if len(dis) else np.zeros(0)
+    excused = int((np.abs(dis_mu) <= BAND).sum())
+    return {"users_sampled": int(len(sample)), "queries": nq, "pairs_checked": int(nq * len(sample)),
+            "disagreements": int(len(dis)), "excused_borderline": excused, "hard_failures": int(len(dis)) - excused,
+            "in_band_pairs": inband, "sets_ascending": ascending,
+            "oracle_members": int(member.sum()), "gpu_members": int(mine.sum()),
+            "rule": "identical sets except |q.u - tau'_k(u)| <= 1e-5 |q||u| (tau' over P minus copies of q, R9)"}
+
+
 # ------------------------------------------------------------------------------ reference arm (oracle)
 
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
-    import oracle
     from synth import make_workload
     w = make_workload(args.config)
     spec = w.spec
-    k = args.k or spec.ks[0]
+    k = args.k or spec.ks[-1]
     cores = os.cpu_count() or 1
-    S = args.ref_users
-    rng = np.random.default_rng(1)
+    S = args.ref_users or (64 if spec.m * spec.d > 1e8 else 1000)
     times = []
     for it in range(args.warmup + args.steps):
-        sample = np.sort(rng.choice(spec.n, S, replace=False))
-        t0 = time.perf_counter()
-        vals, _ = oracle.topk(w.U[sample], w.P, spec.k_max, threads=cores)      # Alg. 1 over all P
-        oracle.rkmips_twophase(w.U[sample], vals, w.Qy, k, threads=cores)       # Def. 2 decisions
-        dt = time.perf_counter() - t0
+        _, _, _, _, p1, p2 = oracle_sample(w, k, S, cores, 100 + it)
         if it >= args.warmup:
-            times.append(dt)
+            times.append(p1 + p2)
     units = S * spec.m + spec.nq * S
     t = sum(times) / len(times)
     v = units / t
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY Appendix C generator, seed 0)",
-            "config": {"workload": spec.name, "n": spec.n, "m": spec.m, "d": spec.d, "k_max": spec.k_max,
-                       "queries": spec.nq, "k": k, "ref_user_sample": S},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "config": _config_dict(spec, k, ws) | {"ref_user_sample": S},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
                              "sample": "%d of %d users per step: exact fp64 top-%d over all %d items + %d query "
-                                       "decisions each" % (S, spec.n, spec.k_max, spec.m, spec.nq)},
+                                       "decisions each" % (S, spec.n, spec.k_max + 1, spec.m, spec.nq)},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
 
 
-def cpu_baseline(w, k, users: int):
-    import oracle
-    spec = w.spec
-    cores = os.cpu_count() or 1
-    rng = np.random.default_rng(2)
-    sample = np.sort(rng.choice(spec.n, users, replace=False))
-    t0 = time.perf_counter()
-    vals, _ = oracle.topk(w.U[sample], w.P, spec.k_max, threads=cores)
-    oracle.rkmips_twophase(w.U[sample], vals, w.Qy, k, threads=cores)
-    dt = time.perf_counter() - t0
-    units = users * spec.m + spec.nq * users
-    return {"value": units / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": "%d of %d users: exact fp64 top-%d over all %d items + %d query decisions each (%.1f s)"
-                      % (users, spec.n, spec.k_max, spec.m, spec.nq, dt)}
+def _config_dict(spec, k, ws):
+    return {"workload": spec.name, "n": spec.n, "m": spec.m, "d": spec.d, "k_max": spec.k_max, "queries": spec.nq,
+            "k": k, "query_batch": "%d calls of <= %d queries" % (len(_batches(spec.nq, spec.batch)), spec.batch),
+            "l2": "flushed (512 MiB memset) before every timed step", "parallelism": "user-shard x%d" % ws}
 
 
 # ------------------------------------------------------------------------------ our arm
 
+def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, cpu=True, k=None):
+    import torch
+    from paper_2110_07131_b200 import rmips
+    from synth import make_workload
+
+    w = make_workload(cfg, seed=0)
+    if rank > 0:
+        w.U = make_workload(cfg, seed=rank).U
+    spec = w.spec
+    k = k or args.k or spec.ks[-1]
+    U = torch.from_numpy(w.U).to(dev)
+    P = torch.from_numpy(w.P).to(dev)
+    Qy = torch.from_numpy(w.Qy).to(dev)
+    batches = _batches(spec.nq, spec.batch)
+    Qb = [Qy[a:b] for a, b in batches]
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    bflags = rmips.RMIPS_BUILD_TIMING | (rmips.RMIPS_BUILD_SIMT if args.simt else 0)
+    qflags = rmips.RMIPS_FLAG_TIMING | (rmips.RMIPS_FLAG_SIMT if args.simt else 0)
+    stream = torch.cuda.current_stream()
+    m_prime = args.pprime * spec.k_max if args.pprime else 0
+    cap = [None]  # learned during the warm-up steps (the first call sizes itself: rmips.py retries once)
+
+    def step():
+        """One pass of the hot path: build + every query call.  Per-call phase times and counters are
+        read right after each call (host reads of values the call already synchronised on)."""
+        if m_prime:
+            idx = rmips.rmips_build_index_pprime(U, P, spec.k_max, m_prime, bflags)
+        else:
+            idx = rmips.rmips_build_index(U, P, spec.k_max, bflags)
+        outs, qph = [], []
+        for q in Qb:
+            off, ids = rmips.rmips_query(idx, q, k, qflags, capacity=cap[0])
+            outs.append((off, ids))
+            qph.append((idx.phase_times(), idx.stats()))
+        return idx, outs, qph
+
+    def readout(idx, outs, qph):
+        pt = idx.phase_times()  # build phases (ms[0..3], launches ms[14]) survive the queries
+        rec = {"prep": pt[0], "contraction": pt[1], "select": pt[2], "build": pt[3], "build_launches": pt[14],
+               "cand_per_user": idx.cand_total / max(1, spec.n), "tiles_issued": idx.tiles_done,
+               "q_prep": sum(p[8] for p, _ in qph), "q_filter": sum(p[9] for p, _ in qph),
+               "q_exact": sum(p[10] for p, _ in qph), "q_output": sum(max(0.0, p[11]) for p, _ in qph),
+               "q_total": sum(p[12] for p, _ in qph), "q_launches": sum(p[15] for p, _ in qph),
+               "tiles_scored": sum(s["tiles_scored"] for _, s in qph), "scans": sum(s["scans"] for _, s in qph),
+               "items_scanned": sum(s["items_scanned"] for _, s in qph),
+               "undecided": sum(s["pairs_undecided"] for _, s in qph),
+               "filter_kernel": min(s["filter_kernel"] for _, s in qph),
+               "result_total": sum(s["result_total"] for _, s in qph)}
+        need = max(int(o[1].numel()) for o in outs)
+        if cap[0] is None or need > cap[0] // 2:
+            cap[0] = max(1 << 16, 2 * need)
+        idx.close()
+        return rec
+
+    for _ in range(warmup):
+        readout(*step())
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    step_ms, recs = [], []
+    last = None
+    sampler = ClockSampler(dev.index)
+    with sampler:
+        tw0 = time.perf_counter()
+        for _ in range(steps):
+            flush.zero_()                               # L2 flush, outside the timed region
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            idx, outs, qph = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            recs.append(readout(idx, outs, qph))        # (frees the index: stream-ordered, after e1)
+            step_ms.append(e0.elapsed_time(e1))
+            last = outs
+        tw1 = time.perf_counter()
+    clocks = sampler.summary(tw0, tw1)
+    torch.cuda.synchronize()
+    t_rank = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([t_rank], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(t.item())
+    else:
+        t_max = t_rank
+    units_step = spec.n * spec.m + spec.nq * spec.n
+    value = ws * units_step * steps / (t_max / 1e3)
+    ms_per_step = t_max / steps
+    med = lambda key: float(np.median([r[key] for r in recs]))  # noqa: E731
+    peaks = _peaks()
+
+    # ---- roofline of the dominant kernel: the build contraction (B4), tensor-core bound.
+    # achieved = algorithmic flops of the (user tile, item tile) contractions actually issued (2 d per
+    # user-item pair; tiles skipped by the Cauchy-Schwarz exit are not counted) / the contraction time;
+    # effective = 2 n m d / time counts the pruned pairs too.
+    kern_ms = med("contraction")
+    tiles = med("tiles_issued")
+    flops_eff = 2.0 * spec.n * spec.m * spec.d
+    flops = 2.0 * tiles * 128 * 128 * spec.d if tiles > 0 else flops_eff
+    achieved = flops / (kern_ms / 1e3) / 1e12
+    # burst peak for a kernel timed alone (ms-scale), the sustained peak (back-to-back matmul for 4 s,
+    # power-capped clocks) for one that runs for tens of ms inside a long step
+    sustained = kern_ms > 20.0 and peaks.get("bf16_tflops_sustained")
+    peak = peaks["bf16_tflops_sustained"] if sustained else peaks["bf16_tflops"]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    kname = "k_build_simt" if args.simt else ("k_build_tc" if spec.d <= 64 else "k_build_tcq")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        traffic = tj.get("cfg%d" % cfg, {}).get("simt" if args.simt else "tc")
+    roof = {"bound": "tensor", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "peak_src": ("MEASURED_PEAKS.json %s (fp16 has the bf16 dense rate)"
+                         % ("bf16_tflops_sustained" if sustained else "bf16_tflops (burst)"))
+            if peaks["src"] == "measured" else "fallback (B200_PROFILING.md)",
+            "flops_per_launch": flops, "flop_unit": "2 d per (user, item) pair of the issued 128 x 128 tiles",
+            "tiles_issued": tiles, "kernel_ms": kern_ms,
+            "effective_tflops_incl_pruned": flops_eff / (kern_ms / 1e3) / 1e12,
+            "share_of_step": kern_ms / ms_per_step}
+
+    # ---- the query filter (Q2+Q3, k_query_tc): HBM-bound stream of the users' fp16 rows + thresholds
+    qf_ms = med("q_filter")
+    qbytes = med("tiles_scored") * 128 * (2 * spec.d + 4)
+    ubytes = spec.n * (2 * spec.d + 4)
+    roof_q = {"bound": "hbm" if ubytes > 126e6 else "l2 (user rows fit in the 126 MB L2)",
+              "kernel": "k_query_simt" if args.simt else "k_query_tc",
+              "achieved": qbytes / (qf_ms / 1e3) / 1e9 if qf_ms > 0 else None, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+              "frac": (qbytes / (qf_ms / 1e3) / 1e9) / peaks["hbm_gbs"] if qf_ms > 0 else None,
+              "bytes_per_step": qbytes, "byte_unit": "(2 d + 4) B per user of every 128-user tile Lemma 3 keeps, "
+                                                      "per query call", "kernel_ms_per_step": qf_ms,
+              "calls": len(batches)}
+
+    # ---- the verification scan (Q5, k_verify_scan), P' index only
+    roof_s = None
+    if m_prime:
+        ex_ms = med("q_exact")
+        sbytes = med("items_scanned") * 4 * (((spec.d + 7) // 8) * 8)
+        p32 = spec.m * 4 * (((spec.d + 7) // 8) * 8)
+        roof_s = {"bound": "hbm" if p32 > 126e6 else "l2 (P32 fits in the 126 MB L2)",
+                  "kernel": "k_exact_decide_pp + k_verify_scan", "kernel_ms": ex_ms, "scans": med("scans"),
+                  "items_scanned": med("items_scanned"), "bytes_per_step": sbytes,
+                  "achieved": sbytes / (ex_ms / 1e3) / 1e9 if ex_ms > 0 else None, "peak": peaks["hbm_gbs"],
+                  "unit": "GB/s", "frac": (sbytes / (ex_ms / 1e3) / 1e9) / peaks["hbm_gbs"] if ex_ms > 0 else None}
+
+    res = {"value": value, "ms_per_step": ms_per_step, "steps": steps, "warmup": warmup,
+           "config": _config_dict(spec, k, ws) | {"kernels": "simt" if args.simt else "tcgen05"},
+           "build": {"ms": med("build"), "inner_products_per_s": spec.n * spec.m / (med("build") / 1e3),
+                     "contraction_ms": kern_ms, "prep_ms": med("prep"), "select_blocks_ms": med("select"),
+                     "candidates_per_user": med("cand_per_user")},
+           "query": {"ms": med("q_total"), "queries_per_s": spec.nq / (med("q_total") / 1e3), "calls": len(batches),
+                     "prep_ms": med("q_prep"), "filter_ms": qf_ms, "exact_ms": med("q_exact"),
+                     "output_ms": med("q_output"), "undecided_pairs": med("undecided"),
+                     "result_ids": recs[-1]["result_total"], "filter_kernel_tcgen05": bool(recs[-1]["filter_kernel"]),
+                     "wall_ms_incl_host": ms_per_step - med("build")},
+           "roofline": roof, "roofline_query": roof_q, "clocks": clocks,
+           "gpu_launches": int(med("build_launches") + med("q_launches")) * steps}
+    if m_prime:
+        res["roofline_scan"] = roof_s
+        res["index"] = "P' over the first %d items (Alg. 1 line 6)" % m_prime
+
+    # ---- parity of the last timed step's output against the oracle (sampled users), rank 0
+    sets = None
+    if parity_users and rank == 0:
+        sets = []
+        for off, ids in last:
+            sets += rmips.split_sets(off, ids)
+    del last
+
+    # ---- end to end through the public API with HOST buffers (copies inside the timed region)
+    if e2e:
+        Uh = torch.from_numpy(w.U).pin_memory()
+        Ph = torch.from_numpy(w.P).pin_memory()
+        Qh = [torch.from_numpy(np.ascontiguousarray(w.Qy[a:b])).pin_memory() for a, b in batches]
+        offh = [torch.empty(b - a + 1, dtype=torch.int64).pin_memory() for a, b in batches]
+        idsh = torch.empty(cap[0], dtype=torch.int32).pin_memory()
+        e2e_ms, d2h = [], 0
+        for it in range(warmup + steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            idx = rmips.rmips_build_index_host(Uh, Ph, spec.k_max)
+            d2h = 0
+            for j, q in enumerate(Qh):
+                off, ids = rmips.rmips_query_host(idx, q, k, out_offsets=offh[j], out_ids=idsh, capacity=idsh.numel())
+                d2h += 8 * int(offh[j].numel()) + 4 * int(len(ids))
+            e1.record(stream)
+            torch.cuda.synchronize()
+            idx.close()
+            if it >= warmup:
+                e2e_ms.append(e0.elapsed_time(e1))
+        t_e2e = sum(e2e_ms)
+        if ws > 1:
+            t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            t_e2e = float(t.item())
+        res["e2e"] = {"value": ws * units_step * steps / (t_e2e / 1e3), "unit": UNIT,
+                      "h2d_bytes_per_step": 4 * spec.d * (spec.n + spec.m + spec.nq), "d2h_bytes_per_step": d2h,
+                      "ms_per_step": t_e2e / steps,
+                      "api": "rmips_build_index_host + %d rmips_query_host calls (pinned host buffers)" % len(batches)}
+    del U, P, Qy, Qb, flush
+    torch.cuda.empty_cache()
+
+    if rank == 0 and (cpu or parity_users):
+        cores = os.cpu_count() or 1
+        if cpu and ws == 1:
+            base, orc = cpu_baseline(w, k, parity_users, args.cpu_users_1t)
+            res["cpu_baseline"] = base
+        else:
+            s_, v_, i_, m_, _, _ = oracle_sample(w, k, parity_users, cores, 2)
+            orc = (s_, v_, i_, m_)
+        if sets is not None:
+            res["parity"] = parity_block(w, k, sets, *orc, threads=cores)
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="rmips", choices=["rmips", "reference"])
-    ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--k", type=int, default=0, help="0 = the config's k (the last of its sweep for configs[2])")
+    ap.add_argument("--extra", default="0,1,2,3", help="configs run after the headline one (extra keys); '' = none")
+    ap.add_argument("--extra-steps", type=int, default=5)
     ap.add_argument("--simt", action="store_true", help="CUDA-core build/query kernels instead of tcgen05")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-users", type=int, default=0, help="oracle user sample (0 = all users of the config)")
-    ap.add_argument("--ref-users", type=int, default=4000)
+    ap.add_argument("--parity-users", type=int, default=0, help="oracle user sample (0 = per-config default)")
+    ap.add_argument("--cpu-users-1t", type=int, default=8, help="users of the one-thread oracle timing")
+    ap.add_argument("--ref-users", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--pprime", type=int, default=0,
                     help="NEXT-1: build the P' index over the first C * k_max items (Alg. 1 as printed) "
@@ -196,192 +492,42 @@ def main():
 
     import __graft_entry__
     __graft_entry__.build()
-    from paper_2110_07131_b200 import rmips
-    from synth import make_workload
 
-    # weak scaling: every rank owns its own user shard of the config's size (users drawn with
-    # seed = rank), the same items and queries (seed 0); users are independent, so the path has
-    # no data-path collective.
-    w = make_workload(args.config, seed=0)
-    if rank > 0:
-        w.U = make_workload(args.config, seed=rank).U
-    spec = w.spec
-    k = args.k or spec.ks[0]
-    U = torch.from_numpy(w.U).to(dev)
-    P = torch.from_numpy(w.P).to(dev)
-    Qy = torch.from_numpy(w.Qy).to(dev)
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    bflags = rmips.RMIPS_BUILD_TIMING | (rmips.RMIPS_BUILD_SIMT if args.simt else 0)
-    qflags = rmips.RMIPS_FLAG_TIMING | (rmips.RMIPS_FLAG_SIMT if args.simt else 0)
-    stream = torch.cuda.current_stream()
+    def pusers(cfg, budget=1.5e10):
+        """oracle user sample: about `budget` fp64 MAC of phase 1 (~2-6 s on the box's cores)"""
+        if args.parity_users:
+            return args.parity_users
+        from synth.generator import CONFIGS
+        s = CONFIGS[cfg]
+        return int(min(s.n, max(64, budget / (s.m * s.d))))
 
-    m_prime = args.pprime * spec.k_max if args.pprime else 0
-
-    def step():
-        """One pass of the hot path (build + the whole query batch); returns the live index so that
-        the instrumentation reads (phase times, counters) happen outside the timed region."""
-        if m_prime:
-            idx = rmips.rmips_build_index_pprime(U, P, spec.k_max, m_prime, bflags)
-        else:
-            idx = rmips.rmips_build_index(U, P, spec.k_max, bflags)
-        off, ids = rmips.rmips_query(idx, Qy, k, qflags)
-        return idx, ids
-
-    def readout(idx, ids):
-        pt = idx.phase_times()
-        st = idx.stats()
-        pt.append(idx.cand_total / max(1, spec.n))
-        pt.append(st["tiles_scored"])
-        pt.append(idx.tiles_done)
-        pt.append(st["scans"])
-        pt.append(st["items_scanned"])
-        total = int(ids.numel())
-        idx.close()
-        return pt, total
-
-    for _ in range(args.warmup):
-        readout(*step())
-    torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
-    step_ms, phases, totals = [], [], []
-    sampler = ClockSampler(dev.index)
-    with sampler:
-        for _ in range(args.steps):
-            flush.zero_()                               # L2 flush, outside the timed region
-            torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            idx, ids = step()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            pt, total = readout(idx, ids)  # (frees the index: stream-ordered, after e1)
-            step_ms.append(e0.elapsed_time(e1))
-            phases.append(pt)
-            totals.append(total)
-    torch.cuda.synchronize()
-    t_rank = sum(step_ms)
-    if ws > 1:
-        t = torch.tensor([t_rank], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        t_max = float(t.item())
-        torch.distributed.barrier()
-    else:
-        t_max = t_rank
-    units_step = spec.n * spec.m + spec.nq * spec.n
-    value = ws * units_step * args.steps / (t_max / 1e3)
-    ms_per_step = t_max / args.steps
-    ph = np.array(phases)
-    med = lambda i: float(np.median(ph[:, i]))  # noqa: E731
-    build_ms, kern_ms, query_ms = med(3), med(1), med(12)
-    peaks = _peaks()
-
-    # ---- roofline of the dominant kernel: the build contraction (B4), tensor (or FFMA) bound.
-    # achieved = algorithmic flops of the (user tile, item tile) contractions actually issued
-    # (2 d per user-item pair; tiles skipped by the Cauchy-Schwarz exit are not counted) / time;
-    # effective = 2 n m d / time counts the pruned pairs too.
-    bn = 128  # item-tile width of both tensor-core build kernels (build_tc.cu, build_tcq.cu)
-    tiles = med(18)
-    flops_eff = 2.0 * spec.n * spec.m * spec.d
-    flops = 2.0 * tiles * 128 * bn * spec.d if tiles > 0 else flops_eff
-    achieved = flops / (kern_ms / 1e3) / 1e12
-    # burst peak for a kernel timed alone (ms-scale), the sustained peak (back-to-back matmul for 4 s,
-    # power-capped clocks) for one that runs for tens of ms inside a long step
-    sustained = kern_ms > 20.0 and peaks.get("bf16_tflops_sustained")
-    peak = peaks["bf16_tflops_sustained"] if sustained else peaks["bf16_tflops"]
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        tj = json.load(open(tpath))
-        traffic = tj.get("cfg%d" % args.config, {}).get("simt" if args.simt else "tc")
-    roof = {"bound": "tensor", "kernel": "k_build_simt" if args.simt else "k_build_tc",
-            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": traffic, "peak_src": ("MEASURED_PEAKS.json %s (fp16 same dense rate)"
-                                                % ("bf16_tflops_sustained" if sustained else "bf16_tflops (burst)"))
-            if peaks["src"] == "measured" else "fallback (B200_PROFILING.md)",
-            "flops_per_launch": flops, "tiles_issued": tiles, "kernel_ms": kern_ms,
-            "effective_tflops_incl_pruned": flops_eff / (kern_ms / 1e3) / 1e12,
-            "share_of_step": kern_ms / ms_per_step}
-
-    # ---- the query filter (Q2+Q3, k_query_tc): HBM-bound stream of the users' fp16 rows + thresholds
-    qf_ms = med(9)
-    # algorithmic bytes: the fp16 user rows (d, unpadded) + fp32 thresholds of the 128-user tiles that
-    # Lemma 3 did not prune whole, once per 256-query sub-batch
-    qbytes = med(17) * 128 * (2 * spec.d + 4)
-    roof_q = {"bound": "hbm", "kernel": "k_query_simt" if args.simt else "k_query_tc",
-              "achieved": qbytes / (qf_ms / 1e3) / 1e9 if qf_ms > 0 else None, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-              "frac": (qbytes / (qf_ms / 1e3) / 1e9) / peaks["hbm_gbs"] if qf_ms > 0 else None,
-              "bytes_per_launch": qbytes, "kernel_ms": qf_ms,
-              "note": "the filter kernel (Lemma 3 + contraction + classify); sub-batches after the first may hit L2 "
-                      "when the user rows fit in it (126 MB)"}
-
-    # ---- the verification scan (Q5, k_verify_scan), P' index only: it streams the norm-sorted
-    # item rows (pd fp32 each) after P' for every pair the O(1) lemmas leave open
-    roof_s = None
-    if m_prime:
-        ex_ms = med(10)
-        sbytes = med(20) * 4 * (((spec.d + 7) // 8) * 8)
-        roof_s = {"bound": "hbm", "kernel": "k_exact_decide_pp + k_verify_scan", "kernel_ms": ex_ms,
-                  "scans": med(19), "items_scanned": med(20), "bytes_per_launch": sbytes,
-                  "achieved": sbytes / (ex_ms / 1e3) / 1e9 if ex_ms > 0 else None, "peak": peaks["hbm_gbs"],
-                  "unit": "GB/s", "frac": (sbytes / (ex_ms / 1e3) / 1e9) / peaks["hbm_gbs"] if ex_ms > 0 else None,
-                  "note": "item rows scanned x pd x 4 B; P32 (%.1f MB) is L2-resident when it fits in 126 MB"
-                          % (spec.m * 4 * (((spec.d + 7) // 8) * 8) / 1e6)}
-
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "fp16-filter/f64-exact",
-            "data": "synthetic (SURVEY Appendix C generator; users seed = rank, items/queries seed 0); stands in for MovieLens-shaped MF vectors",
-            "config": {"workload": spec.name, "n": spec.n, "m": spec.m, "d": spec.d, "k_max": spec.k_max,
-                       "queries": spec.nq, "k": k, "query_batch": "all %d in one rmips_query call" % spec.nq,
-                       "l2": "flushed (512 MiB memset) before every timed step", "kernels": "simt" if args.simt
-                       else "tcgen05", "parallelism": "user-shard x%d (weak)" % ws},
-            "build": {"ms": build_ms, "inner_products_per_s": spec.n * spec.m / (build_ms / 1e3),
-                      "contraction_ms": kern_ms, "prep_ms": med(0), "select_blocks_ms": med(2),
-                      "candidates_per_user": med(16)},
-            "query": {"ms": query_ms, "queries_per_s": spec.nq / (query_ms / 1e3), "prep_ms": med(8), "filter_ms": med(9),
-                      "exact_ms": med(10), "output_ms": med(11), "result_ids": totals[-1]},
-            "roofline": roof, "roofline_query": roof_q, "clocks": sampler.summary(),
-            **({"roofline_scan": roof_s, "index": "P' over the first %d items (Alg. 1 line 6)" % m_prime}
-               if m_prime else {}),
-            "gpu_launches": int(med(14) + med(15)) * args.steps}
-
-    # ---- end to end through the public API with HOST buffers (copies inside the timed region)
-    if not args.no_e2e:
-        Uh = torch.from_numpy(w.U).pin_memory()
-        Ph = torch.from_numpy(w.P).pin_memory()
-        Qh = torch.from_numpy(w.Qy).pin_memory()
-        offh = torch.empty(spec.nq + 1, dtype=torch.int64).pin_memory()
-        idsh = torch.empty(max(1 << 16, 4 * totals[-1] + 1024), dtype=torch.int32).pin_memory()
-        e2e_ms = []
-        for it in range(args.warmup + args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            idx = rmips.rmips_build_index_host(Uh, Ph, spec.k_max)
-            off, ids = rmips.rmips_query_host(idx, Qh, k, out_offsets=offh, out_ids=idsh,
-                                              capacity=idsh.numel())
-            e1.record(stream)
-            torch.cuda.synchronize()
-            idx.close()
-            if it >= args.warmup:
-                e2e_ms.append(e0.elapsed_time(e1))
-        t_e2e = sum(e2e_ms)
-        if ws > 1:
-            t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            t_e2e = float(t.item())
-        line["e2e"] = {"value": ws * units_step * args.steps / (t_e2e / 1e3), "unit": UNIT,
-                       "h2d_bytes_per_step": 4 * spec.d * (spec.n + spec.m + spec.nq),
-                       "d2h_bytes_per_step": 8 * (spec.nq + 1) + 4 * totals[-1],
-                       "ms_per_step": t_e2e / args.steps}
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(w, k, args.cpu_users or spec.n)
-    elif rank == 0 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = None
+    head = run_config(args.config, args, dev, rank, ws, args.steps, args.warmup, pusers(args.config, 5e10),
+                      e2e=not args.no_e2e, cpu=not args.no_cpu_baseline)
+    line = {"metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp16 filter (fp32 accumulate) + f64 exact decisions",
+            "data": "synthetic (SURVEY Appendix C generator, seed 0; users seed = rank); stands in for the paper's "
+                    "MF vectors (P:571-587), configs[4] is beyond the paper"}
+    for key in ("config", "build", "query", "roofline", "roofline_query", "roofline_scan", "index", "clocks",
+                "gpu_launches", "e2e", "cpu_baseline", "parity"):
+        if key in head:
+            line[key] = head[key]
+    extras = {}
+    for c in [int(x) for x in args.extra.split(",") if x.strip() != ""]:
+        if c == args.config:
+            continue
+        r = run_config(c, args, dev, rank, ws, args.extra_steps, 3, pusers(c), e2e=False, cpu=False)
+        extras["cfg%d" % c] = {kk: r[kk] for kk in ("value", "ms_per_step", "config", "build", "query", "roofline",
+                                                    "roofline_query", "clocks", "parity") if kk in r}
+        if c == 2 and args.k == 0:  # configs[2] sweeps k over {1, 5, 10, 25, 50}: the other k values
+            from synth.generator import CONFIGS
+            sweep = {}
+            for kk in CONFIGS[2].ks[:-1]:
+                r2 = run_config(c, args, dev, rank, ws, 3, 3, pusers(c), e2e=False, cpu=False, k=kk)
+                sweep["k%d" % kk] = {x: r2[x] for x in ("value", "ms_per_step", "query", "parity") if x in r2}
+            extras["cfg2"]["k_sweep"] = sweep
+    if extras:
+        line["configs"] = extras
     if rank == 0:
         print(json.dumps(line))
     if ws > 1:

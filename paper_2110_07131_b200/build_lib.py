@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "librmips.so")
 BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["abi.cu", "build.cu", "build_tc.cu", "build_tc2.cu", "build_tcq.cu", "query.cu", "query_tc.cu"]
+SOURCES = ["abi.cu", "build.cu", "build_tc.cu", "build_tcq.cu", "query.cu", "query_tc.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-DRMIPS_BUILD"]
@@ -43,8 +43,9 @@ def build(verbose: bool = False, force: bool = False, profile: bool = False, var
           defines=()) -> str:
     """profile=True builds the development-only instrumented variant librmips_prof.so
     (-DRMIPS_EPI_PROFILE, see tools/epi_profile.py); variant="x" with defines=["-DFOO"] builds the
-    development-only A/B library librmips_x.so (tools/gpu_ab.sh).  The product library is
-    librmips.so."""
+    development-only A/B library librmips_x.so (tools/gpu_ab.sh); build_dev() builds librmips_dev.so
+    with the RMIPS_DEV getenv switches (tests of kernel variants).  The product library is
+    librmips.so, with a fixed code path."""
     os.makedirs(BUILD, exist_ok=True)
     extra, tag = (["-DRMIPS_EPI_PROFILE"], "_prof") if profile else ((), "")
     if variant:
@@ -63,6 +64,12 @@ def build(verbose: bool = False, force: bool = False, profile: bool = False, var
             raise RuntimeError("link failed:\n%s\n%s" % (r.stdout, r.stderr))
         os.replace(OUT + ".tmp", OUT)
     return OUT
+
+
+def build_dev(verbose: bool = False) -> str:
+    """librmips_dev.so: the product sources with -DRMIPS_DEV (getenv switches RMIPS_SEED_TILES,
+    RMIPS_NO_CS, RMIPS_DISABLE_TC for variant tests and A/B experiments)."""
+    return build(verbose=verbose, variant="dev", defines=["-DRMIPS_DEV"])
 
 
 if __name__ == "__main__":

@@ -7,6 +7,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -20,14 +22,27 @@ namespace {
 // pool (cudaEventCreate / Destroy per mark cost several microseconds of host time between the
 // launches of a timed call).
 thread_local std::vector<cudaEvent_t> g_ev_pool;
+// Every mark also closes the previous NVTX range and opens the next phase's (names below), so an
+// Nsight timeline shows the phases of each call; NVTX costs a pointer test when no tool is attached.
 struct PhaseTimer {
   bool on = false;
   cudaStream_t st = nullptr;
   cudaEvent_t ev[8] = {};
   int n = 0;
-  PhaseTimer(bool enable, cudaStream_t s) : on(enable), st(s) {}
+  const char* const* names = nullptr;  // NVTX range opened by mark i (nullptr: none)
+  bool open = false;
+  PhaseTimer(bool enable, cudaStream_t s, const char* const* nm) : on(enable), st(s), names(nm) {}
   void mark() {
-    if (!on || n >= 8) return;
+    if (open) nvtxRangePop();
+    open = false;
+    if (names && n < 8 && names[n]) {
+      nvtxRangePushA(names[n]);
+      open = true;
+    }
+    if (!on || n >= 8) {
+      ++n;
+      return;
+    }
     if (!g_ev_pool.empty()) {
       ev[n] = g_ev_pool.back();
       g_ev_pool.pop_back();
@@ -39,15 +54,24 @@ struct PhaseTimer {
   }
   double between(int a, int b) const {
     float ms = -1.f;
-    if (!on || a >= n || b >= n || !ev[a] || !ev[b]) return -1.0;
+    if (!on || a >= n || b >= n || a >= 8 || b >= 8 || !ev[a] || !ev[b]) return -1.0;
     if (cudaEventElapsedTime(&ms, ev[a], ev[b]) != cudaSuccess) return -1.0;
     return ms;
   }
   ~PhaseTimer() {
-    for (int i = 0; i < n; ++i)
+    if (open) nvtxRangePop();
+    for (int i = 0; i < n && i < 8; ++i)
       if (ev[i]) g_ev_pool.push_back(ev[i]);
   }
 };
+const char* const kBuildPhases[] = {"rmips_build: B1-B3 prep (norms, sort, convert)",
+                                    "rmips_build: B4 contraction + candidate filter",
+                                    "rmips_build: B5-B6 exact select, fallback, blocks", nullptr, nullptr,
+                                    nullptr, nullptr, nullptr};
+const char* const kQueryPhases[] = {"rmips_query: Q1 prep", "rmips_query: Q2-Q3 Lemma 3 + filter",
+                                    "rmips_query: Q4-Q5 exact decide / scan (+ bit-matrix output)",
+                                    "rmips_query: counters readback", "rmips_query: Q6 sorted-key output",
+                                    nullptr, nullptr, nullptr};
 
 thread_local std::string g_err;
 
@@ -160,6 +184,10 @@ int fallback_grid(int64_t m) {
 // arrays, stream-ordered, with no host synchronisation.
 void extend_lists(rmips_index_s* x, int kmax_new, cudaStream_t st) {
   const int64_t n = x->n, m = x->m;
+  if (n == 0) {  // no user lists to extend: every query answers the empty set
+    x->kmax = kmax_new;
+    return;
+  }
   Arena la;
   const size_t o_tau = la.take<double>((int64_t)kmax_new * n), o_ids = la.take<int32_t>((int64_t)kmax_new * n),
                o_thr = la.take<float>((int64_t)kmax_new * n), o_tb = la.take<float>((int64_t)kmax_new * x->nblocks);
@@ -275,7 +303,7 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
   c.idx = x;
   c.mb = x->mprime;
   double* scratch = nullptr;
-  PhaseTimer tm((build_flags & RMIPS_BUILD_TIMING) != 0, st);
+  PhaseTimer tm((build_flags & RMIPS_BUILD_TIMING) != 0, st, kBuildPhases);
   try {
     // index arrays (kept) and build scratch (freed before return): two allocations
     Arena ia;
@@ -515,7 +543,7 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
     std::unique_ptr<PhaseTimer> tm;
     const long long l0 = g_launches.load();
     for (int attempt = 0; attempt < 3; ++attempt) {
-      tm.reset(new PhaseTimer((flags & RMIPS_FLAG_TIMING) != 0, st));
+      tm.reset(new PhaseTimer((flags & RMIPS_FLAG_TIMING) != 0, st, kQueryPhases));
       ensure_ws(x, c, c.nsub, cap, st);
       tm->mark();  // 0
       static_assert(2 * (kNumCounters + 4) <= 128, "zero4 region");
@@ -569,9 +597,13 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
     if (!c.bits) {
       CK(query_sort(c, reserved, 64, st));
       CK(query_output(c, offsets, user_ids, capacity, st));
+      tm->mark();  // 5
+      CK(cudaStreamSynchronize(st));
+    } else {
+      // bit-matrix output: offsets and ids were enqueued before the one synchronisation above
+      tm->mark();  // 5
+      if (tm->on) CK(cudaStreamSynchronize(st));  // (only for the phase timer's last events)
     }
-    tm->mark();  // 5
-    CK(cudaStreamSynchronize(st));
     x->phase_ms[15] = (double)(g_launches.load() - l0);
     if (tm->on) {
       x->phase_ms[8] = tm->between(0, 1);

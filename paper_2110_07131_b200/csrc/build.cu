@@ -95,8 +95,12 @@ __global__ void k_prep_users(const float* __restrict__ Q, int64_t n, int d, int 
   if (lane < kPrepRows && o0 + lane < n) {
     r_l = inv_u[o0 + lane];
     nu_l = (float)__longlong_as_double((long long)keys_u[o0 + lane]);
-    if (!(nu_l > 0.f)) nu_l = 1.f;
-    if (isinf(nu_l)) nu_l = 3.0e38f;
+    // the zero vector: nu = 1.  A norm above FLT_MAX has no fp32 nu that makes u/nu unit-norm (the
+    // precondition of the filter bound): nu = NaN makes the row's filter scores and thresholds NaN,
+    // so the build sends the row to the exact fallback (too few candidates) and every query pair
+    // of the user to the exact path (NaN never classifies)
+    if (isinf(nu_l)) nu_l = __int_as_float(0x7fc00000);
+    else if (!(nu_l > 0.f)) nu_l = 1.f;
     unu[r_l] = nu_l;
   }
   for (int j = 2 * lane; j < dpad; j += 64) {
@@ -215,7 +219,7 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
     float E = __ldg(perr + base);
     cand_chunk([&](int j) { return s[j]; }, E, (int)base, me, sm, tid, e0x2, kmax);
   }
-  cand_finish(me, sm, tid, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
+  cand_finish(me, sm, tid, e0x2, kmax, m, row, n, cand, ccount, ovf_list, ovf_count);
 }
 
 // ------------------------------------------------------------------------------ B5
@@ -365,6 +369,16 @@ __device__ __forceinline__ void sel_sort(SelKey (&key)[4], int cnt) {
 #pragma unroll
     for (int i = 0; i < E; ++i) key[i].v = sel_oval(k[i]), key[i].id = id[i];
   }
+}
+
+// Filter threshold of a finite list value: fp32(tau / nu).  When that is not a finite fp32 (|tau / nu|
+// above FLT_MAX, or nu = NaN for a user whose norm exceeds FLT_MAX) it is NaN, which the query filter
+// never rejects or accepts against (every comparison is false): the pair goes to the exact path.
+// (An infinite threshold would wrongly accept (-inf) or reject (+inf) outright.)  -inf list padding
+// (k > m) keeps -inf: fewer than k items exist, so every user is in the set.
+__device__ __forceinline__ float thr_of(double v, float nu) {
+  const float t = (float)(v / (double)nu);
+  return isfinite(t) ? t : __int_as_float(0x7fc00000);
 }
 
 // 256-bit read-only global load (LDG.256; the address is 32-byte aligned)
@@ -527,7 +541,7 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
           const bool ok = rank < cnt;
           stau[rank * kSelStride + rloc] = ok ? key[i].v : -CUDART_INF;
           sids[rank * kSelStride + rloc] = ok ? key[i].id : -1;
-          sthr[rank * kSelStride + rloc] = ok ? (float)(key[i].v / (double)nu) : -CUDART_INF_F;
+          sthr[rank * kSelStride + rloc] = ok ? thr_of(key[i].v, nu) : -CUDART_INF_F;
         }
       }
     }
@@ -596,7 +610,7 @@ k_exact_row_full(const float* __restrict__ U32, const float* __restrict__ P32, c
         bool ok = bp[0] >= 0;
         tau[(int64_t)r * n + row] = ok ? bv[0] : -CUDART_INF;
         ids[(int64_t)r * n + row] = ok ? bo[0] : -1;
-        thr[(int64_t)r * n + row] = ok ? (float)(bv[0] / (double)nu) : -CUDART_INF_F;
+        thr[(int64_t)r * n + row] = ok ? thr_of(bv[0], nu) : -CUDART_INF_F;
       }
       pv = bv[0];
       po = bo[0];
@@ -675,6 +689,8 @@ struct SortGraph {
   int32_t* vals = nullptr;   // [2 tot]: in, out
   void* tmp = nullptr;
   cudaGraphExec_t exec = nullptr;
+  cudaEvent_t done = nullptr;  // recorded after the last read of keys / vals by the previous build
+  bool used = false;           // done has been recorded at least once
   int busy = 0;  // host threads between sort_graph_get and sort_graph_put (never evicted then)
 };
 constexpr int kSortCache = 4;
@@ -690,6 +706,7 @@ struct SortSeen {
 std::vector<SortSeen> g_sort_seen;
 void sort_graph_free(SortGraph* g) {
   if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->done) cudaEventDestroy(g->done);
   cudaFree(g->keys);
   cudaFree(g->vals);
   cudaFree(g->tmp);
@@ -702,6 +719,10 @@ SortGraph* sort_graph_get(cudaStream_t st, int64_t tot) {
   for (size_t i = 0; i < g_sort.size(); ++i)
     if (g_sort[i]->st == st && g_sort[i]->tot == tot && g_sort[i]->dev == dev) {
       SortGraph* g = g_sort[i];
+      // another host thread is enqueueing on these buffers right now (same stream handle: the
+      // legacy NULL stream, or cudaStreamPerThread, which is a different stream per thread): take
+      // the direct path with this build's own scratch instead
+      if (g->busy) return nullptr;
       g_sort.erase(g_sort.begin() + i);
       g_sort.push_back(g);  // most recently used last
       ++g->busy;
@@ -724,6 +745,7 @@ SortGraph* sort_graph_get(cudaStream_t st, int64_t tot) {
                 cudaSuccess &&
             cudaMalloc(&g->keys, 2 * tot * sizeof(uint64_t)) == cudaSuccess &&
             cudaMalloc(&g->vals, 2 * tot * sizeof(int32_t)) == cudaSuccess && cudaMalloc(&g->tmp, tb) == cudaSuccess &&
+            cudaEventCreateWithFlags(&g->done, cudaEventDisableTiming) == cudaSuccess &&
             cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess &&
             cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
   if (ok) {
@@ -755,9 +777,14 @@ SortGraph* sort_graph_get(cudaStream_t st, int64_t tot) {
   g_sort.push_back(g);
   return g;
 }
-void sort_graph_put(SortGraph* g) {
+// The build's last read of the buffers (k_prep_users / k_prep_items) is enqueued on st: record
+// that point, so that the next build on the same stream HANDLE but a different stream
+// (cudaStreamPerThread from another thread) waits for it before overwriting the keys.
+void sort_graph_put(SortGraph* g, cudaStream_t st) {
   if (!g) return;
+  cudaEventRecord(g->done, st);
   std::lock_guard<std::mutex> lk(g_sort_mu);
+  g->used = true;
   --g->busy;
 }
 }  // namespace
@@ -790,6 +817,13 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
     if (e != cudaSuccess) return e;
   }
   SortGraph* sg = sort_graph_get(st, tot);  // (nullptr: the direct path below)
+  if (sg && sg->used) {
+    cudaError_t e = cudaStreamWaitEvent(st, sg->done, 0);  // the previous user is done with the buffers
+    if (e != cudaSuccess) {
+      sort_graph_put(sg, st);
+      return e;
+    }
+  }
   uint64_t* kin = sg ? sg->keys : c.nkey;
   uint64_t* kout = kin + tot;
   int32_t* vin = sg ? sg->vals : c.nval;
@@ -801,7 +835,7 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
     cudaError_t e = cudaGraphLaunch(sg->exec, st);
     count_launch(1 + kCubSortKernels);
     if (e != cudaSuccess) {
-      sort_graph_put(sg);
+      sort_graph_put(sg, st);
       return e;
     }
   } else {
@@ -820,7 +854,7 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
                                                                                x->U32, x->unu); count_launch();
   k_prep_items<<<nblk(m * 32, 256), 256, 0, st>>>(P, m, d, dpad, x->pd, x->perm_p, x->pnorm, c.maxabs, x->c1, x->c2,
                                                     x->P16, x->P32, x->perr, c.scale_dev); count_launch();
-  sort_graph_put(sg);  // last use of the sort buffers (kin) is enqueued
+  sort_graph_put(sg, st);  // last use of the sort buffers (kin) is enqueued
   return cudaGetLastError();
 }
 

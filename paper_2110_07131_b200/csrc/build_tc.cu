@@ -395,7 +395,7 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
           tc_fence_after();
         }
       }
-      cand_finish(me, sm, rloc, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
+      cand_finish(me, sm, rloc, e0x2, kmax, m, row, n, cand, ccount, ovf_list, ovf_count);
       __syncwarp();
     }
   }
@@ -456,17 +456,22 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int tiles = (int)((x->n + kBM - 1) / kBM);
   const int grid = tiles < sm_count() ? tiles : sm_count();
-  const float* cs = getenv("RMIPS_NO_CS") ? nullptr : c.scale_dev;  // dev A/B switch for the C-S exit
+  const float* cs = c.scale_dev;
   // seed pass length: 16 full tiles (8 maxima per tile, 128 slots of two), at least k_max maxima.
   // Measured (profiles/): -10% contraction on configs[1] (m = 25,000) but +15% on configs[3]
   // (m = 100,000), where the Cauchy-Schwarz exit ends a user tile after a few dozen tiles and the
   // 16 repeated tiles are a large share of the work; so no seed pass for m > 32,768.
   const int nit = (int)((c.mb + kBN - 1) / kBN);
   int seed = (nit >= 32 && nit <= 256) ? 16 : 0;
-  if (const char* e = getenv("RMIPS_SEED_TILES")) {  // dev switch: 0 .. min(32, nit - 1) seed tiles
+#ifdef RMIPS_DEV
+  // development-only A/B switches (librmips_dev.so, tools/gpu_ab.sh); the product library has a
+  // fixed code path
+  if (getenv("RMIPS_NO_CS")) cs = nullptr;  // no Cauchy-Schwarz exit
+  if (const char* e = getenv("RMIPS_SEED_TILES")) {  // 0 .. min(32, nit - 1) seed tiles
     seed = atoi(e);
     seed = seed < 0 ? 0 : seed > 32 ? 32 : seed > nit - 1 ? nit - 1 : seed;
   }
+#endif
   if (8 * seed < x->kmax) seed = 0;
   k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, x->n, c.mb, x->kmax, seed, c.cand,
                                                c.ccount, c.ovf_list, c.ovf_count, c.tiles_done);
@@ -475,19 +480,14 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
 }
 
 cudaError_t build_tc(const BuildCtx& c, cudaStream_t st) {
+#ifdef RMIPS_DEV
   if (getenv("RMIPS_DISABLE_TC")) return cudaErrorNotSupported;
-  if (getenv("RMIPS_BUILD_8W")) {
-    // experiment switch: 8 epilogue warps splitting each tile's columns, 4-byte quantised entries
-    // (build_tc2.cu); measured 35% slower than this kernel on configs[1]
-    const cudaError_t e = build_tc2(c, st);
-    if (e != cudaErrorNotSupported) return e;
-  }
+#endif
   switch (c.idx->dpad) {
     case 64: return launch_tc<1>(c, st);
     default: return build_tcq(c, st);  // d_pad 128..256: build_tcq.cu
   }
 }
-
 }  // namespace rmips
 
 #ifdef RMIPS_EPI_PROFILE

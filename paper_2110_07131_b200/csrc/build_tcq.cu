@@ -348,7 +348,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           tc_fence_after();
         }
       }
-      Pol::finish(me, sb, rr, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
+      Pol::finish(me, sb, rr, e0x2, kmax, m, row, n, cand, ccount, ovf_list, ovf_count);
       __syncwarp();
     }
   }

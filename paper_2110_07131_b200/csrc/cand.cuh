@@ -261,13 +261,16 @@ __device__ __forceinline__ void cand_chunk(ScoreFn s_of, float E, int pos0, Cand
   cand_maybe_refresh(me, sm, rloc, e0x2, kmax);
 }
 
-// Final compaction of every row of the warp, then write the candidates out.
-__device__ __forceinline__ void cand_finish(CandRow& me, CandSmem sm, int rloc, float e0x2, int kmax, int64_t row,
-                                            int64_t n, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
-                                            int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
+// Final compaction of every row of the warp, then write the candidates out.  A live row always
+// holds at least min(k_max, m) entries (see qrow_finish, candq.cuh); fewer means NaN scores (a user
+// whose norm exceeds FLT_MAX) and the row takes the exact fallback.
+__device__ __forceinline__ void cand_finish(CandRow& me, CandSmem sm, int rloc, float e0x2, int kmax, int64_t m,
+                                            int64_t row, int64_t n, int32_t* __restrict__ cand,
+                                            int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list,
+                                            int* __restrict__ ovf_count) {
   me = cand_refresh(me, sm, rloc, e0x2, kmax);
   if (row < n) {
-    if (me.ovf) {
+    if (me.ovf || (int64_t)me.cnt < (m < kmax ? m : (int64_t)kmax)) {
       ccount[row] = -1;
       int slot = atomicAdd(ovf_count, 1);
       ovf_list[slot] = (int32_t)row;

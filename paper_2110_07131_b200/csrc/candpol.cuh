@@ -1,5 +1,5 @@
-// candpol.cuh -- the 4-byte candidate-entry policy of the tensor-core build kernels (build_tc2.cu,
-// build_tcq.cu) behind a small interface:
+// candpol.cuh -- the 4-byte candidate-entry policy of the tensor-core build kernel build_tcq.cu
+// behind a small interface:
 //   QPol  candq.cuh: 12-bit quantised lower bound | 20-bit position (m <= 2^20)
 // It keeps cand.cuh's invariant: theta is a valid lower bound of the row's
 // k_max-th largest true score, an item is appended iff s~ >= theta - E, and an entry is dropped
@@ -35,9 +35,10 @@ struct QPol {
   __device__ static void maybe_refresh(Row& me, Buf sb, int rr, float e0x2, int kmax) {
     qrow_maybe_refresh(me, sb, rr, e0x2, kmax);
   }
-  __device__ static void finish(Row& me, Buf sb, int rr, float e0x2, int kmax, int64_t row, int64_t n, int32_t* cand,
+  __device__ static void finish(Row& me, Buf sb, int rr, float e0x2, int kmax, int64_t m, int64_t row, int64_t n,
+                                int32_t* cand,
                                 int32_t* ccount, int32_t* ovf_list, int* ovf_count) {
-    qrow_finish(me, sb, rr, e0x2, kmax, row, n, cand, ccount, ovf_list, ovf_count);
+    qrow_finish(me, sb, rr, e0x2, kmax, m, row, n, cand, ccount, ovf_list, ovf_count);
   }
   __device__ static int32_t pos(uint32_t e) { return (int32_t)(e & kQPosMask); }
 };

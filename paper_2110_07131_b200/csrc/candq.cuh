@@ -208,13 +208,17 @@ __device__ __forceinline__ void qrow_maybe_refresh(QRow& me, QBuf sb, int rr, fl
   if (__any_sync(0xffffffffu, me.cnt > kQSlots - 32)) me = qrow_refresh(me, sb, rr, e0x2, kmax);
 }
 
-// Final compaction, then the candidate positions (or the overflow mark) are written out.
-__device__ __forceinline__ void qrow_finish(QRow& me, QBuf sb, int rr, float e0x2, int kmax, int64_t row, int64_t n,
-                                            int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
+// Final compaction, then the candidate positions (or the overflow mark) are written out.  A live row
+// always holds at least min(k_max, m) entries (every finite score passes while theta = -inf, and a
+// refresh keeps every entry with lo >= theta, of which there are >= k_max); fewer means scores that
+// never compare (NaN: a user whose norm exceeds FLT_MAX, build.cu) and the row takes the exact
+// fallback.
+__device__ __forceinline__ void qrow_finish(QRow& me, QBuf sb, int rr, float e0x2, int kmax, int64_t m, int64_t row,
+                                            int64_t n, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
                                             int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
   me = qrow_refresh(me, sb, rr, e0x2, kmax);
   if (row < n) {
-    if (me.ovf) {
+    if (me.ovf || (int64_t)me.cnt < (m < kmax ? m : (int64_t)kmax)) {
       ccount[row] = -1;
       const int slot = atomicAdd(ovf_count, 1);
       ovf_list[slot] = (int32_t)row;

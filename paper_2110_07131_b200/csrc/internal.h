@@ -41,7 +41,6 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
 cudaError_t build_simt(const BuildCtx& c, cudaStream_t st);
 cudaError_t build_tc(const BuildCtx& c, cudaStream_t st);  // build_tc.cu; cudaErrorNotSupported if unusable
 cudaError_t build_tcq(const BuildCtx& c, cudaStream_t st);  // build_tcq.cu (d_pad 128..256)
-cudaError_t build_tc2(const BuildCtx& c, cudaStream_t st);  // build_tc2.cu (d_pad 64, m <= 2^20)
 cudaError_t build_select(BuildCtx& c, cudaStream_t st);
 cudaError_t build_fallback(BuildCtx& c, int nrows, double* scratch, int grid, cudaStream_t st);
 cudaError_t build_blocks(BuildCtx& c, cudaStream_t st);

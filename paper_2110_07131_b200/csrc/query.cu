@@ -570,9 +570,11 @@ cudaError_t query_sort(QueryCtx& c, int64_t total, int end_bit, cudaStream_t st)
     uint32_t* kout = kin + total;
     k_pack32<<<nblk(total, 256), 256, 0, st>>>(c.acc, total, (uint32_t)c.idx->n, kin);
     count_launch();
+    // real keys are < span; the sentinel 0xffffffff must sort after them on the low `bits` bits,
+    // so 2^bits > span (a power-of-two span would otherwise tie its largest key with the sentinel)
     const uint64_t span = (uint64_t)c.b * (uint64_t)c.idx->n;
     int bits = 1;
-    while (bits < 32 && (1ull << bits) < span) ++bits;
+    while (bits < 32 && (1ull << bits) <= span) ++bits;
     count_launch(kCubSortKernels);
     return cub::DeviceRadixSort::SortKeys(c.cub_tmp, tb, kin, kout, (int)total, 0, bits, st);
   }

@@ -528,7 +528,9 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
 }
 
 cudaError_t query_filter_tc(QueryCtx& c, cudaStream_t st) {
+#ifdef RMIPS_DEV
   if (getenv("RMIPS_DISABLE_TC")) return cudaErrorNotSupported;
+#endif
   if (c.idx->n == 0) return cudaSuccess;
   switch (c.idx->dpad) {
     case 64: return launch_query_tc<1>(c, st);
