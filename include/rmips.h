@@ -45,7 +45,7 @@ typedef struct rmips_index_s* rmips_index_t; /* opaque; immutable after build */
 
 typedef enum {
   RMIPS_OK = 0,
-  RMIPS_ERR_INVALID = 1,   /* null pointer, n < 0, m < 1, d < 1, b < 0, bad flags */
+  RMIPS_ERR_INVALID = 1,   /* null pointer, n < 0, m < 1, d < 1 or d > 1024, b < 0, bad flags */
   RMIPS_ERR_NONFINITE = 2, /* a NaN/Inf in Q, P or a query vector */
   RMIPS_ERR_K_RANGE = 3,   /* k < 1, k_max < 1, or k > k_max with RMIPS_FLAG_NO_EXTEND */
   RMIPS_ERR_CAPACITY = 4,  /* result ids exceed `capacity`; *total_out and offsets hold the needed size */
@@ -98,9 +98,17 @@ typedef struct {
  *   Q       device, n x d fp32 user vectors (may be NULL iff n == 0)
  *   n       number of users, >= 0
  *   P       device, m x d fp32 item vectors
- *   m       number of items, >= 1
- *   d       dimensionality, >= 1
- *   k_max   largest k the index answers, >= 1 (lists are padded with -inf when k_max > m)
+ *   m       number of items, 1 <= m < 2^31 (m > 2^20 with d > 64 uses 8-byte candidate entries, slower)
+ *   d       dimensionality, 1 <= d <= 1024 (the tensor-core kernels cover every d in that range: K blocks
+ *           of 64 columns, the last one trimmed to 16/32/64 columns; for d > 256 the build and query
+ *           K loops stream the user and query K blocks from L2 instead of keeping them on chip;
+ *           RMIPS_BUILD_SIMT covers d <= 256 only)
+ *   k_max   largest k the index answers, >= 1 (lists are padded with -inf when k_max > m).  The
+ *           build's candidate filter keeps 128 slots per user row for k_max <= 80 and 256 slots above
+ *           (when m <= 2^20); a row whose list cannot be compacted into its slots (k_max above ~90 with
+ *           m > 2^20 or with RMIPS_BUILD_SIMT, k_max above ~220 otherwise, or massive ties) is
+ *           recomputed exactly by a fallback kernel that costs O(k_max m d) per row: correct, slow
+ *           (overflow rows are reported by rmips_index_info)
  *   out     receives the new index handle (NULL on failure)
  * The library copies what it needs; Q and P may be freed after the call returns.
  * Errors: INVALID, NONFINITE, K_RANGE (k_max < 1), OOM, CUDA. */
@@ -162,8 +170,10 @@ RMIPS_API rmips_status_t rmips_query_stats(rmips_index_t idx, rmips_stats_t* out
  *                candidates kept by the build filter (sum over rows),
  *                (128-user tile, item tile) contractions issued by the tensor-core build (0 for the
  *                SIMT build; fewer than all when the Cauchy-Schwarz early exit fired),
- *                m_prime (items the lists are built over; = m for the exact index);
- *                info[11..15] reserved, 0
+ *                m_prime (items the lists are built over; = m for the exact index),
+ *                build kernel (0 SIMT, 1 k_build_tc (d <= 64), 2 k_build_tcq with the user tile in
+ *                tensor memory, 3 k_build_tcq with streamed user K blocks (d > 256)),
+ *                candidate slots per row (128 or 256);  info[13..15] reserved, 0
  *   perm_u[n], perm_p[m]: sorted position -> original id (norm descending, ties by id)
  *   tau[k_max * n] fp64 and ids[k_max * n] int32: column-major by rank, users in ORIGINAL
  *   order: tau[j * n + u] = (j+1)-th largest u.p over P (over P' for a P' index), ids = its

@@ -196,9 +196,10 @@ void extend_lists(rmips_index_s* x, int kmax_new, cudaStream_t st) {
   BuildCtx c;
   c.idx = x;
   c.mb = x->mprime;
+  c.cstride = build_cand_stride(kmax_new, c.mb, x->build_flags);
   const int fb_grid = fallback_grid(m);
   Arena sa;
-  const size_t o_sc = sa.take<float>(4), o_cand = sa.take<int32_t>(n * kCand), o_cc = sa.take<int32_t>(n),
+  const size_t o_sc = sa.take<float>(4), o_cand = sa.take<int32_t>(n * c.cstride), o_cc = sa.take<int32_t>(n),
                o_ovl = sa.take<int32_t>(n), o_ovc = sa.take<int>(1), o_ct = sa.take<unsigned long long>(2),
                o_scr = sa.take<double>((int64_t)fb_grid * m);
   void* sarena = nullptr;
@@ -238,6 +239,7 @@ void extend_lists(rmips_index_s* x, int kmax_new, cudaStream_t st) {
     if (!(x->build_flags & RMIPS_BUILD_SIMT)) e = build_tc(c, st);
     if (e == cudaErrorNotSupported) {
       cudaGetLastError();
+      c.cstride = kCand;  // the SIMT build's lists (cand.cuh)
       e = build_simt(c, st);
     }
     CK(e);
@@ -284,7 +286,9 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
   if (m_prime < 1) return fail(RMIPS_ERR_INVALID, "m_prime < 1");
   *out = nullptr;
   if (n < 0 || m < 1 || d < 1) return fail(RMIPS_ERR_INVALID, "need n >= 0, m >= 1, d >= 1");
-  if (d > 256) return fail(RMIPS_ERR_INVALID, "d > 256 is not supported");
+  if (d > kMaxDim) return fail(RMIPS_ERR_INVALID, "d > 1024 is not supported");
+  if (d > 256 && (build_flags & RMIPS_BUILD_SIMT))
+    return fail(RMIPS_ERR_INVALID, "the SIMT (CUDA-core) build covers d <= 256; the tensor-core build any d");
   if (n >= (int64_t)1 << 31 || m >= (int64_t)1 << 31) return fail(RMIPS_ERR_INVALID, "n, m must be < 2^31");
   if ((n > 0 && !Q) || !P) return fail(RMIPS_ERR_INVALID, "NULL input matrix");
   if (k_max < 1) return fail(RMIPS_ERR_K_RANGE, "k_max < 1");
@@ -338,7 +342,8 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
     const int fb_grid = fallback_grid(m);
     const size_t o_key = sa.take<uint64_t>(2 * (m + n)), o_val = sa.take<int32_t>(2 * (m + n)), o_inv = sa.take<int32_t>(n),
                  o_max = sa.take<unsigned int>(4), o_cub = sa.take<unsigned char>((int64_t)c.cub_bytes),
-                 o_cand = sa.take<int32_t>(n * kCand), o_cc = sa.take<int32_t>(n), o_ovl = sa.take<int32_t>(n),
+                 o_cand = sa.take<int32_t>(n * build_cand_stride(k_max, x->mprime, build_flags)),
+                 o_cc = sa.take<int32_t>(n), o_ovl = sa.take<int32_t>(n),
                  o_ovc = sa.take<int>(1), o_ct = sa.take<unsigned long long>(2),
                  o_scr = sa.take<double>((int64_t)fb_grid * m);
     void* sarena = nullptr;
@@ -351,6 +356,7 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
     c.scale_dev = reinterpret_cast<float*>(c.maxabs + 2);
     c.cub_tmp = S + o_cub;
     c.cand = reinterpret_cast<int32_t*>(S + o_cand);
+    c.cstride = build_cand_stride(k_max, x->mprime, build_flags);
     c.ccount = reinterpret_cast<int32_t*>(S + o_cc);
     c.ovf_list = reinterpret_cast<int32_t*>(S + o_ovl);
     c.ovf_count = reinterpret_cast<int*>(S + o_ovc);
@@ -370,6 +376,7 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
       if (e == cudaErrorNotSupported) {
         cudaGetLastError();
         x->build_flags |= RMIPS_BUILD_SIMT;
+        c.cstride = kCand;  // the SIMT build's lists (cand.cuh)
         e = build_simt(c, st);
       }
       CK(e);
@@ -512,6 +519,8 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
   if (capacity > 0 && !user_ids) return fail(RMIPS_ERR_INVALID, "NULL user_ids with capacity > 0");
   if (k < 1) return fail(RMIPS_ERR_K_RANGE, "k < 1");
   if (k > idx->kmax && (flags & RMIPS_FLAG_NO_EXTEND)) return fail(RMIPS_ERR_K_RANGE, "k > k_max");
+  if ((flags & RMIPS_FLAG_SIMT) && idx->d > 256)
+    return fail(RMIPS_ERR_INVALID, "the SIMT (CUDA-core) query filter covers d <= 256; the tensor-core filter any d");
   if (flags & ~(RMIPS_FLAG_NO_EXTEND | RMIPS_FLAG_NO_BLOCKS | RMIPS_FLAG_VERIFY_SCAN | RMIPS_FLAG_FORCE_VERIFY | RMIPS_FLAG_SIMT | RMIPS_FLAG_TIMING |
                 RMIPS_FLAG_KEY_SORT))
     return fail(RMIPS_ERR_INVALID, "unknown flag bits");
@@ -674,6 +683,8 @@ rmips_status_t rmips_index_info(rmips_index_t idx, int64_t info[16]) {
   info[8] = idx->cand_total;
   info[9] = idx->tiles_done;
   info[10] = idx->mprime;
+  info[11] = idx->build_kernel;
+  info[12] = idx->cand_slots;
   info[0] = idx->n; info[1] = idx->m; info[2] = idx->d; info[3] = idx->kmax;
   info[4] = idx->dpad; info[5] = kTileU; info[6] = idx->overflow_rows; info[7] = idx->build_flags;
   return RMIPS_OK;

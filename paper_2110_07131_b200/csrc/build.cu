@@ -26,7 +26,7 @@ namespace rmips {
 constexpr int kNormRows = 128;
 __global__ void __launch_bounds__(kNormRows)
 k_norms(const float* __restrict__ X, int64_t rows, int d, uint64_t* __restrict__ keys,
-        uint64_t topbit, int* __restrict__ flags, unsigned int* __restrict__ maxabs_bits) {
+        uint64_t topbit, int* __restrict__ flags, unsigned int* __restrict__ maxabs_bits, bool staged) {
   extern __shared__ float xs[];
   const int ds = d | 1;
   const int64_t r0 = blockIdx.x * (int64_t)kNormRows;
@@ -38,12 +38,15 @@ k_norms(const float* __restrict__ X, int64_t rows, int d, uint64_t* __restrict__
     const float v = src[e];
     fin &= isfinite(v);
     mx = fmaxf(mx, fabsf(v));
-    const int rr = e / d;
-    xs[rr * ds + (e - rr * d)] = v;
+    if (staged) {
+      const int rr = e / d;
+      xs[rr * ds + (e - rr * d)] = v;
+    }
   }
   __syncthreads();
   if (threadIdx.x < nr) {
-    const float* x = xs + threadIdx.x * ds;
+    // (d > 400: the 128 rows do not fit in shared memory; each thread re-reads its row, L2-resident)
+    const float* x = staged ? xs + threadIdx.x * ds : src + (int64_t)threadIdx.x * d;
     double s = 0.0;
     for (int j = 0; j < d; ++j) s = __fma_rn((double)x[j], (double)x[j], s);
     keys[r0 + threadIdx.x] = (uint64_t)__double_as_longlong(sqrt(s)) | topbit;
@@ -219,7 +222,7 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
     float E = __ldg(perr + base);
     cand_chunk([&](int j) { return s[j]; }, E, (int)base, me, sm, tid, e0x2, kmax);
   }
-  cand_finish(me, sm, tid, e0x2, kmax, m, row, n, cand, ccount, ovf_list, ovf_count);
+  cand_finish(me, sm, tid, e0x2, kmax, m, row, n, cand, kCand, ccount, ovf_list, ovf_count);
 }
 
 // ------------------------------------------------------------------------------ B5
@@ -339,8 +342,8 @@ __device__ __forceinline__ void warp_bitonic_u64(uint64_t (&key)[E], int (&id)[E
 
 // Sort the first E*32 keys of key[] best first: the integer fast path, then (only when two real
 // keys share a value) the two-field comparator from the unsorted copy.
-template <int E>
-__device__ __forceinline__ void sel_sort(SelKey (&key)[4], int cnt) {
+template <int E, int NK>
+__device__ __forceinline__ void sel_sort(SelKey (&key)[NK], int cnt) {
   const int lane = threadIdx.x & 31;
   uint64_t k[E];
   int id[E];
@@ -404,11 +407,9 @@ constexpr int kSelStride = kSelRows + 1;  // odd stage stride: a warp's 32 ranks
 // [rank][row] and written per rank as one contiguous run of the block's rows: the column-major
 // tables (tau, ids, thr: rank-major, users contiguous) then take full sectors instead of one
 // 4- or 8-byte piece of a sector per (row, rank).
-#ifdef RMIPS_SEL_MINB
-__global__ void __launch_bounds__(32 * kSelWarps, RMIPS_SEL_MINB)
-#else
+// MAXC = candidate slots per row (the build's cstride: 128, or 256 for k_max > 80).
+template <int MAXC>
 __global__ void __launch_bounds__(32 * kSelWarps)
-#endif
 k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, const int32_t* __restrict__ perm_p,
                const float* __restrict__ unu, const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount,
                int64_t n, int d, int pd, int kmax, double* __restrict__ tau, int32_t* __restrict__ ids,
@@ -416,7 +417,8 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
   // shared: per warp the user row [pd] (fp64, zero-padded); the block's staged lists
   extern __shared__ __align__(16) double ssel[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int kc = kmax < kCand ? kmax : kCand;  // ranks staged (beyond kCand: -inf, only when m < k_max)
+  constexpr int NK = MAXC / 32;                  // candidate keys per lane
+  const int kc = kmax < MAXC ? kmax : MAXC;      // ranks staged (beyond MAXC: -inf, only when m < k_max)
   double* urow = ssel + (size_t)w * pd;
   double* stau = ssel + (size_t)kSelWarps * pd;                    // [kc][kSelStride]
   int32_t* sids = reinterpret_cast<int32_t*>(stau + (size_t)kc * kSelStride);
@@ -436,8 +438,8 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
     cnt_n = -1;
     if (r < n) {
       cnt_n = ccount[r];
-      pn0 = cand[r * kCand + lane];
-      pn1 = cand[r * kCand + 32 + lane];
+      pn0 = cand[r * MAXC + lane];
+      pn1 = cand[r * MAXC + 32 + lane];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int t = lane + 32 * i;
@@ -469,19 +471,20 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
         const int t = lane + 32 * i;
         if (t < pd) urow[t] = (double)uc[i];  // zero padding for d <= t < pd
       }
+      for (int t = 256 + lane; t < pd; t += 32) urow[t] = t < d ? (double)U32[row * d + t] : 0.0;  // d > 256
       __syncwarp();
-      SelKey key[4];
+      SelKey key[NK];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) key[i].v = -CUDART_INF, key[i].id = 0x7fffffff;
+      for (int i = 0; i < NK; ++i) key[i].v = -CUDART_INF, key[i].id = 0x7fffffff;
       // candidates c and c + 32 of a lane as two interleaved chains (twice the loads in flight)
 #pragma unroll
-      for (int i = 0; i < 4; i += 2) {
+      for (int i = 0; i < NK; i += 2) {
         if (32 * i >= cnt) break;  // warp-uniform
         const int c0 = 32 * i + lane, c1 = c0 + 32;
         const bool l0 = c0 < cnt, l1 = c1 < cnt;
         int pos0 = 0, pos1 = 0;  // inactive lanes read item row 0 and discard it
-        if (l0) pos0 = i == 0 ? pc0 : cand[row * kCand + c0];
-        if (l1) pos1 = i == 0 ? pc1 : cand[row * kCand + c1];
+        if (l0) pos0 = i == 0 ? pc0 : cand[row * MAXC + c0];
+        if (l1) pos1 = i == 0 ? pc1 : cand[row * MAXC + c1];
         const float* pr0 = P32 + (int64_t)pos0 * pd;  // pd = round_up(d, 8): 32-byte rows
         const float* pr1 = P32 + (int64_t)pos1 * pd;
         double s0 = 0.0, s1 = 0.0;  // dot64: left-to-right fp64 sums of exact fp32 x fp32 products
@@ -527,15 +530,17 @@ k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, con
         if (l1) key[i + 1].v = s1, key[i + 1].id = perm_p[pos1];
       }
       if (cnt <= 32) {  // one key per lane: 15 compare-exchange steps instead of 21 (64) or 28 (128)
-        sel_sort<1>(key, cnt);
+        sel_sort<1, NK>(key, cnt);
       } else if (cnt <= 64) {
-        sel_sort<2>(key, cnt);
+        sel_sort<2, NK>(key, cnt);
+      } else if (NK == 4 || cnt <= 128) {
+        sel_sort<4, NK>(key, cnt);
       } else {
-        sel_sort<4>(key, cnt);
+        sel_sort<(NK > 4 ? NK : 4), NK>(key, cnt);
       }
       const float nu = unu[row];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < NK; ++i) {
         const int rank = i * 32 + lane;
         if (rank < kc) {
           const bool ok = rank < cnt;
@@ -665,6 +670,8 @@ static cudaError_t launch_build_simt(const BuildCtx& c, cudaStream_t st) {
 }
 
 cudaError_t build_simt(const BuildCtx& c, cudaStream_t st) {
+  c.idx->build_kernel = 0;
+  c.idx->cand_slots = kCand;
   switch (c.idx->dpad) {
     case 64: return launch_build_simt<64>(c, st);
     case 128: return launch_build_simt<128>(c, st);
@@ -811,7 +818,8 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
   // B1: norms as sort keys of one concatenated [items | users] sequence (items carry the top
   // bit, so a descending sort puts them first); non-finite check; max |p_j|
   const int64_t tot = m + n;
-  const size_t nsm = (size_t)kNormRows * (d | 1) * sizeof(float);
+  const bool staged = (size_t)kNormRows * (d | 1) * sizeof(float) <= 200 * 1024;
+  const size_t nsm = staged ? (size_t)kNormRows * (d | 1) * sizeof(float) : 0;
   if (nsm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_norms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nsm);
     if (e != cudaSuccess) return e;
@@ -828,8 +836,8 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
   uint64_t* kout = kin + tot;
   int32_t* vin = sg ? sg->vals : c.nval;
   int32_t* vout = vin + tot;
-  k_norms<<<nblk(m, kNormRows), kNormRows, nsm, st>>>(P, m, d, kin, 1ull << 63, x->d_flags, c.maxabs); count_launch();
-  if (n) k_norms<<<nblk(n, kNormRows), kNormRows, nsm, st>>>(Q, n, d, kin + m, 0ull, x->d_flags, nullptr); count_launch();
+  k_norms<<<nblk(m, kNormRows), kNormRows, nsm, st>>>(P, m, d, kin, 1ull << 63, x->d_flags, c.maxabs, staged); count_launch();
+  if (n) k_norms<<<nblk(n, kNormRows), kNormRows, nsm, st>>>(Q, n, d, kin + m, 0ull, x->d_flags, nullptr, staged); count_launch();
   // B2: one stable radix sort (descending norm, ties by ascending index: reading R6)
   if (sg) {
     cudaError_t e = cudaGraphLaunch(sg->exec, st);
@@ -865,23 +873,28 @@ size_t build_cub_bytes(int64_t n, int64_t m) {
   return a;
 }
 
-cudaError_t build_select(BuildCtx& c, cudaStream_t st) {
+template <int MAXC>
+static cudaError_t launch_select(BuildCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
-  if (x->n == 0) return cudaSuccess;
-  const int kc = x->kmax < kCand ? x->kmax : kCand;
+  const int kc = x->kmax < MAXC ? x->kmax : MAXC;
   const size_t smem = (size_t)kSelWarps * x->pd * sizeof(double) + (size_t)kc * kSelStride * (8 + 4 + 4);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_exact_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_exact_select<MAXC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->device);
   const int64_t want = (x->n + kSelRows - 1) / kSelRows;
   const int grid = (int)(want < (int64_t)sms * 8 ? want : (int64_t)sms * 8);
-  k_exact_select<<<grid, 32 * kSelWarps, smem, st>>>(x->U32, x->P32, x->perm_p, x->unu, c.cand, c.ccount, x->n,
-                                                     x->d, x->pd, x->kmax, x->tau, x->ids, x->thr, c.cand_total);
+  k_exact_select<MAXC><<<grid, 32 * kSelWarps, smem, st>>>(x->U32, x->P32, x->perm_p, x->unu, c.cand, c.ccount, x->n,
+                                                           x->d, x->pd, x->kmax, x->tau, x->ids, x->thr, c.cand_total);
   count_launch();
   return cudaGetLastError();
+}
+
+cudaError_t build_select(BuildCtx& c, cudaStream_t st) {
+  if (c.idx->n == 0) return cudaSuccess;
+  return c.cstride == 256 ? launch_select<256>(c, st) : launch_select<kCand>(c, st);
 }
 
 cudaError_t build_fallback(BuildCtx& c, int nrows, double* scratch, int grid, cudaStream_t st) {

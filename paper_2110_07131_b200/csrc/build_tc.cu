@@ -395,7 +395,7 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
           tc_fence_after();
         }
       }
-      cand_finish(me, sm, rloc, e0x2, kmax, m, row, n, cand, ccount, ovf_list, ovf_count);
+      cand_finish(me, sm, rloc, e0x2, kmax, m, row, n, cand, kCand, ccount, ovf_list, ovf_count);
       __syncwarp();
     }
   }
@@ -422,17 +422,28 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }  // namespace
 
 // 2-D fp16 tensor [rows][cols] (cols contiguous), box = box_rows rows x 64 columns, SWIZZLE_128B.
-bool make_tmap_f16_box(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+bool make_tmap_f16_box(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                       uint32_t box_cols) {
   auto fn = encode_fn();
   if (!fn) return false;
+  if (box_cols != 16 && box_cols != 32 && box_cols != 64) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
+  // the swizzle span equals the box row (32, 64 or 128 bytes): sdesc_swz (sm100.cuh) describes it
+  const CUtensorMapSwizzle swz = box_cols == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                  : CU_TENSOR_MAP_SWIZZLE_128B;
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+int tail_cols(int d) {
+  const int used = 16 * ((d + 15) / 16) - 64 * ((d - 1) / 64);  // columns of the last K block that hold data
+  return used <= 16 ? 16 : used <= 32 ? 32 : 64;
 }
 
 static int sm_count() {
@@ -473,6 +484,8 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   }
 #endif
   if (8 * seed < x->kmax) seed = 0;
+  x->build_kernel = 1;
+  x->cand_slots = kCand;
   k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, x->n, c.mb, x->kmax, seed, c.cand,
                                                c.ccount, c.ovf_list, c.ovf_count, c.tiles_done);
   count_launch();
@@ -483,10 +496,10 @@ cudaError_t build_tc(const BuildCtx& c, cudaStream_t st) {
 #ifdef RMIPS_DEV
   if (getenv("RMIPS_DISABLE_TC")) return cudaErrorNotSupported;
 #endif
-  switch (c.idx->dpad) {
-    case 64: return launch_tc<1>(c, st);
-    default: return build_tcq(c, st);  // d_pad 128..256: build_tcq.cu
-  }
+  // d <= 64 with 128-slot lists: this kernel; everything else (d > 64, or k_max > 80 with 256-slot
+  // 4-byte lists): build_tcq.cu
+  if (c.idx->dpad == 64 && c.cstride == kCand) return launch_tc<1>(c, st);
+  return build_tcq(c, st);
 }
 }  // namespace rmips
 

@@ -1,22 +1,26 @@
-// build_tcq.cu -- B4 on the 5th-generation tensor cores for d_pad = 128..256 (build_tc.cu has the
-// d <= 64 kernel): the |Q| x |P| x d contraction of Alg. 1 lines 7-9 (over ALL of P per
-// BASELINE north star) fused with the per-row top-k_max candidate epilogue (candq.cuh: 4-byte
-// quantised entries), so the score matrix never reaches HBM.
+// build_tcq.cu -- B4 on the 5th-generation tensor cores for any d (build_tc.cu has the faster d <= 64
+// kernel for k_max <= 80): the |Q| x |P| x d contraction of Alg. 1 lines 7-9 (over ALL of
+// P per BASELINE north star) fused with the per-row top-k_max candidate epilogue (candpol.cuh), so the
+// score matrix never reaches HBM.
 //
-// k_build_tcq<KB, Pol>: K = 64*KB (d_pad), 128-user tiles, 128-item tiles.  One persistent CTA per
-// SM; per user tile:
-//   warp 0      TMA producer: one ring of 16 KB K-block units; each user tile's sequence is its A tile
-//               (128 x 64*KB fp16, KB units) followed by the item tiles B (KB units each), SWIZZLE_128B
-//   warp 1      MMA warp (all lanes run the loop, one elected lane issues): the A units are copied
-//               into TENSOR memory with tcgen05.cp (8 columns per K step, in issue order after the
-//               previous tile's MMAs) and their ring slots released; every item tile is then one
-//               tcgen05.mma.cta_group::1.kind::f16 chain, M = N = 128, K = 16 x ksteps, with A read
-//               from TMEM and only B from shared memory (an N = 64 MMA that also re-read A from
-//               shared memory needs 192 B/clk at the tensor peak, above the SM's 128 B/clk)
-//   warps 2-5   epilogue: warp w reads TMEM lane quadrant w % 4; every thread owns one user row
-//               and filters its 128 scores per item tile (3-input max trees, one compare per
-//               32-column chunk), with one out-of-line slow path that re-reads flagged chunks.
-// TMEM: NACC = 3 accumulator stages of 128 columns, then the A tile (32 KB columns).
+// k_build_tcq<KB, Pol>: K = 64*KB columns (d_pad), 128-user tiles, 128-item tiles.  One persistent CTA
+// per SM; per user tile:
+//   warp 0      TMA producer: one ring of 16 KB K-block units (128 rows x 64 fp16, SWIZZLE_128B); the
+//               last K block of a row is trimmed to the columns that hold data (a 16-, 32- or 64-column
+//               box, tail_cols(d): d = 200 streams 416 instead of 512 bytes per row)
+//   warp 1      MMA warp (all lanes run the loop, one elected lane issues):
+//                 KB = 1..4  the user tile A is copied into TENSOR memory with tcgen05.cp (8 columns per
+//                            K step, in issue order after the previous tile's MMAs); every item tile is
+//                            then one tcgen05.mma.cta_group::1.kind::f16 chain, M = N = 128,
+//                            K = 16 x ksteps, A from TMEM, only B from shared memory (an MMA that also
+//                            re-read A from shared memory needs more than the SM's 128 B/clk)
+//                 KB = 0     d_pad > 256 (A does not fit next to the accumulators): the K loop streams
+//                            the user tile's K blocks next to the item tile's (A and B from shared
+//                            memory; A re-read from L2 per item tile), kbn = d_pad / 64 at run time
+//   warps 2-5   epilogue: warp w reads TMEM lane quadrant w % 4; every thread owns one user row and
+//               filters its 128 scores per item tile (3-input max trees, one compare per 32-column
+//               chunk), with one out-of-line slow path that re-reads flagged chunks.
+// Pol: the candidate entries (candpol.cuh): 4-byte quantised (m <= 2^20; 128 or 256 slots) or 8-byte.
 // Early termination (Cauchy-Schwarz on the norm-sorted items) as in build_tc.cu.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -35,25 +39,25 @@ extern __device__ unsigned long long g_epi_prof[4][256];  // build_tc.cu
 namespace {
 
 constexpr int kBM = 128;                 // users per tile (TMEM lanes)
-constexpr int kUTile = kBM * 64 * 2;     // one 128 x 64 fp16 tile = 16 KB
+constexpr int kUTile = kBM * 64 * 2;     // one 128 x 64 fp16 K-block unit = 16 KB
 
-template <int KB>
+template <int KB, class Pol>
 struct Cfg {
-  static constexpr int BN = 128;                              // items per tile (= kBM: A and B tiles alike)
-  // the ring holds K-block units (128 rows x 64 fp16 = 16 KB): a tile (A or B) is KB consecutive
-  // units, and the MMA on K block kb starts as soon as that unit has landed
-  static constexpr int NST = 10;
+  static constexpr int BN = 128;                              // items per tile (= kBM: A and B units alike)
+  // ring of K-block units: every unit the shared memory left next to the candidate buffers holds
+  static constexpr int NST_FIT = (232448 - 2048 - Pol::kBufBytes) / kUTile;
+  static constexpr int NST = NST_FIT < 10 ? NST_FIT : 10;
   static constexpr int ACC_COLS = BN;                         // TMEM columns per accumulator stage
-  static constexpr int NACC = 3;
-  static constexpr int A_TMEM = NACC * ACC_COLS;              // column of the A tile in TMEM
+  static constexpr int NACC = KB == 0 ? 4 : 3;
+  static constexpr int A_TMEM = NACC * ACC_COLS;              // column of the A tile in TMEM (KB > 0)
   static constexpr int TMEM_COLS = 512;
-  static_assert(A_TMEM + 32 * KB <= TMEM_COLS, "tensor memory");
+  static_assert(KB == 0 || A_TMEM + 32 * KB <= TMEM_COLS, "tensor memory");
   static constexpr int THREADS = 192;
   static constexpr int RING = 0;
   static constexpr int CAND = RING + NST * kUTile;
-  static constexpr int BAR = CAND + kBM * 128 * 4;  // 128 four-byte candidate slots per row
+  static constexpr int BAR = CAND + Pol::kBufBytes;
   static constexpr int TOTAL = BAR + 512 + 1024;    // barriers + control words, alignment slack
-  static_assert(TOTAL <= 232448, "shared memory");
+  static_assert(NST >= 6 && TOTAL <= 232448, "shared memory");
 };
 
 // Fast path of one 64-column half (scores of this thread's row): 3-input max trees and one
@@ -74,8 +78,8 @@ __device__ __forceinline__ uint32_t epiq_fast(const uint32_t (&h)[64], float E0,
 // re-read each flagged chunk of the current accumulator stage from TMEM, append and refresh.
 template <class Pol>
 __device__ __noinline__ typename Pol::Row epiq_slow(uint32_t bits, uint32_t taddr, int base0, int mi, float4 E4,
-                                                    typename Pol::Row me, typename Pol::Buf sb,
-                                      int rr, float e0x2, int kmax) {
+                                                    typename Pol::Row me, typename Pol::Buf sb, int rr, float e0x2,
+                                                    int kmax) {
 #pragma unroll 1
   while (bits) {
     const int c = __ffs(bits) - 1;
@@ -118,22 +122,27 @@ __device__ __noinline__ typename Pol::Row epiq_slow(uint32_t bits, uint32_t tadd
 
 }  // namespace
 
+// tmA / tmB: 64-column boxes; tmAt / tmBt: the last K block's tail box (tail columns, tail_cols(d)).
 template <int KB, class Pol>
-__global__ void __launch_bounds__(Cfg<KB>::THREADS, 1)
-k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
-           int64_t n, int64_t m, int kmax, int ksteps, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
-           int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count, unsigned long long* __restrict__ tiles_done) {
+__global__ void __launch_bounds__(Cfg<KB, Pol>::THREADS, 1)
+k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAt,
+            const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBt,
+            const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
+            int64_t n, int64_t m, int kmax, int ksteps, int kb_rt, int tail, int32_t* __restrict__ cand,
+            int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count,
+            unsigned long long* __restrict__ tiles_done) {
   using namespace sm100;
-  using C = Cfg<KB>;
+  using C = Cfg<KB, Pol>;
   constexpr int NST = C::NST, NACC = C::NACC, BN = C::BN;
+  constexpr bool kStreamA = KB == 0;
+  const int kbn = kStreamA ? kb_rt : KB;          // K blocks per row
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base, derived from smem_raw by pointer arithmetic so that the compiler
   // keeps the shared state space (LDS/STS rather than generic loads/stores)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t sR = sbase + C::RING;
-  const typename Pol::Buf sb{reinterpret_cast<uint32_t*>(smem + C::CAND), kBM};
+  const typename Pol::Buf sb = Pol::buf(smem + C::CAND);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR);
   const uint32_t bar0 = smem_u32(bars);
   auto BAR = [&](int i) { return bar0 + 8u * i; };
@@ -148,10 +157,13 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_utiles = (int)((n + kBM - 1) / kBM);
   const int nit = (int)((m + BN - 1) / BN);
+  const uint32_t tail_bytes = (uint32_t)(kBM * tail * 2);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    tma_prefetch(&tmAt);
+    tma_prefetch(&tmBt);
     for (int s = 0; s < NST; ++s) mbar_init(BAR(R_FULL + s), 1), mbar_init(BAR(R_EMPTY + s), 1);
     for (int a = 0; a < NACC; ++a) mbar_init(BAR(ACC_FULL + a), 1), mbar_init(BAR(ACC_EMPTY + a), 4);
     *done_cum = 0;
@@ -174,55 +186,65 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       int stage = 0;
       uint32_t ph = 0;
       int t = 0;
+      // one K-block unit (rows r0.., K block kb) of map m / tail map mt into the next ring slot
+      auto load_unit = [&](const CUtensorMap* mfull, const CUtensorMap* mtail, int kb, int r0) {
+        const bool last = kb == kbn - 1;
+        mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
+        mbar_arrive_expect_tx(BAR(R_FULL + stage), last ? tail_bytes : (uint32_t)kUTile);
+        tma_load_2d(sR + stage * kUTile, last ? mtail : mfull, kb * 64, r0, BAR(R_FULL + stage));
+        if (++stage == NST) stage = 0, ph ^= 1;
+      };
       for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
-        for (int kb = 0; kb < KB; ++kb) {  // the user tile A
-          mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
-          mbar_arrive_expect_tx(BAR(R_FULL + stage), kUTile);
-          tma_load_2d(sR + stage * kUTile, &tmA, kb * 64, ut * kBM, BAR(R_FULL + stage));
-          if (++stage == NST) stage = 0, ph ^= 1;
-        }
+        if (!kStreamA)
+          for (int kb = 0; kb < kbn; ++kb) load_unit(&tmA, &tmAt, kb, ut * kBM);  // the user tile A
         for (int it = 0; it < nit; ++it) {
-          bool ended = false;
-          for (int kb = 0; kb < KB; ++kb) {
-            mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
-            if (kb == 0 && *done_cum >= 4 * (t + 1)) {  // every epilogue warp is done with this user tile
-              stage_end[stage] = t + 1;
-              mbar_arrive(BAR(R_FULL + stage));  // release: the marker is visible to the MMA warp
-              if (++stage == NST) stage = 0, ph ^= 1;
-              ended = true;
-              break;
-            }
-            mbar_arrive_expect_tx(BAR(R_FULL + stage), kUTile);
-            tma_load_2d(sR + stage * kUTile, &tmB, kb * 64, it * BN, BAR(R_FULL + stage));
+          mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
+          if (*done_cum >= 4 * (t + 1)) {  // every epilogue warp is done with this user tile
+            stage_end[stage] = t + 1;
+            mbar_arrive(BAR(R_FULL + stage));  // release: the marker is visible to the MMA warp
             if (++stage == NST) stage = 0, ph ^= 1;
+            break;
           }
-          if (ended) break;
+          for (int kb = 0; kb < kbn; ++kb) {
+            if (kStreamA) load_unit(&tmA, &tmAt, kb, ut * kBM);  // K block kb of the user tile ...
+            load_unit(&tmB, &tmBt, kb, it * BN);                 // ... and of the item tile
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA warp
     // All lanes run the loop (warp-uniform state, descriptors in uniform registers); the elected
-    // lane issues.  Descriptors: the entry's base plus a constant per K step (16 fp16 = 32 bytes =
-    // 2 in the 16-byte address field; K block = 16 KB).
+    // lane issues.  Descriptors: the unit's base plus a constant per K step (16 fp16 = 32 bytes =
+    // 2 in the 16-byte address field); the tail unit has its own swizzle.
     constexpr uint32_t idesc = idesc_f16_f32(kBM, BN);
     unsigned long long tiles_issued = 0;  // (user tile, item tile) contractions issued
     int stage = 0, as = 0;
     uint32_t ph = 0, aph = 0;
     int t = 0;
+    auto unit_desc = [&](int st_, int kb) {
+      const uint32_t a = sR + st_ * kUTile;
+      return kb == kbn - 1 ? sdesc_swz(a, 2 * tail) : sdesc_sw128(a);
+    };
+    auto next = [&]() {
+      if (++stage == NST) stage = 0, ph ^= 1;
+    };
     for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
-      for (int kb = 0; kb < KB; ++kb) {  // the user tile: into tensor memory, unit by unit
-        mbar_wait_sleep(BAR(R_FULL + stage), ph);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint64_t adesc = sdesc_sw128(sR + stage * kUTile);
+      if (!kStreamA) {
+        for (int kb = 0; kb < kbn; ++kb) {  // the user tile: into tensor memory, unit by unit
+          mbar_wait_sleep(BAR(R_FULL + stage), ph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t adesc = unit_desc(stage, kb);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            if (4 * kb + kk < ksteps) tmem_cp_128x256b(tmem + C::A_TMEM + 8 * (4 * kb + kk), adesc + (uint64_t)(2 * kk));
-          mma_commit(BAR(R_EMPTY + stage));  // the unit is free once the copy has completed
+            for (int kk = 0; kk < 4; ++kk)
+              if (4 * kb + kk < ksteps)
+                tmem_cp_128x256b(tmem + C::A_TMEM + 8 * (4 * kb + kk), adesc + (uint64_t)(2 * kk));
+            mma_commit(BAR(R_EMPTY + stage));  // the unit is free once the copy has completed
+          }
+          __syncwarp();
+          next();
         }
-        __syncwarp();
-        if (++stage == NST) stage = 0, ph ^= 1;
       }
       for (int it = 0; it < nit; ++it) {
         mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
@@ -235,18 +257,33 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             mbar_arrive(BAR(ACC_FULL + as));
           }
           __syncwarp();
-          if (++stage == NST) stage = 0, ph ^= 1;
+          next();
           if (++as == NACC) as = 0, aph ^= 1;
           break;
         }
         const uint32_t d = tmem + as * C::ACC_COLS;
-        for (int kb = 0; kb < KB; ++kb) {
-          if (kb > 0) {
+        for (int kb = 0; kb < kbn; ++kb) {
+          if (kb > 0) {  // (the first unit of the tile was awaited above)
             mbar_wait_sleep(BAR(R_FULL + stage), ph);
             tc_fence_after();
           }
-          if (elect_one()) {
-            const uint64_t bdesc = sdesc_sw128(sR + stage * kUTile);
+          if (kStreamA) {
+            // unit `stage` = K block kb of the user tile, the next unit = of the item tile
+            const int sa = stage;
+            next();
+            mbar_wait_sleep(BAR(R_FULL + stage), ph);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint64_t adesc = unit_desc(sa, kb), bdesc = unit_desc(stage, kb);
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                if (4 * kb + kk < ksteps)
+                  mma_f16(d, adesc + (uint64_t)(2 * kk), bdesc + (uint64_t)(2 * kk), idesc, (kb | kk) != 0);
+              mma_commit(BAR(R_EMPTY + sa));
+              mma_commit(BAR(R_EMPTY + stage));
+            }
+          } else if (elect_one()) {
+            const uint64_t bdesc = unit_desc(stage, kb);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)  // K steps of 16 (zero padding beyond d skipped)
               if (4 * kb + kk < ksteps)
@@ -254,7 +291,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             mma_commit(BAR(R_EMPTY + stage));
           }
           __syncwarp();
-          if (++stage == NST) stage = 0, ph ^= 1;
+          next();
         }
         if (elect_one()) mma_commit(BAR(ACC_FULL + as));
         __syncwarp();
@@ -370,34 +407,51 @@ static int sm_count_q() {
 
 template <int KB, class Pol>
 static cudaError_t launch_tcq(const BuildCtx& c, cudaStream_t st) {
-  using C = Cfg<KB>;
+  using C = Cfg<KB, Pol>;
   rmips_index_s* x = c.idx;
-  CUtensorMap ta, tb;
-  if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM)) return cudaErrorNotSupported;
-  if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->dpad, C::BN)) return cudaErrorNotSupported;
+  const int tail = tail_cols(x->d);
+  CUtensorMap ta, tat, tb, tbt;
+  if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM) ||
+      !make_tmap_f16_box(&tat, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM, tail) ||
+      !make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->dpad, C::BN) ||
+      !make_tmap_f16_box(&tbt, x->P16, (uint64_t)c.mb, (uint64_t)x->dpad, C::BN, tail))
+    return cudaErrorNotSupported;
   cudaError_t e = cudaFuncSetAttribute(k_build_tcq<KB, Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
   if (e != cudaSuccess) return e;
   const int tiles = (int)((x->n + kBM - 1) / kBM);
   const int grid = tiles < sm_count_q() ? tiles : sm_count_q();
   const int ksteps = (x->d + 15) / 16;  // K steps of 16 that touch real (non-padding) columns
-  k_build_tcq<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tb, x->perr, x->pnorm, c.scale_dev, x->n, c.mb,
-                                                          x->kmax, ksteps, c.cand, c.ccount, c.ovf_list,
-                                                          c.ovf_count, c.tiles_done);
+  x->build_kernel = KB == 0 ? 3 : 2;
+  x->cand_slots = Pol::kSlots;
+  k_build_tcq<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tat, tb, tbt, x->perr, x->pnorm, c.scale_dev, x->n,
+                                                          c.mb, x->kmax, ksteps, x->dpad / 64, tail, c.cand,
+                                                          c.ccount, c.ovf_list, c.ovf_count, c.tiles_done);
   count_launch();
   return cudaGetLastError();
 }
 
-// d_pad = 128..256 with m <= 2^20 (20-bit packed positions); otherwise cudaErrorNotSupported
-// (the SIMT build).
-cudaError_t build_tcq(const BuildCtx& c, cudaStream_t st) {
-  if (c.mb > (int64_t)kQPosMask + 1) return cudaErrorNotSupported;
+template <class Pol>
+static cudaError_t launch_tcq_kb(const BuildCtx& c, cudaStream_t st) {
   switch (c.idx->dpad) {
-    case 128: return launch_tcq<2, QPol>(c, st);
-    case 192: return launch_tcq<3, QPol>(c, st);
-    case 256: return launch_tcq<4, QPol>(c, st);
-    default: return cudaErrorNotSupported;
+    case 64: return launch_tcq<1, Pol>(c, st);
+    case 128: return launch_tcq<2, Pol>(c, st);
+    case 192: return launch_tcq<3, Pol>(c, st);
+    case 256: return launch_tcq<4, Pol>(c, st);
+    default: return launch_tcq<0, Pol>(c, st);  // d_pad > 256: A streamed with B
   }
 }
 
-}  // namespace rmips
+int build_cand_stride(int kmax, int64_t mb, int build_flags) {
+  return (!(build_flags & RMIPS_BUILD_SIMT) && kmax > kQ128MaxKmax && mb <= QPolT<256>::kMaxItems) ? 256 : kCand;
+}
 
+// Any d_pad: the candidate policy by (m, k_max): 4-byte entries when positions fit 20 bits (256 slots
+// above k_max = 80), else 8-byte entries (128 slots: k_max above ~90 then overflows rows to the exact
+// fallback, R11).
+cudaError_t build_tcq(const BuildCtx& c, cudaStream_t st) {
+  if (c.cstride == 256) return launch_tcq_kb<QPolT<256>>(c, st);
+  if (c.mb <= QPolT<128>::kMaxItems) return launch_tcq_kb<QPolT<128>>(c, st);
+  return launch_tcq_kb<FPol>(c, st);
+}
+
+}  // namespace rmips

@@ -265,7 +265,7 @@ __device__ __forceinline__ void cand_chunk(ScoreFn s_of, float E, int pos0, Cand
 // holds at least min(k_max, m) entries (see qrow_finish, candq.cuh); fewer means NaN scores (a user
 // whose norm exceeds FLT_MAX) and the row takes the exact fallback.
 __device__ __forceinline__ void cand_finish(CandRow& me, CandSmem sm, int rloc, float e0x2, int kmax, int64_t m,
-                                            int64_t row, int64_t n, int32_t* __restrict__ cand,
+                                            int64_t row, int64_t n, int32_t* __restrict__ cand, int cstride,
                                             int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list,
                                             int* __restrict__ ovf_count) {
   me = cand_refresh(me, sm, rloc, e0x2, kmax);
@@ -277,7 +277,7 @@ __device__ __forceinline__ void cand_finish(CandRow& me, CandSmem sm, int rloc, 
     } else {
       ccount[row] = me.cnt;
       const uint2* b = sm.buf + rloc;
-      for (int i = 0; i < me.cnt; ++i) cand[row * kCand + i] = (int32_t)b[i * kCandRows].y;
+      for (int i = 0; i < me.cnt; ++i) cand[row * cstride + i] = (int32_t)b[i * kCandRows].y;
     }
   }
 }

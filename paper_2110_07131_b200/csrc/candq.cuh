@@ -19,14 +19,15 @@
 // #{q >= qt} >= k_max; theta <- max(theta, deq(qt)); then one compaction pass that drops
 // entries below base' = theta - 2 E0 - 2 w and re-quantises the survivors on [base', vmax]
 // (base' and w' change, the value each entry stands for only goes down).
-// Positions must be < 2^20 (m <= 1,048,576; larger item sets use the SIMT build).
+// Positions must be < 2^20 (m <= 1,048,576; larger item sets use the 8-byte entries of cand.cuh, FPol in
+// candpol.cuh).  SLOTS (128 or 256) entries per row: 256 for k_max above ~80 (a refresh must leave
+// room for another 32-column chunk above the k_max kept entries).
 #pragma once
 #include "common.cuh"
 #include "sm100.cuh"
 
 namespace rmips {
 
-constexpr int kQSlots = 128;                       // entries per row
 constexpr int kQPosBits = 20;
 constexpr uint32_t kQPosMask = (1u << kQPosBits) - 1u;
 constexpr int kQMax = 4095;                        // 12-bit quantised bound
@@ -81,6 +82,7 @@ __device__ __forceinline__ QRow qrow_init(bool live, float smax) {
 
 // Refresh of this thread's row (all 32 lanes of the warp call it together).  Not inlined: one
 // copy per kernel keeps the hot loops in the instruction cache.
+template <int SLOTS>
 static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float e0x2, int kmax) {
   if (me.ovf) return me;
   sb.assume_shared();
@@ -159,7 +161,7 @@ static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float
     }
   }
   nw.cnt = wpos;
-  if (wpos > kQSlots - 32 || (nth > th && ge < kmax)) {  // no room / unverified theta: exact fallback
+  if (wpos > SLOTS - 32 || (nth > th && ge < kmax)) {  // no room / unverified theta: exact fallback
     nw.ovf = 1;
     nw.theta = __int_as_float(0x7f800000);
   }
@@ -204,8 +206,9 @@ __device__ __forceinline__ void qrow_append_chunk(ScoreFn s_of, const float (&g4
   me.vmax = vmax;
 }
 
+template <int SLOTS>
 __device__ __forceinline__ void qrow_maybe_refresh(QRow& me, QBuf sb, int rr, float e0x2, int kmax) {
-  if (__any_sync(0xffffffffu, me.cnt > kQSlots - 32)) me = qrow_refresh(me, sb, rr, e0x2, kmax);
+  if (__any_sync(0xffffffffu, me.cnt > SLOTS - 32)) me = qrow_refresh<SLOTS>(me, sb, rr, e0x2, kmax);
 }
 
 // Final compaction, then the candidate positions (or the overflow mark) are written out.  A live row
@@ -213,10 +216,12 @@ __device__ __forceinline__ void qrow_maybe_refresh(QRow& me, QBuf sb, int rr, fl
 // refresh keeps every entry with lo >= theta, of which there are >= k_max); fewer means scores that
 // never compare (NaN: a user whose norm exceeds FLT_MAX, build.cu) and the row takes the exact
 // fallback.
+template <int SLOTS>
 __device__ __forceinline__ void qrow_finish(QRow& me, QBuf sb, int rr, float e0x2, int kmax, int64_t m, int64_t row,
-                                            int64_t n, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
-                                            int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
-  me = qrow_refresh(me, sb, rr, e0x2, kmax);
+                                            int64_t n, int32_t* __restrict__ cand, int cstride,
+                                            int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list,
+                                            int* __restrict__ ovf_count) {
+  me = qrow_refresh<SLOTS>(me, sb, rr, e0x2, kmax);
   if (row < n) {
     if (me.ovf || (int64_t)me.cnt < (m < kmax ? m : (int64_t)kmax)) {
       ccount[row] = -1;
@@ -225,7 +230,7 @@ __device__ __forceinline__ void qrow_finish(QRow& me, QBuf sb, int rr, float e0x
     } else {
       ccount[row] = me.cnt;
       const uint32_t* b = sb.buf + rr;
-      for (int i = 0; i < me.cnt; ++i) cand[row * kCand + i] = (int32_t)(b[i * sb.R] & kQPosMask);
+      for (int i = 0; i < me.cnt; ++i) cand[row * cstride + i] = (int32_t)(b[i * sb.R] & kQPosMask);
     }
   }
 }

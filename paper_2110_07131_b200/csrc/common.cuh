@@ -23,6 +23,7 @@ constexpr int kTileU = 128;        // users per tile == Lemma 3 block size (read
 constexpr int kCand = 128;         // candidate slots per user row in the build epilogue
 constexpr int kCandPitch = kCand + 1;  // smem row pitch (bank-conflict-free appends)
 constexpr int kQB = 256;           // queries per kernel batch (tcgen05 N <= 256)
+constexpr int kMaxDim = 1024;      // largest d (the exact select stages fp64 user rows in shared memory)
 
 // Device status flags (bitwise OR into Index::d_flags[0]).
 constexpr int kFlagNonfinite = 1;
@@ -148,6 +149,8 @@ struct rmips_index_s {
   int64_t overflow_rows = 0;
   int64_t cand_total = 0;   // candidates kept by the build filter (sum over non-overflowed rows)
   int64_t tiles_done = 0;   // (128-user tile, item tile) contractions issued by the tensor-core build
+  int build_kernel = 0;     // 0 SIMT, 1 k_build_tc, 2 k_build_tcq (A in TMEM), 3 k_build_tcq (A streamed)
+  int cand_slots = 0;       // candidate slots per row of the build filter (128 or 256)
   float pscale = 1.f;       // items are scaled by 2^e before fp16 rounding
   double c1 = 0, c2 = 0;    // filter error constants (see common.cuh)
 

@@ -28,7 +28,8 @@ struct BuildCtx {
   float* scale_dev = nullptr;     // 2^e
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
-  int32_t* cand = nullptr;        // [n][kCand] candidate item positions
+  int32_t* cand = nullptr;        // [n][cstride] candidate item positions
+  int cstride = kCand;            // candidate slots per row: 128, or 256 for k_max > kQ128MaxKmax
   int32_t* ccount = nullptr;      // [n] candidates per row, -1 = overflowed
   int32_t* ovf_list = nullptr;    // [n] overflowed rows
   int* ovf_count = nullptr;       // device counter
@@ -40,7 +41,11 @@ size_t build_cub_bytes(int64_t n, int64_t m);
 cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t st);
 cudaError_t build_simt(const BuildCtx& c, cudaStream_t st);
 cudaError_t build_tc(const BuildCtx& c, cudaStream_t st);  // build_tc.cu; cudaErrorNotSupported if unusable
-cudaError_t build_tcq(const BuildCtx& c, cudaStream_t st);  // build_tcq.cu (d_pad 128..256)
+cudaError_t build_tcq(const BuildCtx& c, cudaStream_t st);  // build_tcq.cu (any d_pad)
+// Candidate slots per row the build will use (BuildCtx::cstride): 256 when k_max > kQ128MaxKmax and the
+// positions fit the 4-byte entries (m <= 2^20), else 128.
+constexpr int kQ128MaxKmax = 80;
+int build_cand_stride(int kmax, int64_t mb, int build_flags);
 cudaError_t build_select(BuildCtx& c, cudaStream_t st);
 cudaError_t build_fallback(BuildCtx& c, int nrows, double* scratch, int grid, cudaStream_t st);
 cudaError_t build_blocks(BuildCtx& c, cudaStream_t st);
@@ -75,7 +80,12 @@ struct QueryCtx {
 };
 
 // TMA descriptor of a 2-D fp16 tensor [rows][cols], box box_rows x 64, SWIZZLE_128B (build_tc.cu).
-bool make_tmap_f16_box(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+bool make_tmap_f16_box(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                       uint32_t box_cols = 64);
+// Columns TMA loads for the LAST 64-column K block of a d-column row: the K steps of 16 that hold data
+// (16 * ceil(d / 16) - 64 * (KB - 1)), rounded up to a box of 16, 32 or 64 columns (swizzle 32, 64 or
+// 128 bytes).  d = 200: 16 columns, so a row streams 416 bytes instead of 512.
+int tail_cols(int d);
 
 cudaError_t query_prep(QueryCtx& c, cudaStream_t st);
 cudaError_t query_filter_simt(QueryCtx& c, cudaStream_t st);

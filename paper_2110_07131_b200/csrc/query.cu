@@ -286,9 +286,9 @@ k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const 
               int64_t m, int d, int pd, int k, unsigned long long* __restrict__ ctr,
               const uint64_t* __restrict__ und_list, AccSink acc_list, int64_t cap, int64_t start,
               const int32_t* __restrict__ beats0) {
-  __shared__ __align__(16) float su[kScanWarps][256];  // the pair's u, fp32, zero-padded to pd
+  extern __shared__ __align__(16) float su[];  // [kScanWarps][pd]: the pair's u, fp32, zero-padded to pd
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float* uw = su[w];
+  float* uw = su + (size_t)w * pd;
   const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_UND_TOTAL]);
   const double slack = 1.0 + (d + 8) * 2.220446049250313e-16;
   const double n32 = pd / 4 + 2, g32 = n32 * 5.9604644775390625e-08 / (1.0 - n32 * 5.9604644775390625e-08);
@@ -423,15 +423,20 @@ cudaError_t query_filter_simt(QueryCtx& c, cudaStream_t st) {
 cudaError_t query_exact(QueryCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   if (x->n == 0) return cudaSuccess;
+  const size_t scan_smem = (size_t)kScanWarps * x->pd * sizeof(float);
+  if (scan_smem > 48 * 1024 && (c.flags & RMIPS_FLAG_VERIFY_SCAN || x->mprime < x->m)) {
+    cudaError_t e = cudaFuncSetAttribute(k_verify_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem);
+    if (e != cudaSuccess) return e;
+  }
   if (c.flags & RMIPS_FLAG_VERIFY_SCAN) {  // every undecided pair scans all of P (Alg. 2)
-    k_verify_scan<<<148 * 8, 32 * kScanWarps, 0, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
+    k_verify_scan<<<148 * 8, 32 * kScanWarps, scan_smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
                                                            x->d, x->pd, c.k, c.counters, c.und, AccSink{c.acc, c.bits, c.nw}, c.cap, 0,
                                                            nullptr); count_launch();
   } else if (x->mprime < x->m) {  // P' index: Lemmas 1-2 / Cor. 1 per pair, then the scan after P'
     k_exact_decide_pp<<<148 * 8, 256, 0, st>>>(c.q, x->U32, x->unorm, x->pnorm, x->tau, x->n, x->m, x->mprime, c.k,
                                                x->perm_u, x->d, c.counters, c.und, c.scan_cnt, AccSink{c.acc, c.bits, c.nw}, c.cap);
     count_launch();
-    k_verify_scan<<<148 * 8, 32 * kScanWarps, 0, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
+    k_verify_scan<<<148 * 8, 32 * kScanWarps, scan_smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
                                                            x->d, x->pd, c.k, c.counters, c.und, AccSink{c.acc, c.bits, c.nw}, c.cap,
                                                            x->mprime, c.scan_cnt); count_launch();
   } else {

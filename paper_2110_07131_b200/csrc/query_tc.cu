@@ -45,11 +45,14 @@ constexpr int kAcc = 2;
 
 // The user stream is a ring of K-block units (16 KB each): a user tile of d_pad = 64*KB columns
 // takes KB consecutive units, and the MMA on K block kb starts as soon as that unit has landed.
+// KB = 0 (d_pad > 256: the queries do not fit in shared memory next to the ring): every ring unit holds
+// K block kb of the user tile (16 KB) AND of the sub-batch's queries (32 KB, re-read from L2 per tile).
 struct QSmem {
-  static constexpr int NU(int KB) { return KB == 1 ? 4 : 6; }  // ring units
+  static constexpr int NU(int KB) { return KB == 1 ? 4 : KB == 0 ? 4 : 6; }  // ring units
+  static constexpr int UNIT(int KB) { return KB == 0 ? kUTileBytes + kQTileBytes : kUTileBytes; }
   static constexpr int Q = 0;
   static constexpr int A(int KB) { return KB * kQTileBytes; }
-  static constexpr int BAR(int KB) { return A(KB) + NU(KB) * kUTileBytes; }
+  static constexpr int BAR(int KB) { return A(KB) + NU(KB) * UNIT(KB); }
   static constexpr int TOTAL(int KB) { return BAR(KB) + 256 + 1024; }
 };
 
@@ -233,7 +236,8 @@ k_lemma3_lens(const float* __restrict__ tbk, const float* __restrict__ qn, const
 
 template <int KB>
 __global__ void __launch_bounds__(kThreads, 1)
-k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmQ,
+k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmUt,
+           const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQt, int kb_rt, int tail,
            const float* __restrict__ thrk, const float* __restrict__ tbk, const int32_t* __restrict__ perm_u,
            int64_t n, int nblocks, const float* __restrict__ qn, const float* __restrict__ qerr,
            const float* __restrict__ qscale, const int32_t* __restrict__ qperm, const int32_t* __restrict__ qcount,
@@ -241,6 +245,10 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
            AccSink acc_list, uint64_t* __restrict__ und_list, int64_t cap) {
   using namespace sm100;
   constexpr int kStages = QSmem::NU(KB);  // ring units
+  constexpr int kUnit = QSmem::UNIT(KB);
+  constexpr bool kStreamQ = KB == 0;
+  const int kbn = kStreamQ ? kb_rt : KB;  // K blocks per row; the last one is `tail` columns wide
+  const uint32_t utail = (uint32_t)(kBM * tail * 2), qtail = (uint32_t)(kQB * tail * 2);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
@@ -260,6 +268,8 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmU);
     tma_prefetch(&tmQ);
+    tma_prefetch(&tmUt);
+    tma_prefetch(&tmQt);
     mbar_init(BAR(Q_FULL), 1);
     mbar_init(BAR(Q_EMPTY), 1);
     for (int s = 0; s < kStages; ++s) mbar_init(BAR(A_FULL + s), 1), mbar_init(BAR(A_EMPTY + s), 1);
@@ -296,21 +306,26 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
       for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x, next_item(s, t)) {
         const int len = __ldg(wlen + w);
         if (len == 0) continue;
-        if (s != cur_s) {
+        if (!kStreamQ && s != cur_s) {
           if (nq > 0) mbar_wait(BAR(Q_EMPTY), (nq - 1) & 1);
-          mbar_arrive_expect_tx(BAR(Q_FULL), KB * kQTileBytes);
-          for (int kb = 0; kb < KB; ++kb) tma_load_2d(sQ + kb * kQTileBytes, &tmQ, kb * 64, s * kQB, BAR(Q_FULL));
+          mbar_arrive_expect_tx(BAR(Q_FULL), (uint32_t)((kbn - 1) * kQTileBytes) + qtail);
+          for (int kb = 0; kb < kbn; ++kb)
+            tma_load_2d(sQ + kb * kQTileBytes, kb == kbn - 1 ? &tmQt : &tmQ, kb * 64, s * kQB, BAR(Q_FULL));
           ++nq;
           cur_s = s;
         }
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = 0; kb < kbn; ++kb) {
           {
             QPROF_T0();
             mbar_wait(BAR(A_EMPTY + stage), ph ^ 1);
             QPROF_ADD(4);
           }
-          mbar_arrive_expect_tx(BAR(A_FULL + stage), kUTileBytes);
-          tma_load_2d(sA + stage * kUTileBytes, &tmU, kb * 64, t * kBM, BAR(A_FULL + stage));
+          const bool last = kb == kbn - 1;
+          mbar_arrive_expect_tx(BAR(A_FULL + stage), (last ? utail : (uint32_t)kUTileBytes) +
+                                                         (kStreamQ ? (last ? qtail : (uint32_t)kQTileBytes) : 0u));
+          tma_load_2d(sA + stage * kUnit, last ? &tmUt : &tmU, kb * 64, t * kBM, BAR(A_FULL + stage));
+          if (kStreamQ)
+            tma_load_2d(sA + stage * kUnit + kUTileBytes, last ? &tmQt : &tmQ, kb * 64, s * kQB, BAR(A_FULL + stage));
           if (++stage == kStages) stage = 0, ph ^= 1;
         }
       }
@@ -326,7 +341,7 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x, next_item(s, t)) {
       const int len = __ldg(wlen + w);
       if (len == 0) continue;
-      if (s != cur_s) {
+      if (!kStreamQ && s != cur_s) {
         if (nq > 0) {
           if (elect_one()) mma_commit(BAR(Q_EMPTY));  // all MMAs on the previous sub-batch's queries
           __syncwarp();
@@ -345,15 +360,17 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
       const int N = (len + 15) & ~15;
       const uint32_t idesc = idesc_f16_f32(kBM, N);
       const uint32_t d = tmem + as * kAccCols;
-      for (int kb = 0; kb < KB; ++kb) {
+      for (int kb = 0; kb < kbn; ++kb) {
         {
           QPROF_T0();
           mbar_wait(BAR(A_FULL + stage), ph);
           QPROF_ADD(2);
         }
         tc_fence_after();
-        const uint64_t adesc = sdesc_sw128(sA + stage * kUTileBytes);
-        const uint64_t bdesc = sdesc_sw128(sQ + kb * kQTileBytes);
+        const bool last = kb == kbn - 1;  // the tail K block has its own swizzle (tail_cols)
+        const uint32_t ua = sA + stage * kUnit, qa = kStreamQ ? ua + kUTileBytes : sQ + kb * kQTileBytes;
+        const uint64_t adesc = last ? sdesc_swz(ua, 2 * tail) : sdesc_sw128(ua);
+        const uint64_t bdesc = last ? sdesc_swz(qa, 2 * tail) : sdesc_sw128(qa);
         const int kk_end = min(4, ksteps - 4 * kb);  // zero-padding K steps are skipped
         if (elect_one()) {
 #pragma unroll
@@ -507,9 +524,13 @@ static int sm_count_q() {
 template <int KB>
 static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
-  CUtensorMap tu, tq;
-  if (!make_tmap_f16_box(&tu, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM)) return cudaErrorNotSupported;
-  if (!make_tmap_f16_box(&tq, c.Q16, (uint64_t)c.nsub * kQB, (uint64_t)x->dpad, kQB)) return cudaErrorNotSupported;
+  const int tail = tail_cols(x->d);
+  CUtensorMap tu, tut, tq, tqt;
+  if (!make_tmap_f16_box(&tu, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM) ||
+      !make_tmap_f16_box(&tut, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM, tail) ||
+      !make_tmap_f16_box(&tq, c.Q16, (uint64_t)c.nsub * kQB, (uint64_t)x->dpad, kQB) ||
+      !make_tmap_f16_box(&tqt, c.Q16, (uint64_t)c.nsub * kQB, (uint64_t)x->dpad, kQB, tail))
+    return cudaErrorNotSupported;
   const int smem = QSmem::TOTAL(KB);
   cudaError_t e = cudaFuncSetAttribute(k_query_tc<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -519,7 +540,7 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
                                                                  c.qcount, (int)x->nblocks, nwork, c.flags, c.wlen,
                                                                  c.counters);
   count_launch();
-  k_query_tc<KB><<<grid, kThreads, smem, st>>>(tu, tq, x->thr + (int64_t)(c.k - 1) * x->n,
+  k_query_tc<KB><<<grid, kThreads, smem, st>>>(tu, tut, tq, tqt, x->dpad / 64, tail, x->thr + (int64_t)(c.k - 1) * x->n,
                                                x->tb + (int64_t)(c.k - 1) * x->nblocks, x->perm_u, x->n,
                                                (int)x->nblocks, c.qn, c.qerr, c.qscale, c.qperm, c.qcount, c.nsub,
                                                c.flags, (x->d + 15) / 16, c.wlen, c.counters, AccSink{c.acc, c.bits, c.nw}, c.und, c.cap);
@@ -537,7 +558,7 @@ cudaError_t query_filter_tc(QueryCtx& c, cudaStream_t st) {
     case 128: return launch_query_tc<2>(c, st);
     case 192: return launch_query_tc<3>(c, st);
     case 256: return launch_query_tc<4>(c, st);
-    default: return cudaErrorNotSupported;
+    default: return launch_query_tc<0>(c, st);  // d_pad > 256: queries streamed with the users
   }
 }
 

@@ -178,6 +178,20 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// The same for a K-major tile written by TMA with a narrower swizzle, i.e. a K block of fewer than 64
+// fp16 columns (the trimmed last K block of a row): rows of swz bytes (32, 64 or 128),
+// 8-row core groups 8 * swz bytes apart; layout type SWIZZLE_32B = 6, SWIZZLE_64B = 4, SWIZZLE_128B = 2.
+__device__ __forceinline__ uint64_t sdesc_swz(uint32_t smem_addr, int swz) {
+  const uint64_t layout = swz == 32 ? 6 : swz == 64 ? 4 : 2;
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((8 * swz) >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= layout << 61;
+  return d;
+}
+
 // 32 lanes x 32 consecutive 32-bit columns: thread t of the warp gets row (lane base + t).
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(

@@ -113,7 +113,8 @@ class Index:
         info = (ctypes.c_int64 * 16)()
         _check(lib.rmips_index_info(self.handle, info))
         self.n, self.m, self.d, self.k_max, self.d_pad, self.block_size, self.overflow_rows, self.build_flags, \
-            self.cand_total, self.tiles_done, self.m_prime = [int(v) for v in info[:11]]
+            self.cand_total, self.tiles_done, self.m_prime, self.build_kernel, self.cand_slots = \
+            [int(v) for v in info[:13]]
 
     def close(self):
         if self.handle:

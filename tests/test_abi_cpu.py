@@ -50,8 +50,9 @@ def test_validation_without_gpu(lib):
     # m < 1, d < 1
     assert L.rmips_build_index(None, 0, None, 0, 4, 1, None, ctypes.byref(h)) == lib.RMIPS_ERR_INVALID
     assert L.rmips_build_index(None, 0, ctypes.c_void_p(8), 3, 0, 1, None, ctypes.byref(h)) == lib.RMIPS_ERR_INVALID
-    # d > 256 unsupported
-    assert L.rmips_build_index(None, 0, ctypes.c_void_p(8), 3, 300, 1, None, ctypes.byref(h)) == lib.RMIPS_ERR_INVALID
+    # d > 1024 unsupported (the tensor-core path covers 1..1024); the SIMT build d <= 256
+    assert L.rmips_build_index(None, 0, ctypes.c_void_p(8), 3, 1025, 1, None, ctypes.byref(h)) == lib.RMIPS_ERR_INVALID
+    assert L.rmips_build_index_ex(None, 0, ctypes.c_void_p(8), 3, 300, 1, 1, None, ctypes.byref(h)) == lib.RMIPS_ERR_INVALID
     # k_max < 1
     assert L.rmips_build_index(None, 0, ctypes.c_void_p(8), 3, 4, 0, None, ctypes.byref(h)) == lib.RMIPS_ERR_K_RANGE
     # query on a NULL index

@@ -631,3 +631,87 @@ def test_concurrent_builds_same_stream_handle():
     for t_ in ts:
         t_.join()
     assert not errors, errors[:3]
+
+
+# ---------------------------------------------------------------- the full boundary domain
+
+@pytest.mark.parametrize("d", [300, 513, 1000])
+def test_large_d_streamed_k_loop(d):
+    """d > 256: the build streams the user tile's K blocks next to the item tile's (k_build_tcq, KB = 0)
+    and the query filter streams the queries' K blocks (k_query_tc, KB = 0); the last K block is trimmed
+    (d = 513: a 16-column tail).  Sets equal the naive oracle's; tau / ids bitwise."""
+    U, P = gen.random_instance(70 + d, 700, 450, d, "skewed")
+    Qy = np.concatenate([P[:20], gen.random_instance(71 + d, 15, 1, d, "skewed")[0]])
+    idx = rmips.rmips_build_index(_t(U), _t(P), 12)
+    assert idx.build_kernel == 3 and idx.build_flags & rmips.RMIPS_BUILD_SIMT == 0
+    for k in (1, 5, 12):
+        member = oracle.rkmips_naive(U, P, Qy, k)
+        got = rmips.split_sets(*rmips.rmips_query(idx, _t(Qy), k))
+        assert idx.stats()["filter_kernel"] == 1
+        assert_same(got, member, U, P, Qy, k, "d=%d k=%d" % (d, k))
+        got = rmips.split_sets(*rmips.rmips_query(idx, _t(Qy), k, rmips.RMIPS_FLAG_FORCE_VERIFY))
+        assert_same(got, member, U, P, Qy, k, "d=%d k=%d force" % (d, k))
+    _, _, tau, ids = idx.export()
+    vals, oids = oracle.topk(U, P, 12)
+    assert np.array_equal(tau.T, vals) and np.array_equal(ids.T, oids)
+    with pytest.raises(rmips.RmipsError) as e:
+        rmips.rmips_query(idx, _t(Qy), 3, rmips.RMIPS_FLAG_SIMT)
+    assert e.value.status == rmips.RMIPS_ERR_INVALID
+    idx.close()
+
+
+@pytest.mark.parametrize("d", [16, 90, 200])
+def test_trimmed_tail_k_block(d):
+    """The last K block trimmed to a 16- or 32-column box (SWIZZLE_32B / 64B descriptors) in both the
+    build and the query kernels: d = 16 (one 16-column block), 90 (32-column tail), 200 (16-column tail)."""
+    U, P = gen.random_instance(80 + d, 1500, 700, d, "gaussian")
+    Qy = np.concatenate([P[:30], gen.random_instance(81 + d, 30, 1, d)[0]])
+    for kmax, k in ((10, 4), (100, 37)):   # the second: k_max > 80 -> 256-slot lists (k_build_tcq for d = 16)
+        member = oracle.rkmips_naive(U, P, Qy, k)
+        idx = rmips.rmips_build_index(_t(U), _t(P), kmax)
+        assert idx.build_flags & rmips.RMIPS_BUILD_SIMT == 0 and idx.overflow_rows == 0
+        assert idx.cand_slots == (256 if kmax > 80 else 128)
+        got = rmips.split_sets(*rmips.rmips_query(idx, _t(Qy), k))
+        assert_same(got, member, U, P, Qy, k, "tail d=%d kmax=%d" % (d, kmax))
+        _, _, tau, ids = idx.export()
+        vals, oids = oracle.topk(U, P, kmax)
+        assert np.array_equal(tau.T, vals) and np.array_equal(ids.T, oids)
+        idx.close()
+
+
+@pytest.mark.parametrize("d", [50, 100])
+def test_kmax_128_lists_without_fallback(d):
+    """k_max = 128: the 256-slot 4-byte candidate lists hold every row (no exact-fallback
+    rows), the exported lists equal the oracle's bitwise, and k = 100 and 128 answer like the oracle."""
+    U, P = gen.random_instance(90 + d, 3000, 2500, d, "skewed")
+    Qy = P[:40]
+    idx = rmips.rmips_build_index(_t(U), _t(P), 128)
+    assert idx.cand_slots == 256 and idx.build_kernel == 2 and idx.overflow_rows == 0
+    _, _, tau, ids = idx.export()
+    vals, oids = oracle.topk(U, P, 128)
+    assert np.array_equal(tau.T, vals) and np.array_equal(ids.T, oids)
+    for k in (100, 128):
+        member = oracle.rkmips_twophase(U, vals, Qy, k)
+        got = rmips.split_sets(*rmips.rmips_query(idx, _t(Qy), k))
+        assert_same(got, member, label="kmax128 d=%d k=%d" % (d, k))
+    idx.close()
+
+
+def test_m_above_2pow20_tensor_core_build():
+    """m = 1.1 M items with d = 100: item positions no longer fit the 4-byte entries'
+    20 bits, so the tensor-core build keeps 8-byte entries (FPol); it must still be the tcgen05 kernel
+    (not the SIMT build) and give the oracle's exact lists on a user sample."""
+    w = gen.make_workload(4, n=1500, m=1_100_000, nq=30, d=100)
+    idx = rmips.rmips_build_index(_t(w.U), _t(w.P), 20)
+    assert idx.build_kernel == 2 and idx.build_flags & rmips.RMIPS_BUILD_SIMT == 0
+    assert idx.cand_slots == 128 and idx.overflow_rows == 0
+    sample = np.sort(np.random.default_rng(3).choice(w.U.shape[0], 160, replace=False))
+    vals, oids = oracle.topk(w.U[sample], w.P, 20)
+    _, _, tau, ids = idx.export()
+    assert np.array_equal(tau[:, sample].T, vals) and np.array_equal(ids[:, sample].T, oids)
+    off, gids = rmips.rmips_query(idx, _t(w.Qy), 20)
+    sets = rmips.split_sets(off, gids)
+    member = oracle.rkmips_twophase(w.U[sample], vals, w.Qy, 20)
+    for qi in range(w.Qy.shape[0]):
+        assert np.array_equal(np.intersect1d(sets[qi], sample), sample[member[qi]]), qi
+    idx.close()
