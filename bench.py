@@ -297,7 +297,7 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
-    step_ms, recs = [], []
+    step_ms, recs, host_ms = [], [], []
     last = None
     sampler = ClockSampler(dev.index)
     with sampler:
@@ -308,7 +308,9 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
+            th0 = time.perf_counter()
             idx, outs, qph = step()
+            host_ms.append((time.perf_counter() - th0) * 1e3)
             e1.record(stream)
             torch.cuda.synchronize()
             recs.append(readout(idx, outs, qph))        # (frees the index: stream-ordered, after e1)
@@ -384,6 +386,7 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
                   "unit": "GB/s", "frac": (sbytes / (ex_ms / 1e3) / 1e9) / peaks["hbm_gbs"] if ex_ms > 0 else None}
 
     res = {"value": value, "ms_per_step": ms_per_step, "steps": steps, "warmup": warmup,
+           "step_ms": [round(x, 3) for x in step_ms], "host_ms": [round(x, 3) for x in host_ms],
            "config": _config_dict(spec, k, ws) | {"kernels": "simt" if args.simt else "tcgen05"},
            "build": {"ms": med("build"), "inner_products_per_s": spec.n * spec.m / (med("build") / 1e3),
                      "contraction_ms": kern_ms, "prep_ms": med("prep"), "select_blocks_ms": med("select"),

@@ -65,7 +65,7 @@ enum {
   RMIPS_FLAG_TIMING = 16,       /* record per-phase CUDA-event times (rmips_phase_times) */
   RMIPS_FLAG_NO_EXTEND = 32,    /* k > k_max fails with RMIPS_ERR_K_RANGE instead of extending the index */
   RMIPS_FLAG_KEY_SORT = 64      /* output through the sorted (query, user) key list even when the
-                                   b x n bit matrix (b * ceil(n/32) * 4 bytes <= 512 MiB) would be used */
+                                   b x n bit matrix (b * ceil(n/32) * 4 bytes <= 64 MiB) would be used */
 };
 
 /* Per-index build options (rmips_build_index_ex). */
@@ -148,7 +148,7 @@ RMIPS_API rmips_status_t rmips_build_index_host(const float* Q, int64_t n, const
  *   capacity   number of int32 slots in user_ids
  *   total_out  host: receives sum_i |R(q_i)| (also on RMIPS_ERR_CAPACITY, with offsets valid)
  * Output assembly: accepted pairs are set as bits of a b x n matrix in the query workspace when
- * b * ceil(n/32) * 4 <= 512 MiB (read back row by row: no sort and no mid-call host sync), else
+ * b * ceil(n/32) * 4 <= 64 MiB (read back chunk by chunk: no sort, one host sync per call), else
  * appended as (query, user) keys and radix-sorted.  Same offsets and ids either way.
  * Errors: INVALID, NONFINITE (non-finite query), K_RANGE, CAPACITY, OOM, CUDA. */
 RMIPS_API rmips_status_t rmips_query(rmips_index_t idx, const float* q_batch, int32_t b, int32_t k,

@@ -460,11 +460,13 @@ constexpr size_t kBitsMaxBytes = (size_t)64 << 20;  // largest bit-matrix output
 
 static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cudaStream_t st) {
   const int dpad = x->dpad;
-  size_t qcub = query_cub_bytes(cap);
-  const size_t qscan = query_scan_bytes(c.b);
-  if (qscan > qcub) qcub = qscan;
   // accepted pairs as a bit matrix when it is small enough (no key sort, no mid-call sync)
   const int64_t nw = (x->n + 31) / 32;
+  const int64_t nch = query_bits_chunks(c.b, nw);  // its output pass keeps 2 nch int64 in acc_sorted's space
+  if (cap < 2 * nch) cap = 2 * nch;
+  size_t qcub = query_cub_bytes(cap);
+  const size_t qscan = query_scan_bytes(nch);
+  if (qscan > qcub) qcub = qscan;
   const bool use_bits = x->n > 0 && !(c.flags & RMIPS_FLAG_KEY_SORT) && (size_t)c.b * (size_t)nw * 4 <= kBitsMaxBytes &&
                         c.b <= cap;
   size_t off = 0;

@@ -38,6 +38,10 @@ extern __device__ unsigned long long g_epi_prof[4][256];  // build_tc.cu
 
 namespace {
 
+// development-only experiment switches (librmips_dev.so reads them from the environment)
+constexpr int kDevNoFeed = 1;   // RMIPS_NOFEED: item units after the first ring round are not reloaded
+constexpr int kDevEpiSkip = 2;  // RMIPS_EPI_SKIP: the epilogue releases every stage unread
+
 constexpr int kBM = 128;                 // users per tile (TMEM lanes)
 constexpr int kUTile = kBM * 64 * 2;     // one 128 x 64 fp16 K-block unit = 16 KB
 
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(Cfg<KB, Pol>::THREADS, 1)
 k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAt,
             const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBt,
             const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
-            int64_t n, int64_t m, int kmax, int ksteps, int kb_rt, int tail, int32_t* __restrict__ cand,
+            int64_t n, int64_t m, int kmax, int ksteps, int kb_rt, int tail, int dev, int32_t* __restrict__ cand,
             int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count,
             unsigned long long* __restrict__ tiles_done) {
   using namespace sm100;
@@ -187,11 +191,17 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       uint32_t ph = 0;
       int t = 0;
       // one K-block unit (rows r0.., K block kb) of map m / tail map mt into the next ring slot
+      int nloads = 0;
       auto load_unit = [&](const CUtensorMap* mfull, const CUtensorMap* mtail, int kb, int r0) {
         const bool last = kb == kbn - 1;
         mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
-        mbar_arrive_expect_tx(BAR(R_FULL + stage), last ? tail_bytes : (uint32_t)kUTile);
-        tma_load_2d(sR + stage * kUTile, last ? mtail : mfull, kb * 64, r0, BAR(R_FULL + stage));
+        if ((dev & kDevNoFeed) && mfull == &tmB && nloads >= 2 * NST) {
+          mbar_arrive(BAR(R_FULL + stage));  // dev: the MMA re-reads the stale slot (no L2 feed)
+        } else {
+          mbar_arrive_expect_tx(BAR(R_FULL + stage), last ? tail_bytes : (uint32_t)kUTile);
+          tma_load_2d(sR + stage * kUTile, last ? mtail : mfull, kb * 64, r0, BAR(R_FULL + stage));
+        }
+        ++nloads;
         if (++stage == NST) stage = 0, ph ^= 1;
       };
       for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
@@ -332,6 +342,18 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       tmem_ld_wait64(hA);
       int it = 0;
       bool done = false;  // warp-uniform: this warp's rows cannot gain any more
+      if (dev & kDevEpiSkip) {  // dev: release every accumulator stage unread (MMA + feed alone)
+        for (; it < nit; ++it) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
+          if (++as == NACC) as = 0, aph ^= 1;
+          if (it + 1 < nit) {
+            mbar_wait(BAR(ACC_FULL + as), aph);
+            tc_fence_after();
+          }
+        }
+      }
       for (; it < nit; ++it) {
         const int base0 = it * BN;
         const float E[4] = {Eg, Eg, Eg, Eg};
@@ -385,7 +407,11 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           tc_fence_after();
         }
       }
-      Pol::finish(me, sb, rr, e0x2, kmax, m, row, n, cand, ccount, ovf_list, ovf_count);
+      if (dev & kDevEpiSkip) {
+        if (row < n) ccount[row] = 0;  // dev: empty lists, no fallback
+      } else {
+        Pol::finish(me, sb, rr, e0x2, kmax, m, row, n, cand, ccount, ovf_list, ovf_count);
+      }
       __syncwarp();
     }
   }
@@ -421,10 +447,14 @@ static cudaError_t launch_tcq(const BuildCtx& c, cudaStream_t st) {
   const int tiles = (int)((x->n + kBM - 1) / kBM);
   const int grid = tiles < sm_count_q() ? tiles : sm_count_q();
   const int ksteps = (x->d + 15) / 16;  // K steps of 16 that touch real (non-padding) columns
+  int dev = 0;
+#ifdef RMIPS_DEV
+  dev = (getenv("RMIPS_NOFEED") ? kDevNoFeed : 0) | (getenv("RMIPS_EPI_SKIP") ? kDevEpiSkip : 0);
+#endif
   x->build_kernel = KB == 0 ? 3 : 2;
   x->cand_slots = Pol::kSlots;
   k_build_tcq<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tat, tb, tbt, x->perr, x->pnorm, c.scale_dev, x->n,
-                                                          c.mb, x->kmax, ksteps, x->dpad / 64, tail, c.cand,
+                                                          c.mb, x->kmax, ksteps, x->dpad / 64, tail, dev, c.cand,
                                                           c.ccount, c.ovf_list, c.ovf_count, c.tiles_done);
   count_launch();
   return cudaGetLastError();

@@ -93,7 +93,8 @@ cudaError_t query_filter_tc(QueryCtx& c, cudaStream_t st);  // query_tc.cu
 cudaError_t query_exact(QueryCtx& c, cudaStream_t st);
 cudaError_t query_output(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st);
 size_t query_cub_bytes(int64_t cap);
-size_t query_scan_bytes(int b);
+size_t query_scan_bytes(int64_t items);
+int64_t query_bits_chunks(int b, int64_t nw);  // warp chunks of the bit-matrix output (scan items)
 // zero four small regions (counts in 32-bit words, <= 128 each) in one launch (build.cu)
 cudaError_t zero4(cudaStream_t st, void* a, int na, void* b, int nb, void* c, int nc, void* d, int nd);
 cudaError_t query_sort(QueryCtx& c, int64_t total, int end_bit, cudaStream_t st);

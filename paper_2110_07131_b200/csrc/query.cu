@@ -15,44 +15,49 @@
 namespace rmips {
 
 // ------------------------------------------------------------------------------ Q1
-// One CTA (256 threads) per 256-query sub-batch.  Thread t computes the norm of query t; every
-// thread then ranks its query in (norm desc, index asc) order, and all threads write the fp16 rows
-// (q * 2^eq, zero-padded to d_pad) element-parallel.
-__global__ void __launch_bounds__(kQB)
+// One CTA (1024 threads) per 256-query sub-batch.  Warp w computes the norms of queries w, w + 32, ...
+// with coalesced row reads (lanes over the row, fp64 sum; only its rounded-up value is used, so the
+// order does not matter), threads 0..255 rank the queries in (norm desc, index asc) order, and all
+// threads write the fp16 rows (q * 2^eq, zero-padded to d_pad) element-parallel.
+constexpr int kPrepThreads = 1024;
+__global__ void __launch_bounds__(kPrepThreads)
 k_query_prep(const float* __restrict__ q, int b, int d, int dpad, double c1, double c2, __half* __restrict__ Q16,
              float* __restrict__ qn, float* __restrict__ qerr, float* __restrict__ qscale,
              int32_t* __restrict__ qperm, int32_t* __restrict__ qcount, int* __restrict__ flags) {
   __shared__ double nrm[kQB];
-  __shared__ float smax[kQB / 32];
+  __shared__ float smax[kPrepThreads / 32];
   __shared__ int srank[kQB];
   __shared__ float s_scale;
   const int s = blockIdx.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int cnt = min(kQB, b - s * kQB);
   float mx = 0.f;
-  {  // thread t: the norm of query t of the sub-batch (a sequential fp64 sum; only its rounded-up
-     // value is used, so the order does not matter)
+  for (int qi = wid; qi < kQB; qi += kPrepThreads / 32) {
     double acc = 0.0;
     bool fin = true;
-    if (t < cnt) {
-      const float* x = q + (int64_t)(s * kQB + t) * d;
-#pragma unroll 4
-      for (int e = 0; e < d; ++e) {
+    if (qi < cnt) {
+      const float* x = q + (int64_t)(s * kQB + qi) * d;
+      for (int e = lane; e < d; e += 32) {
         const float v = x[e];
         fin &= isfinite(v);
         mx = fmaxf(mx, fabsf(v));
         acc = __fma_rn((double)v, (double)v, acc);
       }
     }
-    double nr = t < cnt ? sqrt(acc) : -1.0;
-    if (t < cnt && !fin) atomicOr(flags, kFlagNonfinite), nr = 0.0;
-    nrm[t] = nr;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    fin = __all_sync(0xffffffffu, fin);
+    if (lane == 0) {
+      double nr = qi < cnt ? sqrt(acc) : -1.0;
+      if (qi < cnt && !fin) atomicOr(flags, kFlagNonfinite), nr = 0.0;
+      nrm[qi] = nr;
+    }
   }
   for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if (lane == 0) smax[wid] = isfinite(mx) ? mx : 0.f;
   __syncthreads();
   if (t == 0) {
     float m2 = 0.f;
-    for (int w = 0; w < kQB / 32; ++w) m2 = fmaxf(m2, smax[w]);
+    for (int w = 0; w < kPrepThreads / 32; ++w) m2 = fmaxf(m2, smax[w]);
     int ex = 0;
     if (m2 > 0.f) frexpf(m2, &ex);
     int e = max(-126, min(126, 14 - ex));
@@ -60,21 +65,24 @@ k_query_prep(const float* __restrict__ q, int b, int d, int dpad, double c1, dou
     qscale[s] = s_scale;
     qcount[s] = cnt;
   }
-  // rank = position in (norm desc, index asc) order
-  const double nr = nrm[t];
-  int rank = t;
-  if (t < cnt) {
-    rank = 0;
-    for (int j = 0; j < cnt; ++j) {
-      const double o = nrm[j];
-      rank += (o > nr) || (o == nr && j < t);
+  if (t < kQB) {
+    // rank = position in (norm desc, index asc) order
+    const double nr = nrm[t];
+    int rank = t;
+    if (t < cnt) {
+      rank = 0;
+      for (int j = 0; j < cnt; ++j) {
+        const double o = nrm[j];
+        rank += (o > nr) || (o == nr && j < t);
+      }
     }
+    srank[t] = rank;
   }
-  srank[t] = rank;
   __syncthreads();
   const float scale = s_scale;
-  {
-    const int64_t slot = (int64_t)s * kQB + rank;
+  if (t < kQB) {
+    const double nr = nrm[t];
+    const int64_t slot = (int64_t)s * kQB + srank[t];
     if (t < cnt) {
       qperm[slot] = s * kQB + t;
       qn[slot] = __double2float_ru(nr * (1.0 + 1e-12));
@@ -85,11 +93,18 @@ k_query_prep(const float* __restrict__ q, int b, int d, int dpad, double c1, dou
       qerr[slot] = 0.f;
     }
   }
-#pragma unroll 4
-  for (int idx = t; idx < kQB * dpad; idx += kQB) {  // fp16 rows, all threads over (query, element)
-    const int src = idx / dpad, e = idx - src * dpad;
+  // fp16 rows, two elements per thread per step (half2 stores; dpad is even)
+  const int hp = dpad / 2;
+  for (int idx = t; idx < kQB * hp; idx += kPrepThreads) {
+    const int src = idx / hp, e = 2 * (idx - src * hp);
     const int64_t slot = (int64_t)s * kQB + srank[src];
-    Q16[slot * dpad + e] = __float2half_rn(src < cnt && e < d ? q[(int64_t)(s * kQB + src) * d + e] * scale : 0.f);
+    float v0 = 0.f, v1 = 0.f;
+    if (src < cnt) {
+      const float* x = q + (int64_t)(s * kQB + src) * d;
+      if (e < d) v0 = x[e] * scale;
+      if (e + 1 < d) v1 = x[e + 1] * scale;
+    }
+    reinterpret_cast<__half2*>(Q16 + slot * dpad)[e >> 1] = __halves2half2(__float2half_rn(v0), __float2half_rn(v1));
   }
 }
 
@@ -390,7 +405,7 @@ static inline unsigned nblk(int64_t work, int t) { return (unsigned)((work + t -
 
 cudaError_t query_prep(QueryCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
-  k_query_prep<<<c.nsub, kQB, 0, st>>>(c.q, c.b, x->d, x->dpad, x->c1, x->c2, c.Q16, c.qn, c.qerr, c.qscale, c.qperm,
+  k_query_prep<<<c.nsub, kPrepThreads, 0, st>>>(c.q, c.b, x->d, x->dpad, x->c1, x->c2, c.Q16, c.qn, c.qerr, c.qscale, c.qperm,
                                        c.qcount, c.flags_dev); count_launch();
   return cudaGetLastError();
 }
@@ -472,85 +487,100 @@ __global__ void k_copy_ids32(const uint32_t* __restrict__ keys, int64_t total, u
   if (i < total) out[i] = (int32_t)(keys[i] % n);
 }
 
-// Bit-matrix output (QueryCtx::bits): per query the popcount of its row, an inclusive scan into
-// offsets[1..b], then the set bits of every row written in ascending user order (the order the
-// sorted-key path produces).  One CTA per query.  The emit pass clears every word it read, so the
+// Bit-matrix output (QueryCtx::bits): the b x n matrix is cut into warp chunks of kChunkWords words of
+// one query row (lane l owns words 32 l .. 32 l + 31 of its warp's chunk).  Pass 1 counts the set bits of
+// every chunk, a scan gives every chunk's first output position (the chunks are in (query, user) order),
+// and pass 2 writes the ids of every chunk in ascending user order and clears the words it read, so the
 // matrix is all zero again for the next batch (it is memset only when its place in the workspace
-// changes).
+// changes).  Every warp works independently: no block-level loop over a whole row.
+constexpr int kChunkWords = 1024;
 constexpr int kBitsThreads = 256;
-__device__ __forceinline__ int64_t block_sum64(int64_t v, int64_t* red) {
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  int64_t t = 0;
-  for (int w = 0; w < kBitsThreads / 32; ++w) t += red[w];
-  __syncthreads();
-  return t;
+__global__ void __launch_bounds__(kBitsThreads)
+k_bits_count(const uint32_t* __restrict__ bits, int64_t nw, int64_t nchunk_total, int64_t* __restrict__ counts) {
+  const int64_t g = (blockIdx.x * (int64_t)kBitsThreads + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= nchunk_total) return;
+  const int64_t per_row = (nw + kChunkWords - 1) / kChunkWords;
+  const int64_t q = g / per_row, c = g - q * per_row;
+  const uint32_t* row = bits + q * nw;
+  const int64_t w0 = c * kChunkWords + 32 * lane;
+  int cnt = 0;
+#pragma unroll 8
+  for (int j = 0; j < 32; ++j)
+    if (w0 + j < nw) cnt += __popc(row[w0 + j]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) counts[g] = cnt;
 }
 __global__ void __launch_bounds__(kBitsThreads)
-k_bits_count(const uint32_t* __restrict__ bits, int64_t nw, int64_t* __restrict__ counts) {
-  __shared__ int64_t red[kBitsThreads / 32];
-  const uint32_t* row = bits + (int64_t)blockIdx.x * nw;
-  int64_t c = 0;
-  for (int64_t i = threadIdx.x; i < nw; i += kBitsThreads) c += __popc(row[i]);
-  c = block_sum64(c, red);
-  if (threadIdx.x == 0) counts[blockIdx.x] = c;
-}
-__global__ void k_offsets_head(int64_t* offsets) { offsets[0] = 0; }
-__global__ void __launch_bounds__(kBitsThreads)
-k_bits_emit(uint32_t* __restrict__ bits, int64_t nw, int b, const int64_t* __restrict__ offsets,
-            int64_t capacity, int32_t* __restrict__ out) {
-  __shared__ int wsum[kBitsThreads / 32];
-  const int q = blockIdx.x;
-  const bool fits = offsets[b] <= capacity;  // ids only when all of them fit (as the sorted-key path)
-  int64_t base = offsets[q];
-  if (offsets[q + 1] == base) return;
-  uint32_t* row = bits + (int64_t)q * nw;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int64_t i0 = 0; i0 < nw; i0 += kBitsThreads) {
-    const int64_t i = i0 + threadIdx.x;
-    uint32_t w = i < nw ? row[i] : 0u;
-    if (w) row[i] = 0u;
-    if (!fits) continue;  // (CTA-uniform: no barrier is skipped by part of the CTA)
-    const int c = __popc(w);
-    int incl = c;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int x = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += x;
+k_bits_emit(uint32_t* __restrict__ bits, int64_t nw, int b, int64_t nchunk_total, const int64_t* __restrict__ counts,
+            const int64_t* __restrict__ chunk_off, int64_t capacity, int64_t* __restrict__ offsets,
+            int32_t* __restrict__ out) {
+  const int64_t g = (blockIdx.x * (int64_t)kBitsThreads + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= nchunk_total) return;
+  const int64_t per_row = (nw + kChunkWords - 1) / kChunkWords;
+  const int64_t q = g / per_row, c = g - q * per_row;
+  const int64_t total = chunk_off[nchunk_total - 1] + counts[nchunk_total - 1];
+  const bool fits = total <= capacity;  // ids only when all of them fit (as the sorted-key path)
+  const int64_t base = chunk_off[g];
+  if (lane == 0) {
+    if (c == 0) offsets[q] = base;
+    if (g == nchunk_total - 1) offsets[b] = total;
+  }
+  if (counts[g] == 0) return;  // (warp-uniform) nothing set in this chunk
+  uint32_t* row = bits + q * nw;
+  const int64_t w0 = c * kChunkWords + 32 * lane;
+  uint32_t wv[32];
+  int cnt = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    wv[j] = w0 + j < nw ? row[w0 + j] : 0u;
+    cnt += __popc(wv[j]);
+  }
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  int64_t pos = base + incl - cnt;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    uint32_t w = wv[j];
+    if (w) {
+      row[w0 + j] = 0u;
+      if (fits) {
+        const int32_t u0 = (int32_t)((w0 + j) * 32);
+        while (w) {
+          const int bit = __ffs(w) - 1;
+          w &= w - 1;
+          out[pos++] = u0 + bit;
+        }
+      }
     }
-    if (lane == 31) wsum[wid] = incl;
-    __syncthreads();
-    int before = 0, total = 0;
-    for (int v = 0; v < kBitsThreads / 32; ++v) {
-      before += v < wid ? wsum[v] : 0;
-      total += wsum[v];
-    }
-    int64_t pos = base + before + incl - c;
-    while (w) {
-      const int j = __ffs(w) - 1;
-      w &= w - 1;
-      out[pos++] = (int32_t)(i * 32 + j);
-    }
-    base += total;
-    __syncthreads();
   }
 }
 
-size_t query_scan_bytes(int b) {
+size_t query_scan_bytes(int64_t items) {
   size_t a = 0;
-  cub::DeviceScan::InclusiveSum((void*)nullptr, a, (const int64_t*)nullptr, (int64_t*)nullptr, b);
+  cub::DeviceScan::ExclusiveSum((void*)nullptr, a, (const int64_t*)nullptr, (int64_t*)nullptr, (int)items);
   return a;
 }
+int64_t query_bits_chunks(int b, int64_t nw) { return (int64_t)b * ((nw + kChunkWords - 1) / kChunkWords); }
 
 cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st) {
+  const int64_t nch = query_bits_chunks(c.b, c.nw);
   int64_t* counts = reinterpret_cast<int64_t*>(c.acc_sorted);  // the sort's space is unused on this path
-  k_bits_count<<<c.b, kBitsThreads, 0, st>>>(c.bits, c.nw, counts); count_launch();
-  k_offsets_head<<<1, 1, 0, st>>>(offsets); count_launch();
+  int64_t* chunk_off = counts + nch;
+  const unsigned grid = (unsigned)((nch * 32 + kBitsThreads - 1) / kBitsThreads);
+  k_bits_count<<<grid, kBitsThreads, 0, st>>>(c.bits, c.nw, nch, counts); count_launch();
   size_t tb = c.cub_bytes;
-  cudaError_t e = cub::DeviceScan::InclusiveSum(c.cub_tmp, tb, counts, offsets + 1, c.b, st);
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(c.cub_tmp, tb, counts, chunk_off, (int)nch, st);
   count_launch(2);
   if (e != cudaSuccess) return e;
-  k_bits_emit<<<c.b, kBitsThreads, 0, st>>>(c.bits, c.nw, c.b, offsets, capacity, user_ids); count_launch();
+  k_bits_emit<<<grid, kBitsThreads, 0, st>>>(c.bits, c.nw, c.b, nch, counts, chunk_off, capacity, offsets, user_ids);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -22,7 +22,8 @@ P = torch.from_numpy(w.P).cuda()
 Q = torch.from_numpy(w.Qy).cuda()
 for _ in range(a.steps):
     idx = rmips.rmips_build_index(U, P, w.spec.k_max, rmips.RMIPS_BUILD_SIMT if a.simt else 0)
-    off, ids = rmips.rmips_query(idx, Q, w.spec.ks[0], a.qflags)
+    for b0 in range(0, Q.shape[0], w.spec.batch):  # the bench's query calls (configs[4]: 40 of 256)
+        off, ids = rmips.rmips_query(idx, Q[b0:b0 + w.spec.batch], w.spec.ks[-1], a.qflags)
     idx.close()
 torch.cuda.synchronize()
 print("ok", int(ids.numel()))

@@ -1,5 +1,7 @@
 """Development timing of one build shape (synthetic cfg4 recipe, custom n / m / d): median contraction
-and build times over a few builds.  Usage: python tools/time_build.py n m d [k_max] [reps]"""
+and build times over a few builds.  Usage: python tools/time_build.py n m d [k_max] [reps]
+Set RMIPS_LIB to librmips_dev.so to use the RMIPS_DEV experiment switches (RMIPS_NOFEED, RMIPS_EPI_SKIP,
+RMIPS_NO_CS, ...)."""
 import os
 import sys
 
@@ -23,5 +25,9 @@ for r in range(reps + 1):
     if r:
         ts.append((pt[1], pt[3], idx.tiles_done))
     idx.close()
-print("n %d m %d d %d: contraction %.3f ms build %.3f ms tiles %d" % (n, m, d, np.median([t[0] for t in ts]),
-                                                                 np.median([t[1] for t in ts]), ts[-1][2]))
+c = float(np.median([t[0] for t in ts]))
+tiles = ts[-1][2]
+kst = 16 * ((d + 15) // 16)
+print("%s n %d m %d d %d: contraction %.3f ms build %.3f ms tiles %d  -> %.1f TFLOP/s (MMA K=%d), %.0f ns/tile/SM"
+      % (os.environ.get("TAG", ""), n, m, d, c, float(np.median([t[1] for t in ts])), tiles,
+         2.0 * tiles * 128 * 128 * kst / (c / 1e3) / 1e12, kst, c * 1e6 * 148 / max(1, tiles)))
