@@ -511,7 +511,7 @@ def main():
             "vs_baseline": None, "dtype": "fp16 filter (fp32 accumulate) + f64 exact decisions",
             "data": "synthetic (SURVEY Appendix C generator, seed 0; users seed = rank); stands in for the paper's "
                     "MF vectors (P:571-587), configs[4] is beyond the paper"}
-    for key in ("config", "build", "query", "roofline", "roofline_query", "roofline_scan", "index", "clocks",
+    for key in ("step_ms", "host_ms", "config", "build", "query", "roofline", "roofline_query", "roofline_scan", "index", "clocks",
                 "gpu_launches", "e2e", "cpu_baseline", "parity"):
         if key in head:
             line[key] = head[key]
@@ -520,7 +520,7 @@ def main():
         if c == args.config:
             continue
         r = run_config(c, args, dev, rank, ws, args.extra_steps, 3, pusers(c), e2e=False, cpu=False)
-        extras["cfg%d" % c] = {kk: r[kk] for kk in ("value", "ms_per_step", "config", "build", "query", "roofline",
+        extras["cfg%d" % c] = {kk: r[kk] for kk in ("value", "ms_per_step", "step_ms", "host_ms", "config", "build", "query", "roofline",
                                                     "roofline_query", "clocks", "parity") if kk in r}
         if c == 2 and args.k == 0:  # configs[2] sweeps k over {1, 5, 10, 25, 50}: the other k values
             from synth.generator import CONFIGS

@@ -298,6 +298,7 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
   x->n = n; x->m = m; x->d = d; x->kmax = k_max; x->build_flags = build_flags;
   x->mprime = m_prime < m ? m_prime : m;
   x->dpad = round_up(d, 64);
+  x->ldh = round_up(d, 16);
   x->pd = round_up(d, 8);
   x->nblocks = (n + kTileU - 1) / kTileU;
   x->c1 = filter_c1(x->dpad);
@@ -314,8 +315,8 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
     const size_t o_flags = ia.take<int>(4), o_ctr = ia.take<unsigned long long>(kNumCounters + 4),
                  o_pu = ia.take<int32_t>(n), o_pp = ia.take<int32_t>(m), o_un = ia.take<double>(n),
                  o_unu = ia.take<float>(n), o_pn = ia.take<double>(m), o_perr = ia.take<float>(m),
-                 o_u16 = ia.take<__half>(n * x->dpad), o_u32 = ia.take<float>(n * d),
-                 o_p16 = ia.take<__half>(m * x->dpad), o_p32 = ia.take<float>(m * x->pd),
+                 o_u16 = ia.take<__half>(n * x->ldh), o_u32 = ia.take<float>(n * d),
+                 o_p16 = ia.take<__half>(m * x->ldh), o_p32 = ia.take<float>(m * x->pd),
                  o_tau = ia.take<double>((int64_t)k_max * n), o_ids = ia.take<int32_t>((int64_t)k_max * n),
                  o_thr = ia.take<float>((int64_t)k_max * n), o_tb = ia.take<float>((int64_t)k_max * x->nblocks);
     CK(cudaMallocAsync(&x->arena, ia.off, st));
@@ -459,7 +460,7 @@ rmips_status_t rmips_build_index_host(const float* Q, int64_t n, const float* P,
 constexpr size_t kBitsMaxBytes = (size_t)64 << 20;  // largest bit-matrix output (rmips.h)
 
 static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cudaStream_t st) {
-  const int dpad = x->dpad;
+  const int ldh = x->ldh;
   // accepted pairs as a bit matrix when it is small enough (no key sort, no mid-call sync)
   const int64_t nw = (x->n + 31) / 32;
   const int64_t nch = query_bits_chunks(c.b, nw);  // its output pass keeps 2 nch int64 in acc_sorted's space
@@ -471,7 +472,7 @@ static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cuda
                         c.b <= cap;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
-  size_t oQ16 = take((size_t)nsub * kQB * dpad * 2), oqn = take((size_t)nsub * kQB * 4),
+  size_t oQ16 = take((size_t)nsub * kQB * ldh * 2), oqn = take((size_t)nsub * kQB * 4),
          oqe = take((size_t)nsub * kQB * 4), oqs = take((size_t)nsub * 4), oqp = take((size_t)nsub * kQB * 4),
          oqc = take((size_t)nsub * 4), owl = take((size_t)nsub * x->nblocks * 4), oacc = take((size_t)cap * 8),
          ound = take((size_t)cap * 8), oscn = take((size_t)cap * 4),

@@ -87,7 +87,7 @@ __global__ void k_split_sorted(const uint64_t* __restrict__ keys, const int32_t*
 // scattered: 0.68 / 0.52 ms on configs[3]); lane l handles the column pairs 2l, 2l + 64, ...
 // keys_u[o] = bits of ||u_o|| (the sort's input keys: the same fp64 value as the sorted norms).
 constexpr int kPrepRows = 8;
-__global__ void k_prep_users(const float* __restrict__ Q, int64_t n, int d, int dpad,
+__global__ void k_prep_users(const float* __restrict__ Q, int64_t n, int d, int ldh,
                              const int32_t* __restrict__ inv_u, const uint64_t* __restrict__ keys_u,
                              __half* __restrict__ U16, float* __restrict__ U32, float* __restrict__ unu) {
   const int64_t o0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * kPrepRows;
@@ -106,7 +106,7 @@ __global__ void k_prep_users(const float* __restrict__ Q, int64_t n, int d, int 
     else if (!(nu_l > 0.f)) nu_l = 1.f;
     unu[r_l] = nu_l;
   }
-  for (int j = 2 * lane; j < dpad; j += 64) {
+  for (int j = 2 * lane; j < ldh; j += 64) {
     float x0[kPrepRows], x1[kPrepRows];
 #pragma unroll
     for (int i = 0; i < kPrepRows; ++i) {
@@ -120,7 +120,7 @@ __global__ void k_prep_users(const float* __restrict__ Q, int64_t n, int d, int 
       const float nu = __shfl_sync(0xffffffffu, nu_l, i);
       const int64_t r = __shfl_sync(0xffffffffu, r_l, i);
       if (o0 + i < n) {
-        reinterpret_cast<__half2*>(U16 + r * dpad)[j >> 1] =
+        reinterpret_cast<__half2*>(U16 + r * ldh)[j >> 1] =
             __halves2half2(__float2half_rn(x0[i] / nu), __float2half_rn(x1[i] / nu));
         if (j < d) U32[r * d + j] = x0[i];
         if (j + 1 < d) U32[r * d + j + 1] = x1[i];
@@ -130,8 +130,8 @@ __global__ void k_prep_users(const float* __restrict__ Q, int64_t n, int d, int 
 }
 
 // Items: P16 = fp16(p * 2^e) with max|p*2^e| < 2^14; perr = filter error bound (scaled units).
-// One warp per row as above; P32 is zero-padded to pd (a multiple of 8, <= dpad).
-__global__ void k_prep_items(const float* __restrict__ P, int64_t m, int d, int dpad, int pd,
+// One warp per row as above; P32 is zero-padded to pd (a multiple of 8, <= ldh).
+__global__ void k_prep_items(const float* __restrict__ P, int64_t m, int d, int ldh, int pd,
                              const int32_t* __restrict__ perm, const double* __restrict__ norm_sorted,
                              const unsigned int* __restrict__ maxabs_bits, double c1, double c2,
                              __half* __restrict__ P16, float* __restrict__ P32, float* __restrict__ perr,
@@ -148,9 +148,9 @@ __global__ void k_prep_items(const float* __restrict__ P, int64_t m, int d, int 
   const int64_t o = perm[r];
   const float* p = P + o * d;
 #pragma unroll 4
-  for (int j = 2 * lane; j < dpad; j += 64) {
+  for (int j = 2 * lane; j < ldh; j += 64) {
     const float x0 = j < d ? p[j] : 0.f, x1 = j + 1 < d ? p[j + 1] : 0.f;
-    reinterpret_cast<__half2*>(P16 + r * dpad)[j >> 1] = __halves2half2(__float2half_rn(x0 * scale), __float2half_rn(x1 * scale));
+    reinterpret_cast<__half2*>(P16 + r * ldh)[j >> 1] = __halves2half2(__float2half_rn(x0 * scale), __float2half_rn(x1 * scale));
     if (j < pd) P32[r * pd + j] = x0;
     if (j + 1 < pd) P32[r * pd + j + 1] = x1;
   }
@@ -168,7 +168,7 @@ __global__ void k_prep_items(const float* __restrict__ P, int64_t m, int d, int 
 template <int DPAD>
 __global__ void __launch_bounds__(128, 1)
 k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, const float* __restrict__ perr,
-             int64_t n, int64_t m, int kmax, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
+             int ldh, int64_t n, int64_t m, int kmax, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
              int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const CandSmem sm = CandSmem::at(smem_raw);                               // candidate buffers
@@ -183,7 +183,7 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
     int r = i / (DPAD / 2), k2 = i % (DPAD / 2);
     int64_t gr = blockIdx.x * (int64_t)128 + r;
     __half2 v = __floats2half2_rn(0.f, 0.f);
-    if (gr < n) v = reinterpret_cast<const __half2*>(U16)[gr * (DPAD / 2) + k2];
+    if (gr < n && 2 * k2 < ldh) v = reinterpret_cast<const __half2*>(U16)[gr * (ldh / 2) + k2];
     us[k2 * 128 + r] = v;
   }
   CandRow me = cand_init(live);
@@ -194,7 +194,7 @@ k_build_simt(const __half* __restrict__ U16, const __half* __restrict__ P16, con
     for (int i = tid; i < 32 * DPAD; i += 128) {
       int jj = i / DPAD, k = i % DPAD;
       __half v = __float2half_rn(0.f);
-      if (base + jj < m) v = P16[(base + jj) * DPAD + k];
+      if (base + jj < m && k < ldh) v = P16[(base + jj) * ldh + k];
       ps[k * 32 + jj] = v;
     }
     __syncthreads();
@@ -663,7 +663,7 @@ static cudaError_t launch_build_simt(const BuildCtx& c, cudaStream_t st) {
   size_t smem = (size_t)kCandSmemBytes + (DPAD / 2) * 128 * 4 + DPAD * 32 * 2;
   cudaError_t e = cudaFuncSetAttribute(k_build_simt<DPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_build_simt<DPAD><<<nblk(c.idx->n, 128), 128, smem, st>>>(c.idx->U16, c.idx->P16, c.idx->perr, c.idx->n,
+  k_build_simt<DPAD><<<nblk(c.idx->n, 128), 128, smem, st>>>(c.idx->U16, c.idx->P16, c.idx->perr, c.idx->ldh, c.idx->n,
                                                              c.mb, c.idx->kmax, c.cand, c.ccount,
                                                              c.ovf_list, c.ovf_count); count_launch();
   return cudaGetLastError();
@@ -814,7 +814,7 @@ cudaError_t zero4(cudaStream_t st, void* a, int na, void* b, int nb, void* c, in
 cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   const int64_t n = x->n, m = x->m;
-  const int d = x->d, dpad = x->dpad;
+  const int d = x->d, ldh = x->ldh;
   // B1: norms as sort keys of one concatenated [items | users] sequence (items carry the top
   // bit, so a descending sort puts them first); non-finite check; max |p_j|
   const int64_t tot = m + n;
@@ -858,9 +858,9 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
   count_launch();
   // B3
   if (n)
-    k_prep_users<<<nblk((n + kPrepRows - 1) / kPrepRows * 32, 256), 256, 0, st>>>(Q, n, d, dpad, c.inv_u, kin + m, x->U16,
+    k_prep_users<<<nblk((n + kPrepRows - 1) / kPrepRows * 32, 256), 256, 0, st>>>(Q, n, d, ldh, c.inv_u, kin + m, x->U16,
                                                                                x->U32, x->unu); count_launch();
-  k_prep_items<<<nblk(m * 32, 256), 256, 0, st>>>(P, m, d, dpad, x->pd, x->perm_p, x->pnorm, c.maxabs, x->c1, x->c2,
+  k_prep_items<<<nblk(m * 32, 256), 256, 0, st>>>(P, m, d, ldh, x->pd, x->perm_p, x->pnorm, c.maxabs, x->c1, x->c2,
                                                     x->P16, x->P32, x->perr, c.scale_dev); count_launch();
   sort_graph_put(sg, st);  // last use of the sort buffers (kin) is enqueued
   return cudaGetLastError();

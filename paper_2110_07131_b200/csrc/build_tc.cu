@@ -460,8 +460,8 @@ template <int KB>
 static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   CUtensorMap ta, tb;
-  if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM)) return cudaErrorNotSupported;
-  if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->dpad, kBN)) return cudaErrorNotSupported;
+  if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->ldh, kBM)) return cudaErrorNotSupported;
+  if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->ldh, kBN)) return cudaErrorNotSupported;
   const int smem = Smem::TOTAL(KB);
   cudaError_t e = cudaFuncSetAttribute(k_build_tc<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

@@ -437,10 +437,10 @@ static cudaError_t launch_tcq(const BuildCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   const int tail = tail_cols(x->d);
   CUtensorMap ta, tat, tb, tbt;
-  if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM) ||
-      !make_tmap_f16_box(&tat, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM, tail) ||
-      !make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->dpad, C::BN) ||
-      !make_tmap_f16_box(&tbt, x->P16, (uint64_t)c.mb, (uint64_t)x->dpad, C::BN, tail))
+  if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->ldh, kBM) ||
+      !make_tmap_f16_box(&tat, x->U16, (uint64_t)x->n, (uint64_t)x->ldh, kBM, tail) ||
+      !make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->ldh, C::BN) ||
+      !make_tmap_f16_box(&tbt, x->P16, (uint64_t)c.mb, (uint64_t)x->ldh, C::BN, tail))
     return cudaErrorNotSupported;
   cudaError_t e = cudaFuncSetAttribute(k_build_tcq<KB, Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
   if (e != cudaSuccess) return e;

@@ -143,6 +143,9 @@ struct rmips_index_s {
   int64_t mprime = 0;       // items the top-k_max lists are built over: the first mprime of the
                             // norm-sorted P (Alg. 1 line 6); mprime = m is the exact index
   int d = 0, dpad = 0, kmax = 0, build_flags = 0;
+  int ldh = 0;              // row stride of U16 / P16 / Q16 in halves: d rounded up to 16 (whole 32-byte
+                            // sectors, so a row streams 2 ldh bytes; TMA boxes past it are zero-filled);
+                            // dpad = d rounded up to 64 is the K-block geometry of the kernels
   int pd = 0;               // P32 row pitch in floats: d rounded up to 8 (whole 32-byte sectors)
   int device = 0;
   int64_t nblocks = 0;
@@ -161,9 +164,9 @@ struct rmips_index_s {
   float* unu = nullptr;        // [n] nu = fp32 scale used to unit-normalise the fp16 user rows
   double* pnorm = nullptr;     // [m] ||p|| fp64 (sorted order)
   float* perr = nullptr;       // [m] filter error bound of item p in scaled score units
-  __half* U16 = nullptr;       // [n][dpad] fp16 u/nu (sorted)
+  __half* U16 = nullptr;       // [n][ldh] fp16 u/nu (sorted)
   float* U32 = nullptr;        // [n][d] fp32 u (sorted) -- exact path
-  __half* P16 = nullptr;       // [m][dpad] fp16 p*2^e (sorted)
+  __half* P16 = nullptr;       // [m][ldh] fp16 p*2^e (sorted)
   float* P32 = nullptr;        // [m][pd] fp32 p (sorted, zero-padded rows) -- exact path
 
   // exact lower-bound arrays (Def. 4), column-major by rank: x[j*n + u]

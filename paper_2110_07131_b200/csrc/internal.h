@@ -57,7 +57,7 @@ struct QueryCtx {
   int b = 0, k = 0, flags = 0;
   int nsub = 0;                  // sub-batches of kQB queries
   // per sub-batch, sorted by norm descending (Alg. 3 line 1 computes ||q||)
-  __half* Q16 = nullptr;         // [nsub][kQB][dpad] fp16 q*2^eq (sorted)
+  __half* Q16 = nullptr;         // [nsub][kQB][ldh] fp16 q*2^eq (sorted)
   float* qn = nullptr;           // [nsub][kQB] ||q|| rounded up (sorted; -1 padding)
   float* qerr = nullptr;         // [nsub][kQB] filter error bound, scaled units
   float* qscale = nullptr;       // [nsub] 2^eq

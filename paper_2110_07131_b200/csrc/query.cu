@@ -21,7 +21,7 @@ namespace rmips {
 // threads write the fp16 rows (q * 2^eq, zero-padded to d_pad) element-parallel.
 constexpr int kPrepThreads = 1024;
 __global__ void __launch_bounds__(kPrepThreads)
-k_query_prep(const float* __restrict__ q, int b, int d, int dpad, double c1, double c2, __half* __restrict__ Q16,
+k_query_prep(const float* __restrict__ q, int b, int d, int ldh, double c1, double c2, __half* __restrict__ Q16,
              float* __restrict__ qn, float* __restrict__ qerr, float* __restrict__ qscale,
              int32_t* __restrict__ qperm, int32_t* __restrict__ qcount, int* __restrict__ flags) {
   __shared__ double nrm[kQB];
@@ -93,8 +93,8 @@ k_query_prep(const float* __restrict__ q, int b, int d, int dpad, double c1, dou
       qerr[slot] = 0.f;
     }
   }
-  // fp16 rows, two elements per thread per step (half2 stores; dpad is even)
-  const int hp = dpad / 2;
+  // fp16 rows, two elements per thread per step (half2 stores; ldh is a multiple of 16)
+  const int hp = ldh / 2;
   for (int idx = t; idx < kQB * hp; idx += kPrepThreads) {
     const int src = idx / hp, e = 2 * (idx - src * hp);
     const int64_t slot = (int64_t)s * kQB + srank[src];
@@ -104,7 +104,7 @@ k_query_prep(const float* __restrict__ q, int b, int d, int dpad, double c1, dou
       if (e < d) v0 = x[e] * scale;
       if (e + 1 < d) v1 = x[e + 1] * scale;
     }
-    reinterpret_cast<__half2*>(Q16 + slot * dpad)[e >> 1] = __halves2half2(__float2half_rn(v0), __float2half_rn(v1));
+    reinterpret_cast<__half2*>(Q16 + slot * ldh)[e >> 1] = __halves2half2(__float2half_rn(v0), __float2half_rn(v1));
   }
 }
 
@@ -132,7 +132,7 @@ __device__ __forceinline__ int classify(float acc, float thr_s, float qe) {
 // ------------------------------------------------------------------------------ Q2 + Q3 (SIMT)
 template <int DPAD>
 __global__ void __launch_bounds__(128)
-k_query_simt(const __half* __restrict__ U16, const float* __restrict__ thrk, const float* __restrict__ tbk,
+k_query_simt(const __half* __restrict__ U16, int ldh, const float* __restrict__ thrk, const float* __restrict__ tbk,
              const int32_t* __restrict__ perm_u, int64_t n, const __half* __restrict__ Q16,
              const float* __restrict__ qn, const float* __restrict__ qerr, const float* __restrict__ qscale,
              const int32_t* __restrict__ qperm, const int32_t* __restrict__ qcount, int flags,
@@ -161,11 +161,14 @@ k_query_simt(const __half* __restrict__ U16, const float* __restrict__ thrk, con
   for (int i = tid; i < 128 * (DPAD / 2); i += 128) {
     int r = i / (DPAD / 2), k2 = i % (DPAD / 2);
     int64_t gr = (int64_t)tile * 128 + r;
-    us[k2 * 128 + r] = gr < n ? reinterpret_cast<const __half2*>(U16)[gr * (DPAD / 2) + k2]
-                              : __floats2half2_rn(0.f, 0.f);
+    us[k2 * 128 + r] = gr < n && 2 * k2 < ldh ? reinterpret_cast<const __half2*>(U16)[gr * (ldh / 2) + k2]
+                                              : __floats2half2_rn(0.f, 0.f);
   }
-  const __half2* qsrc = reinterpret_cast<const __half2*>(Q16) + (int64_t)s * kQB * (DPAD / 2);
-  for (int i = tid; i < len * (DPAD / 2); i += 128) qs[i] = qsrc[i];
+  const __half2* qsrc = reinterpret_cast<const __half2*>(Q16) + (int64_t)s * kQB * (ldh / 2);
+  for (int i = tid; i < len * (DPAD / 2); i += 128) {
+    const int qr = i / (DPAD / 2), k2 = i - qr * (DPAD / 2);
+    qs[i] = 2 * k2 < ldh ? qsrc[qr * (ldh / 2) + k2] : __floats2half2_rn(0.f, 0.f);
+  }
   __syncthreads();
   const float sc = qscale[s];
   const float thr_s = live ? thrk[row] * sc : 0.f;
@@ -405,7 +408,7 @@ static inline unsigned nblk(int64_t work, int t) { return (unsigned)((work + t -
 
 cudaError_t query_prep(QueryCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
-  k_query_prep<<<c.nsub, kPrepThreads, 0, st>>>(c.q, c.b, x->d, x->dpad, x->c1, x->c2, c.Q16, c.qn, c.qerr, c.qscale, c.qperm,
+  k_query_prep<<<c.nsub, kPrepThreads, 0, st>>>(c.q, c.b, x->d, x->ldh, x->c1, x->c2, c.Q16, c.qn, c.qerr, c.qscale, c.qperm,
                                        c.qcount, c.flags_dev); count_launch();
   return cudaGetLastError();
 }
@@ -417,7 +420,7 @@ static cudaError_t launch_query_simt(QueryCtx& c, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(k_query_simt<DPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)x->nblocks, (unsigned)c.nsub);
-  k_query_simt<DPAD><<<grid, 128, smem, st>>>(x->U16, x->thr + (int64_t)(c.k - 1) * x->n,
+  k_query_simt<DPAD><<<grid, 128, smem, st>>>(x->U16, x->ldh, x->thr + (int64_t)(c.k - 1) * x->n,
                                               x->tb + (int64_t)(c.k - 1) * x->nblocks, x->perm_u, x->n, c.Q16, c.qn,
                                               c.qerr, c.qscale, c.qperm, c.qcount, c.flags, c.counters, AccSink{c.acc, c.bits, c.nw}, c.und,
                                               c.cap); count_launch();

@@ -526,10 +526,10 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   const int tail = tail_cols(x->d);
   CUtensorMap tu, tut, tq, tqt;
-  if (!make_tmap_f16_box(&tu, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM) ||
-      !make_tmap_f16_box(&tut, x->U16, (uint64_t)x->n, (uint64_t)x->dpad, kBM, tail) ||
-      !make_tmap_f16_box(&tq, c.Q16, (uint64_t)c.nsub * kQB, (uint64_t)x->dpad, kQB) ||
-      !make_tmap_f16_box(&tqt, c.Q16, (uint64_t)c.nsub * kQB, (uint64_t)x->dpad, kQB, tail))
+  if (!make_tmap_f16_box(&tu, x->U16, (uint64_t)x->n, (uint64_t)x->ldh, kBM) ||
+      !make_tmap_f16_box(&tut, x->U16, (uint64_t)x->n, (uint64_t)x->ldh, kBM, tail) ||
+      !make_tmap_f16_box(&tq, c.Q16, (uint64_t)c.nsub * kQB, (uint64_t)x->ldh, kQB) ||
+      !make_tmap_f16_box(&tqt, c.Q16, (uint64_t)c.nsub * kQB, (uint64_t)x->ldh, kQB, tail))
     return cudaErrorNotSupported;
   const int smem = QSmem::TOTAL(KB);
   cudaError_t e = cudaFuncSetAttribute(k_query_tc<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
