@@ -82,7 +82,11 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
-            time.sleep(0.3)  # the first samples land before the timed region starts
+            # nvidia-smi's start-up (NVML initialisation) can stall CUDA work for ~0.2 s: wait for its
+            # first samples so that it happens before the timed region
+            t0 = time.perf_counter()
+            while len(self.lines) < 3 and time.perf_counter() - t0 < 10:
+                time.sleep(0.05)
         except Exception:
             self.proc = None
         return self

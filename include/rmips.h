@@ -172,7 +172,8 @@ RMIPS_API rmips_status_t rmips_query_stats(rmips_index_t idx, rmips_stats_t* out
  *                SIMT build; fewer than all when the Cauchy-Schwarz early exit fired),
  *                m_prime (items the lists are built over; = m for the exact index),
  *                build kernel (0 SIMT, 1 k_build_tc (d <= 64), 2 k_build_tcq with the user tile in
- *                tensor memory, 3 k_build_tcq with streamed user K blocks (d > 256)),
+ *                tensor memory, 3 k_build_tcq with streamed user K blocks (d > 256), 4 k_build_tc2cta
+ *                (CTA pairs, tcgen05.mma.cta_group::2, 64 < d <= 256)),
  *                candidate slots per row (128 or 256);  info[13..15] reserved, 0
  *   perm_u[n], perm_p[m]: sorted position -> original id (norm descending, ties by id)
  *   tau[k_max * n] fp64 and ids[k_max * n] int32: column-major by rank, users in ORIGINAL

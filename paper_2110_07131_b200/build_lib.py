@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "librmips.so")
 BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["abi.cu", "build.cu", "build_tc.cu", "build_tcq.cu", "query.cu", "query_tc.cu"]
+SOURCES = ["abi.cu", "build.cu", "build_tc.cu", "build_tcq.cu", "build_tc2cta.cu", "query.cu", "query_tc.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-DRMIPS_BUILD"]

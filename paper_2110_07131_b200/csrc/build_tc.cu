@@ -496,8 +496,18 @@ cudaError_t build_tc(const BuildCtx& c, cudaStream_t st) {
 #ifdef RMIPS_DEV
   if (getenv("RMIPS_DISABLE_TC")) return cudaErrorNotSupported;
 #endif
-  // d <= 64 with 128-slot lists: this kernel; everything else (d > 64, or k_max > 80 with 256-slot
-  // 4-byte lists): build_tcq.cu
+  // d_pad 128..256 with 128-slot 4-byte lists: CTA pairs (build_tc2cta.cu); d <= 64 with 128-slot
+  // lists: this kernel; everything else (d > 256, m > 2^20 with d > 64, or k_max > 80): build_tcq.cu
+  bool pair = c.idx->dpad > 64;
+#ifdef RMIPS_DEV
+  if (getenv("RMIPS_NO_2CTA")) pair = false;
+  if (getenv("RMIPS_2CTA_D64")) pair = true;
+#endif
+  if (pair) {
+    const cudaError_t e = build_tc2cta(c, st);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();
+  }
   if (c.idx->dpad == 64 && c.cstride == kCand) return launch_tc<1>(c, st);
   return build_tcq(c, st);
 }

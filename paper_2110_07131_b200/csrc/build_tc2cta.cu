@@ -1,0 +1,397 @@
+// build_tc2cta.cu -- B4 over CTA PAIRS: the |Q| x |P| x d contraction of Alg. 1 lines 7-9 (
+// over ALL of P per BASELINE north star) on tcgen05.mma.cta_group::2 (M = 256 users of two SMs,
+// N = 128 items), fused with the per-row top-k_max candidate epilogue (candpol.cuh / epiq.cuh).
+//
+// Why pairs: with one SM per 128-user tile (build_tcq.cu) every byte of an item tile is written into
+// shared memory by TMA and read once by the MMA, 2 x 64 B/clk at the tensor rate -- the SM's whole
+// shared-memory bandwidth.  In a pair each SM holds and feeds HALF of every item tile (64 of its 128
+// rows) and the 2-SM MMA reads both halves, so each SM's shared-memory traffic per flop halves.
+//
+// Cluster of 2 CTAs (rank 0 = leader L, rank 1 = follower F), persistent over user-tile PAIRS: the pair
+// processes user tiles 2 tp + rank against the same item tiles.  Per CTA:
+//   warp 0   TMA producer: the CTA's user tile A (KB K-block units of 128 x 64, last one trimmed to
+//            tail_cols(d)) into its A buffer, and its half of every item tile (KB units of 64 x 64) into
+//            a ring of 8 KB slots; every load completes its bytes on the LEADER's barriers (.cta_group::2)
+//   warp 1   leader only: tcgen05.cp.cta_group::2 of the A tiles into both TMEMs, then one
+//            tcgen05.mma.cta_group::2 chain per item tile (A from TMEM, B halves from both shared
+//            memories), tcgen05.commit multicast to both CTAs' barriers
+//   warps 2-5 epilogue of the CTA's own 128 rows, exactly as build_tcq.cu
+// Early termination (Cauchy-Schwarz) is decided per PAIR: all 8 epilogue warps report to the leader's
+// done counter; the leader's producer decides for every group of kGroup item tiles, one group ahead, and
+// tells the follower's producer (DEC barriers), so both halves of a tile are either loaded or both
+// skipped; the leader ends the user-tile pair with a marker.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "candpol.cuh"
+#include "common.cuh"
+#include "epiq.cuh"
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace rmips {
+namespace {
+
+constexpr int kBM = 128;                 // users per CTA (TMEM lanes)
+constexpr int kAUnit = 128 * 64 * 2;     // one K block of a user tile: 16 KB
+constexpr int kBUnit = 64 * 64 * 2;      // one K block of this CTA's half item tile: 8 KB
+constexpr int kGroup = 4;                // item tiles per end-of-pair decision (the C-S check period)
+
+template <int KB, class Pol>
+struct Cfg2 {
+  static constexpr int BN = 128;                 // items per pair MMA tile (64 rows in each CTA)
+  static constexpr int RING = KB * kAUnit;       // after the A buffer
+  static constexpr int NSB_FIT = (232448 - 3072 - RING - Pol::kBufBytes) / kBUnit;
+  static constexpr int NSB = NSB_FIT < 24 ? NSB_FIT : 24;
+  static constexpr int CAND = RING + NSB * kBUnit;
+  static constexpr int BAR = CAND + Pol::kBufBytes;
+  static constexpr int NACC = 3, ACC_COLS = 128, A_TMEM = NACC * ACC_COLS, TMEM_COLS = 512;
+  static constexpr int THREADS = 192;
+  // barriers R_FULL[NSB] R_EMPTY[NSB] DEC[NSB] ACC_FULL[NACC] ACC_EMPTY[NACC] A_FULL A_EMPTY, then words
+  static constexpr int NBARS = 3 * NSB + 2 * NACC + 2;
+  static constexpr int TOTAL = BAR + NBARS * 8 + (4 + 2 * NSB + NACC) * 4 + 1024;
+  static_assert(KB >= 1 && KB <= 4 && A_TMEM + 32 * KB <= TMEM_COLS, "tensor memory");
+  static_assert(NSB >= 2 * KB && NSB >= 8 && TOTAL <= 232448, "shared memory");
+};
+
+}  // namespace
+
+template <int KB, class Pol>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<KB, Pol>::THREADS, 1)
+k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAt,
+               const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBt,
+               const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
+               int64_t n, int64_t m, int kmax, int ksteps, int tail, int32_t* __restrict__ cand,
+               int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count,
+               unsigned long long* __restrict__ tiles_done) {
+  using namespace sm100;
+  using C = Cfg2<KB, Pol>;
+  constexpr int NSB = C::NSB, NACC = C::NACC, BN = C::BN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sA = sbase, sR = sbase + C::RING;
+  const typename Pol::Buf sb = Pol::buf(smem + C::CAND);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR);
+  const uint32_t bar0 = smem_u32(bars);
+  auto BAR = [&](int i) { return bar0 + 8u * i; };
+  const int R_FULL = 0, R_EMPTY = NSB, DEC = 2 * NSB, ACC_FULL = 3 * NSB, ACC_EMPTY = 3 * NSB + NACC,
+            A_FULL = 3 * NSB + 2 * NACC, A_EMPTY = A_FULL + 1;
+  uint32_t* words = reinterpret_cast<uint32_t*>(bars + C::NBARS);
+  uint32_t* tmem_slot = words;
+  volatile uint32_t* done_cum = words + 1;   // leader: epilogue warps of the pair done with a tile pair (8 each)
+  volatile uint32_t* stage_end = words + 2;  // [NSB] leader: producer -> MMA end marker (t + 1)
+  volatile uint32_t* acc_end = stage_end + NSB;  // [NACC] both: MMA -> epilogue end marker
+  volatile uint32_t* dec = acc_end + NACC;   // [NSB] follower: the leader's decision for an item tile
+  const uint32_t w_done = smem_u32(words + 1), w_acc_end = smem_u32(words + 2 + NSB),
+                 w_dec = smem_u32(words + 2 + NSB + NACC);
+
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_utiles = (int)((n + kBM - 1) / kBM);
+  const int num_tp = (num_utiles + 1) / 2;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int nit = (int)((m + BN - 1) / BN);
+  const uint32_t a_tail_bytes = (uint32_t)(kBM * tail * 2), b_tail_bytes = (uint32_t)(64 * tail * 2);
+  const uint32_t a_bytes = (uint32_t)((KB - 1) * kAUnit) + a_tail_bytes;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    tma_prefetch(&tmAt);
+    tma_prefetch(&tmBt);
+    for (int s = 0; s < NSB; ++s)
+      mbar_init(BAR(R_FULL + s), 1), mbar_init(BAR(R_EMPTY + s), 1), mbar_init(BAR(DEC + s), 1);
+    for (int a = 0; a < NACC; ++a) mbar_init(BAR(ACC_FULL + a), 1), mbar_init(BAR(ACC_EMPTY + a), 8);
+    mbar_init(BAR(A_FULL), 1);
+    mbar_init(BAR(A_EMPTY), 1);
+    *done_cum = 0;
+    for (int s = 0; s < NSB; ++s) stage_end[s] = 0, dec[s] = 0;
+    for (int a = 0; a < NACC; ++a) acc_end[a] = 0;
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc_cg2(smem_u32(tmem_slot), C::TMEM_COLS);
+    tmem_relinquish_cg2();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // both CTAs' barriers exist before any remote arrive or TMA completion
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  auto L = [&](uint32_t a) { return mapa_shared(a, 0); };  // the leader's copy of a shared address
+  auto F = [&](uint32_t a) { return mapa_shared(a, 1); };  // the follower's
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0, decph = 0;  // ring phase; per-slot DEC phase bits
+      int t = 0;
+      auto next = [&]() {
+        if (++stage == NSB) stage = 0, ph ^= 1;
+      };
+      for (int tp = pair; tp < num_tp; tp += npairs, ++t) {
+        const int ut = 2 * tp + (int)rank;  // (the follower of an odd last pair reads rows >= n: zero fill)
+        mbar_wait_sleep(BAR(A_EMPTY), (t & 1) ^ 1);
+        if (leader) mbar_arrive_expect_tx(BAR(A_FULL), 2 * a_bytes);
+        for (int kb = 0; kb < KB; ++kb)
+          tma_load_2d_cg2(sA + kb * kAUnit, kb == KB - 1 ? &tmAt : &tmA, kb * 64, ut * kBM, L(BAR(A_FULL)));
+        // Item tiles go in groups of kGroup.  At the start of group g the leader decides whether group
+        // g + 1 is issued (every epilogue warp of the pair done -> the pair ends there) and sends that
+        // decision to the follower a whole group AHEAD, so the follower's wait for it is off the feed's
+        // critical path; group 0 is always issued.  (At most two groups of tiles follow the last
+        // report; the epilogue drains them unread.)
+        bool end_next = false;
+        for (int it = 0; it < nit; ++it) {
+          if (it % kGroup == 0) {
+            const int g = it / kGroup;
+            bool end = false;
+            if (leader) {
+              end = end_next;
+              if (end) {
+                mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
+                stage_end[stage] = t + 1;
+                mbar_arrive(BAR(R_FULL + stage));  // the marker (no bytes) for the MMA warp
+              } else if ((g + 1) * kGroup < nit) {
+                end_next = *done_cum >= 8u * (uint32_t)(t + 1);  // every epilogue warp of the pair is done
+                st_cluster_u32(F(w_dec + 4 * ((g + 1) & 7)), end_next ? 1u : 0u);
+                mbar_arrive_cluster(F(BAR(DEC + ((g + 1) & 7))));
+              }
+            } else if (g > 0) {
+              // (8 decision barriers: the leader runs at most NSB <= 24 units, i.e. fewer than 8 groups,
+              // ahead of the follower, so a barrier never advances twice before the follower's wait)
+              mbar_wait_cluster(BAR(DEC + (g & 7)), (decph >> (g & 7)) & 1u);
+              decph ^= 1u << (g & 7);
+              end = dec[g & 7] != 0;
+            }
+            if (end) {
+              next();
+              break;
+            }
+          }
+          for (int kb = 0; kb < KB; ++kb) {
+            mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
+            const bool last = kb == KB - 1;
+            if (leader) mbar_arrive_expect_tx(BAR(R_FULL + stage), 2 * (last ? b_tail_bytes : (uint32_t)kBUnit));
+            tma_load_2d_cg2(sR + stage * kBUnit, last ? &tmBt : &tmB, kb * 64, it * BN + 64 * (int)rank,
+                            L(BAR(R_FULL + stage)));
+            next();
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA warp (leader only)
+    if (leader) {
+      constexpr uint32_t idesc = idesc_f16_f32(2 * kBM, BN);
+      unsigned long long tiles_issued = 0;
+      int stage = 0, as = 0;
+      uint32_t ph = 0, aph = 0;
+      int t = 0;
+      auto next = [&]() {
+        if (++stage == NSB) stage = 0, ph ^= 1;
+      };
+      auto bdesc_of = [&](int kb) {
+        const uint32_t a = sR + stage * kBUnit;
+        return kb == KB - 1 ? sdesc_swz(a, 2 * tail) : sdesc_sw128(a);
+      };
+      for (int tp = pair; tp < num_tp; tp += npairs, ++t) {
+        mbar_wait_sleep(BAR(A_FULL), t & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kb = 0; kb < KB; ++kb) {
+            const uint32_t a = sA + kb * kAUnit;
+            const uint64_t adesc = kb == KB - 1 ? sdesc_swz(a, 2 * tail) : sdesc_sw128(a);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              if (4 * kb + kk < ksteps)
+                tmem_cp_128x256b_cg2(tmem + C::A_TMEM + 8 * (4 * kb + kk), adesc + (uint64_t)(2 * kk));
+          }
+          mma_commit_cg2(BAR(A_EMPTY), 3);  // both A buffers are free once the copies completed
+        }
+        __syncwarp();
+        for (int it = 0; it < nit; ++it) {
+          mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
+          mbar_wait_sleep(BAR(R_FULL + stage), ph);
+          tc_fence_after();
+          if (stage_end[stage] == (uint32_t)(t + 1)) {  // the producer ended this tile pair: forward
+            if (elect_one()) {
+              mbar_arrive(BAR(R_EMPTY + stage));
+              mbar_arrive_cluster(F(BAR(R_EMPTY + stage)));
+              acc_end[as] = t + 1;
+              st_cluster_u32(F(w_acc_end + 4 * as), (uint32_t)(t + 1));
+              mbar_arrive(BAR(ACC_FULL + as));
+              mbar_arrive_cluster(F(BAR(ACC_FULL + as)));
+            }
+            __syncwarp();
+            next();
+            if (++as == NACC) as = 0, aph ^= 1;
+            break;
+          }
+          const uint32_t d = tmem + as * C::ACC_COLS;
+          for (int kb = 0; kb < KB; ++kb) {
+            if (kb > 0) {
+              mbar_wait_sleep(BAR(R_FULL + stage), ph);
+              tc_fence_after();
+            }
+            if (elect_one()) {
+              const uint64_t bdesc = bdesc_of(kb);
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                if (4 * kb + kk < ksteps)
+                  mma_f16_ts_cg2(d, tmem + C::A_TMEM + 8 * (4 * kb + kk), bdesc + (uint64_t)(2 * kk), idesc,
+                                 (kb | kk) != 0);
+              mma_commit_cg2(BAR(R_EMPTY + stage), 3);
+            }
+            __syncwarp();
+            next();
+          }
+          if (elect_one()) mma_commit_cg2(BAR(ACC_FULL + as), 3);
+          __syncwarp();
+          tiles_issued += 2;  // two 128 x 128 (user tile, item tile) contractions
+          if (++as == NACC) as = 0, aph ^= 1;
+        }
+      }
+      if (lane == 0) atomicAdd(tiles_done, tiles_issued);
+    }
+  } else {
+    // ------------------------------------------------ epilogue: one thread per user row (both CTAs)
+    const int q = warp & 3;
+    const int rr = q * 32 + lane;
+    const int mi = (int)m;
+    const float e0x2 = __fadd_ru(__ldg(perr), __ldg(perr));
+    const float smax = __fadd_ru(__fmul_ru((float)(__ldg(pnorm) * (double)__ldg(pscale)), 1.02f), __fmul_ru(2.f, e0x2));
+    const float pscl = __ldg(pscale);
+    int as = 0;
+    uint32_t aph = 0;
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+    constexpr int kCsEvery = 4;
+    uint32_t hA[64], hB[64];
+    int t = 0;
+    auto release = [&](int a) {  // this warp is done reading accumulator stage a (the leader's barrier)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(BAR(ACC_EMPTY + a));
+        else mbar_arrive_remote(L(BAR(ACC_EMPTY + a)));
+      }
+    };
+    for (int tp = pair; tp < num_tp; tp += npairs, ++t) {
+      const int ut = 2 * tp + (int)rank;
+      const int64_t row = (int64_t)ut * kBM + rr;
+      typename Pol::Row me = Pol::init(row < n, smax);
+      float Eg = __ldg(perr), EgN = (kCsEvery * BN < mi) ? __ldg(perr + kCsEvery * BN) : 0.f;
+      double pnr = nit > kCsEvery ? __ldg(pnorm + kCsEvery * BN) : 0.0;
+      mbar_wait(BAR(ACC_FULL + as), aph);
+      tc_fence_after();
+      tmem_ld64(tq + as * C::ACC_COLS, hA);
+      tmem_ld_wait64(hA);
+      int it = 0;
+      bool done = false;
+      for (; it < nit; ++it) {
+        const int base0 = it * BN;
+        const float E[4] = {Eg, Eg, Eg, Eg};
+        const uint32_t tcur = tq + as * C::ACC_COLS;
+        tmem_ld64(tcur + 64, hB);
+        uint32_t bits = epiq_fast(hA, E[0], E[1], me.theta);
+        const bool more = it + 1 < nit;
+        const int as_next = as + 1 == NACC ? 0 : as + 1;
+        const uint32_t aph_next = as + 1 == NACC ? aph ^ 1 : aph;
+        tmem_ld_wait64(hB);
+        bits |= epiq_fast(hB, E[2], E[3], me.theta) << 2;
+        if (bits) me = epiq_slow<Pol>(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, sb, rr, e0x2, kmax);
+        release(as);
+        if (more) {
+          mbar_wait(BAR(ACC_FULL + as_next), aph_next);
+          tc_fence_after();
+          tmem_ld64(tq + as_next * C::ACC_COLS, hA);
+          tmem_ld_wait64(hA);
+        }
+        as = as_next;
+        aph = aph_next;
+        if ((it + 1) % kCsEvery == 0 && more) {
+          const uint32_t mk = __reduce_min_sync(0xffffffffu, f2key(me.theta));
+          const float pnn = __double2float_ru(pnr * (double)pscl);
+          if (__fmul_ru(pnn, 1.0000153f) < key2f(mk)) {
+            done = true;
+            break;
+          }
+          Eg = EgN;
+          if (base0 + (kCsEvery + 1) * BN < mi) {
+            pnr = __ldg(pnorm + base0 + (kCsEvery + 1) * BN);
+            EgN = __ldg(perr + base0 + (kCsEvery + 1) * BN);
+          }
+        }
+      }
+      if (lane == 0) {  // one event per warp and tile pair, on the leader's counter
+        if (leader) atomicAdd(const_cast<uint32_t*>(done_cum), 1u);
+        else red_add_cluster_u32(L(w_done), 1u);
+      }
+      // a warp that is not done never meets an end marker: the leader ends a tile pair only after all 8
+      // epilogue warps (this one included) reported
+      if (done) {  // drain: release the remaining stages unread up to the end marker
+        for (++it; it < nit; ++it) {
+          mbar_wait_cluster(BAR(ACC_FULL + as), aph);  // (complete: acquires the leader's marker write)
+          const bool end = acc_end[as] == (uint32_t)(t + 1);
+          release(as);
+          if (++as == NACC) as = 0, aph ^= 1;
+          if (end || it + 1 == nit) break;
+          mbar_wait(BAR(ACC_FULL + as), aph);
+          tc_fence_after();
+        }
+      }
+      Pol::finish(me, sb, rr, e0x2, kmax, m, row, n, cand, ccount, ovf_list, ovf_count);
+      __syncwarp();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no remote barrier / shared-memory access of the peer is outstanding
+  if (warp == 1) tmem_dealloc_cg2(tmem, C::TMEM_COLS);
+}
+
+// ------------------------------------------------------------------------------ host side
+template <int KB, class Pol>
+static cudaError_t launch_tc2cta(const BuildCtx& c, cudaStream_t st) {
+  using C = Cfg2<KB, Pol>;
+  rmips_index_s* x = c.idx;
+  const int tail = tail_cols(x->d);
+  CUtensorMap ta, tat, tb, tbt;
+  if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->ldh, kBM) ||
+      !make_tmap_f16_box(&tat, x->U16, (uint64_t)x->n, (uint64_t)x->ldh, kBM, tail) ||
+      !make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->ldh, 64) ||
+      !make_tmap_f16_box(&tbt, x->P16, (uint64_t)c.mb, (uint64_t)x->ldh, 64, tail))
+    return cudaErrorNotSupported;
+  cudaError_t e = cudaFuncSetAttribute(k_build_tc2cta<KB, Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
+  if (e != cudaSuccess) return e;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->device);
+  const int tiles = (int)((x->n + kBM - 1) / kBM);
+  const int pairs_needed = (tiles + 1) / 2, pairs_max = sms / 2;
+  const int grid = 2 * (pairs_needed < pairs_max ? pairs_needed : pairs_max);
+  x->build_kernel = 4;
+  x->cand_slots = Pol::kSlots;
+  k_build_tc2cta<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tat, tb, tbt, x->perr, x->pnorm, c.scale_dev, x->n,
+                                                              c.mb, x->kmax, (x->d + 15) / 16, tail, c.cand, c.ccount,
+                                                              c.ovf_list, c.ovf_count, c.tiles_done);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// CTA-pair build for d_pad <= 256 with 128-slot 4-byte candidate lists (m <= 2^20, k_max <= 80);
+// cudaErrorNotSupported otherwise (the caller then takes build_tcq).
+cudaError_t build_tc2cta(const BuildCtx& c, cudaStream_t st) {
+  if (c.cstride != kCand || c.mb > QPolT<128>::kMaxItems) return cudaErrorNotSupported;
+  switch (c.idx->dpad) {
+    case 64: return launch_tc2cta<1, QPolT<128>>(c, st);
+    case 128: return launch_tc2cta<2, QPolT<128>>(c, st);
+    case 192: return launch_tc2cta<3, QPolT<128>>(c, st);
+    case 256: return launch_tc2cta<4, QPolT<128>>(c, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace rmips

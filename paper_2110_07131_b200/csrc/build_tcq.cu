@@ -27,20 +27,18 @@
 
 #include "candpol.cuh"
 #include "common.cuh"
+#include "epiq.cuh"
 #include "internal.h"
 #include "sm100.cuh"
 
 namespace rmips {
-
-#ifdef RMIPS_EPI_PROFILE
-extern __device__ unsigned long long g_epi_prof[4][256];  // build_tc.cu
-#endif
 
 namespace {
 
 // development-only experiment switches (librmips_dev.so reads them from the environment)
 constexpr int kDevNoFeed = 1;   // RMIPS_NOFEED: item units after the first ring round are not reloaded
 constexpr int kDevEpiSkip = 2;  // RMIPS_EPI_SKIP: the epilogue releases every stage unread
+constexpr int kDevEpiLoad = 4;  // RMIPS_EPI_LOAD: ... after reading it from TMEM (no filter work)
 
 constexpr int kBM = 128;                 // users per tile (TMEM lanes)
 constexpr int kUTile = kBM * 64 * 2;     // one 128 x 64 fp16 K-block unit = 16 KB
@@ -64,66 +62,6 @@ struct Cfg {
   static_assert(NST >= 6 && TOTAL <= 232448, "shared memory");
 };
 
-// Fast path of one 64-column half (scores of this thread's row): 3-input max trees and one
-// compare per 32-column chunk.  Returns a warp-uniform 2-bit mask of the chunks in which some
-// lane may append.  Padding columns of a ragged last tile (TMA zero fill) are not masked here: at
-// worst they flag a chunk, and the slow path masks them before anything is appended.
-__device__ __forceinline__ uint32_t epiq_fast(const uint32_t (&h)[64], float E0, float E1, float theta) {
-  uint32_t bits = 0;
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    const float mx = sm100::max32_bits(h + 32 * c);
-    bits |= (uint32_t)__any_sync(0xffffffffu, __fadd_ru(mx, c ? E1 : E0) >= theta) << c;
-  }
-  return bits;
-}
-
-// Slow path (one copy in the kernel, so the hot loop stays inside the instruction cache):
-// re-read each flagged chunk of the current accumulator stage from TMEM, append and refresh.
-template <class Pol>
-__device__ __noinline__ typename Pol::Row epiq_slow(uint32_t bits, uint32_t taddr, int base0, int mi, float4 E4,
-                                                    typename Pol::Row me, typename Pol::Buf sb, int rr, float e0x2,
-                                                    int kmax) {
-#pragma unroll 1
-  while (bits) {
-    const int c = __ffs(bits) - 1;
-    bits &= bits - 1;
-    uint32_t r[32];
-    sm100::tmem_ld32(taddr + 32 * c, r);
-    sm100::tmem_ld_wait(r);
-    const int pos0 = base0 + 32 * c;
-    if (pos0 + 32 > mi) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (pos0 + j >= mi) r[j] = 0xff800000u;  // -inf
-    }
-    const float E = c == 0 ? E4.x : c == 1 ? E4.y : c == 2 ? E4.z : E4.w;
-    float g4[8];
-#pragma unroll
-    for (int g = 0; g < 8; ++g)
-      g4[g] = fmaxf(fmaxf(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1])),
-                    fmaxf(__uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3])));
-#ifdef RMIPS_EPI_PROFILE
-    const long long p0 = clock64();
-#endif
-    Pol::append([&](int j) { return __uint_as_float(r[j]); }, g4, E, pos0, mi, me, sb, rr);
-#ifdef RMIPS_EPI_PROFILE
-    const long long p1 = clock64();
-    const bool rf = __any_sync(0xffffffffu, me.cnt > Pol::kSlots - 32);
-#endif
-    Pol::maybe_refresh(me, sb, rr, e0x2, kmax);
-#ifdef RMIPS_EPI_PROFILE
-    if ((threadIdx.x & 31) == 0) {
-      atomicAdd(&g_epi_prof[2][0], 1ull);
-      atomicAdd(&g_epi_prof[2][1], (unsigned long long)(p1 - p0));
-      atomicAdd(&g_epi_prof[2][2], (unsigned long long)(clock64() - p1));
-      atomicAdd(&g_epi_prof[2][3], (unsigned long long)rf);
-    }
-#endif
-  }
-  return me;
-}
-
 }  // namespace
 
 // tmA / tmB: 64-column boxes; tmAt / tmBt: the last K block's tail box (tail columns, tail_cols(d)).
@@ -140,6 +78,8 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   constexpr int NST = C::NST, NACC = C::NACC, BN = C::BN;
   constexpr bool kStreamA = KB == 0;
   const int kbn = kStreamA ? kb_rt : KB;          // K blocks per row
+  // ring slots in use: NST (dev: RMIPS_NST=k limits it, for the feed-latency experiments)
+  const int nst = ((dev >> 8) & 0xff) ? min(NST, (dev >> 8) & 0xff) : NST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base, derived from smem_raw by pointer arithmetic so that the compiler
   // keeps the shared state space (LDS/STS rather than generic loads/stores)
@@ -202,7 +142,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           tma_load_2d(sR + stage * kUTile, last ? mtail : mfull, kb * 64, r0, BAR(R_FULL + stage));
         }
         ++nloads;
-        if (++stage == NST) stage = 0, ph ^= 1;
+        if (++stage == nst) stage = 0, ph ^= 1;
       };
       for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
         if (!kStreamA)
@@ -212,7 +152,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           if (*done_cum >= 4 * (t + 1)) {  // every epilogue warp is done with this user tile
             stage_end[stage] = t + 1;
             mbar_arrive(BAR(R_FULL + stage));  // release: the marker is visible to the MMA warp
-            if (++stage == NST) stage = 0, ph ^= 1;
+            if (++stage == nst) stage = 0, ph ^= 1;
             break;
           }
           for (int kb = 0; kb < kbn; ++kb) {
@@ -237,7 +177,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       return kb == kbn - 1 ? sdesc_swz(a, 2 * tail) : sdesc_sw128(a);
     };
     auto next = [&]() {
-      if (++stage == NST) stage = 0, ph ^= 1;
+      if (++stage == nst) stage = 0, ph ^= 1;
     };
     for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
       if (!kStreamA) {
@@ -342,8 +282,17 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       tmem_ld_wait64(hA);
       int it = 0;
       bool done = false;  // warp-uniform: this warp's rows cannot gain any more
-      if (dev & kDevEpiSkip) {  // dev: release every accumulator stage unread (MMA + feed alone)
+      if (dev & (kDevEpiSkip | kDevEpiLoad)) {  // dev: release every accumulator stage (MMA + feed alone)
+        uint32_t sink = 0;
         for (; it < nit; ++it) {
+          if (dev & kDevEpiLoad) {
+            const uint32_t tcur = tq + as * C::ACC_COLS;
+            tmem_ld64(tcur, hA);
+            tmem_ld64(tcur + 64, hB);
+            tmem_ld_wait64(hA);
+            tmem_ld_wait64(hB);
+            sink ^= hA[0] ^ hB[63];  // (constant indices: the arrays stay in registers)
+          }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
@@ -353,6 +302,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             tc_fence_after();
           }
         }
+        if (sink == 0x12345678u) ccount[0] = 0;  // keeps the loads
       }
       for (; it < nit; ++it) {
         const int base0 = it * BN;
@@ -407,7 +357,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           tc_fence_after();
         }
       }
-      if (dev & kDevEpiSkip) {
+      if (dev & (kDevEpiSkip | kDevEpiLoad)) {
         if (row < n) ccount[row] = 0;  // dev: empty lists, no fallback
       } else {
         Pol::finish(me, sb, rr, e0x2, kmax, m, row, n, cand, ccount, ovf_list, ovf_count);
@@ -449,7 +399,9 @@ static cudaError_t launch_tcq(const BuildCtx& c, cudaStream_t st) {
   const int ksteps = (x->d + 15) / 16;  // K steps of 16 that touch real (non-padding) columns
   int dev = 0;
 #ifdef RMIPS_DEV
-  dev = (getenv("RMIPS_NOFEED") ? kDevNoFeed : 0) | (getenv("RMIPS_EPI_SKIP") ? kDevEpiSkip : 0);
+  dev = (getenv("RMIPS_NOFEED") ? kDevNoFeed : 0) | (getenv("RMIPS_EPI_SKIP") ? kDevEpiSkip : 0) |
+        (getenv("RMIPS_EPI_LOAD") ? kDevEpiLoad : 0);
+  if (const char* v = getenv("RMIPS_NST")) dev |= (atoi(v) & 0xff) << 8;
 #endif
   x->build_kernel = KB == 0 ? 3 : 2;
   x->cand_slots = Pol::kSlots;

@@ -42,6 +42,7 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
 cudaError_t build_simt(const BuildCtx& c, cudaStream_t st);
 cudaError_t build_tc(const BuildCtx& c, cudaStream_t st);  // build_tc.cu; cudaErrorNotSupported if unusable
 cudaError_t build_tcq(const BuildCtx& c, cudaStream_t st);  // build_tcq.cu (any d_pad)
+cudaError_t build_tc2cta(const BuildCtx& c, cudaStream_t st);  // build_tc2cta.cu (CTA pairs, d_pad <= 256)
 // Candidate slots per row the build will use (BuildCtx::cstride): 256 when k_max > kQ128MaxKmax and the
 // positions fit the 4-byte entries (m <= 2^20), else 128.
 constexpr int kQ128MaxKmax = 80;

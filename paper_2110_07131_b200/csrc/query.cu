@@ -93,18 +93,27 @@ k_query_prep(const float* __restrict__ q, int b, int d, int ldh, double c1, doub
       qerr[slot] = 0.f;
     }
   }
-  // fp16 rows, two elements per thread per step (half2 stores; ldh is a multiple of 16)
-  const int hp = ldh / 2;
-  for (int idx = t; idx < kQB * hp; idx += kPrepThreads) {
-    const int src = idx / hp, e = 2 * (idx - src * hp);
-    const int64_t slot = (int64_t)s * kQB + srank[src];
+}
+
+// The fp16 query rows (q * 2^eq, zero-padded to ldh) in their norm-sorted slots: one warp per slot
+// (row read coalesced through qperm, half2 stores), kConvWarps slots per CTA.
+constexpr int kConvWarps = 8;
+__global__ void __launch_bounds__(32 * kConvWarps)
+k_query_convert(const float* __restrict__ q, int d, int ldh, const int32_t* __restrict__ qperm,
+                const float* __restrict__ qscale, __half* __restrict__ Q16) {
+  const int64_t slot = blockIdx.x * (int64_t)kConvWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int src = qperm[slot];
+  const float scale = qscale[slot / kQB];
+  const float* x = q + (int64_t)(src < 0 ? 0 : src) * d;
+  __half2* out = reinterpret_cast<__half2*>(Q16 + slot * ldh);
+  for (int e = 2 * lane; e < ldh; e += 64) {
     float v0 = 0.f, v1 = 0.f;
-    if (src < cnt) {
-      const float* x = q + (int64_t)(s * kQB + src) * d;
+    if (src >= 0) {
       if (e < d) v0 = x[e] * scale;
       if (e + 1 < d) v1 = x[e + 1] * scale;
     }
-    reinterpret_cast<__half2*>(Q16 + slot * ldh)[e >> 1] = __halves2half2(__float2half_rn(v0), __float2half_rn(v1));
+    out[e >> 1] = __halves2half2(__float2half_rn(v0), __float2half_rn(v1));
   }
 }
 
@@ -410,6 +419,9 @@ cudaError_t query_prep(QueryCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   k_query_prep<<<c.nsub, kPrepThreads, 0, st>>>(c.q, c.b, x->d, x->ldh, x->c1, x->c2, c.Q16, c.qn, c.qerr, c.qscale, c.qperm,
                                        c.qcount, c.flags_dev); count_launch();
+  k_query_convert<<<(unsigned)((int64_t)c.nsub * kQB / kConvWarps), 32 * kConvWarps, 0, st>>>(c.q, x->d, x->ldh, c.qperm,
+                                                                                           c.qscale, c.Q16);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -310,6 +310,7 @@ def _sampled_full_config(cfg, n_sample, batch=None, query_stride=1):
     idx = rmips.rmips_build_index(_t(w.U), _t(w.P), spec.k_max)
     assert idx.overflow_rows == 0
     assert idx.build_flags & rmips.RMIPS_BUILD_SIMT == 0  # the tcgen05 build ran
+    assert idx.build_kernel == (4 if spec.d > 64 else 1)  # CTA pairs for d_pad 128..256
     rng = np.random.default_rng(cfg)
     sample = np.sort(rng.choice(spec.n, n_sample, replace=False))
     vals, oids = oracle.topk(w.U[sample], w.P, spec.k_max)
@@ -664,13 +665,15 @@ def test_large_d_streamed_k_loop(d):
 def test_trimmed_tail_k_block(d):
     """The last K block trimmed to a 16- or 32-column box (SWIZZLE_32B / 64B descriptors) in both the
     build and the query kernels: d = 16 (one 16-column block), 90 (32-column tail), 200 (16-column tail)."""
-    U, P = gen.random_instance(80 + d, 1500, 700, d, "gaussian")
+    U, P = gen.random_instance(80 + d, 1300, 700, d, "gaussian")  # 11 user tiles: the last CTA pair has one
     Qy = np.concatenate([P[:30], gen.random_instance(81 + d, 30, 1, d)[0]])
     for kmax, k in ((10, 4), (100, 37)):   # the second: k_max > 80 -> 256-slot lists (k_build_tcq for d = 16)
         member = oracle.rkmips_naive(U, P, Qy, k)
         idx = rmips.rmips_build_index(_t(U), _t(P), kmax)
         assert idx.build_flags & rmips.RMIPS_BUILD_SIMT == 0 and idx.overflow_rows == 0
         assert idx.cand_slots == (256 if kmax > 80 else 128)
+        if d > 64 and kmax <= 80:
+            assert idx.build_kernel == 4  # CTA pairs (tcgen05.mma.cta_group::2)
         got = rmips.split_sets(*rmips.rmips_query(idx, _t(Qy), k))
         assert_same(got, member, U, P, Qy, k, "tail d=%d kmax=%d" % (d, kmax))
         _, _, tau, ids = idx.export()
@@ -704,7 +707,7 @@ def test_m_above_2pow20_tensor_core_build():
     (not the SIMT build) and give the oracle's exact lists on a user sample."""
     w = gen.make_workload(4, n=1500, m=1_100_000, nq=30, d=100)
     idx = rmips.rmips_build_index(_t(w.U), _t(w.P), 20)
-    assert idx.build_kernel == 2 and idx.build_flags & rmips.RMIPS_BUILD_SIMT == 0
+    assert idx.build_kernel == 2 and idx.build_flags & rmips.RMIPS_BUILD_SIMT == 0  # (8-byte entries: 1 CTA)
     assert idx.cand_slots == 128 and idx.overflow_rows == 0
     sample = np.sort(np.random.default_rng(3).choice(w.U.shape[0], 160, replace=False))
     vals, oids = oracle.topk(w.U[sample], w.P, 20)
@@ -715,4 +718,20 @@ def test_m_above_2pow20_tensor_core_build():
     member = oracle.rkmips_twophase(w.U[sample], vals, w.Qy, 20)
     for qi in range(w.Qy.shape[0]):
         assert np.array_equal(np.intersect1d(sets[qi], sample), sample[member[qi]]), qi
+    idx.close()
+
+
+@pytest.mark.parametrize("n", [1, 127, 128, 129, 255, 383])
+def test_cta_pair_build_ragged_user_tiles(n):
+    """The CTA-pair build (k_build_tc2cta) with every user-tile parity: a single tile (the follower's rows
+    all past n), odd and even tile counts, ragged last tiles; lists bitwise equal to the oracle's."""
+    U, P = gen.random_instance(100 + n, n, 900, 100, "skewed")
+    idx = rmips.rmips_build_index(_t(U), _t(P), 16)
+    assert idx.build_kernel == 4 and idx.overflow_rows == 0
+    _, _, tau, ids = idx.export()
+    vals, oids = oracle.topk(U, P, 16)
+    assert np.array_equal(tau.T, vals) and np.array_equal(ids.T, oids)
+    Qy = P[:12]
+    member = oracle.rkmips_twophase(U, vals, Qy, 7)
+    assert_same(rmips.split_sets(*rmips.rmips_query(idx, _t(Qy), 7)), member, label="pair n=%d" % n)
     idx.close()
