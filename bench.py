@@ -263,14 +263,17 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
     stream = torch.cuda.current_stream()
     m_prime = args.pprime * spec.k_max if args.pprime else 0
     cap = [None]  # learned during the warm-up steps (the first call sizes itself: rmips.py retries once)
+    host_build_ms = []
 
     def step():
         """One pass of the hot path: build + every query call.  Per-call phase times and counters are
         read right after each call (host reads of values the call already synchronised on)."""
+        tb0 = time.perf_counter()
         if m_prime:
             idx = rmips.rmips_build_index_pprime(U, P, spec.k_max, m_prime, bflags)
         else:
             idx = rmips.rmips_build_index(U, P, spec.k_max, bflags)
+        host_build_ms.append((time.perf_counter() - tb0) * 1e3)
         outs, qph = [], []
         for q in Qb:
             off, ids = rmips.rmips_query(idx, q, k, qflags, capacity=cap[0])
@@ -303,6 +306,9 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
         torch.distributed.barrier()
     step_ms, recs, host_ms = [], [], []
     last = None
+    import gc
+    gc.collect()
+    gc.disable()  # (no collector pause inside the timed region; re-enabled right after it)
     sampler = ClockSampler(dev.index)
     with sampler:
         tw0 = time.perf_counter()
@@ -321,6 +327,7 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
             step_ms.append(e0.elapsed_time(e1))
             last = outs
         tw1 = time.perf_counter()
+    gc.enable()
     clocks = sampler.summary(tw0, tw1)
     torch.cuda.synchronize()
     t_rank = sum(step_ms)
@@ -391,6 +398,7 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
 
     res = {"value": value, "ms_per_step": ms_per_step, "steps": steps, "warmup": warmup,
            "step_ms": [round(x, 3) for x in step_ms], "host_ms": [round(x, 3) for x in host_ms],
+           "host_build_ms": [round(x, 3) for x in host_build_ms[-steps:]],
            "config": _config_dict(spec, k, ws) | {"kernels": "simt" if args.simt else "tcgen05"},
            "build": {"ms": med("build"), "inner_products_per_s": spec.n * spec.m / (med("build") / 1e3),
                      "contraction_ms": kern_ms, "prep_ms": med("prep"), "select_blocks_ms": med("select"),
@@ -515,7 +523,7 @@ def main():
             "vs_baseline": None, "dtype": "fp16 filter (fp32 accumulate) + f64 exact decisions",
             "data": "synthetic (SURVEY Appendix C generator, seed 0; users seed = rank); stands in for the paper's "
                     "MF vectors (P:571-587), configs[4] is beyond the paper"}
-    for key in ("step_ms", "host_ms", "config", "build", "query", "roofline", "roofline_query", "roofline_scan", "index", "clocks",
+    for key in ("step_ms", "host_ms", "host_build_ms", "config", "build", "query", "roofline", "roofline_query", "roofline_scan", "index", "clocks",
                 "gpu_launches", "e2e", "cpu_baseline", "parity"):
         if key in head:
             line[key] = head[key]
