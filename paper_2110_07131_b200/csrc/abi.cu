@@ -474,7 +474,8 @@ static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cuda
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
   size_t oQ16 = take((size_t)nsub * kQB * ldh * 2), oqn = take((size_t)nsub * kQB * 4),
          oqe = take((size_t)nsub * kQB * 4), oqs = take((size_t)nsub * 4), oqp = take((size_t)nsub * kQB * 4),
-         oqc = take((size_t)nsub * 4), owl = take((size_t)nsub * x->nblocks * 4), oacc = take((size_t)cap * 8),
+         oqc = take((size_t)nsub * 4), oqnr = take((size_t)nsub * kQB * 8), oqcm = take((size_t)nsub * kQB / 8 * 4),
+         owl = take((size_t)nsub * x->nblocks * 4), oacc = take((size_t)cap * 8),
          ound = take((size_t)cap * 8), oscn = take((size_t)cap * 4),
          osrt = take((size_t)cap * 8), ocub = take(qcub), obits = take(use_bits ? (size_t)c.b * nw * 4 : 0);
   if (off > x->ws_bytes) {
@@ -491,6 +492,8 @@ static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cuda
   c.qscale = reinterpret_cast<float*>(b + oqs);
   c.qperm = reinterpret_cast<int32_t*>(b + oqp);
   c.qcount = reinterpret_cast<int32_t*>(b + oqc);
+  c.qnrm = reinterpret_cast<double*>(b + oqnr);
+  c.qcmax = reinterpret_cast<float*>(b + oqcm);
   c.wlen = reinterpret_cast<int32_t*>(b + owl);
   c.acc = reinterpret_cast<uint64_t*>(b + oacc);
   c.und = reinterpret_cast<uint64_t*>(b + ound);

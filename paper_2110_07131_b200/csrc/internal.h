@@ -64,6 +64,8 @@ struct QueryCtx {
   float* qscale = nullptr;       // [nsub] 2^eq
   int32_t* qperm = nullptr;      // [nsub][kQB] sorted slot -> input query index (-1 padding)
   int32_t* qcount = nullptr;     // [nsub] queries in the sub-batch
+  double* qnrm = nullptr;        // [nsub][kQB] ||q|| in input order (query prep scratch)
+  float* qcmax = nullptr;        // [nsub][kQB / 8] max |q_j| per prep CTA (query prep scratch)
   int32_t* wlen = nullptr;       // [nsub * nblocks] Lemma 3 prefix of every (sub-batch, user tile)
   // outputs of the filter
   unsigned long long* counters = nullptr;  // kNumCounters (+ accepted / undecided list sizes)

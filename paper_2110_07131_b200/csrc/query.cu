@@ -15,74 +15,84 @@
 namespace rmips {
 
 // ------------------------------------------------------------------------------ Q1
-// One CTA (1024 threads) per 256-query sub-batch.  Warp w computes the norms of queries w, w + 32, ...
-// with coalesced row reads (lanes over the row, fp64 sum; only its rounded-up value is used, so the
-// order does not matter), threads 0..255 rank the queries in (norm desc, index asc) order, and all
-// threads write the fp16 rows (q * 2^eq, zero-padded to d_pad) element-parallel.
-constexpr int kPrepThreads = 1024;
-__global__ void __launch_bounds__(kPrepThreads)
-k_query_prep(const float* __restrict__ q, int b, int d, int ldh, double c1, double c2, __half* __restrict__ Q16,
-             float* __restrict__ qn, float* __restrict__ qerr, float* __restrict__ qscale,
-             int32_t* __restrict__ qperm, int32_t* __restrict__ qcount, int* __restrict__ flags) {
-  __shared__ double nrm[kQB];
-  __shared__ float smax[kPrepThreads / 32];
-  __shared__ int srank[kQB];
-  __shared__ float s_scale;
-  const int s = blockIdx.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  const int cnt = min(kQB, b - s * kQB);
+// Two launches over warps, one warp per query (kPrepWarps per CTA):
+//   k_query_norms   ||q|| with coalesced row reads (lanes over the row, fp64 sum; only its rounded-up
+//                   value is used, so the order does not matter), the finite check, and each CTA's
+//                   max |q_j| for the sub-batch's power-of-two scale
+//   k_query_finish  the query's rank in (norm desc, index asc) order within its 256-query sub-batch
+//                   (Alg. 3 line 1 sorts by ||q||), its slot's metadata, and its fp16 row q * 2^eq
+//                   (zero-padded to ldh) in that slot
+constexpr int kPrepWarps = 8;
+constexpr int kPrepCtas = kQB / kPrepWarps;  // CTAs per sub-batch
+__global__ void __launch_bounds__(32 * kPrepWarps)
+k_query_norms(const float* __restrict__ q, int b, int d, double* __restrict__ nrm, float* __restrict__ cmax,
+              int* __restrict__ flags) {
+  __shared__ float smax[kPrepWarps];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t qi = (int64_t)blockIdx.x * kPrepWarps + wid;  // sub-batch slot of the INPUT order
   float mx = 0.f;
-  for (int qi = wid; qi < kQB; qi += kPrepThreads / 32) {
-    double acc = 0.0;
-    bool fin = true;
-    if (qi < cnt) {
-      const float* x = q + (int64_t)(s * kQB + qi) * d;
-      for (int e = lane; e < d; e += 32) {
-        const float v = x[e];
-        fin &= isfinite(v);
-        mx = fmaxf(mx, fabsf(v));
-        acc = __fma_rn((double)v, (double)v, acc);
-      }
+  double acc = 0.0;
+  bool fin = true;
+  if (qi < b) {
+    const float* x = q + qi * d;
+    for (int e = lane; e < d; e += 32) {
+      const float v = x[e];
+      fin &= isfinite(v);
+      mx = fmaxf(mx, fabsf(v));
+      acc = __fma_rn((double)v, (double)v, acc);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  fin = __all_sync(0xffffffffu, fin);
+  if (lane == 0) {
+    double nr = qi < b ? sqrt(acc) : -1.0;
+    if (qi < b && !fin) atomicOr(flags, kFlagNonfinite), nr = 0.0;
+    nrm[qi] = nr;
+    smax[wid] = isfinite(mx) ? mx : 0.f;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m2 = 0.f;
+    for (int w = 0; w < kPrepWarps; ++w) m2 = fmaxf(m2, smax[w]);
+    cmax[blockIdx.x] = m2;
+  }
+}
+
+__global__ void __launch_bounds__(32 * kPrepWarps)
+k_query_finish(const float* __restrict__ q, int b, int d, int ldh, double c1, double c2,
+               const double* __restrict__ nrm, const float* __restrict__ cmax, __half* __restrict__ Q16,
+               float* __restrict__ qn, float* __restrict__ qerr, float* __restrict__ qscale,
+               int32_t* __restrict__ qperm, int32_t* __restrict__ qcount) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int s = blockIdx.x / kPrepCtas;
+  const int t = (blockIdx.x - s * kPrepCtas) * kPrepWarps + wid;  // query t of sub-batch s (input order)
+  const int cnt = min(kQB, b - s * kQB);
+  // the sub-batch's scale 2^e: max |q_j| < 2^14 after scaling (the filter's fp16 range)
+  float m2 = lane < kPrepCtas ? cmax[s * kPrepCtas + lane] : 0.f;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m2 = fmaxf(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+  int ex = 0;
+  if (m2 > 0.f) frexpf(m2, &ex);
+  const float scale = ldexpf(1.f, max(-126, min(126, 14 - ex)));
+  const double* nr_s = nrm + (int64_t)s * kQB;
+  const double nr = nr_s[t];
+  int rank = t;  // padding (t >= cnt) keeps its own slot
+  if (t < cnt) {
+    int r = 0;
+    for (int j = lane; j < cnt; j += 32) {
+      const double o = nr_s[j];
+      r += (o > nr) || (o == nr && j < t);
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    fin = __all_sync(0xffffffffu, fin);
-    if (lane == 0) {
-      double nr = qi < cnt ? sqrt(acc) : -1.0;
-      if (qi < cnt && !fin) atomicOr(flags, kFlagNonfinite), nr = 0.0;
-      nrm[qi] = nr;
-    }
+    for (int o = 16; o; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    rank = r;
   }
-  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) smax[wid] = isfinite(mx) ? mx : 0.f;
-  __syncthreads();
-  if (t == 0) {
-    float m2 = 0.f;
-    for (int w = 0; w < kPrepThreads / 32; ++w) m2 = fmaxf(m2, smax[w]);
-    int ex = 0;
-    if (m2 > 0.f) frexpf(m2, &ex);
-    int e = max(-126, min(126, 14 - ex));
-    s_scale = ldexpf(1.f, e);
-    qscale[s] = s_scale;
-    qcount[s] = cnt;
-  }
-  if (t < kQB) {
-    // rank = position in (norm desc, index asc) order
-    const double nr = nrm[t];
-    int rank = t;
-    if (t < cnt) {
-      rank = 0;
-      for (int j = 0; j < cnt; ++j) {
-        const double o = nrm[j];
-        rank += (o > nr) || (o == nr && j < t);
-      }
-    }
-    srank[t] = rank;
-  }
-  __syncthreads();
-  const float scale = s_scale;
-  if (t < kQB) {
-    const double nr = nrm[t];
-    const int64_t slot = (int64_t)s * kQB + srank[t];
+  const int64_t slot = (int64_t)s * kQB + rank;
+  if (lane == 0) {
     if (t < cnt) {
       qperm[slot] = s * kQB + t;
       qn[slot] = __double2float_ru(nr * (1.0 + 1e-12));
@@ -92,24 +102,16 @@ k_query_prep(const float* __restrict__ q, int b, int d, int ldh, double c1, doub
       qn[slot] = -CUDART_INF_F;
       qerr[slot] = 0.f;
     }
+    if (t == 0) {
+      qscale[s] = scale;
+      qcount[s] = cnt;
+    }
   }
-}
-
-// The fp16 query rows (q * 2^eq, zero-padded to ldh) in their norm-sorted slots: one warp per slot
-// (row read coalesced through qperm, half2 stores), kConvWarps slots per CTA.
-constexpr int kConvWarps = 8;
-__global__ void __launch_bounds__(32 * kConvWarps)
-k_query_convert(const float* __restrict__ q, int d, int ldh, const int32_t* __restrict__ qperm,
-                const float* __restrict__ qscale, __half* __restrict__ Q16) {
-  const int64_t slot = blockIdx.x * (int64_t)kConvWarps + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  const int src = qperm[slot];
-  const float scale = qscale[slot / kQB];
-  const float* x = q + (int64_t)(src < 0 ? 0 : src) * d;
+  const float* x = q + (int64_t)(s * kQB + (t < cnt ? t : 0)) * d;
   __half2* out = reinterpret_cast<__half2*>(Q16 + slot * ldh);
   for (int e = 2 * lane; e < ldh; e += 64) {
     float v0 = 0.f, v1 = 0.f;
-    if (src >= 0) {
+    if (t < cnt) {
       if (e < d) v0 = x[e] * scale;
       if (e + 1 < d) v1 = x[e + 1] * scale;
     }
@@ -417,10 +419,11 @@ static inline unsigned nblk(int64_t work, int t) { return (unsigned)((work + t -
 
 cudaError_t query_prep(QueryCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
-  k_query_prep<<<c.nsub, kPrepThreads, 0, st>>>(c.q, c.b, x->d, x->ldh, x->c1, x->c2, c.Q16, c.qn, c.qerr, c.qscale, c.qperm,
-                                       c.qcount, c.flags_dev); count_launch();
-  k_query_convert<<<(unsigned)((int64_t)c.nsub * kQB / kConvWarps), 32 * kConvWarps, 0, st>>>(c.q, x->d, x->ldh, c.qperm,
-                                                                                           c.qscale, c.Q16);
+  const unsigned grid = (unsigned)(c.nsub * kPrepCtas);
+  k_query_norms<<<grid, 32 * kPrepWarps, 0, st>>>(c.q, c.b, x->d, c.qnrm, c.qcmax, c.flags_dev);
+  count_launch();
+  k_query_finish<<<grid, 32 * kPrepWarps, 0, st>>>(c.q, c.b, x->d, x->ldh, x->c1, x->c2, c.qnrm, c.qcmax, c.Q16, c.qn,
+                                                   c.qerr, c.qscale, c.qperm, c.qcount);
   count_launch();
   return cudaGetLastError();
 }
@@ -470,7 +473,7 @@ cudaError_t query_exact(QueryCtx& c, cudaStream_t st) {
                                                            x->d, x->pd, c.k, c.counters, c.und, AccSink{c.acc, c.bits, c.nw}, c.cap,
                                                            x->mprime, c.scan_cnt); count_launch();
   } else {
-    k_exact_decide<<<148 * 8, 256, 0, st>>>(c.q, x->U32, x->tau + (int64_t)(c.k - 1) * x->n, x->perm_u, x->d,
+    k_exact_decide<<<148, 256, 0, st>>>(c.q, x->U32, x->tau + (int64_t)(c.k - 1) * x->n, x->perm_u, x->d,
                                             c.counters, c.und, AccSink{c.acc, c.bits, c.nw}, c.cap); count_launch();
   }
   return cudaGetLastError();
@@ -503,10 +506,11 @@ __global__ void k_copy_ids32(const uint32_t* __restrict__ keys, int64_t total, u
 }
 
 // Bit-matrix output (QueryCtx::bits): the b x n matrix is cut into warp chunks of kChunkWords words of
-// one query row (lane l owns words 32 l .. 32 l + 31 of its warp's chunk).  Pass 1 counts the set bits of
-// every chunk, a scan gives every chunk's first output position (the chunks are in (query, user) order),
-// and pass 2 writes the ids of every chunk in ascending user order and clears the words it read, so the
-// matrix is all zero again for the next batch (it is memset only when its place in the workspace
+// one query row.  A warp reads its chunk in 32 coalesced steps (step i: lane l holds word 32 i + l).
+// Pass 1 counts the set bits of every chunk, a scan gives every chunk's first output position (the
+// chunks are in (query, user) order), and pass 2 re-reads the chunk, writes the ids of every step in
+// ascending user order (a warp prefix sum over the lanes' popcounts) and clears the words it read, so
+// the matrix is all zero again for the next batch (it is memset only when its place in the workspace
 // changes).  Every warp works independently: no block-level loop over a whole row.
 constexpr int kChunkWords = 1024;
 constexpr int kBitsThreads = 256;
@@ -518,11 +522,11 @@ k_bits_count(const uint32_t* __restrict__ bits, int64_t nw, int64_t nchunk_total
   const int64_t per_row = (nw + kChunkWords - 1) / kChunkWords;
   const int64_t q = g / per_row, c = g - q * per_row;
   const uint32_t* row = bits + q * nw;
-  const int64_t w0 = c * kChunkWords + 32 * lane;
+  const int64_t w0 = c * kChunkWords + lane;
   int cnt = 0;
 #pragma unroll 8
-  for (int j = 0; j < 32; ++j)
-    if (w0 + j < nw) cnt += __popc(row[w0 + j]);
+  for (int i = 0; i < 32; ++i)
+    if (w0 + 32 * i < nw) cnt += __popc(__ldcs(row + w0 + 32 * i));  // (streamed: read once more by the emit)
 #pragma unroll
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   if (lane == 0) counts[g] = cnt;
@@ -538,35 +542,35 @@ k_bits_emit(uint32_t* __restrict__ bits, int64_t nw, int b, int64_t nchunk_total
   const int64_t q = g / per_row, c = g - q * per_row;
   const int64_t total = chunk_off[nchunk_total - 1] + counts[nchunk_total - 1];
   const bool fits = total <= capacity;  // ids only when all of them fit (as the sorted-key path)
-  const int64_t base = chunk_off[g];
+  int64_t base = chunk_off[g];
   if (lane == 0) {
     if (c == 0) offsets[q] = base;
     if (g == nchunk_total - 1) offsets[b] = total;
   }
   if (counts[g] == 0) return;  // (warp-uniform) nothing set in this chunk
   uint32_t* row = bits + q * nw;
-  const int64_t w0 = c * kChunkWords + 32 * lane;
+  const int64_t w0 = c * kChunkWords + lane;
   uint32_t wv[32];
-  int cnt = 0;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    wv[j] = w0 + j < nw ? row[w0 + j] : 0u;
-    cnt += __popc(wv[j]);
-  }
-  int incl = cnt;
+  for (int i = 0; i < 32; ++i) wv[i] = w0 + 32 * i < nw ? row[w0 + 32 * i] : 0u;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int x = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += x;
-  }
-  int64_t pos = base + incl - cnt;
+  for (int i = 0; i < 32; ++i) {
+    uint32_t w = wv[i];
+    const uint32_t any = __ballot_sync(0xffffffffu, w != 0u);
+    if (!any) continue;
+    const int cnt = __popc(w);
+    int incl = cnt;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    uint32_t w = wv[j];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
     if (w) {
-      row[w0 + j] = 0u;
+      const int64_t wi = w0 + 32 * i;
+      row[wi] = 0u;
       if (fits) {
-        const int32_t u0 = (int32_t)((w0 + j) * 32);
+        int64_t pos = base + incl - cnt;
+        const int32_t u0 = (int32_t)(wi * 32);
         while (w) {
           const int bit = __ffs(w) - 1;
           w &= w - 1;
@@ -574,6 +578,7 @@ k_bits_emit(uint32_t* __restrict__ bits, int64_t nw, int b, int64_t nchunk_total
         }
       }
     }
+    base += __shfl_sync(0xffffffffu, incl, 31);
   }
 }
 

@@ -47,13 +47,28 @@ constexpr int kAcc = 2;
 // takes KB consecutive units, and the MMA on K block kb starts as soon as that unit has landed.
 // KB = 0 (d_pad > 256: the queries do not fit in shared memory next to the ring): every ring unit holds
 // K block kb of the user tile (16 KB) AND of the sub-batch's queries (32 KB, re-read from L2 per tile).
-struct QSmem {
-  static constexpr int NU(int KB) { return KB == 1 ? 4 : KB == 0 ? 4 : 6; }  // ring units
-  static constexpr int UNIT(int KB) { return KB == 0 ? kUTileBytes + kQTileBytes : kUTileBytes; }
-  static constexpr int Q = 0;
-  static constexpr int A(int KB) { return KB * kQTileBytes; }
-  static constexpr int BAR(int KB) { return A(KB) + NU(KB) * UNIT(KB); }
-  static constexpr int TOTAL(int KB) { return BAR(KB) + 256 + 1024; }
+// KB = 1..4: the resident queries take (KB - 1) 32 KB units plus the trimmed tail unit (256 x tail
+// columns), and the ring gets every 16 KB unit left (at most kMaxNU): d = 200 keeps 104 KB of queries and
+// 7 ring units.  The layout is computed at run time (QLayout) from KB and the tail width.
+constexpr int kMaxNU = 8;
+struct QLayout {
+  int nu, unit, a, bar, total;  // ring units, unit bytes, ring offset, barrier offset, dynamic smem bytes
+  __host__ __device__ static QLayout make(int KB, int tail) {
+    QLayout l;
+    if (KB == 0) {
+      l.unit = kUTileBytes + kQTileBytes;
+      l.a = 0;
+      l.nu = 4;
+    } else {
+      l.unit = kUTileBytes;
+      l.a = ((KB - 1) * kQTileBytes + kQB * tail * 2 + 1023) / 1024 * 1024;
+      l.nu = (232448 - 1024 - 512 - l.a) / l.unit;
+      if (l.nu > kMaxNU) l.nu = kMaxNU;
+    }
+    l.bar = l.a + l.nu * l.unit;
+    l.total = l.bar + 512 + 1024;  // barriers (<= 2 + 2 kMaxNU + 4) + TMEM slot, alignment slack
+    return l;
+  }
 };
 
 __device__ __forceinline__ int lemma3_len(const float* __restrict__ qn_sub, int cnt, float tbv) {
@@ -244,17 +259,18 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
            int nsub, int flags, int ksteps, const int32_t* __restrict__ wlen, unsigned long long* __restrict__ ctr,
            AccSink acc_list, uint64_t* __restrict__ und_list, int64_t cap) {
   using namespace sm100;
-  constexpr int kStages = QSmem::NU(KB);  // ring units
-  constexpr int kUnit = QSmem::UNIT(KB);
+  const QLayout lay = QLayout::make(KB, tail);
+  const int kStages = lay.nu;  // ring units
+  const int kUnit = lay.unit;
   constexpr bool kStreamQ = KB == 0;
   const int kbn = kStreamQ ? kb_rt : KB;  // K blocks per row; the last one is `tail` columns wide
   const uint32_t utail = (uint32_t)(kBM * tail * 2), qtail = (uint32_t)(kQB * tail * 2);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t sQ = sbase + QSmem::Q;
-  const uint32_t sA = sbase + QSmem::A(KB);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + QSmem::BAR(KB));
+  const uint32_t sQ = sbase;
+  const uint32_t sA = sbase + lay.a;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + lay.bar);
   const uint32_t bar0 = smem_u32(bars);
   auto BAR = [&](int i) { return bar0 + 8u * i; };
   const int Q_FULL = 0, Q_EMPTY = 1, A_FULL = 2, A_EMPTY = 2 + kStages, ACC_FULL = 2 + 2 * kStages,
@@ -531,7 +547,7 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
       !make_tmap_f16_box(&tq, c.Q16, (uint64_t)c.nsub * kQB, (uint64_t)x->ldh, kQB) ||
       !make_tmap_f16_box(&tqt, c.Q16, (uint64_t)c.nsub * kQB, (uint64_t)x->ldh, kQB, tail))
     return cudaErrorNotSupported;
-  const int smem = QSmem::TOTAL(KB);
+  const int smem = QLayout::make(KB, tail).total;
   cudaError_t e = cudaFuncSetAttribute(k_query_tc<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t nwork = (int64_t)c.nsub * x->nblocks;
