@@ -37,21 +37,26 @@ constexpr int kAUnit = 128 * 64 * 2;     // one K block of a user tile: 16 KB
 constexpr int kBUnit = 64 * 64 * 2;      // one K block of this CTA's half item tile: 8 KB
 constexpr int kGroup = 4;                // item tiles per end-of-pair decision (the C-S check period)
 
+// The ring holds whole item tiles: a slot is this CTA's KB K-block units of one item tile (one full
+// barrier, one 13-MMA chain, one commit per tile: the MMA warp's per-tile overhead does not scale with
+// the K blocks).
 template <int KB, class Pol>
 struct Cfg2 {
   static constexpr int BN = 128;                 // items per pair MMA tile (64 rows in each CTA)
+  static constexpr int TS = KB * kBUnit;         // bytes of a tile slot
   static constexpr int RING = KB * kAUnit;       // after the A buffer
-  static constexpr int NSB_FIT = (232448 - 3072 - RING - Pol::kBufBytes) / kBUnit;
-  static constexpr int NSB = NSB_FIT < 24 ? NSB_FIT : 24;
-  static constexpr int CAND = RING + NSB * kBUnit;
+  static constexpr int NSB_FIT = (232448 - 3072 - RING - Pol::kBufBytes) / TS;
+  static constexpr int NSB = NSB_FIT < 8 ? NSB_FIT : 8;  // tile slots
+  static constexpr int NDEC = 8;                 // end-of-pair decision barriers (see the producer)
+  static constexpr int CAND = RING + NSB * TS;
   static constexpr int BAR = CAND + Pol::kBufBytes;
   static constexpr int NACC = 3, ACC_COLS = 128, A_TMEM = NACC * ACC_COLS, TMEM_COLS = 512;
   static constexpr int THREADS = 192;
-  // barriers R_FULL[NSB] R_EMPTY[NSB] DEC[NSB] ACC_FULL[NACC] ACC_EMPTY[NACC] A_FULL A_EMPTY, then words
-  static constexpr int NBARS = 3 * NSB + 2 * NACC + 2;
-  static constexpr int TOTAL = BAR + NBARS * 8 + (4 + 2 * NSB + NACC) * 4 + 1024;
+  // barriers R_FULL[NSB] R_EMPTY[NSB] DEC[NDEC] ACC_FULL[NACC] ACC_EMPTY[NACC] A_FULL A_EMPTY, then words
+  static constexpr int NBARS = 2 * NSB + NDEC + 2 * NACC + 2;
+  static constexpr int TOTAL = BAR + NBARS * 8 + (4 + NSB + NDEC + NACC) * 4 + 1024;
   static_assert(KB >= 1 && KB <= 4 && A_TMEM + 32 * KB <= TMEM_COLS, "tensor memory");
-  static_assert(NSB >= 2 * KB && NSB >= 8 && TOTAL <= 232448, "shared memory");
+  static_assert(NSB >= 2 && TOTAL <= 232448, "shared memory");
 };
 
 }  // namespace
@@ -66,7 +71,7 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                unsigned long long* __restrict__ tiles_done) {
   using namespace sm100;
   using C = Cfg2<KB, Pol>;
-  constexpr int NSB = C::NSB, NACC = C::NACC, BN = C::BN;
+  constexpr int NSB = C::NSB, NDEC = C::NDEC, NACC = C::NACC, BN = C::BN, TS = C::TS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
@@ -75,14 +80,14 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR);
   const uint32_t bar0 = smem_u32(bars);
   auto BAR = [&](int i) { return bar0 + 8u * i; };
-  const int R_FULL = 0, R_EMPTY = NSB, DEC = 2 * NSB, ACC_FULL = 3 * NSB, ACC_EMPTY = 3 * NSB + NACC,
-            A_FULL = 3 * NSB + 2 * NACC, A_EMPTY = A_FULL + 1;
+  const int R_FULL = 0, R_EMPTY = NSB, DEC = 2 * NSB, ACC_FULL = 2 * NSB + NDEC, ACC_EMPTY = ACC_FULL + NACC,
+            A_FULL = ACC_EMPTY + NACC, A_EMPTY = A_FULL + 1;
   uint32_t* words = reinterpret_cast<uint32_t*>(bars + C::NBARS);
   uint32_t* tmem_slot = words;
   volatile uint32_t* done_cum = words + 1;   // leader: epilogue warps of the pair done with a tile pair (8 each)
   volatile uint32_t* stage_end = words + 2;  // [NSB] leader: producer -> MMA end marker (t + 1)
   volatile uint32_t* acc_end = stage_end + NSB;  // [NACC] both: MMA -> epilogue end marker
-  volatile uint32_t* dec = acc_end + NACC;   // [NSB] follower: the leader's decision for an item tile
+  volatile uint32_t* dec = acc_end + NACC;   // [NDEC] follower: the leader's decision for a group of tiles
   const uint32_t w_done = smem_u32(words + 1), w_acc_end = smem_u32(words + 2 + NSB),
                  w_dec = smem_u32(words + 2 + NSB + NACC);
 
@@ -95,19 +100,21 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int nit = (int)((m + BN - 1) / BN);
   const uint32_t a_tail_bytes = (uint32_t)(kBM * tail * 2), b_tail_bytes = (uint32_t)(64 * tail * 2);
   const uint32_t a_bytes = (uint32_t)((KB - 1) * kAUnit) + a_tail_bytes;
+  const uint32_t b_bytes = (uint32_t)((KB - 1) * kBUnit) + b_tail_bytes;  // this CTA's half of an item tile
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     tma_prefetch(&tmAt);
     tma_prefetch(&tmBt);
-    for (int s = 0; s < NSB; ++s)
-      mbar_init(BAR(R_FULL + s), 1), mbar_init(BAR(R_EMPTY + s), 1), mbar_init(BAR(DEC + s), 1);
+    for (int s = 0; s < NSB; ++s) mbar_init(BAR(R_FULL + s), 1), mbar_init(BAR(R_EMPTY + s), 1);
+    for (int s = 0; s < NDEC; ++s) mbar_init(BAR(DEC + s), 1);
     for (int a = 0; a < NACC; ++a) mbar_init(BAR(ACC_FULL + a), 1), mbar_init(BAR(ACC_EMPTY + a), 8);
     mbar_init(BAR(A_FULL), 1);
     mbar_init(BAR(A_EMPTY), 1);
     *done_cum = 0;
-    for (int s = 0; s < NSB; ++s) stage_end[s] = 0, dec[s] = 0;
+    for (int s = 0; s < NSB; ++s) stage_end[s] = 0;
+    for (int s = 0; s < NDEC; ++s) dec[s] = 0;
     for (int a = 0; a < NACC; ++a) acc_end[a] = 0;
     fence_mbar_init();
   }
@@ -160,8 +167,8 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 mbar_arrive_cluster(F(BAR(DEC + ((g + 1) & 7))));
               }
             } else if (g > 0) {
-              // (8 decision barriers: the leader runs at most NSB <= 24 units, i.e. fewer than 8 groups,
-              // ahead of the follower, so a barrier never advances twice before the follower's wait)
+              // (NDEC = 8 decision barriers: the leader runs at most NSB <= 8 tiles, i.e. fewer than 8
+              // groups, ahead of the follower, so a barrier never advances twice before its wait)
               mbar_wait_cluster(BAR(DEC + (g & 7)), (decph >> (g & 7)) & 1u);
               decph ^= 1u << (g & 7);
               end = dec[g & 7] != 0;
@@ -171,14 +178,12 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               break;
             }
           }
-          for (int kb = 0; kb < KB; ++kb) {
-            mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
-            const bool last = kb == KB - 1;
-            if (leader) mbar_arrive_expect_tx(BAR(R_FULL + stage), 2 * (last ? b_tail_bytes : (uint32_t)kBUnit));
-            tma_load_2d_cg2(sR + stage * kBUnit, last ? &tmBt : &tmB, kb * 64, it * BN + 64 * (int)rank,
-                            L(BAR(R_FULL + stage)));
-            next();
-          }
+          mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(BAR(R_FULL + stage), 2 * b_bytes);
+          for (int kb = 0; kb < KB; ++kb)
+            tma_load_2d_cg2(sR + stage * TS + kb * kBUnit, kb == KB - 1 ? &tmBt : &tmB, kb * 64,
+                            it * BN + 64 * (int)rank, L(BAR(R_FULL + stage)));
+          next();
         }
       }
     }
@@ -194,7 +199,7 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if (++stage == NSB) stage = 0, ph ^= 1;
       };
       auto bdesc_of = [&](int kb) {
-        const uint32_t a = sR + stage * kBUnit;
+        const uint32_t a = sR + stage * TS + kb * kBUnit;
         return kb == KB - 1 ? sdesc_swz(a, 2 * tail) : sdesc_sw128(a);
       };
       for (int tp = pair; tp < num_tp; tp += npairs, ++t) {
@@ -232,23 +237,20 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             break;
           }
           const uint32_t d = tmem + as * C::ACC_COLS;
-          for (int kb = 0; kb < KB; ++kb) {
-            if (kb > 0) {
-              mbar_wait_sleep(BAR(R_FULL + stage), ph);
-              tc_fence_after();
-            }
-            if (elect_one()) {
+          if (elect_one()) {
+#pragma unroll
+            for (int kb = 0; kb < KB; ++kb) {
               const uint64_t bdesc = bdesc_of(kb);
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk)
                 if (4 * kb + kk < ksteps)
                   mma_f16_ts_cg2(d, tmem + C::A_TMEM + 8 * (4 * kb + kk), bdesc + (uint64_t)(2 * kk), idesc,
                                  (kb | kk) != 0);
-              mma_commit_cg2(BAR(R_EMPTY + stage), 3);
             }
-            __syncwarp();
-            next();
+            mma_commit_cg2(BAR(R_EMPTY + stage), 3);
           }
+          __syncwarp();
+          next();
           if (elect_one()) mma_commit_cg2(BAR(ACC_FULL + as), 3);
           __syncwarp();
           tiles_issued += 2;  // two 128 x 128 (user tile, item tile) contractions
