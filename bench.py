@@ -299,7 +299,14 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
         idx.close()
         return rec
 
+    # the clock sampler starts before the warm-up steps: nvidia-smi's start-up (NVML initialisation)
+    # stalled CUDA calls for ~0.2 s when it overlapped the first timed steps
+    sampler = ClockSampler(dev.index)
+    sampler.__enter__()
+    ts0 = time.perf_counter()
     for _ in range(warmup):
+        readout(*step())
+    while time.perf_counter() - ts0 < 2.0:  # at least 2 s of sampling before the timed region
         readout(*step())
     torch.cuda.synchronize()
     if ws > 1:
@@ -309,8 +316,7 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
     import gc
     gc.collect()
     gc.disable()  # (no collector pause inside the timed region; re-enabled right after it)
-    sampler = ClockSampler(dev.index)
-    with sampler:
+    try:
         tw0 = time.perf_counter()
         for _ in range(steps):
             flush.zero_()                               # L2 flush, outside the timed region
@@ -327,6 +333,8 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
             step_ms.append(e0.elapsed_time(e1))
             last = outs
         tw1 = time.perf_counter()
+    finally:
+        sampler.__exit__(None, None, None)
     gc.enable()
     clocks = sampler.summary(tw0, tw1)
     torch.cuda.synchronize()

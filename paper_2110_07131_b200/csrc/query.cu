@@ -217,30 +217,43 @@ k_query_simt(const __half* __restrict__ U16, int ldh, const float* __restrict__ 
 
 // ------------------------------------------------------------------------------ Q4
 // u in R_k(q) <=> dot64(q, u) >= tau_k(u)  (reading R8; same dot routine as the build).
-__global__ void k_exact_decide(const float* __restrict__ q, const float* __restrict__ U32,
-                               const double* __restrict__ tauk, const int32_t* __restrict__ perm_u, int d,
-                               unsigned long long* __restrict__ ctr, const uint64_t* __restrict__ und_list,
-                               AccSink acc_list, int64_t cap) {
+// One warp per undecided pair: the lanes load 32 coordinates of q and u at a time (coalesced) and form
+// their exact fp64 products; every lane then adds the products in index order, taking each one by a
+// broadcast shuffle, so the sum is dot64's left-to-right fp64 sum bit for bit (each product of two fp32
+// values is exact in fp64, so fma(a, b, s) and s + a*b round identically).
+__global__ void __launch_bounds__(256)
+k_exact_decide(const float* __restrict__ q, const float* __restrict__ U32, const double* __restrict__ tauk,
+               const int32_t* __restrict__ perm_u, int d, unsigned long long* __restrict__ ctr,
+               const uint64_t* __restrict__ und_list, AccSink acc_list, int64_t cap) {
   const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_UND_TOTAL]);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < total; base += stride) {
-    int64_t i = base + threadIdx.x;
-    bool ok = i < total;
-    bool yes = false;
-    uint64_t key = 0;
-    if (ok && und_list[i] == kSentinel) ok = false;  // unused reserved slot
-    if (ok) {
-      uint64_t rec = und_list[i];
-      uint32_t qin = (uint32_t)(rec >> 32);
-      int64_t row = (int64_t)(rec & 0xffffffffu);
-      double g = dot64(q + (int64_t)qin * d, U32 + row * d, d);
-      yes = g >= tauk[row];
-      key = ((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row];
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  unsigned n_und = 0, n_yes = 0;
+  for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < total; i += wstride) {
+    const uint64_t rec = und_list[i];
+    if (rec == kSentinel) continue;  // unused reserved slot (warp-uniform)
+    const uint32_t qin = (uint32_t)(rec >> 32);
+    const int64_t row = (int64_t)(rec & 0xffffffffu);
+    const float* qa = q + (int64_t)qin * d;
+    const float* ua = U32 + row * d;
+    double g = 0.0;
+    for (int c = 0; c < d; c += 32) {
+      const double pc = c + lane < d ? (double)__ldg(qa + c + lane) * (double)__ldg(ua + c + lane) : 0.0;
+      const int nj = min(32, d - c);
+      for (int jj = 0; jj < nj; ++jj) g = __dadd_rn(g, __shfl_sync(0xffffffffu, pc, jj));
     }
-    warp_count(ok, ctr + C_UNDECIDED);
-    warp_count(yes, ctr + C_EXACT_ACCEPT);
-    acc_list.put(yes, key, ctr + C_ACCEPTED_TOTAL, cap);
-    warp_count(yes, ctr + C_ACC_REAL);
+    ++n_und;
+    if (g >= tauk[row]) {  // u in R_k(q) <=> dot64(q, u) >= tau_k(u)  (reading R8)
+      ++n_yes;
+      if (lane == 0) acc_list.put_one(((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row], ctr + C_ACCEPTED_TOTAL, cap);
+    }
+  }
+  if (lane == 0 && n_und) {
+    atomicAdd(ctr + C_UNDECIDED, (unsigned long long)n_und);
+    if (n_yes) {
+      atomicAdd(ctr + C_EXACT_ACCEPT, (unsigned long long)n_yes);
+      atomicAdd(ctr + C_ACC_REAL, (unsigned long long)n_yes);
+    }
   }
 }
 
@@ -473,7 +486,7 @@ cudaError_t query_exact(QueryCtx& c, cudaStream_t st) {
                                                            x->d, x->pd, c.k, c.counters, c.und, AccSink{c.acc, c.bits, c.nw}, c.cap,
                                                            x->mprime, c.scan_cnt); count_launch();
   } else {
-    k_exact_decide<<<148, 256, 0, st>>>(c.q, x->U32, x->tau + (int64_t)(c.k - 1) * x->n, x->perm_u, x->d,
+    k_exact_decide<<<148 * 4, 256, 0, st>>>(c.q, x->U32, x->tau + (int64_t)(c.k - 1) * x->n, x->perm_u, x->d,
                                             c.counters, c.und, AccSink{c.acc, c.bits, c.nw}, c.cap); count_launch();
   }
   return cudaGetLastError();

@@ -376,26 +376,59 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
       const int N = (len + 15) & ~15;
       const uint32_t idesc = idesc_f16_f32(kBM, N);
       const uint32_t d = tmem + as * kAccCols;
-      for (int kb = 0; kb < kbn; ++kb) {
-        {
+      if (!kStreamQ) {
+        // the work item's KB units are all awaited first, then one elected MMA chain (13 MMAs at
+        // d = 200) with one commit per unit: the MMA warp's per-item overhead does not scale with KB
+        int st_ = stage;
+        uint32_t ph_ = ph;
+        for (int kb = 0; kb < kbn; ++kb) {
           QPROF_T0();
-          mbar_wait(BAR(A_FULL + stage), ph);
+          mbar_wait(BAR(A_FULL + st_), ph_);
           QPROF_ADD(2);
+          if (++st_ == kStages) st_ = 0, ph_ ^= 1;
         }
         tc_fence_after();
-        const bool last = kb == kbn - 1;  // the tail K block has its own swizzle (tail_cols)
-        const uint32_t ua = sA + stage * kUnit, qa = kStreamQ ? ua + kUTileBytes : sQ + kb * kQTileBytes;
-        const uint64_t adesc = last ? sdesc_swz(ua, 2 * tail) : sdesc_sw128(ua);
-        const uint64_t bdesc = last ? sdesc_swz(qa, 2 * tail) : sdesc_sw128(qa);
-        const int kk_end = min(4, ksteps - 4 * kb);  // zero-padding K steps are skipped
         if (elect_one()) {
+          int su = stage;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)  // K advance: 32 bytes = 2 in the 16-byte address field
-            if (kk < kk_end) mma_f16(d, adesc + (uint64_t)(2 * kk), bdesc + (uint64_t)(2 * kk), idesc, (kb | kk) != 0);
-          mma_commit(BAR(A_EMPTY + stage));
+          for (int kb = 0; kb < KB; ++kb) {
+            const bool last = kb == KB - 1;  // the tail K block has its own swizzle (tail_cols)
+            const uint32_t ua = sA + su * kUnit, qa = sQ + kb * kQTileBytes;
+            const uint64_t adesc = last ? sdesc_swz(ua, 2 * tail) : sdesc_sw128(ua);
+            const uint64_t bdesc = last ? sdesc_swz(qa, 2 * tail) : sdesc_sw128(qa);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)  // K advance: 32 bytes = 2 in the 16-byte address field
+              if (4 * kb + kk < ksteps)
+                mma_f16(d, adesc + (uint64_t)(2 * kk), bdesc + (uint64_t)(2 * kk), idesc, (kb | kk) != 0);
+            mma_commit(BAR(A_EMPTY + su));
+            if (++su == kStages) su = 0;
+          }
         }
         __syncwarp();
-        if (++stage == kStages) stage = 0, ph ^= 1;
+        stage = st_;
+        ph = ph_;
+      } else {  // KB = 0: per unit (the queries' K blocks stream with the users')
+        for (int kb = 0; kb < kbn; ++kb) {
+          {
+            QPROF_T0();
+            mbar_wait(BAR(A_FULL + stage), ph);
+            QPROF_ADD(2);
+          }
+          tc_fence_after();
+          const bool last = kb == kbn - 1;  // the tail K block has its own swizzle (tail_cols)
+          const uint32_t ua = sA + stage * kUnit, qa = kStreamQ ? ua + kUTileBytes : sQ + kb * kQTileBytes;
+          const uint64_t adesc = last ? sdesc_swz(ua, 2 * tail) : sdesc_sw128(ua);
+          const uint64_t bdesc = last ? sdesc_swz(qa, 2 * tail) : sdesc_sw128(qa);
+          const int kk_end = min(4, ksteps - 4 * kb);  // zero-padding K steps are skipped
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)  // K advance: 32 bytes = 2 in the 16-byte address field
+              if (kk < kk_end) mma_f16(d, adesc + (uint64_t)(2 * kk), bdesc + (uint64_t)(2 * kk), idesc, (kb | kk) != 0);
+            mma_commit(BAR(A_EMPTY + stage));
+          }
+          __syncwarp();
+          if (++stage == kStages) stage = 0, ph ^= 1;
+        }
       }
       if (elect_one()) mma_commit(BAR(ACC_FULL + as));
       __syncwarp();
