@@ -540,7 +540,7 @@ def main():
         if c == args.config:
             continue
         r = run_config(c, args, dev, rank, ws, args.extra_steps, 3, pusers(c), e2e=False, cpu=False)
-        extras["cfg%d" % c] = {kk: r[kk] for kk in ("value", "ms_per_step", "step_ms", "host_ms", "config", "build", "query", "roofline",
+        extras["cfg%d" % c] = {kk: r[kk] for kk in ("value", "ms_per_step", "step_ms", "host_ms", "host_build_ms", "config", "build", "query", "roofline",
                                                     "roofline_query", "clocks", "parity") if kk in r}
         if c == 2 and args.k == 0:  # configs[2] sweeps k over {1, 5, 10, 25, 50}: the other k values
             from synth.generator import CONFIGS

@@ -229,23 +229,32 @@ k_exact_decide(const float* __restrict__ q, const float* __restrict__ U32, const
   const int lane = threadIdx.x & 31;
   const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
   unsigned n_und = 0, n_yes = 0;
-  for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < total; i += wstride) {
-    const uint64_t rec = und_list[i];
-    if (rec == kSentinel) continue;  // unused reserved slot (warp-uniform)
-    const uint32_t qin = (uint32_t)(rec >> 32);
-    const int64_t row = (int64_t)(rec & 0xffffffffu);
-    const float* qa = q + (int64_t)qin * d;
-    const float* ua = U32 + row * d;
-    double g = 0.0;
-    for (int c = 0; c < d; c += 32) {
-      const double pc = c + lane < d ? (double)__ldg(qa + c + lane) * (double)__ldg(ua + c + lane) : 0.0;
-      const int nj = min(32, d - c);
-      for (int jj = 0; jj < nj; ++jj) g = __dadd_rn(g, __shfl_sync(0xffffffffu, pc, jj));
-    }
-    ++n_und;
-    if (g >= tauk[row]) {  // u in R_k(q) <=> dot64(q, u) >= tau_k(u)  (reading R8)
-      ++n_yes;
-      if (lane == 0) acc_list.put_one(((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row], ctr + C_ACCEPTED_TOTAL, cap);
+  // each warp scans 32 list slots at a time (the filter reserves slots in blocks, so most are sentinel
+  // padding) and runs the exact dot product of every real pair among them
+  for (int64_t i0 = (blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; i0 < total; i0 += wstride * 32) {
+    const uint64_t mine = i0 + lane < total ? und_list[i0 + lane] : kSentinel;
+    uint32_t live = __ballot_sync(0xffffffffu, mine != kSentinel);
+    while (live) {
+      const int src = __ffs(live) - 1;
+      live &= live - 1;
+      const uint64_t rec = __shfl_sync(0xffffffffu, mine, src);
+      const uint32_t qin = (uint32_t)(rec >> 32);
+      const int64_t row = (int64_t)(rec & 0xffffffffu);
+      const float* qa = q + (int64_t)qin * d;
+      const float* ua = U32 + row * d;
+      double g = 0.0;
+      for (int c = 0; c < d; c += 32) {
+        const double pc = c + lane < d ? (double)__ldg(qa + c + lane) * (double)__ldg(ua + c + lane) : 0.0;
+        const int nj = min(32, d - c);
+#pragma unroll 8
+        for (int jj = 0; jj < nj; ++jj) g = __dadd_rn(g, __shfl_sync(0xffffffffu, pc, jj));
+      }
+      ++n_und;
+      if (g >= tauk[row]) {  // u in R_k(q) <=> dot64(q, u) >= tau_k(u)  (reading R8)
+        ++n_yes;
+        if (lane == 0)
+          acc_list.put_one(((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row], ctr + C_ACCEPTED_TOTAL, cap);
+      }
     }
   }
   if (lane == 0 && n_und) {
