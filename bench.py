@@ -247,14 +247,32 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
     from paper_2110_07131_b200 import rmips
     from synth import make_workload
 
-    w = make_workload(cfg, seed=0)
-    if rank > 0:
-        w.U = make_workload(cfg, seed=rank).U
-    spec = w.spec
+    from paper_2110_07131_b200.shard import gather_csr, user_shard
+    from synth.generator import CONFIGS
+
+    # N > 1: ONE problem sharded by users -- rank 0 generates the workload and
+    # broadcasts the users, the items and the queries over NCCL; each rank keeps its contiguous user
+    # range [a, b), builds its own index and answers every query batch; the per-query lists are
+    # exchanged device-side (shard.gather_csr) inside the timed step.  Strong scaling: the total work is
+    # the config's, whatever N.
+    spec = CONFIGS[cfg]
+    w = make_workload(cfg, seed=0) if rank == 0 else None
     k = k or args.k or spec.ks[-1]
-    U = torch.from_numpy(w.U).to(dev)
-    P = torch.from_numpy(w.P).to(dev)
-    Qy = torch.from_numpy(w.Qy).to(dev)
+    if ws > 1:
+        nq_eff = spec.nq if spec.query_mode != "from_p" else min(spec.nq, spec.m)
+        Uf = torch.from_numpy(w.U).to(dev) if rank == 0 else torch.empty(spec.n, spec.d, device=dev)
+        P = torch.from_numpy(w.P).to(dev) if rank == 0 else torch.empty(spec.m, spec.d, device=dev)
+        Qy = torch.from_numpy(w.Qy).to(dev) if rank == 0 else torch.empty(nq_eff, spec.d, device=dev)
+        for t_ in (Uf, P, Qy):
+            torch.distributed.broadcast(t_, 0)
+        sa, sb = user_shard(spec.n, ws, rank)
+        U = Uf[sa:sb].contiguous()
+        del Uf
+    else:
+        sa, sb = 0, spec.n
+        U = torch.from_numpy(w.U).to(dev)
+        P = torch.from_numpy(w.P).to(dev)
+        Qy = torch.from_numpy(w.Qy).to(dev)
     batches = _batches(spec.nq, spec.batch)
     Qb = [Qy[a:b] for a, b in batches]
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -277,8 +295,10 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
         outs, qph = [], []
         for q in Qb:
             off, ids = rmips.rmips_query(idx, q, k, qflags, capacity=cap[0])
-            outs.append((off, ids))
             qph.append((idx.phase_times(), idx.stats()))
+            if ws > 1:  # the exchange step: every rank gets the global lists (NCCL all_gathers)
+                off, ids = gather_csr(off, ids, sa)
+            outs.append((off, ids))
         return idx, outs, qph
 
     def readout(idx, outs, qph):
@@ -307,7 +327,10 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
     for _ in range(warmup):
         readout(*step())
     while time.perf_counter() - ts0 < 2.0:  # at least 2 s of sampling before the timed region
-        readout(*step())
+        if ws > 1:  # (every rank must run the same steps: their collectives pair up)
+            time.sleep(0.05)
+        else:
+            readout(*step())
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
@@ -345,8 +368,8 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
         t_max = float(t.item())
     else:
         t_max = t_rank
-    units_step = spec.n * spec.m + spec.nq * spec.n
-    value = ws * units_step * steps / (t_max / 1e3)
+    units_step = spec.n * spec.m + spec.nq * spec.n  # the whole config, split over the ws ranks
+    value = units_step * steps / (t_max / 1e3)
     ms_per_step = t_max / steps
     med = lambda key: float(np.median([r[key] for r in recs]))  # noqa: E731
     peaks = _peaks()
@@ -432,9 +455,9 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
 
     # ---- end to end through the public API with HOST buffers (copies inside the timed region)
     if e2e:
-        Uh = torch.from_numpy(w.U).pin_memory()
-        Ph = torch.from_numpy(w.P).pin_memory()
-        Qh = [torch.from_numpy(np.ascontiguousarray(w.Qy[a:b])).pin_memory() for a, b in batches]
+        Uh = U.cpu().pin_memory()  # this rank's users (all of them at N = 1)
+        Ph = P.cpu().pin_memory()
+        Qh = [Qy[a:b].cpu().pin_memory() for a, b in batches]
         offh = [torch.empty(b - a + 1, dtype=torch.int64).pin_memory() for a, b in batches]
         idsh = torch.empty(cap[0], dtype=torch.int32).pin_memory()
         e2e_ms, d2h = [], 0
@@ -448,7 +471,10 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
             d2h = 0
             for j, q in enumerate(Qh):
                 off, ids = rmips.rmips_query_host(idx, q, k, out_offsets=offh[j], out_ids=idsh, capacity=idsh.numel())
-                d2h += 8 * int(offh[j].numel()) + 4 * int(len(ids))
+                if ws > 1:  # the exchange: this rank's host lists -> device -> NCCL gather -> host
+                    g_off, g_ids = gather_csr(off.to(dev, non_blocking=True), ids.to(dev, non_blocking=True), sa)
+                    off, ids = g_off.cpu(), g_ids.cpu()
+                d2h += 8 * int(off.numel()) + 4 * int(len(ids))
             e1.record(stream)
             torch.cuda.synchronize()
             idx.close()
@@ -459,14 +485,17 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
             t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             t_e2e = float(t.item())
-        res["e2e"] = {"value": ws * units_step * steps / (t_e2e / 1e3), "unit": UNIT,
-                      "h2d_bytes_per_step": 4 * spec.d * (spec.n + spec.m + spec.nq), "d2h_bytes_per_step": d2h,
+        res["e2e"] = {"value": units_step * steps / (t_e2e / 1e3), "unit": UNIT,
+                      "h2d_bytes_per_step": 4 * spec.d * ((sb - sa) + spec.m + spec.nq), "d2h_bytes_per_step": d2h,
                       "ms_per_step": t_e2e / steps,
-                      "api": "rmips_build_index_host + %d rmips_query_host calls (pinned host buffers)" % len(batches)}
+                      "api": "rmips_build_index_host + %d rmips_query_host calls (pinned host buffers)%s"
+                             % (len(batches), " + shard.gather_csr per call" if ws > 1 else "")}
     del U, P, Qy, Qb, flush
     torch.cuda.empty_cache()
 
     if rank == 0 and (cpu or parity_users):
+        if w is None:
+            w = make_workload(cfg, seed=0)
         cores = os.cpu_count() or 1
         if cpu and ws == 1:
             base, orc = cpu_baseline(w, k, parity_users, args.cpu_users_1t)
@@ -527,10 +556,11 @@ def main():
     head = run_config(args.config, args, dev, rank, ws, args.steps, args.warmup, pusers(args.config, 5e10),
                       e2e=not args.no_e2e, cpu=not args.no_cpu_baseline)
     line = {"metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong" if ws > 1 else "weak",
             "vs_baseline": None, "dtype": "fp16 filter (fp32 accumulate) + f64 exact decisions",
-            "data": "synthetic (SURVEY Appendix C generator, seed 0; users seed = rank); stands in for the paper's "
-                    "MF vectors (P:571-587), configs[4] is beyond the paper"}
+            "data": "synthetic (SURVEY Appendix C generator, seed 0; at N > 1 one problem split by users); stands in "
+                    "for the paper's MF vectors (P:571-587), configs[4] is beyond the paper"}
     for key in ("step_ms", "host_ms", "host_build_ms", "config", "build", "query", "roofline", "roofline_query", "roofline_scan", "index", "clocks",
                 "gpu_launches", "e2e", "cpu_baseline", "parity"):
         if key in head:

@@ -1,16 +1,19 @@
-"""N > 1 path on CPU (world_size 2, gloo): user sharding and the gathered result sets equal the
-single-process answer.  The per-rank reverse k-MIPS here is the oracle (this is the host-side
-plumbing test; the GPU path per rank is the same C ABI the parity tests cover)."""
+"""N > 1 path on CPU (world_size 2 and 3, gloo): user sharding and the device-side CSR gather
+(shard.gather_csr: all_gather of counts, padded all_gather of ids, scatter into the global CSR) give
+the single-process answer.  The per-rank reverse k-MIPS here is the oracle (this is the host-side
+plumbing test; tests/test_multigpu.py runs the same gather over NCCL with the CUDA path per rank when
+two GPUs are present)."""
 import os
 import socket
 
 import numpy as np
 import pytest
+import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_2110_07131_b200.shard import gather_sets, merge_shards, user_shard
+from paper_2110_07131_b200.shard import gather_csr, merge_shards, user_shard
 from synth import generator as gen
 
 
@@ -35,11 +38,9 @@ def _worker(rank, world, port, U, P, Qy, k, out_path):
     try:
         a, b = user_shard(U.shape[0], world, rank)
         off, ids = _csr(oracle.rkmips_naive(U[a:b], P, Qy, k))  # shard-local user ids
-        g_off, g_ids = gather_sets(off, ids, a)
-        if rank == 0:
-            np.savez(out_path, off=g_off, ids=g_ids)
+        g_off, g_ids = gather_csr(torch.from_numpy(off), torch.from_numpy(ids.astype(np.int32)), a)
+        np.savez(out_path + ".%d.npz" % rank, off=g_off.numpy(), ids=g_ids.numpy())
         # the timing reduction bench.py uses (max over ranks)
-        import torch
         t = torch.tensor([float(rank + 1)], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         assert t.item() == world
@@ -65,13 +66,15 @@ def test_merge_shards_keeps_ascending_order():
 
 
 @pytest.mark.timeout(300)
-def test_two_rank_gloo_gather_equals_single_process(tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_gather_csr_equals_single_process(tmp_path, world):
     U, P = gen.random_instance(31, 301, 90, 12, "skewed")
     Qy = np.concatenate([P[:10], gen.random_instance(32, 6, 1, 12, "skewed")[0]])
     k = 5
-    out = str(tmp_path / "r0.npz")
-    mp.spawn(_worker, args=(2, _free_port(), U, P, Qy, k, out), nprocs=2, join=True)
-    got = np.load(out)
+    out = str(tmp_path / "r")
+    mp.spawn(_worker, args=(world, _free_port(), U, P, Qy, k, out), nprocs=world, join=True)
     want_off, want_ids = _csr(oracle.rkmips_naive(U, P, Qy, k))
-    assert np.array_equal(got["off"], want_off)
-    assert np.array_equal(got["ids"], want_ids)
+    for r in range(world):  # every rank holds the global result
+        got = np.load(out + ".%d.npz" % r)
+        assert np.array_equal(got["off"], want_off)
+        assert np.array_equal(got["ids"], want_ids)
