@@ -341,7 +341,7 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
     gc.disable()  # (no collector pause inside the timed region; re-enabled right after it)
     try:
         tw0 = time.perf_counter()
-        for _ in range(steps):
+        for si in range(steps):
             flush.zero_()                               # L2 flush, outside the timed region
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
@@ -354,7 +354,10 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
             torch.cuda.synchronize()
             recs.append(readout(idx, outs, qph))        # (frees the index: stream-ordered, after e1)
             step_ms.append(e0.elapsed_time(e1))
-            last = outs
+            if si == steps - 1:
+                last = outs  # (only the last step's lists are kept: the device memory of every step is
+                             # reused by the next, so no step allocates more than the warm-up ones did)
+            del outs
         tw1 = time.perf_counter()
     finally:
         sampler.__exit__(None, None, None)
