@@ -190,7 +190,7 @@ void extend_lists(rmips_index_s* x, int kmax_new, cudaStream_t st) {
   }
   Arena la;
   const size_t o_tau = la.take<double>((int64_t)kmax_new * n), o_ids = la.take<int32_t>((int64_t)kmax_new * n),
-               o_thr = la.take<float>((int64_t)kmax_new * n), o_tb = la.take<float>((int64_t)kmax_new * x->nblocks);
+               o_thr = la.take<float>((int64_t)kmax_new * n), o_tb = la.take<float>((int64_t)kmax_new * x->nlb);
   void* larena = nullptr;
   CK(cudaMallocAsync(&larena, la.off, st));
   BuildCtx c;
@@ -301,6 +301,12 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
   x->ldh = round_up(d, 16);
   x->pd = round_up(d, 8);
   x->nblocks = (n + kTileU - 1) / kTileU;
+  if (x->mprime < m) {  // P' index: blocks of ceil(log2 n) users (the paper's O(log n))
+    int lg = 1;
+    while (((int64_t)1 << lg) < n) ++lg;
+    x->bsz = lg;
+  }
+  x->nlb = (n + x->bsz - 1) / x->bsz;
   x->c1 = filter_c1(x->dpad);
   x->c2 = filter_c2(x->dpad);
   cudaGetDevice(&x->device);
@@ -318,7 +324,7 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
                  o_u16 = ia.take<__half>(n * x->ldh), o_u32 = ia.take<float>(n * d),
                  o_p16 = ia.take<__half>(m * x->ldh), o_p32 = ia.take<float>(m * x->pd),
                  o_tau = ia.take<double>((int64_t)k_max * n), o_ids = ia.take<int32_t>((int64_t)k_max * n),
-                 o_thr = ia.take<float>((int64_t)k_max * n), o_tb = ia.take<float>((int64_t)k_max * x->nblocks);
+                 o_thr = ia.take<float>((int64_t)k_max * n), o_tb = ia.take<float>((int64_t)k_max * x->nlb);
     CK(cudaMallocAsync(&x->arena, ia.off, st));
     char* A = static_cast<char*>(x->arena);
     x->d_flags = reinterpret_cast<int*>(A + o_flags);
@@ -477,6 +483,7 @@ static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cuda
          oqc = take((size_t)nsub * 4), oqnr = take((size_t)nsub * kQB * 8), oqcm = take((size_t)nsub * kQB / 8 * 4),
          owl = take((size_t)nsub * x->nblocks * 4), oacc = take((size_t)cap * 8),
          ound = take((size_t)cap * 8), oscn = take((size_t)cap * 4),
+         osrec = take((size_t)cap * 8), osbt = take((size_t)cap * 4),
          osrt = take((size_t)cap * 8), ocub = take(qcub), obits = take(use_bits ? (size_t)c.b * nw * 4 : 0);
   if (off > x->ws_bytes) {
     x->bits_len = 0;
@@ -498,6 +505,8 @@ static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cuda
   c.acc = reinterpret_cast<uint64_t*>(b + oacc);
   c.und = reinterpret_cast<uint64_t*>(b + ound);
   c.scan_cnt = reinterpret_cast<int32_t*>(b + oscn);
+  c.scan_rec = reinterpret_cast<uint64_t*>(b + osrec);
+  c.scan_beats = reinterpret_cast<int32_t*>(b + osbt);
   c.acc_sorted = reinterpret_cast<uint64_t*>(b + osrt);
   c.cub_tmp = b + ocub;
   c.bits = use_bits ? reinterpret_cast<uint32_t*>(b + obits) : nullptr;
@@ -692,7 +701,7 @@ rmips_status_t rmips_index_info(rmips_index_t idx, int64_t info[16]) {
   info[11] = idx->build_kernel;
   info[12] = idx->cand_slots;
   info[0] = idx->n; info[1] = idx->m; info[2] = idx->d; info[3] = idx->kmax;
-  info[4] = idx->dpad; info[5] = kTileU; info[6] = idx->overflow_rows; info[7] = idx->build_flags;
+  info[4] = idx->dpad; info[5] = idx->bsz; info[6] = idx->overflow_rows; info[7] = idx->build_flags;
   return RMIPS_OK;
 }
 

@@ -634,13 +634,13 @@ k_exact_row_full(const float* __restrict__ U32, const float* __restrict__ P32, c
 // One warp per (block B, rank j): the block's kTileU values of column j are read coalesced (lane
 // r reads rows lo + r, lo + r + 32, ...) and min-reduced.
 __global__ void k_blocks(const double* __restrict__ tau, const double* __restrict__ unorm, int64_t n, int kmax,
-                         int64_t nblocks, float* __restrict__ tb) {
+                         int64_t nblocks, int bsz, float* __restrict__ tb) {
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (wid >= nblocks * kmax) return;
   const int64_t B = wid % nblocks;
   const int j = (int)(wid / nblocks);
-  const int64_t lo = B * kTileU, hi = min(n, lo + kTileU);
+  const int64_t lo = B * bsz, hi = min(n, lo + bsz);
   double L = CUDART_INF;
   for (int64_t i = lo + lane; i < hi; i += 32) L = fmin(L, tau[(int64_t)j * n + i]);
 #pragma unroll
@@ -908,7 +908,8 @@ cudaError_t build_fallback(BuildCtx& c, int nrows, double* scratch, int grid, cu
 cudaError_t build_blocks(BuildCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   if (x->n == 0) return cudaSuccess;
-  k_blocks<<<nblk(x->nblocks * x->kmax * 32, 256), 256, 0, st>>>(x->tau, x->unorm, x->n, x->kmax, x->nblocks, x->tb);
+  k_blocks<<<nblk(x->nlb * x->kmax * 32, 256), 256, 0, st>>>(x->tau, x->unorm, x->n, x->kmax, x->nlb, x->bsz,
+                                                             x->tb);
   count_launch();
   return cudaGetLastError();
 }

@@ -112,6 +112,25 @@ struct AccSink {
   }
 };
 
+// Lemma 3 over the blocks of bsz users that overlap the 128-user tile t: len = the longest
+// norm-sorted query prefix any of them keeps (the tile's MMA N; the rows of blocks with shorter
+// prefixes reject the extra pairs exactly by Lemma 1), and the (block, query) pair counts of the blocks
+// whose first user lies in the tile (every block is counted once).  len_of(tb) = #{queries : ||q|| >= tb}.
+template <class LenFn>
+__device__ __forceinline__ int tile_lemma3(int64_t t, int bsz, int64_t nlb, int cnt, bool no_blocks,
+                                           const float* __restrict__ tbk, LenFn len_of,
+                                           unsigned long long& pairs, unsigned long long& pruned) {
+  const int64_t r0 = t * kTileU, r1 = r0 + kTileU;
+  const int64_t b_first = r0 / bsz, b_last = min(nlb - 1, (r1 - 1) / bsz);
+  int len = 0;
+  for (int64_t bl = b_first; bl <= b_last; ++bl) {
+    const int l = len_of(no_blocks ? -CUDART_INF_F : tbk[bl]);
+    len = max(len, l);
+    if (bl * bsz >= r0) pairs += cnt, pruned += cnt - l;
+  }
+  return len;
+}
+
 __device__ __forceinline__ void warp_count(bool pred, unsigned long long* ctr) {
   uint32_t bal = __ballot_sync(0xffffffffu, pred);
   if ((threadIdx.x & 31) == __ffs(bal | 0x80000000u) - 1 && bal) atomicAdd(ctr, (unsigned long long)__popc(bal));
@@ -148,7 +167,10 @@ struct rmips_index_s {
                             // dpad = d rounded up to 64 is the K-block geometry of the kernels
   int pd = 0;               // P32 row pitch in floats: d rounded up to 8 (whole 32-byte sectors)
   int device = 0;
-  int64_t nblocks = 0;
+  int64_t nblocks = 0;      // 128-user tiles (the kernels' work unit)
+  int bsz = rmips::kTileU;  // users per Lemma-3 block (Eq. 1): one tile for the exact index, ceil(log2 n)
+                            // for a P' index (the paper's O(log n))
+  int64_t nlb = 0;          // Lemma-3 blocks, ceil(n / bsz)
   int64_t overflow_rows = 0;
   int64_t cand_total = 0;   // candidates kept by the build filter (sum over non-overflowed rows)
   int64_t tiles_done = 0;   // (128-user tile, item tile) contractions issued by the tensor-core build
@@ -173,7 +195,7 @@ struct rmips_index_s {
   double* tau = nullptr;       // [kmax][n] (j+1)-th largest u.p over P, fp64 (sorted users)
   int32_t* ids = nullptr;      // [kmax][n] original item id of that value
   float* thr = nullptr;        // [kmax][n] tau/nu in fp32 (filter threshold, unscaled)
-  float* tb = nullptr;         // [kmax][nblocks] Lemma 3: L^j(B) / ||u_first(B)||, rounded down
+  float* tb = nullptr;         // [kmax][nlb] Lemma 3: L^j(B) / ||u_first(B)||, rounded down
 
   void* arena = nullptr;       // the single allocation every array above lives in
   void* list_arena = nullptr;  // tau / ids / thr / tb after an in-place extension of k_max (NEXT-2)

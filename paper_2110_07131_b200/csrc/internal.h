@@ -74,6 +74,8 @@ struct QueryCtx {
   int64_t nw = 0;                // words per query row of bits, ceil(n / 32)
   uint64_t* und = nullptr;       // undecided (q_input << 32 | sorted user position)
   int32_t* scan_cnt = nullptr;   // [cap] P' index: items of P' that beat q, for the scan after P'
+  uint64_t* scan_rec = nullptr;  // [cap] the pairs left for Alg. 2's scan, packed densely
+  int32_t* scan_beats = nullptr; // [cap] ... with the count of items already known to beat q
   int64_t cap = 0;               // capacity of acc and of und
   int64_t sorted_n = 0;          // keys sorted by query_sort (reserved slots, sentinels last)
   uint64_t* acc_sorted = nullptr;  // (also holds the 32-bit packed keys of the fast output path)

@@ -144,6 +144,7 @@ __device__ __forceinline__ int classify(float acc, float thr_s, float qe) {
 template <int DPAD>
 __global__ void __launch_bounds__(128)
 k_query_simt(const __half* __restrict__ U16, int ldh, const float* __restrict__ thrk, const float* __restrict__ tbk,
+             int bsz, int64_t nlb,
              const int32_t* __restrict__ perm_u, int64_t n, const __half* __restrict__ Q16,
              const float* __restrict__ qn, const float* __restrict__ qerr, const float* __restrict__ qscale,
              const int32_t* __restrict__ qperm, const int32_t* __restrict__ qcount, int flags,
@@ -157,11 +158,12 @@ k_query_simt(const __half* __restrict__ U16, int ldh, const float* __restrict__ 
   const int cnt = qcount[s];
   const float* qn_sub = qn + (int64_t)s * kQB;
   if (tid == 0) {
-    float tbv = (flags & RMIPS_FLAG_NO_BLOCKS) ? -CUDART_INF_F : tbk[tile];
-    int len = lemma3_prefix(qn_sub, cnt, tbv);
+    unsigned long long pairs = 0, pruned = 0;
+    const int len = tile_lemma3(tile, bsz, nlb, cnt, (flags & RMIPS_FLAG_NO_BLOCKS) != 0, tbk,
+                                [&](float tbv) { return lemma3_prefix(qn_sub, cnt, tbv); }, pairs, pruned);
     s_len = len;
-    atomicAdd(ctr + C_BLOCK_PAIRS, (unsigned long long)cnt);
-    atomicAdd(ctr + C_BLOCK_PRUNED, (unsigned long long)(cnt - len));
+    atomicAdd(ctr + C_BLOCK_PAIRS, pairs);
+    atomicAdd(ctr + C_BLOCK_PRUNED, pruned);
   }
   __syncthreads();
   const int len = s_len;
@@ -317,102 +319,184 @@ __global__ void k_exact_decide_pp(const float* __restrict__ q, const float* __re
 }
 
 // ------------------------------------------------------------------------------ Q5
-// Alg. 2 for one undecided pair per warp.  Items are visited in norm-descending order (Alg. 1
-// line 5), 32 per step, lane j taking item base + j straight from the sector-padded P32 rows
-// (consecutive lanes read consecutive rows: one contiguous 32 x pd x 4-byte stream per step).
-// Corollary 1 (yes): u.q >= ||u|| ||p_j|| (both rounded up to cover the fp64 rounding of every
-// later gamma) means no later item can beat q.  Corollary 2 (no): once k items have
-// gamma = p.u > u.q.  Falling off the end: yes (R4).
-// Each gamma is first scored in fp32 (four independent FMA chains over the zero-padded row,
-// u from shared memory) with a rigorous bound |s - dot64(p, u)| <= E = (gamma32(pd/4 + 2) +
-// gamma64(d)) ||p|| ||u|| (rounded up, plus an absolute term for subnormal products); only items
-// with |s - u.q| <= E (or a non-finite s) are re-evaluated with dot64, so every "beats" decision
-// is the exact fp64 one of the oracle (reading R7).
-// start / beats0: the scan begins at item `start` with beats0[i] items already known to beat q
-// (P' index: start = mprime, beats0 = c' from k_exact_decide_pp); 0 / NULL scans all of P.
+// Alg. 2 with Corollaries 1-2, readings R3/R4, for the undecided pairs.
+// Items are visited in norm-descending order (Alg. 1 line 5).  Corollary 1 (yes): u.q >= ||u|| ||p_j||
+// (both rounded up to cover the fp64 rounding of every later gamma) means no later item can beat q.
+// Corollary 2 (no): once k items have gamma = p.u > u.q.  Falling off the end: yes (R4).
+// Each gamma is first scored in fp32 (four independent FMA chains over the zero-padded row) with a
+// rigorous bound |s - dot64(p, u)| <= E = (gamma32(pd/4 + 2) + gamma64(d)) ||p|| ||u|| (rounded up,
+// plus an absolute term for subnormal products); only items with |s - u.q| <= E (or a non-finite s)
+// are re-evaluated with the left-to-right fp64 sum, so every "beats" decision is the oracle's (R7).
+//
+// Layout (north star (d)): the scan streams the norm-sorted P32 through SHARED MEMORY, one tile of
+// kScanRows rows at a time, and every warp of the CTA scores its pairs against the staged tile: a CTA
+// batch of up to 32 pairs reads each tile from L2 / HBM once instead of once per pair.  Lane l scores
+// item row l of a 32-row step (rows staged at an odd number of float4s per row: conflict-free 128-bit
+// loads); the pair's u is broadcast from shared memory.  The batch ends when every pair decided.
+// k_scan_compact first packs the real pairs (the exact-decide pass leaves sentinels) densely.
+// start / beats0: the scan begins at item `start` with beats0 items already known to beat q (P' index:
+// start = mprime, beats0 = c' from k_exact_decide_pp); 0 / NULL scans all of P.
 constexpr int kScanWarps = 8;
+constexpr int C_SCAN_LIST = kNumCounters;  // (spare counter slot) pairs in the dense scan list
+__global__ void k_scan_compact(const uint64_t* __restrict__ und_list, const int32_t* __restrict__ beats0,
+                               unsigned long long* __restrict__ ctr, int64_t cap, uint64_t* __restrict__ out_rec,
+                               int32_t* __restrict__ out_beats) {
+  const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_UND_TOTAL]);
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < total; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const uint64_t rec = i < total ? und_list[i] : kSentinel;
+    const bool live = rec != kSentinel;
+    const uint32_t bal = __ballot_sync(0xffffffffu, live);
+    if (!bal) continue;
+    unsigned long long base = 0;
+    if (lane == __ffs(bal) - 1) base = atomicAdd(ctr + C_SCAN_LIST, (unsigned long long)__popc(bal));
+    base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+    if (live) {
+      const unsigned long long pos = base + __popc(bal & lanemask_lt());
+      out_rec[pos] = rec;
+      out_beats[pos] = beats0 ? beats0[i] : 0;
+    }
+  }
+}
+
+// pw pairs per warp (4 for pd <= 256, else 1); rows staged per tile: 64 (pd <= 256) or 32
 __global__ void __launch_bounds__(32 * kScanWarps)
 k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const double* __restrict__ unorm,
               const float* __restrict__ P32, const double* __restrict__ pnorm, const int32_t* __restrict__ perm_u,
               int64_t m, int d, int pd, int k, unsigned long long* __restrict__ ctr,
-              const uint64_t* __restrict__ und_list, AccSink acc_list, int64_t cap, int64_t start,
-              const int32_t* __restrict__ beats0) {
-  extern __shared__ __align__(16) float su[];  // [kScanWarps][pd]: the pair's u, fp32, zero-padded to pd
+              const uint64_t* __restrict__ scan_rec, const int32_t* __restrict__ scan_beats, AccSink acc_list,
+              int64_t cap, int64_t start, bool count_undecided, int pw, int rows) {
+  extern __shared__ __align__(16) float ssc[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float* uw = su + (size_t)w * pd;
-  const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_UND_TOTAL]);
+  const int s4 = (pd / 4) | 1;                      // row stride in float4 (odd: conflict-free LDS.128)
+  float4* tile = reinterpret_cast<float4*>(ssc);    // [rows][s4]
+  float* su = ssc + (size_t)rows * s4 * 4;          // [kScanWarps * pw][pd]
+  __shared__ int s_live;
+  const int64_t npairs = (int64_t)min((unsigned long long)cap, ctr[C_SCAN_LIST]);
   const double slack = 1.0 + (d + 8) * 2.220446049250313e-16;
   const double n32 = pd / 4 + 2, g32 = n32 * 5.9604644775390625e-08 / (1.0 - n32 * 5.9604644775390625e-08);
   const double g64 = (d + 2) * 1.1102230246251565e-16 / (1.0 - (d + 2) * 1.1102230246251565e-16);
   const double efac = (g32 + g64) * slack * slack * (1.0 + 1e-6);
   const int nq4 = pd / 4;
-  for (int64_t i = blockIdx.x * (int64_t)kScanWarps + w; i < total; i += (int64_t)gridDim.x * kScanWarps) {
-    const uint64_t rec = und_list[i];
-    if (rec == kSentinel) continue;  // decided / unused slot (warp-uniform: one record per warp)
-    const uint32_t qin = (uint32_t)(rec >> 32);
-    const int64_t row = (int64_t)(rec & 0xffffffffu);
-    const float* u = U32 + row * d;
-    __syncwarp();
-    for (int t = lane; t < pd; t += 32) uw[t] = t < d ? __ldg(u + t) : 0.f;
-    __syncwarp();
-    const double uq = dot64(q + (int64_t)qin * d, u, d);
-    const double un = unorm[row];
-    const double unc = un * slack;
-    int beats = beats0 ? beats0[i] : 0;
+  const int per_cta = kScanWarps * pw;
+  constexpr int kMaxPw = 4;
+  for (int64_t b0 = (int64_t)blockIdx.x * per_cta; b0 < npairs; b0 += (int64_t)gridDim.x * per_cta) {
+    // this warp's pairs: u staged, u.q and ||u|| computed, state in registers (lane-uniform)
+    uint32_t qin[kMaxPw];
+    int64_t row[kMaxPw];
+    double uq[kMaxPw], un[kMaxPw];
+    int beats[kMaxPw];
+    bool active[kMaxPw], yes[kMaxPw];
     int64_t scanned = 0, exact = 0;
-    bool yes = true, decided = false;
-    for (int64_t base = start; base < m && !decided; base += 32) {
-      const int nrow = (int)min((int64_t)32, m - base);
-      const int64_t j = base + lane;
-      const bool in = lane < nrow;
-      const double pn = in ? pnorm[j] : 0.0;
-      const bool cor1 = in && (uq >= unc * pn * slack);
-      const uint32_t ycut = __ballot_sync(0xffffffffu, cor1);  // first lane where Cor. 1 fires
-      const int lim = ycut ? (__ffs(ycut) - 1) : nrow;
-      bool beat = false;
-      if (lane < lim) {
-        const float4* pr = reinterpret_cast<const float4*>(P32 + j * pd);
-        const float4* u4 = reinterpret_cast<const float4*>(uw);
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+    for (int p = 0; p < kMaxPw; ++p) {
+      const int64_t i = b0 + w * pw + p;
+      active[p] = p < pw && i < npairs;
+      yes[p] = true;
+      qin[p] = 0, row[p] = 0, uq[p] = 0.0, un[p] = 0.0, beats[p] = 0;
+      if (active[p]) {
+        const uint64_t rec = scan_rec[i];
+        qin[p] = (uint32_t)(rec >> 32);
+        row[p] = (int64_t)(rec & 0xffffffffu);
+        const float* u = U32 + row[p] * d;
+        float* uw = su + (size_t)(w * pw + p) * pd;
+        for (int t = lane; t < pd; t += 32) uw[t] = t < d ? __ldg(u + t) : 0.f;
+        uq[p] = dot64(q + (int64_t)qin[p] * d, u, d);
+        un[p] = unorm[row[p]];
+        beats[p] = scan_beats[i];
+      }
+    }
+    __syncwarp();
+    for (int64_t base = start; base < m; base += rows) {
+      // any pair of the CTA still undecided?  (also orders the previous tile's reads before the reload)
+      const bool mine = active[0] | active[1] | active[2] | active[3];
+      if (threadIdx.x == 0) s_live = 0;
+      __syncthreads();
+      if (mine && lane == 0) s_live = 1;
+      __syncthreads();
+      if (!s_live) break;
+      const int nrow = (int)min((int64_t)rows, m - base);
+      for (int r = w; r < nrow; r += kScanWarps) {  // stage the tile: one warp per row, float4 over the row
+        const float4* src = reinterpret_cast<const float4*>(P32 + (base + r) * pd);
+        for (int t = lane; t < nq4; t += 32) tile[r * s4 + t] = __ldg(src + t);
+      }
+      __syncthreads();
+      for (int st = 0; st < nrow; st += 32) {
+        const int nr = min(32, nrow - st);
+        const int64_t j = base + st + lane;
+        const bool in = lane < nr;
+        const double pn = in ? pnorm[j] : 0.0;
+        const float4* pr = tile + (st + lane) * s4;
+#pragma unroll
+        for (int p = 0; p < kMaxPw; ++p) {
+          if (!active[p]) continue;  // (warp-uniform)
+          const double unc = un[p] * slack;
+          const bool cor1 = in && (uq[p] >= unc * pn * slack);
+          const uint32_t ycut = __ballot_sync(0xffffffffu, cor1);  // first lane where Cor. 1 fires
+          const int lim = ycut ? (__ffs(ycut) - 1) : nr;
+          const float4* u4 = reinterpret_cast<const float4*>(su + (size_t)(w * pw + p) * pd);
+          bool beat = false;
+          if (lane < lim) {
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll 4
-        for (int t = 0; t < nq4; ++t) {
-          const float4 x = __ldg(pr + t), y = u4[t];
-          a0 = fmaf(x.x, y.x, a0);
-          a1 = fmaf(x.y, y.y, a1);
-          a2 = fmaf(x.z, y.z, a2);
-          a3 = fmaf(x.w, y.w, a3);
-        }
-        const float s = (a0 + a1) + (a2 + a3);
-        const double E = efac * pn * un + 1e-40;
-        const double sd = (double)s;
-        if (isfinite(s) && sd - E > uq) {
-          beat = true;
-        } else if (!(isfinite(s) && sd + E <= uq)) {  // inside the band: the exact fp64 value
-          double g = 0.0;
-          const float* prf = P32 + j * pd;
-          for (int t = 0; t < d; ++t) g = __fma_rn((double)__ldg(prf + t), (double)uw[t], g);
-          beat = g > uq;
-          ++exact;
+            for (int t = 0; t < nq4; ++t) {
+              const float4 x = pr[t], y = u4[t];
+              a0 = fmaf(x.x, y.x, a0);
+              a1 = fmaf(x.y, y.y, a1);
+              a2 = fmaf(x.z, y.z, a2);
+              a3 = fmaf(x.w, y.w, a3);
+            }
+            const float sc = (a0 + a1) + (a2 + a3);
+            const double E = efac * pn * un[p] + 1e-40;
+            const double sd = (double)sc;
+            if (isfinite(sc) && sd - E > uq[p]) {
+              beat = true;
+            } else if (!(isfinite(sc) && sd + E <= uq[p])) {  // inside the band: the exact fp64 value
+              const float* prf = reinterpret_cast<const float*>(pr);
+              const float* uf = su + (size_t)(w * pw + p) * pd;
+              double g = 0.0;
+              for (int t = 0; t < d; ++t) g = __fma_rn((double)prf[t], (double)uf[t], g);
+              beat = g > uq[p];
+              ++exact;
+            }
+          }
+          scanned += lim;
+          const uint32_t bb = __ballot_sync(0xffffffffu, beat);
+          // Alg. 2 visits items in order: the k-th beat (if any) decides "no"
+          const int nb = __popc(bb);
+          if (beats[p] + nb >= k) {
+            yes[p] = false;
+            active[p] = false;
+          } else if (ycut) {
+            active[p] = false;  // yes
+          }
+          beats[p] += nb;
         }
       }
-      scanned += lim;
-      const uint32_t bb = __ballot_sync(0xffffffffu, beat);
-      // Alg. 2 visits items in order: the k-th beat (if any) at lane position decides "no"
-      const int nb = __popc(bb);
-      if (beats + nb >= k) { yes = false; decided = true; }
-      else if (ycut) { yes = true; decided = true; }
-      beats += nb;
     }
     for (int o = 16; o; o >>= 1) exact += __shfl_xor_sync(0xffffffffu, exact, o);
     if (lane == 0) {
-      atomicAdd(ctr + C_SCANS, 1ull);
-      atomicAdd(ctr + C_ITEMS_SCANNED, (unsigned long long)scanned);
-      atomicAdd(ctr + C_SCAN_EXACT, (unsigned long long)exact);
-      if (!beats0) atomicAdd(ctr + C_UNDECIDED, 1ull);  // (P' index: counted by k_exact_decide_pp)
-      if (yes) {
-        atomicAdd(ctr + C_EXACT_ACCEPT, 1ull);
-        atomicAdd(ctr + C_ACC_REAL, 1ull);
-        acc_list.put_one(((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row], ctr + C_ACCEPTED_TOTAL, cap);
+      int nsc = 0, nyes = 0;
+#pragma unroll
+      for (int p = 0; p < kMaxPw; ++p) {
+        const int64_t i = b0 + w * pw + p;
+        if (p >= pw || i >= npairs) continue;
+        ++nsc;
+        if (yes[p]) {
+          ++nyes;
+          acc_list.put_one(((uint64_t)qin[p] << 32) | (uint64_t)(uint32_t)perm_u[row[p]], ctr + C_ACCEPTED_TOTAL, cap);
+        }
+      }
+      if (nsc) {
+        atomicAdd(ctr + C_SCANS, (unsigned long long)nsc);
+        atomicAdd(ctr + C_ITEMS_SCANNED, (unsigned long long)scanned);
+        atomicAdd(ctr + C_SCAN_EXACT, (unsigned long long)exact);
+        if (count_undecided) atomicAdd(ctr + C_UNDECIDED, (unsigned long long)nsc);  // (P': counted already)
+        if (nyes) {
+          atomicAdd(ctr + C_EXACT_ACCEPT, (unsigned long long)nyes);
+          atomicAdd(ctr + C_ACC_REAL, (unsigned long long)nyes);
+        }
       }
     }
   }
@@ -458,7 +542,7 @@ static cudaError_t launch_query_simt(QueryCtx& c, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)x->nblocks, (unsigned)c.nsub);
   k_query_simt<DPAD><<<grid, 128, smem, st>>>(x->U16, x->ldh, x->thr + (int64_t)(c.k - 1) * x->n,
-                                              x->tb + (int64_t)(c.k - 1) * x->nblocks, x->perm_u, x->n, c.Q16, c.qn,
+                                              x->tb + (int64_t)(c.k - 1) * x->nlb, x->bsz, x->nlb, x->perm_u, x->n, c.Q16, c.qn,
                                               c.qerr, c.qscale, c.qperm, c.qcount, c.flags, c.counters, AccSink{c.acc, c.bits, c.nw}, c.und,
                                               c.cap); count_launch();
   return cudaGetLastError();
@@ -475,25 +559,38 @@ cudaError_t query_filter_simt(QueryCtx& c, cudaStream_t st) {
   }
 }
 
+#define CK_RET(expr)                     \
+  do {                                   \
+    const cudaError_t e_ = (expr);       \
+    if (e_ != cudaSuccess) return e_;    \
+  } while (0)
+
+// Alg. 2 over the undecided pairs: compaction into the dense scan list, then the tiled scan.
+static cudaError_t launch_scan(QueryCtx& c, int64_t start, const int32_t* beats0, bool count_und, cudaStream_t st) {
+  rmips_index_s* x = c.idx;
+  k_scan_compact<<<148 * 4, 256, 0, st>>>(c.und, beats0, c.counters, c.cap, c.scan_rec, c.scan_beats);
+  count_launch();
+  const int pw = x->pd <= 256 ? 4 : 1, rows = x->pd <= 256 ? 64 : 32;
+  const int s4 = (x->pd / 4) | 1;
+  const size_t smem = (size_t)rows * s4 * 16 + (size_t)kScanWarps * pw * x->pd * sizeof(float);
+  if (smem > 48 * 1024) CK_RET(cudaFuncSetAttribute(k_verify_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_verify_scan<<<148 * 2, 32 * kScanWarps, smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m, x->d,
+                                                        x->pd, c.k, c.counters, c.scan_rec, c.scan_beats,
+                                                        AccSink{c.acc, c.bits, c.nw}, c.cap, start, count_und, pw, rows);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t query_exact(QueryCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   if (x->n == 0) return cudaSuccess;
-  const size_t scan_smem = (size_t)kScanWarps * x->pd * sizeof(float);
-  if (scan_smem > 48 * 1024 && (c.flags & RMIPS_FLAG_VERIFY_SCAN || x->mprime < x->m)) {
-    cudaError_t e = cudaFuncSetAttribute(k_verify_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem);
-    if (e != cudaSuccess) return e;
-  }
   if (c.flags & RMIPS_FLAG_VERIFY_SCAN) {  // every undecided pair scans all of P (Alg. 2)
-    k_verify_scan<<<148 * 8, 32 * kScanWarps, scan_smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
-                                                           x->d, x->pd, c.k, c.counters, c.und, AccSink{c.acc, c.bits, c.nw}, c.cap, 0,
-                                                           nullptr); count_launch();
+    CK_RET(launch_scan(c, 0, nullptr, true, st));
   } else if (x->mprime < x->m) {  // P' index: Lemmas 1-2 / Cor. 1 per pair, then the scan after P'
     k_exact_decide_pp<<<148 * 8, 256, 0, st>>>(c.q, x->U32, x->unorm, x->pnorm, x->tau, x->n, x->m, x->mprime, c.k,
                                                x->perm_u, x->d, c.counters, c.und, c.scan_cnt, AccSink{c.acc, c.bits, c.nw}, c.cap);
     count_launch();
-    k_verify_scan<<<148 * 8, 32 * kScanWarps, scan_smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m,
-                                                           x->d, x->pd, c.k, c.counters, c.und, AccSink{c.acc, c.bits, c.nw}, c.cap,
-                                                           x->mprime, c.scan_cnt); count_launch();
+    CK_RET(launch_scan(c, x->mprime, c.scan_cnt, false, st));
   } else {
     k_exact_decide<<<148 * 4, 256, 0, st>>>(c.q, x->U32, x->tau + (int64_t)(c.k - 1) * x->n, x->perm_u, x->d,
                                             c.counters, c.und, AccSink{c.acc, c.bits, c.nw}, c.cap); count_launch();

@@ -223,17 +223,17 @@ __device__ __noinline__ QSlowOut q_slow(QPool pool, uint32_t flag, uint32_t tbas
 // norm-sorted queries with ||q|| >= tb_k(t) (0 prunes the item whole), plus the block counters.
 __global__ void __launch_bounds__(256)
 k_lemma3_lens(const float* __restrict__ tbk, const float* __restrict__ qn, const int32_t* __restrict__ qcount,
-              int nblocks, int64_t nwork, int flags, int32_t* __restrict__ wlen, unsigned long long* __restrict__ ctr) {
+              int nblocks, int bsz, int64_t nlb, int64_t nwork, int flags, int32_t* __restrict__ wlen,
+              unsigned long long* __restrict__ ctr) {
   const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   unsigned long long pairs = 0, pruned = 0, scored = 0;
   if (w < nwork) {
     const int s = (int)(w / nblocks), t = (int)(w - (int64_t)s * nblocks);
     const int cnt = qcount[s];
-    const float tbv = (flags & RMIPS_FLAG_NO_BLOCKS) ? -CUDART_INF_F : tbk[t];
-    const int len = lemma3_len(qn + (int64_t)s * kQB, cnt, tbv);
+    const float* qs = qn + (int64_t)s * kQB;
+    const int len = tile_lemma3(t, bsz, nlb, cnt, (flags & RMIPS_FLAG_NO_BLOCKS) != 0, tbk,
+                                [&](float tbv) { return lemma3_len(qs, cnt, tbv); }, pairs, pruned);
     wlen[w] = len;
-    pairs = cnt;
-    pruned = cnt - len;
     scored = len > 0;
   }
 #pragma unroll
@@ -585,12 +585,13 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int64_t nwork = (int64_t)c.nsub * x->nblocks;
   const int grid = (int)(nwork < sm_count_q() ? nwork : sm_count_q());
-  k_lemma3_lens<<<(unsigned)((nwork + 255) / 256), 256, 0, st>>>(x->tb + (int64_t)(c.k - 1) * x->nblocks, c.qn,
-                                                                 c.qcount, (int)x->nblocks, nwork, c.flags, c.wlen,
+  k_lemma3_lens<<<(unsigned)((nwork + 255) / 256), 256, 0, st>>>(x->tb + (int64_t)(c.k - 1) * x->nlb, c.qn,
+                                                                 c.qcount, (int)x->nblocks, x->bsz, x->nlb, nwork,
+                                                                 c.flags, c.wlen,
                                                                  c.counters);
   count_launch();
   k_query_tc<KB><<<grid, kThreads, smem, st>>>(tu, tut, tq, tqt, x->dpad / 64, tail, x->thr + (int64_t)(c.k - 1) * x->n,
-                                               x->tb + (int64_t)(c.k - 1) * x->nblocks, x->perm_u, x->n,
+                                               x->tb + (int64_t)(c.k - 1) * x->nlb, x->perm_u, x->n,
                                                (int)x->nblocks, c.qn, c.qerr, c.qscale, c.qperm, c.qcount, c.nsub,
                                                c.flags, (x->d + 15) / 16, c.wlen, c.counters, AccSink{c.acc, c.bits, c.nw}, c.und, c.cap);
   count_launch();

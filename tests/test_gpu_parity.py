@@ -451,6 +451,8 @@ def test_cfg0_pprime_parity(cfg0, name, bf, c):
     st = idx.stats()
     assert st["pairs_accepted_fast"] == 0  # the filter never accepts on a P' index
     assert st["scans"] > 0 and st["items_scanned"] > 0
+    # Lemma-3 blocks of ceil(log2 n) users: n = 2,000 -> 11 users, 182 blocks
+    assert idx.block_size == 11 and st["block_query_pairs"] == 100 * 182
     # Alg. 2 over all of P (stress) on the same index agrees
     off, ids = rmips.rmips_query(idx, _t(w.Qy), 10, rmips.RMIPS_FLAG_VERIFY_SCAN)
     assert_same(rmips.split_sets(off, ids), member, label="cfg0/pprime scan-all")
