@@ -360,7 +360,98 @@ __global__ void k_scan_compact(const uint64_t* __restrict__ und_list, const int3
   }
 }
 
-// pw pairs per warp (4 for pd <= 256, else 1); rows staged per tile: 64 (pd <= 256) or 32
+// Warp-per-pair form (P32 small enough to stay in L2, m pd 4 <= kScanL2Bytes): lane j scores item
+// base + j straight from the sector-padded P32 rows (consecutive lanes read consecutive rows), so a pair
+// stops at its own depth -- the tiled form's CTA batches run to their deepest pair, which costs more than
+// it saves when the rows are L2 hits anyway (configs[1] P': 19 vs 29 ms).
+constexpr int64_t kScanL2Bytes = (int64_t)64 << 20;
+__global__ void __launch_bounds__(32 * kScanWarps)
+k_verify_scan_warp(const float* __restrict__ q, const float* __restrict__ U32, const double* __restrict__ unorm,
+                   const float* __restrict__ P32, const double* __restrict__ pnorm, const int32_t* __restrict__ perm_u,
+                   int64_t m, int d, int pd, int k, unsigned long long* __restrict__ ctr,
+                   const uint64_t* __restrict__ scan_rec, const int32_t* __restrict__ scan_beats, AccSink acc_list,
+                   int64_t cap, int64_t start, bool count_undecided) {
+  extern __shared__ __align__(16) float sw[];  // [kScanWarps][pd]: the pair's u, fp32, zero-padded to pd
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* uw = sw + (size_t)w * pd;
+  const int64_t npairs = (int64_t)min((unsigned long long)cap, ctr[C_SCAN_LIST]);
+  const double slack = 1.0 + (d + 8) * 2.220446049250313e-16;
+  const double n32 = pd / 4 + 2, g32 = n32 * 5.9604644775390625e-08 / (1.0 - n32 * 5.9604644775390625e-08);
+  const double g64 = (d + 2) * 1.1102230246251565e-16 / (1.0 - (d + 2) * 1.1102230246251565e-16);
+  const double efac = (g32 + g64) * slack * slack * (1.0 + 1e-6);
+  const int nq4 = pd / 4;
+  for (int64_t i = blockIdx.x * (int64_t)kScanWarps + w; i < npairs; i += (int64_t)gridDim.x * kScanWarps) {
+    const uint64_t rec = scan_rec[i];
+    const uint32_t qin = (uint32_t)(rec >> 32);
+    const int64_t row = (int64_t)(rec & 0xffffffffu);
+    const float* u = U32 + row * d;
+    __syncwarp();
+    for (int t = lane; t < pd; t += 32) uw[t] = t < d ? __ldg(u + t) : 0.f;
+    __syncwarp();
+    const double uq = dot64(q + (int64_t)qin * d, u, d);
+    const double un = unorm[row];
+    const double unc = un * slack;
+    int beats = scan_beats[i];
+    int64_t scanned = 0, exact = 0;
+    bool yes = true, decided = false;
+    for (int64_t base = start; base < m && !decided; base += 32) {
+      const int nrow = (int)min((int64_t)32, m - base);
+      const int64_t j = base + lane;
+      const bool in = lane < nrow;
+      const double pn = in ? pnorm[j] : 0.0;
+      const bool cor1 = in && (uq >= unc * pn * slack);
+      const uint32_t ycut = __ballot_sync(0xffffffffu, cor1);  // first lane where Cor. 1 fires
+      const int lim = ycut ? (__ffs(ycut) - 1) : nrow;
+      bool beat = false;
+      if (lane < lim) {
+        const float4* pr = reinterpret_cast<const float4*>(P32 + j * pd);
+        const float4* u4 = reinterpret_cast<const float4*>(uw);
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 4
+        for (int t = 0; t < nq4; ++t) {
+          const float4 x = __ldg(pr + t), y = u4[t];
+          a0 = fmaf(x.x, y.x, a0);
+          a1 = fmaf(x.y, y.y, a1);
+          a2 = fmaf(x.z, y.z, a2);
+          a3 = fmaf(x.w, y.w, a3);
+        }
+        const float sc = (a0 + a1) + (a2 + a3);
+        const double E = efac * pn * un + 1e-40;
+        const double sd = (double)sc;
+        if (isfinite(sc) && sd - E > uq) {
+          beat = true;
+        } else if (!(isfinite(sc) && sd + E <= uq)) {  // inside the band: the exact fp64 value
+          double g = 0.0;
+          const float* prf = P32 + j * pd;
+          for (int t = 0; t < d; ++t) g = __fma_rn((double)__ldg(prf + t), (double)uw[t], g);
+          beat = g > uq;
+          ++exact;
+        }
+      }
+      scanned += lim;
+      const uint32_t bb = __ballot_sync(0xffffffffu, beat);
+      const int nb = __popc(bb);
+      if (beats + nb >= k) { yes = false; decided = true; }
+      else if (ycut) { yes = true; decided = true; }
+      beats += nb;
+    }
+    for (int o = 16; o; o >>= 1) exact += __shfl_xor_sync(0xffffffffu, exact, o);
+    if (lane == 0) {
+      atomicAdd(ctr + C_SCANS, 1ull);
+      atomicAdd(ctr + C_ITEMS_SCANNED, (unsigned long long)scanned);
+      atomicAdd(ctr + C_SCAN_EXACT, (unsigned long long)exact);
+      if (count_undecided) atomicAdd(ctr + C_UNDECIDED, 1ull);
+      if (yes) {
+        atomicAdd(ctr + C_EXACT_ACCEPT, 1ull);
+        atomicAdd(ctr + C_ACC_REAL, 1ull);
+        acc_list.put_one(((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row], ctr + C_ACCEPTED_TOTAL, cap);
+      }
+    }
+  }
+}
+
+// Tiled form (P32 larger than kScanL2Bytes): pw pairs per warp (4 for pd <= 256, else 1); rows staged
+// per tile: 64 (pd <= 256) or 32
 __global__ void __launch_bounds__(32 * kScanWarps)
 k_verify_scan(const float* __restrict__ q, const float* __restrict__ U32, const double* __restrict__ unorm,
               const float* __restrict__ P32, const double* __restrict__ pnorm, const int32_t* __restrict__ perm_u,
@@ -570,6 +661,21 @@ static cudaError_t launch_scan(QueryCtx& c, int64_t start, const int32_t* beats0
   rmips_index_s* x = c.idx;
   k_scan_compact<<<148 * 4, 256, 0, st>>>(c.und, beats0, c.counters, c.cap, c.scan_rec, c.scan_beats);
   count_launch();
+  bool tiled = (int64_t)x->m * x->pd * 4 > kScanL2Bytes;
+#ifdef RMIPS_DEV
+  if (getenv("RMIPS_SCAN_TILED")) tiled = true;  // (development library: the tiled form on small P)
+#endif
+  if (!tiled) {
+    const size_t smem = (size_t)kScanWarps * x->pd * sizeof(float);
+    if (smem > 48 * 1024)
+      CK_RET(cudaFuncSetAttribute(k_verify_scan_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_verify_scan_warp<<<148 * 8, 32 * kScanWarps, smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u,
+                                                                x->m, x->d, x->pd, c.k, c.counters, c.scan_rec,
+                                                                c.scan_beats, AccSink{c.acc, c.bits, c.nw}, c.cap, start,
+                                                                count_und);
+    count_launch();
+    return cudaGetLastError();
+  }
   const int pw = x->pd <= 256 ? 4 : 1, rows = x->pd <= 256 ? 64 : 32;
   const int s4 = (x->pd / 4) | 1;
   const size_t smem = (size_t)rows * s4 * 16 + (size_t)kScanWarps * pw * x->pd * sizeof(float);

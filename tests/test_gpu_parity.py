@@ -737,3 +737,43 @@ def test_cta_pair_build_ragged_user_tiles(n):
     member = oracle.rkmips_twophase(U, vals, Qy, 7)
     assert_same(rmips.split_sets(*rmips.rmips_query(idx, _t(Qy), 7)), member, label="pair n=%d" % n)
     idx.close()
+
+
+_TILED_SCRIPT = """
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2110_07131_b200 import rmips
+from synth import generator as gen
+import oracle
+dev = torch.device("cuda:0")
+t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev)
+bad = 0
+for (seed, n, m, d, kmax, k, pp) in [(0, 2000, 1000, 50, 10, 10, 20), (1, 900, 700, 200, 8, 5, 16),
+                                     (2, 500, 300, 520, 6, 4, 12), (3, 700, 400, 30, 10, 3, 0)]:
+    U, P = gen.random_instance(seed, n, m, d, "skewed")
+    Qy = np.concatenate([P[:20], gen.random_instance(seed + 9, 10, 1, d, "skewed")[0]])
+    member = oracle.rkmips_naive(U, P, Qy, k)
+    want = oracle.sets_from_member(member)
+    idx = rmips.rmips_build_index_pprime(t(U), t(P), kmax, pp) if pp else rmips.rmips_build_index(t(U), t(P), kmax)
+    for fl in (0, rmips.RMIPS_FLAG_VERIFY_SCAN, rmips.RMIPS_FLAG_VERIFY_SCAN | rmips.RMIPS_FLAG_FORCE_VERIFY):
+        got = rmips.split_sets(*rmips.rmips_query(idx, t(Qy), k, fl))
+        bad += sum(not np.array_equal(a, b) for a, b in zip(got, want))
+    idx.close()
+print("BAD", bad)
+"""
+
+
+def test_tiled_verification_scan_dev():
+    """The shared-memory tiled form of Alg. 2's scan (used when P32 exceeds the L2 budget) forced on
+    small instances through the development library (RMIPS_SCAN_TILED): P' indexes and the scan-all
+    stress modes, d = 50 / 200 / 520 (1 pair per warp, 32-row tiles), against the naive oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    from paper_2110_07131_b200 import build_lib
+    e = dict(os.environ, RMIPS_LIB=build_lib.build_dev(), RMIPS_SCAN_TILED="1")
+    r = subprocess.run([sys.executable, "-c", _TILED_SCRIPT, root], env=e, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "BAD 0" in r.stdout, r.stdout[-500:]
