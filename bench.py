@@ -305,6 +305,7 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
         pt = idx.phase_times()  # build phases (ms[0..3], launches ms[14]) survive the queries
         rec = {"prep": pt[0], "contraction": pt[1], "select": pt[2], "build": pt[3], "build_launches": pt[14],
                "cand_per_user": idx.cand_total / max(1, spec.n), "tiles_issued": idx.tiles_done,
+               "build_kernel": idx.build_kernel,
                "q_prep": sum(p[8] for p, _ in qph), "q_filter": sum(p[9] for p, _ in qph),
                "q_exact": sum(p[10] for p, _ in qph), "q_output": sum(max(0.0, p[11]) for p, _ in qph),
                "q_total": sum(p[12] for p, _ in qph), "q_launches": sum(p[15] for p, _ in qph),
@@ -392,7 +393,8 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
     peak = peaks["bf16_tflops_sustained"] if sustained else peaks["bf16_tflops"]
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    kname = "k_build_simt" if args.simt else ("k_build_tc" if spec.d <= 64 else "k_build_tcq")
+    kname = {0: "k_build_simt", 1: "k_build_tc", 2: "k_build_tcq", 3: "k_build_tcq (streamed A)",
+             4: "k_build_tc2cta (CTA pairs, cta_group::2)"}.get(recs[-1]["build_kernel"], "?")
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
         traffic = tj.get("cfg%d" % cfg, {}).get("simt" if args.simt else "tc")

@@ -219,44 +219,38 @@ k_query_simt(const __half* __restrict__ U16, int ldh, const float* __restrict__ 
 
 // ------------------------------------------------------------------------------ Q4
 // u in R_k(q) <=> dot64(q, u) >= tau_k(u)  (reading R8; same dot routine as the build).
-// One warp per undecided pair: the lanes load 32 coordinates of q and u at a time (coalesced) and form
-// their exact fp64 products; every lane then adds the products in index order, taking each one by a
-// broadcast shuffle, so the sum is dot64's left-to-right fp64 sum bit for bit (each product of two fp32
+// One warp per undecided pair of the DENSE list (k_scan_compact packs the real records first: the filter
+// reserves list slots in blocks, so the real pairs cluster, and a warp per slot window would run its
+// cluster's pairs one after another): the lanes load 32 coordinates of q and u at a time (coalesced) and
+// form their exact fp64 products; every lane then adds the products in index order, taking each one by
+// a broadcast shuffle, so the sum is dot64's left-to-right fp64 sum bit for bit (each product of two fp32
 // values is exact in fp64, so fma(a, b, s) and s + a*b round identically).
+constexpr int C_SCAN_LIST = kNumCounters;  // (spare counter slot) pairs in the dense list
 __global__ void __launch_bounds__(256)
 k_exact_decide(const float* __restrict__ q, const float* __restrict__ U32, const double* __restrict__ tauk,
                const int32_t* __restrict__ perm_u, int d, unsigned long long* __restrict__ ctr,
-               const uint64_t* __restrict__ und_list, AccSink acc_list, int64_t cap) {
-  const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_UND_TOTAL]);
+               const uint64_t* __restrict__ dense, AccSink acc_list, int64_t cap) {
+  const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_SCAN_LIST]);
   const int lane = threadIdx.x & 31;
   const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
   unsigned n_und = 0, n_yes = 0;
-  // each warp scans 32 list slots at a time (the filter reserves slots in blocks, so most are sentinel
-  // padding) and runs the exact dot product of every real pair among them
-  for (int64_t i0 = (blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; i0 < total; i0 += wstride * 32) {
-    const uint64_t mine = i0 + lane < total ? und_list[i0 + lane] : kSentinel;
-    uint32_t live = __ballot_sync(0xffffffffu, mine != kSentinel);
-    while (live) {
-      const int src = __ffs(live) - 1;
-      live &= live - 1;
-      const uint64_t rec = __shfl_sync(0xffffffffu, mine, src);
-      const uint32_t qin = (uint32_t)(rec >> 32);
-      const int64_t row = (int64_t)(rec & 0xffffffffu);
-      const float* qa = q + (int64_t)qin * d;
-      const float* ua = U32 + row * d;
-      double g = 0.0;
-      for (int c = 0; c < d; c += 32) {
-        const double pc = c + lane < d ? (double)__ldg(qa + c + lane) * (double)__ldg(ua + c + lane) : 0.0;
-        const int nj = min(32, d - c);
+  for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < total; i += wstride) {
+    const uint64_t rec = dense[i];
+    const uint32_t qin = (uint32_t)(rec >> 32);
+    const int64_t row = (int64_t)(rec & 0xffffffffu);
+    const float* qa = q + (int64_t)qin * d;
+    const float* ua = U32 + row * d;
+    double g = 0.0;
+    for (int c = 0; c < d; c += 32) {
+      const double pc = c + lane < d ? (double)__ldg(qa + c + lane) * (double)__ldg(ua + c + lane) : 0.0;
+      const int nj = min(32, d - c);
 #pragma unroll 8
-        for (int jj = 0; jj < nj; ++jj) g = __dadd_rn(g, __shfl_sync(0xffffffffu, pc, jj));
-      }
-      ++n_und;
-      if (g >= tauk[row]) {  // u in R_k(q) <=> dot64(q, u) >= tau_k(u)  (reading R8)
-        ++n_yes;
-        if (lane == 0)
-          acc_list.put_one(((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row], ctr + C_ACCEPTED_TOTAL, cap);
-      }
+      for (int jj = 0; jj < nj; ++jj) g = __dadd_rn(g, __shfl_sync(0xffffffffu, pc, jj));
+    }
+    ++n_und;
+    if (g >= tauk[row]) {  // u in R_k(q) <=> dot64(q, u) >= tau_k(u)  (reading R8)
+      ++n_yes;
+      if (lane == 0) acc_list.put_one(((uint64_t)qin << 32) | (uint64_t)(uint32_t)perm_u[row], ctr + C_ACCEPTED_TOTAL, cap);
     }
   }
   if (lane == 0 && n_und) {
@@ -337,7 +331,6 @@ __global__ void k_exact_decide_pp(const float* __restrict__ q, const float* __re
 // start / beats0: the scan begins at item `start` with beats0 items already known to beat q (P' index:
 // start = mprime, beats0 = c' from k_exact_decide_pp); 0 / NULL scans all of P.
 constexpr int kScanWarps = 8;
-constexpr int C_SCAN_LIST = kNumCounters;  // (spare counter slot) pairs in the dense scan list
 __global__ void k_scan_compact(const uint64_t* __restrict__ und_list, const int32_t* __restrict__ beats0,
                                unsigned long long* __restrict__ ctr, int64_t cap, uint64_t* __restrict__ out_rec,
                                int32_t* __restrict__ out_beats) {
@@ -698,8 +691,11 @@ cudaError_t query_exact(QueryCtx& c, cudaStream_t st) {
     count_launch();
     CK_RET(launch_scan(c, x->mprime, c.scan_cnt, false, st));
   } else {
+    k_scan_compact<<<148 * 4, 256, 0, st>>>(c.und, nullptr, c.counters, c.cap, c.scan_rec, c.scan_beats);
+    count_launch();
     k_exact_decide<<<148 * 4, 256, 0, st>>>(c.q, x->U32, x->tau + (int64_t)(c.k - 1) * x->n, x->perm_u, x->d,
-                                            c.counters, c.und, AccSink{c.acc, c.bits, c.nw}, c.cap); count_launch();
+                                            c.counters, c.scan_rec, AccSink{c.acc, c.bits, c.nw}, c.cap);
+    count_launch();
   }
   return cudaGetLastError();
 }
