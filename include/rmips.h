@@ -190,6 +190,7 @@ RMIPS_API rmips_status_t rmips_index_export(rmips_index_t idx, int64_t* perm_u, 
  *   ms[2] exact select + fallback + blocks     ms[3] build total
  *   ms[8] query prep   ms[9] query filter contraction   ms[10] exact decide / scan
  *   ms[11] output (sort, offsets, copy)       ms[12] query total
+ *   ms[13] the tcgen05 query filter kernel alone (k_query_tc, events right around its launch)
  *   ms[14] kernels launched by the last build  ms[15] kernels launched by the last query
  * Entries not measured are -1.  ms must hold 16 doubles. */
 RMIPS_API rmips_status_t rmips_phase_times(rmips_index_t idx, double ms[16]);

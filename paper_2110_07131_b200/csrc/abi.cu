@@ -75,6 +75,23 @@ const char* const kQueryPhases[] = {"rmips_query: Q1 prep", "rmips_query: Q2-Q3 
 
 thread_local std::string g_err;
 
+// Two events around the query filter kernel itself (timing only): the roofline of k_query_tc is its own
+// duration, without the host's launch gaps before it.
+struct KernelEvents {
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  ~KernelEvents() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  bool get(cudaEvent_t (&out)[2]) {
+    for (int i = 0; i < 2; ++i)
+      if (!ev[i] && cudaEventCreate(&ev[i]) != cudaSuccess) return false;
+    out[0] = ev[0], out[1] = ev[1];
+    return true;
+  }
+};
+thread_local KernelEvents g_kev;
+
 rmips_status_t fail(rmips_status_t s, const std::string& msg) {
   g_err = msg;
   return s;
@@ -568,6 +585,7 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
     const long long l0 = g_launches.load();
     for (int attempt = 0; attempt < 3; ++attempt) {
       tm.reset(new PhaseTimer((flags & RMIPS_FLAG_TIMING) != 0, st, kQueryPhases));
+      if (tm->on) g_kev.get(c.ev_k);
       ensure_ws(x, c, c.nsub, cap, st);
       tm->mark();  // 0
       static_assert(2 * (kNumCounters + 4) <= 128, "zero4 region");
@@ -635,6 +653,9 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
       x->phase_ms[10] = tm->between(2, 3);
       x->phase_ms[11] = tm->between(4, 5);
       x->phase_ms[12] = tm->between(0, 5);
+      float kms = -1.f;
+      x->phase_ms[13] = (c.ev_k[0] && x->stats.filter_kernel && cudaEventElapsedTime(&kms, c.ev_k[0], c.ev_k[1]) == cudaSuccess)
+                            ? kms : -1.0;
     }
     *total_out = total;
     if (total > capacity) return fail(RMIPS_ERR_CAPACITY, "result ids exceed capacity");

@@ -661,7 +661,7 @@ static inline unsigned nblk(int64_t work, int t) { return (unsigned)((work + t -
 template <int DPAD>
 static cudaError_t launch_build_simt(const BuildCtx& c, cudaStream_t st) {
   size_t smem = (size_t)kCandSmemBytes + (DPAD / 2) * 128 * 4 + DPAD * 32 * 2;
-  cudaError_t e = cudaFuncSetAttribute(k_build_simt<DPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_attr((const void*)k_build_simt<DPAD>, (int)smem);
   if (e != cudaSuccess) return e;
   k_build_simt<DPAD><<<nblk(c.idx->n, 128), 128, smem, st>>>(c.idx->U16, c.idx->P16, c.idx->perr, c.idx->ldh, c.idx->n,
                                                              c.mb, c.idx->kmax, c.cand, c.ccount,
@@ -821,7 +821,7 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
   const bool staged = (size_t)kNormRows * (d | 1) * sizeof(float) <= 200 * 1024;
   const size_t nsm = staged ? (size_t)kNormRows * (d | 1) * sizeof(float) : 0;
   if (nsm > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_norms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nsm);
+    cudaError_t e = set_smem_attr((const void*)k_norms, (int)nsm);
     if (e != cudaSuccess) return e;
   }
   SortGraph* sg = sort_graph_get(st, tot);  // (nullptr: the direct path below)
@@ -879,7 +879,7 @@ static cudaError_t launch_select(BuildCtx& c, cudaStream_t st) {
   const int kc = x->kmax < MAXC ? x->kmax : MAXC;
   const size_t smem = (size_t)kSelWarps * x->pd * sizeof(double) + (size_t)kc * kSelStride * (8 + 4 + 4);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_exact_select<MAXC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = set_smem_attr((const void*)k_exact_select<MAXC>, (int)smem);
     if (e != cudaSuccess) return e;
   }
   int sms = 148;

@@ -463,7 +463,7 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   if (!make_tmap_f16_box(&ta, x->U16, (uint64_t)x->n, (uint64_t)x->ldh, kBM)) return cudaErrorNotSupported;
   if (!make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->ldh, kBN)) return cudaErrorNotSupported;
   const int smem = Smem::TOTAL(KB);
-  cudaError_t e = cudaFuncSetAttribute(k_build_tc<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = set_smem_attr((const void*)k_build_tc<KB>, smem);
   if (e != cudaSuccess) return e;
   const int tiles = (int)((x->n + kBM - 1) / kBM);
   const int grid = tiles < sm_count() ? tiles : sm_count();

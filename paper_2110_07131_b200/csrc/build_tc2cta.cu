@@ -367,7 +367,7 @@ static cudaError_t launch_tc2cta(const BuildCtx& c, cudaStream_t st) {
       !make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->ldh, 64) ||
       !make_tmap_f16_box(&tbt, x->P16, (uint64_t)c.mb, (uint64_t)x->ldh, 64, tail))
     return cudaErrorNotSupported;
-  cudaError_t e = cudaFuncSetAttribute(k_build_tc2cta<KB, Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
+  cudaError_t e = set_smem_attr((const void*)k_build_tc2cta<KB, Pol>, C::TOTAL);
   if (e != cudaSuccess) return e;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->device);

@@ -392,7 +392,7 @@ static cudaError_t launch_tcq(const BuildCtx& c, cudaStream_t st) {
       !make_tmap_f16_box(&tb, x->P16, (uint64_t)c.mb, (uint64_t)x->ldh, C::BN) ||
       !make_tmap_f16_box(&tbt, x->P16, (uint64_t)c.mb, (uint64_t)x->ldh, C::BN, tail))
     return cudaErrorNotSupported;
-  cudaError_t e = cudaFuncSetAttribute(k_build_tcq<KB, Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
+  cudaError_t e = set_smem_attr((const void*)k_build_tcq<KB, Pol>, C::TOTAL);
   if (e != cudaSuccess) return e;
   const int tiles = (int)((x->n + kBM - 1) / kBM);
   const int grid = tiles < sm_count_q() ? tiles : sm_count_q();

@@ -6,6 +6,8 @@
 #include "common.cuh"
 
 #include <atomic>
+#include <mutex>
+#include <unordered_map>
 
 namespace rmips {
 
@@ -15,6 +17,21 @@ namespace rmips {
 extern std::atomic<long long> g_launches;
 constexpr int kCubSortKernels = 10;  // histogram + exclusive-sum + 8 onesweep passes (64-bit keys)
 inline void count_launch(int k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size): the call costs
+// microseconds of host time, and query calls are short enough for that to show.
+inline cudaError_t set_smem_attr(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> done[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[dev & 15][func];
+  if (have >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
 
 // Scratch of one build call (owned by abi.cu, freed before rmips_build_index returns).
 struct BuildCtx {
@@ -82,6 +99,7 @@ struct QueryCtx {
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   int* flags_dev = nullptr;
+  cudaEvent_t ev_k[2] = {nullptr, nullptr};  // (timing only) around the filter kernel itself
 };
 
 // TMA descriptor of a 2-D fp16 tensor [rows][cols], box box_rows x 64, SWIZZLE_128B (build_tc.cu).

@@ -622,7 +622,7 @@ template <int DPAD>
 static cudaError_t launch_query_simt(QueryCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   size_t smem = (size_t)(DPAD / 2) * 128 * 4 + (size_t)kQB * (DPAD / 2) * 4;
-  cudaError_t e = cudaFuncSetAttribute(k_query_simt<DPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_attr((const void*)k_query_simt<DPAD>, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)x->nblocks, (unsigned)c.nsub);
   k_query_simt<DPAD><<<grid, 128, smem, st>>>(x->U16, x->ldh, x->thr + (int64_t)(c.k - 1) * x->n,
@@ -661,7 +661,7 @@ static cudaError_t launch_scan(QueryCtx& c, int64_t start, const int32_t* beats0
   if (!tiled) {
     const size_t smem = (size_t)kScanWarps * x->pd * sizeof(float);
     if (smem > 48 * 1024)
-      CK_RET(cudaFuncSetAttribute(k_verify_scan_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CK_RET(set_smem_attr((const void*)k_verify_scan_warp, (int)smem));
     k_verify_scan_warp<<<148 * 8, 32 * kScanWarps, smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u,
                                                                 x->m, x->d, x->pd, c.k, c.counters, c.scan_rec,
                                                                 c.scan_beats, AccSink{c.acc, c.bits, c.nw}, c.cap, start,
@@ -672,7 +672,7 @@ static cudaError_t launch_scan(QueryCtx& c, int64_t start, const int32_t* beats0
   const int pw = x->pd <= 256 ? 4 : 1, rows = x->pd <= 256 ? 64 : 32;
   const int s4 = (x->pd / 4) | 1;
   const size_t smem = (size_t)rows * s4 * 16 + (size_t)kScanWarps * pw * x->pd * sizeof(float);
-  if (smem > 48 * 1024) CK_RET(cudaFuncSetAttribute(k_verify_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem > 48 * 1024) CK_RET(set_smem_attr((const void*)k_verify_scan, (int)smem));
   k_verify_scan<<<148 * 2, 32 * kScanWarps, smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m, x->d,
                                                         x->pd, c.k, c.counters, c.scan_rec, c.scan_beats,
                                                         AccSink{c.acc, c.bits, c.nw}, c.cap, start, count_und, pw, rows);

@@ -581,7 +581,7 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
       !make_tmap_f16_box(&tqt, c.Q16, (uint64_t)c.nsub * kQB, (uint64_t)x->ldh, kQB, tail))
     return cudaErrorNotSupported;
   const int smem = QLayout::make(KB, tail).total;
-  cudaError_t e = cudaFuncSetAttribute(k_query_tc<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = set_smem_attr((const void*)k_query_tc<KB>, smem);
   if (e != cudaSuccess) return e;
   const int64_t nwork = (int64_t)c.nsub * x->nblocks;
   const int grid = (int)(nwork < sm_count_q() ? nwork : sm_count_q());
@@ -590,11 +590,13 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
                                                                  c.flags, c.wlen,
                                                                  c.counters);
   count_launch();
+  if (c.ev_k[0]) cudaEventRecord(c.ev_k[0], st);
   k_query_tc<KB><<<grid, kThreads, smem, st>>>(tu, tut, tq, tqt, x->dpad / 64, tail, x->thr + (int64_t)(c.k - 1) * x->n,
                                                x->tb + (int64_t)(c.k - 1) * x->nlb, x->perm_u, x->n,
                                                (int)x->nblocks, c.qn, c.qerr, c.qscale, c.qperm, c.qcount, c.nsub,
                                                c.flags, (x->d + 15) / 16, c.wlen, c.counters, AccSink{c.acc, c.bits, c.nw}, c.und, c.cap);
   count_launch();
+  if (c.ev_k[1]) cudaEventRecord(c.ev_k[1], st);
   return cudaGetLastError();
 }
 
