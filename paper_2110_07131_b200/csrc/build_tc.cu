@@ -35,6 +35,11 @@ constexpr int kStages = 4;        // smem ring depth for item tiles
 constexpr int kAcc = 4;           // TMEM accumulator stages (kAcc * kBN = 512 columns)
 constexpr int kTileBytes = kBM * 64 * 2;  // one 128 x 64 fp16 tile = 16 KB
 constexpr int kThreads = 192;
+// development-only switches (librmips_dev.so; always 0 in the product library)
+constexpr int kDevEpiSkip = 2;   // RMIPS_EPI_SKIP: the epilogue releases every stage unread
+constexpr int kDevEpiLoad = 4;   // RMIPS_EPI_LOAD: ... after reading it from TMEM (no filter work)
+constexpr int kDevFastOnly = 8;  // RMIPS_FAST_ONLY: fast path only (no appends: wrong lists, timing only)
+// RMIPS_SLOW_LIMIT=T (dev >> 8): the slow path runs only on item tiles < T (wrong lists, timing only)
 static_assert(kStages == kAcc, "the producer recycles item stages on the accumulator barriers");
 
 struct Smem {
@@ -107,15 +112,15 @@ __device__ __noinline__ CandRow epi_slow(uint32_t bits, uint32_t taddr, int base
   return me;
 }
 
-// maxima of the two 16-column groups of chunk c of a half tile, minus E (rounded down)
-__device__ __forceinline__ uint2 group_max16(const uint32_t (&h)[64], int c, float E) {
+// maxima of the four 8-column groups of chunk c of a half tile, minus E (rounded down)
+__device__ __forceinline__ uint4 group_max8(const uint32_t (&h)[64], int c, float E) {
   float g[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
     g[i] = fmaxf(fmaxf(__uint_as_float(h[32 * c + 4 * i]), __uint_as_float(h[32 * c + 4 * i + 1])),
                  fmaxf(__uint_as_float(h[32 * c + 4 * i + 2]), __uint_as_float(h[32 * c + 4 * i + 3])));
-  return make_uint2(__float_as_uint(__fsub_rd(fmaxf(fmaxf(g[0], g[1]), fmaxf(g[2], g[3])), E)),
-                    __float_as_uint(__fsub_rd(fmaxf(fmaxf(g[4], g[5]), fmaxf(g[6], g[7])), E)));
+  return make_uint4(__float_as_uint(__fsub_rd(fmaxf(g[0], g[1]), E)), __float_as_uint(__fsub_rd(fmaxf(g[2], g[3]), E)),
+                    __float_as_uint(__fsub_rd(fmaxf(g[4], g[5]), E)), __float_as_uint(__fsub_rd(fmaxf(g[6], g[7]), E)));
 }
 
 }  // namespace
@@ -125,7 +130,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
            int64_t n, int64_t m, int kmax, int seed_tiles, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
-           int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count, unsigned long long* __restrict__ tiles_done) {
+           int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count, unsigned long long* __restrict__ tiles_done,
+           int dev) {
   using namespace sm100;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base, derived from smem_raw by pointer arithmetic so that the compiler
@@ -292,18 +298,21 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       tmem_ld_wait64(hA);
       if (seed_tiles > 0) {
         // Seed pass over item tiles 0 .. seed_tiles-1 (full tiles; contracted again below): the
-        // 16-column group maxima minus E are lower bounds of distinct items' true scores, so the
+        // 8-column group maxima minus E are lower bounds of distinct items' true scores, so the
         // k_max-th largest of them (cand_seed) is a valid starting theta.  It spares the filter
         // the dense phase in which theta would otherwise climb from -inf through appends and
-        // refreshes.  The maxima sit in this row's (still empty) candidate slots, two per slot.
+        // refreshes.  The 16 maxima of a tile sit in 8 of this row's (still empty) candidate
+        // slots, two per slot (16 seed tiles fill all kCand = 128 slots).
         uint2* sb = sm.buf + rloc;
         float vmx = -__int_as_float(0x7f800000);
+        const auto f = [](uint32_t u) { return __uint_as_float(u); };
+        const auto mx4 = [&](uint4 v) { return fmaxf(fmaxf(f(v.x), f(v.y)), fmaxf(f(v.z), f(v.w))); };
         for (int j = 0; j < seed_tiles; ++j) {
           const int base0 = j * kBN;
           tmem_ld64(tq + as * kBN + 64, hB);
           const float E0 = __ldg(perr + base0), E1 = __ldg(perr + base0 + 32), E2 = __ldg(perr + base0 + 64),
                       E3 = __ldg(perr + base0 + 96);
-          uint2 l0 = group_max16(hA, 0, E0), l1 = group_max16(hA, 1, E1);
+          const uint4 l0 = group_max8(hA, 0, E0), l1 = group_max8(hA, 1, E1);
           const int as_next = as + 1 == kAcc ? 0 : as + 1;
           const uint32_t aph_next = as + 1 == kAcc ? aph ^ 1 : aph;
           tmem_ld_wait64(hB);
@@ -315,17 +324,20 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
           tmem_ld64(tq + as_next * kBN, hA);
           as = as_next;
           aph = aph_next;
-          const uint2 l2 = group_max16(hB, 0, E2), l3 = group_max16(hB, 1, E3);
-          sb[(4 * j) * kCandRows] = l0;
-          sb[(4 * j + 1) * kCandRows] = l1;
-          sb[(4 * j + 2) * kCandRows] = l2;
-          sb[(4 * j + 3) * kCandRows] = l3;
-          const auto f = [](uint32_t u) { return __uint_as_float(u); };
-          vmx = fmaxf(vmx, fmaxf(fmaxf(fmaxf(f(l0.x), f(l0.y)), fmaxf(f(l1.x), f(l1.y))),
-                                 fmaxf(fmaxf(f(l2.x), f(l2.y)), fmaxf(f(l3.x), f(l3.y)))));
+          const uint4 l2 = group_max8(hB, 0, E2), l3 = group_max8(hB, 1, E3);
+          uint2* o = sb + (8 * j) * kCandRows;
+          o[0 * kCandRows] = make_uint2(l0.x, l0.y);
+          o[1 * kCandRows] = make_uint2(l0.z, l0.w);
+          o[2 * kCandRows] = make_uint2(l1.x, l1.y);
+          o[3 * kCandRows] = make_uint2(l1.z, l1.w);
+          o[4 * kCandRows] = make_uint2(l2.x, l2.y);
+          o[5 * kCandRows] = make_uint2(l2.z, l2.w);
+          o[6 * kCandRows] = make_uint2(l3.x, l3.y);
+          o[7 * kCandRows] = make_uint2(l3.z, l3.w);
+          vmx = fmaxf(vmx, fmaxf(fmaxf(mx4(l0), mx4(l1)), fmaxf(mx4(l2), mx4(l3))));
           tmem_ld_wait64(hA);
         }
-        me.cnt = 4 * seed_tiles;
+        me.cnt = 8 * seed_tiles;
         me.vmax = vmx;
         me.theta = fmaxf(me.theta, cand_seed(me, sm, rloc, kmax));  // dead rows keep +inf
         me.cnt = 0;
@@ -333,6 +345,27 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       }
       int it = 0;
       bool done = false;                        // warp-uniform: this warp's rows cannot gain any more
+      if (dev & (kDevEpiSkip | kDevEpiLoad)) {  // dev: release every accumulator stage (MMA + feed alone)
+        uint32_t sink = 0;
+        for (; it < nit; ++it) {
+          if (dev & kDevEpiLoad) {
+            tmem_ld64(tq + as * kBN, hA);
+            tmem_ld64(tq + as * kBN + 64, hB);
+            tmem_ld_wait64(hA);
+            tmem_ld_wait64(hB);
+            sink ^= hA[0] ^ hB[63];  // (constant indices: the arrays stay in registers)
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
+          if (++as == kAcc) as = 0, aph ^= 1;
+          if (it + 1 < nit) {
+            mbar_wait(BAR(ACC_FULL + as), aph);
+            tc_fence_after();
+          }
+        }
+        if (sink == 0x12345678u) ccount[0] = 0;  // keeps the loads
+      }
       for (; it < nit; ++it) {
         const int base0 = it * kBN;
         const float E[4] = {Eg, Eg, Eg, Eg};
@@ -352,7 +385,8 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         // completion, and the MMA -> epilogue -> MMA round trip then throttles the tensor pipe.)
         tmem_ld_wait64(hB);
         bits |= epi_fast(hB, E[2], E[3], me.theta) << 2;
-        if (bits) me = epi_slow(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, sm, rloc, e0x2, kmax);
+        if (bits && !(dev & kDevFastOnly) && (dev < 256 || it < (dev >> 8)))
+          me = epi_slow(bits, tcur, base0, mi, make_float4(E[0], E[1], E[2], E[3]), me, sm, rloc, e0x2, kmax);
         tc_fence_before();                      // this stage is no longer read: release it
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
@@ -468,26 +502,31 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   const int tiles = (int)((x->n + kBM - 1) / kBM);
   const int grid = tiles < sm_count() ? tiles : sm_count();
   const float* cs = c.scale_dev;
-  // seed pass length: 16 full tiles (8 maxima per tile, 128 slots of two), at least k_max maxima.
-  // Measured (profiles/): -10% contraction on configs[1] (m = 25,000) but +15% on configs[3]
-  // (m = 100,000), where the Cauchy-Schwarz exit ends a user tile after a few dozen tiles and the
-  // 16 repeated tiles are a large share of the work; so no seed pass for m > 32,768.
+  // seed pass length: 16 full tiles (16 maxima of 8 items per tile fill the 128 slots of two),
+  // at least k_max maxima.  With 8-item groups the seed's theta leaves no 32-row warp of
+  // configs[1..3] above the refresh mark (16-item groups left 98 % of them there).
   const int nit = (int)((c.mb + kBN - 1) / kBN);
-  int seed = (nit >= 32 && nit <= 256) ? 16 : 0;
+  int seed = nit >= 32 ? 16 : 0;
 #ifdef RMIPS_DEV
   // development-only A/B switches (librmips_dev.so, tools/gpu_ab.sh); the product library has a
   // fixed code path
   if (getenv("RMIPS_NO_CS")) cs = nullptr;  // no Cauchy-Schwarz exit
-  if (const char* e = getenv("RMIPS_SEED_TILES")) {  // 0 .. min(32, nit - 1) seed tiles
+  if (const char* e = getenv("RMIPS_SEED_TILES")) {  // 0 .. min(16, nit - 1) seed tiles
     seed = atoi(e);
-    seed = seed < 0 ? 0 : seed > 32 ? 32 : seed > nit - 1 ? nit - 1 : seed;
+    seed = seed < 0 ? 0 : seed > 16 ? 16 : seed > nit - 1 ? nit - 1 : seed;
   }
 #endif
-  if (8 * seed < x->kmax) seed = 0;
+  int dev = 0;
+#ifdef RMIPS_DEV
+  dev = (getenv("RMIPS_EPI_SKIP") ? kDevEpiSkip : 0) | (getenv("RMIPS_EPI_LOAD") ? kDevEpiLoad : 0) |
+        (getenv("RMIPS_FAST_ONLY") ? kDevFastOnly : 0);
+  if (const char* e = getenv("RMIPS_SLOW_LIMIT")) dev |= (atoi(e) & 0xffff) << 8;
+#endif
+  if (16 * seed < x->kmax) seed = 0;
   x->build_kernel = 1;
   x->cand_slots = kCand;
   k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, x->n, c.mb, x->kmax, seed, c.cand,
-                                               c.ccount, c.ovf_list, c.ovf_count, c.tiles_done);
+                                               c.ccount, c.ovf_list, c.ovf_count, c.tiles_done, dev);
   count_launch();
   return cudaGetLastError();
 }
