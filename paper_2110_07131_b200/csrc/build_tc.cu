@@ -502,11 +502,11 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   const int tiles = (int)((x->n + kBM - 1) / kBM);
   const int grid = tiles < sm_count() ? tiles : sm_count();
   const float* cs = c.scale_dev;
-  // seed pass length: 16 full tiles (16 maxima of 8 items per tile fill the 128 slots of two),
-  // at least k_max maxima.  With 8-item groups the seed's theta leaves no 32-row warp of
-  // configs[1..3] above the refresh mark (16-item groups left 98 % of them there).
+  // seed pass length: 8 full tiles (16 maxima of 8 items per tile, two per slot), at least k_max
+  // maxima.  Measured on configs[1..3] (tools/gpu_seed_ab.sh, one box): 8 tiles 0.830 / 2.905 /
+  // 6.06 ms, 16 tiles 0.860 / 3.032 / 6.81 ms, none 0.938 / 3.460 / 6.20 ms.
   const int nit = (int)((c.mb + kBN - 1) / kBN);
-  int seed = nit >= 32 ? 16 : 0;
+  int seed = nit >= 32 ? 8 : 0;
 #ifdef RMIPS_DEV
   // development-only A/B switches (librmips_dev.so, tools/gpu_ab.sh); the product library has a
   // fixed code path

@@ -40,6 +40,13 @@ constexpr int kBM = 128;                  // users per tile (TMEM lanes)
 constexpr int kUTileBytes = kBM * 64 * 2; // one K block of a user tile: 128 x 64 fp16 = 16 KB
 constexpr int kQTileBytes = kQB * 64 * 2; // 256 x 64 fp16 = 32 KB
 constexpr int kThreads = 320;           // producer, MMA, 8 epilogue warps (2 per TMEM lane quadrant)
+// development-only switch bits OR-ed into `flags` by librmips_dev.so (never set in the product)
+constexpr int kDevQEpiSkip = 1 << 28;  // RMIPS_Q_EPI_SKIP: the epilogue releases every stage unread
+constexpr int kDevQNoSlow = 1 << 27;   // RMIPS_Q_NO_SLOW: flagged chunks are not classified (timing only)
+constexpr int kDevQCount = 1 << 26;    // RMIPS_Q_COUNT: count flagged / examined warp-chunks (g_qdev)
+#ifdef RMIPS_DEV
+__device__ unsigned long long g_qdev[4];  // dev: [0] flagged warp-chunks, [1] examined warp-chunks
+#endif
 constexpr int kAccCols = 256;             // TMEM columns per accumulator stage
 constexpr int kAcc = 2;
 
@@ -132,7 +139,9 @@ struct QSlowOut {
 
 // Classify every pair of the flagged 32-column chunks (re-read from TMEM), then compact the
 // accepted and undecided pairs of the warp: one atomic per list per chunk.  Returns this
-// thread's (accepted, undecided) counts.
+// thread's (accepted, undecided) counts.  The stage stays held until this returns, so the chain
+// is kept short: the chunk's 32 error bounds are one coalesced load issued with the TMEM read and
+// broadcast by shuffles, and every pair is classified branch-free (as classify_tc).
 __device__ __noinline__ QSlowOut q_slow(QPool pool, uint32_t flag, uint32_t tbase, int len, bool live, float thr_s,
                                         const float* __restrict__ qe_sub, const int32_t* __restrict__ qp_sub,
                                         uint64_t uo, int64_t row, bool force, unsigned long long* __restrict__ ctr,
@@ -149,30 +158,20 @@ __device__ __noinline__ QSlowOut q_slow(QPool pool, uint32_t flag, uint32_t tbas
     const int col0 = 32 * ci;
     uint32_t r[32];
     tmem_ld32(tbase + col0, r);
+    const float qv = __ldg(qe_sub + col0 + lane);  // qerr of slot col0 + lane (broadcast below)
     tmem_ld_wait(r);
+    const int lim = live ? min(32, len - col0) : 0;  // columns of this chunk that are scored
     uint32_t am = 0, um = 0;
-    // groups of 4 columns whose max cannot be rejected with the chunk's largest error bound (qerr
-    // is non-increasing along the slots); only those are classified pair by pair
-    const float emax = __fadd_ru(__ldg(qe_sub + col0), thr_abs);
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      const float gm = fmaxf(fmaxf(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1])),
-                             fmaxf(__uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3])));
-      const bool gp = live && col0 + 4 * g < len && !(__fadd_ru(gm, emax) < thr_s);
-      if (__any_sync(0xffffffffu, gp)) {
-        if (gp) {
-#pragma unroll
-          for (int j = 4 * g; j < 4 * g + 4; ++j) {
-            if (col0 + j < len) {
-              int cls = classify_tc(__uint_as_float(r[j]), thr_s, __ldg(qe_sub + col0 + j));
-              if (force && cls == 1) cls = 2;
-              am |= (uint32_t)(cls == 1) << j;
-              um |= (uint32_t)(cls == 2) << j;
-            }
-          }
-        }
-      }
+    for (int j = 0; j < 32; ++j) {
+      const float E = __fadd_ru(__shfl_sync(0xffffffffu, qv, j), thr_abs);
+      const float a = __uint_as_float(r[j]);
+      const bool keep = j < lim && !(__fadd_ru(a, E) < thr_s);  // not rejected (classify_tc: 0)
+      const bool acc = keep && __fsub_rd(a, E) >= thr_s;          // accepted (1); else undecided (2)
+      am |= (uint32_t)acc << j;
+      um |= (uint32_t)(keep && !acc) << j;
     }
+    if (force) um |= am, am = 0;
     if (!__any_sync(0xffffffffu, (am | um) != 0)) continue;
     const int na = __popc(am), nu = __popc(um);
     n_acc += na;
@@ -311,6 +310,27 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     t += gridDim.x;
     while (t >= nblocks) t -= nblocks, ++s;
   };
+  // Lemma 3 prefix lengths of this CTA's items, loaded four items ahead (the producer and MMA warps
+  // otherwise start every item with a dependent global load)
+  struct LenQ {
+    int v0, v1, v2, v3;
+  };
+  auto lenq_init = [&]() {
+    LenQ q;
+    const int64_t g = gridDim.x, w0 = blockIdx.x;
+    q.v0 = w0 < nwork ? __ldg(wlen + w0) : 0;
+    q.v1 = w0 + g < nwork ? __ldg(wlen + w0 + g) : 0;
+    q.v2 = w0 + 2 * g < nwork ? __ldg(wlen + w0 + 2 * g) : 0;
+    q.v3 = w0 + 3 * g < nwork ? __ldg(wlen + w0 + 3 * g) : 0;
+    return q;
+  };
+  auto lenq_pop = [&](LenQ& q, int64_t w) {  // the length of item w; item w + 4 g is requested
+    const int len = q.v0;
+    q.v0 = q.v1, q.v1 = q.v2, q.v2 = q.v3;
+    const int64_t w4 = w + 4 * (int64_t)gridDim.x;
+    q.v3 = w4 < nwork ? __ldg(wlen + w4) : 0;
+    return len;
+  };
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -319,8 +339,9 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
       uint32_t ph = 0;
       int s, t;
       first_item(s, t);
+      LenQ lq = lenq_init();
       for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x, next_item(s, t)) {
-        const int len = __ldg(wlen + w);
+        const int len = lenq_pop(lq, w);
         if (len == 0) continue;
         if (!kStreamQ && s != cur_s) {
           if (nq > 0) mbar_wait(BAR(Q_EMPTY), (nq - 1) & 1);
@@ -354,8 +375,9 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
     uint32_t ph = 0, aph = 0;
     int s, t;
     first_item(s, t);
+    LenQ lq = lenq_init();
     for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x, next_item(s, t)) {
-      const int len = __ldg(wlen + w);
+      const int len = lenq_pop(lq, w);
       if (len == 0) continue;
       if (!kStreamQ && s != cur_s) {
         if (nq > 0) {
@@ -485,6 +507,15 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
       const float thr_abs = fabsf(thr_s) * 2.384185791015625e-07f;
       const float* qe_sub = qerr + (int64_t)s * kQB;
       const int hlen = min(128, max(0, len - 128 * hsel));  // scored columns of this warp's half
+      if (flags & kDevQEpiSkip) {  // dev: MMA + feed alone
+        mbar_wait(BAR(ACC_FULL + as), aph);
+        tc_fence_after();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(ACC_EMPTY + as));
+        if (++as == kAcc) as = 0, aph ^= 1;
+        continue;
+      }
       if (live) n_scored += hlen;
       // qerr is non-increasing along the norm-sorted slots: a chunk's first slot bounds it
       // (chunks at or beyond len are masked below, so their entries never matter)
@@ -522,7 +553,13 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
       }
       // chunks at or beyond len are never classified
       flag &= len >= 256 ? 0xffu : ((1u << ((len + 31) >> 5)) - 1u);
-      if (flag) {
+#ifdef RMIPS_DEV
+      if (lane == 0 && (flags & kDevQCount) && hsel * 128 < len) {
+        atomicAdd(&g_qdev[0], (unsigned long long)__popc(flag));
+        atomicAdd(&g_qdev[1], (unsigned long long)((min(len, 128 * hsel + 128) - 128 * hsel + 31) / 32));
+      }
+#endif
+      if (flag && !(flags & kDevQNoSlow)) {
         const uint64_t uo = live ? (uint64_t)(uint32_t)__ldg(perm_u + row) : 0;
         const QSlowOut o = q_slow(pool, flag, tbase, len, live, thr_s, qe_sub, qperm + (int64_t)s * kQB, uo, row,
                                   force, ctr, acc_list, und_list, cap);
@@ -585,6 +622,12 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int64_t nwork = (int64_t)c.nsub * x->nblocks;
   const int grid = (int)(nwork < sm_count_q() ? nwork : sm_count_q());
+  int kflags = c.flags & 0xffff;  // bits 16.. carry the dev switches only
+#ifdef RMIPS_DEV
+  if (getenv("RMIPS_Q_EPI_SKIP")) kflags |= kDevQEpiSkip;
+  if (getenv("RMIPS_Q_NO_SLOW")) kflags |= kDevQNoSlow;
+  if (getenv("RMIPS_Q_COUNT")) kflags |= kDevQCount;
+#endif
   k_lemma3_lens<<<(unsigned)((nwork + 255) / 256), 256, 0, st>>>(x->tb + (int64_t)(c.k - 1) * x->nlb, c.qn,
                                                                  c.qcount, (int)x->nblocks, x->bsz, x->nlb, nwork,
                                                                  c.flags, c.wlen,
@@ -594,7 +637,7 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
   k_query_tc<KB><<<grid, kThreads, smem, st>>>(tu, tut, tq, tqt, x->dpad / 64, tail, x->thr + (int64_t)(c.k - 1) * x->n,
                                                x->tb + (int64_t)(c.k - 1) * x->nlb, x->perm_u, x->n,
                                                (int)x->nblocks, c.qn, c.qerr, c.qscale, c.qperm, c.qcount, c.nsub,
-                                               c.flags, (x->d + 15) / 16, c.wlen, c.counters, AccSink{c.acc, c.bits, c.nw}, c.und, c.cap);
+                                               kflags, (x->d + 15) / 16, c.wlen, c.counters, AccSink{c.acc, c.bits, c.nw}, c.und, c.cap);
   count_launch();
   if (c.ev_k[1]) cudaEventRecord(c.ev_k[1], st);
   return cudaGetLastError();
@@ -622,6 +665,17 @@ extern "C" RMIPS_API int rmips_debug_query_profile(unsigned long long* out, int 
   if (reset) {
     static unsigned long long z[8] = {};
     cudaMemcpyToSymbol(rmips::g_qprof, z, sizeof z);
+  }
+  return 0;
+}
+#endif
+
+#ifdef RMIPS_DEV
+extern "C" RMIPS_API int rmips_debug_qdev(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, rmips::g_qdev, sizeof(rmips::g_qdev));
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(rmips::g_qdev, z, sizeof z);
   }
   return 0;
 }

@@ -1,5 +1,5 @@
 """Aggregate an ncu --set full report's warp-stall samples per CUDA source line (needs -lineinfo).
-Usage: python tools/ncu_src_lines.py report.ncu-rep [top_n]"""
+Usage: python tools/ncu_src_lines.py report.ncu-rep [top_n] [kernel-regex]"""
 import csv
 import io
 import subprocess
@@ -7,7 +7,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kf = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep] + kf + ["--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 recs, tot, cur = [], 0, None
 hdr = None
