@@ -236,7 +236,7 @@ def run_reference(args):
 
 def _config_dict(spec, k, ws):
     return {"workload": spec.name, "n": spec.n, "m": spec.m, "d": spec.d, "k_max": spec.k_max, "queries": spec.nq,
-            "k": k, "query_batch": "%d calls of <= %d queries" % (len(_batches(spec.nq, spec.batch)), spec.batch),
+            "k": k, "query_batch": "%d batches of <= %d queries" % (len(_batches(spec.nq, spec.batch)), spec.batch),
             "l2": "flushed (512 MiB memset) before every timed step", "parallelism": "user-shard x%d" % ws}
 
 
@@ -293,8 +293,15 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
             idx = rmips.rmips_build_index(U, P, spec.k_max, bflags)
         host_build_ms.append((time.perf_counter() - tb0) * 1e3)
         outs, qph = [], []
-        for q in Qb:
-            off, ids = rmips.rmips_query(idx, q, k, qflags, capacity=cap[0])
+        if args.query_api == "batches":  # every batch of the config in one call, one host sync
+            qsets = [(Qy, rmips.rmips_query_batches)]
+        else:  # one rmips_query call (and host sync) per batch
+            qsets = [(q, None) for q in Qb]
+        for q, fn in qsets:
+            if fn is not None:
+                off, ids = fn(idx, q, spec.batch, k, qflags, capacity=cap[0])
+            else:
+                off, ids = rmips.rmips_query(idx, q, k, qflags, capacity=cap[0])
             qph.append((idx.phase_times(), idx.stats()))
             if ws > 1:  # the exchange step: every rank gets the global lists (NCCL all_gathers)
                 off, ids = gather_csr(off, ids, sa)
@@ -443,6 +450,8 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
                      "contraction_ms": kern_ms, "prep_ms": med("prep"), "select_blocks_ms": med("select"),
                      "candidates_per_user": med("cand_per_user")},
            "query": {"ms": med("q_total"), "queries_per_s": spec.nq / (med("q_total") / 1e3), "calls": len(batches),
+                     "api": "rmips_query_batches (one call, %d batches)" % len(batches) if args.query_api == "batches"
+                     else "%d rmips_query calls" % len(batches),
                      "prep_ms": med("q_prep"), "filter_ms": qf_ms, "filter_phase_ms": med("q_filter"), "exact_ms": med("q_exact"),
                      "output_ms": med("q_output"), "undecided_pairs": med("undecided"),
                      "result_ids": recs[-1]["result_total"], "filter_kernel_tcgen05": bool(recs[-1]["filter_kernel"]),
@@ -465,8 +474,8 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
     if e2e:
         Uh = U.cpu().pin_memory()  # this rank's users (all of them at N = 1)
         Ph = P.cpu().pin_memory()
-        Qh = [Qy[a:b].cpu().pin_memory() for a, b in batches]
-        offh = [torch.empty(b - a + 1, dtype=torch.int64).pin_memory() for a, b in batches]
+        Qh = [Qy.cpu().pin_memory()] if args.query_api == "batches" else [Qy[a:b].cpu().pin_memory() for a, b in batches]
+        offh = [torch.empty(q.shape[0] + 1, dtype=torch.int64).pin_memory() for q in Qh]
         idsh = torch.empty(cap[0], dtype=torch.int32).pin_memory()
         e2e_ms, d2h = [], 0
         for it in range(warmup + steps):
@@ -478,7 +487,12 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
             idx = rmips.rmips_build_index_host(Uh, Ph, spec.k_max)
             d2h = 0
             for j, q in enumerate(Qh):
-                off, ids = rmips.rmips_query_host(idx, q, k, out_offsets=offh[j], out_ids=idsh, capacity=idsh.numel())
+                if args.query_api == "batches":
+                    off, ids = rmips.rmips_query_batches_host(idx, q, spec.batch, k, out_offsets=offh[j], out_ids=idsh,
+                                                              capacity=idsh.numel())
+                else:
+                    off, ids = rmips.rmips_query_host(idx, q, k, out_offsets=offh[j], out_ids=idsh,
+                                                      capacity=idsh.numel())
                 if ws > 1:  # the exchange: this rank's host lists -> device -> NCCL gather -> host
                     g_off, g_ids = gather_csr(off.to(dev, non_blocking=True), ids.to(dev, non_blocking=True), sa)
                     off, ids = g_off.cpu(), g_ids.cpu()
@@ -496,8 +510,10 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
         res["e2e"] = {"value": units_step * steps / (t_e2e / 1e3), "unit": UNIT,
                       "h2d_bytes_per_step": 4 * spec.d * ((sb - sa) + spec.m + spec.nq), "d2h_bytes_per_step": d2h,
                       "ms_per_step": t_e2e / steps,
-                      "api": "rmips_build_index_host + %d rmips_query_host calls (pinned host buffers)%s"
-                             % (len(batches), " + shard.gather_csr per call" if ws > 1 else "")}
+                      "api": ("rmips_build_index_host + rmips_query_batches_host (%d batches, pinned host buffers)%s"
+                              if args.query_api == "batches" else
+                              "rmips_build_index_host + %d rmips_query_host calls (pinned host buffers)%s")
+                             % (len(batches), " + shard.gather_csr" if ws > 1 else "")}
     del U, P, Qy, Qb, flush
     torch.cuda.empty_cache()
 
@@ -535,6 +551,9 @@ def main():
     ap.add_argument("--pprime", type=int, default=0,
                     help="NEXT-1: build the P' index over the first C * k_max items (Alg. 1 as printed) "
                          "and answer through Lemmas 1-2 and Alg. 2's scan; 0 = exact index over all of P")
+    ap.add_argument("--query-api", default="batches", choices=["batches", "calls"],
+                    help="batches: one rmips_query_batches call per step (the config's batches back to back, one "
+                         "host sync); calls: one rmips_query call per batch")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps

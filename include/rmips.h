@@ -162,6 +162,27 @@ RMIPS_API rmips_status_t rmips_query_host(rmips_index_t idx, const float* q_batc
                                 int64_t* offsets, int32_t* user_ids, int64_t capacity,
                                 int64_t* total_out, void* cuda_stream);
 
+/* rmips_query_batches -- a stream of queries answered in consecutive batches of `batch` (BASELINE
+ * configs[4]: "10,000 freshly generated queries in batches of 256"): the result equals calling
+ * rmips_query_ex on q_all[0 .. batch), q_all[batch .. 2 batch), ... and concatenating the sets in
+ * query order, but the batches run back to back on the stream with ONE host synchronisation at the
+ * end (each batch's output offsets continue from a device-side running total).
+ *   q_all      device, nq x d fp32 (may be NULL iff nq == 0); nq >= 0, batch >= 1
+ *   offsets    device, nq + 1 int64 (global: query i's users are user_ids[offsets[i] .. offsets[i+1]))
+ *   user_ids, capacity, total_out, flags, k: as rmips_query_ex (k > k_max extends once, up front)
+ * Shapes outside the bit-matrix output (RMIPS_FLAG_KEY_SORT, batch * ceil(n/32) * 4 > 64 MiB, n == 0)
+ * run as one rmips_query_ex per batch (one synchronisation each); same results.  The counters of
+ * rmips_query_stats are summed over the batches.  A batch that outgrows the pair workspace makes the
+ * call run every batch again with a larger one (the results never depend on it).
+ * Errors: as rmips_query_ex. */
+RMIPS_API rmips_status_t rmips_query_batches(rmips_index_t idx, const float* q_all, int64_t nq, int32_t batch,
+                                   int32_t k, int32_t flags, int64_t* offsets, int32_t* user_ids,
+                                   int64_t capacity, int64_t* total_out, void* cuda_stream);
+/* Same, with q_all, offsets and user_ids in HOST memory (one copy each way inside the call). */
+RMIPS_API rmips_status_t rmips_query_batches_host(rmips_index_t idx, const float* q_all, int64_t nq,
+                                        int32_t batch, int32_t k, int64_t* offsets, int32_t* user_ids,
+                                        int64_t capacity, int64_t* total_out, void* cuda_stream);
+
 /* Counters of the last rmips_query on idx (host struct filled). */
 RMIPS_API rmips_status_t rmips_query_stats(rmips_index_t idx, rmips_stats_t* out);
 

@@ -667,6 +667,235 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
   return RMIPS_OK;
 }
 
+// rmips_query_batches: per batch, the counters the host checks after a single call are folded on the
+// device (sums; the largest pair-workspace need; the OR of the error flags), so the batches run back
+// to back with one synchronisation at the end.
+__global__ void k_batch_fold(const unsigned long long* __restrict__ ctr, const int* __restrict__ flags,
+                             unsigned long long* __restrict__ acc) {
+  const int i = threadIdx.x;
+  if (i < kNumCounters) acc[i] += ctr[i];
+  if (i == 0) {
+    const unsigned long long need = ctr[C_ACCEPTED_TOTAL] > ctr[C_UND_TOTAL] ? ctr[C_ACCEPTED_TOTAL] : ctr[C_UND_TOTAL];
+    if (need > acc[kNumCounters]) acc[kNumCounters] = need;
+    acc[kNumCounters + 1] |= (unsigned long long)(unsigned)flags[0];
+  }
+}
+
+__global__ void k_shift_offsets(int64_t* __restrict__ off, int64_t cnt, int64_t base) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < cnt) off[i] += base;
+}
+
+static void fill_stats(rmips_index_s* x, const unsigned long long* hc, int64_t nq) {
+  rmips_stats_t& S = x->stats;
+  S.queries = nq;
+  S.block_query_pairs = hc[C_BLOCK_PAIRS];
+  S.block_query_pruned = hc[C_BLOCK_PRUNED];
+  S.pairs_scored = hc[C_SCORED];
+  S.pairs_rejected = hc[C_REJECTED];
+  S.pairs_accepted_fast = hc[C_ACCEPT_FAST];
+  S.pairs_undecided = hc[C_UNDECIDED];
+  S.pairs_exact_accepted = hc[C_EXACT_ACCEPT];
+  S.scans = hc[C_SCANS];
+  S.items_scanned = hc[C_ITEMS_SCANNED];
+  S.result_total = hc[C_ACC_REAL];
+  S.tiles_scored = hc[C_TILES_SCORED];
+  S.scan_exact = hc[C_SCAN_EXACT];
+}
+
+// Events of a timed rmips_query_batches: per batch, 4 phase marks + 2 around the filter kernel.
+thread_local std::vector<cudaEvent_t> g_bev;
+static cudaEvent_t* batch_events(size_t count) {
+  while (g_bev.size() < count) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    g_bev.push_back(e);
+  }
+  return g_bev.data();
+}
+
+rmips_status_t rmips_query_batches(rmips_index_t idx, const float* q_all, int64_t nq, int32_t batch, int32_t k,
+                                   int32_t flags, int64_t* offsets, int32_t* user_ids, int64_t capacity,
+                                   int64_t* total_out, void* cuda_stream) {
+  if (!idx || !total_out) return fail(RMIPS_ERR_INVALID, "NULL index or total_out");
+  if (nq < 0 || batch < 1 || capacity < 0) return fail(RMIPS_ERR_INVALID, "nq < 0, batch < 1 or capacity < 0");
+  if (nq > 0 && (!q_all || !offsets)) return fail(RMIPS_ERR_INVALID, "NULL q_all or offsets");
+  if (capacity > 0 && !user_ids) return fail(RMIPS_ERR_INVALID, "NULL user_ids with capacity > 0");
+  if (k < 1) return fail(RMIPS_ERR_K_RANGE, "k < 1");
+  if (k > idx->kmax && (flags & RMIPS_FLAG_NO_EXTEND)) return fail(RMIPS_ERR_K_RANGE, "k > k_max");
+  if ((flags & RMIPS_FLAG_SIMT) && idx->d > 256)
+    return fail(RMIPS_ERR_INVALID, "the SIMT (CUDA-core) query filter covers d <= 256; the tensor-core filter any d");
+  if (flags & ~(RMIPS_FLAG_NO_EXTEND | RMIPS_FLAG_NO_BLOCKS | RMIPS_FLAG_VERIFY_SCAN | RMIPS_FLAG_FORCE_VERIFY |
+                RMIPS_FLAG_SIMT | RMIPS_FLAG_TIMING | RMIPS_FLAG_KEY_SORT))
+    return fail(RMIPS_ERR_INVALID, "unknown flag bits");
+  rmips_index_s* x = idx;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  const int d = x->d;
+  *total_out = 0;
+  const int64_t nw = (x->n + 31) / 32;
+  const bool bits_path = nq > 0 && x->n > 0 && !(flags & RMIPS_FLAG_KEY_SORT) && (size_t)batch * nw * 4 <= kBitsMaxBytes;
+  if (!bits_path) {
+    // one rmips_query_ex per batch (a host synchronisation each), offsets shifted to the running total
+    int64_t base = 0;
+    bool over = false;
+    unsigned long long sums[kNumCounters] = {};
+    for (int64_t b0 = 0; b0 < nq || (nq == 0 && b0 == 0); b0 += batch) {
+      const int32_t bt = (int32_t)(nq - b0 < batch ? nq - b0 : batch);
+      int64_t t = 0;
+      const int64_t room = over || base > capacity ? 0 : capacity - base;
+      rmips_status_t s = rmips_query_ex(idx, bt ? q_all + b0 * d : nullptr, bt, k, flags, offsets + b0,
+                                        room ? user_ids + base : nullptr, room, &t, cuda_stream);
+      if (s == RMIPS_ERR_CAPACITY) over = true;
+      else if (s != RMIPS_OK) return s;
+      if (base && bt) {
+        k_shift_offsets<<<(unsigned)((bt + 1 + 255) / 256), 256, 0, st>>>(offsets + b0, bt + 1, base);
+        if (cudaGetLastError() != cudaSuccess) return fail(RMIPS_ERR_CUDA, "offset shift failed");
+      }
+      const rmips_stats_t& S = x->stats;
+      sums[C_BLOCK_PAIRS] += S.block_query_pairs, sums[C_BLOCK_PRUNED] += S.block_query_pruned;
+      sums[C_SCORED] += S.pairs_scored, sums[C_REJECTED] += S.pairs_rejected;
+      sums[C_ACCEPT_FAST] += S.pairs_accepted_fast, sums[C_UNDECIDED] += S.pairs_undecided;
+      sums[C_EXACT_ACCEPT] += S.pairs_exact_accepted, sums[C_SCANS] += S.scans;
+      sums[C_ITEMS_SCANNED] += S.items_scanned, sums[C_ACC_REAL] += S.result_total;
+      sums[C_TILES_SCORED] += S.tiles_scored, sums[C_SCAN_EXACT] += S.scan_exact;
+      base += t;
+      if (nq == 0) break;
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess) return fail(RMIPS_ERR_CUDA, "synchronisation failed");
+    fill_stats(x, sums, nq);
+    *total_out = base;
+    return over || base > capacity ? fail(RMIPS_ERR_CAPACITY, "result ids exceed capacity") : RMIPS_OK;
+  }
+  x->last_stream = st;
+  memset(&x->stats, 0, sizeof x->stats);
+  unsigned long long* acc = nullptr;  // [kNumCounters] sums, [.] largest need, [.] flags OR, then run[2]
+  try {
+    if (k > x->kmax) extend_lists(x, k, st);
+    const int64_t nb = (nq + batch - 1) / batch;
+    const int nacc = kNumCounters + 2 + 2;
+    acc = dalloc<unsigned long long>(nacc, st);
+    int64_t* run = reinterpret_cast<int64_t*>(acc + kNumCounters + 2);  // running totals (ping-pong)
+    int64_t cap = x->pair_cap > 0 ? x->pair_cap : (int64_t)1 << 20;
+    unsigned long long* hc = g_pin.get<unsigned long long>();
+    static_assert((kNumCounters + 4) * 8 <= 4096, "pinned staging");
+    cudaEvent_t* E = (flags & RMIPS_FLAG_TIMING) ? batch_events((size_t)6 * nb) : nullptr;
+    const long long l0 = g_launches.load();
+    for (int attempt = 0;; ++attempt) {
+      CK(cudaMemsetAsync(acc, 0, (size_t)nacc * 8, st));
+      for (int64_t t = 0; t < nb; ++t) {
+        if (E) CK(cudaEventRecord(E[6 * t], st));
+        const int64_t b0 = t * batch;
+        QueryCtx c;
+        c.idx = x; c.q = q_all + b0 * d; c.b = (int)(nq - b0 < batch ? nq - b0 : batch); c.k = k; c.flags = flags;
+        if (x->mprime < x->m) c.flags |= RMIPS_FLAG_FORCE_VERIFY;  // as rmips_query_ex
+        c.nsub = (c.b + kQB - 1) / kQB;
+        c.counters = x->d_counters;
+        c.flags_dev = x->d_flags;
+        if (E) c.ev_k[0] = E[6 * t + 4], c.ev_k[1] = E[6 * t + 5];
+        ensure_ws(x, c, c.nsub, cap, st);
+        if (!c.bits) throw CudaFail{cudaErrorUnknown, "bit-matrix workspace (always fits on this path)", __LINE__};
+        CK(zero4(st, x->d_counters, 2 * (kNumCounters + 4), x->d_flags, 4, nullptr, 0, nullptr, 0));
+        CK(query_prep(c, st));
+        if (E) CK(cudaEventRecord(E[6 * t + 1], st));
+        cudaError_t e = cudaErrorNotSupported;
+        if (!(flags & RMIPS_FLAG_SIMT) && !(x->build_flags & RMIPS_BUILD_SIMT)) e = query_filter_tc(c, st);
+        x->stats.filter_kernel = (e != cudaErrorNotSupported);
+        if (e == cudaErrorNotSupported) {
+          cudaGetLastError();
+          e = query_filter_simt(c, st);
+        }
+        CK(e);
+        if (E) CK(cudaEventRecord(E[6 * t + 2], st));
+        CK(query_exact(c, st));
+        CK(query_output_bits(c, offsets + b0, user_ids, capacity, st, run + (t & 1), run + ((t + 1) & 1)));
+        k_batch_fold<<<1, 64, 0, st>>>(x->d_counters, x->d_flags, acc);
+        count_launch();
+        CK(cudaGetLastError());
+        if (E) CK(cudaEventRecord(E[6 * t + 3], st));
+      }
+      CK(cudaMemcpyAsync(hc, acc, (size_t)(kNumCounters + 2) * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hc + kNumCounters + 2, run + (nb & 1), 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (hc[kNumCounters + 1] & kFlagNonfinite) {
+        dfree(acc, st);
+        return fail(RMIPS_ERR_NONFINITE, "query vector contains a NaN or Inf");
+      }
+      const unsigned long long need = hc[kNumCounters];
+      if ((int64_t)need <= cap) break;
+      cap = (int64_t)(need + need / 4 + 1024);  // a batch outgrew the pair workspace: run them all again
+      if (attempt == 2) {
+        dfree(acc, st);
+        return fail(RMIPS_ERR_CUDA, "pair workspace did not converge");
+      }
+    }
+    fill_stats(x, hc, nq);
+    x->phase_ms[15] = (double)(g_launches.load() - l0);
+    if (E) {  // phase times summed over the batches (rmips_phase_times: ms[8..13])
+      double ph[4] = {0, 0, 0, 0};
+      float ms = 0.f;
+      bool ok = true;
+      for (int64_t t = 0; t < nb; ++t) {
+        for (int i = 0; i < 3; ++i) {
+          ok = ok && cudaEventElapsedTime(&ms, E[6 * t + i], E[6 * t + i + 1]) == cudaSuccess;
+          ph[i] += ms;
+        }
+        if (x->stats.filter_kernel) {
+          ok = ok && cudaEventElapsedTime(&ms, E[6 * t + 4], E[6 * t + 5]) == cudaSuccess;
+          ph[3] += ms;
+        }
+      }
+      ok = ok && cudaEventElapsedTime(&ms, E[0], E[6 * (nb - 1) + 3]) == cudaSuccess;
+      x->phase_ms[8] = ok ? ph[0] : -1.0;
+      x->phase_ms[9] = ok ? ph[1] : -1.0;
+      x->phase_ms[10] = ok ? ph[2] : -1.0;
+      x->phase_ms[11] = 0.0;
+      x->phase_ms[12] = ok ? ms : -1.0;
+      x->phase_ms[13] = ok && x->stats.filter_kernel ? ph[3] : -1.0;
+    }
+    const int64_t total = (int64_t)hc[kNumCounters + 2];
+    dfree(acc, st);
+    acc = nullptr;
+    *total_out = total;
+    if (total > capacity) return fail(RMIPS_ERR_CAPACITY, "result ids exceed capacity");
+  } catch (const CudaFail& f) {
+    cudaStreamSynchronize(st);
+    x->bits_len = 0;
+    if (acc) dfree(acc, st);
+    return from_cuda(f);
+  }
+  return RMIPS_OK;
+}
+
+rmips_status_t rmips_query_batches_host(rmips_index_t idx, const float* q_all, int64_t nq, int32_t batch, int32_t k,
+                                        int64_t* offsets, int32_t* user_ids, int64_t capacity, int64_t* total_out,
+                                        void* cuda_stream) {
+  if (!idx || !total_out) return fail(RMIPS_ERR_INVALID, "NULL index or total_out");
+  if (nq < 0 || batch < 1 || capacity < 0) return fail(RMIPS_ERR_INVALID, "nq < 0, batch < 1 or capacity < 0");
+  if (nq > 0 && (!q_all || !offsets)) return fail(RMIPS_ERR_INVALID, "NULL q_all or offsets");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  float* dq = nullptr;
+  int64_t* doff = nullptr;
+  int32_t* dids = nullptr;
+  rmips_status_t s;
+  try {
+    dq = dalloc<float>(nq * idx->d, st);
+    doff = dalloc<int64_t>(nq + 1, st);
+    dids = dalloc<int32_t>(capacity, st);
+    if (nq) CK(cudaMemcpyAsync(dq, q_all, (size_t)nq * idx->d * 4, cudaMemcpyHostToDevice, st));
+    s = rmips_query_batches(idx, dq, nq, batch, k, RMIPS_FLAG_NONE, doff, dids, capacity, total_out, cuda_stream);
+    if (s == RMIPS_OK || s == RMIPS_ERR_CAPACITY) {
+      CK(cudaMemcpyAsync(offsets, doff, (size_t)(nq + 1) * 8, cudaMemcpyDeviceToHost, st));
+      if (s == RMIPS_OK && *total_out > 0)
+        CK(cudaMemcpyAsync(user_ids, dids, (size_t)*total_out * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+  } catch (const CudaFail& f) {
+    s = from_cuda(f);
+  }
+  dfree(dq, st); dfree(doff, st); dfree(dids, st);
+  return s;
+}
+
 rmips_status_t rmips_query(rmips_index_t idx, const float* q_batch, int32_t b, int32_t k, int64_t* offsets,
                            int32_t* user_ids, int64_t capacity, int64_t* total_out, void* cuda_stream) {
   return rmips_query_ex(idx, q_batch, b, k, RMIPS_FLAG_NONE, offsets, user_ids, capacity, total_out, cuda_stream);

@@ -121,6 +121,9 @@ int64_t query_bits_chunks(int b, int64_t nw);  // warp chunks of the bit-matrix 
 // zero four small regions (counts in 32-bit words, <= 128 each) in one launch (build.cu)
 cudaError_t zero4(cudaStream_t st, void* a, int na, void* b, int nb, void* c, int nc, void* d, int nd);
 cudaError_t query_sort(QueryCtx& c, int64_t total, int end_bit, cudaStream_t st);
-cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st);
+// obase / obase_next (device words, both NULL for a single call): ids already written by earlier batches
+// of rmips_query_batches; this batch's running total is stored to obase_next
+cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st,
+                              const int64_t* obase = nullptr, int64_t* obase_next = nullptr);
 
 }  // namespace rmips

@@ -755,18 +755,24 @@ k_bits_count(const uint32_t* __restrict__ bits, int64_t nw, int64_t nchunk_total
 __global__ void __launch_bounds__(kBitsThreads)
 k_bits_emit(uint32_t* __restrict__ bits, int64_t nw, int b, int64_t nchunk_total, const int64_t* __restrict__ counts,
             const int64_t* __restrict__ chunk_off, int64_t capacity, int64_t* __restrict__ offsets,
-            int32_t* __restrict__ out) {
+            int32_t* __restrict__ out, const int64_t* __restrict__ obase, int64_t* __restrict__ obase_next) {
   const int64_t g = (blockIdx.x * (int64_t)kBitsThreads + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (g >= nchunk_total) return;
   const int64_t per_row = (nw + kChunkWords - 1) / kChunkWords;
   const int64_t q = g / per_row, c = g - q * per_row;
-  const int64_t total = chunk_off[nchunk_total - 1] + counts[nchunk_total - 1];
+  // obase (batched calls, rmips_query_batches): the ids of the earlier batches already in `out`; this
+  // batch's running total goes to obase_next (a different word: every block reads obase)
+  const int64_t b0 = obase ? *obase : 0;
+  const int64_t total = b0 + chunk_off[nchunk_total - 1] + counts[nchunk_total - 1];
   const bool fits = total <= capacity;  // ids only when all of them fit (as the sorted-key path)
-  int64_t base = chunk_off[g];
+  int64_t base = b0 + chunk_off[g];
   if (lane == 0) {
     if (c == 0) offsets[q] = base;
-    if (g == nchunk_total - 1) offsets[b] = total;
+    if (g == nchunk_total - 1) {
+      offsets[b] = total;
+      if (obase_next) *obase_next = total;
+    }
   }
   if (counts[g] == 0) return;  // (warp-uniform) nothing set in this chunk
   uint32_t* row = bits + q * nw;
@@ -810,7 +816,8 @@ size_t query_scan_bytes(int64_t items) {
 }
 int64_t query_bits_chunks(int b, int64_t nw) { return (int64_t)b * ((nw + kChunkWords - 1) / kChunkWords); }
 
-cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st) {
+cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st,
+                              const int64_t* obase, int64_t* obase_next) {
   const int64_t nch = query_bits_chunks(c.b, c.nw);
   int64_t* counts = reinterpret_cast<int64_t*>(c.acc_sorted);  // the sort's space is unused on this path
   int64_t* chunk_off = counts + nch;
@@ -820,7 +827,8 @@ cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, 
   cudaError_t e = cub::DeviceScan::ExclusiveSum(c.cub_tmp, tb, counts, chunk_off, (int)nch, st);
   count_launch(2);
   if (e != cudaSuccess) return e;
-  k_bits_emit<<<grid, kBitsThreads, 0, st>>>(c.bits, c.nw, c.b, nch, counts, chunk_off, capacity, offsets, user_ids);
+  k_bits_emit<<<grid, kBitsThreads, 0, st>>>(c.bits, c.nw, c.b, nch, counts, chunk_off, capacity, offsets, user_ids,
+                                              obase, obase_next);
   count_launch();
   return cudaGetLastError();
 }

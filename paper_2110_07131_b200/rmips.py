@@ -30,7 +30,7 @@ RMIPS_BUILD_SIMT = 1
 RMIPS_BUILD_TIMING = 2
 
 EXPORTED = ["rmips_build_index", "rmips_build_index_ex", "rmips_build_index_pprime", "rmips_build_index_host", "rmips_query", "rmips_query_ex",
-            "rmips_query_host", "rmips_query_stats", "rmips_phase_times", "rmips_index_info", "rmips_index_export", "rmips_free_index",
+            "rmips_query_host", "rmips_query_batches", "rmips_query_batches_host", "rmips_query_stats", "rmips_phase_times", "rmips_index_info", "rmips_index_export", "rmips_free_index",
             "rmips_status_string", "rmips_last_error", "rmips_version"]
 
 
@@ -64,6 +64,8 @@ def _load() -> ctypes.CDLL:
     lib.rmips_query.argtypes = [VP, P, I32, I32, P, P, I64, ctypes.POINTER(I64), VP]
     lib.rmips_query_ex.argtypes = [VP, P, I32, I32, I32, P, P, I64, ctypes.POINTER(I64), VP]
     lib.rmips_query_host.argtypes = [VP, P, I32, I32, P, P, I64, ctypes.POINTER(I64), VP]
+    lib.rmips_query_batches.argtypes = [VP, P, I64, I32, I32, I32, P, P, I64, ctypes.POINTER(I64), VP]
+    lib.rmips_query_batches_host.argtypes = [VP, P, I64, I32, I32, P, P, I64, ctypes.POINTER(I64), VP]
     lib.rmips_query_stats.argtypes = [VP, ctypes.POINTER(Stats)]
     lib.rmips_index_info.argtypes = [VP, ctypes.POINTER(I64)]
     lib.rmips_phase_times.argtypes = [VP, ctypes.POINTER(ctypes.c_double)]
@@ -75,7 +77,8 @@ def _load() -> ctypes.CDLL:
     lib.rmips_status_string.argtypes = [ctypes.c_int]
     for f in ("rmips_build_index", "rmips_build_index_ex", "rmips_build_index_pprime", "rmips_build_index_host",
               "rmips_query",
-              "rmips_query_ex", "rmips_query_host", "rmips_query_stats", "rmips_phase_times", "rmips_index_info", "rmips_index_export"):
+              "rmips_query_ex", "rmips_query_host", "rmips_query_batches", "rmips_query_batches_host", "rmips_query_stats",
+              "rmips_phase_times", "rmips_index_info", "rmips_index_export"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -224,6 +227,50 @@ def rmips_query(index: Index, q_batch, k: int, flags: int = RMIPS_FLAG_NONE, cap
         ids = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
         st = lib.rmips_query_ex(index.handle, q_batch.data_ptr() if b else None, b, int(k), int(flags),
                                 offsets.data_ptr(), ids.data_ptr(), cap, ctypes.byref(total), _stream_ptr(stream))
+        if st == RMIPS_ERR_CAPACITY and capacity is None:
+            cap = int(total.value)
+            continue
+        _check(st)
+        break
+    return offsets, ids[: total.value]
+
+
+def rmips_query_batches(index: Index, q_all, batch: int, k: int, flags: int = RMIPS_FLAG_NONE,
+                        capacity: Optional[int] = None, stream=None) -> Tuple["object", "object"]:
+    """q_all [nq, d] (device) answered in consecutive batches of `batch`, one host sync in total.
+    Returns (offsets int64 [nq+1], user_ids int32 [total]) as CUDA tensors, as rmips_query."""
+    import torch
+    q_all = _dev_f32(q_all)
+    nq = int(q_all.shape[0])
+    dev = q_all.device
+    offsets = torch.empty(nq + 1, dtype=torch.int64, device=dev)
+    cap = int(capacity) if capacity is not None else max(1 << 16, 64 * nq)
+    total = ctypes.c_int64(0)
+    for _ in range(2):
+        ids = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        st = lib.rmips_query_batches(index.handle, q_all.data_ptr() if nq else None, nq, int(batch), int(k),
+                                     int(flags), offsets.data_ptr(), ids.data_ptr(), cap, ctypes.byref(total),
+                                     _stream_ptr(stream))
+        if st == RMIPS_ERR_CAPACITY and capacity is None:
+            cap = int(total.value)
+            continue
+        _check(st)
+        break
+    return offsets, ids[: total.value]
+
+
+def rmips_query_batches_host(index: Index, q_all, batch: int, k: int, capacity: Optional[int] = None,
+                             out_offsets=None, out_ids=None, stream=None):
+    """Host-buffer variant of rmips_query_batches (one copy each way inside the call)."""
+    q_all = _host_f32(q_all)
+    nq = q_all.shape[0]
+    offsets = out_offsets if out_offsets is not None else np.empty(nq + 1, np.int64)
+    cap = int(capacity) if capacity is not None else max(1 << 16, 64 * nq)
+    total = ctypes.c_int64(0)
+    for _ in range(2):
+        ids = out_ids if (out_ids is not None and _numel(out_ids) >= cap) else np.empty(max(cap, 1), np.int32)
+        st = lib.rmips_query_batches_host(index.handle, _hptr(q_all) if nq else None, nq, int(batch), int(k),
+                                          _hptr(offsets), _hptr(ids), cap, ctypes.byref(total), _stream_ptr(stream))
         if st == RMIPS_ERR_CAPACITY and capacity is None:
             cap = int(total.value)
             continue

@@ -777,3 +777,46 @@ def test_tiled_verification_scan_dev():
                        timeout=900)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "BAD 0" in r.stdout, r.stdout[-500:]
+
+
+def _np(t):
+    return t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)
+
+
+def test_query_batches_equals_single_calls(cfg0):
+    """rmips_query_batches (one host sync for all batches) = rmips_query per batch, concatenated:
+    ragged last batch, several batch sizes, the key-sort fallback, k > k_max, capacity, host variant."""
+    w, member = cfg0
+    idx = rmips.rmips_build_index(_t(w.U), _t(w.P), 10)
+    off, ids = rmips.rmips_query_batches(idx, _t(w.Qy), 32, 10)  # 100 queries: 32, 32, 32, 4
+    assert_same(rmips.split_sets(off, ids), member, w.U, w.P, w.Qy, 10, "cfg0 batches")
+    assert idx.stats()["queries"] == 100 and idx.stats()["result_total"] == int(member.sum())
+    U, P = gen.random_instance(21, 3000, 700, 40)
+    Qy = P[np.arange(700) % len(P)]
+    idx2 = rmips.rmips_build_index(_t(U), _t(P), 12)
+    for batch in (256, 100, 700, 1000, 1):
+        for fl in (0, rmips.RMIPS_FLAG_KEY_SORT):
+            o1, i1 = rmips.rmips_query_batches(idx2, _t(Qy[:300] if batch == 1 else Qy), batch, 9, fl)
+            q = Qy[:300] if batch == 1 else Qy
+            parts = [rmips.rmips_query(idx2, _t(q[b0:b0 + batch]), 9) for b0 in range(0, len(q), batch)]
+            want = [s for o, i in parts for s in rmips.split_sets(o, i)]
+            got = rmips.split_sets(o1, i1)
+            assert len(got) == len(q) and all(np.array_equal(a, b) for a, b in zip(got, want)), (batch, fl)
+            assert int(_np(o1)[0]) == 0 and int(_np(o1)[-1]) == len(_np(i1))
+    # k > k_max extends once, up front (the same sets as single calls after the extension)
+    o1, i1 = rmips.rmips_query_batches(idx2, _t(Qy[:500]), 256, 20)
+    parts = [rmips.rmips_query(idx2, _t(Qy[b0:b0 + 256]), 20) for b0 in (0, 256)]
+    want = [s for o, i in parts for s in rmips.split_sets(o, i)]
+    assert all(np.array_equal(a, b) for a, b in zip(rmips.split_sets(o1, i1), want))
+    # capacity: an explicit small capacity fails with the needed total; None retries
+    with pytest.raises(rmips.RmipsError) as e:
+        rmips.rmips_query_batches(idx2, _t(Qy), 256, 9, capacity=3)
+    assert e.value.status == rmips.RMIPS_ERR_CAPACITY
+    o1, i1 = rmips.rmips_query_batches(idx2, _t(Qy), 256, 9)
+    ho, hi = rmips.rmips_query_batches_host(idx2, Qy, 256, 9)
+    assert np.array_equal(_np(o1), ho) and np.array_equal(_np(i1), hi)
+    # nq = 0
+    o0, i0 = rmips.rmips_query_batches(idx2, _t(Qy[:0]), 256, 9)
+    assert _np(o0).tolist() == [0] and len(_np(i0)) == 0
+    idx.close()
+    idx2.close()
