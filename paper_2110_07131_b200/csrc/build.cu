@@ -24,7 +24,8 @@ namespace rmips {
 // A CTA stages its kNormRows rows in shared memory with coalesced loads (odd row stride: no bank
 // conflicts), then each thread sums its own row left to right (the oracle's order).
 constexpr int kNormRows = 128;
-__global__ void __launch_bounds__(kNormRows)
+constexpr int kNormThreads = 512;  // all load (more bytes in flight); the first kNormRows sum the rows
+__global__ void __launch_bounds__(kNormThreads)
 k_norms(const float* __restrict__ X, int64_t rows, int d, uint64_t* __restrict__ keys,
         uint64_t topbit, int* __restrict__ flags, unsigned int* __restrict__ maxabs_bits, bool staged) {
   extern __shared__ float xs[];
@@ -34,34 +35,52 @@ k_norms(const float* __restrict__ X, int64_t rows, int d, uint64_t* __restrict__
   const float* src = X + r0 * d;
   float mx = 0.f;
   bool fin = true;
-  // the block's rows are one contiguous run of nr * d floats: coalesced loads, eight independent
-  // ones in flight per thread (a load-then-use loop kept one: 1 TB/s on configs[4])
+  // the block's rows are one contiguous run of nr * d floats, 16-byte aligned when X is (r0 * d * 4 is
+  // a multiple of 512): 16-byte loads, eight independent ones (128 bytes) in flight per thread (scalar
+  // loads kept too few bytes in flight: 1.2 TB/s on configs[4])
   const int tot = nr * d;
   const float inv_d = 1.f / (float)d;  // row of element e: floor((e + 0.5) / d), exact for e < 2^17, d <= 1024
-  for (int e0 = threadIdx.x; e0 < tot; e0 += 8 * kNormRows) {
-    float v[8];
+  auto take = [&](int e, float v) {
+    fin &= isfinite(v);
+    mx = fmaxf(mx, fabsf(v));
+    if (staged) {
+      const int rr = __float2int_rz(((float)e + 0.5f) * inv_d);
+      xs[rr * ds + (e - rr * d)] = v;
+    }
+  };
+  // (a caller's view may start anywhere: unaligned X takes the scalar tail loop for every element)
+  const int n4 = (reinterpret_cast<uintptr_t>(X) & 15u) == 0 ? tot >> 2 : 0;
+  const float4* src4 = reinterpret_cast<const float4*>(src);
+  for (int i0 = threadIdx.x; i0 < n4; i0 += 8 * kNormThreads) {
+    float4 v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * kNormRows;
-      v[u] = e < tot ? __ldg(src + e) : 0.f;
+      const int i = i0 + u * kNormThreads;
+      v[u] = i < n4 ? __ldg(src4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * kNormRows;
-      fin &= isfinite(v[u]);
-      mx = fmaxf(mx, fabsf(v[u]));
-      if (staged && e < tot) {
-        const int rr = __float2int_rz(((float)e + 0.5f) * inv_d);
-        xs[rr * ds + (e - rr * d)] = v[u];
+      const int i = i0 + u * kNormThreads;
+      if (i < n4) {
+        take(4 * i, v[u].x);
+        take(4 * i + 1, v[u].y);
+        take(4 * i + 2, v[u].z);
+        take(4 * i + 3, v[u].w);
       }
     }
   }
+  for (int e = 4 * n4 + threadIdx.x; e < tot; e += kNormThreads) take(e, __ldg(src + e));  // (tot % 4 tail, unaligned X)
   __syncthreads();
   if (threadIdx.x < nr) {
-    // (d > 400: the 128 rows do not fit in shared memory; each thread re-reads its row, L2-resident)
-    const float* x = staged ? xs + threadIdx.x * ds : src + (int64_t)threadIdx.x * d;
     double s = 0.0;
-    for (int j = 0; j < d; ++j) s = __fma_rn((double)x[j], (double)x[j], s);
+    if (staged) {  // (a shared-memory pointer of its own: LDS, not generic loads)
+      const float* x = xs + threadIdx.x * ds;
+#pragma unroll 8
+      for (int j = 0; j < d; ++j) s = __fma_rn((double)x[j], (double)x[j], s);
+    } else {  // d > 400: the 128 rows do not fit in shared memory; each thread re-reads its row (L2)
+      const float* x = src + (int64_t)threadIdx.x * d;
+      for (int j = 0; j < d; ++j) s = __fma_rn((double)__ldg(x + j), (double)__ldg(x + j), s);
+    }
     keys[r0 + threadIdx.x] = (uint64_t)__double_as_longlong(sqrt(s)) | topbit;
   }
   if (__any_sync(0xffffffffu, !fin) && (threadIdx.x & 31) == 0) atomicOr(flags, kFlagNonfinite);
@@ -849,8 +868,10 @@ cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t
   uint64_t* kout = kin + tot;
   int32_t* vin = sg ? sg->vals : c.nval;
   int32_t* vout = vin + tot;
-  k_norms<<<nblk(m, kNormRows), kNormRows, nsm, st>>>(P, m, d, kin, 1ull << 63, x->d_flags, c.maxabs, staged); count_launch();
-  if (n) k_norms<<<nblk(n, kNormRows), kNormRows, nsm, st>>>(Q, n, d, kin + m, 0ull, x->d_flags, nullptr, staged); count_launch();
+  k_norms<<<nblk(m, kNormRows), kNormThreads, nsm, st>>>(P, m, d, kin, 1ull << 63, x->d_flags, c.maxabs, staged);
+  count_launch();
+  if (n) k_norms<<<nblk(n, kNormRows), kNormThreads, nsm, st>>>(Q, n, d, kin + m, 0ull, x->d_flags, nullptr, staged);
+  if (n) count_launch();
   // B2: one stable radix sort (descending norm, ties by ascending index: reading R6)
   if (sg) {
     cudaError_t e = cudaGraphLaunch(sg->exec, st);

@@ -820,3 +820,21 @@ def test_query_batches_equals_single_calls(cfg0):
     assert _np(o0).tolist() == [0] and len(_np(i0)) == 0
     idx.close()
     idx2.close()
+
+
+def test_unaligned_input_views_build_identical_index():
+    """Q and P given as row-slice views whose data pointers are not 16-byte aligned (d = 50: a one-row
+    offset is 200 bytes) build the same index, bit for bit, as aligned copies."""
+    import torch
+    U, P = gen.random_instance(31, 1500, 700, 50)
+    Ub = torch.from_numpy(np.vstack([U[:1], U])).cuda()
+    Pb = torch.from_numpy(np.vstack([P[:1], P])).cuda()
+    Uv, Pv = Ub[1:], Pb[1:]
+    assert Uv.data_ptr() % 16 != 0 and Pv.data_ptr() % 16 != 0
+    a = rmips.rmips_build_index(Uv, Pv, 10)
+    b = rmips.rmips_build_index(_t(U), _t(P), 10)
+    ta, tb = a.export(), b.export()
+    for x, y in zip(ta, tb):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
+    a.close()
+    b.close()
