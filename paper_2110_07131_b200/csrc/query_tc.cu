@@ -44,6 +44,7 @@ constexpr int kThreads = 320;           // producer, MMA, 8 epilogue warps (2 pe
 constexpr int kDevQEpiSkip = 1 << 28;  // RMIPS_Q_EPI_SKIP: the epilogue releases every stage unread
 constexpr int kDevQNoSlow = 1 << 27;   // RMIPS_Q_NO_SLOW: flagged chunks are not classified (timing only)
 constexpr int kDevQCount = 1 << 26;    // RMIPS_Q_COUNT: count flagged / examined warp-chunks (g_qdev)
+constexpr int kDevQNoFeed = 1 << 25;   // RMIPS_Q_NOFEED: ring units after the first round are not reloaded
 #ifdef RMIPS_DEV
 __device__ unsigned long long g_qdev[4];  // dev: [0] flagged warp-chunks, [1] examined warp-chunks
 #endif
@@ -335,7 +336,7 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
-      int stage = 0, cur_s = -1, nq = 0;
+      int stage = 0, cur_s = -1, nq = 0, nloads = 0;
       uint32_t ph = 0;
       int s, t;
       first_item(s, t);
@@ -358,6 +359,12 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
             QPROF_ADD(4);
           }
           const bool last = kb == kbn - 1;
+          if ((flags & kDevQNoFeed) && nloads >= kStages) {  // dev: stale unit, no HBM traffic
+            mbar_arrive(BAR(A_FULL + stage));
+            if (++stage == kStages) stage = 0, ph ^= 1;
+            continue;
+          }
+          ++nloads;
           mbar_arrive_expect_tx(BAR(A_FULL + stage), (last ? utail : (uint32_t)kUTileBytes) +
                                                          (kStreamQ ? (last ? qtail : (uint32_t)kQTileBytes) : 0u));
           tma_load_2d(sA + stage * kUnit, last ? &tmUt : &tmU, kb * 64, t * kBM, BAR(A_FULL + stage));
@@ -627,6 +634,7 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
   if (getenv("RMIPS_Q_EPI_SKIP")) kflags |= kDevQEpiSkip;
   if (getenv("RMIPS_Q_NO_SLOW")) kflags |= kDevQNoSlow;
   if (getenv("RMIPS_Q_COUNT")) kflags |= kDevQCount;
+  if (getenv("RMIPS_Q_NOFEED")) kflags |= kDevQNoFeed;
 #endif
   k_lemma3_lens<<<(unsigned)((nwork + 255) / 256), 256, 0, st>>>(x->tb + (int64_t)(c.k - 1) * x->nlb, c.qn,
                                                                  c.qcount, (int)x->nblocks, x->bsz, x->nlb, nwork,
