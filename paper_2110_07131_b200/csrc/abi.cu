@@ -501,7 +501,8 @@ static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cuda
          owl = take((size_t)nsub * x->nblocks * 4), oacc = take((size_t)cap * 8),
          ound = take((size_t)cap * 8), oscn = take((size_t)cap * 4),
          osrec = take((size_t)cap * 8), osbt = take((size_t)cap * 4),
-         osrt = take((size_t)cap * 8), ocub = take(qcub), obits = take(use_bits ? (size_t)c.b * nw * 4 : 0);
+         osrt = take((size_t)cap * 8), ocub = take(qcub),
+         obits = take(use_bits ? (size_t)c.b * nw * 4 + (size_t)c.b * ((nw + 31) / 32) : 0);  // + dirty bytes
   if (off > x->ws_bytes) {
     x->bits_len = 0;
     if (x->ws) cudaFreeAsync(x->ws, st);
@@ -528,9 +529,11 @@ static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cuda
   c.cub_tmp = b + ocub;
   c.bits = use_bits ? reinterpret_cast<uint32_t*>(b + obits) : nullptr;
   c.nw = nw;
+  c.nbr = (nw + 31) / 32;
+  c.dirty = use_bits ? reinterpret_cast<uint8_t*>(c.bits + (size_t)c.b * nw) : nullptr;
   // the matrix is left all zero by every completed query (k_bits_emit clears what it reads); it
   // is cleared here only when its place or size changed, or after a failed call
-  const size_t nbits = use_bits ? (size_t)c.b * nw * 4 : 0;
+  const size_t nbits = use_bits ? (size_t)c.b * nw * 4 + (size_t)c.b * c.nbr : 0;  // words + dirty bytes
   if (!use_bits) x->bits_len = 0;  // this layout may write over the old matrix
   if (use_bits && (x->bits_off != obits || x->bits_len < nbits)) {
     CK(cudaMemsetAsync(c.bits, 0, nbits, st));

@@ -90,6 +90,8 @@ struct AccSink {
   uint64_t* list;
   uint32_t* bits;
   int64_t nw;
+  uint8_t* dirty;  // bits path: one byte per 32-word block (1024 users) of a query row, set with its bits
+  int64_t nbr;     // blocks per row
   // warp-collective: every lane calls it (bits is warp-uniform)
   __device__ __forceinline__ void put(bool pred, uint64_t key, unsigned long long* count, int64_t cap) const {
     if (bits) {
@@ -108,7 +110,9 @@ struct AccSink {
   }
   __device__ __forceinline__ void set(uint64_t key) const {
     const uint32_t u = (uint32_t)key;
-    atomicOr(bits + (int64_t)(key >> 32) * nw + (u >> 5), 1u << (u & 31));
+    const int64_t q = (int64_t)(key >> 32);
+    atomicOr(bits + q * nw + (u >> 5), 1u << (u & 31));
+    dirty[q * nbr + (u >> 10)] = 1;  // (every writer stores 1: no race to resolve)
   }
 };
 

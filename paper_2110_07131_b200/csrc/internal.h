@@ -89,6 +89,8 @@ struct QueryCtx {
   uint64_t* acc = nullptr;       // accepted keys (q_input << 32 | original user id)
   uint32_t* bits = nullptr;      // or: accepted pairs as bits of a [b][nw] word matrix (no sort)
   int64_t nw = 0;                // words per query row of bits, ceil(n / 32)
+  uint8_t* dirty = nullptr;      // [b][nbr] one byte per 32-word block of bits: set when a bit in it is
+  int64_t nbr = 0;               // blocks per query row, ceil(nw / 32)
   uint64_t* und = nullptr;       // undecided (q_input << 32 | sorted user position)
   int32_t* scan_cnt = nullptr;   // [cap] P' index: items of P' that beat q, for the scan after P'
   uint64_t* scan_rec = nullptr;  // [cap] the pairs left for Alg. 2's scan, packed densely

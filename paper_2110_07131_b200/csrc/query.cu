@@ -627,7 +627,7 @@ static cudaError_t launch_query_simt(QueryCtx& c, cudaStream_t st) {
   dim3 grid((unsigned)x->nblocks, (unsigned)c.nsub);
   k_query_simt<DPAD><<<grid, 128, smem, st>>>(x->U16, x->ldh, x->thr + (int64_t)(c.k - 1) * x->n,
                                               x->tb + (int64_t)(c.k - 1) * x->nlb, x->bsz, x->nlb, x->perm_u, x->n, c.Q16, c.qn,
-                                              c.qerr, c.qscale, c.qperm, c.qcount, c.flags, c.counters, AccSink{c.acc, c.bits, c.nw}, c.und,
+                                              c.qerr, c.qscale, c.qperm, c.qcount, c.flags, c.counters, AccSink{c.acc, c.bits, c.nw, c.dirty, c.nbr}, c.und,
                                               c.cap); count_launch();
   return cudaGetLastError();
 }
@@ -664,7 +664,7 @@ static cudaError_t launch_scan(QueryCtx& c, int64_t start, const int32_t* beats0
       CK_RET(set_smem_attr((const void*)k_verify_scan_warp, (int)smem));
     k_verify_scan_warp<<<148 * 8, 32 * kScanWarps, smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u,
                                                                 x->m, x->d, x->pd, c.k, c.counters, c.scan_rec,
-                                                                c.scan_beats, AccSink{c.acc, c.bits, c.nw}, c.cap, start,
+                                                                c.scan_beats, AccSink{c.acc, c.bits, c.nw, c.dirty, c.nbr}, c.cap, start,
                                                                 count_und);
     count_launch();
     return cudaGetLastError();
@@ -675,7 +675,7 @@ static cudaError_t launch_scan(QueryCtx& c, int64_t start, const int32_t* beats0
   if (smem > 48 * 1024) CK_RET(set_smem_attr((const void*)k_verify_scan, (int)smem));
   k_verify_scan<<<148 * 2, 32 * kScanWarps, smem, st>>>(c.q, x->U32, x->unorm, x->P32, x->pnorm, x->perm_u, x->m, x->d,
                                                         x->pd, c.k, c.counters, c.scan_rec, c.scan_beats,
-                                                        AccSink{c.acc, c.bits, c.nw}, c.cap, start, count_und, pw, rows);
+                                                        AccSink{c.acc, c.bits, c.nw, c.dirty, c.nbr}, c.cap, start, count_und, pw, rows);
   count_launch();
   return cudaGetLastError();
 }
@@ -687,14 +687,14 @@ cudaError_t query_exact(QueryCtx& c, cudaStream_t st) {
     CK_RET(launch_scan(c, 0, nullptr, true, st));
   } else if (x->mprime < x->m) {  // P' index: Lemmas 1-2 / Cor. 1 per pair, then the scan after P'
     k_exact_decide_pp<<<148 * 8, 256, 0, st>>>(c.q, x->U32, x->unorm, x->pnorm, x->tau, x->n, x->m, x->mprime, c.k,
-                                               x->perm_u, x->d, c.counters, c.und, c.scan_cnt, AccSink{c.acc, c.bits, c.nw}, c.cap);
+                                               x->perm_u, x->d, c.counters, c.und, c.scan_cnt, AccSink{c.acc, c.bits, c.nw, c.dirty, c.nbr}, c.cap);
     count_launch();
     CK_RET(launch_scan(c, x->mprime, c.scan_cnt, false, st));
   } else {
     k_scan_compact<<<148 * 4, 256, 0, st>>>(c.und, nullptr, c.counters, c.cap, c.scan_rec, c.scan_beats);
     count_launch();
     k_exact_decide<<<148 * 4, 256, 0, st>>>(c.q, x->U32, x->tau + (int64_t)(c.k - 1) * x->n, x->perm_u, x->d,
-                                            c.counters, c.scan_rec, AccSink{c.acc, c.bits, c.nw}, c.cap);
+                                            c.counters, c.scan_rec, AccSink{c.acc, c.bits, c.nw, c.dirty, c.nbr}, c.cap);
     count_launch();
   }
   return cudaGetLastError();
@@ -727,35 +727,40 @@ __global__ void k_copy_ids32(const uint32_t* __restrict__ keys, int64_t total, u
 }
 
 // Bit-matrix output (QueryCtx::bits): the b x n matrix is cut into warp chunks of kChunkWords words of
-// one query row.  A warp reads its chunk in 32 coalesced steps (step i: lane l holds word 32 i + l).
-// Pass 1 counts the set bits of every chunk, a scan gives every chunk's first output position (the
-// chunks are in (query, user) order), and pass 2 re-reads the chunk, writes the ids of every step in
-// ascending user order (a warp prefix sum over the lanes' popcounts) and clears the words it read, so
-// the matrix is all zero again for the next batch (it is memset only when its place in the workspace
-// changes).  Every warp works independently: no block-level loop over a whole row.
+// one query row; lane l of a chunk's warp owns block l (32 consecutive words, 1024 users).  Only blocks
+// whose dirty byte is set (AccSink::set) are read: a 256-query batch of configs[4] sets ~11,000 of
+// 256 M bits, so the passes read the 0.25 MB of dirty bytes and ~1 MB of words instead of the 32 MB
+// matrix.  Pass 1 counts the set bits of every chunk, a scan gives every chunk's first output position
+// (the chunks are in (query, user) order), and pass 2 re-reads the dirty blocks, writes the ids in
+// ascending user order (a warp prefix sum over the lanes' block counts) and clears the words and dirty
+// bytes it read, so both are all zero again for the next batch (they are memset only when their place
+// in the workspace changes).  Every warp works independently.
 constexpr int kChunkWords = 1024;
 constexpr int kBitsThreads = 256;
 __global__ void __launch_bounds__(kBitsThreads)
-k_bits_count(const uint32_t* __restrict__ bits, int64_t nw, int64_t nchunk_total, int64_t* __restrict__ counts) {
+k_bits_count(const uint32_t* __restrict__ bits, const uint8_t* __restrict__ dirty, int64_t nw, int64_t nbr,
+             int64_t nchunk_total, int64_t* __restrict__ counts) {
   const int64_t g = (blockIdx.x * (int64_t)kBitsThreads + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (g >= nchunk_total) return;
   const int64_t per_row = (nw + kChunkWords - 1) / kChunkWords;
   const int64_t q = g / per_row, c = g - q * per_row;
-  const uint32_t* row = bits + q * nw;
-  const int64_t w0 = c * kChunkWords + lane;
+  const int64_t blk = c * 32 + lane;  // this lane's block of the row
   int cnt = 0;
-#pragma unroll 8
-  for (int i = 0; i < 32; ++i)
-    if (w0 + 32 * i < nw) cnt += __popc(__ldcs(row + w0 + 32 * i));  // (streamed: read once more by the emit)
+  if (blk < nbr && dirty[q * nbr + blk]) {
+    const uint32_t* wp = bits + q * nw + blk * 32;
+    const int nwb = (int)min((int64_t)32, nw - blk * 32);
+    for (int i = 0; i < nwb; ++i) cnt += __popc(wp[i]);
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   if (lane == 0) counts[g] = cnt;
 }
 __global__ void __launch_bounds__(kBitsThreads)
-k_bits_emit(uint32_t* __restrict__ bits, int64_t nw, int b, int64_t nchunk_total, const int64_t* __restrict__ counts,
-            const int64_t* __restrict__ chunk_off, int64_t capacity, int64_t* __restrict__ offsets,
-            int32_t* __restrict__ out, const int64_t* __restrict__ obase, int64_t* __restrict__ obase_next) {
+k_bits_emit(uint32_t* __restrict__ bits, uint8_t* __restrict__ dirty, int64_t nw, int64_t nbr, int b,
+            int64_t nchunk_total, const int64_t* __restrict__ counts, const int64_t* __restrict__ chunk_off,
+            int64_t capacity, int64_t* __restrict__ offsets, int32_t* __restrict__ out,
+            const int64_t* __restrict__ obase, int64_t* __restrict__ obase_next) {
   const int64_t g = (blockIdx.x * (int64_t)kBitsThreads + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (g >= nchunk_total) return;
@@ -766,7 +771,7 @@ k_bits_emit(uint32_t* __restrict__ bits, int64_t nw, int b, int64_t nchunk_total
   const int64_t b0 = obase ? *obase : 0;
   const int64_t total = b0 + chunk_off[nchunk_total - 1] + counts[nchunk_total - 1];
   const bool fits = total <= capacity;  // ids only when all of them fit (as the sorted-key path)
-  int64_t base = b0 + chunk_off[g];
+  const int64_t base = b0 + chunk_off[g];
   if (lane == 0) {
     if (c == 0) offsets[q] = base;
     if (g == nchunk_total - 1) {
@@ -775,29 +780,27 @@ k_bits_emit(uint32_t* __restrict__ bits, int64_t nw, int b, int64_t nchunk_total
     }
   }
   if (counts[g] == 0) return;  // (warp-uniform) nothing set in this chunk
-  uint32_t* row = bits + q * nw;
-  const int64_t w0 = c * kChunkWords + lane;
-  uint32_t wv[32];
+  const int64_t blk = c * 32 + lane;
+  const bool mine = blk < nbr && dirty[q * nbr + blk];
+  uint32_t* wp = bits + q * nw + blk * 32;
+  const int nwb = mine ? (int)min((int64_t)32, nw - blk * 32) : 0;
+  int cnt = 0;
+  for (int i = 0; i < nwb; ++i) cnt += __popc(wp[i]);
+  int incl = cnt;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) wv[i] = w0 + 32 * i < nw ? row[w0 + 32 * i] : 0u;
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    uint32_t w = wv[i];
-    const uint32_t any = __ballot_sync(0xffffffffu, w != 0u);
-    if (!any) continue;
-    const int cnt = __popc(w);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int x = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += x;
-    }
-    if (w) {
-      const int64_t wi = w0 + 32 * i;
-      row[wi] = 0u;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  if (mine) {
+    int64_t pos = base + incl - cnt;
+    const int32_t u_blk = (int32_t)(blk * 1024);
+    for (int i = 0; i < nwb; ++i) {
+      uint32_t w = wp[i];
+      if (!w) continue;
+      wp[i] = 0u;
       if (fits) {
-        int64_t pos = base + incl - cnt;
-        const int32_t u0 = (int32_t)(wi * 32);
+        const int32_t u0 = u_blk + 32 * i;
         while (w) {
           const int bit = __ffs(w) - 1;
           w &= w - 1;
@@ -805,7 +808,7 @@ k_bits_emit(uint32_t* __restrict__ bits, int64_t nw, int b, int64_t nchunk_total
         }
       }
     }
-    base += __shfl_sync(0xffffffffu, incl, 31);
+    dirty[q * nbr + blk] = 0;
   }
 }
 
@@ -822,13 +825,13 @@ cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, 
   int64_t* counts = reinterpret_cast<int64_t*>(c.acc_sorted);  // the sort's space is unused on this path
   int64_t* chunk_off = counts + nch;
   const unsigned grid = (unsigned)((nch * 32 + kBitsThreads - 1) / kBitsThreads);
-  k_bits_count<<<grid, kBitsThreads, 0, st>>>(c.bits, c.nw, nch, counts); count_launch();
+  k_bits_count<<<grid, kBitsThreads, 0, st>>>(c.bits, c.dirty, c.nw, c.nbr, nch, counts); count_launch();
   size_t tb = c.cub_bytes;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(c.cub_tmp, tb, counts, chunk_off, (int)nch, st);
   count_launch(2);
   if (e != cudaSuccess) return e;
-  k_bits_emit<<<grid, kBitsThreads, 0, st>>>(c.bits, c.nw, c.b, nch, counts, chunk_off, capacity, offsets, user_ids,
-                                              obase, obase_next);
+  k_bits_emit<<<grid, kBitsThreads, 0, st>>>(c.bits, c.dirty, c.nw, c.nbr, c.b, nch, counts, chunk_off, capacity,
+                                              offsets, user_ids, obase, obase_next);
   count_launch();
   return cudaGetLastError();
 }

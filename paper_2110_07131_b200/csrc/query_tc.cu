@@ -645,7 +645,7 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
   k_query_tc<KB><<<grid, kThreads, smem, st>>>(tu, tut, tq, tqt, x->dpad / 64, tail, x->thr + (int64_t)(c.k - 1) * x->n,
                                                x->tb + (int64_t)(c.k - 1) * x->nlb, x->perm_u, x->n,
                                                (int)x->nblocks, c.qn, c.qerr, c.qscale, c.qperm, c.qcount, c.nsub,
-                                               kflags, (x->d + 15) / 16, c.wlen, c.counters, AccSink{c.acc, c.bits, c.nw}, c.und, c.cap);
+                                               kflags, (x->d + 15) / 16, c.wlen, c.counters, AccSink{c.acc, c.bits, c.nw, c.dirty, c.nbr}, c.und, c.cap);
   count_launch();
   if (c.ev_k[1]) cudaEventRecord(c.ev_k[1], st);
   return cudaGetLastError();
