@@ -671,19 +671,8 @@ rmips_status_t rmips_query_ex(rmips_index_t idx, const float* q_batch, int32_t b
 }
 
 // rmips_query_batches: per batch, the counters the host checks after a single call are folded on the
-// device (sums; the largest pair-workspace need; the OR of the error flags), so the batches run back
-// to back with one synchronisation at the end.
-__global__ void k_batch_fold(const unsigned long long* __restrict__ ctr, const int* __restrict__ flags,
-                             unsigned long long* __restrict__ acc) {
-  const int i = threadIdx.x;
-  if (i < kNumCounters) acc[i] += ctr[i];
-  if (i == 0) {
-    const unsigned long long need = ctr[C_ACCEPTED_TOTAL] > ctr[C_UND_TOTAL] ? ctr[C_ACCEPTED_TOTAL] : ctr[C_UND_TOTAL];
-    if (need > acc[kNumCounters]) acc[kNumCounters] = need;
-    acc[kNumCounters + 1] |= (unsigned long long)(unsigned)flags[0];
-  }
-}
-
+// device by k_bits_emit (sums; the largest pair-workspace need; the OR of the error flags), so the
+// batches run back to back with one synchronisation at the end.
 __global__ void k_shift_offsets(int64_t* __restrict__ off, int64_t cnt, int64_t base) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < cnt) off[i] += base;
@@ -810,10 +799,7 @@ rmips_status_t rmips_query_batches(rmips_index_t idx, const float* q_all, int64_
         CK(e);
         if (E) CK(cudaEventRecord(E[6 * t + 2], st));
         CK(query_exact(c, st));
-        CK(query_output_bits(c, offsets + b0, user_ids, capacity, st, run + (t & 1), run + ((t + 1) & 1)));
-        k_batch_fold<<<1, 64, 0, st>>>(x->d_counters, x->d_flags, acc);
-        count_launch();
-        CK(cudaGetLastError());
+        CK(query_output_bits(c, offsets + b0, user_ids, capacity, st, run + (t & 1), run + ((t + 1) & 1), acc));
         if (E) CK(cudaEventRecord(E[6 * t + 3], st));
       }
       CK(cudaMemcpyAsync(hc, acc, (size_t)(kNumCounters + 2) * 8, cudaMemcpyDeviceToHost, st));

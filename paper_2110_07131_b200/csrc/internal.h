@@ -125,7 +125,9 @@ cudaError_t zero4(cudaStream_t st, void* a, int na, void* b, int nb, void* c, in
 cudaError_t query_sort(QueryCtx& c, int64_t total, int end_bit, cudaStream_t st);
 // obase / obase_next (device words, both NULL for a single call): ids already written by earlier batches
 // of rmips_query_batches; this batch's running total is stored to obase_next
+// fold (batched calls): the batch's counters are folded into it (see k_bits_emit)
 cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st,
-                              const int64_t* obase = nullptr, int64_t* obase_next = nullptr);
+                              const int64_t* obase = nullptr, int64_t* obase_next = nullptr,
+                              unsigned long long* fold = nullptr);
 
 }  // namespace rmips

@@ -760,10 +760,22 @@ __global__ void __launch_bounds__(kBitsThreads)
 k_bits_emit(uint32_t* __restrict__ bits, uint8_t* __restrict__ dirty, int64_t nw, int64_t nbr, int b,
             int64_t nchunk_total, const int64_t* __restrict__ counts, const int64_t* __restrict__ chunk_off,
             int64_t capacity, int64_t* __restrict__ offsets, int32_t* __restrict__ out,
-            const int64_t* __restrict__ obase, int64_t* __restrict__ obase_next) {
+            const int64_t* __restrict__ obase, int64_t* __restrict__ obase_next,
+            const unsigned long long* __restrict__ ctr, const int* __restrict__ flags_dev,
+            unsigned long long* __restrict__ fold) {
   const int64_t g = (blockIdx.x * (int64_t)kBitsThreads + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (g >= nchunk_total) return;
+  if (fold && g == nchunk_total - 1) {
+    // batched calls: this batch's counters folded into the call's (sums; the largest pair-workspace
+    // need; the OR of the error flags), read by the host once after the last batch
+    for (int i = lane; i < kNumCounters; i += 32) fold[i] += ctr[i];
+    if (lane == 0) {
+      const unsigned long long need = ctr[C_ACCEPTED_TOTAL] > ctr[C_UND_TOTAL] ? ctr[C_ACCEPTED_TOTAL] : ctr[C_UND_TOTAL];
+      if (need > fold[kNumCounters]) fold[kNumCounters] = need;
+      fold[kNumCounters + 1] |= (unsigned long long)(unsigned)flags_dev[0];
+    }
+  }
   const int64_t per_row = (nw + kChunkWords - 1) / kChunkWords;
   const int64_t q = g / per_row, c = g - q * per_row;
   // obase (batched calls, rmips_query_batches): the ids of the earlier batches already in `out`; this
@@ -812,6 +824,44 @@ k_bits_emit(uint32_t* __restrict__ bits, uint8_t* __restrict__ dirty, int64_t nw
   }
 }
 
+// Exclusive scan of up to kScanSmallMax chunk counts in one CTA (one launch instead of the device-wide
+// scan's two): thread t owns a contiguous run of the values.
+constexpr int kScanSmallThreads = 1024;
+constexpr int64_t kScanSmallMax = (int64_t)kScanSmallThreads * 32;
+__global__ void __launch_bounds__(kScanSmallThreads)
+k_scan_small(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t cnt) {
+  __shared__ int64_t wsum[kScanSmallThreads / 32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t per = (cnt + kScanSmallThreads - 1) / kScanSmallThreads;
+  const int64_t a = (int64_t)t * per, e = a + per < cnt ? a + per : cnt;
+  int64_t sum = 0;
+  for (int64_t i = a; i < e; ++i) sum += in[i];
+  int64_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int64_t v = wsum[lane], vi = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t x = __shfl_up_sync(0xffffffffu, vi, o);
+      if (lane >= o) vi += x;
+    }
+    wsum[lane] = vi - v;  // exclusive prefix of the warps
+  }
+  __syncthreads();
+  int64_t run = wsum[w] + incl - sum;
+  for (int64_t i = a; i < e; ++i) {
+    const int64_t v = in[i];
+    out[i] = run;
+    run += v;
+  }
+}
+
 size_t query_scan_bytes(int64_t items) {
   size_t a = 0;
   cub::DeviceScan::ExclusiveSum((void*)nullptr, a, (const int64_t*)nullptr, (int64_t*)nullptr, (int)items);
@@ -820,18 +870,23 @@ size_t query_scan_bytes(int64_t items) {
 int64_t query_bits_chunks(int b, int64_t nw) { return (int64_t)b * ((nw + kChunkWords - 1) / kChunkWords); }
 
 cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st,
-                              const int64_t* obase, int64_t* obase_next) {
+                              const int64_t* obase, int64_t* obase_next, unsigned long long* fold) {
   const int64_t nch = query_bits_chunks(c.b, c.nw);
   int64_t* counts = reinterpret_cast<int64_t*>(c.acc_sorted);  // the sort's space is unused on this path
   int64_t* chunk_off = counts + nch;
   const unsigned grid = (unsigned)((nch * 32 + kBitsThreads - 1) / kBitsThreads);
   k_bits_count<<<grid, kBitsThreads, 0, st>>>(c.bits, c.dirty, c.nw, c.nbr, nch, counts); count_launch();
-  size_t tb = c.cub_bytes;
-  cudaError_t e = cub::DeviceScan::ExclusiveSum(c.cub_tmp, tb, counts, chunk_off, (int)nch, st);
-  count_launch(2);
-  if (e != cudaSuccess) return e;
+  if (nch <= kScanSmallMax) {
+    k_scan_small<<<1, kScanSmallThreads, 0, st>>>(counts, chunk_off, nch);
+    count_launch();
+  } else {
+    size_t tb = c.cub_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(c.cub_tmp, tb, counts, chunk_off, (int)nch, st);
+    count_launch(2);
+    if (e != cudaSuccess) return e;
+  }
   k_bits_emit<<<grid, kBitsThreads, 0, st>>>(c.bits, c.dirty, c.nw, c.nbr, c.b, nch, counts, chunk_off, capacity,
-                                              offsets, user_ids, obase, obase_next);
+                                              offsets, user_ids, obase, obase_next, c.counters, c.flags_dev, fold);
   count_launch();
   return cudaGetLastError();
 }
