@@ -225,7 +225,8 @@ k_query_simt(const __half* __restrict__ U16, int ldh, const float* __restrict__ 
 // form their exact fp64 products; every lane then adds the products in index order, taking each one by
 // a broadcast shuffle, so the sum is dot64's left-to-right fp64 sum bit for bit (each product of two fp32
 // values is exact in fp64, so fma(a, b, s) and s + a*b round identically).
-constexpr int C_SCAN_LIST = kNumCounters;  // (spare counter slot) pairs in the dense list
+constexpr int C_SCAN_LIST = kNumCounters;      // (spare counter slot) pairs in the dense list
+constexpr int C_SCAN_NEXT = kNumCounters + 1;  // (spare, zeroed per call) next pair for k_verify_scan_warp
 __global__ void __launch_bounds__(256)
 k_exact_decide(const float* __restrict__ q, const float* __restrict__ U32, const double* __restrict__ tauk,
                const int32_t* __restrict__ perm_u, int d, unsigned long long* __restrict__ ctr,
@@ -373,7 +374,13 @@ k_verify_scan_warp(const float* __restrict__ q, const float* __restrict__ U32, c
   const double g64 = (d + 2) * 1.1102230246251565e-16 / (1.0 - (d + 2) * 1.1102230246251565e-16);
   const double efac = (g32 + g64) * slack * slack * (1.0 + 1e-6);
   const int nq4 = pd / 4;
-  for (int64_t i = blockIdx.x * (int64_t)kScanWarps + w; i < npairs; i += (int64_t)gridDim.x * kScanWarps) {
+  // pairs are taken one at a time from a counter: scan lengths differ by orders of magnitude (each pair
+  // stops at its own depth), and a static stride left each launch waiting on its longest warps
+  for (;;) {
+    unsigned long long gi = 0;
+    if (lane == 0) gi = atomicAdd(ctr + C_SCAN_NEXT, 1ull);
+    const int64_t i = (int64_t)__shfl_sync(0xffffffffu, gi, 0);
+    if (i >= npairs) break;
     const uint64_t rec = scan_rec[i];
     const uint32_t qin = (uint32_t)(rec >> 32);
     const int64_t row = (int64_t)(rec & 0xffffffffu);
