@@ -839,10 +839,15 @@ __global__ void __launch_bounds__(kScanSmallThreads)
 k_scan_small(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t cnt) {
   __shared__ int64_t wsum[kScanSmallThreads / 32];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int64_t per = (cnt + kScanSmallThreads - 1) / kScanSmallThreads;
+  const int64_t per = (cnt + kScanSmallThreads - 1) / kScanSmallThreads;  // <= 32
   const int64_t a = (int64_t)t * per, e = a + per < cnt ? a + per : cnt;
+  int64_t v[32];  // this thread's values, read once (unrolled: registers)
   int64_t sum = 0;
-  for (int64_t i = a; i < e; ++i) sum += in[i];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    v[i] = a + i < e ? in[a + i] : 0;
+    sum += v[i];
+  }
   int64_t incl = sum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -862,10 +867,10 @@ k_scan_small(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t 
   }
   __syncthreads();
   int64_t run = wsum[w] + incl - sum;
-  for (int64_t i = a; i < e; ++i) {
-    const int64_t v = in[i];
-    out[i] = run;
-    run += v;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if (a + i < e) out[a + i] = run;
+    run += v[i];
   }
 }
 

@@ -26,3 +26,6 @@ timeout 300 python tools/prof_step.py --config 1 --steps 2 > gpurun_out/p1.log 2
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_build_tc|k_exact_select|k_query_tc" -s 3 -c 3 -o gpurun_out/r02_cfg1 -f \
   python tools/prof_step.py --config 1 --steps 2 > gpurun_out/p_ncu1.log 2>&1
 echo "cfg1 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_norms|k_prep_users|k_prep_items" -c 3 -o gpurun_out/r02_cfg4_prep -f \
+  python tools/prof_step.py --config 4 --steps 1 > gpurun_out/p_ncu4p.log 2>&1
+echo "cfg4 prep rc=$?"

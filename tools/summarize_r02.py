@@ -92,7 +92,9 @@ def main():
             ("r02_cfg3", "# r02 -- ncu --set full, configs[3] (full size)", "`tools/prof_step.py --config 3 --steps 1`, -s 1 -c 3."),
             ("r02_cfg3_scan", "# r02 -- ncu --set full, configs[3] P' index (|P'| = 2 k_max): Alg. 2's verification scan",
              "`tools/prof_step.py --config 3 --steps 1 --pprime 2` (P32 = 100,000 x 56 x 4 B = 22 MB: L2-resident, so the scan's fraction is of L2, not HBM)."),
-            ("r02_cfg1", "# r02 -- ncu --set full, configs[1] (full size)", "`tools/prof_step.py --config 1 --steps 2`, -s 3 -c 3.")]
+            ("r02_cfg1", "# r02 -- ncu --set full, configs[1] (full size)", "`tools/prof_step.py --config 1 --steps 2`, -s 3 -c 3."),
+            ("r02_cfg4_prep", "# r02 -- ncu --set full, configs[4] build prep (norms, permute + convert)",
+             "`tools/prof_step.py --config 4 --steps 1`, -k regex:'k_norms|k_prep_users|k_prep_items' -c 3.")]
     for rep, title, how in caps:
         p = os.path.join(G, rep + ".ncu-rep")
         if not os.path.exists(p):
