@@ -838,3 +838,25 @@ def test_unaligned_input_views_build_identical_index():
         assert np.array_equal(np.asarray(x), np.asarray(y))
     a.close()
     b.close()
+
+
+def test_query_batches_other_paths_equal_single_calls():
+    """rmips_query_batches on the other query paths (Alg. 2's scan for every undecided pair, no Lemma 3
+    blocks, a P' index) = rmips_query per batch, and the oracle on the P' index."""
+    U, P = gen.random_instance(41, 1200, 500, 24)
+    Qy = P[np.arange(300) % len(P)]
+    idx = rmips.rmips_build_index(_t(U), _t(P), 8)
+    pidx = rmips.rmips_build_index_pprime(_t(U), _t(P), 8, 16)
+    cases = [(idx, rmips.RMIPS_FLAG_VERIFY_SCAN), (idx, rmips.RMIPS_FLAG_NO_BLOCKS), (pidx, 0),
+             (pidx, rmips.RMIPS_FLAG_KEY_SORT)]
+    for ix, fl in cases:
+        o1, i1 = rmips.rmips_query_batches(ix, _t(Qy), 128, 6, fl)
+        parts = [rmips.rmips_query(ix, _t(Qy[b0:b0 + 128]), 6, fl) for b0 in range(0, len(Qy), 128)]
+        want = [s for o, i in parts for s in rmips.split_sets(o, i)]
+        got = rmips.split_sets(o1, i1)
+        assert len(got) == len(Qy) and all(np.array_equal(a, b) for a, b in zip(got, want)), fl
+    member = oracle.rkmips_naive(U, P, Qy, 6)
+    assert_same(rmips.split_sets(*rmips.rmips_query_batches(pidx, _t(Qy), 100, 6)), member, U, P, Qy, 6,
+                "P' batches")
+    idx.close()
+    pidx.close()
