@@ -131,7 +131,7 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
            const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
            int64_t n, int64_t m, int kmax, int seed_tiles, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
            int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count, unsigned long long* __restrict__ tiles_done,
-           int dev) {
+           int dev, int stale_every) {
   using namespace sm100;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base, derived from smem_raw by pointer arithmetic so that the compiler
@@ -281,6 +281,7 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
       const int64_t row = (int64_t)ut * kBM + rloc;
       CandRow me = cand_init(row < n);  // dead rows (user >= n) have theta = +inf and never pass
+      int lastc = 0;  // the row's entry count at its last checkpoint refresh
       // C-S check every kCsEvery tiles, on the scaled norm of the first item of the next tile
       // (prefetched one check ahead).  A warp that is not done never meets an end marker: the
       // producer ends a user tile only after all four warps (this one included) reported.
@@ -409,6 +410,16 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
             done = true;
             break;
           }
+          // stale-theta checkpoint refresh, as build_tc2cta.cu: rows that appended since their last refresh
+          if (stale_every > 0 && (it + 1) % stale_every == 0 && __fmul_ru(pnn, 1.0000153f) < 1.5f * key2f(mk) &&
+              __any_sync(0xffffffffu, me.cnt != lastc)) {  // (only near the exit: within 1.5x of the stale one)
+            me = cand_refresh(me, sm, rloc, e0x2, kmax);
+            lastc = me.cnt;
+            if (__fmul_ru(pnn, 1.0000153f) < key2f(__reduce_min_sync(0xffffffffu, f2key(me.theta)))) {
+              done = true;
+              break;
+            }
+          }
           Eg = EgN;
           if (base0 + (kCsEvery + 1) * kBN < mi) {
             pnr = __ldg(pnorm + base0 + (kCsEvery + 1) * kBN);
@@ -522,11 +533,17 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
         (getenv("RMIPS_FAST_ONLY") ? kDevFastOnly : 0);
   if (const char* e = getenv("RMIPS_SLOW_LIMIT")) dev |= (atoi(e) & 0xffff) << 8;
 #endif
+  // stale-theta checkpoint refresh (as build_tc2cta.cu): off here -- at d <= 64 an item tile is too short
+  // for the refresh to pay (configs[1..3]: +1 to +5 % contraction time even where it cut the tiles 14 %)
+  int stale_every = 0;
+#ifdef RMIPS_DEV
+  if (const char* e = getenv("RMIPS_STALE_EVERY")) stale_every = atoi(e);  // 0: off
+#endif
   if (16 * seed < x->kmax) seed = 0;
   x->build_kernel = 1;
   x->cand_slots = kCand;
   k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, x->n, c.mb, x->kmax, seed, c.cand,
-                                               c.ccount, c.ovf_list, c.ovf_count, c.tiles_done, dev);
+                                               c.ccount, c.ovf_list, c.ovf_count, c.tiles_done, dev, stale_every);
   count_launch();
   return cudaGetLastError();
 }

@@ -68,7 +68,7 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
                int64_t n, int64_t m, int kmax, int ksteps, int tail, int32_t* __restrict__ cand,
                int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count,
-               unsigned long long* __restrict__ tiles_done) {
+               unsigned long long* __restrict__ tiles_done, int stale_every) {
   using namespace sm100;
   using C = Cfg2<KB, Pol>;
   constexpr int NSB = C::NSB, NDEC = C::NDEC, NACC = C::NACC, BN = C::BN, TS = C::TS;
@@ -285,6 +285,7 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int ut = 2 * tp + (int)rank;
       const int64_t row = (int64_t)ut * kBM + rr;
       typename Pol::Row me = Pol::init(row < n, smax);
+      int lastc = 0;  // the row's entry count at its last checkpoint refresh (below)
       float Eg = __ldg(perr), EgN = (kCsEvery * BN < mi) ? __ldg(perr + kCsEvery * BN) : 0.f;
       double pnr = nit > kCsEvery ? __ldg(pnorm + kCsEvery * BN) : 0.0;
       mbar_wait(BAR(ACC_FULL + as), aph);
@@ -315,11 +316,27 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         as = as_next;
         aph = aph_next;
         if ((it + 1) % kCsEvery == 0 && more) {
-          const uint32_t mk = __reduce_min_sync(0xffffffffu, f2key(me.theta));
+          uint32_t mk = __reduce_min_sync(0xffffffffu, f2key(me.theta));
           const float pnn = __double2float_ru(pnr * (double)pscl);
           if (__fmul_ru(pnn, 1.0000153f) < key2f(mk)) {
             done = true;
             break;
+          }
+          // Late in the scan appends are rare, so a row's buffer seldom reaches the refresh mark and its
+          // theta (last set at a refresh) lags the k_max-th largest lower bound it already holds, which
+          // delays this exit: every stale_every tiles the warp refreshes rows that appended since their
+          // last refresh (theta stays a valid lower bound: the same refresh) and tests the exit again.
+          // (An always-current theta exits where the final thresholds do: 2,330 of 7,813 item tiles per
+          // user tile of configs[4] against 2,577 with the refresh mark alone.)
+          if (stale_every > 0 && (it + 1) % stale_every == 0 && __fmul_ru(pnn, 1.0000153f) < 1.5f * key2f(mk) &&
+              __any_sync(0xffffffffu, me.cnt != lastc)) {  // (only near the exit: within 1.5x of the stale one)
+            Pol::refresh_theta(me, sb, rr, e0x2, kmax);
+            lastc = me.cnt;
+            mk = __reduce_min_sync(0xffffffffu, f2key(me.theta));
+            if (__fmul_ru(pnn, 1.0000153f) < key2f(mk)) {
+              done = true;
+              break;
+            }
           }
           Eg = EgN;
           if (base0 + (kCsEvery + 1) * BN < mi) {
@@ -376,9 +393,13 @@ static cudaError_t launch_tc2cta(const BuildCtx& c, cudaStream_t st) {
   const int grid = 2 * (pairs_needed < pairs_max ? pairs_needed : pairs_max);
   x->build_kernel = 4;
   x->cand_slots = Pol::kSlots;
+  int stale_every = 16;  // checkpoint refresh period in item tiles (a multiple of the C-S check period 4)
+#ifdef RMIPS_DEV
+  if (const char* e = getenv("RMIPS_STALE_EVERY")) stale_every = atoi(e);  // 0: off
+#endif
   k_build_tc2cta<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tat, tb, tbt, x->perr, x->pnorm, c.scale_dev, x->n,
                                                               c.mb, x->kmax, (x->d + 15) / 16, tail, c.cand, c.ccount,
-                                                              c.ovf_list, c.ovf_count, c.tiles_done);
+                                                              c.ovf_list, c.ovf_count, c.tiles_done, stale_every);
   count_launch();
   return cudaGetLastError();
 }

@@ -72,7 +72,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
             int64_t n, int64_t m, int kmax, int ksteps, int kb_rt, int tail, int dev, int32_t* __restrict__ cand,
             int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count,
-            unsigned long long* __restrict__ tiles_done) {
+            unsigned long long* __restrict__ tiles_done, int stale_every) {
   using namespace sm100;
   using C = Cfg<KB, Pol>;
   constexpr int NST = C::NST, NACC = C::NACC, BN = C::BN;
@@ -271,6 +271,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
       const int64_t row = (int64_t)ut * kBM + q * 32 + lane;
       typename Pol::Row me = Pol::init(row < n, smax);  // dead rows (user >= n): theta = +inf, never pass
+      int lastc = 0;  // the row's entry count at its last checkpoint refresh
       // error bound of every chunk of a group of kCsEvery item tiles: perr of the group's first item
       // (perr is non-increasing along the norm-sorted items, so it bounds every later item's);
       // the next group's is prefetched a whole group ahead
@@ -336,6 +337,16 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           if (__fmul_ru(pnn, 1.0000153f) < key2f(mk)) {
             done = true;
             break;
+          }
+          // stale-theta checkpoint refresh, as build_tc2cta.cu: rows that appended since their last refresh
+          if (stale_every > 0 && (it + 1) % stale_every == 0 && __fmul_ru(pnn, 1.0000153f) < 1.5f * key2f(mk) &&
+              __any_sync(0xffffffffu, me.cnt != lastc)) {  // (only near the exit: within 1.5x of the stale one)
+            Pol::refresh_theta(me, sb, rr, e0x2, kmax);
+            lastc = me.cnt;
+            if (__fmul_ru(pnn, 1.0000153f) < key2f(__reduce_min_sync(0xffffffffu, f2key(me.theta)))) {
+              done = true;
+              break;
+            }
           }
           Eg = EgN;
           if (base0 + (kCsEvery + 1) * BN < mi) {
@@ -405,9 +416,13 @@ static cudaError_t launch_tcq(const BuildCtx& c, cudaStream_t st) {
 #endif
   x->build_kernel = KB == 0 ? 3 : 2;
   x->cand_slots = Pol::kSlots;
+  int stale_every = 16;  // stale-theta checkpoint refresh period (item tiles), as build_tc2cta.cu
+#ifdef RMIPS_DEV
+  if (const char* e = getenv("RMIPS_STALE_EVERY")) stale_every = atoi(e);  // 0: off
+#endif
   k_build_tcq<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tat, tb, tbt, x->perr, x->pnorm, c.scale_dev, x->n,
                                                           c.mb, x->kmax, ksteps, x->dpad / 64, tail, dev, c.cand,
-                                                          c.ccount, c.ovf_list, c.ovf_count, c.tiles_done);
+                                                          c.ccount, c.ovf_list, c.ovf_count, c.tiles_done, stale_every);
   count_launch();
   return cudaGetLastError();
 }

@@ -82,8 +82,11 @@ __device__ __forceinline__ QRow qrow_init(bool live, float smax) {
 
 // Refresh of this thread's row (all 32 lanes of the warp call it together).  Not inlined: one
 // copy per kernel keeps the hot loops in the instruction cache.
+// theta_only (the build kernels' stale-theta checkpoints): the search starts at the current theta and
+// only theta moves (no compaction, no re-quantisation: the entries stay valid under the old quantiser).
 template <int SLOTS>
-static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float e0x2, int kmax) {
+static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float e0x2, int kmax,
+                                                 bool theta_only = false) {
   if (me.ovf) return me;
   sb.assume_shared();
   uint32_t* b = sb.buf + rr;
@@ -96,6 +99,9 @@ static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float
     // resulting deq(qL) is a valid theta whatever the history of re-quantisation
     int qL = 0;
     int qU = (int)q_of(me.vmax, me) + 1;  // exclusive upper end
+    // (theta_only: deq(q_of(theta)) <= theta, and #{q >= q_of(theta)} >= #{lo >= theta} >= k_max holds
+    // since the last full refresh verified it; the search below keeps its own counts anyway)
+    if (theta_only && th > me.base) qL = min((int)q_of(th, me), qU - 1);
 #pragma unroll 1
     for (int pass = 0; pass < 6 && qU - qL > 1; ++pass) {
       const int span = qU - qL;
@@ -123,6 +129,10 @@ static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float
       else qU = m1;
     }
     nth = fmaxf(th, deq((uint32_t)qL, me));
+  }
+  if (theta_only) {
+    me.theta = nth;
+    return me;
   }
   // re-quantise the survivors on [base', vmax], base' = theta - 2 E0 - 2 w: an entry's true lower
   // bound lo is < deq(q) + w, so x = deq(q) < base' implies lo + 2 E < theta (droppable), and every
