@@ -213,7 +213,7 @@ void extend_lists(rmips_index_s* x, int kmax_new, cudaStream_t st) {
   BuildCtx c;
   c.idx = x;
   c.mb = x->mprime;
-  c.cstride = build_cand_stride(kmax_new, c.mb, x->build_flags);
+  c.cstride = build_cand_stride(kmax_new, c.mb, x->build_flags, x->d);
   const int fb_grid = fallback_grid(m);
   Arena sa;
   const size_t o_sc = sa.take<float>(4), o_cand = sa.take<int32_t>(n * c.cstride), o_cc = sa.take<int32_t>(n),
@@ -366,7 +366,7 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
     const int fb_grid = fallback_grid(m);
     const size_t o_key = sa.take<uint64_t>(2 * (m + n)), o_val = sa.take<int32_t>(2 * (m + n)), o_inv = sa.take<int32_t>(n),
                  o_max = sa.take<unsigned int>(4), o_cub = sa.take<unsigned char>((int64_t)c.cub_bytes),
-                 o_cand = sa.take<int32_t>(n * build_cand_stride(k_max, x->mprime, build_flags)),
+                 o_cand = sa.take<int32_t>(n * build_cand_stride(k_max, x->mprime, build_flags, d)),
                  o_cc = sa.take<int32_t>(n), o_ovl = sa.take<int32_t>(n),
                  o_ovc = sa.take<int>(1), o_ct = sa.take<unsigned long long>(2),
                  o_scr = sa.take<double>((int64_t)fb_grid * m);
@@ -380,7 +380,7 @@ rmips_status_t rmips_build_index_pprime(const float* Q, int64_t n, const float* 
     c.scale_dev = reinterpret_cast<float*>(c.maxabs + 2);
     c.cub_tmp = S + o_cub;
     c.cand = reinterpret_cast<int32_t*>(S + o_cand);
-    c.cstride = build_cand_stride(k_max, x->mprime, build_flags);
+    c.cstride = build_cand_stride(k_max, x->mprime, build_flags, d);
     c.ccount = reinterpret_cast<int32_t*>(S + o_cc);
     c.ovf_list = reinterpret_cast<int32_t*>(S + o_ovl);
     c.ovf_count = reinterpret_cast<int*>(S + o_ovc);

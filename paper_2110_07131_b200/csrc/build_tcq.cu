@@ -438,8 +438,12 @@ static cudaError_t launch_tcq_kb(const BuildCtx& c, cudaStream_t st) {
   }
 }
 
-int build_cand_stride(int kmax, int64_t mb, int build_flags) {
-  return (!(build_flags & RMIPS_BUILD_SIMT) && kmax > kQ128MaxKmax && mb <= QPolT<256>::kMaxItems) ? 256 : kCand;
+// 256 slots also for d > 256: there the scores crowd near the k_max-th largest, and more than 96 entries
+// often fall inside the error band a refresh must keep, which sent rows to the exact fallback
+// (d = 513, configs[4] recipe: 1,115 of 148,000 rows with 128 slots, 8.8 s of fallback).
+int build_cand_stride(int kmax, int64_t mb, int build_flags, int d) {
+  return (!(build_flags & RMIPS_BUILD_SIMT) && (kmax > kQ128MaxKmax || d > 256) && mb <= QPolT<256>::kMaxItems)
+             ? 256 : kCand;
 }
 
 // Any d_pad: the candidate policy by (m, k_max): 4-byte entries when positions fit 20 bits (256 slots

@@ -63,7 +63,7 @@ cudaError_t build_tc2cta(const BuildCtx& c, cudaStream_t st);  // build_tc2cta.c
 // Candidate slots per row the build will use (BuildCtx::cstride): 256 when k_max > kQ128MaxKmax and the
 // positions fit the 4-byte entries (m <= 2^20), else 128.
 constexpr int kQ128MaxKmax = 80;
-int build_cand_stride(int kmax, int64_t mb, int build_flags);
+int build_cand_stride(int kmax, int64_t mb, int build_flags, int d);
 cudaError_t build_select(BuildCtx& c, cudaStream_t st);
 cudaError_t build_fallback(BuildCtx& c, int nrows, double* scratch, int grid, cudaStream_t st);
 cudaError_t build_blocks(BuildCtx& c, cudaStream_t st);

@@ -860,3 +860,19 @@ def test_query_batches_other_paths_equal_single_calls():
                 "P' batches")
     idx.close()
     pidx.close()
+
+
+def test_large_d_lists_do_not_overflow():
+    """d > 256 (configs[4] recipe): the 256-slot lists hold every row (with 128 slots, d = 300 / 513 sent
+    hundreds of rows per 100k to the O(m d) exact fallback); the tables still equal the oracle's."""
+    from synth.generator import make_workload
+    for d in (300, 513):
+        w = make_workload(4, n=6000, m=120000, d=d, nq=4)
+        idx = rmips.rmips_build_index(_t(w.U), _t(w.P), 50)
+        idx.refresh_info()
+        assert idx.overflow_rows == 0 and idx.cand_slots == 256, (d, idx.overflow_rows, idx.cand_slots)
+        pu, pp, tau, ids = idx.export()
+        users = np.arange(0, 6000, 997)
+        vals, oids = oracle.topk(w.U[users], w.P, 50)
+        assert np.array_equal(tau[:, users].T, vals) and np.array_equal(ids[:, users].T, oids), d
+        idx.close()
