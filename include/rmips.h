@@ -104,7 +104,7 @@ typedef struct {
  *           K loops stream the user and query K blocks from L2 instead of keeping them on chip;
  *           RMIPS_BUILD_SIMT covers d <= 256 only)
  *   k_max   largest k the index answers, >= 1 (lists are padded with -inf when k_max > m).  The
- *           build's candidate filter keeps 128 slots per user row for k_max <= 80 and d <= 256, and 256
+ *           build's candidate filter keeps 128 slots per user row for k_max <= 80 and d <= 240, and 256
  *           slots for larger k_max or d (when m <= 2^20); a row whose list cannot be compacted into its slots (k_max above ~90 with
  *           m > 2^20 or with RMIPS_BUILD_SIMT, k_max above ~220 otherwise, or massive ties) is
  *           recomputed exactly by a fallback kernel that costs O(k_max m d) per row: correct, slow

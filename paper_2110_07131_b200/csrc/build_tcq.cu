@@ -438,11 +438,12 @@ static cudaError_t launch_tcq_kb(const BuildCtx& c, cudaStream_t st) {
   }
 }
 
-// 256 slots also for d > 256: there the scores crowd near the k_max-th largest, and more than 96 entries
+// 256 slots also for d > 240: there the scores crowd near the k_max-th largest, and more than 96 entries
 // often fall inside the error band a refresh must keep, which sent rows to the exact fallback
-// (d = 513, configs[4] recipe: 1,115 of 148,000 rows with 128 slots, 8.8 s of fallback).
+// (configs[4] recipe, 148,000 users x 1 M items, 128 slots: d = 256 10 rows (+210 ms), d = 513 1,115
+// rows (8.8 s); d = 240: none).  These shapes take build_tcq (the CTA-pair kernel has no room for them).
 int build_cand_stride(int kmax, int64_t mb, int build_flags, int d) {
-  return (!(build_flags & RMIPS_BUILD_SIMT) && (kmax > kQ128MaxKmax || d > 256) && mb <= QPolT<256>::kMaxItems)
+  return (!(build_flags & RMIPS_BUILD_SIMT) && (kmax > kQ128MaxKmax || d > 240) && mb <= QPolT<256>::kMaxItems)
              ? 256 : kCand;
 }
 
