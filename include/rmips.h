@@ -104,11 +104,13 @@ typedef struct {
  *           K loops stream the user and query K blocks from L2 instead of keeping them on chip;
  *           RMIPS_BUILD_SIMT covers d <= 256 only)
  *   k_max   largest k the index answers, >= 1 (lists are padded with -inf when k_max > m).  The
- *           build's candidate filter keeps 128 slots per user row for k_max <= 80 and d <= 240, and 256
- *           slots for larger k_max or d (when m <= 2^20); a row whose list cannot be compacted into its slots (k_max above ~90 with
- *           m > 2^20 or with RMIPS_BUILD_SIMT, k_max above ~220 otherwise, or massive ties) is
- *           recomputed exactly by a fallback kernel that costs O(k_max m d) per row: correct, slow
- *           (overflow rows are reported by rmips_index_info)
+ *           build's candidate filter keeps 128 slots per user row for k_max <= 80 and d <= 240 (m <=
+ *           2^20), and 256 slots for larger k_max or d, and for 2^20 < m <= 2^21 (4-byte entries with 21-bit
+ *           positions); beyond m = 2^21, and with RMIPS_BUILD_SIMT, 128 slots of 8-byte entries.  A row
+ *           whose list cannot be compacted into its slots (k_max above ~220 with 256 slots; k_max above
+ *           ~60 or crowded scores at large d with 128 8-byte slots; massive ties) is recomputed exactly
+ *           by a fallback kernel that costs O(k_max m d) per row: correct, slow (overflow rows are
+ *           reported by rmips_index_info)
  *   out     receives the new index handle (NULL on failure)
  * The library copies what it needs; Q and P may be freed after the call returns.
  * Errors: INVALID, NONFINITE, K_RANGE (k_max < 1), OOM, CUDA. */

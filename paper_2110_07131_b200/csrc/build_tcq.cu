@@ -442,15 +442,19 @@ static cudaError_t launch_tcq_kb(const BuildCtx& c, cudaStream_t st) {
 // often fall inside the error band a refresh must keep, which sent rows to the exact fallback
 // (configs[4] recipe, 148,000 users x 1 M items, 128 slots: d = 256 10 rows (+210 ms), d = 513 1,115
 // rows (8.8 s); d = 240: none).  These shapes take build_tcq (the CTA-pair kernel has no room for them).
+// m in (2^20, 2^21]: 256 slots of 21-bit positions (QPolT<256, 21>) whatever k_max and d -- the 8-byte
+// entries (128 slots) overflowed rows there (m = 1.3 M: k_max = 80 at d = 256, or d >= 513).
 int build_cand_stride(int kmax, int64_t mb, int build_flags, int d) {
-  return (!(build_flags & RMIPS_BUILD_SIMT) && (kmax > kQ128MaxKmax || d > 240) && mb <= QPolT<256>::kMaxItems)
-             ? 256 : kCand;
+  if (build_flags & RMIPS_BUILD_SIMT) return kCand;
+  if (mb <= QPolT<256>::kMaxItems) return (kmax > kQ128MaxKmax || d > 240) ? 256 : kCand;
+  return mb <= QPolT<256, 21>::kMaxItems ? 256 : kCand;
 }
 
-// Any d_pad: the candidate policy by (m, k_max): 4-byte entries when positions fit 20 bits (256 slots
-// above k_max = 80), else 8-byte entries (128 slots: k_max above ~90 then overflows rows to the exact
-// fallback, R11).
+// Any d_pad: the candidate policy by (m, k_max, d): 4-byte entries while positions fit 20 bits (256
+// slots above k_max = 80 or d = 240) or 21 bits (256 slots, an 11-bit bound), else 8-byte entries (128
+// slots: crowded rows then overflow to the exact fallback, R11).
 cudaError_t build_tcq(const BuildCtx& c, cudaStream_t st) {
+  if (c.cstride == 256 && c.mb > QPolT<256>::kMaxItems) return launch_tcq_kb<QPolT<256, 21>>(c, st);
   if (c.cstride == 256) return launch_tcq_kb<QPolT<256>>(c, st);
   if (c.mb <= QPolT<128>::kMaxItems) return launch_tcq_kb<QPolT<128>>(c, st);
   return launch_tcq_kb<FPol>(c, st);

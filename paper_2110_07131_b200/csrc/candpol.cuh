@@ -1,6 +1,6 @@
 // candpol.cuh -- the candidate-entry policies of the tensor-core build kernel build_tcq.cu behind one
 // small interface:
-//   QPolT<SLOTS>  candq.cuh: 4-byte entries, 12-bit quantised lower bound | 20-bit position
+//   QPolT<SLOTS, PB>  candq.cuh: 4-byte entries, quantised lower bound | PB-bit position (PB = 20 or 21)
 //                 (m <= 2^20); SLOTS = 128 (k_max <= 80) or 256 (larger k_max)
 //   FPol          cand.cuh: 8-byte entries {lo, position} (any m < 2^31), 128 slots
 // Every policy keeps cand.cuh's invariant: theta is a valid lower bound of the row's
@@ -13,28 +13,28 @@
 
 namespace rmips {
 
-template <int SLOTS>
+template <int SLOTS, int PB = 20>  // PB position bits (20: m <= 2^20; 21: m <= 2^21, an 11-bit bound)
 struct QPolT {
   using Row = QRow;
   using Buf = QBuf;
   static constexpr int kSlots = SLOTS;
   static constexpr int kBufBytes = 128 * SLOTS * 4;  // 128 rows
-  static constexpr int64_t kMaxItems = (int64_t)kQPosMask + 1;
+  static constexpr int64_t kMaxItems = (int64_t)QFmt<PB>::kPosMask + 1;
   __device__ static Buf buf(uint8_t* p) { return QBuf{reinterpret_cast<uint32_t*>(p), 128}; }
-  __device__ static Row init(bool live, float smax) { return qrow_init(live, smax); }
+  __device__ static Row init(bool live, float smax) { return qrow_init<PB>(live, smax); }
   template <typename F>
   __device__ static void append(F f, const float (&g4)[8], float E, int pos0, int mi, Row& me, Buf sb, int rr) {
-    qrow_append_chunk(f, g4, E, pos0, mi, me, sb, rr);
+    qrow_append_chunk<PB>(f, g4, E, pos0, mi, me, sb, rr);
   }
   __device__ static void maybe_refresh(Row& me, Buf sb, int rr, float e0x2, int kmax) {
-    qrow_maybe_refresh<SLOTS>(me, sb, rr, e0x2, kmax);
+    qrow_maybe_refresh<SLOTS, PB>(me, sb, rr, e0x2, kmax);
   }
   __device__ static void refresh_theta(Row& me, Buf sb, int rr, float e0x2, int kmax) {  // (whole warp)
-    me = qrow_refresh<SLOTS>(me, sb, rr, e0x2, kmax, true);
+    me = qrow_refresh<SLOTS, PB>(me, sb, rr, e0x2, kmax, true);
   }
   __device__ static void finish(Row& me, Buf sb, int rr, float e0x2, int kmax, int64_t m, int64_t row, int64_t n,
                                 int32_t* cand, int32_t* ccount, int32_t* ovf_list, int* ovf_count) {
-    qrow_finish<SLOTS>(me, sb, rr, e0x2, kmax, m, row, n, cand, SLOTS, ccount, ovf_list, ovf_count);
+    qrow_finish<SLOTS, PB>(me, sb, rr, e0x2, kmax, m, row, n, cand, SLOTS, ccount, ovf_list, ovf_count);
   }
 };
 

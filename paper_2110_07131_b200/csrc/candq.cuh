@@ -28,9 +28,17 @@
 
 namespace rmips {
 
-constexpr int kQPosBits = 20;
-constexpr uint32_t kQPosMask = (1u << kQPosBits) - 1u;
-constexpr int kQMax = 4095;                        // 12-bit quantised bound
+// Entry format: (q << PB) | position, PB position bits (20: m <= 2^20 with a 12-bit bound; 21: m <= 2^21
+// with an 11-bit bound).
+template <int PB>
+struct QFmt {
+  static constexpr int kPosBits = PB;
+  static constexpr uint32_t kPosMask = (1u << PB) - 1u;
+  static constexpr int kQMax = (1 << (32 - PB)) - 1;  // largest quantised bound
+};
+constexpr int kQPosBits = 20;  // (the default format)
+constexpr uint32_t kQPosMask = QFmt<20>::kPosMask;
+constexpr int kQMax = QFmt<20>::kQMax;
 
 struct QRow {
   float theta;  // valid lower bound of the k_max-th largest true score (scaled units)
@@ -59,19 +67,21 @@ struct QBuf {
 // Quantised lower bound of x (base <= x <= smax): floor((x - base) / w) <= 4095.  The quantum
 // covers [base, smax], never only [base, vmax]: a saturated q would no longer bound lo from above
 // (lo < deq(q) + w), and the drop test relies on that.
+template <int PB = 20>
 __device__ __forceinline__ uint32_t q_of(float x, const QRow& me) {
   const float dd = __fsub_rd(x, me.base) * me.inv;  // exact power-of-two scaling of a rounded-down gap
-  return dd >= (float)kQMax ? (uint32_t)kQMax : (uint32_t)dd;
+  return dd >= (float)QFmt<PB>::kQMax ? (uint32_t)QFmt<PB>::kQMax : (uint32_t)dd;
 }
 __device__ __forceinline__ float deq(uint32_t q, const QRow& me) { return __fadd_rd(me.base, (float)q * me.w); }
 
 // smax bounds |s~| for every item (scores are in [-smax, smax]).
+template <int PB = 20>
 __device__ __forceinline__ QRow qrow_init(bool live, float smax) {
   const float inf = __int_as_float(0x7f800000);
   QRow r;
   r.theta = live ? -inf : inf;
   r.base = -smax;
-  r.w = pow2_ceil(fmaxf(2.f * smax, 1e-30f) / (float)kQMax);
+  r.w = pow2_ceil(fmaxf(2.f * smax, 1e-30f) / (float)QFmt<PB>::kQMax);
   r.inv = 1.f / r.w;
   r.smax = smax;
   r.vmax = -inf;
@@ -84,9 +94,12 @@ __device__ __forceinline__ QRow qrow_init(bool live, float smax) {
 // copy per kernel keeps the hot loops in the instruction cache.
 // theta_only (the build kernels' stale-theta checkpoints): the search starts at the current theta and
 // only theta moves (no compaction, no re-quantisation: the entries stay valid under the old quantiser).
-template <int SLOTS>
+template <int SLOTS, int PB = 20>
 static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float e0x2, int kmax,
                                                  bool theta_only = false) {
+  constexpr int kQPosBits = PB;  // (this function's entry format)
+  constexpr uint32_t kQPosMask = QFmt<PB>::kPosMask;
+  constexpr int kQMax = QFmt<PB>::kQMax;
   if (me.ovf) return me;
   sb.assume_shared();
   uint32_t* b = sb.buf + rr;
@@ -98,10 +111,10 @@ static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float
     // #{q >= 0} = cn >= kmax; the search keeps #{q >= qL} >= kmax (verified counts only), so the
     // resulting deq(qL) is a valid theta whatever the history of re-quantisation
     int qL = 0;
-    int qU = (int)q_of(me.vmax, me) + 1;  // exclusive upper end
-    // (theta_only: deq(q_of(theta)) <= theta, and #{q >= q_of(theta)} >= #{lo >= theta} >= k_max holds
+    int qU = (int)q_of<PB>(me.vmax, me) + 1;  // exclusive upper end
+    // (theta_only: deq(q_of<PB>(theta)) <= theta, and #{q >= q_of<PB>(theta)} >= #{lo >= theta} >= k_max holds
     // since the last full refresh verified it; the search below keeps its own counts anyway)
-    if (theta_only && th > me.base) qL = min((int)q_of(th, me), qU - 1);
+    if (theta_only && th > me.base) qL = min((int)q_of<PB>(th, me), qU - 1);
 #pragma unroll 1
     for (int pass = 0; pass < 6 && qU - qL > 1; ++pass) {
       const int span = qU - qL;
@@ -156,7 +169,7 @@ static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float
       const float x = deq(v[u] >> kQPosBits, me);
       ge += x >= nth;
       if (!rebase || x >= nw.base) {  // x < base' = theta - 2 E0: upper bound below theta
-        b[wpos * R] = rebase ? ((q_of(x, nw) << kQPosBits) | (v[u] & kQPosMask)) : v[u];
+        b[wpos * R] = rebase ? ((q_of<PB>(x, nw) << kQPosBits) | (v[u] & kQPosMask)) : v[u];
         ++wpos;
       }
     }
@@ -166,7 +179,7 @@ static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float
     const float x = deq(v0 >> kQPosBits, me);
     ge += x >= nth;
     if (!rebase || x >= nw.base) {
-      b[wpos * R] = rebase ? ((q_of(x, nw) << kQPosBits) | (v0 & kQPosMask)) : v0;
+      b[wpos * R] = rebase ? ((q_of<PB>(x, nw) << kQPosBits) | (v0 & kQPosMask)) : v0;
       ++wpos;
     }
   }
@@ -181,9 +194,10 @@ static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float
 // Append pass of one 32-column chunk (scores via s_of(j), positions pos0 + j; columns >= mi are
 // padding), called by the whole warp; g4[8] are the 4-column group maxima.  Groups are skipped
 // warp-uniformly; inside a group the 4 slots come from a prefix of predicates.
-template <typename ScoreFn>
+template <int PB = 20, typename ScoreFn>
 __device__ __forceinline__ void qrow_append_chunk(ScoreFn s_of, const float (&g4)[8], float E, int pos0, int mi,
                                                   QRow& me, QBuf sb, int rr) {
+  constexpr int kQPosBits = PB;  // (this function's entry format)
   sb.assume_shared();
   uint32_t* b = sb.buf + rr;
   const int R = sb.R;
@@ -204,10 +218,10 @@ __device__ __forceinline__ void qrow_append_chunk(ScoreFn s_of, const float (&g4
         p[j] = sj >= thr && pos0 + 4 * g + j < mi && lo[j] >= me.base;
       }
       const int o1 = c + p[0], o2 = o1 + p[1], o3 = o2 + p[2];
-      if (p[0]) b[c * R] = (q_of(lo[0], me) << kQPosBits) | (uint32_t)(pos0 + 4 * g);
-      if (p[1]) b[o1 * R] = (q_of(lo[1], me) << kQPosBits) | (uint32_t)(pos0 + 4 * g + 1);
-      if (p[2]) b[o2 * R] = (q_of(lo[2], me) << kQPosBits) | (uint32_t)(pos0 + 4 * g + 2);
-      if (p[3]) b[o3 * R] = (q_of(lo[3], me) << kQPosBits) | (uint32_t)(pos0 + 4 * g + 3);
+      if (p[0]) b[c * R] = (q_of<PB>(lo[0], me) << kQPosBits) | (uint32_t)(pos0 + 4 * g);
+      if (p[1]) b[o1 * R] = (q_of<PB>(lo[1], me) << kQPosBits) | (uint32_t)(pos0 + 4 * g + 1);
+      if (p[2]) b[o2 * R] = (q_of<PB>(lo[2], me) << kQPosBits) | (uint32_t)(pos0 + 4 * g + 2);
+      if (p[3]) b[o3 * R] = (q_of<PB>(lo[3], me) << kQPosBits) | (uint32_t)(pos0 + 4 * g + 3);
       c = o3 + p[3];
       if (p[0] | p[1] | p[2] | p[3]) vmax = fmaxf(vmax, __fsub_rd(g4[g], E));
     }
@@ -216,9 +230,9 @@ __device__ __forceinline__ void qrow_append_chunk(ScoreFn s_of, const float (&g4
   me.vmax = vmax;
 }
 
-template <int SLOTS>
+template <int SLOTS, int PB = 20>
 __device__ __forceinline__ void qrow_maybe_refresh(QRow& me, QBuf sb, int rr, float e0x2, int kmax) {
-  if (__any_sync(0xffffffffu, me.cnt > SLOTS - 32)) me = qrow_refresh<SLOTS>(me, sb, rr, e0x2, kmax);
+  if (__any_sync(0xffffffffu, me.cnt > SLOTS - 32)) me = qrow_refresh<SLOTS, PB>(me, sb, rr, e0x2, kmax);
 }
 
 // Final compaction, then the candidate positions (or the overflow mark) are written out.  A live row
@@ -226,12 +240,12 @@ __device__ __forceinline__ void qrow_maybe_refresh(QRow& me, QBuf sb, int rr, fl
 // refresh keeps every entry with lo >= theta, of which there are >= k_max); fewer means scores that
 // never compare (NaN: a user whose norm exceeds FLT_MAX, build.cu) and the row takes the exact
 // fallback.
-template <int SLOTS>
+template <int SLOTS, int PB = 20>
 __device__ __forceinline__ void qrow_finish(QRow& me, QBuf sb, int rr, float e0x2, int kmax, int64_t m, int64_t row,
                                             int64_t n, int32_t* __restrict__ cand, int cstride,
                                             int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list,
                                             int* __restrict__ ovf_count) {
-  me = qrow_refresh<SLOTS>(me, sb, rr, e0x2, kmax);
+  me = qrow_refresh<SLOTS, PB>(me, sb, rr, e0x2, kmax);
   if (row < n) {
     if (me.ovf || (int64_t)me.cnt < (m < kmax ? m : (int64_t)kmax)) {
       ccount[row] = -1;
@@ -240,7 +254,7 @@ __device__ __forceinline__ void qrow_finish(QRow& me, QBuf sb, int rr, float e0x
     } else {
       ccount[row] = me.cnt;
       const uint32_t* b = sb.buf + rr;
-      for (int i = 0; i < me.cnt; ++i) cand[row * cstride + i] = (int32_t)(b[i * sb.R] & kQPosMask);
+      for (int i = 0; i < me.cnt; ++i) cand[row * cstride + i] = (int32_t)(b[i * sb.R] & QFmt<PB>::kPosMask);
     }
   }
 }

@@ -703,14 +703,15 @@ def test_kmax_128_lists_without_fallback(d):
     idx.close()
 
 
-def test_m_above_2pow20_tensor_core_build():
-    """m = 1.1 M items with d = 100: item positions no longer fit the 4-byte entries'
-    20 bits, so the tensor-core build keeps 8-byte entries (FPol); it must still be the tcgen05 kernel
-    (not the SIMT build) and give the oracle's exact lists on a user sample."""
-    w = gen.make_workload(4, n=1500, m=1_100_000, nq=30, d=100)
+@pytest.mark.parametrize("m,slots", [(1_100_000, 256), (2_100_000, 128)])
+def test_m_above_2pow20_tensor_core_build(m, slots):
+    """m above 2^20: positions no longer fit 20 bits -- up to 2^21 the build keeps 4-byte
+    entries with 21-bit positions (256 slots), beyond that 8-byte entries (128 slots); either way the
+    tcgen05 kernel (not the SIMT build) with the oracle's exact lists on a user sample."""
+    w = gen.make_workload(4, n=1500, m=m, nq=30, d=100)
     idx = rmips.rmips_build_index(_t(w.U), _t(w.P), 20)
-    assert idx.build_kernel == 2 and idx.build_flags & rmips.RMIPS_BUILD_SIMT == 0  # (8-byte entries: 1 CTA)
-    assert idx.cand_slots == 128 and idx.overflow_rows == 0
+    assert idx.build_kernel == 2 and idx.build_flags & rmips.RMIPS_BUILD_SIMT == 0  # (1-CTA kernel)
+    assert idx.cand_slots == slots and idx.overflow_rows == 0
     sample = np.sort(np.random.default_rng(3).choice(w.U.shape[0], 160, replace=False))
     vals, oids = oracle.topk(w.U[sample], w.P, 20)
     _, _, tau, ids = idx.export()
