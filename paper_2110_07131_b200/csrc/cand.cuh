@@ -55,7 +55,10 @@ __device__ __forceinline__ CandRow cand_init(bool live) {
 // Per-thread refresh of this thread's row (called by all 32 lanes together).  Not inlined (one
 // copy per kernel keeps the hot loops inside the instruction cache); the row state travels in
 // registers.  e0x2 >= 2 * (every chunk error bound E used at append time), rounded up.
-static __device__ __noinline__ CandRow cand_refresh(CandRow me, CandSmem sm, int rloc, float e0x2, int kmax) {
+// theta_only (the build kernels' stale-theta checkpoints): the search starts at the current theta and only
+// theta moves (no compaction).
+static __device__ __noinline__ CandRow cand_refresh(CandRow me, CandSmem sm, int rloc, float e0x2, int kmax,
+                                                    bool theta_only = false) {
   if (me.ovf) return me;
   const int cn = me.cnt;
   sm.assume_shared();
@@ -65,7 +68,9 @@ static __device__ __noinline__ CandRow cand_refresh(CandRow me, CandSmem sm, int
   if (cn >= kmax) {
     float L = th;
     const float U = me.vmax;
-    if (!(L > -3.402823466e38f)) {  // first refresh: bracket from the smallest entry
+    if (theta_only && L > -3.402823466e38f && L < U) {
+      // (#{lo >= theta} >= k_max since the last full refresh: theta is a valid lower end)
+    } else if (!(L > -3.402823466e38f)) {  // first refresh: bracket from the smallest entry
       float m0 = U, m1 = U, m2 = U, m3 = U;
       int i = 0;
       for (; i + 4 <= cn; i += 4) {
@@ -106,6 +111,10 @@ static __device__ __noinline__ CandRow cand_refresh(CandRow me, CandSmem sm, int
     }
     nth = L;
     nth = fmaxf(nth, th);
+  }
+  if (theta_only) {
+    me.theta = nth;
+    return me;
   }
   const float keep = __fsub_rd(nth, e0x2);  // lo < keep  =>  lo + 2E < theta: cannot be top-k_max
   int wpos = 0, ge = 0, i = 0;

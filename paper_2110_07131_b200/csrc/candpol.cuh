@@ -54,7 +54,7 @@ struct FPol {
     cand_maybe_refresh(me, sb, rr, e0x2, kmax);
   }
   __device__ static void refresh_theta(Row& me, Buf sb, int rr, float e0x2, int kmax) {  // (whole warp)
-    me = cand_refresh(me, sb, rr, e0x2, kmax);
+    me = cand_refresh(me, sb, rr, e0x2, kmax, true);
   }
   __device__ static void finish(Row& me, Buf sb, int rr, float e0x2, int kmax, int64_t m, int64_t row, int64_t n,
                                 int32_t* cand, int32_t* ccount, int32_t* ovf_list, int* ovf_count) {
