@@ -86,7 +86,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t sR = sbase + C::RING;
-  const typename Pol::Buf sb = Pol::buf(smem + C::CAND);
+  const typename Pol::Buf sb = Pol::buf(smem + C::CAND, perr);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR);
   const uint32_t bar0 = smem_u32(bars);
   auto BAR = [&](int i) { return bar0 + 8u * i; };
@@ -266,6 +266,7 @@ k_build_tcq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     uint32_t aph = 0;
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
     constexpr int kCsEvery = 4;   // Cauchy-Schwarz check period (item tiles)
+    static_assert(kCsEvery * C::BN == (int)kPerrGroup, "candq.cuh drops on perr[j & ~(kPerrGroup - 1)]");
     uint32_t hA[64], hB[64];
     int t = 0;
     for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {

@@ -20,7 +20,8 @@ struct QPolT {
   static constexpr int kSlots = SLOTS;
   static constexpr int kBufBytes = 128 * SLOTS * 4;  // 128 rows
   static constexpr int64_t kMaxItems = (int64_t)QFmt<PB>::kPosMask + 1;
-  __device__ static Buf buf(uint8_t* p) { return QBuf{reinterpret_cast<uint32_t*>(p), 128}; }
+  // perr: the per-item error table (the final drop tests each entry's own bound, candq.cuh)
+  __device__ static Buf buf(uint8_t* p, const float* perr) { return QBuf{reinterpret_cast<uint32_t*>(p), 128, perr}; }
   __device__ static Row init(bool live, float smax) { return qrow_init<PB>(live, smax); }
   template <typename F>
   __device__ static void append(F f, const float (&g4)[8], float E, int pos0, int mi, Row& me, Buf sb, int rr) {
@@ -44,7 +45,7 @@ struct FPol {
   static constexpr int kSlots = kCand;
   static constexpr int kBufBytes = kCandSmemBytes;
   static constexpr int64_t kMaxItems = (int64_t)1 << 31;
-  __device__ static Buf buf(uint8_t* p) { return CandSmem::at(p); }
+  __device__ static Buf buf(uint8_t* p, const float*) { return CandSmem::at(p); }
   __device__ static Row init(bool live, float) { return cand_init(live); }
   template <typename F>
   __device__ static void append(F f, const float (&g4)[8], float E, int pos0, int, Row& me, Buf sb, int rr) {

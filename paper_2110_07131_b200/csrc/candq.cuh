@@ -9,18 +9,20 @@
 //   a slot-major shared-memory buffer of packed entries (q << 20) | position, where q is a
 //           12-bit QUANTISED LOWER BOUND of the item's score:
 //              deq(q) = base + q * w  (rounded down, w a power of two)  <=  lo = s~ - E  <=  s,
-//           and lo < deq(q) + w.  Quantising rounds down, so every dequantised value is still a
-//           lower bound.
+//           and lo < deq(q) + qe, qe = w (1 + 2^-10).  The row's quantiser (base = -smax, w) is
+//           fixed for its whole scan, so every entry is quantised exactly once and the bound qe
+//           holds for all of them (re-quantising on a rebased grid would add up to one quantum per
+//           rebase to that bound; measured, it also kept more candidates).
 // An item is appended iff s~ >= theta - E; an entry is dropped only when its upper bound
-// (< deq(q) + w + 2 E0, E0 = the largest E) is below theta.  Every true top-k_max item has
-// s >= tau_kmax >= theta, so it is never rejected or dropped.
+// (< deq(q) + qe + 2 E, rounded up; E0 = the largest E during the scan, the entry's own group bound
+// at the end) is below theta.  Every true top-k_max item has s >= tau_kmax >= theta, so it is never
+// rejected or dropped.
 // Refresh (when a row of the warp may not have room for another 32-column chunk): a quaternary
-// search over q (4 passes, integer compares on the packed words) for the largest qt with
-// #{q >= qt} >= k_max; theta <- max(theta, deq(qt)); then one compaction pass that drops
-// entries below base' = theta - 2 E0 - 2 w and re-quantises the survivors on [base', vmax]
-// (base' and w' change, the value each entry stands for only goes down).
-// Positions must be < 2^20 (m <= 1,048,576; larger item sets use the 8-byte entries of cand.cuh, FPol in
-// candpol.cuh).  SLOTS (128 or 256) entries per row: 256 for k_max above ~80 (a refresh must leave
+// search over q (integer compares on the packed words) for the largest qt with #{q >= qt} >= k_max;
+// theta <- max(theta, deq(qt)); then one compaction pass that drops entries below
+// theta - 2 E0 - qe.
+// Positions must be < 2^PB (PB = 20: m <= 1,048,576 with 12-bit bounds; PB = 21: m <= 2^21 with
+// 11-bit bounds; larger item sets use the 8-byte entries of cand.cuh, FPol in candpol.cuh).  SLOTS (128 or 256) entries per row: 256 for k_max above ~80 (a refresh must leave
 // room for another 32-column chunk above the k_max kept entries).
 #pragma once
 #include "common.cuh"
@@ -58,9 +60,11 @@ __device__ __forceinline__ float pow2_ceil(float x) {  // smallest power of two 
 }
 
 // Buffer of R rows: entry i of row r at buf[i * R + r].
+// perr (optional): the per-item error table, entry j appended with E = perr[j & ~(kPerrGroup - 1)].
 struct QBuf {
   uint32_t* buf;
   int R;
+  const float* perr;
   __device__ __forceinline__ void assume_shared() const { __builtin_assume(__isShared(buf)); }
 };
 
@@ -73,6 +77,17 @@ __device__ __forceinline__ uint32_t q_of(float x, const QRow& me) {
   return dd >= (float)QFmt<PB>::kQMax ? (uint32_t)QFmt<PB>::kQMax : (uint32_t)dd;
 }
 __device__ __forceinline__ float deq(uint32_t q, const QRow& me) { return __fadd_rd(me.base, (float)q * me.w); }
+// lo - deq(q) < qe = w (1 + 2^-10): the quantum plus the rounding of deq.  Entries are quantised once
+// (the quantiser of a row never changes), so this bounds every entry of the buffer.
+__device__ __forceinline__ float qrow_qe(const QRow& me) { return __fmul_ru(me.w, 1.0009765625f); }
+
+// The build kernels bound the scores of a group of kPerrGroup = 4 item tiles of 128 by the error
+// bound of the group's first item (perr is non-increasing along the norm-sorted items).
+constexpr uint32_t kPerrGroup = 512;
+// Upper bound of the true score of an entry with dequantised value x at item position j.
+__device__ __forceinline__ float entry_ub(float x, float qe, const float* __restrict__ perr, uint32_t j) {
+  return __fadd_ru(__fadd_ru(x, qe), __fmul_ru(2.f, __ldg(perr + (j & ~(kPerrGroup - 1u)))));
+}
 
 // smax bounds |s~| for every item (scores are in [-smax, smax]).
 template <int PB = 20>
@@ -96,7 +111,7 @@ __device__ __forceinline__ QRow qrow_init(bool live, float smax) {
 // only theta moves (no compaction, no re-quantisation: the entries stay valid under the old quantiser).
 template <int SLOTS, int PB = 20>
 static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float e0x2, int kmax,
-                                                 bool theta_only = false) {
+                                                 bool theta_only = false, bool final_pass = false) {
   constexpr int kQPosBits = PB;  // (this function's entry format)
   constexpr uint32_t kQPosMask = QFmt<PB>::kPosMask;
   constexpr int kQMax = QFmt<PB>::kQMax;
@@ -147,18 +162,16 @@ static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float
     me.theta = nth;
     return me;
   }
-  // re-quantise the survivors on [base', vmax], base' = theta - 2 E0 - 2 w: an entry's true lower
-  // bound lo is < deq(q) + w, so x = deq(q) < base' implies lo + 2 E < theta (droppable), and every
-  // kept entry is representable (x >= base') with its new value <= x <= lo
+  // compaction: an entry's true score s < deq(q) + qe + 2 E (E the bound its score was appended
+  // with, see the file header), so an entry whose bound, rounded up, is below theta is dropped.  The
+  // scan's refreshes test E = E0 (the largest bound, no table loads); the final one, and a refresh
+  // that would otherwise leave no room (exact fallback), test each entry's own group bound
+  // perr[j & ~(kPerrGroup - 1)] (sb.perr, when the kernel supplies it).  The quantiser never changes,
+  // so every entry was quantised once.
   QRow nw = me;
   nw.theta = nth;
-  if (nth > -3.402823466e38f) {
-    nw.base = __fsub_rd(__fsub_rd(nth, e0x2), __fmul_ru(2.f, me.w));
-    const float span = __fsub_ru(me.smax, nw.base);
-    nw.w = pow2_ceil(fmaxf(span, fabsf(nw.base) * 1e-6f + 1e-30f) / (float)kQMax);
-    nw.inv = 1.f / nw.w;
-  }
-  const bool rebase = nth > -3.402823466e38f;
+  const float qe = qrow_qe(me);
+  const float keep0 = __fsub_rd(__fsub_rd(nth, e0x2), qe);  // x >= keep0 stays
   int wpos = 0, ge = 0, i = 0;
   for (; i + 8 <= cn; i += 8) {
     uint32_t v[8];
@@ -168,19 +181,22 @@ static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float
     for (int u = 0; u < 8; ++u) {
       const float x = deq(v[u] >> kQPosBits, me);
       ge += x >= nth;
-      if (!rebase || x >= nw.base) {  // x < base' = theta - 2 E0: upper bound below theta
-        b[wpos * R] = rebase ? ((q_of<PB>(x, nw) << kQPosBits) | (v[u] & kQPosMask)) : v[u];
-        ++wpos;
-      }
+      if (x >= keep0) b[wpos++ * R] = v[u];
     }
   }
   for (; i < cn; ++i) {
     const uint32_t v0 = b[i * R];
     const float x = deq(v0 >> kQPosBits, me);
     ge += x >= nth;
-    if (!rebase || x >= nw.base) {
-      b[wpos * R] = rebase ? ((q_of<PB>(x, nw) << kQPosBits) | (v0 & kQPosMask)) : v0;
-      ++wpos;
+    if (x >= keep0) b[wpos++ * R] = v0;
+  }
+  const float* __restrict__ perr = sb.perr;
+  if (perr && (final_pass || wpos > SLOTS - 32) && nth > -3.402823466e38f) {
+    const int c0 = wpos;
+    wpos = 0;
+    for (i = 0; i < c0; ++i) {
+      const uint32_t v0 = b[i * R];
+      if (!(entry_ub(deq(v0 >> kQPosBits, me), qe, perr, v0 & kQPosMask) < nth)) b[wpos++ * R] = v0;
     }
   }
   nw.cnt = wpos;
@@ -245,7 +261,7 @@ __device__ __forceinline__ void qrow_finish(QRow& me, QBuf sb, int rr, float e0x
                                             int64_t n, int32_t* __restrict__ cand, int cstride,
                                             int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list,
                                             int* __restrict__ ovf_count) {
-  me = qrow_refresh<SLOTS, PB>(me, sb, rr, e0x2, kmax);
+  me = qrow_refresh<SLOTS, PB>(me, sb, rr, e0x2, kmax, false, true);
   if (row < n) {
     if (me.ovf || (int64_t)me.cnt < (m < kmax ? m : (int64_t)kmax)) {
       ccount[row] = -1;
