@@ -440,8 +440,13 @@ constexpr int kSelStride = kSelRows + 1;  // odd stage stride: a warp's 32 ranks
 // tables (tau, ids, thr: rank-major, users contiguous) then take full sectors instead of one
 // 4- or 8-byte piece of a sector per (row, rank).
 // MAXC = candidate slots per row (the build's cstride: 128, or 256 for k_max > 80).
+// Occupancy: the kernel is bound by L1 wavefronts and L2 latency of the row gathers, so resident warps
+// matter more than a few spilled registers: 4 CTAs per SM (64 registers, 104 bytes of spill) for
+// 128 slots, 3 for 256.  Measured against the unconstrained 114 registers (2 CTAs per SM): configs[3]
+// 4.82 -> 2.97 ms, configs[4] 11.0 -> 9.1 ms, configs[1] 0.378 -> 0.292 ms (same box; a
+// preloaded-rows variant, every 256-bit load of a row issued before its chain, was 15 % slower).
 template <int MAXC>
-__global__ void __launch_bounds__(32 * kSelWarps)
+__global__ void __launch_bounds__(32 * kSelWarps, MAXC == 128 ? 4 : 3)
 k_exact_select(const float* __restrict__ U32, const float* __restrict__ P32, const int32_t* __restrict__ perm_p,
                const float* __restrict__ unu, const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount,
                int64_t n, int d, int pd, int kmax, double* __restrict__ tau, int32_t* __restrict__ ids,
