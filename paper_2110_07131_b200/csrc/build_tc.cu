@@ -131,7 +131,8 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
            const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
            int64_t n, int64_t m, int kmax, int seed_tiles, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
            int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count, unsigned long long* __restrict__ tiles_done,
-           int dev, int stale_every) {
+           int dev, int stale_every, int nit_cap, float* __restrict__ theta_out,
+           const float* __restrict__ theta_in, const int32_t* __restrict__ row_map) {
   using namespace sm100;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base, derived from smem_raw by pointer arithmetic so that the compiler
@@ -158,7 +159,8 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_utiles = (int)((n + kBM - 1) / kBM);
-  const int nit = (int)((m + kBN - 1) / kBN);
+  // head pass (nit_cap > 0): only the first nit_cap item tiles (build_tc2cta.cu, regrouping)
+  const int nit = nit_cap > 0 && (int64_t)nit_cap * kBN < m ? nit_cap : (int)((m + kBN - 1) / kBN);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -344,6 +346,9 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         me.cnt = 0;
         me.vmax = -__int_as_float(0x7f800000);
       }
+      // regrouped pass: the head pass's theta of this row is a valid lower bound of its k_max-th largest
+      // true score
+      if (theta_in && row < n) me.theta = fmaxf(me.theta, __ldg(theta_in + row));
       int it = 0;
       bool done = false;                        // warp-uniform: this warp's rows cannot gain any more
       if (dev & (kDevEpiSkip | kDevEpiLoad)) {  // dev: release every accumulator stage (MMA + feed alone)
@@ -440,7 +445,13 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
           tc_fence_after();
         }
       }
-      cand_finish(me, sm, rloc, e0x2, kmax, m, row, n, cand, kCand, ccount, ovf_list, ovf_count);
+      if (theta_out) {  // head pass: the row's theta only (verified counts, no lists)
+        me = cand_refresh(me, sm, rloc, e0x2, kmax, true);
+        if (row < n) theta_out[row] = me.ovf ? -__int_as_float(0x7f800000) : me.theta;
+      } else {  // lists go to the row's place in the index order (row_map: regrouped pass)
+        const int64_t orow = row_map && row < n ? (int64_t)__ldg(row_map + row) : row;
+        cand_finish(me, sm, rloc, e0x2, kmax, m, orow, n, cand, kCand, ccount, ovf_list, ovf_count);
+      }
       __syncwarp();
     }
   }
@@ -542,10 +553,43 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   if (16 * seed < x->kmax) seed = 0;
   x->build_kernel = 1;
   x->cand_slots = kCand;
-  k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, x->n, c.mb, x->kmax, seed, c.cand,
-                                               c.ccount, c.ovf_list, c.ovf_count, c.tiles_done, dev, stale_every);
+  // regrouping (as build_tc2cta.cu, but the main pass restarts at item tile 0 from the head thetas, no seed
+  // pass): off -- configs[1..3] measured 6.30 -> 7.00, 3.02 -> 3.59, 0.86 -> 1.07 ms with 8 head tiles
+  // (configs[3]: 26 % fewer item tiles, but the head's dense phase is paid twice)
+  int head = 0;
+#ifdef RMIPS_DEV
+  if (const char* e = getenv("RMIPS_HEAD_TILES")) head = atoi(e) & ~3;  // 0: no regrouping
+#endif
+  const int64_t n = x->n;
+  if (head <= 0 || nit < 16 * head || tiles < 4 * sm_count() || head * kBN < x->kmax) {
+    k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, n, c.mb, x->kmax, seed, c.cand,
+                                                 c.ccount, c.ovf_list, c.ovf_count, c.tiles_done, dev, stale_every, 0,
+                                                 nullptr, nullptr, nullptr);
+    count_launch();
+    return cudaGetLastError();
+  }
+  Regroup g;
+  e = regroup_alloc(g, n, x->ldh, 0, st);
+  if (e != cudaSuccess) return e;
+  CUtensorMap ga;
+  if (!make_tmap_f16_box(&ga, g.U16b, (uint64_t)n, (uint64_t)x->ldh, kBM)) {
+    regroup_free(g, st);
+    return cudaErrorNotSupported;
+  }
+  k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, n, c.mb, x->kmax, seed, c.cand, c.ccount,
+                                               c.ovf_list, c.ovf_count, c.tiles_done, dev, stale_every, head, g.th,
+                                               nullptr, nullptr);
   count_launch();
-  return cudaGetLastError();
+  e = regroup_rows(g, x->U16, n, x->ldh, st);
+  if (e == cudaSuccess) {
+    k_build_tc<KB><<<grid, kThreads, smem, st>>>(ga, tb, x->perr, x->pnorm, cs, n, c.mb, x->kmax, 0, c.cand, c.ccount,
+                                                 c.ovf_list, c.ovf_count, c.tiles_done, dev, stale_every, 0, nullptr,
+                                                 g.ths, g.pm);
+    count_launch();
+    e = cudaGetLastError();
+  }
+  regroup_free(g, st);
+  return e;
 }
 
 cudaError_t build_tc(const BuildCtx& c, cudaStream_t st) {

@@ -23,6 +23,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cub/cub.cuh>
+
 #include "candpol.cuh"
 #include "common.cuh"
 #include "epiq.cuh"
@@ -68,7 +70,9 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
                int64_t n, int64_t m, int kmax, int ksteps, int tail, int32_t* __restrict__ cand,
                int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count,
-               unsigned long long* __restrict__ tiles_done, int stale_every) {
+               unsigned long long* __restrict__ tiles_done, int stale_every, int it0, int nit_cap,
+               float* __restrict__ theta_out, uint32_t* __restrict__ st_ent, uint4* __restrict__ st_meta,
+               const int32_t* __restrict__ row_map) {
   using namespace sm100;
   using C = Cfg2<KB, Pol>;
   constexpr int NSB = C::NSB, NDEC = C::NDEC, NACC = C::NACC, BN = C::BN, TS = C::TS;
@@ -97,7 +101,9 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int num_utiles = (int)((n + kBM - 1) / kBM);
   const int num_tp = (num_utiles + 1) / 2;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int nit = (int)((m + BN - 1) / BN);
+  // head pass (nit_cap > 0): only the first nit_cap item tiles; regrouped pass: item tiles it0 .. (see
+  // the host side; it0 is a multiple of kGroup)
+  const int nit = nit_cap > 0 && (int64_t)nit_cap * BN < m ? nit_cap : (int)((m + BN - 1) / BN);
   const uint32_t a_tail_bytes = (uint32_t)(kBM * tail * 2), b_tail_bytes = (uint32_t)(64 * tail * 2);
   const uint32_t a_bytes = (uint32_t)((KB - 1) * kAUnit) + a_tail_bytes;
   const uint32_t b_bytes = (uint32_t)((KB - 1) * kBUnit) + b_tail_bytes;  // this CTA's half of an item tile
@@ -151,9 +157,9 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         // critical path; group 0 is always issued.  (At most two groups of tiles follow the last
         // report; the epilogue drains them unread.)
         bool end_next = false;
-        for (int it = 0; it < nit; ++it) {
-          if (it % kGroup == 0) {
-            const int g = it / kGroup;
+        for (int it = it0; it < nit; ++it) {
+          if ((it - it0) % kGroup == 0) {
+            const int g = (it - it0) / kGroup;  // (groups counted from the pass's first tile)
             bool end = false;
             if (leader) {
               end = end_next;
@@ -161,7 +167,7 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
                 stage_end[stage] = t + 1;
                 mbar_arrive(BAR(R_FULL + stage));  // the marker (no bytes) for the MMA warp
-              } else if ((g + 1) * kGroup < nit) {
+              } else if ((g + 1) * kGroup < nit - it0) {
                 end_next = *done_cum >= 8u * (uint32_t)(t + 1);  // every epilogue warp of the pair is done
                 st_cluster_u32(F(w_dec + 4 * ((g + 1) & 7)), end_next ? 1u : 0u);
                 mbar_arrive_cluster(F(BAR(DEC + ((g + 1) & 7))));
@@ -218,7 +224,7 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           mma_commit_cg2(BAR(A_EMPTY), 3);  // both A buffers are free once the copies completed
         }
         __syncwarp();
-        for (int it = 0; it < nit; ++it) {
+        for (int it = it0; it < nit; ++it) {
           mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
           mbar_wait_sleep(BAR(R_FULL + stage), ph);
           tc_fence_after();
@@ -286,14 +292,19 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int ut = 2 * tp + (int)rank;
       const int64_t row = (int64_t)ut * kBM + rr;
       typename Pol::Row me = Pol::init(row < n, smax);
-      int lastc = 0;  // the row's entry count at its last checkpoint refresh (below)
-      float Eg = __ldg(perr), EgN = (kCsEvery * BN < mi) ? __ldg(perr + kCsEvery * BN) : 0.f;
-      double pnr = nit > kCsEvery ? __ldg(pnorm + kCsEvery * BN) : 0.0;
+      // regrouped pass: the row continues from its head-pass state (theta, entries), saved at the row's
+      // index place
+      const int64_t orow = row_map && row < n ? (int64_t)__ldg(row_map + row) : row;
+      if (row_map && row < n) Pol::load(me, sb, rr, st_ent, st_meta, orow);
+      int lastc = me.cnt;  // the row's entry count at its last checkpoint refresh (below)
+      const int b0 = it0 * BN;
+      float Eg = __ldg(perr + b0), EgN = (b0 + kCsEvery * BN < mi) ? __ldg(perr + b0 + kCsEvery * BN) : 0.f;
+      double pnr = nit > it0 + kCsEvery ? __ldg(pnorm + b0 + kCsEvery * BN) : 0.0;
       mbar_wait(BAR(ACC_FULL + as), aph);
       tc_fence_after();
       tmem_ld64(tq + as * C::ACC_COLS, hA);
       tmem_ld_wait64(hA);
-      int it = 0;
+      int it = it0;
       bool done = false;
       for (; it < nit; ++it) {
         const int base0 = it * BN;
@@ -363,7 +374,15 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           tc_fence_after();
         }
       }
-      Pol::finish(me, sb, rr, e0x2, kmax, m, row, n, cand, ccount, ovf_list, ovf_count);
+      if (theta_out) {  // head pass: compact, save the row's state, and its theta as the regrouping key
+        Pol::compact(me, sb, rr, e0x2, kmax);
+        if (row < n) {
+          Pol::save(me, sb, rr, st_ent, st_meta, row);
+          theta_out[row] = me.ovf ? -__int_as_float(0x7f800000) : me.theta;
+        }
+      } else {  // lists go to the row's place in the index order (row_map: regrouped pass)
+        Pol::finish(me, sb, rr, e0x2, kmax, m, orow, n, cand, ccount, ovf_list, ovf_count);
+      }
       __syncwarp();
     }
   }
@@ -374,6 +393,79 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------------------ host side
+// Regrouping (two passes).  A tile pair ends at the Cauchy-Schwarz exit of its LAST row, i.e. at the
+// largest exit point over 256 users, and norm-sorted users have unrelated exit points (the exit of row u
+// is where ||p|| 2^e drops below theta_u ~ tau_kmax(u) / ||u||, a function of u's direction).  So:
+//   head pass   the first `head` item tiles of every user tile; each row is compacted and its state
+//               (theta, entries) saved at its index place, its theta (a valid lower bound of tau_kmax)
+//               written as the regrouping key;
+//   sort        rows by that theta, descending (CUB radix sort of n float keys), and gather a copy of
+//               U16 in that order;
+//   main pass   item tiles head .. over the regrouped rows, each row continuing from its saved state,
+//               the lists written to the rows' index places (row_map).
+// Offline (configs[4] recipe, 4,096 users, exact taus): random 256-row groups exit at 2,318 item tiles
+// on average, groups sorted by the theta of the first 32 item tiles at 2,076 (by the exact exit: 2,058).
+// The head items are paid once (the dense phase, where theta climbs from -inf, costs ~10x a steady-state
+// tile: ncu, configs[4], 16 head tiles = 8.3 ms of the build).
+__global__ void k_iota32(int32_t* __restrict__ v, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int32_t)i;
+}
+
+// out row i = in row perm[i]; rows of ldh halves (ldh a multiple of 16: 32-byte rows), 16-byte copies
+__global__ void k_gather_rows16(const uint4* __restrict__ in, const int32_t* __restrict__ perm, int64_t n,
+                                int vec_per_row, uint4* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t r = i / vec_per_row;
+  if (r >= n) return;
+  const int v = (int)(i - r * vec_per_row);
+  out[i] = __ldg(in + (int64_t)__ldg(perm + r) * vec_per_row + v);
+}
+
+// Scratch of a regrouped build (one allocation, freed stream-ordered by regroup_free).
+cudaError_t regroup_alloc(Regroup& g, int64_t n, int ldh, int slots, cudaStream_t st) {
+  g.cub_bytes = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, g.cub_bytes, (const float*)nullptr, (float*)nullptr,
+                                            (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+  auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t o_th = 0, o_ths = o_th + up(n * 4), o_io = o_ths + up(n * 4), o_pm = o_io + up(n * 4),
+               o_cub = o_pm + up(n * 4), o_u = o_cub + up(g.cub_bytes), o_me = o_u + up((size_t)n * ldh * 2),
+               o_en = o_me + up((size_t)n * 16), total = o_en + up((size_t)n * slots * 4);
+  const cudaError_t e = cudaMallocAsync(&g.buf, total, st);
+  if (e != cudaSuccess) return e;
+  char* B = static_cast<char*>(g.buf);
+  g.th = reinterpret_cast<float*>(B + o_th);
+  g.ths = reinterpret_cast<float*>(B + o_ths);
+  g.io = reinterpret_cast<int32_t*>(B + o_io);
+  g.pm = reinterpret_cast<int32_t*>(B + o_pm);
+  g.cub = B + o_cub;
+  g.U16b = reinterpret_cast<__half*>(B + o_u);
+  g.meta = reinterpret_cast<uint4*>(B + o_me);
+  g.ent = reinterpret_cast<uint32_t*>(B + o_en);
+  return cudaSuccess;
+}
+
+void regroup_free(Regroup& g, cudaStream_t st) {
+  if (g.buf) cudaFreeAsync(g.buf, st);
+  g.buf = nullptr;
+}
+
+// rows sorted by their head theta (descending; ties by row: the sort is stable), U16 gathered in that
+// order; g.ths = the sorted thetas (the regrouped pass's theta_in), g.pm = regrouped row -> index row
+cudaError_t regroup_rows(Regroup& g, const __half* U16, int64_t n, int ldh, cudaStream_t st) {
+  k_iota32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g.io, n);
+  count_launch();
+  cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(g.cub, g.cub_bytes, g.th, g.ths, g.io, g.pm, (int)n, 0, 32, st);
+  count_launch(6);  // (CUB: histogram, exclusive sum, 4 onesweep passes)
+  if (e != cudaSuccess) return e;
+  const int vpr = ldh / 8;
+  const int64_t tot = n * vpr;
+  k_gather_rows16<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(reinterpret_cast<const uint4*>(U16), g.pm, n, vpr,
+                                                                 reinterpret_cast<uint4*>(g.U16b));
+  count_launch();
+  return cudaGetLastError();
+}
+
 template <int KB, class Pol>
 static cudaError_t launch_tc2cta(const BuildCtx& c, cudaStream_t st) {
   using C = Cfg2<KB, Pol>;
@@ -395,14 +487,49 @@ static cudaError_t launch_tc2cta(const BuildCtx& c, cudaStream_t st) {
   x->build_kernel = 4;
   x->cand_slots = Pol::kSlots;
   int stale_every = 16;  // checkpoint refresh period in item tiles (a multiple of the C-S check period 4)
+  // head pass length in item tiles (a multiple of the C-S check period); regrouping pays when the item
+  // set is long against the head and there are several waves of tile pairs to regroup
+  int head = 32;
 #ifdef RMIPS_DEV
   if (const char* e = getenv("RMIPS_STALE_EVERY")) stale_every = atoi(e);  // 0: off
+  if (const char* e = getenv("RMIPS_HEAD_TILES")) head = atoi(e) & ~3;    // 0: no regrouping
 #endif
-  k_build_tc2cta<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tat, tb, tbt, x->perr, x->pnorm, c.scale_dev, x->n,
-                                                              c.mb, x->kmax, (x->d + 15) / 16, tail, c.cand, c.ccount,
-                                                              c.ovf_list, c.ovf_count, c.tiles_done, stale_every);
+  const int64_t nit = (c.mb + 127) / 128;
+  const int kmax = x->kmax, ksteps = (x->d + 15) / 16;
+  const int64_t n = x->n;
+  if (head <= 0 || nit < 16 * (int64_t)head || tiles < 4 * sms || (int64_t)head * 128 < kmax) {
+    k_build_tc2cta<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tat, tb, tbt, x->perr, x->pnorm, c.scale_dev, n,
+                                                                c.mb, kmax, ksteps, tail, c.cand, c.ccount, c.ovf_list,
+                                                                c.ovf_count, c.tiles_done, stale_every, 0, 0, nullptr,
+                                                                nullptr, nullptr, nullptr);
+    count_launch();
+    return cudaGetLastError();
+  }
+  Regroup g;
+  e = regroup_alloc(g, n, x->ldh, Pol::kSlots, st);
+  if (e != cudaSuccess) return e;
+  CUtensorMap ga, gat;
+  if (!make_tmap_f16_box(&ga, g.U16b, (uint64_t)n, (uint64_t)x->ldh, kBM) ||
+      !make_tmap_f16_box(&gat, g.U16b, (uint64_t)n, (uint64_t)x->ldh, kBM, tail)) {
+    regroup_free(g, st);
+    return cudaErrorNotSupported;
+  }
+  k_build_tc2cta<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tat, tb, tbt, x->perr, x->pnorm, c.scale_dev, n, c.mb,
+                                                              kmax, ksteps, tail, c.cand, c.ccount, c.ovf_list,
+                                                              c.ovf_count, c.tiles_done, stale_every, 0, head, g.th,
+                                                              g.ent, g.meta, nullptr);
   count_launch();
-  return cudaGetLastError();
+  e = regroup_rows(g, x->U16, n, x->ldh, st);
+  if (e == cudaSuccess) {
+    k_build_tc2cta<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ga, gat, tb, tbt, x->perr, x->pnorm, c.scale_dev, n,
+                                                                c.mb, kmax, ksteps, tail, c.cand, c.ccount,
+                                                                c.ovf_list, c.ovf_count, c.tiles_done, stale_every, head,
+                                                                0, nullptr, g.ent, g.meta, g.pm);
+    count_launch();
+    e = cudaGetLastError();
+  }
+  regroup_free(g, st);
+  return e;
 }
 
 // CTA-pair build for d_pad <= 256 with 128-slot 4-byte candidate lists (m <= 2^20, k_max <= 80);

@@ -33,6 +33,29 @@ struct QPolT {
   __device__ static void refresh_theta(Row& me, Buf sb, int rr, float e0x2, int kmax) {  // (whole warp)
     me = qrow_refresh<SLOTS, PB>(me, sb, rr, e0x2, kmax, true);
   }
+  __device__ static void compact(Row& me, Buf sb, int rr, float e0x2, int kmax) {  // (whole warp)
+    me = qrow_refresh<SLOTS, PB>(me, sb, rr, e0x2, kmax);
+  }
+  // Row state of a two-pass (regrouped) build: entries row-major at ent[row * SLOTS ..], {theta, vmax,
+  // cnt, ovf} at meta[row]; the quantiser (base, w) depends on smax only, the same in both passes
+  __device__ static void save(const Row& me, Buf sb, int rr, uint32_t* ent, uint4* meta, int64_t row) {
+    sb.assume_shared();
+    const uint32_t* b = sb.buf + rr;
+    uint32_t* o = ent + row * SLOTS;
+    for (int i = 0; i < me.cnt; ++i) o[i] = b[i * sb.R];
+    meta[row] = make_uint4(__float_as_uint(me.theta), __float_as_uint(me.vmax), (uint32_t)me.cnt, (uint32_t)me.ovf);
+  }
+  __device__ static void load(Row& me, Buf sb, int rr, const uint32_t* ent, const uint4* meta, int64_t row) {
+    const uint4 mt = __ldg(meta + row);
+    me.theta = __uint_as_float(mt.x);
+    me.vmax = __uint_as_float(mt.y);
+    me.cnt = (int)mt.z;
+    me.ovf = (int)mt.w;
+    sb.assume_shared();
+    uint32_t* b = sb.buf + rr;
+    const uint32_t* s = ent + row * SLOTS;
+    for (int i = 0; i < me.cnt; ++i) b[i * sb.R] = __ldg(s + i);
+  }
   __device__ static void finish(Row& me, Buf sb, int rr, float e0x2, int kmax, int64_t m, int64_t row, int64_t n,
                                 int32_t* cand, int32_t* ccount, int32_t* ovf_list, int* ovf_count) {
     qrow_finish<SLOTS, PB>(me, sb, rr, e0x2, kmax, m, row, n, cand, SLOTS, ccount, ovf_list, ovf_count);

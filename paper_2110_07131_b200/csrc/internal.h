@@ -54,6 +54,23 @@ struct BuildCtx {
   unsigned long long* tiles_done = nullptr;  // device: (128-user tile, item tile) contractions issued
 };
 
+// Regrouped tensor-core builds (build_tc2cta.cu): head-pass thetas -> rows sorted by theta -> U16 copy
+struct Regroup {
+  void* buf = nullptr;   // the one scratch allocation
+  float* th = nullptr;   // [n] head-pass theta per index row
+  float* ths = nullptr;  // [n] sorted (descending): theta per regrouped row
+  int32_t* io = nullptr; // [n] iota
+  int32_t* pm = nullptr; // [n] regrouped row -> index row
+  void* cub = nullptr;
+  size_t cub_bytes = 0;
+  __half* U16b = nullptr;  // [n][ldh] U16 rows in regrouped order
+  uint32_t* ent = nullptr; // [n][slots] head-pass candidate entries (index row order)
+  uint4* meta = nullptr;   // [n] head-pass row state
+};
+cudaError_t regroup_alloc(Regroup& g, int64_t n, int ldh, int slots, cudaStream_t st);
+cudaError_t regroup_rows(Regroup& g, const __half* U16, int64_t n, int ldh, cudaStream_t st);
+void regroup_free(Regroup& g, cudaStream_t st);
+
 size_t build_cub_bytes(int64_t n, int64_t m);
 cudaError_t build_prep(BuildCtx& c, const float* Q, const float* P, cudaStream_t st);
 cudaError_t build_simt(const BuildCtx& c, cudaStream_t st);

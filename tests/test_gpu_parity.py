@@ -877,3 +877,57 @@ def test_large_d_lists_do_not_overflow():
         vals, oids = oracle.topk(w.U[users], w.P, 50)
         assert np.array_equal(tau[:, users].T, vals) and np.array_equal(ids[:, users].T, oids), d
         idx.close()
+
+
+_REGROUP_SCRIPT = """
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2110_07131_b200 import rmips
+from synth import generator as gen
+d = int(sys.argv[3])
+w = gen.make_workload(4, n=80001, m=70000, nq=8, d=d)
+dev = torch.device("cuda:0")
+idx = rmips.rmips_build_index(torch.from_numpy(w.U).to(dev), torch.from_numpy(w.P).to(dev), 10)
+assert idx.build_kernel == (4 if d > 64 else 1) and idx.overflow_rows == 0
+_, _, tau, ids = idx.export()
+np.savez(sys.argv[2], tau=tau, ids=ids, tiles=idx.tiles_done, lib=rmips.LIB_PATH)
+"""
+
+
+@pytest.mark.parametrize("d", [50, 100])
+def test_regrouped_build_equals_single_pass(tmp_path, d):
+    """The tensor-core builds' head pass + regrouping (rows sorted by their head theta, lists written back
+    to the index order) triggers at n >= 4 * 148 * 128 users and >= 16 head lengths of item tiles: on
+    80,001 x 70,000 (ragged last user tile), k_max = 10, d = 50 (k_build_tc) and d = 100 (the CTA-pair
+    kernel), the lists equal the oracle's on a user sample (the
+    last rows included) and the whole tables equal those of the single-pass build (development library,
+    RMIPS_HEAD_TILES=0), bitwise."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    from paper_2110_07131_b200 import build_lib
+    devlib = build_lib.build_dev()
+    got = {}
+    # (d <= 64: regrouping is off in the product library; forced on here)
+    for name, env in (("regroup", {"RMIPS_HEAD_TILES": "8" if d == 50 else "32"}), ("single", {"RMIPS_HEAD_TILES": "0"})):
+        out = str(tmp_path / (name + ".npz"))
+        e = dict(os.environ, RMIPS_LIB=devlib, **env)
+        r = subprocess.run([sys.executable, "-c", _REGROUP_SCRIPT, root, out, str(d)], env=e, capture_output=True, text=True,
+                           timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        got[name] = np.load(out)
+    assert np.array_equal(got["regroup"]["tau"], got["single"]["tau"])
+    assert np.array_equal(got["regroup"]["ids"], got["single"]["ids"])
+    assert got["regroup"]["tiles"] < got["single"]["tiles"] or d == 50
+    w = gen.make_workload(4, n=80001, m=70000, nq=8, d=d)
+    rng = np.random.default_rng(11)
+    sample = np.unique(np.concatenate([rng.choice(80001, 250, replace=False), np.arange(80001 - 40, 80001)]))
+    vals, oids = oracle.topk(w.U[sample], w.P, 10)
+    # (export returns users in their original order)
+    idx = rmips.rmips_build_index(_t(w.U), _t(w.P), 10)
+    _, _, tau, ids = idx.export()
+    idx.close()
+    assert np.array_equal(tau, got["regroup"]["tau"]) and np.array_equal(ids, got["regroup"]["ids"])
+    assert np.array_equal(tau[:, sample].T, vals)
+    assert np.array_equal(ids[:, sample].T, oids)
