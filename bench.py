@@ -402,7 +402,8 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     kname = {0: "k_build_simt", 1: "k_build_tc", 2: "k_build_tcq", 3: "k_build_tcq (streamed A)",
-             4: "k_build_tc2cta (CTA pairs, cta_group::2)"}.get(recs[-1]["build_kernel"], "?")
+             4: "k_build_tc2cta (CTA pairs, cta_group::2; head pass + regrouped main pass when n >= 4 x 148 x 128"
+                ", m >= 512 x 128)"}.get(recs[-1]["build_kernel"], "?")
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
         traffic = tj.get("cfg%d" % cfg, {}).get("simt" if args.simt else "tc")
@@ -429,6 +430,16 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
               "timing": "CUDA events right around each k_query_tc launch, summed over the step's calls",
               "phase_ms_per_step": med("q_filter"),
               "calls": len(batches)}
+    # the same kernel against the tensor roofline: at d = 200 a 256-query call is ~1.1e11 flop of MMA for
+    # ~0.4 GB of user rows, so the filter is co-bound (upper bound of the issued flops: MMA N = the Lemma 3
+    # prefix <= the sub-batch's queries)
+    qcols = min(256, max(b_ - a_ for a_, b_ in batches)) if batches else 0
+    qflops = med("tiles_scored") * 128 * qcols * 2 * (16 * ((spec.d + 15) // 16))
+    qpeak = peaks["bf16_tflops_sustained"] if qf_ms > 20.0 and peaks.get("bf16_tflops_sustained") else peaks["bf16_tflops"]
+    if qf_ms > 0 and not args.simt:
+        roof_q["tensor"] = {"achieved": qflops / (qf_ms / 1e3) / 1e12, "peak": qpeak, "unit": "TFLOP/s",
+                            "frac": qflops / (qf_ms / 1e3) / 1e12 / qpeak,
+                            "flop_unit": "2 K_pad per (user, query) slot of every scored 128-user x <= 256-query tile"}
 
     # ---- the verification scan (Q5, k_verify_scan), P' index only
     roof_s = None
