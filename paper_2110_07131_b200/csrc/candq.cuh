@@ -217,8 +217,10 @@ __device__ __forceinline__ void qrow_append_chunk(ScoreFn s_of, const float (&g4
   sb.assume_shared();
   uint32_t* b = sb.buf + rr;
   const int R = sb.R;
-  // padding (-inf) never passes; after the first refresh, lo >= base is implied by s~ >= thr
-  const float thr = fmaxf(__fsub_rd(me.theta, E), -3.402823466e38f);
+  // padding columns (>= mi) hold -inf (epiq_slow) and never pass.  The quantisable-bound condition
+  // lo = rd(s~ - E) >= base is folded into the threshold: it holds iff s~ >= base + E (base is a float),
+  // iff s~ >= ru(base + E) -- the same appends as testing it per column
+  const float thr = fmaxf(fmaxf(__fsub_rd(me.theta, E), __fadd_ru(me.base, E)), -3.402823466e38f);
   int c = me.cnt;
   float vmax = me.vmax;
 #pragma unroll
@@ -231,7 +233,7 @@ __device__ __forceinline__ void qrow_append_chunk(ScoreFn s_of, const float (&g4
       for (int j = 0; j < 4; ++j) {
         const float sj = s_of(4 * g + j);
         lo[j] = __fsub_rd(sj, E);
-        p[j] = sj >= thr && pos0 + 4 * g + j < mi && lo[j] >= me.base;
+        p[j] = sj >= thr;
       }
       const int o1 = c + p[0], o2 = o1 + p[1], o3 = o2 + p[2];
       if (p[0]) b[c * R] = (q_of<PB>(lo[0], me) << kQPosBits) | (uint32_t)(pos0 + 4 * g);

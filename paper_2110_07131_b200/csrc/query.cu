@@ -242,7 +242,23 @@ k_exact_decide(const float* __restrict__ q, const float* __restrict__ U32, const
     const float* qa = q + (int64_t)qin * d;
     const float* ua = U32 + row * d;
     double g = 0.0;
-    for (int c = 0; c < d; c += 32) {
+    // the first kPre chunks' products are loaded before the first add (one memory latency per pair
+    // instead of one per 32 coordinates; a call's few hundred pairs are latency-bound)
+    constexpr int kPre = 8;
+    double pcs[kPre];
+#pragma unroll
+    for (int i = 0; i < kPre; ++i) {
+      const int t = 32 * i + lane;
+      pcs[i] = t < d ? (double)__ldg(qa + t) * (double)__ldg(ua + t) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < kPre; ++i) {
+      if (32 * i >= d) break;
+      const int nj = min(32, d - 32 * i);
+#pragma unroll 8
+      for (int jj = 0; jj < nj; ++jj) g = __dadd_rn(g, __shfl_sync(0xffffffffu, pcs[i], jj));
+    }
+    for (int c = 32 * kPre; c < d; c += 32) {
       const double pc = c + lane < d ? (double)__ldg(qa + c + lane) * (double)__ldg(ua + c + lane) : 0.0;
       const int nj = min(32, d - c);
 #pragma unroll 8
@@ -744,24 +760,71 @@ __global__ void k_copy_ids32(const uint32_t* __restrict__ keys, int64_t total, u
 // in the workspace changes).  Every warp works independently.
 constexpr int kChunkWords = 1024;
 constexpr int kBitsThreads = 256;
+constexpr int C_BITS_TICKET = kNumCounters + 2;  // (spare, zeroed per call / batch) k_bits_count CTAs done
 __global__ void __launch_bounds__(kBitsThreads)
 k_bits_count(const uint32_t* __restrict__ bits, const uint8_t* __restrict__ dirty, int64_t nw, int64_t nbr,
-             int64_t nchunk_total, int64_t* __restrict__ counts) {
+             int64_t nchunk_total, int64_t* __restrict__ counts, int64_t* __restrict__ chunk_off,
+             unsigned long long* __restrict__ ticket) {  // ticket: zeroed before the launch
   const int64_t g = (blockIdx.x * (int64_t)kBitsThreads + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (g >= nchunk_total) return;
-  const int64_t per_row = (nw + kChunkWords - 1) / kChunkWords;
-  const int64_t q = g / per_row, c = g - q * per_row;
-  const int64_t blk = c * 32 + lane;  // this lane's block of the row
-  int cnt = 0;
-  if (blk < nbr && dirty[q * nbr + blk]) {
-    const uint32_t* wp = bits + q * nw + blk * 32;
-    const int nwb = (int)min((int64_t)32, nw - blk * 32);
-    for (int i = 0; i < nwb; ++i) cnt += __popc(wp[i]);
-  }
+  if (g < nchunk_total) {  // (no early return: the last CTA's scan below needs every thread)
+    const int64_t per_row = (nw + kChunkWords - 1) / kChunkWords;
+    const int64_t q = g / per_row, c = g - q * per_row;
+    const int64_t blk = c * 32 + lane;  // this lane's block of the row
+    int cnt = 0;
+    if (blk < nbr && dirty[q * nbr + blk]) {
+      const uint32_t* wp = bits + q * nw + blk * 32;
+      const int nwb = (int)min((int64_t)32, nw - blk * 32);
+      for (int i = 0; i < nwb; ++i) cnt += __popc(wp[i]);
+    }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if (lane == 0) counts[g] = cnt;
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) counts[g] = cnt;
+  }
+  // The last CTA to finish scans the chunk counts (exclusive), so the emit pass needs no separate scan
+  // launch: every CTA publishes its counts (fence) before taking a ticket.
+  __shared__ int last;
+  __shared__ int64_t wsum[kBitsThreads / 32];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1ull) == (unsigned long long)gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int t = threadIdx.x, w = t >> 5;
+  constexpr int kPer = 8;
+  int64_t carry = 0;
+  for (int64_t base = 0; base < nchunk_total; base += (int64_t)kBitsThreads * kPer) {
+    const int64_t a = base + (int64_t)t * kPer;
+    int64_t v[kPer], sum = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      v[i] = a + i < nchunk_total ? __ldcg(counts + a + i) : 0;
+      sum += v[i];
+    }
+    int64_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    int64_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < kBitsThreads / 32; ++i) {
+      wpre += i < w ? wsum[i] : 0;
+      tot += wsum[i];
+    }
+    int64_t run = carry + wpre + incl - sum;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      if (a + i < nchunk_total) chunk_off[a + i] = run;
+      run += v[i];
+    }
+    carry += tot;
+    __syncthreads();  // wsum is reused by the next round
+  }
 }
 __global__ void __launch_bounds__(kBitsThreads)
 k_bits_emit(uint32_t* __restrict__ bits, uint8_t* __restrict__ dirty, int64_t nw, int64_t nbr, int b,
@@ -831,49 +894,6 @@ k_bits_emit(uint32_t* __restrict__ bits, uint8_t* __restrict__ dirty, int64_t nw
   }
 }
 
-// Exclusive scan of up to kScanSmallMax chunk counts in one CTA (one launch instead of the device-wide
-// scan's two): thread t owns a contiguous run of the values.
-constexpr int kScanSmallThreads = 1024;
-constexpr int64_t kScanSmallMax = (int64_t)kScanSmallThreads * 32;
-__global__ void __launch_bounds__(kScanSmallThreads)
-k_scan_small(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t cnt) {
-  __shared__ int64_t wsum[kScanSmallThreads / 32];
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int64_t per = (cnt + kScanSmallThreads - 1) / kScanSmallThreads;  // <= 32
-  const int64_t a = (int64_t)t * per, e = a + per < cnt ? a + per : cnt;
-  int64_t v[32];  // this thread's values, read once (unrolled: registers)
-  int64_t sum = 0;
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    v[i] = a + i < e ? in[a + i] : 0;
-    sum += v[i];
-  }
-  int64_t incl = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int64_t x = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += x;
-  }
-  if (lane == 31) wsum[w] = incl;
-  __syncthreads();
-  if (w == 0) {
-    int64_t v = wsum[lane], vi = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t x = __shfl_up_sync(0xffffffffu, vi, o);
-      if (lane >= o) vi += x;
-    }
-    wsum[lane] = vi - v;  // exclusive prefix of the warps
-  }
-  __syncthreads();
-  int64_t run = wsum[w] + incl - sum;
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    if (a + i < e) out[a + i] = run;
-    run += v[i];
-  }
-}
-
 size_t query_scan_bytes(int64_t items) {
   size_t a = 0;
   cub::DeviceScan::ExclusiveSum((void*)nullptr, a, (const int64_t*)nullptr, (int64_t*)nullptr, (int)items);
@@ -887,16 +907,10 @@ cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, 
   int64_t* counts = reinterpret_cast<int64_t*>(c.acc_sorted);  // the sort's space is unused on this path
   int64_t* chunk_off = counts + nch;
   const unsigned grid = (unsigned)((nch * 32 + kBitsThreads - 1) / kBitsThreads);
-  k_bits_count<<<grid, kBitsThreads, 0, st>>>(c.bits, c.dirty, c.nw, c.nbr, nch, counts); count_launch();
-  if (nch <= kScanSmallMax) {
-    k_scan_small<<<1, kScanSmallThreads, 0, st>>>(counts, chunk_off, nch);
-    count_launch();
-  } else {
-    size_t tb = c.cub_bytes;
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(c.cub_tmp, tb, counts, chunk_off, (int)nch, st);
-    count_launch(2);
-    if (e != cudaSuccess) return e;
-  }
+  // the chunk counts are scanned by the count kernel's last CTA (no separate scan launch)
+  k_bits_count<<<grid, kBitsThreads, 0, st>>>(c.bits, c.dirty, c.nw, c.nbr, nch, counts, chunk_off,
+                                               c.counters + C_BITS_TICKET);
+  count_launch();
   k_bits_emit<<<grid, kBitsThreads, 0, st>>>(c.bits, c.dirty, c.nw, c.nbr, c.b, nch, counts, chunk_off, capacity,
                                               offsets, user_ids, obase, obase_next, c.counters, c.flags_dev, fold);
   count_launch();
