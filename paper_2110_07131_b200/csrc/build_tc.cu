@@ -131,8 +131,8 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
            const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
            int64_t n, int64_t m, int kmax, int seed_tiles, int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
            int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count, unsigned long long* __restrict__ tiles_done,
-           int dev, int stale_every, int nit_cap, float* __restrict__ theta_out,
-           const float* __restrict__ theta_in, const int32_t* __restrict__ row_map) {
+           int dev, int stale_every, int it0, int nit_cap, float* __restrict__ theta_out,
+           uint2* __restrict__ st_ent, uint4* __restrict__ st_meta, const int32_t* __restrict__ row_map) {
   using namespace sm100;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base, derived from smem_raw by pointer arithmetic so that the compiler
@@ -193,8 +193,8 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         if (t > 0) mbar_wait_sleep(BAR(A_EMPTY), (t - 1) & 1);
         mbar_arrive_expect_tx(BAR(A_FULL), KB * kTileBytes);
         for (int kb = 0; kb < KB; ++kb) tma_load_2d(sA + kb * kTileBytes, &tmA, kb * 64, ut * kBM, BAR(A_FULL));
-        for (int j = 0; j < seed_tiles + nit; ++j) {  // seed pass, then all item tiles
-          const int it = j < seed_tiles ? j : j - seed_tiles;
+        for (int j = 0; j < seed_tiles + nit - it0; ++j) {  // seed pass, then item tiles it0 ..
+          const int it = j < seed_tiles ? j : it0 + j - seed_tiles;
           // the smem stage and the accumulator stage of a tile have the same index (kStages == kAcc):
           // the tile's ACC_FULL commit (its MMAs are done) also frees the item tile's stage
           mbar_wait_sleep(BAR(ACC_FULL + stage), ph ^ 1);
@@ -224,7 +224,7 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     for (int ut = blockIdx.x; ut < num_utiles; ut += gridDim.x, ++t) {
       mbar_wait_sleep(BAR(A_FULL), t & 1);
       tc_fence_after();
-      for (int j = 0; j < seed_tiles + nit; ++j) {
+      for (int j = 0; j < seed_tiles + nit - it0; ++j) {
         mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
         mbar_wait_sleep(BAR(B_FULL + stage), ph);
         tc_fence_after();
@@ -291,10 +291,11 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       // error bound of every chunk of a group of kCsEvery item tiles: perr of the group's first item
       // (perr is non-increasing along the norm-sorted items, so it bounds every later item's);
       // the next group's is prefetched a whole group ahead
-      float Eg = __ldg(perr), EgN = (kCsEvery * kBN < mi) ? __ldg(perr + kCsEvery * kBN) : 0.f;
+      const int b0 = it0 * kBN;  // (it0: a multiple of kCsEvery)
+      float Eg = __ldg(perr + b0), EgN = (b0 + kCsEvery * kBN < mi) ? __ldg(perr + b0 + kCsEvery * kBN) : 0.f;
       // (the raw fp64 norm is prefetched; it is scaled and rounded only at the check, so the load's
       // latency is not exposed where it is issued)
-      double pnr = nit > kCsEvery ? __ldg(pnorm + kCsEvery * kBN) : 0.0;
+      double pnr = nit > it0 + kCsEvery ? __ldg(pnorm + b0 + kCsEvery * kBN) : 0.0;
       mbar_wait(BAR(ACC_FULL + as), aph);
       tc_fence_after();
       tmem_ld64(tq + as * kBN, hA);
@@ -346,10 +347,13 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         me.cnt = 0;
         me.vmax = -__int_as_float(0x7f800000);
       }
-      // regrouped pass: the head pass's theta of this row is a valid lower bound of its k_max-th largest
-      // true score
-      if (theta_in && row < n) me.theta = fmaxf(me.theta, __ldg(theta_in + row));
-      int it = 0;
+      // regrouped pass: the row continues from its head-pass state (theta, entries), saved at its index row
+      const int64_t orow = row_map && row < n ? (int64_t)__ldg(row_map + row) : row;
+      if (row_map && row < n) {
+        cand_load(me, sm, rloc, st_ent, st_meta, orow);
+        lastc = me.cnt;
+      }
+      int it = it0;
       bool done = false;                        // warp-uniform: this warp's rows cannot gain any more
       if (dev & (kDevEpiSkip | kDevEpiLoad)) {  // dev: release every accumulator stage (MMA + feed alone)
         uint32_t sink = 0;
@@ -445,11 +449,13 @@ k_build_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
           tc_fence_after();
         }
       }
-      if (theta_out) {  // head pass: the row's theta only (verified counts, no lists)
-        me = cand_refresh(me, sm, rloc, e0x2, kmax, true);
-        if (row < n) theta_out[row] = me.ovf ? -__int_as_float(0x7f800000) : me.theta;
+      if (theta_out) {  // head pass: compact, save the row's state, and its theta as the regrouping key
+        me = cand_refresh(me, sm, rloc, e0x2, kmax);
+        if (row < n) {
+          cand_save(me, sm, rloc, st_ent, st_meta, row);
+          theta_out[row] = me.ovf ? -__int_as_float(0x7f800000) : me.theta;
+        }
       } else {  // lists go to the row's place in the index order (row_map: regrouped pass)
-        const int64_t orow = row_map && row < n ? (int64_t)__ldg(row_map + row) : row;
         cand_finish(me, sm, rloc, e0x2, kmax, m, orow, n, cand, kCand, ccount, ovf_list, ovf_count);
       }
       __syncwarp();
@@ -553,38 +559,42 @@ static cudaError_t launch_tc(const BuildCtx& c, cudaStream_t st) {
   if (16 * seed < x->kmax) seed = 0;
   x->build_kernel = 1;
   x->cand_slots = kCand;
-  // regrouping (as build_tc2cta.cu, but the main pass restarts at item tile 0 from the head thetas, no seed
-  // pass): off -- configs[1..3] measured 6.30 -> 7.00, 3.02 -> 3.59, 0.86 -> 1.07 ms with 8 head tiles
-  // (configs[3]: 26 % fewer item tiles, but the head's dense phase is paid twice)
+  // regrouping (as build_tc2cta.cu): a head pass over the first `head` item tiles (with its seed pass) saves
+  // each row's state and theta, the rows are sorted by theta, and the main pass continues from item tile
+  // `head` over the regrouped rows.  Off in the product: at d <= 64 the head (seed + 8 tiles + state save)
+  // is 3.05 ms of configs[3]'s 6.3 ms build, so although the main pass issues 34 % fewer item tiles the two
+  // passes take 6.44 ms (head 4 / 8 / 12: 6.46 / 6.44 / 6.64); configs[1], [2] (no C-S exits) lose 20 %
+  // (tools/gpu_probe3.sh).  Kept for the tests (RMIPS_HEAD_TILES in the development library).
   int head = 0;
 #ifdef RMIPS_DEV
-  if (const char* e = getenv("RMIPS_HEAD_TILES")) head = atoi(e) & ~3;  // 0: no regrouping
+  if (const char* e = getenv("RMIPS_HEAD_TILES")) head = atoi(e) & ~3;  // 0: one pass
 #endif
   const int64_t n = x->n;
   if (head <= 0 || nit < 16 * head || tiles < 4 * sm_count() || head * kBN < x->kmax) {
     k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, n, c.mb, x->kmax, seed, c.cand,
                                                  c.ccount, c.ovf_list, c.ovf_count, c.tiles_done, dev, stale_every, 0,
-                                                 nullptr, nullptr, nullptr);
+                                                 0, nullptr, nullptr, nullptr, nullptr);
     count_launch();
     return cudaGetLastError();
   }
   Regroup g;
-  e = regroup_alloc(g, n, x->ldh, 0, st);
+  e = regroup_alloc(g, n, x->ldh, 2 * kCand, st);  // 8-byte entries
   if (e != cudaSuccess) return e;
   CUtensorMap ga;
   if (!make_tmap_f16_box(&ga, g.U16b, (uint64_t)n, (uint64_t)x->ldh, kBM)) {
     regroup_free(g, st);
     return cudaErrorNotSupported;
   }
+  uint2* ent = reinterpret_cast<uint2*>(g.ent);
   k_build_tc<KB><<<grid, kThreads, smem, st>>>(ta, tb, x->perr, x->pnorm, cs, n, c.mb, x->kmax, seed, c.cand, c.ccount,
-                                               c.ovf_list, c.ovf_count, c.tiles_done, dev, stale_every, head, g.th,
-                                               nullptr, nullptr);
+                                               c.ovf_list, c.ovf_count, c.tiles_done, dev, stale_every, 0, head, g.th,
+                                               ent, g.meta, nullptr);
   count_launch();
   e = regroup_rows(g, x->U16, n, x->ldh, st);
   if (e == cudaSuccess) {
     k_build_tc<KB><<<grid, kThreads, smem, st>>>(ga, tb, x->perr, x->pnorm, cs, n, c.mb, x->kmax, 0, c.cand, c.ccount,
-                                                 c.ovf_list, c.ovf_count, c.tiles_done, dev, stale_every, 0, nullptr,
-                                                 g.ths, g.pm);
+                                                 c.ovf_list, c.ovf_count, c.tiles_done, dev, stale_every, head, 0,
+                                                 nullptr, ent, g.meta, g.pm);
     count_launch();
     e = cudaGetLastError();
   }

@@ -291,6 +291,29 @@ __device__ __forceinline__ void cand_finish(CandRow& me, CandSmem sm, int rloc, 
   }
 }
 
+// Row state of a two-pass (regrouped) build: entries row-major at ent[row * kCand ..], {theta, vmax, cnt,
+// ovf} at meta[row].
+__device__ __forceinline__ void cand_save(const CandRow& me, CandSmem sm, int rloc, uint2* __restrict__ ent,
+                                          uint4* __restrict__ meta, int64_t row) {
+  sm.assume_shared();
+  const uint2* b = sm.buf + rloc;
+  uint2* o = ent + row * kCand;
+  for (int i = 0; i < me.cnt; ++i) o[i] = b[i * kCandRows];
+  meta[row] = make_uint4(__float_as_uint(me.theta), __float_as_uint(me.vmax), (uint32_t)me.cnt, (uint32_t)me.ovf);
+}
+__device__ __forceinline__ void cand_load(CandRow& me, CandSmem sm, int rloc, const uint2* __restrict__ ent,
+                                          const uint4* __restrict__ meta, int64_t row) {
+  const uint4 mt = __ldg(meta + row);
+  me.theta = __uint_as_float(mt.x);
+  me.vmax = __uint_as_float(mt.y);
+  me.cnt = (int)mt.z;
+  me.ovf = (int)mt.w;
+  sm.assume_shared();
+  uint2* b = sm.buf + rloc;
+  const uint2* s = ent + row * kCand;
+  for (int i = 0; i < me.cnt; ++i) b[i * kCandRows] = __ldg(s + i);
+}
+
 // 2 * E0 rounded up, E0 = perr[0] >= every item's bound (perr is non-increasing along the
 // norm-sorted items).
 __device__ __forceinline__ float cand_e0x2(const float* __restrict__ perr) {
