@@ -70,7 +70,7 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                const float* __restrict__ perr, const double* __restrict__ pnorm, const float* __restrict__ pscale,
                int64_t n, int64_t m, int kmax, int ksteps, int tail, int32_t* __restrict__ cand,
                int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count,
-               unsigned long long* __restrict__ tiles_done, int stale_every, int it0, int nit_cap,
+               unsigned long long* __restrict__ tiles_done, int stale_every, int seed, int it0, int nit_cap,
                float* __restrict__ theta_out, uint32_t* __restrict__ st_ent, uint4* __restrict__ st_meta,
                const int32_t* __restrict__ row_map) {
   using namespace sm100;
@@ -156,10 +156,14 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         // decision to the follower a whole group AHEAD, so the follower's wait for it is off the feed's
         // critical path; group 0 is always issued.  (At most two groups of tiles follow the last
         // report; the epilogue drains them unread.)
+        // (seed pass: item tiles 0 .. seed-1 are issued first, then the pass's tiles it0 ..; groups are
+        // counted over that whole sequence)
         bool end_next = false;
-        for (int it = it0; it < nit; ++it) {
-          if ((it - it0) % kGroup == 0) {
-            const int g = (it - it0) / kGroup;  // (groups counted from the pass's first tile)
+        const int ntot = seed + nit - it0;
+        for (int jj = 0; jj < ntot; ++jj) {
+          const int it = jj < seed ? jj : it0 + jj - seed;
+          if (jj % kGroup == 0) {
+            const int g = jj / kGroup;
             bool end = false;
             if (leader) {
               end = end_next;
@@ -167,7 +171,7 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 mbar_wait_sleep(BAR(R_EMPTY + stage), ph ^ 1);
                 stage_end[stage] = t + 1;
                 mbar_arrive(BAR(R_FULL + stage));  // the marker (no bytes) for the MMA warp
-              } else if ((g + 1) * kGroup < nit - it0) {
+              } else if ((g + 1) * kGroup < ntot) {
                 end_next = *done_cum >= 8u * (uint32_t)(t + 1);  // every epilogue warp of the pair is done
                 st_cluster_u32(F(w_dec + 4 * ((g + 1) & 7)), end_next ? 1u : 0u);
                 mbar_arrive_cluster(F(BAR(DEC + ((g + 1) & 7))));
@@ -224,7 +228,7 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           mma_commit_cg2(BAR(A_EMPTY), 3);  // both A buffers are free once the copies completed
         }
         __syncwarp();
-        for (int it = it0; it < nit; ++it) {
+        for (int jj = 0; jj < seed + nit - it0; ++jj) {
           mbar_wait_sleep(BAR(ACC_EMPTY + as), aph ^ 1);
           mbar_wait_sleep(BAR(R_FULL + stage), ph);
           tc_fence_after();
@@ -259,7 +263,8 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           next();
           if (elect_one()) mma_commit_cg2(BAR(ACC_FULL + as), 3);
           __syncwarp();
-          tiles_issued += 2;  // two 128 x 128 (user tile, item tile) contractions
+          tiles_issued += jj >= seed ? 2 : 0;  // two 128 x 128 (user tile, item tile) contractions (the seed
+                                               // pass repeats tiles: not counted)
           if (++as == NACC) as = 0, aph ^= 1;
         }
       }
@@ -300,6 +305,36 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int b0 = it0 * BN;
       float Eg = __ldg(perr + b0), EgN = (b0 + kCsEvery * BN < mi) ? __ldg(perr + b0 + kCsEvery * BN) : 0.f;
       double pnr = nit > it0 + kCsEvery ? __ldg(pnorm + b0 + kCsEvery * BN) : 0.0;
+      if (seed > 0) {
+        // Seed pass over item tiles 0 .. seed-1 (contracted again below): the maxima of the 16 groups of 8
+        // items of each tile, minus the tile's error bound (rounded down), are lower bounds of distinct items'
+        // true scores, so the k_max-th largest of them is a valid starting theta (qrow_seed).  They sit in the
+        // row's (still empty) candidate slots, 16 per tile.
+        float vmx = -__int_as_float(0x7f800000);
+        uint32_t* sbr = sb.buf + rr;
+        for (int j = 0; j < seed; ++j) {
+          mbar_wait(BAR(ACC_FULL + as), aph);
+          tc_fence_after();
+          tmem_ld64(tq + as * C::ACC_COLS, hA);
+          tmem_ld64(tq + as * C::ACC_COLS + 64, hB);
+          const float Ej = __ldg(perr + j * BN);  // bounds every item of tile j (perr is non-increasing)
+          tmem_ld_wait64(hA);
+          tmem_ld_wait64(hB);
+          release(as);
+          if (++as == NACC) as = 0, aph ^= 1;
+#pragma unroll
+          for (int g = 0; g < 16; ++g) {
+            const uint32_t* h = g < 8 ? hA + 8 * g : hB + 8 * (g - 8);
+            const auto f = [](uint32_t u) { return __uint_as_float(u); };
+            const float gm = fmaxf(fmaxf(fmaxf(f(h[0]), f(h[1])), fmaxf(f(h[2]), f(h[3]))),
+                                   fmaxf(fmaxf(f(h[4]), f(h[5])), fmaxf(f(h[6]), f(h[7]))));
+            const float lo = __fsub_rd(gm, Ej);
+            sbr[(16 * j + g) * sb.R] = __float_as_uint(lo);
+            vmx = fmaxf(vmx, lo);
+          }
+        }
+        me.theta = fmaxf(me.theta, qrow_seed(sb, rr, 16 * seed, vmx, kmax));  // dead rows keep +inf
+      }
       mbar_wait(BAR(ACC_FULL + as), aph);
       tc_fence_after();
       tmem_ld64(tq + as * C::ACC_COLS, hA);
@@ -502,12 +537,17 @@ static cudaError_t launch_tc2cta(const BuildCtx& c, cudaStream_t st) {
   if (const char* e = getenv("RMIPS_STALE_EVERY")) stale_every = atoi(e);  // 0: off
 #endif
   const int kmax = x->kmax, ksteps = (x->d + 15) / 16;
+  // seed pass (the single pass and the head pass): 8 item tiles, 128 group maxima in the row's 128 slots
+  int seed = nit >= 32 && Pol::kSlots >= 128 && 128 >= kmax ? 8 : 0;
+#ifdef RMIPS_DEV
+  if (const char* e = getenv("RMIPS_SEED_TILES")) seed = atoi(e) > 0 ? seed : 0;  // 0: no seed pass
+#endif
   const int64_t n = x->n;
   if (!regroup) {
     k_build_tc2cta<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tat, tb, tbt, x->perr, x->pnorm, c.scale_dev, n,
                                                                 c.mb, kmax, ksteps, tail, c.cand, c.ccount, c.ovf_list,
-                                                                c.ovf_count, c.tiles_done, stale_every, 0, 0, nullptr,
-                                                                nullptr, nullptr, nullptr);
+                                                                c.ovf_count, c.tiles_done, stale_every, seed, 0, 0,
+                                                                nullptr, nullptr, nullptr, nullptr);
     count_launch();
     return cudaGetLastError();
   }
@@ -522,15 +562,15 @@ static cudaError_t launch_tc2cta(const BuildCtx& c, cudaStream_t st) {
   }
   k_build_tc2cta<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tat, tb, tbt, x->perr, x->pnorm, c.scale_dev, n, c.mb,
                                                               kmax, ksteps, tail, c.cand, c.ccount, c.ovf_list,
-                                                              c.ovf_count, c.tiles_done, stale_every, 0, head, g.th,
-                                                              g.ent, g.meta, nullptr);
+                                                              c.ovf_count, c.tiles_done, stale_every, seed, 0, head,
+                                                              g.th, g.ent, g.meta, nullptr);
   count_launch();
   e = regroup_rows(g, x->U16, n, x->ldh, st);
   if (e == cudaSuccess) {
     k_build_tc2cta<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ga, gat, tb, tbt, x->perr, x->pnorm, c.scale_dev, n,
                                                                 c.mb, kmax, ksteps, tail, c.cand, c.ccount,
-                                                                c.ovf_list, c.ovf_count, c.tiles_done, stale_every, head,
-                                                                0, nullptr, g.ent, g.meta, g.pm);
+                                                                c.ovf_list, c.ovf_count, c.tiles_done, stale_every, 0,
+                                                                head, 0, nullptr, g.ent, g.meta, g.pm);
     count_launch();
     e = cudaGetLastError();
   }

@@ -207,6 +207,47 @@ static __device__ __noinline__ QRow qrow_refresh(QRow me, QBuf sb, int rr, float
   return nw;
 }
 
+// Seed threshold (build_tc2cta.cu's seed pass): slots [0, cnt) of row rr hold, as float bits, lower bounds of
+// the maxima of disjoint item groups (group max of s~ minus E, rounded down: <= the true score of a distinct
+// item), so the k_max-th largest of them is a valid lower bound of tau_kmax.  Returns the largest level of a
+// 5-pass quaternary search over [min, vmax] that keeps at least k_max of them (-inf if cnt < k_max).
+static __device__ __noinline__ float qrow_seed(QBuf sb, int rr, int cnt, float vmax, int kmax) {
+  if (cnt < kmax) return -__int_as_float(0x7f800000);
+  sb.assume_shared();
+  const uint32_t* b = sb.buf + rr;
+  const int R = sb.R;
+  float m0 = vmax, m1 = vmax;
+  int i = 0;
+  for (; i + 2 <= cnt; i += 2) m0 = fminf(m0, __uint_as_float(b[i * R])), m1 = fminf(m1, __uint_as_float(b[(i + 1) * R]));
+  for (; i < cnt; ++i) m0 = fminf(m0, __uint_as_float(b[i * R]));
+  float L = fminf(m0, m1), U2 = vmax;
+#pragma unroll 1
+  for (int pass = 0; pass < 5; ++pass) {
+    const float w = U2 - L;
+    const float t1 = fmaf(w, 0.25f, L), t2 = fmaf(w, 0.5f, L), t3 = fmaf(w, 0.75f, L);
+    int a1[4] = {0, 0, 0, 0}, a2[4] = {0, 0, 0, 0}, a3[4] = {0, 0, 0, 0};
+    int j = 0;
+    for (; j + 8 <= cnt; j += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __uint_as_float(b[(j + u) * R]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a1[u & 3] += v[u] >= t1, a2[u & 3] += v[u] >= t2, a3[u & 3] += v[u] >= t3;
+    }
+    for (; j < cnt; ++j) {
+      const float v0 = __uint_as_float(b[j * R]);
+      a1[0] += v0 >= t1, a2[0] += v0 >= t2, a3[0] += v0 >= t3;
+    }
+    const int c1 = (a1[0] + a1[1]) + (a1[2] + a1[3]), c2 = (a2[0] + a2[1]) + (a2[2] + a2[3]),
+              c3 = (a3[0] + a3[1]) + (a3[2] + a3[3]);
+    if (c3 >= kmax) L = t3;
+    else if (c2 >= kmax) L = t2, U2 = t3;
+    else if (c1 >= kmax) L = t1, U2 = t2;
+    else U2 = t1;
+  }
+  return L;
+}
+
 // Append pass of one 32-column chunk (scores via s_of(j), positions pos0 + j; columns >= mi are
 // padding), called by the whole warp; g4[8] are the 4-column group maxima.  Groups are skipped
 // warp-uniformly; inside a group the 4 slots come from a prefix of predicates.

@@ -373,7 +373,7 @@ import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
 from paper_2110_07131_b200 import rmips
 from synth import generator as gen
-U, P = gen.random_instance(77, 20000, 6000, 50, "skewed")
+U, P = gen.random_instance(77, 20000, 6000, int(sys.argv[3]) if len(sys.argv) > 3 else 50, "skewed")
 dev = torch.device("cuda:0")
 idx = rmips.rmips_build_index(torch.from_numpy(U).to(dev), torch.from_numpy(P).to(dev), 50)
 assert idx.build_flags & rmips.RMIPS_BUILD_SIMT == 0
@@ -931,3 +931,27 @@ def test_regrouped_build_equals_single_pass(tmp_path, d):
     assert np.array_equal(tau, got["regroup"]["tau"]) and np.array_equal(ids, got["regroup"]["ids"])
     assert np.array_equal(tau[:, sample].T, vals)
     assert np.array_equal(ids[:, sample].T, oids)
+
+
+@pytest.mark.parametrize("env", [{}, {"RMIPS_SEED_TILES": "0"}], ids=["default", "seed0"])
+def test_pair_build_seed_pass_bitwise(env, tmp_path):
+    """The CTA-pair build's seed pass (8 item tiles of 8-item group maxima -> a starting theta) on the single
+    pass (20,000 users: no regrouping), d = 120, m = 6,000 (47 item tiles), k_max = 50: the lists equal the
+    oracle's on a user sample with and without the seed pass (development library switches)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    from paper_2110_07131_b200 import build_lib
+    devlib = build_lib.build_dev()
+    out = str(tmp_path / "v.npz")
+    e = dict(os.environ, RMIPS_LIB=devlib, **env)
+    r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root, out, "120"], env=e, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = np.load(out)
+    U, P = gen.random_instance(77, 20000, 6000, 120, "skewed")
+    sample = np.sort(np.random.default_rng(8).choice(U.shape[0], 500, replace=False))
+    vals, oids = oracle.topk(U[sample], P, 50)
+    assert np.array_equal(got["tau"][:, sample].T, vals)
+    assert np.array_equal(got["ids"][:, sample].T, oids)
