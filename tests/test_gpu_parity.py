@@ -955,3 +955,25 @@ def test_pair_build_seed_pass_bitwise(env, tmp_path):
     vals, oids = oracle.topk(U[sample], P, 50)
     assert np.array_equal(got["tau"][:, sample].T, vals)
     assert np.array_equal(got["ids"][:, sample].T, oids)
+
+
+def test_regrouped_build_overflowed_rows():
+    """Rows that overflow their candidate buffer in the regrouped CTA-pair build's HEAD pass (150 identical
+    items with the largest norm: massive ties for every user with a positive cosine to them) are saved with
+    the overflow mark (their theta sorts last), skip the main pass and take the exact fallback at their index
+    rows; the sampled tables equal the oracle's (ties by ascending item id)."""
+    w = gen.make_workload(4, n=80001, m=70000, nq=8, d=100)
+    P = w.P.copy()
+    nrm = np.linalg.norm(P.astype(np.float64), axis=1)
+    p = P[int(np.argmax(nrm))].astype(np.float64)
+    P[:150] = (p / np.linalg.norm(p) * 2.0 * nrm.max()).astype(np.float32)
+    idx = rmips.rmips_build_index(_t(w.U), _t(P), 10)
+    assert idx.build_kernel == 4
+    assert idx.overflow_rows > 1000
+    _, _, tau, ids = idx.export()
+    idx.close()
+    rng = np.random.default_rng(5)
+    sample = np.sort(rng.choice(80001, 300, replace=False))
+    vals, oids = oracle.topk(w.U[sample], P, 10)
+    assert np.array_equal(tau[:, sample].T, vals)
+    assert np.array_equal(ids[:, sample].T, oids)
