@@ -791,39 +791,44 @@ k_bits_count(const uint32_t* __restrict__ bits, const uint8_t* __restrict__ dirt
   __syncthreads();
   if (!last) return;
   __threadfence();
+  // thread t owns the contiguous run [t per, (t + 1) per) of the counts: one pass over registers when
+  // per <= 32 (every load in flight at once), else a sum pass and a write pass over the run
   const int t = threadIdx.x, w = t >> 5;
-  constexpr int kPer = 8;
-  int64_t carry = 0;
-  for (int64_t base = 0; base < nchunk_total; base += (int64_t)kBitsThreads * kPer) {
-    const int64_t a = base + (int64_t)t * kPer;
-    int64_t v[kPer], sum = 0;
+  const int64_t per = (nchunk_total + kBitsThreads - 1) / kBitsThreads;
+  const int64_t a = (int64_t)t * per, e = a + per < nchunk_total ? a + per : nchunk_total;
+  int64_t v[32], sum = 0;
+  if (per <= 32) {
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      v[i] = a + i < nchunk_total ? __ldcg(counts + a + i) : 0;
+    for (int i = 0; i < 32; ++i) {
+      v[i] = a + i < e ? __ldcg(counts + a + i) : 0;
       sum += v[i];
     }
-    int64_t incl = sum;
+  } else {
+#pragma unroll 8
+    for (int64_t i = a; i < e; ++i) sum += __ldcg(counts + i);
+  }
+  int64_t incl = sum;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t x = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += x;
-    }
-    if (lane == 31) wsum[w] = incl;
-    __syncthreads();
-    int64_t wpre = 0, tot = 0;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  int64_t run = incl - sum;
 #pragma unroll
-    for (int i = 0; i < kBitsThreads / 32; ++i) {
-      wpre += i < w ? wsum[i] : 0;
-      tot += wsum[i];
-    }
-    int64_t run = carry + wpre + incl - sum;
+  for (int i = 0; i < kBitsThreads / 32; ++i) run += i < w ? wsum[i] : 0;
+  if (per <= 32) {
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      if (a + i < nchunk_total) chunk_off[a + i] = run;
+    for (int i = 0; i < 32; ++i) {
+      if (a + i < e) chunk_off[a + i] = run;
       run += v[i];
     }
-    carry += tot;
-    __syncthreads();  // wsum is reused by the next round
+  } else {
+    for (int64_t i = a; i < e; ++i) {
+      chunk_off[i] = run;
+      run += __ldcg(counts + i);
+    }
   }
 }
 __global__ void __launch_bounds__(kBitsThreads)
