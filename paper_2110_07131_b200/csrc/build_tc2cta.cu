@@ -71,7 +71,7 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                int64_t n, int64_t m, int kmax, int ksteps, int tail, int32_t* __restrict__ cand,
                int32_t* __restrict__ ccount, int32_t* __restrict__ ovf_list, int* __restrict__ ovf_count,
                unsigned long long* __restrict__ tiles_done, int stale_every, int seed, int it0, int nit_cap,
-               float* __restrict__ theta_out, uint32_t* __restrict__ st_ent, uint4* __restrict__ st_meta,
+               float* __restrict__ theta_out, uint32_t* __restrict__ st_ent, uint4* __restrict__ st_meta,  // (entries: Pol's format)
                const int32_t* __restrict__ row_map) {
   using namespace sm100;
   using C = Cfg2<KB, Pol>;
@@ -308,10 +308,9 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       if (seed > 0) {
         // Seed pass over item tiles 0 .. seed-1 (contracted again below): the maxima of the 16 groups of 8
         // items of each tile, minus the tile's error bound (rounded down), are lower bounds of distinct items'
-        // true scores, so the k_max-th largest of them is a valid starting theta (qrow_seed).  They sit in the
+        // true scores, so the k_max-th largest of them is a valid starting theta (Pol::seed_theta).  They sit in the
         // row's (still empty) candidate slots, 16 per tile.
         float vmx = -__int_as_float(0x7f800000);
-        uint32_t* sbr = sb.buf + rr;
         for (int j = 0; j < seed; ++j) {
           mbar_wait(BAR(ACC_FULL + as), aph);
           tc_fence_after();
@@ -329,11 +328,11 @@ k_build_tc2cta(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             const float gm = fmaxf(fmaxf(fmaxf(f(h[0]), f(h[1])), fmaxf(f(h[2]), f(h[3]))),
                                    fmaxf(fmaxf(f(h[4]), f(h[5])), fmaxf(f(h[6]), f(h[7]))));
             const float lo = __fsub_rd(gm, Ej);
-            sbr[(16 * j + g) * sb.R] = __float_as_uint(lo);
+            Pol::seed_store(sb, rr, 16 * j + g, lo);
             vmx = fmaxf(vmx, lo);
           }
         }
-        me.theta = fmaxf(me.theta, qrow_seed(sb, rr, 16 * seed, vmx, kmax));  // dead rows keep +inf
+        me.theta = fmaxf(me.theta, Pol::seed_theta(sb, rr, 16 * seed, vmx, kmax));  // dead rows keep +inf
       }
       mbar_wait(BAR(ACC_FULL + as), aph);
       tc_fence_after();
@@ -552,7 +551,7 @@ static cudaError_t launch_tc2cta(const BuildCtx& c, cudaStream_t st) {
     return cudaGetLastError();
   }
   Regroup g;
-  e = regroup_alloc(g, n, x->ldh, Pol::kSlots, st);
+  e = regroup_alloc(g, n, x->ldh, Pol::kEntWords, st);
   if (e != cudaSuccess) return e;
   CUtensorMap ga, gat;
   if (!make_tmap_f16_box(&ga, g.U16b, (uint64_t)n, (uint64_t)x->ldh, kBM) ||
@@ -583,7 +582,12 @@ static cudaError_t launch_tc2cta(const BuildCtx& c, cudaStream_t st) {
 cudaError_t build_tc2cta(const BuildCtx& c, cudaStream_t st) {
   if (c.cstride != kCand || c.mb > QPolT<128>::kMaxItems) return cudaErrorNotSupported;
   switch (c.idx->dpad) {
-    case 64: return launch_tc2cta<1, QPolT<128>>(c, st);
+    case 64:
+#ifdef RMIPS_DEV
+      if (const char* e = getenv("RMIPS_2CTA_FPOL"))  // 8-byte entries (cand.cuh); 2: branch-free appends
+        return atoi(e) == 2 ? launch_tc2cta<1, FPolFlat>(c, st) : launch_tc2cta<1, FPol>(c, st);
+#endif
+      return launch_tc2cta<1, QPolT<128>>(c, st);
     case 128: return launch_tc2cta<2, QPolT<128>>(c, st);
     case 192: return launch_tc2cta<3, QPolT<128>>(c, st);
     case 256: return launch_tc2cta<4, QPolT<128>>(c, st);

@@ -36,6 +36,12 @@ struct QPolT {
   __device__ static void compact(Row& me, Buf sb, int rr, float e0x2, int kmax) {  // (whole warp)
     me = qrow_refresh<SLOTS, PB>(me, sb, rr, e0x2, kmax);
   }
+  static constexpr int kEntWords = SLOTS;  // 32-bit words of a row's saved entries
+  // seed pass: value i of the row (float bits) in slot i; the k_max-th largest of cnt values
+  __device__ static void seed_store(Buf sb, int rr, int i, float v) { sb.buf[i * sb.R + rr] = __float_as_uint(v); }
+  __device__ static float seed_theta(Buf sb, int rr, int cnt, float vmax, int kmax) {
+    return qrow_seed(sb, rr, cnt, vmax, kmax);
+  }
   // Row state of a two-pass (regrouped) build: entries row-major at ent[row * SLOTS ..], {theta, vmax,
   // cnt, ovf} at meta[row]; the quantiser (base, w) depends on smax only, the same in both passes
   __device__ static void save(const Row& me, Buf sb, int rr, uint32_t* ent, uint4* meta, int64_t row) {
@@ -83,6 +89,37 @@ struct FPol {
   __device__ static void finish(Row& me, Buf sb, int rr, float e0x2, int kmax, int64_t m, int64_t row, int64_t n,
                                 int32_t* cand, int32_t* ccount, int32_t* ovf_list, int* ovf_count) {
     cand_finish(me, sb, rr, e0x2, kmax, m, row, n, cand, kCand, ccount, ovf_list, ovf_count);
+  }
+  __device__ static void compact(Row& me, Buf sb, int rr, float e0x2, int kmax) {  // (whole warp)
+    me = cand_refresh(me, sb, rr, e0x2, kmax);
+  }
+  static constexpr int kEntWords = 2 * kCand;  // 8-byte entries
+  __device__ static void save(const Row& me, Buf sb, int rr, uint32_t* ent, uint4* meta, int64_t row) {
+    cand_save(me, sb, rr, reinterpret_cast<uint2*>(ent), meta, row);
+  }
+  __device__ static void load(Row& me, Buf sb, int rr, const uint32_t* ent, const uint4* meta, int64_t row) {
+    cand_load(me, sb, rr, reinterpret_cast<const uint2*>(ent), meta, row);
+  }
+  // seed pass: two values per 8-byte slot (as k_build_tc's seed), the k_max-th largest via cand_seed
+  __device__ static void seed_store(Buf sb, int rr, int i, float v) {
+    uint32_t* w = reinterpret_cast<uint32_t*>(sb.buf + (i >> 1) * kCandRows + rr);
+    w[i & 1] = __float_as_uint(v);
+  }
+  __device__ static float seed_theta(Buf sb, int rr, int cnt, float vmax, int kmax) {
+    CandRow t = cand_init(true);
+    t.cnt = cnt >> 1;
+    t.vmax = vmax;
+    return cand_seed(t, sb, rr, kmax);
+  }
+};
+
+// FPol with the branch-free append of k_build_tc's slow path (every column's slot from a running count; no
+// per-group votes): the CTA-pair kernel at d_pad = 64 (development switch RMIPS_2CTA_FPOL=2)
+struct FPolFlat : FPol {
+  template <typename F>
+  __device__ static void append(F f, const float (&g4)[8], float E, int pos0, int, Row& me, Buf sb, int rr) {
+    const float mx = fmaxf(fmaxf(fmaxf(g4[0], g4[1]), fmaxf(g4[2], g4[3])), fmaxf(fmaxf(g4[4], g4[5]), fmaxf(g4[6], g4[7])));
+    cand_append_flat(f, mx, E, pos0, me, sb, rr);  // columns >= m hold -inf (epiq_slow): never appended
   }
 };
 

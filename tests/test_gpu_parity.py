@@ -977,3 +977,29 @@ def test_regrouped_build_overflowed_rows():
     vals, oids = oracle.topk(w.U[sample], P, 10)
     assert np.array_equal(tau[:, sample].T, vals)
     assert np.array_equal(ids[:, sample].T, oids)
+
+
+@pytest.mark.parametrize("env", [{"RMIPS_2CTA_D64": "1"}, {"RMIPS_2CTA_D64": "1", "RMIPS_2CTA_FPOL": "1"},
+                                 {"RMIPS_2CTA_D64": "1", "RMIPS_2CTA_FPOL": "2"}],
+                         ids=["pair-qpol", "pair-fpol", "pair-fpol-flat"])
+def test_pair_build_at_d64_bitwise(env, tmp_path):
+    """The CTA-pair kernel forced onto d_pad = 64 (development switches) with its 4-byte (QPolT) and 8-byte
+    (FPol) candidate lists, single pass with the seed pass (20,000 users, 47 item tiles, k_max = 50): the
+    lists equal the oracle's on a user sample."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    from paper_2110_07131_b200 import build_lib
+    devlib = build_lib.build_dev()
+    out = str(tmp_path / "v.npz")
+    e = dict(os.environ, RMIPS_LIB=devlib, **env)
+    r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root, out, "50"], env=e, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = np.load(out)
+    U, P = gen.random_instance(77, 20000, 6000, 50, "skewed")
+    sample = np.sort(np.random.default_rng(9).choice(U.shape[0], 500, replace=False))
+    vals, oids = oracle.topk(U[sample], P, 50)
+    assert np.array_equal(got["tau"][:, sample].T, vals)
+    assert np.array_equal(got["ids"][:, sample].T, oids)
