@@ -542,22 +542,28 @@ static cudaError_t launch_tc2cta(const BuildCtx& c, cudaStream_t st) {
   if (const char* e = getenv("RMIPS_SEED_TILES")) seed = atoi(e) > 0 ? seed : 0;  // 0: no seed pass
 #endif
   const int64_t n = x->n;
-  if (!regroup) {
+  // the two-pass scratch (~n (0.5 KB + 2 ldh) bytes); when it cannot be had the build takes the single pass
+  Regroup g;
+  CUtensorMap ga, gat;
+  bool two = regroup;
+  if (two && regroup_alloc(g, n, x->ldh, Pol::kEntWords, st) != cudaSuccess) {
+    cudaGetLastError();
+    g.buf = nullptr;
+    two = false;
+  }
+  if (two && (!make_tmap_f16_box(&ga, g.U16b, (uint64_t)n, (uint64_t)x->ldh, kBM) ||
+              !make_tmap_f16_box(&gat, g.U16b, (uint64_t)n, (uint64_t)x->ldh, kBM, tail))) {
+    regroup_free(g, st);
+    two = false;
+  }
+  if (!two) {
+    if (regroup) stale_every = 16;  // (the single pass's period)
     k_build_tc2cta<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tat, tb, tbt, x->perr, x->pnorm, c.scale_dev, n,
                                                                 c.mb, kmax, ksteps, tail, c.cand, c.ccount, c.ovf_list,
                                                                 c.ovf_count, c.tiles_done, stale_every, seed, 0, 0,
                                                                 nullptr, nullptr, nullptr, nullptr);
     count_launch();
     return cudaGetLastError();
-  }
-  Regroup g;
-  e = regroup_alloc(g, n, x->ldh, Pol::kEntWords, st);
-  if (e != cudaSuccess) return e;
-  CUtensorMap ga, gat;
-  if (!make_tmap_f16_box(&ga, g.U16b, (uint64_t)n, (uint64_t)x->ldh, kBM) ||
-      !make_tmap_f16_box(&gat, g.U16b, (uint64_t)n, (uint64_t)x->ldh, kBM, tail)) {
-    regroup_free(g, st);
-    return cudaErrorNotSupported;
   }
   k_build_tc2cta<KB, Pol><<<grid, C::THREADS, C::TOTAL, st>>>(ta, tat, tb, tbt, x->perr, x->pnorm, c.scale_dev, n, c.mb,
                                                               kmax, ksteps, tail, c.cand, c.ccount, c.ovf_list,
