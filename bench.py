@@ -414,6 +414,10 @@ def run_config(cfg, args, dev, rank, ws, steps, warmup, parity_users, e2e=True, 
             if peaks["src"] == "measured" else "fallback (B200_PROFILING.md)",
             "flops_per_launch": flops, "flop_unit": "2 d per (user, item) pair of the issued 128 x 128 tiles",
             "tiles_issued": tiles, "kernel_ms": kern_ms,
+            "launches_per_build": 2 if recs[-1]["build_kernel"] == 4 and spec.n >= 4 * 148 * 128 and spec.m >= 512 * 128 else 1,
+            "time_basis": "the build's contraction phase (CUDA events): every contraction launch of the build (head + "
+                          "regrouped main pass where they apply) and the regroup sort / gather between them; flops "
+                          "are those of all issued tiles (seed-pass repeats not counted)",
             "effective_tflops_incl_pruned": flops_eff / (kern_ms / 1e3) / 1e12,
             "share_of_step": kern_ms / ms_per_step}
 
