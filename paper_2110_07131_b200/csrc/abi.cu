@@ -15,6 +15,7 @@
 using namespace rmips;
 
 std::atomic<long long> rmips::g_launches{0};
+bool rmips::g_pdl = true;
 
 namespace {
 

@@ -835,6 +835,7 @@ void sort_graph_put(SortGraph* g, cudaStream_t st) {
 
 // Zero up to four small device regions (word counts) in one launch instead of four memsets.
 __global__ void k_zero4(uint32_t* a, int na, uint32_t* b, int nb, uint32_t* c, int nc, uint32_t* d, int nd) {
+  pdl_enter();  // (PDL: see launch_pdl)
   const int t = threadIdx.x;
   if (t < na) a[t] = 0u;
   if (t < nb) b[t] = 0u;
@@ -842,8 +843,8 @@ __global__ void k_zero4(uint32_t* a, int na, uint32_t* b, int nb, uint32_t* c, i
   if (t < nd) d[t] = 0u;
 }
 cudaError_t zero4(cudaStream_t st, void* a, int na, void* b, int nb, void* c, int nc, void* d, int nd) {
-  k_zero4<<<1, 128, 0, st>>>(static_cast<uint32_t*>(a), na, static_cast<uint32_t*>(b), nb, static_cast<uint32_t*>(c),
-                             nc, static_cast<uint32_t*>(d), nd);
+  CK_PDL(launch_pdl(k_zero4, dim3(1), dim3(128), 0, st, static_cast<uint32_t*>(a), na, static_cast<uint32_t*>(b), nb, static_cast<uint32_t*>(c),
+                             nc, static_cast<uint32_t*>(d), nd));
   count_launch();
   return cudaGetLastError();
 }

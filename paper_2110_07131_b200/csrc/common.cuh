@@ -17,6 +17,14 @@
 
 namespace rmips {
 
+// Programmatic dependent launch (the query chain, internal.h launch_pdl): a kernel lets its dependent start
+// launching at once and waits for its own predecessor (complete, memory flushed) before touching any of its
+// outputs.  Both are no-ops when the kernel was launched without the attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------------------
 // Fixed geometry.
 constexpr int kTileU = 128;        // users per tile == Lemma 3 block size (reading R5)

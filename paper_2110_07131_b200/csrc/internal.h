@@ -6,8 +6,10 @@
 #include "common.cuh"
 
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
+#include <utility>
 
 namespace rmips {
 
@@ -34,6 +36,33 @@ inline cudaError_t set_smem_attr(const void* func, int bytes) {
 }
 
 // Scratch of one build call (owned by abi.cu, freed before rmips_build_index returns).
+#define CK_PDL(x)                    \
+  do {                               \
+    const cudaError_t e_pdl_ = (x);  \
+    if (e_pdl_ != cudaSuccess) return e_pdl_; \
+  } while (0)
+// Launch with programmatic stream serialisation (PDL): the kernel may start while its stream predecessor
+// drains; it must call pdl_enter() (common.cuh) before reading anything the predecessor writes.
+extern bool g_pdl;  // (on; the development library reads RMIPS_NO_PDL at every launch instead)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+#ifdef RMIPS_DEV
+  cfg.numAttrs = getenv("RMIPS_NO_PDL") ? 0 : 1;  // development: the chain without PDL
+#else
+  cfg.numAttrs = g_pdl ? 1 : 0;
+#endif
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 struct BuildCtx {
   rmips_index_s* idx = nullptr;
   int64_t mb = 0;                 // items the lists are built over (idx->mprime)

@@ -27,6 +27,7 @@ constexpr int kPrepCtas = kQB / kPrepWarps;  // CTAs per sub-batch
 __global__ void __launch_bounds__(32 * kPrepWarps)
 k_query_norms(const float* __restrict__ q, int b, int d, double* __restrict__ nrm, float* __restrict__ cmax,
               int* __restrict__ flags) {
+  pdl_enter();  // (PDL: see launch_pdl)
   __shared__ float smax[kPrepWarps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t qi = (int64_t)blockIdx.x * kPrepWarps + wid;  // sub-batch slot of the INPUT order
@@ -67,6 +68,7 @@ k_query_finish(const float* __restrict__ q, int b, int d, int ldh, double c1, do
                const double* __restrict__ nrm, const float* __restrict__ cmax, __half* __restrict__ Q16,
                float* __restrict__ qn, float* __restrict__ qerr, float* __restrict__ qscale,
                int32_t* __restrict__ qperm, int32_t* __restrict__ qcount) {
+  pdl_enter();  // (PDL: see launch_pdl)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int s = blockIdx.x / kPrepCtas;
   const int t = (blockIdx.x - s * kPrepCtas) * kPrepWarps + wid;  // query t of sub-batch s (input order)
@@ -231,6 +233,7 @@ __global__ void __launch_bounds__(256)
 k_exact_decide(const float* __restrict__ q, const float* __restrict__ U32, const double* __restrict__ tauk,
                const int32_t* __restrict__ perm_u, int d, unsigned long long* __restrict__ ctr,
                const uint64_t* __restrict__ dense, AccSink acc_list, int64_t cap) {
+  pdl_enter();  // (PDL: see launch_pdl)
   const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_SCAN_LIST]);
   const int lane = threadIdx.x & 31;
   const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -351,6 +354,7 @@ constexpr int kScanWarps = 8;
 __global__ void k_scan_compact(const uint64_t* __restrict__ und_list, const int32_t* __restrict__ beats0,
                                unsigned long long* __restrict__ ctr, int64_t cap, uint64_t* __restrict__ out_rec,
                                int32_t* __restrict__ out_beats) {
+  pdl_enter();  // (PDL: see launch_pdl)
   const int64_t total = (int64_t)min((unsigned long long)cap, ctr[C_UND_TOTAL]);
   const int lane = threadIdx.x & 31;
   for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < total; i0 += (int64_t)gridDim.x * blockDim.x) {
@@ -633,10 +637,10 @@ static inline unsigned nblk(int64_t work, int t) { return (unsigned)((work + t -
 cudaError_t query_prep(QueryCtx& c, cudaStream_t st) {
   rmips_index_s* x = c.idx;
   const unsigned grid = (unsigned)(c.nsub * kPrepCtas);
-  k_query_norms<<<grid, 32 * kPrepWarps, 0, st>>>(c.q, c.b, x->d, c.qnrm, c.qcmax, c.flags_dev);
+  CK_PDL(launch_pdl(k_query_norms, dim3(grid), dim3(32 * kPrepWarps), 0, st, c.q, c.b, x->d, c.qnrm, c.qcmax, c.flags_dev));
   count_launch();
-  k_query_finish<<<grid, 32 * kPrepWarps, 0, st>>>(c.q, c.b, x->d, x->ldh, x->c1, x->c2, c.qnrm, c.qcmax, c.Q16, c.qn,
-                                                   c.qerr, c.qscale, c.qperm, c.qcount);
+  CK_PDL(launch_pdl(k_query_finish, dim3(grid), dim3(32 * kPrepWarps), 0, st, c.q, c.b, x->d, x->ldh, x->c1, x->c2, c.qnrm, c.qcmax, c.Q16, c.qn,
+                                                   c.qerr, c.qscale, c.qperm, c.qcount));
   count_launch();
   return cudaGetLastError();
 }
@@ -714,10 +718,11 @@ cudaError_t query_exact(QueryCtx& c, cudaStream_t st) {
     count_launch();
     CK_RET(launch_scan(c, x->mprime, c.scan_cnt, false, st));
   } else {
-    k_scan_compact<<<148 * 4, 256, 0, st>>>(c.und, nullptr, c.counters, c.cap, c.scan_rec, c.scan_beats);
+    CK_PDL(launch_pdl(k_scan_compact, dim3(148 * 4), dim3(256), 0, st, c.und, nullptr, c.counters, c.cap, c.scan_rec,
+                      c.scan_beats));
     count_launch();
-    k_exact_decide<<<148 * 4, 256, 0, st>>>(c.q, x->U32, x->tau + (int64_t)(c.k - 1) * x->n, x->perm_u, x->d,
-                                            c.counters, c.scan_rec, AccSink{c.acc, c.bits, c.nw, c.dirty, c.nbr}, c.cap);
+    CK_PDL(launch_pdl(k_exact_decide, dim3(148 * 4), dim3(256), 0, st, c.q, x->U32, x->tau + (int64_t)(c.k - 1) * x->n, x->perm_u, x->d,
+                                            c.counters, c.scan_rec, AccSink{c.acc, c.bits, c.nw, c.dirty, c.nbr}, c.cap));
     count_launch();
   }
   return cudaGetLastError();
@@ -765,6 +770,7 @@ __global__ void __launch_bounds__(kBitsThreads)
 k_bits_count(const uint32_t* __restrict__ bits, const uint8_t* __restrict__ dirty, int64_t nw, int64_t nbr,
              int64_t nchunk_total, int64_t* __restrict__ counts, int64_t* __restrict__ chunk_off,
              unsigned long long* __restrict__ ticket) {  // ticket: zeroed before the launch
+  pdl_enter();  // (PDL: see launch_pdl)
   const int64_t g = (blockIdx.x * (int64_t)kBitsThreads + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (g < nchunk_total) {  // (no early return: the last CTA's scan below needs every thread)
@@ -773,6 +779,7 @@ k_bits_count(const uint32_t* __restrict__ bits, const uint8_t* __restrict__ dirt
     const int64_t blk = c * 32 + lane;  // this lane's block of the row
     int cnt = 0;
     if (blk < nbr && dirty[q * nbr + blk]) {
+  pdl_enter();  // (PDL: see launch_pdl)
       const uint32_t* wp = bits + q * nw + blk * 32;
       const int nwb = (int)min((int64_t)32, nw - blk * 32);
       for (int i = 0; i < nwb; ++i) cnt += __popc(wp[i]);
@@ -838,6 +845,7 @@ k_bits_emit(uint32_t* __restrict__ bits, uint8_t* __restrict__ dirty, int64_t nw
             const int64_t* __restrict__ obase, int64_t* __restrict__ obase_next,
             const unsigned long long* __restrict__ ctr, const int* __restrict__ flags_dev,
             unsigned long long* __restrict__ fold) {
+  pdl_enter();  // (PDL: see launch_pdl)
   const int64_t g = (blockIdx.x * (int64_t)kBitsThreads + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (g >= nchunk_total) return;
@@ -913,11 +921,11 @@ cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, 
   int64_t* chunk_off = counts + nch;
   const unsigned grid = (unsigned)((nch * 32 + kBitsThreads - 1) / kBitsThreads);
   // the chunk counts are scanned by the count kernel's last CTA (no separate scan launch)
-  k_bits_count<<<grid, kBitsThreads, 0, st>>>(c.bits, c.dirty, c.nw, c.nbr, nch, counts, chunk_off,
-                                               c.counters + C_BITS_TICKET);
+  CK_PDL(launch_pdl(k_bits_count, dim3(grid), dim3(kBitsThreads), 0, st, c.bits, c.dirty, c.nw, c.nbr, nch, counts, chunk_off,
+                                               c.counters + C_BITS_TICKET));
   count_launch();
-  k_bits_emit<<<grid, kBitsThreads, 0, st>>>(c.bits, c.dirty, c.nw, c.nbr, c.b, nch, counts, chunk_off, capacity,
-                                              offsets, user_ids, obase, obase_next, c.counters, c.flags_dev, fold);
+  CK_PDL(launch_pdl(k_bits_emit, dim3(grid), dim3(kBitsThreads), 0, st, c.bits, c.dirty, c.nw, c.nbr, c.b, nch, counts, chunk_off, capacity,
+                                              offsets, user_ids, obase, obase_next, c.counters, c.flags_dev, fold));
   count_launch();
   return cudaGetLastError();
 }

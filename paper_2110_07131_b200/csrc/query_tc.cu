@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(256)
 k_lemma3_lens(const float* __restrict__ tbk, const float* __restrict__ qn, const int32_t* __restrict__ qcount,
               int nblocks, int bsz, int64_t nlb, int64_t nwork, int flags, int32_t* __restrict__ wlen,
               unsigned long long* __restrict__ ctr) {
+  pdl_enter();  // (PDL: see launch_pdl)
   const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   unsigned long long pairs = 0, pruned = 0, scored = 0;
   if (w < nwork) {
@@ -258,6 +259,7 @@ k_query_tc(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUte
            const float* __restrict__ qscale, const int32_t* __restrict__ qperm, const int32_t* __restrict__ qcount,
            int nsub, int flags, int ksteps, const int32_t* __restrict__ wlen, unsigned long long* __restrict__ ctr,
            AccSink acc_list, uint64_t* __restrict__ und_list, int64_t cap) {
+  pdl_enter();  // (PDL: see launch_pdl)
   using namespace sm100;
   const QLayout lay = QLayout::make(KB, tail);
   const int kStages = lay.nu;  // ring units
@@ -636,16 +638,16 @@ static cudaError_t launch_query_tc(QueryCtx& c, cudaStream_t st) {
   if (getenv("RMIPS_Q_COUNT")) kflags |= kDevQCount;
   if (getenv("RMIPS_Q_NOFEED")) kflags |= kDevQNoFeed;
 #endif
-  k_lemma3_lens<<<(unsigned)((nwork + 255) / 256), 256, 0, st>>>(x->tb + (int64_t)(c.k - 1) * x->nlb, c.qn,
+  CK_PDL(launch_pdl(k_lemma3_lens, dim3((unsigned)((nwork + 255) / 256)), dim3(256), 0, st, x->tb + (int64_t)(c.k - 1) * x->nlb, c.qn,
                                                                  c.qcount, (int)x->nblocks, x->bsz, x->nlb, nwork,
                                                                  c.flags, c.wlen,
-                                                                 c.counters);
+                                                                 c.counters));
   count_launch();
   if (c.ev_k[0]) cudaEventRecord(c.ev_k[0], st);
-  k_query_tc<KB><<<grid, kThreads, smem, st>>>(tu, tut, tq, tqt, x->dpad / 64, tail, x->thr + (int64_t)(c.k - 1) * x->n,
+  CK_PDL(launch_pdl(k_query_tc<KB>, dim3(grid), dim3(kThreads), smem, st, tu, tut, tq, tqt, x->dpad / 64, tail, x->thr + (int64_t)(c.k - 1) * x->n,
                                                x->tb + (int64_t)(c.k - 1) * x->nlb, x->perm_u, x->n,
                                                (int)x->nblocks, c.qn, c.qerr, c.qscale, c.qperm, c.qcount, c.nsub,
-                                               kflags, (x->d + 15) / 16, c.wlen, c.counters, AccSink{c.acc, c.bits, c.nw, c.dirty, c.nbr}, c.und, c.cap);
+                                               kflags, (x->d + 15) / 16, c.wlen, c.counters, AccSink{c.acc, c.bits, c.nw, c.dirty, c.nbr}, c.und, c.cap));
   count_launch();
   if (c.ev_k[1]) cudaEventRecord(c.ev_k[1], st);
   return cudaGetLastError();
