@@ -779,20 +779,20 @@ k_bits_count(const uint32_t* __restrict__ bits, const uint8_t* __restrict__ dirt
     const int64_t blk = c * 32 + lane;  // this lane's block of the row
     int cnt = 0;
     if (blk < nbr && dirty[q * nbr + blk]) {
-  pdl_enter();  // (PDL: see launch_pdl)
       const uint32_t* wp = bits + q * nw + blk * 32;
       const int nwb = (int)min((int64_t)32, nw - blk * 32);
-      for (int i = 0; i < nwb; ++i) cnt += __popc(wp[i]);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) cnt += i < nwb ? __popc(wp[i]) : 0;  // (all 32 loads in flight)
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if (lane == 0) counts[g] = cnt;
   }
   // The last CTA to finish scans the chunk counts (exclusive), so the emit pass needs no separate scan
-  // launch: every CTA publishes its counts (fence) before taking a ticket.
+  // launch: every CTA's writers publish their counts (fence) before thread 0 takes the CTA's ticket.
   __shared__ int last;
   __shared__ int64_t wsum[kBitsThreads / 32];
-  __threadfence();
+  if (lane == 0) __threadfence();  // (the lanes that wrote a count publish it)
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(ticket, 1ull) == (unsigned long long)gridDim.x - 1;
   __syncthreads();
@@ -880,7 +880,12 @@ k_bits_emit(uint32_t* __restrict__ bits, uint8_t* __restrict__ dirty, int64_t nw
   uint32_t* wp = bits + q * nw + blk * 32;
   const int nwb = mine ? (int)min((int64_t)32, nw - blk * 32) : 0;
   int cnt = 0;
-  for (int i = 0; i < nwb; ++i) cnt += __popc(wp[i]);
+  uint32_t wv[32];  // the block's words, every load in flight at once
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    wv[i] = i < nwb ? wp[i] : 0u;
+    cnt += __popc(wv[i]);
+  }
   int incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -890,8 +895,9 @@ k_bits_emit(uint32_t* __restrict__ bits, uint8_t* __restrict__ dirty, int64_t nw
   if (mine) {
     int64_t pos = base + incl - cnt;
     const int32_t u_blk = (int32_t)(blk * 1024);
-    for (int i = 0; i < nwb; ++i) {
-      uint32_t w = wp[i];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      uint32_t w = wv[i];
       if (!w) continue;
       wp[i] = 0u;
       if (fits) {

@@ -226,14 +226,35 @@ k_lemma3_lens(const float* __restrict__ tbk, const float* __restrict__ qn, const
               int nblocks, int bsz, int64_t nlb, int64_t nwork, int flags, int32_t* __restrict__ wlen,
               unsigned long long* __restrict__ ctr) {
   pdl_enter();  // (PDL: see launch_pdl)
-  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // the norms of the (at most kStage) sub-batches this CTA's items fall in are staged in shared memory, so
+  // each binary search is a chain of shared loads instead of ~8 dependent L2 round trips
+  constexpr int kStage = 4;
+  __shared__ float sq[kStage * kQB];
+  const int64_t w0 = blockIdx.x * (int64_t)blockDim.x;
+  const int64_t wl = min(w0 + (int64_t)blockDim.x, nwork) - 1;
+  const int s0 = (int)(w0 / nblocks), ns = wl >= w0 ? (int)(wl / nblocks) - s0 + 1 : 0;
+  const bool staged = ns <= kStage;
+  if (staged)
+    for (int i = threadIdx.x; i < ns * kQB; i += blockDim.x) sq[i] = __ldg(qn + (int64_t)s0 * kQB + i);
+  __syncthreads();
+  const int64_t w = w0 + threadIdx.x;
   unsigned long long pairs = 0, pruned = 0, scored = 0;
   if (w < nwork) {
     const int s = (int)(w / nblocks), t = (int)(w - (int64_t)s * nblocks);
     const int cnt = qcount[s];
     const float* qs = qn + (int64_t)s * kQB;
+    const float* ss = sq + (s - s0) * kQB;
     const int len = tile_lemma3(t, bsz, nlb, cnt, (flags & RMIPS_FLAG_NO_BLOCKS) != 0, tbk,
-                                [&](float tbv) { return lemma3_len(qs, cnt, tbv); }, pairs, pruned);
+                                [&](float tbv) {
+                                  if (!staged) return lemma3_len(qs, cnt, tbv);
+                                  int lo = 0, hi = cnt;  // as lemma3_len, on the staged copy
+                                  while (lo < hi) {
+                                    const int mid = (lo + hi) >> 1;
+                                    if (ss[mid] >= tbv) lo = mid + 1; else hi = mid;
+                                  }
+                                  return lo;
+                                },
+                                pairs, pruned);
     wlen[w] = len;
     scored = len > 0;
   }
