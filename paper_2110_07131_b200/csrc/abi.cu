@@ -487,8 +487,8 @@ static void ensure_ws(rmips_index_s* x, QueryCtx& c, int nsub, int64_t cap, cuda
   const int ldh = x->ldh;
   // accepted pairs as a bit matrix when it is small enough (no key sort, no mid-call sync)
   const int64_t nw = (x->n + 31) / 32;
-  const int64_t nch = query_bits_chunks(c.b, nw);  // its output pass keeps 2 nch int64 in acc_sorted's space
-  if (cap < 2 * nch) cap = 2 * nch;
+  const int64_t nch = query_bits_chunks(c.b, nw);  // its output pass keeps <= 3 nch int64 in acc_sorted's space
+  if (cap < 3 * nch) cap = 3 * nch;  // (the output pass's counts, in-CTA offsets and CTA totals)
   size_t qcub = query_cub_bytes(cap);
   const size_t qscan = query_scan_bytes(nch);
   if (qscan > qcub) qcub = qscan;

@@ -768,16 +768,20 @@ constexpr int kBitsThreads = 256;
 constexpr int C_BITS_TICKET = kNumCounters + 2;  // (spare, zeroed per call / batch) k_bits_count CTAs done
 __global__ void __launch_bounds__(kBitsThreads)
 k_bits_count(const uint32_t* __restrict__ bits, const uint8_t* __restrict__ dirty, int64_t nw, int64_t nbr,
-             int64_t nchunk_total, int64_t* __restrict__ counts, int64_t* __restrict__ chunk_off,
+             int64_t nchunk_total, int64_t* __restrict__ counts, int64_t* __restrict__ local_off,
+             int64_t* __restrict__ cta_sum, int64_t* __restrict__ cta_off,
              unsigned long long* __restrict__ ticket) {  // ticket: zeroed before the launch
   pdl_enter();  // (PDL: see launch_pdl)
+  constexpr int kWarps = kBitsThreads / 32;
+  __shared__ int last;
+  __shared__ int64_t wsum[kWarps];
   const int64_t g = (blockIdx.x * (int64_t)kBitsThreads + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (g < nchunk_total) {  // (no early return: the last CTA's scan below needs every thread)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int cnt = 0;
+  if (g < nchunk_total) {  // (no early return: the CTA sync and the last CTA's scan below need every thread)
     const int64_t per_row = (nw + kChunkWords - 1) / kChunkWords;
     const int64_t q = g / per_row, c = g - q * per_row;
     const int64_t blk = c * 32 + lane;  // this lane's block of the row
-    int cnt = 0;
     if (blk < nbr && dirty[q * nbr + blk]) {
       const uint32_t* wp = bits + q * nw + blk * 32;
       const int nwb = (int)min((int64_t)32, nw - blk * 32);
@@ -786,61 +790,55 @@ k_bits_count(const uint32_t* __restrict__ bits, const uint8_t* __restrict__ dirt
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) counts[g] = cnt;
   }
-  // The last CTA to finish scans the chunk counts (exclusive), so the emit pass needs no separate scan
-  // launch: every CTA's writers publish their counts (fence) before thread 0 takes the CTA's ticket.
-  __shared__ int last;
-  __shared__ int64_t wsum[kBitsThreads / 32];
-  if (lane == 0) __threadfence();  // (the lanes that wrote a count publish it)
+  // two levels: each chunk's offset within its CTA (local_off) and every CTA's total (cta_sum); the last
+  // CTA to finish scans the CTA totals (cta_off), k_bits_emit adds the two
+  if (lane == 0) wsum[wid] = cnt;
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(ticket, 1ull) == (unsigned long long)gridDim.x - 1;
+  if (lane == 0 && g < nchunk_total) {
+    int64_t pre = 0;
+    for (int i = 0; i < wid; ++i) pre += wsum[i];
+    counts[g] = cnt;
+    local_off[g] = pre;
+  }
+  if (threadIdx.x == 0) {
+    int64_t tot = 0;
+    for (int i = 0; i < kWarps; ++i) tot += wsum[i];
+    cta_sum[blockIdx.x] = tot;
+    __threadfence();  // (every write the last CTA reads is thread 0's, published before its ticket)
+    last = atomicAdd(ticket, 1ull) == (unsigned long long)gridDim.x - 1;
+  }
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // thread t owns the contiguous run [t per, (t + 1) per) of the counts: one pass over registers when
-  // per <= 32 (every load in flight at once), else a sum pass and a write pass over the run
-  const int t = threadIdx.x, w = t >> 5;
-  const int64_t per = (nchunk_total + kBitsThreads - 1) / kBitsThreads;
-  const int64_t a = (int64_t)t * per, e = a + per < nchunk_total ? a + per : nchunk_total;
-  int64_t v[32], sum = 0;
-  if (per <= 32) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      v[i] = a + i < e ? __ldcg(counts + a + i) : 0;
-      sum += v[i];
-    }
-  } else {
-#pragma unroll 8
-    for (int64_t i = a; i < e; ++i) sum += __ldcg(counts + i);
-  }
+  // exclusive scan of the gridDim.x CTA totals: thread t owns the contiguous run [t per, (t + 1) per)
+  const int64_t nc = gridDim.x;
+  const int t = threadIdx.x;
+  const int64_t per = (nc + kBitsThreads - 1) / kBitsThreads;
+  const int64_t a = (int64_t)t * per, e = a + per < nc ? a + per : nc;
+  int64_t sum = 0;
+  for (int64_t i = a; i < e; ++i) sum += __ldcg(cta_sum + i);
   int64_t incl = sum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int64_t x = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += x;
   }
-  if (lane == 31) wsum[w] = incl;
+  __syncthreads();  // (wsum is reused)
+  if (lane == 31) wsum[wid] = incl;
   __syncthreads();
   int64_t run = incl - sum;
 #pragma unroll
-  for (int i = 0; i < kBitsThreads / 32; ++i) run += i < w ? wsum[i] : 0;
-  if (per <= 32) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      if (a + i < e) chunk_off[a + i] = run;
-      run += v[i];
-    }
-  } else {
-    for (int64_t i = a; i < e; ++i) {
-      chunk_off[i] = run;
-      run += __ldcg(counts + i);
-    }
+  for (int i = 0; i < kWarps; ++i) run += i < wid ? wsum[i] : 0;
+  for (int64_t i = a; i < e; ++i) {
+    cta_off[i] = run;
+    run += __ldcg(cta_sum + i);
   }
 }
 __global__ void __launch_bounds__(kBitsThreads)
 k_bits_emit(uint32_t* __restrict__ bits, uint8_t* __restrict__ dirty, int64_t nw, int64_t nbr, int b,
-            int64_t nchunk_total, const int64_t* __restrict__ counts, const int64_t* __restrict__ chunk_off,
+            int64_t nchunk_total, const int64_t* __restrict__ counts, const int64_t* __restrict__ local_off,
+            const int64_t* __restrict__ cta_sum, const int64_t* __restrict__ cta_off,
             int64_t capacity, int64_t* __restrict__ offsets, int32_t* __restrict__ out,
             const int64_t* __restrict__ obase, int64_t* __restrict__ obase_next,
             const unsigned long long* __restrict__ ctr, const int* __restrict__ flags_dev,
@@ -864,9 +862,10 @@ k_bits_emit(uint32_t* __restrict__ bits, uint8_t* __restrict__ dirty, int64_t nw
   // obase (batched calls, rmips_query_batches): the ids of the earlier batches already in `out`; this
   // batch's running total goes to obase_next (a different word: every block reads obase)
   const int64_t b0 = obase ? *obase : 0;
-  const int64_t total = b0 + chunk_off[nchunk_total - 1] + counts[nchunk_total - 1];
+  const int64_t lc = (nchunk_total - 1) / (kBitsThreads / 32);  // the last CTA of the count pass
+  const int64_t total = b0 + cta_off[lc] + cta_sum[lc];
   const bool fits = total <= capacity;  // ids only when all of them fit (as the sorted-key path)
-  const int64_t base = b0 + chunk_off[g];
+  const int64_t base = b0 + cta_off[g / (kBitsThreads / 32)] + local_off[g];
   if (lane == 0) {
     if (c == 0) offsets[q] = base;
     if (g == nchunk_total - 1) {
@@ -923,14 +922,18 @@ int64_t query_bits_chunks(int b, int64_t nw) { return (int64_t)b * ((nw + kChunk
 cudaError_t query_output_bits(QueryCtx& c, int64_t* offsets, int32_t* user_ids, int64_t capacity, cudaStream_t st,
                               const int64_t* obase, int64_t* obase_next, unsigned long long* fold) {
   const int64_t nch = query_bits_chunks(c.b, c.nw);
-  int64_t* counts = reinterpret_cast<int64_t*>(c.acc_sorted);  // the sort's space is unused on this path
-  int64_t* chunk_off = counts + nch;
+  // (the sort's space is unused on this path: 2 nch + 2 grid <= 3 nch words, ensure_ws)
   const unsigned grid = (unsigned)((nch * 32 + kBitsThreads - 1) / kBitsThreads);
-  // the chunk counts are scanned by the count kernel's last CTA (no separate scan launch)
-  CK_PDL(launch_pdl(k_bits_count, dim3(grid), dim3(kBitsThreads), 0, st, c.bits, c.dirty, c.nw, c.nbr, nch, counts, chunk_off,
-                                               c.counters + C_BITS_TICKET));
+  int64_t* counts = reinterpret_cast<int64_t*>(c.acc_sorted);
+  int64_t* local_off = counts + nch;
+  int64_t* cta_sum = local_off + nch;
+  int64_t* cta_off = cta_sum + grid;
+  // the CTA totals are scanned by the count kernel's last CTA (no separate scan launch)
+  CK_PDL(launch_pdl(k_bits_count, dim3(grid), dim3(kBitsThreads), 0, st, c.bits, c.dirty, c.nw, c.nbr, nch, counts,
+                    local_off, cta_sum, cta_off, c.counters + C_BITS_TICKET));
   count_launch();
-  CK_PDL(launch_pdl(k_bits_emit, dim3(grid), dim3(kBitsThreads), 0, st, c.bits, c.dirty, c.nw, c.nbr, c.b, nch, counts, chunk_off, capacity,
+  CK_PDL(launch_pdl(k_bits_emit, dim3(grid), dim3(kBitsThreads), 0, st, c.bits, c.dirty, c.nw, c.nbr, c.b, nch, counts,
+                    local_off, cta_sum, cta_off, capacity,
                                               offsets, user_ids, obase, obase_next, c.counters, c.flags_dev, fold));
   count_launch();
   return cudaGetLastError();
